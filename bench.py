@@ -1,0 +1,525 @@
+"""Benchmark of the B200 codec hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one GoP (9 frames) of every stream on this GPU through the full
+path: scale_gop(down) + encode_gop + token_similarity -> intelligent drop
+(build_drop_mask + apply_token_mask, P layer) -> packetize (quantise, header,
+mask, payload, CRC-32) -> parse + first-wins reassembly + mask-aware decode ->
+scale_gop(up, crop) + blend_boundary, all 9 output frames materialised.
+
+Workload (BASELINE.json configs[2]+[4]): S concurrent 1080p streams per GPU
+(default 64), variable-resolution mode (half the streams at scale 3, half at
+scale 2, pattern 3,3,2,2 per stream), 10% intelligent P-token drop, blend
+width 2.  Weak scaling: every rank runs its own S streams (stream ids
+rank*S + i); no collective touches the data path.
+
+`value` is device-resident throughput (inputs already in HBM; every step's
+input is 14.3 GB at S=64, far larger than the 126 MB L2, so no flush is
+needed).  `e2e` runs the same pipeline through the public batched API with
+pinned HOST frames: H2D of the step's input, the sender's packets D2H and the
+receiver's packets H2D (the network boundary), and D2H of the reconstructed
+frames, all inside the timed region.
+
+--impl reference times the reference algorithm's CPU implementation (the
+oracle port, oracle/semstream_oracle.py -- the reference itself is numpy and
+cannot travel to the GPU box) on the host cores, one GoP per worker process
+per step, on the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "1080p encode+decode frames/sec per B200 (1/2/4/8 GPU); PSNR delta vs CPU ref"
+UNIT = "frames/s"
+GOP = 9
+SCALE_PATTERN = (3, 3, 2, 2)     # per-stream GoP scale sequence (variable resolution)
+FALLBACK_HBM_GBS = 6650.0        # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--streams", type=int, default=64, help="streams per GPU")
+    ap.add_argument("--height", type=int, default=1080)
+    ap.add_argument("--width", type=int, default=1920)
+    ap.add_argument("--drop", type=float, default=0.10)
+    ap.add_argument("--e2e-streams", type=int, default=8)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-workers", type=int, default=0, help="0 = auto")
+    return ap.parse_args()
+
+
+def workload_config(a) -> dict:
+    return {
+        "workload": f"{a.streams} concurrent {a.height}p streams per GPU, variable-resolution "
+                    f"(scales {SCALE_PATTERN} per stream, half the streams at each scale), "
+                    f"{int(a.drop * 100)}% intelligent P-token drop, blend n=2, no network loss",
+        "streams_per_gpu": a.streams,
+        "frame": [a.height, a.width, 3],
+        "frame_dtype": "float32 in / float32 out (reference Frame dtype)",
+        "gop_frames": GOP,
+        "drop_rate": a.drop,
+        "blend_width": 2,
+        "l2": "inputs larger than L2 (each step reads a fresh 14.3 GB GoP batch at 64 streams)",
+    }
+
+
+# ---------------------------------------------------------------------------
+# helpers
+
+def scale_of(stream: int, k: int) -> int:
+    half = 0 if stream % 2 == 0 else 2          # odd streams run the pattern shifted by 2 GoPs
+    return SCALE_PATTERN[(k + half) % len(SCALE_PATTERN)]
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self._proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self._t = threading.Thread(target=self._read, daemon=True)
+            self._t.start()
+        except (OSError, FileNotFoundError):
+            self._proc = None
+        return self
+
+    def _read(self):
+        for line in self._proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 8:
+                self.samples.append(parts)
+
+    def __exit__(self, *exc):
+        if self._proc is not None:
+            self._proc.terminate()
+            try:
+                self._proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self._proc.kill()
+
+    def summary(self) -> dict:
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if s[4 + i].strip().lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def measured_hbm_peak():
+    p = ROOT / "MEASURED_PEAKS.json"
+    try:
+        d = json.loads(p.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the dominant kernels from the committed ncu
+    --set full capture (profiles/*_traffic.json), or None."""
+    best = None
+    for p in sorted((ROOT / "profiles").glob("*_traffic.json")):
+        try:
+            best = json.loads(p.read_text())
+        except Exception:
+            pass
+    return best
+
+
+# ---------------------------------------------------------------------------
+# device input generation (synthetic clips of the named shape)
+
+def make_inputs(stream_ids, H, W, device, n_sets=2):
+    """[n_sets][n_streams, 9, H, W, 3] float32: per stream a textured square
+    moving over a gradient (moving-square style) plus per-frame noise on odd
+    streams (noisy-motion style); every stream has its own seed."""
+    import torch
+    n_streams = len(stream_ids)
+    sets = []
+    yy = torch.linspace(0, 1, H, device=device)[:, None]
+    xx = torch.linspace(0, 1, W, device=device)[None, :]
+    base = torch.stack([(0.25 + 0.5 * xx).expand(H, W), (0.25 + 0.5 * yy).expand(H, W),
+                        torch.full((H, W), 0.4, device=device)], dim=-1)
+    side = max(8, min(H, W) // 4)
+    for k in range(n_sets):
+        frames = torch.empty((n_streams, GOP, H, W, 3), dtype=torch.float32, device=device)
+        for i, sid in enumerate(stream_ids):
+            g = torch.Generator(device=device)
+            g.manual_seed(1000 + sid)
+            tex = torch.rand((side // 4 + 1, side // 4 + 1, 3), generator=g, device=device)
+            tex = tex.repeat_interleave(4, 0).repeat_interleave(4, 1)[:side, :side]
+            for t in range(GOP):
+                idx = k * GOP + t
+                img = base.clone()
+                x = (4 * idx + 37 * sid) % max(W - side, 1)
+                y = (2 * idx + 11 * sid) % max(H - side, 1)
+                img[y:y + side, x:x + side] = tex
+                if sid % 2:
+                    img = img + 0.15 * (torch.rand((H, W, 3), generator=g, device=device) - 0.5)
+                frames[i, t] = img.clamp_(0.0, 1.0)
+        sets.append(frames)
+    return sets
+
+
+# ---------------------------------------------------------------------------
+# our arm
+
+def run_ours(a, rank, world, local_rank):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_03529_b200.pipeline import StageTimer, StreamBank
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    S, H, W = a.streams, a.height, a.width
+    # streams with the even pattern phase first, odd phase second: each scale
+    # group is a contiguous slice of the batch every step
+    even = [i for i in range(S) if i % 2 == 0]
+    odd = [i for i in range(S) if i % 2 == 1]
+    ne = len(even)
+    inputs = make_inputs([rank * S + i for i in even + odd], H, W, dev)
+    out = torch.empty_like(inputs[0])
+    bank = StreamBank(S, H, W)
+
+    def groups(k):
+        s_even, s_odd = scale_of(0, k), scale_of(1, k)
+        fr = inputs[k % 2]
+        if s_even == s_odd:
+            return ({s_even: fr}, {s_even: out}, {s_even: list(range(S))})
+        return ({s_even: fr[:ne], s_odd: fr[ne:]}, {s_even: out[:ne], s_odd: out[ne:]},
+                {s_even: list(range(ne)), s_odd: list(range(ne, S))})
+
+    def one_step(k):
+        fr, ou, ids = groups(k)
+        bank.step(fr, ou, ids, {s: [k] * len(v) for s, v in ids.items()}, drop_rate=a.drop)
+
+    for k in range(a.warmup):
+        one_step(k)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches0 = bank.launches
+    timer = StageTimer()
+    bank.set_timer(timer)
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clocks:
+        torch.cuda.synchronize()
+        t_start.record()
+        for k in range(a.warmup, a.warmup + a.steps):
+            one_step(k)
+        t_end.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    bank.set_timer(None)
+    ms = t_start.elapsed_time(t_end)
+    ms_max = ms
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    launches = bank.launches - launches0
+    stages = timer.summary()
+    frames_total = S * GOP * a.steps * world
+    value = frames_total / (ms_max / 1000.0)
+
+    # quality of one GoP per scale vs the source (device metric)
+    psnr = {}
+    fr, ou, ids = groups(a.warmup + a.steps - 1)
+    for s, o in ou.items():
+        src = fr[s][0]
+        mse = ((o[0].double() - src.double()) ** 2).mean().item()
+        psnr[f"s{s}"] = 99.0 if mse <= 0 else min(99.0, 10 * np.log10(1.0 / mse))
+
+    res = dict(ms=ms_max, value=value, stages=stages, launches=launches,
+               clocks=clocks.summary(), psnr=psnr)
+    res["roofline"] = roofline(a, stages, S)
+    if not a.no_e2e:
+        del inputs, out
+        torch.cuda.empty_cache()
+        res["e2e"] = run_e2e(a, rank, world, local_rank)
+    return res
+
+
+def roofline(a, stages, S) -> dict:
+    """Achieved GB/s of the dominant kernel: algorithmic bytes per launch /
+    average CUDA-event launch duration inside the timed region."""
+    H, W = a.height, a.width
+    frame_bytes = H * W * 3 * 4
+    # per GoP (one stream): K1 reads 9 frames + writes tokens/sim;
+    # K5 writes 9 frames + reads the two working images (+ the previous P image)
+    def tokens_bytes(s):
+        h, w = -(-H // s), -(-W // s)
+        ht, wt = -(-h // 8), -(-w // 8)
+        return ht * wt * (2 * 12 * 8 + 8), 3 * h * w * 3 * 4
+    avg_tok = sum(tokens_bytes(s)[0] for s in (2, 3)) / 2
+    avg_img = sum(tokens_bytes(s)[1] for s in (2, 3)) / 2
+    per_gop = {"K1_encode": GOP * frame_bytes + avg_tok,
+               "K5_upscale_blend": GOP * frame_bytes + avg_img}
+    peak, peak_src = measured_hbm_peak()
+    best = None
+    for name, bytes_gop in per_gop.items():
+        if name not in stages:
+            continue
+        tot_ms, launches = stages[name]
+        gops_per_launch = S * a.steps / launches          # GoPs processed per launch
+        algo = bytes_gop * gops_per_launch
+        avg_s = tot_ms / launches / 1000.0
+        ach = algo / avg_s / 1e9
+        cand = dict(kernel=name, bound="hbm", achieved=round(ach, 1), peak=peak, unit="GB/s",
+                    frac=round(ach / peak, 4), peak_source=peak_src,
+                    algorithmic_bytes_per_launch=int(algo),
+                    avg_launch_ms=round(avg_s * 1000, 4))
+        if best is None or tot_ms > best["_tot"]:
+            best = dict(cand, _tot=tot_ms)
+    if best is None:
+        return None
+    best.pop("_tot")
+    tr = ncu_traffic()
+    best["traffic"] = None
+    if tr and best["kernel"] in tr:
+        best["traffic"] = tr[best["kernel"]]
+        best["traffic_source"] = tr.get("_source")
+    return best
+
+
+def run_e2e(a, rank, world, local_rank) -> dict:
+    """Same pipeline through the public batched API with pinned host buffers:
+    frames H2D -> sender (K1-K3) -> packets D2H -> packets H2D -> receiver
+    (K4, K5) -> frames D2H, every step, inside the timed region."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2602_03529_b200.pipeline import StreamBank
+
+    dev = torch.device("cuda", local_rank)
+    E, H, W = a.e2e_streams, a.height, a.width
+    src_dev = make_inputs([rank * E + i for i in range(E)], H, W, dev, n_sets=1)[0]
+    host_in = torch.empty(src_dev.shape, dtype=torch.float32, pin_memory=True)
+    host_in.copy_(src_dev)
+    host_out = torch.empty_like(host_in, pin_memory=True)
+    del src_dev
+    d_in = torch.empty(host_in.shape, dtype=torch.float32, device=dev)
+    d_out = torch.empty_like(d_in)
+    bank = StreamBank(E, H, W)
+    # the scale alternates per GoP for all e2e streams (variable resolution)
+    codecs = bank.codecs
+    pk_host = {s: torch.empty(c.arena.shape, dtype=torch.uint8, pin_memory=True)
+               for s, c in codecs.items()}
+    len_host = {s: torch.empty(c.lengths.shape, dtype=torch.int32, pin_memory=True)
+                for s, c in codecs.items()}
+    h2d = d2h = 0
+
+    def one(k):
+        nonlocal h2d, d2h
+        s = SCALE_PATTERN[k % len(SCALE_PATTERN)]
+        c = codecs[s]
+        d_in.copy_(host_in, non_blocking=True)
+        h2d += host_in.numel() * 4
+        parity = bank.step_idx & 1
+        c.set_gop_ids([k] * E)
+        c.encode(d_in, E, c.drop_k(a.drop))
+        npk = E * c.n_pkt_per_gop
+        # sender -> wire -> receiver
+        pk_host[s][:npk].copy_(c.arena[:npk], non_blocking=True)
+        len_host[s][:npk].copy_(c.lengths[:npk], non_blocking=True)
+        d2h += npk * c.slot + npk * 4
+        c.arena[:npk].copy_(pk_host[s][:npk], non_blocking=True)
+        c.lengths[:npk].copy_(len_host[s][:npk], non_blocking=True)
+        h2d += npk * c.slot + npk * 4
+        c.decode(E, parity)
+        staged = bank._prev_descs(s, list(range(E)))
+        c.reconstruct(E, parity, d_out, None if staged is None else staged[0])
+        if staged is not None:
+            bank.rings[s].release(staged[1])
+        for i in range(E):
+            bank.last[i] = (s, parity, i)
+        bank.step_idx += 1
+        host_out.copy_(d_out, non_blocking=True)
+        d2h += host_out.numel() * 4
+
+    for k in range(a.warmup):
+        one(k)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    h2d = d2h = 0
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    wall0 = time.perf_counter()
+    t0.record()
+    for k in range(a.warmup, a.warmup + a.steps):
+        one(k)
+    t1.record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - wall0
+    ms = t0.elapsed_time(t1)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    frames = E * GOP * a.steps * world
+    return {"value": round(frames / (ms / 1000.0), 2), "unit": UNIT,
+            "h2d_bytes_per_step": int(h2d // a.steps), "d2h_bytes_per_step": int(d2h // a.steps),
+            "streams_per_gpu": E, "wall_s": round(wall, 3),
+            "path": "StreamBank/GopCodec public API, pinned host frames in/out + packet "
+                    "round trip through host memory"}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle port of the reference algorithm)
+
+def _cpu_worker(job):
+    import numpy as np
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    from oracle import semstream_oracle as O
+    from oracle.synth import make_clip
+    H, W, sid, k, s, drop = job
+    name = "moving-square" if sid % 2 == 0 else "noisy-motion"
+    clip = make_clip(name, W, H, GOP * (k + 1), seed=sid)
+    frames = clip.gop(k)
+    t0 = time.perf_counter()
+    res = O.pipeline_gop(frames, s, gop_id=k, drop_rate=drop)
+    dt = time.perf_counter() - t0
+    psnr, _ = O.gop_psnr(list(frames), res["frames"])
+    return dt, psnr
+
+
+def cpu_workers(a) -> int:
+    if a.cpu_workers:
+        return a.cpu_workers
+    n = os.cpu_count() or 1
+    try:
+        import psutil
+        mem = psutil.virtual_memory().available
+        n = min(n, max(1, int(mem // (3 * 1024 ** 3))))     # ~3 GB per 1080p GoP worker
+    except Exception:
+        pass
+    return max(1, min(n, 64))
+
+
+def cpu_sample(a, steps: int, warm: int = 0):
+    """Time `steps` rounds of one GoP per worker; returns per-round wall times."""
+    import multiprocessing as mp
+    n = cpu_workers(a)
+    ctx = mp.get_context("spawn")
+    walls = []
+    psnrs = []
+    with ctx.Pool(n, initializer=os.environ.setdefault, initargs=("OMP_NUM_THREADS", "1")) as pool:
+        for r in range(warm + steps):
+            jobs = [(a.height, a.width, i, 0, scale_of(i, r), a.drop) for i in range(n)]
+            t0 = time.perf_counter()
+            out = pool.map(_cpu_worker, jobs)
+            wall = time.perf_counter() - t0
+            if r >= warm:
+                walls.append(wall)
+                psnrs.extend(p for _, p in out)
+    return n, walls, psnrs
+
+
+def run_reference(a) -> dict:
+    n, walls, psnrs = cpu_sample(a, a.steps, a.warmup)
+    total = sum(walls)
+    value = n * GOP * a.steps / total
+    return dict(value=value, ms=1000 * total / a.steps, cores=n, psnr=statistics.mean(psnrs))
+
+
+def cpu_baseline(a) -> dict:
+    n, walls, _ = cpu_sample(a, 1, 0)
+    return {"value": round(n * GOP / walls[0], 3), "unit": UNIT, "cores": n, "kind": "port",
+            "sample": f"{n} worker processes x one {a.height}p GoP each (9 frames, "
+                      f"scales {sorted({scale_of(i, 0) for i in range(n)})}, "
+                      f"{int(a.drop * 100)}% drop), oracle/semstream_oracle.py pipeline_gop, "
+                      f"wall {walls[0]:.1f} s"}
+
+
+# ---------------------------------------------------------------------------
+
+def main():
+    a = parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    base = {"metric": METRIC, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(a)}
+
+    if a.impl == "reference":
+        if rank != 0:
+            return
+        r = run_reference(a)
+        line = dict(base, impl="reference", value=round(r["value"], 3),
+                    ms_per_step=round(r["ms"], 2),
+                    cpu_baseline={"value": round(r["value"], 3), "unit": UNIT,
+                                  "cores": r["cores"], "kind": "port",
+                                  "sample": f"{r['cores']} processes x one {a.height}p GoP per "
+                                            f"step, oracle port of the reference algorithm"},
+                    e2e={"value": round(r["value"], 3), "unit": UNIT,
+                         "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                    psnr_db=round(r["psnr"], 3))
+        line["config"] = dict(line["config"], streams_per_step=r["cores"])
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    res = run_ours(a, rank, world, local_rank)
+    if rank == 0:
+        line = dict(base, value=round(res["value"], 2), ms_per_step=round(res["ms"] / a.steps, 3),
+                    roofline=res["roofline"], gpu_launches=res["launches"],
+                    clocks=res["clocks"],
+                    stages={k: {"ms_total": round(v[0], 3), "launches": v[1]}
+                            for k, v in res["stages"].items()},
+                    psnr_db=res["psnr"])
+        line["e2e"] = res.get("e2e")
+        if world == 1 and not a.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(a)
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,230 @@
+/*
+ * semstream_b200.h -- C ABI of the B200-native semstream codec hot path.
+ *
+ * Drop-in boundary for the reference package `semstream`
+ * (/root/reference/pkg/src/semstream, a pure numpy/scipy implementation).
+ * Each entry point below replaces one reference function (cited file:line,
+ * relative to pkg/src/semstream/) and reproduces its results bit-for-bit on
+ * the same inputs.  A maintainer binds them from Python with ctypes; see
+ * INTEGRATION.md.
+ *
+ * Conventions
+ *   - All array pointers are DEVICE pointers owned by the caller (no
+ *     allocation, no global state inside the library).  `stream` is a
+ *     cudaStream_t passed as void*; every call is stream-ordered and
+ *     non-blocking.  Calls are thread-safe for distinct (stream, buffers).
+ *   - Return value: SST_OK (0) or a negative SST_ERR_* code for argument /
+ *     launch errors.  Per-packet problems are reported in per-packet status
+ *     words (SST_PKT_*), never as call failures.
+ *   - Layouts (row-major, C order):
+ *       frames      float32 [n][H][W][3]            (video.py:20-54 Frame)
+ *       tokens      float64 [m][H'][W'][C]          (codec.py:49-91 TokenMatrix.values)
+ *       token mask  uint8   [m][H'][W']  1 = valid  (TokenMatrix.mask)
+ *       GoP batch   frames [G][9][H][W][3]; tokens [G][2][H'][W'][12] (I then P)
+ *   - dtype of the arithmetic: float64 where the reference is float64,
+ *     float32 storage where the reference stores float32.
+ */
+#ifndef SEMSTREAM_B200_H_
+#define SEMSTREAM_B200_H_
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define SST_API __attribute__((visibility("default")))
+#else
+#define SST_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SST_ABI_VERSION 1
+
+/* call status */
+#define SST_OK 0
+#define SST_ERR_ARG (-1)         /* bad shape / scale / pointer */
+#define SST_ERR_ROWS_16BIT (-2)  /* > 65535 token rows: transport.py:331-333 "16-bit" */
+#define SST_ERR_CUDA (-3)        /* CUDA runtime / launch failure */
+#define SST_ERR_UNSUPPORTED (-4) /* e.g. channel count the kernel does not handle */
+
+/* per-packet status (parse_packet, transport.py:151-157, 241-271; reassemble, 274-305) */
+#define SST_PKT_OK 0
+#define SST_PKT_SHORT 1        /* "packet shorter than its checksum" */
+#define SST_PKT_CRC 2          /* "crc32 mismatch" */
+#define SST_PKT_BODY_SHORT 3   /* "packet body too short" */
+#define SST_PKT_MAGIC 4        /* "bad magic" */
+#define SST_PKT_VERSION 5      /* "unsupported version" */
+#define SST_PKT_KIND 6         /* not a token packet (kind holds the raw kind byte) */
+#define SST_PKT_HDR_TRUNC 7    /* "token packet header truncated" */
+#define SST_PKT_MASK_TRUNC 8   /* "token packet mask truncated" */
+#define SST_PKT_PAYLOAD_LEN 9  /* "payload length != popcount(mask)*C" */
+#define SST_PKT_NEG_RANGE 10   /* "negative quantization range" */
+#define SST_PKT_ABSENT 11      /* slot not present (lost in the network) */
+#define SST_PKT_FOREIGN 12     /* kind / gop_id differ from the routed matrix (reassemble ValueError) */
+#define SST_PKT_ROW_RANGE 13   /* row >= H': discarded, counted corrupt */
+#define SST_PKT_DUP 14         /* duplicate row: a packet that arrived earlier wins */
+#define SST_PKT_SHAPE 15       /* width / channel count incompatible with the matrix */
+
+/* Parsed token-packet header (TokenPacket fields, transport.py:82-95). */
+typedef struct SstPacketInfo {
+  int32_t status;      /* SST_PKT_* */
+  int32_t kind;        /* 0 = I, 1 = P */
+  uint32_t gop_id;
+  int32_t row;
+  int32_t width;       /* width_tokens W' */
+  int32_t channels;    /* C */
+  int32_t scale;
+  int32_t valid;       /* popcount(mask) */
+  float qmin;          /* quant_min as carried on the wire */
+  float qrange;        /* quant_range */
+  int32_t mask_off;    /* byte offset of the mask inside the packet */
+  int32_t payload_off; /* byte offset of the payload inside the packet */
+  double dqmin;        /* quant_min / quant_range used by dequantisation: the */
+  double dqrange;      /* wire float32 widened (parse), or a caller's float64 */
+} SstPacketInfo;
+
+/* Previous GoP of a stream, for boundary blending (codec.py:278-296). */
+typedef struct SstPrevDesc {
+  const float* p_img;  /* previous GoP's concealed P image, [h][w][3] at its working res; NULL = none */
+  int32_t h, w, s;     /* its working size and scale */
+  int32_t reserved;
+} SstPrevDesc;
+
+SST_API int sst_abi_version(void);
+
+/* Wire size of one token packet: transport.py:308-313 token_packet_wire_size. */
+SST_API int64_t sst_packet_wire_size(int width_tokens, int channels, int valid_count);
+
+/* ---- scaling ------------------------------------------------------------ */
+
+/* downscale_frame (codec.py:202-214) for n frames: s x s box mean with edge
+ * replication; out is [n][ceil(H/s)][ceil(W/s)][3] float32. */
+SST_API int sst_downscale(const float* frames, int64_t n, int H, int W, int s, float* out, void* stream);
+
+/* upscale_frame + crop (codec.py:238-245, 264-266): bilinear x s, clip to
+ * [0,1], float32, crop to (crop_h, crop_w) (<= s*h, s*w). */
+SST_API int sst_upscale(const float* img, int64_t n, int h, int w, int s, int crop_h, int crop_w,
+                float* out, void* stream);
+
+/* bilinear_upscale (codec.py:217-235): raw float64 result, no clip. */
+SST_API int sst_bilinear_f64(const double* img, int64_t n, int h, int w, int s, double* out, void* stream);
+
+/* np.clip(x, 0, 1).astype(float32): epilogue of upscale_frame for a
+ * user-supplied upscaler (codec.py:243-245). */
+SST_API int sst_clip_cast(const double* x, int64_t count, float* out, void* stream);
+
+/* blend_boundary (codec.py:278-296) for G GoP pairs: out = curr with frames
+ * 0..n-1 replaced by alpha*prev[9-n+i-1] + (1-alpha)*curr[i-1], alpha=(n-i)/n.
+ * prev, curr, out: [G][9][H][W][3]; out may alias curr. */
+SST_API int sst_blend(const float* prev, const float* curr, int G, int H, int W, int n, float* out,
+              void* stream);
+
+/* ---- tokenizer ---------------------------------------------------------- */
+
+/* scale_gop(down) (codec.py:248-254) fused with encode_gop (codec.py:143-157)
+ * and token_similarity(P, I) (selection.py:33-52).
+ *   frames: [G][9][H][W][3] full resolution; s in {1 (frames already at
+ *   working resolution: plain encode_gop), 2, 3}.
+ *   tok: [G][2][H'][W'][12] float64 (I, P); sim: [G][H'][W'] float64 or NULL.
+ * H' = ceil(ceil(H/s)/8), W' = ceil(ceil(W/s)/8). */
+SST_API int sst_encode(const float* frames, int G, int H, int W, int s, double* tok, double* sim,
+               void* stream);
+
+/* decode_gop (codec.py:160-186): IDCT of I and P tokens, crop to (h, w),
+ * clip, conceal invalid P blocks with I blocks.
+ *   i_tok, p_tok: [G][H'][W'][12] (any batch stride via tok_stride elements);
+ *   p_mask: [G][H'][W'] or NULL (all valid); out: [G][2][h][w][3] float32
+ *   (I image, concealed P image). */
+SST_API int sst_decode(const double* i_tok, const double* p_tok, int64_t tok_stride, const uint8_t* p_mask,
+               int G, int Ht, int Wt, int h, int w, float* out, void* stream);
+
+/* ---- selection ---------------------------------------------------------- */
+
+/* token_similarity (selection.py:33-52) for n token pairs with C channels. */
+SST_API int sst_similarity(const double* p, const double* i, int64_t n, int C, double* sim, void* stream);
+
+/* top_k_drop_mask (selection.py:55-67): per map g, mark the k[g] largest
+ * similarities (ties: lower row-major index first).  k is a DEVICE int32[G]. */
+SST_API int sst_topk_mask(const double* sim, int G, int64_t n, const int32_t* k, uint8_t* drop,
+                  void* stream);
+
+/* apply_token_mask (codec.py:189-196) in place: mask &= ~drop, values of
+ * invalid positions set to 0.0. */
+SST_API int sst_apply_mask(double* values, uint8_t* mask, const uint8_t* drop, int64_t n, int C,
+                   void* stream);
+
+/* Fused intelligent drop for a GoP batch: top_k_drop_mask on sim[g] then
+ * apply_token_mask on the P tokens of tok[g] ([G][2][H'][W'][12] layout).
+ * mask: the batch's token mask [G][2][H'][W'] (the P half is updated);
+ * drop: [G][H'][W'] out or NULL. */
+SST_API int sst_select_drop(const double* sim, double* tok, uint8_t* mask, int G, int Ht, int Wt,
+                    const int32_t* k, uint8_t* drop, void* stream);
+
+/* ---- wire format -------------------------------------------------------- */
+
+/* packetize_tokens + TokenPacket.to_bytes (transport.py:323-358, 184-189):
+ * one sealed packet per token row, written to arena[(m*Ht + row)*slot].
+ *   values [m][H'][W'][C], mask [m][H'][W'] (NULL = all valid); kind/gop_id/
+ *   scale per matrix (DEVICE arrays, length m); lengths: int32 [m*H'].
+ *   slot >= sst_packet_wire_size(W', C, W') and a multiple of 16. */
+SST_API int sst_packetize(const double* values, const uint8_t* mask, int m, int Ht, int Wt, int C,
+                  const uint8_t* kind, const uint32_t* gop_id, const uint8_t* scale,
+                  uint8_t* arena, int64_t slot, int32_t* lengths, void* stream);
+
+/* TokenPacket.to_bytes for packets given field-wise (transport.py:184-189):
+ *   info[n] supplies kind/gop/row/width/channels/scale/qmin/qrange/valid;
+ *   mask bits (ceil(width/8) bytes, MSB first) at masks + mask_off[i];
+ *   payload (valid*channels bytes) at payload + payload_off[i];
+ *   output at out + out_off[i], sst_packet_wire_size(width, channels, valid) bytes. */
+SST_API int sst_serialize(const SstPacketInfo* info, const uint8_t* masks, const int64_t* mask_off,
+                  const uint8_t* payload, const int64_t* payload_off, int64_t n, uint8_t* out,
+                  const int64_t* out_off, void* stream);
+
+/* parse_packet (transport.py:151-157, 241-271) for n packets at buf+off[i]
+ * of len[i] bytes.  present (NULL = all) marks delivered packets. */
+SST_API int sst_parse(const uint8_t* buf, const int64_t* off, const int32_t* len, const uint8_t* present,
+              int64_t n, SstPacketInfo* info, void* stream);
+
+/* reassemble (transport.py:274-305, dequantized 108-112) into m matrices.
+ *   target[i] = matrix the caller routed packet i to (arrival order = i);
+ *   exp_kind / exp_gop: expected kind and gop_id per matrix (DEVICE, len m);
+ *   winner: uint32 [m][H'] workspace; values/mask: outputs [m][H'][W'][C],
+ *   [m][H'][W']; stats: int32 [m][2] = {corrupt, rows_received}.
+ *   Packet status is updated in place (FOREIGN, ROW_RANGE, DUP). */
+SST_API int sst_reassemble(const uint8_t* buf, const int64_t* off, SstPacketInfo* info,
+                   const int32_t* target, int64_t n, int m, int Ht, int Wt, int C,
+                   const uint8_t* exp_kind, const uint32_t* exp_gop, uint32_t* winner,
+                   double* values, uint8_t* mask, int32_t* stats, void* stream);
+
+/* reassemble x2 + decode_gop fused: the mask-aware decoder reads each token
+ * straight out of the winning packet (no token matrix in HBM).
+ *   packets routed per GoP g as target[i] = 2*g + kind; exp_gop[G];
+ *   out: [G][2][h][w][3] float32 (I image, concealed P image). */
+SST_API int sst_unpack_decode(const uint8_t* buf, const int64_t* off, SstPacketInfo* info,
+                      const int32_t* target, int64_t n, int G, int Ht, int Wt, int h, int w,
+                      const uint32_t* exp_gop, uint32_t* winner, int32_t* stats, float* out,
+                      void* stream);
+
+/* ---- reconstruction ----------------------------------------------------- */
+
+/* scale_gop(up, crop) (codec.py:255-269) + blend_boundary (codec.py:278-296)
+ * fused, materialising all 9 output frames of each GoP.
+ *   img: [G][2][h][w][3] (I image, concealed P image) at scale s;
+ *   prev: DEVICE SstPrevDesc[G] (p_img NULL = first GoP of its stream, no
+ *   blend) or NULL; requires blend_n <= 4 when any prev is set (the blended
+ *   tail frames are then unblended P reconstructions of the previous GoP);
+ *   out: [G][9][H][W][3]. */
+SST_API int sst_upscale_blend(const float* img, int G, int h, int w, int s, int H, int W,
+                      const SstPrevDesc* prev, int blend_n, float* out, void* stream);
+
+/* ---- metrics ------------------------------------------------------------ */
+
+/* mse (video.py:265-270) per frame pair: out[i] = mean((a-b)^2) in float64. */
+SST_API int sst_mse(const float* a, const float* b, int64_t n, int64_t elems, double* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SEMSTREAM_B200_H_ */

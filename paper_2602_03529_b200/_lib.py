@@ -1,0 +1,128 @@
+"""ctypes binding of the sm_100a C-ABI library (include/semstream_b200.h).
+
+The library is built in-tree (``_build.py``) and loaded from this package
+directory.  There is no CPU fallback: if the shared object or a CUDA device
+is missing, every codec call raises ``RuntimeError``.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+LIB_PATH = Path(__file__).resolve().parent / "libsemstream_b200.so"
+
+SST_OK = 0
+SST_ERR_ARG = -1
+SST_ERR_ROWS_16BIT = -2
+SST_ERR_CUDA = -3
+SST_ERR_UNSUPPORTED = -4
+
+# per-packet status words (include/semstream_b200.h SST_PKT_*)
+PKT_OK, PKT_SHORT, PKT_CRC, PKT_BODY_SHORT, PKT_MAGIC, PKT_VERSION, PKT_KIND, \
+    PKT_HDR_TRUNC, PKT_MASK_TRUNC, PKT_PAYLOAD_LEN, PKT_NEG_RANGE, PKT_ABSENT, \
+    PKT_FOREIGN, PKT_ROW_RANGE, PKT_DUP, PKT_SHAPE = range(16)
+
+
+class SstPacketInfo(C.Structure):
+    _fields_ = [("status", C.c_int32), ("kind", C.c_int32), ("gop_id", C.c_uint32),
+                ("row", C.c_int32), ("width", C.c_int32), ("channels", C.c_int32),
+                ("scale", C.c_int32), ("valid", C.c_int32), ("qmin", C.c_float),
+                ("qrange", C.c_float), ("mask_off", C.c_int32), ("payload_off", C.c_int32),
+                ("dqmin", C.c_double), ("dqrange", C.c_double)]
+
+
+class SstPrevDesc(C.Structure):
+    _fields_ = [("p_img", C.c_void_p), ("h", C.c_int32), ("w", C.c_int32), ("s", C.c_int32),
+                ("reserved", C.c_int32)]
+
+
+INFO_BYTES = C.sizeof(SstPacketInfo)          # 64
+PREV_BYTES = C.sizeof(SstPrevDesc)            # 24
+
+_P = C.c_void_p
+_I = C.c_int
+_L = C.c_int64
+
+# name -> (restype, argtypes); mirrors include/semstream_b200.h
+SIGNATURES = {
+    "sst_abi_version": (_I, []),
+    "sst_packet_wire_size": (_L, [_I, _I, _I]),
+    "sst_downscale": (_I, [_P, _L, _I, _I, _I, _P, _P]),
+    "sst_upscale": (_I, [_P, _L, _I, _I, _I, _I, _I, _P, _P]),
+    "sst_bilinear_f64": (_I, [_P, _L, _I, _I, _I, _P, _P]),
+    "sst_clip_cast": (_I, [_P, _L, _P, _P]),
+    "sst_blend": (_I, [_P, _P, _I, _I, _I, _I, _P, _P]),
+    "sst_encode": (_I, [_P, _I, _I, _I, _I, _P, _P, _P]),
+    "sst_decode": (_I, [_P, _P, _L, _P, _I, _I, _I, _I, _I, _P, _P]),
+    "sst_similarity": (_I, [_P, _P, _L, _I, _P, _P]),
+    "sst_topk_mask": (_I, [_P, _I, _L, _P, _P, _P]),
+    "sst_apply_mask": (_I, [_P, _P, _P, _L, _I, _P]),
+    "sst_select_drop": (_I, [_P, _P, _P, _I, _I, _I, _P, _P, _P]),
+    "sst_packetize": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _L, _P, _P]),
+    "sst_serialize": (_I, [_P, _P, _P, _P, _P, _L, _P, _P, _P]),
+    "sst_parse": (_I, [_P, _P, _P, _P, _L, _P, _P]),
+    "sst_reassemble": (_I, [_P, _P, _P, _P, _L, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
+    "sst_unpack_decode": (_I, [_P, _P, _P, _P, _L, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
+    "sst_upscale_blend": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P]),
+    "sst_mse": (_I, [_P, _P, _L, _L, _P, _P]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load (once) and return the C-ABI library; raises if it was never built."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not LIB_PATH.exists():
+                raise RuntimeError(
+                    f"semstream_b200 CUDA extension not built ({LIB_PATH} missing); "
+                    "run `python -m paper_2602_03529_b200._build` -- there is no CPU fallback")
+            lib = C.CDLL(str(LIB_PATH))
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+class CudaCallError(RuntimeError):
+    pass
+
+
+def check(rc: int, what: str) -> None:
+    if rc == SST_OK:
+        return
+    if rc == SST_ERR_ROWS_16BIT:
+        raise ValueError(f"{what}: matrix has more than 65535 rows; the row index field is 16-bit")
+    if rc == SST_ERR_ARG:
+        raise ValueError(f"{what}: invalid argument")
+    if rc == SST_ERR_UNSUPPORTED:
+        raise ValueError(f"{what}: unsupported shape for the CUDA kernel")
+    raise CudaCallError(f"{what}: CUDA launch failed (status {rc})")
+
+
+def call(name: str, *args) -> None:
+    rc = getattr(load(), name)(*args)
+    check(rc, name)
+
+
+# numpy view of SstPacketInfo (same 64-byte layout)
+try:
+    import numpy as _np
+
+    INFO_DTYPE = _np.dtype([("status", "<i4"), ("kind", "<i4"), ("gop_id", "<u4"), ("row", "<i4"),
+                            ("width", "<i4"), ("channels", "<i4"), ("scale", "<i4"),
+                            ("valid", "<i4"), ("qmin", "<f4"), ("qrange", "<f4"),
+                            ("mask_off", "<i4"), ("payload_off", "<i4"), ("dqmin", "<f8"),
+                            ("dqrange", "<f8")])
+    PREV_DTYPE = _np.dtype([("p_img", "<u8"), ("h", "<i4"), ("w", "<i4"), ("s", "<i4"),
+                            ("reserved", "<i4")])
+    assert INFO_DTYPE.itemsize == INFO_BYTES and PREV_DTYPE.itemsize == PREV_BYTES
+except ImportError:  # pragma: no cover
+    pass

@@ -1,0 +1,220 @@
+// K4: mask-aware decoder (decode_gop, codec.py:160-186; _detokenize,
+// codec.py:131-140), optionally fused with reassemble (transport.py:274-305).
+//
+// One CTA decodes 8 consecutive tokens of one token row for both layers:
+//   tokens (from a token matrix, or dequantised straight out of the winning
+//   row packet -- the "first conv" of the mask-aware decoder consumes the
+//   packet scatter directly, no token matrix is materialised)
+//   -> 4-coefficient IDCT along y (ducc0 order, fct 1/16) into smem
+//   -> IDCT along x per pixel row, clip to [0,1]
+//   -> temporal-reference concealment (invalid P block <- I block)
+//   -> float32 working-resolution I and P images, cropped to (h, w).
+#include "common.cuh"
+#include "dct8.cuh"
+
+namespace sst {
+
+constexpr int kDecTok = 8;      // tokens per CTA
+constexpr int kDecThreads = 256;
+
+struct DecArgs {
+  // token-matrix source
+  const double* i_tok;
+  const double* p_tok;
+  int64_t tok_stride;          // elements between consecutive GoPs in i_tok / p_tok
+  const uint8_t* p_mask;       // [G][Ht][Wt] or null
+  // packet source (when buf != null)
+  const uint8_t* buf;
+  const int64_t* off;
+  SstPacketInfo* info;
+  const uint32_t* winner;      // [G*2][Ht]
+  int32_t* stats;              // [G*2][2]
+  int G, Ht, Wt, h, w;
+  float* out;                  // [G][2][h][w][3]
+};
+
+template <bool kFromPackets>
+__global__ void __launch_bounds__(kDecThreads) k_decode(DecArgs a) {
+  __shared__ double tok[2][kDecTok][kChannels];
+  __shared__ uint8_t valid[kDecTok];
+  __shared__ double s1[2][kDecTok][3][8][8];       // [img][tok][ch][y][x]
+  __shared__ float pix[2][8][kDecTok * 8][3];      // output tile
+
+  const int tid = threadIdx.x;
+  const int tx0 = blockIdx.x * kDecTok;
+  const int ty = blockIdx.y;
+  const int g = blockIdx.z;
+
+  // ---- 1. gather the tokens ----
+  if (kFromPackets) {
+    // warp 0 -> I row, warp 1 -> P row
+    const int wid = tid >> 5, lane = tid & 31;
+    if (wid < 2) {
+      const int mat = g * 2 + wid;
+      const uint32_t win = a.winner[(int64_t)mat * a.Ht + ty];
+      bool ok = win != 0xFFFFFFFFu;
+      const uint8_t* pkt = nullptr;
+      SstPacketInfo* p = nullptr;
+      if (ok) {
+        p = &a.info[win];
+        pkt = a.buf + a.off[win];
+        // shape contract of the fused path: W' tokens of 12 channels
+        bool bad = p->channels != kChannels || p->width < a.Wt;
+        for (int x = a.Wt + lane; !bad && x < p->width; x += 32)
+          if ((pkt[p->mask_off + (x >> 3)] >> (7 - (x & 7))) & 1) bad = true;
+        bad = __any_sync(0xffffffffu, bad);
+        if (bad) {
+          if (lane == 0) p->status = SST_PKT_SHAPE;
+          ok = false;
+        } else if (lane == 0 && blockIdx.x == 0) {
+          atomicAdd(&a.stats[2 * mat + 1], 1);          // rows_received
+        }
+      }
+      // lanes 0..7 handle one token each
+      if (lane < kDecTok) {
+        const int tx = tx0 + lane;
+        bool v = false;
+        double* dst = tok[wid][lane];
+        if (ok && tx < a.Wt) {
+          const uint8_t* mb = pkt + p->mask_off;
+          v = (mb[tx >> 3] >> (7 - (tx & 7))) & 1;
+          if (v) {
+            int pre = 0;
+            for (int b = 0; b < (tx >> 3); ++b) pre += __popc((uint32_t)mb[b]);
+            uint32_t part = (uint32_t)mb[tx >> 3] >> (8 - (tx & 7));
+            pre += __popc(part);
+            const uint8_t* src = pkt + p->payload_off + pre * kChannels;
+            const double qmin = p->dqmin;
+            const double step = p->dqrange / 255.0;    // transport.py:199
+#pragma unroll
+            for (int c = 0; c < kChannels; ++c) dst[c] = qmin + (double)src[c] * step;
+          }
+        }
+        if (!v) {
+#pragma unroll
+          for (int c = 0; c < kChannels; ++c) dst[c] = 0.0;
+        }
+        if (wid == 1) valid[lane] = v ? 1 : 0;
+      }
+    }
+  } else {
+    for (int e = tid; e < 2 * kDecTok * kChannels; e += kDecThreads) {
+      int im = e / (kDecTok * kChannels);
+      int t = (e / kChannels) % kDecTok;
+      int c = e % kChannels;
+      int tx = tx0 + t;
+      double v = 0.0;
+      if (tx < a.Wt) {
+        const double* src = (im == 0 ? a.i_tok : a.p_tok) + (int64_t)g * a.tok_stride;
+        v = src[((int64_t)ty * a.Wt + tx) * kChannels + c];
+      }
+      tok[im][t][c] = v;
+    }
+    if (tid < kDecTok) {
+      int tx = tx0 + tid;
+      valid[tid] = (tx < a.Wt && a.p_mask) ? a.p_mask[((int64_t)g * a.Ht + ty) * a.Wt + tx] : 1;
+    }
+  }
+  __syncthreads();
+
+  // ---- 2. IDCT along y for every block column x (coefficients at (0,0),
+  //         (0,1), (1,0), (2,0); codec.py:134-138) ----
+  for (int it = tid; it < 2 * kDecTok * 3 * 8; it += kDecThreads) {
+    int im = it / (kDecTok * 24);
+    int t = (it / 24) % kDecTok;
+    int ch = (it / 8) % 3;
+    int x = it % 8;
+    const double* v = tok[im][t] + ch * 4;
+    double c[8];
+#pragma unroll
+    for (int y = 0; y < 8; ++y) c[y] = 0.0;
+    if (x == 0) { c[0] = v[0]; c[1] = v[2]; c[2] = v[3]; }
+    if (x == 1) { c[0] = v[1]; }
+    dct3_8<true>(c, 1.0 / 16.0);
+#pragma unroll
+    for (int y = 0; y < 8; ++y) s1[im][t][ch][y][x] = c[y];
+  }
+  __syncthreads();
+
+  // ---- 3. IDCT along x per pixel row, clip, conceal ----
+  for (int it = tid; it < kDecTok * 3 * 8; it += kDecThreads) {
+    int t = it / 24;
+    int ch = (it / 8) % 3;
+    int y = it % 8;
+    double ci[8], cp[8];
+#pragma unroll
+    for (int x = 0; x < 8; ++x) { ci[x] = s1[0][t][ch][y][x]; cp[x] = s1[1][t][ch][y][x]; }
+    dct3_8<false>(ci, 1.0);
+    dct3_8<false>(cp, 1.0);
+    const bool keep_p = valid[t] != 0;
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+      double iv = clip01(ci[x]);
+      double pv = keep_p ? clip01(cp[x]) : iv;
+      pix[0][y][t * 8 + x][ch] = (float)iv;
+      pix[1][y][t * 8 + x][ch] = (float)pv;
+    }
+  }
+  __syncthreads();
+
+  // ---- 4. store the cropped tile ----
+  const int y0 = ty * 8, x0 = tx0 * 8;
+  const int rows = min(8, a.h - y0);
+  const int cols = min(kDecTok * 8, a.w - x0);
+  for (int e = tid; e < 2 * 8 * kDecTok * 8 * 3; e += kDecThreads) {
+    int im = e / (8 * kDecTok * 24);
+    int r = (e / (kDecTok * 24)) % 8;
+    int q = e % (kDecTok * 24);       // pixel*3 + ch within the row
+    if (r < rows && q < cols * 3) {
+      float v = (&pix[im][r][0][0])[q];
+      a.out[((((int64_t)g * 2 + im) * a.h + y0 + r) * a.w + x0) * 3 + q] = v;
+    }
+  }
+}
+
+int route_packets(SstPacketInfo* info, const int32_t* target, int64_t n, int m, int Ht,
+                  const uint8_t* exp_kind, const uint32_t* exp_gop, uint32_t* winner,
+                  int32_t* stats, cudaStream_t st);
+
+}  // namespace sst
+
+using namespace sst;
+
+extern "C" int sst_decode(const double* i_tok, const double* p_tok, int64_t tok_stride,
+                          const uint8_t* p_mask, int G, int Ht, int Wt, int h, int w, float* out,
+                          void* stream) {
+  if (G < 0 || Ht <= 0 || Wt <= 0 || h <= 0 || w <= 0) return SST_ERR_ARG;
+  if (h > Ht * 8 || w > Wt * 8) return SST_ERR_ARG;
+  if (G == 0) return SST_OK;
+  if (!i_tok || !p_tok || !out) return SST_ERR_ARG;
+  if (Ht > 65535 || G > 65535) return SST_ERR_ARG;
+  DecArgs a{};
+  a.i_tok = i_tok; a.p_tok = p_tok; a.tok_stride = tok_stride; a.p_mask = p_mask;
+  a.G = G; a.Ht = Ht; a.Wt = Wt; a.h = h; a.w = w; a.out = out;
+  dim3 grid(ceil_div(Wt, kDecTok), Ht, G);
+  k_decode<false><<<grid, kDecThreads, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+extern "C" int sst_unpack_decode(const uint8_t* buf, const int64_t* off, SstPacketInfo* info,
+                                 const int32_t* target, int64_t n, int G, int Ht, int Wt, int h,
+                                 int w, const uint32_t* exp_gop, uint32_t* winner, int32_t* stats,
+                                 float* out, void* stream) {
+  if (n < 0 || G < 0 || Ht <= 0 || Wt <= 0 || h <= 0 || w <= 0) return SST_ERR_ARG;
+  if (h > Ht * 8 || w > Wt * 8) return SST_ERR_ARG;
+  if (G == 0) return SST_OK;
+  if (!exp_gop || !winner || !stats || !out) return SST_ERR_ARG;
+  if (n > 0 && (!buf || !off || !info || !target)) return SST_ERR_ARG;
+  if (Ht > 65535 || G > 65535) return SST_ERR_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = route_packets(info, target, n, 2 * G, Ht, nullptr, exp_gop, winner, stats, st);
+  if (rc != SST_OK) return rc;
+  DecArgs a{};
+  a.buf = buf; a.off = off; a.info = info; a.winner = winner; a.stats = stats;
+  a.G = G; a.Ht = Ht; a.Wt = Wt; a.h = h; a.w = w; a.out = out;
+  dim3 grid(ceil_div(Wt, kDecTok), Ht, G);
+  k_decode<true><<<grid, kDecThreads, 0, st>>>(a);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}

@@ -1,0 +1,317 @@
+// K1: scale_gop(down) + encode_gop + token_similarity, fused.
+//
+// Reference: codec.py:202-214 (downscale_frame), codec.py:99-128
+// (_pad_to_block/_blockify/_tokenize_image), codec.py:143-157 (encode_gop),
+// selection.py:33-52 (token_similarity).
+//
+// One CTA owns one token row x TPB token columns of one GoP.  It streams the
+// 9 full-resolution frame tiles it needs (8s rows x TPB*8s pixels x RGB)
+// through a 4-deep TMA ring (mbarrier completion), box-filters them in
+// float64 into registers (frame 0 -> I source, frames 1..8 -> running P sum),
+// then runs the ducc0-exact 8x8 DCT on the two working-resolution blocks per
+// token and channel, and finally the cosine similarity of each token pair.
+// HBM traffic is one read of every input pixel plus the token write.
+#include <cstring>
+
+#include "common.cuh"
+#include "dct8.cuh"
+#include "tma.cuh"
+
+namespace sst {
+
+template <int S>
+struct EncCfg {
+  static constexpr int TPB = (S == 3) ? 3 : 4;      // tokens per CTA
+  static constexpr int R = 8 * S;                   // full-res rows per tile
+  static constexpr int IN = TPB * 8 * S * 3;        // floats per tile row
+  static constexpr int NT = 64 * TPB;               // one thread per working pixel
+  static constexpr int NST = 4;                     // TMA ring depth
+  static constexpr int TILE = R * IN;               // floats per tile
+  static constexpr int RING_BYTES = NST * TILE * 4;
+  static constexpr int IMG_D = 2 * 8 * 8 * TPB * 3;            // imgbuf doubles
+  static constexpr int S1_D = 2 * TPB * 3 * 3 * 8;             // stage-1 doubles
+  static constexpr int TOK_D = 2 * TPB * kChannels;            // token doubles
+  static constexpr int DCT_BYTES = (IMG_D + S1_D + TOK_D) * 8;
+  static constexpr int MAIN_BYTES = RING_BYTES > DCT_BYTES ? RING_BYTES : DCT_BYTES;
+  static constexpr int SMEM = MAIN_BYTES + 128 + NST * 8;
+};
+
+struct EncArgs {
+  const float* frames;
+  int G, H, W, h, w, Ht, Wt;
+  double* tok;
+  double* sim;
+};
+
+// numpy pairwise order for a 12-long reduction (8-way unrolled block + tail)
+__device__ __forceinline__ double pairwise12(const double* x) {
+  double r = ((x[0] + x[1]) + (x[2] + x[3])) + ((x[4] + x[5]) + (x[6] + x[7]));
+  r = r + x[8];
+  r = r + x[9];
+  r = r + x[10];
+  r = r + x[11];
+  return 0.0 + r;  // add.reduce identity start
+}
+
+__device__ __forceinline__ double cosine12(const double* p, const double* i) {
+  double a[12], b[12], c[12];
+#pragma unroll
+  for (int k = 0; k < 12; ++k) {
+    a[k] = p[k] * i[k];
+    b[k] = p[k] * p[k];
+    c[k] = i[k] * i[k];
+  }
+  double dot = pairwise12(a);
+  double pn = sqrt(pairwise12(b));
+  double in = sqrt(pairwise12(c));
+  double denom = pn * in;
+  double s = denom > 0.0 ? dot / denom : 0.0;
+  if (pn == 0.0 && in == 0.0) s = 1.0;
+  return clip_pm1(s);
+}
+
+template <int S, bool kTMA>
+__global__ void __launch_bounds__(EncCfg<S>::NT)
+    k_encode(const __grid_constant__ CUtensorMap tmap, EncArgs a) {
+  using C = EncCfg<S>;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  float* ring = reinterpret_cast<float*>(smem_raw);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + C::MAIN_BYTES);  // mbarriers
+
+  const int tid = threadIdx.x;
+  const int tx0 = blockIdx.x * C::TPB;
+  const int ty = blockIdx.y;
+  const int g = blockIdx.z;
+  const int row0 = ty * C::R;                 // first full-res row of the tile
+  const int col0 = tx0 * 8 * S;               // first full-res pixel column
+  const size_t frame_elems = (size_t)a.H * a.W * 3;
+  const float* gop = a.frames + (size_t)g * kGop * frame_elems;
+
+  if (kTMA && tid == 0) {
+    for (int st = 0; st < C::NST; ++st) mbar_init(&full[st], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (kTMA && tid == 0) {
+    for (int f = 0; f < C::NST; ++f) {
+      mbar_expect_tx(&full[f], C::TILE * 4);
+      tma_load_3d(ring + f * C::TILE, &tmap, col0 * 3, row0, g * kGop + f, &full[f]);
+    }
+  }
+
+  // this thread's working pixel (clamped = working-res edge replication,
+  // codec.py:99-105) and its s x s full-res window (clamped = full-res edge
+  // replication, codec.py:209-211), as offsets inside a tile
+  const int wy = tid / (8 * C::TPB);
+  const int wx = tid % (8 * C::TPB);
+  const int ay = min(ty * 8 + wy, a.h - 1);
+  const int ax = min(tx0 * 8 + wx, a.w - 1);
+  int off[S * S];
+#pragma unroll
+  for (int j = 0; j < S; ++j) {
+    int r = min(ay * S + j, a.H - 1) - row0;
+#pragma unroll
+    for (int l = 0; l < S; ++l) {
+      int c = min(ax * S + l, a.W - 1) - col0;
+      off[j * S + l] = r * C::IN + c * 3;
+    }
+  }
+
+  float ival[3];
+  double pacc[3];
+  constexpr double div_ss = (double)(S * S);
+
+  for (int f = 0; f < kGop; ++f) {
+    const int st = f % C::NST;
+    float* tile = ring + st * C::TILE;
+    if (kTMA) {
+      mbar_wait(&full[st], (f / C::NST) & 1);
+    } else {
+      // plain cooperative load of the in-bounds part of the tile
+      const float* src = gop + (size_t)f * frame_elems;
+      for (int e = tid; e < C::TILE; e += C::NT) {
+        int r = e / C::IN, c = e % C::IN;
+        int gr = row0 + r, gc = col0 * 3 + c;
+        if (gr < a.H && gc < a.W * 3) tile[e] = __ldg(src + (size_t)gr * a.W * 3 + gc);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      // numpy add.reduce starts from the identity 0.0 (matters only for -0.0)
+      double acc = 0.0 + (double)tile[off[0] + ch];
+#pragma unroll
+      for (int q = 1; q < S * S; ++q) acc = acc + (double)tile[off[q] + ch];
+      float wv = __double2float_rn(acc / div_ss);     // Frame float32 storage
+      if (f == 0) {
+        ival[ch] = wv;
+      } else if (f == 1) {
+        pacc[ch] = 0.0 + (double)wv;
+      } else {
+        pacc[ch] = pacc[ch] + (double)wv;              // codec.py:151-152, sequential
+      }
+    }
+    __syncthreads();  // everyone is done with this stage
+    if (kTMA && tid == 0 && f + C::NST < kGop) {
+      mbar_expect_tx(&full[st], C::TILE * 4);
+      tma_load_3d(tile, &tmap, col0 * 3, row0, g * kGop + f + C::NST, &full[st]);
+    }
+  }
+
+  // ---- 8x8 DCT of the I and P working blocks (ring is free now) ----
+  double* img = reinterpret_cast<double*>(smem_raw);                 // [2][8][8*TPB][3]
+  double* s1 = img + C::IMG_D;                                       // [2][TPB][3][3][8]
+  double* tk = s1 + C::S1_D;                                         // [2][TPB][12]
+  {
+    const int base = (wy * 8 * C::TPB + wx) * 3;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      img[base + ch] = (double)ival[ch];
+      img[8 * 8 * C::TPB * 3 + base + ch] = pacc[ch] / 8.0;
+    }
+  }
+  __syncthreads();
+  // stage 1: along y (axis -2) for every block column, fct = 1/16
+  for (int it = tid; it < 48 * C::TPB; it += C::NT) {
+    int im = it / (24 * C::TPB);
+    int rem = it % (24 * C::TPB);
+    int t = rem / 24, ch = (rem % 24) / 8, x = rem % 8;
+    double c[8];
+    const double* src = img + im * (8 * 8 * C::TPB * 3) + (t * 8 + x) * 3 + ch;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) c[y] = src[y * 8 * C::TPB * 3];
+    dct2_8<true>(c, 1.0 / 16.0);
+    double* dst = s1 + ((im * C::TPB + t) * 3 + ch) * 24;
+    dst[x] = c[0];
+    dst[8 + x] = c[1];
+    dst[16 + x] = c[2];
+  }
+  __syncthreads();
+  // stage 2: along x for rows y = 0, 1, 2; keep (0,0) (0,1) (1,0) (2,0)
+  for (int it = tid; it < 18 * C::TPB; it += C::NT) {
+    int im = it / (9 * C::TPB);
+    int rem = it % (9 * C::TPB);
+    int t = rem / 9, ch = (rem % 9) / 3, yk = rem % 3;
+    double c[8];
+    const double* src = s1 + ((im * C::TPB + t) * 3 + ch) * 24 + yk * 8;
+#pragma unroll
+    for (int x = 0; x < 8; ++x) c[x] = src[x];
+    dct2_8<false>(c, 1.0);
+    double* dst = tk + (im * C::TPB + t) * kChannels + ch * 4;
+    if (yk == 0) {
+      dst[0] = c[0];
+      dst[1] = c[1];
+    } else {
+      dst[yk + 1] = c[0];
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < 2 * C::TPB * kChannels; e += C::NT) {
+    int im = e / (C::TPB * kChannels);
+    int t = (e / kChannels) % C::TPB;
+    int k = e % kChannels;
+    int tx = tx0 + t;
+    if (tx < a.Wt)
+      a.tok[((((size_t)g * 2 + im) * a.Ht + ty) * a.Wt + tx) * kChannels + k] = tk[e];
+  }
+  if (a.sim != nullptr && tid < C::TPB && tx0 + tid < a.Wt) {
+    const double* iv = tk + tid * kChannels;
+    const double* pv = tk + (C::TPB + tid) * kChannels;
+    a.sim[((size_t)g * a.Ht + ty) * a.Wt + tx0 + tid] = cosine12(pv, iv);
+  }
+}
+
+// ---- standalone box downscale (downscale_frame, codec.py:202-214) ----
+template <int S>
+__global__ void k_downscale(const float* __restrict__ src, int64_t n, int H, int W, int h, int w,
+                            float* __restrict__ dst) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t total = n * h * w;
+  if (idx >= total) return;
+  int x = (int)(idx % w);
+  int64_t t = idx / w;
+  int y = (int)(t % h);
+  int64_t f = t / h;
+  const float* fr = src + f * (int64_t)H * W * 3;
+  float* out = dst + idx * 3;
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      int r = min(y * S + j, H - 1);
+#pragma unroll
+      for (int l = 0; l < S; ++l) {
+        int c = min(x * S + l, W - 1);
+        double v = (double)__ldg(fr + ((int64_t)r * W + c) * 3 + ch);
+        acc = acc + v;
+      }
+    }
+    out[ch] = __double2float_rn(acc / (double)(S * S));
+  }
+}
+
+template <int S>
+static int launch_encode(const float* frames, int G, int H, int W, double* tok, double* sim,
+                         cudaStream_t stream) {
+  using C = EncCfg<S>;
+  EncArgs a;
+  a.frames = frames;
+  a.G = G; a.H = H; a.W = W;
+  a.h = ceil_div(H, S);
+  a.w = ceil_div(W, S);
+  a.Ht = ceil_div(a.h, kBlock);
+  a.Wt = ceil_div(a.w, kBlock);
+  a.tok = tok;
+  a.sim = sim;
+  if (a.Ht > 65535 || G > 65535) return SST_ERR_ARG;
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  bool use_tma = make_tmap_f32_3d(&tmap, frames, (uint64_t)W * 3, (uint64_t)H, (uint64_t)G * kGop,
+                                  C::IN, C::R);
+  dim3 grid(ceil_div(a.Wt, C::TPB), a.Ht, G);
+  if (use_tma) {
+    SST_CUDA_TRY(cudaFuncSetAttribute(k_encode<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      C::SMEM));
+    k_encode<S, true><<<grid, C::NT, C::SMEM, stream>>>(tmap, a);
+  } else {
+    SST_CUDA_TRY(cudaFuncSetAttribute(k_encode<S, false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+    k_encode<S, false><<<grid, C::NT, C::SMEM, stream>>>(tmap, a);
+  }
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+}  // namespace sst
+
+using namespace sst;
+
+extern "C" int sst_encode(const float* frames, int G, int H, int W, int s, double* tok, double* sim,
+                          void* stream) {
+  if (!frames || !tok || G <= 0 || H <= 0 || W <= 0) return SST_ERR_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (s) {
+    case 1: return launch_encode<1>(frames, G, H, W, tok, sim, st);
+    case 2: return launch_encode<2>(frames, G, H, W, tok, sim, st);
+    case 3: return launch_encode<3>(frames, G, H, W, tok, sim, st);
+    default: return SST_ERR_ARG;
+  }
+}
+
+extern "C" int sst_downscale(const float* frames, int64_t n, int H, int W, int s, float* out,
+                             void* stream) {
+  if (!frames || !out || n <= 0 || H <= 0 || W <= 0) return SST_ERR_ARG;
+  if (s != 2 && s != 3) return SST_ERR_ARG;
+  int h = ceil_div(H, s), w = ceil_div(W, s);
+  int64_t total = n * h * w;
+  int threads = 256;
+  int64_t blocks = ceil_div64(total, threads);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  if (s == 2)
+    k_downscale<2><<<(unsigned)blocks, threads, 0, st>>>(frames, n, H, W, h, w, out);
+  else
+    k_downscale<3><<<(unsigned)blocks, threads, 0, st>>>(frames, n, H, W, h, w, out);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}

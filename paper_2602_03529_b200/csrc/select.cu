@@ -1,0 +1,215 @@
+// K2: intelligent dropping -- token_similarity, top_k_drop_mask,
+// apply_token_mask (selection.py:33-79, codec.py:189-196).
+//
+// The top-k is an exact radix select over orderable 64-bit similarity keys
+// (8 passes x 8 bits, one CTA per map) followed by an index-ordered scan of
+// the keys equal to the k-th largest, which reproduces the reference's stable
+// argsort tie-break (row-major order among equal similarities) without a sort.
+#include "common.cuh"
+
+namespace sst {
+
+// numpy pairwise_sum (n <= 128 path: 8 accumulators, combine, tail); the
+// reduction result is identity (0.0) + pairwise block.
+__device__ double np_sum(const double* x, int n) {
+  if (n < 8) {
+    double r = 0.0;
+    for (int i = 0; i < n; ++i) r = r + x[i];
+    return 0.0 + r;
+  }
+  double r0 = x[0], r1 = x[1], r2 = x[2], r3 = x[3], r4 = x[4], r5 = x[5], r6 = x[6], r7 = x[7];
+  int i = 8;
+  for (; i < n - (n % 8); i += 8) {
+    r0 = r0 + x[i]; r1 = r1 + x[i + 1]; r2 = r2 + x[i + 2]; r3 = r3 + x[i + 3];
+    r4 = r4 + x[i + 4]; r5 = r5 + x[i + 5]; r6 = r6 + x[i + 6]; r7 = r7 + x[i + 7];
+  }
+  double r = ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7));
+  for (; i < n; ++i) r = r + x[i];
+  return 0.0 + r;
+}
+
+constexpr int kMaxSimC = 128;
+
+__global__ void k_similarity(const double* __restrict__ p, const double* __restrict__ iv,
+                             int64_t n, int C, double* __restrict__ sim) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  const double* pp = p + t * C;
+  const double* ii = iv + t * C;
+  double a[kMaxSimC];
+  for (int k = 0; k < C; ++k) a[k] = pp[k] * ii[k];
+  double dot = np_sum(a, C);
+  for (int k = 0; k < C; ++k) a[k] = pp[k] * pp[k];
+  double pn = sqrt(np_sum(a, C));
+  for (int k = 0; k < C; ++k) a[k] = ii[k] * ii[k];
+  double in = sqrt(np_sum(a, C));
+  double denom = pn * in;
+  double s = denom > 0.0 ? dot / denom : 0.0;
+  if (pn == 0.0 && in == 0.0) s = 1.0;
+  sim[t] = clip_pm1(s);
+}
+
+// larger similarity -> larger key; -0.0 and +0.0 map to the same key
+__device__ __forceinline__ uint64_t sim_key(double x) {
+  if (x == 0.0) x = 0.0;
+  uint64_t b = (uint64_t)__double_as_longlong(x);
+  return (b & 0x8000000000000000ull) ? ~b : (b | 0x8000000000000000ull);
+}
+
+constexpr int kSelThreads = 1024;
+
+// Per map g: drop[j] = 1 for the k[g] highest-similarity positions.
+// Optionally applies the drop to the P tokens / mask of a [G][2][n][12]
+// token batch and its [G][2][n] mask (fused apply_token_mask).
+__global__ void __launch_bounds__(kSelThreads)
+    k_topk(const double* __restrict__ sim, int64_t n, const int32_t* __restrict__ kk,
+           uint8_t* __restrict__ drop, double* tok, uint8_t* p_mask) {
+  __shared__ uint32_t hist[256];
+  __shared__ uint64_t s_prefix;
+  __shared__ int64_t s_krem;
+  __shared__ int s_warp[kSelThreads / 32];
+  __shared__ int64_t s_running;
+
+  const int g = blockIdx.x;
+  const int tid = threadIdx.x;
+  const double* sm = sim + (int64_t)g * n;
+  int64_t k = kk[g];
+  if (k < 0) k = 0;
+  if (k > n) k = n;
+
+  uint64_t prefix = 0, pmask = 0;
+  int64_t krem = k;
+  if (k > 0) {
+    // radix select of the k-th largest key (1-indexed), MSB digit first
+    for (int shift = 56; shift >= 0; shift -= 8) {
+      for (int b = tid; b < 256; b += kSelThreads) hist[b] = 0;
+      __syncthreads();
+      for (int64_t j = tid; j < n; j += kSelThreads) {
+        uint64_t key = sim_key(__ldg(sm + j));
+        if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 0xFF], 1u);
+      }
+      __syncthreads();
+      if (tid == 0) {
+        int64_t cum = 0;
+        int d = 255;
+        for (; d >= 0; --d) {
+          if (cum + hist[d] >= krem) break;
+          cum += hist[d];
+        }
+        s_prefix = prefix | ((uint64_t)d << shift);
+        s_krem = krem - cum;
+      }
+      __syncthreads();
+      prefix = s_prefix;
+      krem = s_krem;
+      pmask |= (0xFFull << shift);
+      __syncthreads();
+    }
+    // prefix is now the k-th largest key T; krem = how many of the keys == T
+    // (in index order) are dropped.
+  }
+  if (tid == 0) s_running = 0;
+  __syncthreads();
+  const uint64_t T = prefix;
+  const int lane = tid & 31, wid = tid >> 5;
+  for (int64_t base = 0; base < n; base += kSelThreads) {
+    int64_t j = base + tid;
+    uint64_t key = 0;
+    bool valid = j < n;
+    if (valid) key = sim_key(__ldg(sm + j));
+    bool eq = valid && k > 0 && key == T;
+    unsigned bal = __ballot_sync(0xffffffffu, eq);
+    int before = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 31) s_warp[wid] = __popc(bal);
+    __syncthreads();
+    int warp_off = 0;
+    for (int w2 = 0; w2 < wid; ++w2) warp_off += s_warp[w2];
+    int64_t rank = s_running + warp_off + before;   // index-ordered rank among equals
+    if (valid) {
+      bool d = k > 0 && (key > T || (eq && rank < krem));
+      if (drop) drop[(int64_t)g * n + j] = d ? 1 : 0;
+      if (tok) {
+        // apply_token_mask on the P matrix (codec.py:189-196)
+        uint8_t* mrow = p_mask + ((int64_t)g * 2 + 1) * n + j;   // [G][2][n]: P half
+        uint8_t m = *mrow;
+        uint8_t nm = (m && !d) ? 1 : 0;
+        *mrow = nm;
+        if (!nm) {
+          double* v = tok + (((int64_t)g * 2 + 1) * n + j) * kChannels;
+#pragma unroll
+          for (int c = 0; c < kChannels; ++c) v[c] = 0.0;
+        }
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int tot = 0;
+      for (int w2 = 0; w2 < kSelThreads / 32; ++w2) tot += s_warp[w2];
+      s_running += tot;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void k_apply_mask(double* __restrict__ values, uint8_t* __restrict__ mask,
+                             const uint8_t* __restrict__ drop, int64_t n, int C) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  uint8_t nm = (mask[t] && !drop[t]) ? 1 : 0;
+  mask[t] = nm;
+  if (!nm) {
+    double* v = values + t * C;
+    for (int c = 0; c < C; ++c) v[c] = 0.0;
+  }
+}
+
+}  // namespace sst
+
+using namespace sst;
+
+extern "C" int sst_similarity(const double* p, const double* i, int64_t n, int C, double* sim,
+                              void* stream) {
+  if (n < 0 || C < 0) return SST_ERR_ARG;
+  if (n == 0) return SST_OK;
+  if (!p || !i || !sim) return SST_ERR_ARG;
+  if (C > kMaxSimC) return SST_ERR_UNSUPPORTED;
+  int threads = 128;
+  k_similarity<<<(unsigned)ceil_div64(n, threads), threads, 0, static_cast<cudaStream_t>(stream)>>>(
+      p, i, n, C, sim);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+extern "C" int sst_topk_mask(const double* sim, int G, int64_t n, const int32_t* k, uint8_t* drop,
+                             void* stream) {
+  if (G < 0 || n < 0) return SST_ERR_ARG;
+  if (G == 0 || n == 0) return SST_OK;
+  if (!sim || !k || !drop) return SST_ERR_ARG;
+  k_topk<<<G, kSelThreads, 0, static_cast<cudaStream_t>(stream)>>>(sim, n, k, drop, nullptr,
+                                                                    nullptr);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+extern "C" int sst_apply_mask(double* values, uint8_t* mask, const uint8_t* drop, int64_t n, int C,
+                              void* stream) {
+  if (n < 0 || C < 0) return SST_ERR_ARG;
+  if (n == 0) return SST_OK;
+  if (!values || !mask || !drop) return SST_ERR_ARG;
+  int threads = 256;
+  k_apply_mask<<<(unsigned)ceil_div64(n, threads), threads, 0, static_cast<cudaStream_t>(stream)>>>(
+      values, mask, drop, n, C);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+extern "C" int sst_select_drop(const double* sim, double* tok, uint8_t* p_mask, int G, int Ht,
+                               int Wt, const int32_t* k, uint8_t* drop, void* stream) {
+  if (G < 0 || Ht < 0 || Wt < 0) return SST_ERR_ARG;
+  int64_t n = (int64_t)Ht * Wt;
+  if (G == 0 || n == 0) return SST_OK;
+  if (!sim || !tok || !p_mask || !k) return SST_ERR_ARG;
+  k_topk<<<G, kSelThreads, 0, static_cast<cudaStream_t>(stream)>>>(sim, n, k, drop, tok, p_mask);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}

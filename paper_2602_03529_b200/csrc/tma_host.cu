@@ -1,0 +1,41 @@
+// Host-side tensor map encoding (cuTensorMapEncodeTiled via the runtime's
+// driver entry point, so the library does not link libcuda directly).
+#include <cudaTypedefs.h>
+#include <mutex>
+
+#include "tma.cuh"
+
+namespace sst {
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool make_tmap_f32_3d(CUtensorMap* map, const void* base, uint64_t dim0, uint64_t dim1,
+                      uint64_t dim2, uint32_t box0, uint32_t box1) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const uint64_t row_bytes = dim0 * sizeof(float);
+  if ((reinterpret_cast<uintptr_t>(base) & 15u) || (row_bytes & 15u)) return false;
+  if (box0 > 256 || box1 > 256 || (box0 * sizeof(float)) % 16 != 0) return false;
+  if (dim0 >= (1ull << 32) || dim1 >= (1ull << 32) || dim2 >= (1ull << 32)) return false;
+  cuuint64_t gdim[3] = {dim0, dim1, dim2};
+  cuuint64_t gstride[2] = {row_bytes, row_bytes * dim1};
+  cuuint32_t box[3] = {box0, box1, 1};
+  cuuint32_t estride[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), gdim, gstride,
+                  box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace sst

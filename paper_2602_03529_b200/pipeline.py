@@ -1,0 +1,286 @@
+"""Batched, device-resident codec path: the B200 hot path behind the
+reference API.
+
+``GopCodec`` runs a batch of GoPs of one geometry (H, W, s) through
+
+    K1 sst_encode        scale_gop(down) + encode_gop + token_similarity
+    K2 sst_select_drop   build_drop_mask + apply_token_mask (P layer)
+    K3 sst_packetize     packetize_tokens + TokenPacket.to_bytes (I rows, P rows)
+    K4 sst_parse +       parse_packet + reassemble x2 + decode_gop
+       sst_unpack_decode (mask-aware decoder reads tokens out of the packets)
+    K5 sst_upscale_blend scale_gop(up, crop) + blend_boundary, 9 frames out
+
+which is the reference's per-GoP composition (session.py:134-170 sender,
+session.py:323-348 receiver) minus the emulated network.  All buffers are
+allocated once; every call is stream-ordered on torch's current stream.
+
+``StreamBank`` keeps many independent streams (each with its own previous
+GoP for boundary blending and its own per-GoP scale) and routes every step's
+GoPs to one ``GopCodec`` per scale.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _dev, _lib
+from .transport import token_packet_wire_size
+
+GOP = 9
+CHANNELS = 12
+
+
+def _cdiv(a: int, b: int) -> int:
+    return -(-a // b)
+
+
+class StageTimer:
+    """CUDA-event timing of each kernel stage on the launching (current) stream."""
+
+    def __init__(self):
+        self.pairs: dict = {}
+        self._open: dict = {}
+
+    def begin(self, name: str) -> None:
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self._open[name] = ev
+
+    def end(self, name: str) -> None:
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self.pairs.setdefault(name, []).append((self._open.pop(name), ev))
+
+    def reset(self) -> None:
+        self.pairs.clear()
+        self._open.clear()
+
+    def summary(self) -> dict:
+        """{stage: (total_ms, launches)} -- call after synchronising."""
+        return {k: (sum(a.elapsed_time(b) for a, b in v), len(v)) for k, v in self.pairs.items()}
+
+
+class _NoTimer:
+    def begin(self, name):
+        pass
+
+    def end(self, name):
+        pass
+
+
+_NO_TIMER = _NoTimer()
+
+
+class GopCodec:
+    """Device buffers + kernel launches for up to ``g_max`` GoPs of (H, W, s)."""
+
+    def __init__(self, g_max: int, H: int, W: int, s: int, blend_n: int = 2):
+        if s not in (2, 3):
+            raise ValueError(f"scale must be 2 or 3, got {s}")
+        dev = _dev.device()
+        self.g_max, self.H, self.W, self.s, self.blend_n = g_max, H, W, s, blend_n
+        self.h, self.w = _cdiv(H, s), _cdiv(W, s)
+        self.Ht, self.Wt = _cdiv(self.h, 8), _cdiv(self.w, 8)
+        if self.Ht > 0xFFFF:
+            raise ValueError(f"matrix has {self.Ht} rows; the row index field is 16-bit")
+        n = self.Ht * self.Wt
+        self.slot = (token_packet_wire_size(self.Wt, CHANNELS) + 15) & ~15
+        self.n_pkt_per_gop = 2 * self.Ht
+        G = g_max
+        f64, u8, i32 = torch.float64, torch.uint8, torch.int32
+        self.tok = torch.empty((G, 2, self.Ht, self.Wt, CHANNELS), dtype=f64, device=dev)
+        self.sim = torch.empty((G, self.Ht, self.Wt), dtype=f64, device=dev)
+        self.mask = torch.ones((G, 2, self.Ht, self.Wt), dtype=u8, device=dev)
+        self.drop = torch.zeros((G, self.Ht, self.Wt), dtype=u8, device=dev)
+        self.k = torch.zeros((G,), dtype=i32, device=dev)
+        self.kind = torch.tensor([0, 1] * G, dtype=u8, device=dev)
+        self.gop_id = torch.zeros((2 * G,), dtype=torch.int32, device=dev)   # u32 bits
+        self.scale = torch.full((2 * G,), s, dtype=u8, device=dev)
+        npk = G * self.n_pkt_per_gop
+        self.arena = torch.empty((npk, self.slot), dtype=u8, device=dev)
+        self.lengths = torch.empty((npk,), dtype=i32, device=dev)
+        self.offsets = torch.arange(npk, dtype=torch.int64, device=dev) * self.slot
+        self.info = torch.empty((npk * _lib.INFO_BYTES,), dtype=u8, device=dev)
+        # arrival order = slot order: packet p of GoP g targets matrix 2g + kind
+        tgt = np.repeat(np.arange(G) * 2, self.n_pkt_per_gop) + \
+            np.tile(np.repeat([0, 1], self.Ht), G)
+        self.target = torch.from_numpy(tgt.astype(np.int32)).to(dev)
+        self.exp_gop = torch.zeros((G,), dtype=torch.int32, device=dev)
+        self.winner = torch.empty((2 * G * self.Ht,), dtype=torch.int32, device=dev)
+        self.stats = torch.empty((2 * G * 2,), dtype=i32, device=dev)
+        # double-buffered working images so the next step can still read the
+        # previous GoP's P image for boundary blending
+        self.img = [torch.empty((G, 2, self.h, self.w, 3), dtype=torch.float32, device=dev)
+                    for _ in range(2)]
+        self.n = n
+        self.timer = _NO_TIMER
+
+    # -- helpers -------------------------------------------------------
+    def drop_k(self, rate: float) -> int:
+        return int(np.floor(rate * self.n + 0.5))
+
+    def set_gop_ids(self, gop_ids) -> None:
+        ids = torch.as_tensor(np.asarray(gop_ids, dtype=np.uint32).view(np.int32),
+                              device=self.exp_gop.device)
+        g = ids.numel()
+        self.exp_gop[:g].copy_(ids)
+        self.gop_id[:2 * g].copy_(ids.repeat_interleave(2))
+
+    # -- sender --------------------------------------------------------
+    def encode(self, frames: torch.Tensor, g: int, drop_k: int = 0) -> None:
+        """K1 + K2 + K3 for frames[:g] ([g, 9, H, W, 3] float32, contiguous)."""
+        st = _dev.stream()
+        tm = self.timer
+        tm.begin("K1_encode")
+        _lib.call("sst_encode", frames.data_ptr(), g, self.H, self.W, self.s,
+                  self.tok.data_ptr(), self.sim.data_ptr(), st)
+        tm.end("K1_encode")
+        self.mask[:g].fill_(1)
+        if drop_k > 0:
+            self.k[:g].fill_(drop_k)
+            tm.begin("K2_select_drop")
+            _lib.call("sst_select_drop", self.sim.data_ptr(), self.tok.data_ptr(),
+                      self.mask.data_ptr(), g, self.Ht, self.Wt, self.k.data_ptr(),
+                      self.drop.data_ptr(), st)
+            tm.end("K2_select_drop")
+        tm.begin("K3_packetize")
+        _lib.call("sst_packetize", self.tok.data_ptr(), self.mask.data_ptr(), 2 * g, self.Ht,
+                  self.Wt, CHANNELS, self.kind.data_ptr(), self.gop_id.data_ptr(),
+                  self.scale.data_ptr(), self.arena.data_ptr(), self.slot,
+                  self.lengths.data_ptr(), st)
+        tm.end("K3_packetize")
+
+    # -- receiver ------------------------------------------------------
+    def decode(self, g: int, parity: int, arena: torch.Tensor | None = None,
+               present: torch.Tensor | None = None) -> torch.Tensor:
+        """K4: parse + first-wins reassembly + mask-aware decode of the packet
+        slots of g GoPs; returns the [g, 2, h, w, 3] working images."""
+        st = _dev.stream()
+        arena = self.arena if arena is None else arena
+        npk = g * self.n_pkt_per_gop
+        img = self.img[parity]
+        tm = self.timer
+        tm.begin("K4_parse")
+        _lib.call("sst_parse", arena.data_ptr(), self.offsets.data_ptr(),
+                  self.lengths.data_ptr(), None if present is None else present.data_ptr(), npk,
+                  self.info.data_ptr(), st)
+        tm.end("K4_parse")
+        tm.begin("K4_unpack_decode")
+        _lib.call("sst_unpack_decode", arena.data_ptr(), self.offsets.data_ptr(),
+                  self.info.data_ptr(), self.target.data_ptr(), npk, g, self.Ht, self.Wt, self.h,
+                  self.w, self.exp_gop.data_ptr(), self.winner.data_ptr(), self.stats.data_ptr(),
+                  img.data_ptr(), st)
+        tm.end("K4_unpack_decode")
+        return img[:g]
+
+    # -- reconstruction ------------------------------------------------
+    def reconstruct(self, g: int, parity: int, out: torch.Tensor,
+                    prev: torch.Tensor | None = None) -> None:
+        """K5: [g, 9, H, W, 3] float32 output frames; prev = device
+        SstPrevDesc[g] as uint8 bytes (or None: no blending)."""
+        self.timer.begin("K5_upscale_blend")
+        _lib.call("sst_upscale_blend", self.img[parity].data_ptr(), g, self.h, self.w, self.s,
+                  self.H, self.W, None if prev is None else prev.data_ptr(), self.blend_n,
+                  out.data_ptr(), _dev.stream())
+        self.timer.end("K5_upscale_blend")
+
+    def packet_status(self, g: int) -> np.ndarray:
+        info = _dev.d2h(self.info[: g * self.n_pkt_per_gop * _lib.INFO_BYTES])
+        return info.view(_lib.INFO_DTYPE)["status"]
+
+
+class _DescRing:
+    """Pinned-host -> device staging for small per-step descriptor tables.
+    A slot is reused only after the kernel that consumed it has completed
+    (CUDA event), so the host may run several steps ahead of the GPU."""
+
+    def __init__(self, nbytes: int, slots: int = 4):
+        dev = _dev.device()
+        self.host = [torch.empty((nbytes,), dtype=torch.uint8, pin_memory=True) for _ in range(slots)]
+        self.dev = [torch.empty((nbytes,), dtype=torch.uint8, device=dev) for _ in range(slots)]
+        self.events = [None] * slots
+        self.i = 0
+
+    def stage(self, raw: np.ndarray) -> tuple:
+        j = self.i
+        self.i = (self.i + 1) % len(self.host)
+        if self.events[j] is not None:
+            self.events[j].synchronize()
+        n = raw.nbytes
+        self.host[j][:n].copy_(torch.from_numpy(raw.view(np.uint8)))
+        self.dev[j][:n].copy_(self.host[j][:n], non_blocking=True)
+        return self.dev[j], j
+
+    def release(self, j: int) -> None:
+        ev = torch.cuda.Event()
+        ev.record()
+        self.events[j] = ev
+
+
+class StreamBank:
+    """``n_streams`` independent streams of (H, W) video; each step encodes,
+    transports and reconstructs one GoP per stream.  Streams may change scale
+    from GoP to GoP (variable-resolution mode); boundary blending always uses
+    the stream's previous reconstruction, at whatever scale it was coded."""
+
+    def __init__(self, n_streams: int, H: int, W: int, scales=(2, 3), blend_n: int = 2):
+        if blend_n > 4:
+            raise ValueError("the fused reconstruction blends at most 4 frames")
+        self.n, self.H, self.W, self.blend_n = n_streams, H, W, blend_n
+        self.codecs = {s: GopCodec(n_streams, H, W, s, blend_n) for s in scales}
+        self.prev_host = np.zeros(n_streams, dtype=_lib.PREV_DTYPE)
+        self.rings = {s: _DescRing(n_streams * _lib.PREV_BYTES) for s in scales}
+        self.step_idx = 0
+        self.launches = 0          # kernels of this library launched by step()
+        # where each stream's last P image lives: (scale, parity, slot) or None
+        self.last = [None] * n_streams
+
+    def step(self, frames_by_scale: dict, out_by_scale: dict, stream_ids_by_scale: dict,
+             gop_ids_by_scale: dict, drop_rate: float = 0.0, present_by_scale: dict | None = None
+             ) -> None:
+        """One GoP for every stream.  ``frames_by_scale[s]`` holds the GoPs of
+        the streams coded at scale s this step ([g, 9, H, W, 3]); outputs go to
+        ``out_by_scale[s]`` in the same order.  ``present_by_scale[s]`` (uint8
+        per packet slot, I rows then P rows per GoP) simulates network loss."""
+        parity = self.step_idx & 1
+        for s, frames in frames_by_scale.items():
+            codec = self.codecs[s]
+            ids = stream_ids_by_scale[s]
+            g = len(ids)
+            if g == 0:
+                continue
+            codec.set_gop_ids(gop_ids_by_scale[s])
+            codec.encode(frames, g, codec.drop_k(drop_rate))
+            present = None if present_by_scale is None else present_by_scale.get(s)
+            codec.decode(g, parity, present=present)
+            # K1 + K2 (if dropping) + K3 + K4 parse + 4 (init/route/dups/decode) + K5
+            self.launches += 1 + (1 if codec.drop_k(drop_rate) > 0 else 0) + 1 + 1 + 4 + 1
+            staged = self._prev_descs(s, ids)
+            codec.reconstruct(g, parity, out_by_scale[s], None if staged is None else staged[0])
+            if staged is not None:
+                self.rings[s].release(staged[1])
+        for s, ids in stream_ids_by_scale.items():
+            for slot, sid in enumerate(ids):
+                self.last[sid] = (s, parity, slot)
+        self.step_idx += 1
+
+    def set_timer(self, timer) -> None:
+        for c in self.codecs.values():
+            c.timer = timer if timer is not None else _NO_TIMER
+
+    def _prev_descs(self, s: int, ids):
+        if all(self.last[i] is None for i in ids):
+            return None
+        rec = self.prev_host[:len(ids)]
+        rec[:] = 0
+        for j, sid in enumerate(ids):
+            loc = self.last[sid]
+            if loc is None:
+                continue
+            s, par, slot = loc
+            c = self.codecs[s]
+            img = c.img[par]
+            rec[j]["p_img"] = img.data_ptr() + ((slot * 2 + 1) * c.h * c.w * 3) * 4
+            rec[j]["h"], rec[j]["w"], rec[j]["s"] = c.h, c.w, s
+        return self.rings[s].stage(rec)

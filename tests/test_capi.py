@@ -1,0 +1,90 @@
+"""CPU: the C-ABI library loads without a GPU and exports exactly the entry
+points include/semstream_b200.h declares (no compute calls here)."""
+
+import ctypes
+import re
+import subprocess
+from pathlib import Path
+
+import pytest
+
+ROOT = Path(__file__).resolve().parent.parent
+HEADER = ROOT / "include" / "semstream_b200.h"
+
+
+def _declared():
+    txt = HEADER.read_text()
+    return sorted(set(re.findall(r"SST_API\s+\w+\s+(sst_\w+)\s*\(", txt)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2602_03529_b200 import _build, _lib
+    _build.build()
+    return _lib.load()
+
+
+def test_header_declares_the_path(lib):
+    names = _declared()
+    for must in ("sst_encode", "sst_select_drop", "sst_packetize", "sst_parse",
+                 "sst_reassemble", "sst_unpack_decode", "sst_upscale_blend", "sst_decode",
+                 "sst_similarity", "sst_topk_mask", "sst_downscale", "sst_upscale", "sst_blend"):
+        assert must in names
+
+
+def test_every_declared_symbol_is_exported(lib):
+    from paper_2602_03529_b200 import _lib
+    out = subprocess.run(["nm", "-D", "--defined-only", str(_lib.LIB_PATH)], capture_output=True,
+                         text=True, check=True).stdout
+    exported = set(re.findall(r" T (sst_\w+)", out))
+    declared = set(_declared())
+    assert declared == exported, (declared ^ exported)
+    assert declared == set(_lib.SIGNATURES), (declared ^ set(_lib.SIGNATURES))
+
+
+def test_struct_layouts(lib):
+    from paper_2602_03529_b200 import _lib
+    assert ctypes.sizeof(_lib.SstPacketInfo) == 64
+    assert ctypes.sizeof(_lib.SstPrevDesc) == 24
+    assert _lib.INFO_DTYPE.itemsize == 64
+
+
+def test_pure_host_entry_points(lib):
+    # metadata-only entry points (no device work)
+    assert lib.sst_abi_version() == 1
+    # transport.py:221-226 / SURVEY §8 packet sizes
+    assert lib.sst_packet_wire_size(80, 12, 80) == 996
+    assert lib.sst_packet_wire_size(120, 12, 120) == 1481
+    assert lib.sst_packet_wire_size(54, 12, 54) == 681
+    assert lib.sst_packet_wire_size(16, 12, 16) == 220
+    assert lib.sst_packet_wire_size(32, 12, 32) == 414
+    assert lib.sst_packet_wire_size(3, 1, 2) == 22 + 1 + 2 + 4
+
+
+def test_argument_errors_without_device(lib):
+    # argument validation happens before any CUDA call
+    assert lib.sst_encode(None, 1, 16, 16, 2, None, None, None) == -1
+    assert lib.sst_encode(ctypes.c_void_p(16), 1, 16, 16, 5, ctypes.c_void_p(16), None, None) == -1
+    assert lib.sst_packetize(ctypes.c_void_p(16), None, 1, 70000, 1, 1, ctypes.c_void_p(16),
+                             ctypes.c_void_p(16), ctypes.c_void_p(16), ctypes.c_void_p(16), 64,
+                             ctypes.c_void_p(16), None) == -2
+    assert lib.sst_upscale_blend(ctypes.c_void_p(16), 1, 8, 8, 2, 16, 16, ctypes.c_void_p(16), 5,
+                                 ctypes.c_void_p(16), None) == -4
+    assert lib.sst_blend(None, None, 1, 4, 4, 0, None, None) == -1
+
+
+def test_sass_is_sm100a_with_tma(lib):
+    """The kernels are compiled for sm_100a only and the encoder uses TMA."""
+    from paper_2602_03529_b200 import _lib
+    cuobjdump = "/usr/local/cuda/bin/cuobjdump"
+    if not Path(cuobjdump).exists():
+        pytest.skip("cuobjdump missing")
+    elfs = subprocess.run([cuobjdump, "--list-elf", str(_lib.LIB_PATH)], capture_output=True,
+                          text=True).stdout
+    assert "sm_100a" in elfs
+    ptx = subprocess.run([cuobjdump, "--list-ptx", str(_lib.LIB_PATH)], capture_output=True,
+                         text=True).stdout
+    assert "compute_100" not in ptx.replace("compute_100a", "")   # no generic PTX embedded
+    sass = subprocess.run([cuobjdump, "-sass", str(_lib.LIB_PATH)], capture_output=True,
+                          text=True).stdout
+    assert "UTMALDG" in sass           # cp.async.bulk.tensor loads in the encoder
