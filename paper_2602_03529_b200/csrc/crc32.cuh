@@ -44,6 +44,24 @@ constexpr CrcTables make_crc_tables() {
   return t;
 }
 
+// x^(8n) mod P for n < kShiftN: appending n zero bytes is one multiply
+constexpr int kShiftN = 4096;
+struct CrcShiftTable {
+  uint32_t v[kShiftN];
+};
+constexpr CrcShiftTable make_crc_shift_table() {
+  CrcShiftTable t{};
+  uint32_t x8 = 1u << 30;                                   // x^1
+  for (int i = 0; i < 3; ++i) x8 = crc_multmodp(x8, x8);    // x^8
+  uint32_t p = 1u << 31;                                    // x^0
+  for (int n = 0; n < kShiftN; ++n) {
+    t.v[n] = p;
+    p = crc_multmodp(x8, p);
+  }
+  return t;
+}
+__device__ const CrcShiftTable kCrcShift = make_crc_shift_table();
+
 __device__ __forceinline__ uint32_t crc_mul(uint32_t a, uint32_t b) {
   uint32_t m = 1u << 31, p = 0;
   while (true) {
@@ -82,7 +100,12 @@ __device__ __forceinline__ uint32_t warp_crc32(const uint8_t* data, int len, con
   uint32_t c = 0xFFFFFFFFu;
   for (int i = beg; i < end; ++i) c = tab[(c ^ data[i]) & 0xFFu] ^ (c >> 8);
   c = ~c;                                    // == zlib.crc32(chunk); 0 for an empty chunk
-  uint32_t part = (end > beg) ? crc_mul(crc_shift_op((uint32_t)(len - end), x2n), c) : 0u;
+  uint32_t part = 0u;
+  if (end > beg) {
+    const uint32_t n = (uint32_t)(len - end);
+    const uint32_t op = n < (uint32_t)kShiftN ? __ldg(&kCrcShift.v[n]) : crc_shift_op(n, x2n);
+    part = crc_mul(op, c);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) part ^= __shfl_xor_sync(0xffffffffu, part, o);
   return part;

@@ -14,8 +14,8 @@
 
 namespace sst {
 
-constexpr int kDecTok = 8;      // tokens per CTA
-constexpr int kDecThreads = 256;
+constexpr int kDecTok = 16;     // tokens per CTA
+constexpr int kDecThreads = 384; // = kDecTok * 3 channels * 8 pixel rows
 
 struct DecArgs {
   // token-matrix source
@@ -37,7 +37,8 @@ template <bool kFromPackets>
 __global__ void __launch_bounds__(kDecThreads) k_decode(DecArgs a) {
   __shared__ double tok[2][kDecTok][kChannels];
   __shared__ uint8_t valid[kDecTok];
-  __shared__ double s1[2][kDecTok][3][8][8];       // [img][tok][ch][y][x]
+  __shared__ double s1[2][kDecTok][3][8][2];       // [img][tok][ch][y][x] for block columns 0, 1
+  __shared__ double zc[8];                         // column IDCT of an all-zero column
   __shared__ float pix[2][8][kDecTok * 8][3];      // output tile
 
   const int tid = threadIdx.x;
@@ -118,18 +119,25 @@ __global__ void __launch_bounds__(kDecThreads) k_decode(DecArgs a) {
   __syncthreads();
 
   // ---- 2. IDCT along y for every block column x (coefficients at (0,0),
-  //         (0,1), (1,0), (2,0); codec.py:134-138) ----
-  for (int it = tid; it < 2 * kDecTok * 3 * 8; it += kDecThreads) {
-    int im = it / (kDecTok * 24);
-    int t = (it / 24) % kDecTok;
-    int ch = (it / 8) % 3;
-    int x = it % 8;
-    const double* v = tok[im][t] + ch * 4;
+  //         (0,1), (1,0), (2,0); codec.py:134-138).  Columns 2..7 hold only
+  //         zeros, so their (identical) result is computed once. ----
+  for (int it = tid; it < 2 * kDecTok * 3 * 2 + 1; it += kDecThreads) {
     double c[8];
 #pragma unroll
     for (int y = 0; y < 8; ++y) c[y] = 0.0;
+    if (it == 2 * kDecTok * 3 * 2) {
+      dct3_8<true>(c, 1.0 / 16.0);
+#pragma unroll
+      for (int y = 0; y < 8; ++y) zc[y] = c[y];
+      continue;
+    }
+    int im = it / (kDecTok * 6);
+    int t = (it / 6) % kDecTok;
+    int ch = (it / 2) % 3;
+    int x = it % 2;
+    const double* v = tok[im][t] + ch * 4;
     if (x == 0) { c[0] = v[0]; c[1] = v[2]; c[2] = v[3]; }
-    if (x == 1) { c[0] = v[1]; }
+    else { c[0] = v[1]; }
     dct3_8<true>(c, 1.0 / 16.0);
 #pragma unroll
     for (int y = 0; y < 8; ++y) s1[im][t][ch][y][x] = c[y];
@@ -142,8 +150,11 @@ __global__ void __launch_bounds__(kDecThreads) k_decode(DecArgs a) {
     int ch = (it / 8) % 3;
     int y = it % 8;
     double ci[8], cp[8];
+    ci[0] = s1[0][t][ch][y][0]; ci[1] = s1[0][t][ch][y][1];
+    cp[0] = s1[1][t][ch][y][0]; cp[1] = s1[1][t][ch][y][1];
+    const double z = zc[y];
 #pragma unroll
-    for (int x = 0; x < 8; ++x) { ci[x] = s1[0][t][ch][y][x]; cp[x] = s1[1][t][ch][y][x]; }
+    for (int x = 2; x < 8; ++x) { ci[x] = z; cp[x] = z; }
     dct3_8<false>(ci, 1.0);
     dct3_8<false>(cp, 1.0);
     const bool keep_p = valid[t] != 0;

@@ -84,9 +84,18 @@ __global__ void __launch_bounds__(kSelThreads)
     for (int shift = 56; shift >= 0; shift -= 8) {
       for (int b = tid; b < 256; b += kSelThreads) hist[b] = 0;
       __syncthreads();
-      for (int64_t j = tid; j < n; j += kSelThreads) {
-        uint64_t key = sim_key(__ldg(sm + j));
-        if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 0xFF], 1u);
+      for (int64_t base = 0; base < n; base += kSelThreads) {
+        const int64_t j = base + tid;
+        uint64_t key = j < n ? sim_key(__ldg(sm + j)) : 0;
+        const bool in = j < n && (key & pmask) == prefix;
+        // warp-aggregated histogram update: similarity maps are dominated by
+        // ties (static content), so many lanes share one bin
+        const unsigned act = __ballot_sync(0xffffffffu, in);
+        if (in) {
+          const unsigned bin = (unsigned)((key >> shift) & 0xFF);
+          const unsigned peers = __match_any_sync(act, bin);
+          if ((threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&hist[bin], (unsigned)__popc(peers));
+        }
       }
       __syncthreads();
       if (tid == 0) {

@@ -10,7 +10,11 @@
 // upscale, P upscale and -- for boundary frames -- the previous GoP's P
 // upscale recomputed from its small working image instead of re-reading two
 // full-resolution frames) and streams the 9 frames out.
+#include <cstdlib>
+#include <cstring>
+
 #include "common.cuh"
+#include "tma.cuh"
 
 namespace sst {
 
@@ -46,69 +50,297 @@ __device__ __forceinline__ double bilerp(const T* img, int w, const AxisTap& ty,
   return top * ty.g + bot * ty.f;
 }
 
+// np.clip(x, 0, 1) for values that are provably >= 0 or -0.0: every K5
+// intermediate is a sum of products of non-negative factors (samples in
+// [0, 1], bilinear weights f, 1 - f in [0, 1], blend weights in [0, 1]), so
+// the lower bound never triggers and -0.0 passes through exactly as in numpy.
+__device__ __forceinline__ double clip_hi1(double x) { return x > 1.0 ? 1.0 : x; }
+
 __device__ __forceinline__ float blend_px(float prev, float curr, double alpha) {
   double v = alpha * (double)prev + (1.0 - alpha) * (double)curr;   // codec.py:293
   return (float)clip01(v);
 }
 
 // ---- fused upscale + blend + 9-frame store ----
-constexpr int kUpRows = 8;
-constexpr int kUpCols = 64;
-constexpr int kUpThreads = 256;
+//
+// One thread owns one output float column (pixel x, channel) of a band of
+// kUpRows output rows and walks down it.  The bilinear filter is separable in
+// the reference's own operation order: top = a*(1-fx) + b*fx is a function of
+// (source row, output column) only, so each thread evaluates it once per
+// source row and keeps the last two rows in registers; the per-output-row work
+// is the vertical mix top*(1-fy) + bot*fy.  The I, P and previous-GoP P images
+// are read through L1/L2 (they are 1/s^2 of a frame); the 9 frames are written
+// with streaming stores, each warp covering 128 contiguous bytes per frame row.
+constexpr int kUpThreads = 128;
+constexpr int kUpRows = 32;
 
 struct UpArgs {
   const float* img;            // [G][2][h][w][3]
   int G, h, w, s, H, W;
   const SstPrevDesc* prev;     // [G] or null
-  int n;                       // blend width
+  int n;                       // blend width (<= 4 when prev is used)
+  double alpha[4], beta[4];    // alpha_i = (n - i) / n, beta = 1 - alpha (i = 1..n)
   float* out;                  // [G][9][H][W][3]
 };
 
-__global__ void __launch_bounds__(kUpThreads) k_upscale_blend(UpArgs a) {
-  __shared__ AxisTap ty_c[kUpRows], tx_c[kUpCols];
-  __shared__ AxisTap ty_p[kUpRows], tx_p[kUpCols];
+struct RowCache {
+  int ya, yb;
+  double a0, a1, b0, b1;       // horizontal taps of up to two images at rows ya / yb
+};
+
+template <int NIMG>
+__device__ __forceinline__ void hrow(const float* i0, const float* i1, int w, int y,
+                                     const AxisTap& tx, int ch, double* o) {
+  const int64_t r = (int64_t)y * w;
+  {
+    double a = (double)__ldg(i0 + (r + tx.lo) * 3 + ch), b = (double)__ldg(i0 + (r + tx.hi) * 3 + ch);
+    o[0] = a * tx.g + b * tx.f;
+  }
+  if (NIMG == 2) {
+    double a = (double)__ldg(i1 + (r + tx.lo) * 3 + ch), b = (double)__ldg(i1 + (r + tx.hi) * 3 + ch);
+    o[1] = a * tx.g + b * tx.f;
+  }
+}
+
+// vertical step for output row taps `ty`; returns the clipped float32 samples
+template <int NIMG>
+__device__ __forceinline__ void vstep(RowCache& c, const float* i0, const float* i1, int w,
+                                      const AxisTap& ty, const AxisTap& tx, int ch, float* u) {
+  double lo[2], hi[2];
+  if (ty.lo == c.ya) { lo[0] = c.a0; lo[1] = c.a1; }
+  else if (ty.lo == c.yb) { lo[0] = c.b0; lo[1] = c.b1; }
+  else hrow<NIMG>(i0, i1, w, ty.lo, tx, ch, lo);
+  if (ty.hi == ty.lo) { hi[0] = lo[0]; hi[1] = lo[1]; }
+  else if (ty.hi == c.ya) { hi[0] = c.a0; hi[1] = c.a1; }
+  else if (ty.hi == c.yb) { hi[0] = c.b0; hi[1] = c.b1; }
+  else hrow<NIMG>(i0, i1, w, ty.hi, tx, ch, hi);
+  c.ya = ty.lo; c.a0 = lo[0]; c.a1 = lo[1];
+  c.yb = ty.hi; c.b0 = hi[0]; c.b1 = hi[1];
+  u[0] = (float)clip01(lo[0] * ty.g + hi[0] * ty.f);          // codec.py:235
+  if (NIMG == 2) u[1] = (float)clip01(lo[1] * ty.g + hi[1] * ty.f);
+}
+
+__global__ void __launch_bounds__(kUpThreads) k_upscale_blend(const __grid_constant__ UpArgs a) {
+  __shared__ AxisTap ty_c[kUpRows], ty_p[kUpRows];
   const int tid = threadIdx.x;
-  const int x0 = blockIdx.x * kUpCols;
-  const int y0 = blockIdx.y * kUpRows;
+  const int q = blockIdx.x * kUpThreads + tid;       // float column: pixel*3 + channel
+  const int oy0 = blockIdx.y * kUpRows;
   const int g = blockIdx.z;
   SstPrevDesc pd;
   pd.p_img = nullptr;
+  pd.h = pd.w = pd.s = 1;
   if (a.prev) pd = a.prev[g];
   const bool has_prev = pd.p_img != nullptr;
-  if (tid < kUpRows) ty_c[tid] = axis_tap(y0 + tid, a.h, a.s);
-  else if (tid < kUpRows + kUpCols) tx_c[tid - kUpRows] = axis_tap(x0 + tid - kUpRows, a.w, a.s);
-  else if (has_prev && tid < 2 * kUpRows + kUpCols) ty_p[tid - kUpRows - kUpCols] =
-      axis_tap(y0 + tid - kUpRows - kUpCols, pd.h, pd.s);
-  else if (has_prev && tid >= 128 && tid < 128 + kUpCols)
-    tx_p[tid - 128] = axis_tap(x0 + tid - 128, pd.w, pd.s);
+  if (tid < kUpRows) ty_c[tid] = axis_tap(oy0 + tid, a.h, a.s);
+  else if (has_prev && tid < 2 * kUpRows) ty_p[tid - kUpRows] = axis_tap(oy0 + tid - kUpRows, pd.h, pd.s);
+  __syncthreads();
+  if (q >= a.W * 3) return;
+  const int ox = q / 3, ch = q - ox * 3;
+  const AxisTap tx = axis_tap(ox, a.w, a.s);
+  const float* iimg = a.img + (int64_t)g * 2 * a.h * a.w * 3;
+  const float* pimg = iimg + (int64_t)a.h * a.w * 3;
+  const int64_t fstride = (int64_t)a.H * a.W * 3;
+  float* o = a.out + (int64_t)g * kGop * fstride + (int64_t)oy0 * a.W * 3 + q;
+  const int rows = min(kUpRows, a.H - oy0);
+  RowCache cc{-1, -1, 0.0, 0.0, 0.0, 0.0};
+  if (!has_prev) {
+    for (int r = 0; r < rows; ++r, o += a.W * 3) {
+      float u[2];
+      vstep<2>(cc, iimg, pimg, a.w, ty_c[r], tx, ch, u);
+      __stcs(o, u[0]);
+#pragma unroll
+      for (int f = 1; f < kGop; ++f) __stcs(o + f * fstride, u[1]);
+    }
+    return;
+  }
+  const AxisTap txp = axis_tap(ox, pd.w, pd.s);
+  RowCache cp{-1, -1, 0.0, 0.0, 0.0, 0.0};
+  for (int r = 0; r < rows; ++r, o += a.W * 3) {
+    float u[2], uq[2];
+    vstep<2>(cc, iimg, pimg, a.w, ty_c[r], tx, ch, u);
+    vstep<1>(cp, pd.p_img, nullptr, pd.w, ty_p[r], txp, ch, uq);
+    // frame f < n: alpha*prev[9-n+f] + (1-alpha)*curr[f]  (codec.py:289-293);
+    // the previous GoP's tail frames are its unblended P upscale when n <= 4
+    __stcs(o, (float)clip01(a.alpha[0] * (double)uq[0] + a.beta[0] * (double)u[0]));
+#pragma unroll
+    for (int f = 1; f < kGop; ++f) {
+      float v = u[1];
+      if (f < a.n) v = (float)clip01(a.alpha[f] * (double)uq[0] + a.beta[f] * (double)u[1]);
+      __stcs(o + f * fstride, v);
+    }
+  }
+}
+
+// ---- fused upscale + blend, TMA-store variant (aligned widths) ----
+//
+// A CTA owns a band of kBand output rows x kTQ output floats of one GoP
+// (kTQ threads, one output float column each).
+//   setup:  row taps of the band, the band's source windows (I, P, previous
+//           P; float32) copied to smem with one batch of coalesced loads;
+//   compute: each thread walks its column down the band: the horizontal pass
+//           a*(1-fx) + b*fx (codec.py:233) once per source row, cached in
+//           registers; the vertical pass top*(1-fy) + bot*fy (codec.py:235)
+//           per output row; clip, float32, blend (codec.py:289-293);
+//   store:  every kTR rows the n+1 distinct tiles (blended frames 0..n-1, P)
+//           leave through one TMA bulk tensor store per output frame (frames
+//           n..8 share the P tile); TMA clips the crop edges.
+constexpr int kTR = 8;                     // output rows per stored tile
+constexpr int kBand = 32;                  // output rows per CTA
+constexpr int kTQ = 256;                   // output floats per tile row (= threads)
+constexpr int kWR = kBand / 2 + 2;         // max source rows per band (s >= 2)
+constexpr int kWF = (kTQ / 6 + 3) * 3 + 3; // max source floats per window row (s >= 2)
+
+struct UpTmaSmem {
+  float win[3][kWR][kWF];                  // I, P, previous P windows
+  AxisTap ty_c[kBand], ty_p[kBand];
+  int wx0[2], wx1[2];                      // window column range (source px) cur / prev
+};
+typedef float UpTile[kTR][kTQ];
+constexpr int kTileOff = (int)((sizeof(UpTmaSmem) + 127) / 128 * 128);   // TMA needs 128-B
+// dynamic smem when `ntiles` output tiles are used (n blended frames + P)
+__host__ __device__ constexpr int up_tma_smem(int ntiles) {
+  return kTileOff + ntiles * (int)sizeof(UpTile);
+}
+
+__device__ __forceinline__ void load_window(float* win, const float* img, int w, int r0, int r1,
+                                           int c0f, int c1f, int tid) {
+  const int ncol = c1f - c0f;
+  const int lane = tid & 31, wid = tid >> 5;
+  for (int j = wid; j <= r1 - r0; j += kTQ / 32) {
+    const float* src = img + ((int64_t)(r0 + j) * w) * 3 + c0f;
+    float* dst = win + j * kWF;
+#pragma unroll
+    for (int c = lane; c < kWF; c += 32)
+      if (c < ncol) dst[c] = __ldg(src + c);
+  }
+}
+
+template <bool kPrev, int kN>
+__global__ void __launch_bounds__(kTQ)
+    k_upscale_blend_tma(const __grid_constant__ CUtensorMap omap, const __grid_constant__ UpArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  UpTmaSmem& S = *reinterpret_cast<UpTmaSmem*>(smem_raw);
+  UpTile* tile = reinterpret_cast<UpTile*>(smem_raw + kTileOff);
+  const int tid = threadIdx.x;
+  const int q0 = blockIdx.x * kTQ;
+  const int oy0 = blockIdx.y * kBand;
+  const int g = blockIdx.z;
+  SstPrevDesc pd;
+  pd.p_img = nullptr;
+  pd.h = pd.w = pd.s = 1;
+  if (kPrev) pd = a.prev[g];
+  const bool has_prev = kPrev && pd.p_img != nullptr;
+  const int rows = min(kBand, a.H - oy0);
+  const int qlast = min(q0 + kTQ, a.W * 3) - 1;
+  if (tid < kBand) S.ty_c[tid] = axis_tap(oy0 + min(tid, rows - 1), a.h, a.s);
+  else if (tid < 2 * kBand) {
+    if (has_prev) S.ty_p[tid - kBand] = axis_tap(oy0 + min(tid - kBand, rows - 1), pd.h, pd.s);
+  } else if (tid == 2 * kBand) {
+    S.wx0[0] = axis_tap(q0 / 3, a.w, a.s).lo;
+    S.wx1[0] = axis_tap(qlast / 3, a.w, a.s).hi;
+  } else if (tid == 2 * kBand + 32 && has_prev) {
+    S.wx0[1] = axis_tap(q0 / 3, pd.w, pd.s).lo;
+    S.wx1[1] = axis_tap(qlast / 3, pd.w, pd.s).hi;
+  }
   __syncthreads();
 
   const float* iimg = a.img + (int64_t)g * 2 * a.h * a.w * 3;
   const float* pimg = iimg + (int64_t)a.h * a.w * 3;
-  const int64_t fstride = (int64_t)a.H * a.W * 3;
-  float* og = a.out + (int64_t)g * kGop * fstride;
-  const int rows = min(kUpRows, a.H - y0);
-  const int cols = min(kUpCols, a.W - x0);
-  for (int e = tid; e < kUpRows * kUpCols * 3; e += kUpThreads) {
-    const int r = e / (kUpCols * 3);
-    const int q = e % (kUpCols * 3);
-    const int px = q / 3, ch = q % 3;
-    if (r >= rows || px >= cols) continue;
-    const float ui = (float)clip01(bilerp(iimg, a.w, ty_c[r], tx_c[px], ch));
-    const float up = (float)clip01(bilerp(pimg, a.w, ty_c[r], tx_c[px], ch));
-    float* o = og + ((int64_t)(y0 + r) * a.W + x0) * 3 + q;
-    if (has_prev) {
-      const float uq = (float)clip01(bilerp(pd.p_img, pd.w, ty_p[r], tx_p[px], ch));
-      // frame f < n: i = f + 1, alpha = (n - i) / n, prev frame 9 - n + f (= uq)
-      __stcs(o, blend_px(uq, ui, (double)(a.n - 1) / (double)a.n));
-      for (int f = 1; f < kGop; ++f)
-        __stcs(o + f * fstride, f < a.n ? blend_px(uq, up, (double)(a.n - 1 - f) / (double)a.n) : up);
-    } else {
-      __stcs(o, ui);
+  const int r0 = S.ty_c[0].lo;
+  const int pr0 = has_prev ? S.ty_p[0].lo : 0;
+  {
+    const int r1 = S.ty_c[rows - 1].hi;
+    load_window(&S.win[0][0][0], iimg, a.w, r0, r1, S.wx0[0] * 3, S.wx1[0] * 3 + 3, tid);
+    load_window(&S.win[1][0][0], pimg, a.w, r0, r1, S.wx0[0] * 3, S.wx1[0] * 3 + 3, tid);
+    if (has_prev)
+      load_window(&S.win[2][0][0], pd.p_img, pd.w, pr0, S.ty_p[rows - 1].hi, S.wx0[1] * 3,
+                  S.wx1[1] * 3 + 3, tid);
+  }
+  __syncthreads();
+
+  const int q = min(q0 + tid, a.W * 3 - 1);       // columns past the crop are clipped by TMA
+  const int ox = q / 3, ch = q - ox * 3;
+  const int nb = has_prev ? kN : 1;                // tiles 0..nb-1: frames 0..nb-1; tile nb: P
+  const AxisTap tx = axis_tap(ox, a.w, a.s);
+  const int xl = (tx.lo - S.wx0[0]) * 3 + ch, xh = (tx.hi - S.wx0[0]) * 3 + ch;
+  AxisTap txp = tx;
+  int pxl = 0, pxh = 0;
+  if (has_prev) {
+    txp = axis_tap(ox, pd.w, pd.s);
+    pxl = (txp.lo - S.wx0[1]) * 3 + ch;
+    pxh = (txp.hi - S.wx0[1]) * 3 + ch;
+  }
+  int ya = -1, yb = -1, qa = -1, qb = -1;
+  double ia = 0, pa = 0, ib = 0, pb = 0, qva = 0, qvb = 0;   // horizontal taps at cached rows
+  const int z0 = g * kGop;
+  for (int c0 = 0; c0 < rows; c0 += kTR) {
+    if (c0 > 0) {                                  // tiles free again once TMA has read them
+      if (tid == 0) tma_store_wait_read();
+      __syncthreads();
+    }
+    const int cend = min(c0 + kTR, rows);
+    for (int r = c0; r < cend; ++r) {
+      const AxisTap ty = S.ty_c[r];
+      if (ty.lo != ya) {
+        if (ty.lo == yb) { ia = ib; pa = pb; }
+        else {
+          const float* wi = &S.win[0][ty.lo - r0][0];
+          const float* wp = &S.win[1][ty.lo - r0][0];
+          ia = (double)wi[xl] * tx.g + (double)wi[xh] * tx.f;
+          pa = (double)wp[xl] * tx.g + (double)wp[xh] * tx.f;
+        }
+        ya = ty.lo;
+      }
+      if (ty.hi != yb) {
+        if (ty.hi == ya) { ib = ia; pb = pa; }
+        else {
+          const float* wi = &S.win[0][ty.hi - r0][0];
+          const float* wp = &S.win[1][ty.hi - r0][0];
+          ib = (double)wi[xl] * tx.g + (double)wi[xh] * tx.f;
+          pb = (double)wp[xl] * tx.g + (double)wp[xh] * tx.f;
+        }
+        yb = ty.hi;
+      }
+      const float ui = (float)clip_hi1(ia * ty.g + ib * ty.f);
+      const float up = (float)clip_hi1(pa * ty.g + pb * ty.f);
+      const int rr = r - c0;
+      tile[nb][rr][tid] = up;
+      if (has_prev) {
+        const AxisTap tp = S.ty_p[r];
+        if (tp.lo != qa) {
+          if (tp.lo == qb) qva = qvb;
+          else {
+            const float* wq = &S.win[2][tp.lo - pr0][0];
+            qva = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
+          }
+          qa = tp.lo;
+        }
+        if (tp.hi != qb) {
+          if (tp.hi == qa) qvb = qva;
+          else {
+            const float* wq = &S.win[2][tp.hi - pr0][0];
+            qvb = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
+          }
+          qb = tp.hi;
+        }
+        const double dq = (double)(float)clip_hi1(qva * tp.g + qvb * tp.f);
+        tile[0][rr][tid] = (float)clip_hi1(a.alpha[0] * dq + a.beta[0] * (double)ui);
+        const double dp = (double)up;
 #pragma unroll
-      for (int f = 1; f < kGop; ++f) __stcs(o + f * fstride, up);
+        for (int f = 1; f < kN; ++f) tile[f][rr][tid] = (float)clip_hi1(a.alpha[f] * dq + a.beta[f] * dp);
+      } else {
+        tile[0][rr][tid] = ui;
+      }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      for (int f = 0; f < kGop; ++f)
+        tma_store_3d(&omap, &tile[f < nb ? f : nb][0][0], q0, oy0 + c0, z0 + f);
+      tma_store_commit();
     }
   }
+  if (tid == 0) tma_store_wait_read();
 }
 
 // ---- standalone kernels ----
@@ -188,10 +420,40 @@ extern "C" int sst_upscale_blend(const float* img, int G, int h, int w, int s, i
   if (G == 0) return SST_OK;
   if (!img || !out) return SST_ERR_ARG;
   if (G > 65535) return SST_ERR_ARG;
-  UpArgs a{img, G, h, w, s, H, W, prev, blend_n, out};
-  dim3 grid(ceil_div(W, kUpCols), ceil_div(H, kUpRows), G);
+  UpArgs a{};
+  a.img = img; a.G = G; a.h = h; a.w = w; a.s = s; a.H = H; a.W = W;
+  a.prev = prev; a.n = blend_n; a.out = out;
+  for (int i = 1; i <= 4; ++i) {
+    a.alpha[i - 1] = (double)(blend_n - i) / (double)blend_n;   // python (n - i) / n
+    a.beta[i - 1] = 1.0 - a.alpha[i - 1];
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUtensorMap omap;
+  memset(&omap, 0, sizeof(omap));
+  const char* var = getenv("SST_K5_VARIANT");          // A/B switch for profiling
+  const bool want_tma = !(var && var[0] == '2');
+  if (want_tma &&
+      make_tmap_f32_3d(&omap, out, (uint64_t)W * 3, (uint64_t)H, (uint64_t)G * kGop, kTQ, kTR)) {
+    dim3 grid(ceil_div(W * 3, kTQ), ceil_div(H, kBand), G);
+    if (grid.y > 65535) return SST_ERR_ARG;
+    const int smem = up_tma_smem((prev ? blend_n : 1) + 1);
+    auto kern = k_upscale_blend_tma<false, 1>;
+    if (prev) {
+      switch (blend_n) {
+        case 1: kern = k_upscale_blend_tma<true, 1>; break;
+        case 2: kern = k_upscale_blend_tma<true, 2>; break;
+        case 3: kern = k_upscale_blend_tma<true, 3>; break;
+        default: kern = k_upscale_blend_tma<true, 4>; break;
+      }
+    }
+    SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    kern<<<grid, kTQ, smem, st>>>(omap, a);
+    SST_LAUNCH_CHECK();
+    return SST_OK;
+  }
+  dim3 grid(ceil_div(W * 3, kUpThreads), ceil_div(H, kUpRows), G);
   if (grid.y > 65535) return SST_ERR_ARG;
-  k_upscale_blend<<<grid, kUpThreads, 0, static_cast<cudaStream_t>(stream)>>>(a);
+  k_upscale_blend<<<grid, kUpThreads, 0, st>>>(a);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }

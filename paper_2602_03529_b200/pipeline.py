@@ -224,13 +224,18 @@ class StreamBank:
     from GoP to GoP (variable-resolution mode); boundary blending always uses
     the stream's previous reconstruction, at whatever scale it was coded."""
 
-    def __init__(self, n_streams: int, H: int, W: int, scales=(2, 3), blend_n: int = 2):
+    def __init__(self, n_streams: int, H: int, W: int, scales=(2, 3), blend_n: int = 2,
+                 concurrent_groups: bool = True):
         if blend_n > 4:
             raise ValueError("the fused reconstruction blends at most 4 frames")
         self.n, self.H, self.W, self.blend_n = n_streams, H, W, blend_n
         self.codecs = {s: GopCodec(n_streams, H, W, s, blend_n) for s in scales}
         self.prev_host = np.zeros(n_streams, dtype=_lib.PREV_DTYPE)
         self.rings = {s: _DescRing(n_streams * _lib.PREV_BYTES) for s in scales}
+        # each scale group runs on its own CUDA stream so the latency-bound
+        # middle kernels of one group overlap the HBM-bound K1/K5 of the other
+        self.group_streams = ({s: torch.cuda.Stream(device=_dev.device()) for s in scales}
+                              if concurrent_groups else None)
         self.step_idx = 0
         self.launches = 0          # kernels of this library launched by step()
         # where each stream's last P image lives: (scale, parity, slot) or None
@@ -244,22 +249,32 @@ class StreamBank:
         ``out_by_scale[s]`` in the same order.  ``present_by_scale[s]`` (uint8
         per packet slot, I rows then P rows per GoP) simulates network loss."""
         parity = self.step_idx & 1
+        main = torch.cuda.current_stream()
+        joined = []
         for s, frames in frames_by_scale.items():
             codec = self.codecs[s]
             ids = stream_ids_by_scale[s]
             g = len(ids)
             if g == 0:
                 continue
-            codec.set_gop_ids(gop_ids_by_scale[s])
-            codec.encode(frames, g, codec.drop_k(drop_rate))
-            present = None if present_by_scale is None else present_by_scale.get(s)
-            codec.decode(g, parity, present=present)
-            # K1 + K2 (if dropping) + K3 + K4 parse + 4 (init/route/dups/decode) + K5
-            self.launches += 1 + (1 if codec.drop_k(drop_rate) > 0 else 0) + 1 + 1 + 4 + 1
-            staged = self._prev_descs(s, ids)
-            codec.reconstruct(g, parity, out_by_scale[s], None if staged is None else staged[0])
-            if staged is not None:
-                self.rings[s].release(staged[1])
+            gs = self.group_streams[s] if self.group_streams and len(frames_by_scale) > 1 else main
+            if gs is not main:
+                gs.wait_stream(main)
+                joined.append(gs)
+            with torch.cuda.stream(gs):
+                codec.set_gop_ids(gop_ids_by_scale[s])
+                codec.encode(frames, g, codec.drop_k(drop_rate))
+                present = None if present_by_scale is None else present_by_scale.get(s)
+                codec.decode(g, parity, present=present)
+                # K1 + K2 (if dropping) + K3 + K4 parse + 4 (init/route/dups/decode) + K5
+                self.launches += 1 + (1 if codec.drop_k(drop_rate) > 0 else 0) + 1 + 1 + 4 + 1
+                staged = self._prev_descs(s, ids)
+                codec.reconstruct(g, parity, out_by_scale[s],
+                                  None if staged is None else staged[0])
+                if staged is not None:
+                    self.rings[s].release(staged[1])
+        for gs in joined:
+            main.wait_stream(gs)
         for s, ids in stream_ids_by_scale.items():
             for slot, sid in enumerate(ids):
                 self.last[sid] = (s, parity, slot)
