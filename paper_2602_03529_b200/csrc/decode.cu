@@ -71,27 +71,31 @@ __global__ void __launch_bounds__(kDecThreads) k_decode(DecArgs a) {
           atomicAdd(&a.stats[2 * mat + 1], 1);          // rows_received
         }
       }
-      // lanes 0..7 handle one token each
+      // prefix count of valid tokens left of this CTA's first token
+      // (popcount of the whole mask bytes before it), spread over the lanes
+      const uint8_t* mb = ok ? pkt + p->mask_off : nullptr;
+      int pre0 = 0;
+      if (ok)
+        for (int b = lane; b < (tx0 >> 3); b += 32) pre0 += __popc((uint32_t)mb[b]);
+      pre0 = __reduce_add_sync(0xffffffffu, pre0);
+      // lane t < kDecTok owns token tx0 + t (kDecTok is a multiple of 8, so
+      // the tokens before tx0 are exactly the whole bytes counted above)
+      const int tx = tx0 + lane;
+      const bool v = ok && lane < kDecTok && tx < a.Wt && ((mb[tx >> 3] >> (7 - (tx & 7))) & 1);
+      const unsigned bal = __ballot_sync(0xffffffffu, v);
       if (lane < kDecTok) {
-        const int tx = tx0 + lane;
-        bool v = false;
         double* dst = tok[wid][lane];
-        if (ok && tx < a.Wt) {
-          const uint8_t* mb = pkt + p->mask_off;
-          v = (mb[tx >> 3] >> (7 - (tx & 7))) & 1;
-          if (v) {
-            int pre = 0;
-            for (int b = 0; b < (tx >> 3); ++b) pre += __popc((uint32_t)mb[b]);
-            uint32_t part = (uint32_t)mb[tx >> 3] >> (8 - (tx & 7));
-            pre += __popc(part);
-            const uint8_t* src = pkt + p->payload_off + pre * kChannels;
-            const double qmin = p->dqmin;
-            const double step = p->dqrange / 255.0;    // transport.py:199
+        if (v) {
+          const int pre = pre0 + __popc(bal & ((1u << lane) - 1u));
+          const uint8_t* src = pkt + p->payload_off + pre * kChannels;
+          uint8_t raw[kChannels];
 #pragma unroll
-            for (int c = 0; c < kChannels; ++c) dst[c] = qmin + (double)src[c] * step;
-          }
-        }
-        if (!v) {
+          for (int c = 0; c < kChannels; ++c) raw[c] = src[c];
+          const double qmin = p->dqmin;
+          const double step = p->dqrange / 255.0;    // transport.py:199
+#pragma unroll
+          for (int c = 0; c < kChannels; ++c) dst[c] = qmin + (double)raw[c] * step;
+        } else {
 #pragma unroll
           for (int c = 0; c < kChannels; ++c) dst[c] = 0.0;
         }
@@ -168,17 +172,33 @@ __global__ void __launch_bounds__(kDecThreads) k_decode(DecArgs a) {
   }
   __syncthreads();
 
-  // ---- 4. store the cropped tile ----
+  // ---- 4. store the cropped tile (16-byte stores when rows are aligned) ----
   const int y0 = ty * 8, x0 = tx0 * 8;
   const int rows = min(8, a.h - y0);
-  const int cols = min(kDecTok * 8, a.w - x0);
-  for (int e = tid; e < 2 * 8 * kDecTok * 8 * 3; e += kDecThreads) {
-    int im = e / (8 * kDecTok * 24);
-    int r = (e / (kDecTok * 24)) % 8;
-    int q = e % (kDecTok * 24);       // pixel*3 + ch within the row
-    if (r < rows && q < cols * 3) {
-      float v = (&pix[im][r][0][0])[q];
-      a.out[((((int64_t)g * 2 + im) * a.h + y0 + r) * a.w + x0) * 3 + q] = v;
+  const int nq = min(kDecTok * 8, a.w - x0) * 3;          // floats per tile row
+  constexpr int kRowF = kDecTok * 8 * 3;
+  if ((a.w & 3) == 0) {
+    constexpr int kRow4 = kRowF / 4;
+    for (int e = tid; e < 2 * 8 * kRow4; e += kDecThreads) {
+      const int im = e / (8 * kRow4);
+      const int r = (e / kRow4) % 8;
+      const int q = (e % kRow4) * 4;
+      if (r >= rows || q >= nq) continue;
+      const float* srcp = &pix[im][r][0][0] + q;
+      float* dstp = a.out + ((((int64_t)g * 2 + im) * a.h + y0 + r) * a.w + x0) * 3 + q;
+      if (q + 4 <= nq) {
+        *reinterpret_cast<float4*>(dstp) = make_float4(srcp[0], srcp[1], srcp[2], srcp[3]);
+      } else {
+        for (int u = 0; u < nq - q; ++u) dstp[u] = srcp[u];
+      }
+    }
+  } else {
+    for (int e = tid; e < 2 * 8 * kRowF; e += kDecThreads) {
+      const int im = e / (8 * kRowF);
+      const int r = (e / kRowF) % 8;
+      const int q = e % kRowF;
+      if (r < rows && q < nq)
+        a.out[((((int64_t)g * 2 + im) * a.h + y0 + r) * a.w + x0) * 3 + q] = (&pix[im][r][0][0])[q];
     }
   }
 }

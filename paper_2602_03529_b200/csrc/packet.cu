@@ -100,12 +100,22 @@ __global__ void __launch_bounds__(kPackWarps * 32) k_packetize(PackArgs a) {
   double lo = 0.0, hi = 0.0;
   bool any = false;
   const int64_t nel = (int64_t)Wt * C;
-  for (int64_t e = lane; e < nel; e += 32) {
-    int t = (int)(e / C);
-    if (mrow && !mrow[t]) continue;
-    double v = vrow[e];
-    if (!any) { lo = v; hi = v; any = true; }
-    else { lo = min_total(lo, v); hi = max_total(hi, v); }
+  // batches of 4 independent loads per lane keep several requests in flight
+  for (int64_t e0 = lane; e0 < nel; e0 += 32 * 4) {
+    double v[4];
+    bool ok[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t e = e0 + 32 * u;
+      ok[u] = e < nel && (mrow == nullptr || mrow[(int)(e / C)] != 0);
+      v[u] = ok[u] ? __ldg(vrow + e) : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (!ok[u]) continue;
+      if (!any) { lo = v[u]; hi = v[u]; any = true; }
+      else { lo = min_total(lo, v[u]); hi = max_total(hi, v[u]); }
+    }
   }
   // lanes without values contribute neutral elements
   const double kInf = __longlong_as_double(0x7ff0000000000000ll);

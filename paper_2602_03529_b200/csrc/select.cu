@@ -98,15 +98,35 @@ __global__ void __launch_bounds__(kSelThreads)
         }
       }
       __syncthreads();
-      if (tid == 0) {
-        int64_t cum = 0;
-        int d = 255;
-        for (; d >= 0; --d) {
-          if (cum + hist[d] >= krem) break;
-          cum += hist[d];
+      // warp 0 locates the digit holding the krem-th largest key: suffix
+      // sums over the 256 bins (8 per lane, lane 0 = top bins)
+      if (tid < 32) {
+        uint32_t c[8];
+        uint32_t local = 0;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          c[i] = hist[255 - (tid * 8 + i)];
+          local += c[i];
         }
-        s_prefix = prefix | ((uint64_t)d << shift);
-        s_krem = krem - cum;
+        uint32_t incl = local;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+          if (tid >= o) incl += v;
+        }
+        const int64_t before = (int64_t)(incl - local);   // keys in higher digits
+        const bool here = before < krem && before + (int64_t)local >= krem;
+        if (here) {
+          int64_t cum = before;
+          int i = 0;
+          for (; i < 8; ++i) {
+            if (cum + c[i] >= krem) break;
+            cum += c[i];
+          }
+          const int d = 255 - (tid * 8 + i);
+          s_prefix = prefix | ((uint64_t)d << shift);
+          s_krem = krem - cum;
+        }
       }
       __syncthreads();
       prefix = s_prefix;
