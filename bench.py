@@ -63,6 +63,8 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-workers", type=int, default=0, help="0 = auto")
+    ap.add_argument("--roofline-steps", type=int, default=3,
+                    help="extra serialised steps timing each kernel alone")
     return ap.parse_args()
 
 
@@ -276,8 +278,6 @@ def run_ours(a, rank, world, local_rank):
     if world > 1:
         dist.barrier()
     launches0 = bank.launches
-    timer = StageTimer()
-    bank.set_timer(timer)
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local_rank) as clocks:
@@ -292,7 +292,6 @@ def run_ours(a, rank, world, local_rank):
         torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    bank.set_timer(None)
     ms = t_start.elapsed_time(t_end)
     ms_max = ms
     if world > 1:
@@ -300,6 +299,19 @@ def run_ours(a, rank, world, local_rank):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max = float(t.item())
     launches = bank.launches - launches0
+    # Per-kernel roofline: a few extra steps with the lanes serialised on one
+    # stream so that every kernel's CUDA-event duration is its own (in the
+    # timed run the two lanes overlap and each kernel shares the HBM).
+    timer = StageTimer()
+    bank.set_timer(timer)
+    for k in range(a.warmup + a.steps, a.warmup + a.steps + a.roofline_steps):
+        fr = inputs[k % 2]
+        for ln in lanes:
+            s = scale_of(ln["phase"], k)
+            ln["bank"].step({s: fr[ln["sl"]]}, {s: out[ln["sl"]]}, {s: list(range(ln["n"]))},
+                            {s: [k] * ln["n"]}, drop_rate=a.drop)
+    torch.cuda.synchronize()
+    bank.set_timer(None)
     stages = timer.summary()
     frames_total = S * GOP * a.steps * world
     value = frames_total / (ms_max / 1000.0)
@@ -314,7 +326,7 @@ def run_ours(a, rank, world, local_rank):
 
     res = dict(ms=ms_max, value=value, stages=stages, launches=launches,
                clocks=clocks.summary(), psnr=psnr)
-    res["roofline"] = roofline(a, stages, S)
+    res["roofline"] = roofline(a, stages, S // 2, a.roofline_steps * 2)
     if not a.no_e2e:
         del inputs, out
         torch.cuda.empty_cache()
@@ -322,7 +334,7 @@ def run_ours(a, rank, world, local_rank):
     return res
 
 
-def roofline(a, stages, S) -> dict:
+def roofline(a, stages, gops_per_launch, _launches_hint=None) -> dict:
     """Achieved GB/s of the dominant kernel: algorithmic bytes per launch /
     average CUDA-event launch duration inside the timed region."""
     H, W = a.height, a.width
@@ -343,7 +355,6 @@ def roofline(a, stages, S) -> dict:
         if name not in stages:
             continue
         tot_ms, launches = stages[name]
-        gops_per_launch = S * a.steps / launches          # GoPs processed per launch
         algo = bytes_gop * gops_per_launch
         avg_s = tot_ms / launches / 1000.0
         ach = algo / avg_s / 1e9
@@ -360,10 +371,20 @@ def roofline(a, stages, S) -> dict:
     best["traffic"] = None
     if tr and best["kernel"] in tr:
         # ncu --set full DRAM bytes per GoP x GoPs per launch of this run
-        launches = stages[best["kernel"]][1]
-        best["traffic"] = int(tr[best["kernel"]] * S * a.steps / launches)
+        best["traffic"] = int(tr[best["kernel"]] * gops_per_launch)
         best["traffic_source"] = tr.get("_source")
     return best
+
+
+def path_roofline(a, fps) -> dict:
+    """Whole path against HBM: SURVEY §8(d) algorithmic bytes per frame
+    (read the frame once, write it once, fp32, + packets) x frames/s."""
+    peak, src = measured_hbm_peak()
+    per_frame = a.height * a.width * 3 * (4 + 4)
+    ach = per_frame * fps / 1e9
+    return {"bytes_per_frame": per_frame, "achieved": round(ach, 1), "peak": peak,
+            "unit": "GB/s", "frac": round(ach / peak, 4),
+            "roofline_fps": round(peak * 1e9 / per_frame, 1)}
 
 
 def run_e2e(a, rank, world, local_rank) -> dict:
@@ -593,8 +614,9 @@ def main():
         line = dict(base, value=round(res["value"], 2), ms_per_step=round(res["ms"] / a.steps, 3),
                     roofline=res["roofline"], gpu_launches=res["launches"],
                     clocks=res["clocks"],
-                    stages={k: {"ms_total": round(v[0], 3), "launches": v[1]}
+                    stages={k: {"ms_per_launch": round(v[0] / v[1], 4), "launches": v[1]}
                             for k, v in res["stages"].items()},
+                    path_roofline=path_roofline(a, res["value"]),
                     psnr_db=res["psnr"])
         line["e2e"] = res.get("e2e")
         if world == 1 and not a.no_cpu_baseline:

@@ -115,17 +115,29 @@ class GopCodec:
                     for _ in range(2)]
         self.n = n
         self.timer = _NO_TIMER
+        self._id_ring = _DescRing(3 * G * 4)
 
     # -- helpers -------------------------------------------------------
     def drop_k(self, rate: float) -> int:
         return int(np.floor(rate * self.n + 0.5))
 
     def set_gop_ids(self, gop_ids) -> None:
-        ids = torch.as_tensor(np.asarray(gop_ids, dtype=np.uint32).view(np.int32),
-                              device=self.exp_gop.device)
-        g = ids.numel()
-        self.exp_gop[:g].copy_(ids)
-        self.gop_id[:2 * g].copy_(ids.repeat_interleave(2))
+        """Per-GoP gop_id of the next batch.  Never blocks the host: a uniform
+        id is a device fill, otherwise the ids go through a pinned staging
+        ring (a pageable H2D copy would synchronise the stream)."""
+        ids = np.asarray(gop_ids, dtype=np.uint32)
+        g = ids.size
+        if g and (ids == ids[0]).all():
+            v = int(ids[0].view(np.int32))
+            self.exp_gop[:g].fill_(v)
+            self.gop_id[:2 * g].fill_(v)
+            return
+        raw = np.repeat(ids, 2)
+        staged, slot = self._id_ring.stage(np.concatenate([ids, raw]).view(np.uint8))
+        both = staged[:3 * g * 4].view(torch.int32)
+        self.exp_gop[:g].copy_(both[:g])
+        self.gop_id[:2 * g].copy_(both[g:])
+        self._id_ring.release(slot)
 
     # -- sender --------------------------------------------------------
     def encode(self, frames: torch.Tensor, g: int, drop_k: int = 0) -> None:

@@ -352,3 +352,45 @@ def test_api_parity_awkward_shapes(rng, hw):
     i, p = C.encode_gop(g, CFG)                      # direct (s = 1) tokenizer
     oi, op = O.encode(frames)
     assert _bits(i.values, oi) and _bits(p.values, op)
+
+
+# ---------------------------------------------------------------------------
+# size extremes
+
+def test_large_packets_crc_beyond_shift_table(rng):
+    # 3000-token rows: ~36 KB packets, so lane chunks sit > 4096 bytes from the
+    # end and the CRC merge takes the square-and-multiply path
+    h, w, c = 2, 3000, 12
+    vals = rng.uniform(-3, 3, (h, w, c))
+    mask = rng.random((h, w)) > 0.2
+    vals = np.where(mask[..., None], vals, 0.0)
+    m = C.TokenMatrix("P", vals, mask, gop_id=77)
+    pk = T.packetize_tokens(m, scale=3)
+    wire = [p.to_bytes() for p in pk]
+    assert wire == O.packetize(O.KIND_P, 77, vals, mask, 3)
+    assert len(wire[0]) > 25000
+    back = T.reassemble(T.parse_packets(wire), (h, w, c), "P", gop_id=77)
+    ov, om = O.reassemble([O.parse(d) for d in wire], (h, w, c))
+    assert _bits(back.values, ov) and np.array_equal(back.mask, om)
+    # field-wise serialisation of the same packets (user-built TokenPacket)
+    rebuilt = [T.TokenPacket(p.kind, p.gop_id, p.row_index, p.width_tokens, p.channels, p.scale,
+                             p.quant_min, p.quant_range, p.mask, p.payload) for p in pk]
+    assert [p.to_bytes() for p in rebuilt] == wire
+
+
+def test_many_rows_and_single_column(rng):
+    # tall, 1-token-wide matrices: 20000 row packets in one launch
+    h, w, c = 20000, 1, 3
+    vals = rng.uniform(-1, 1, (h, w, c))
+    m = C.TokenMatrix("I", vals, np.ones((h, w), bool), gop_id=5)
+    wire = [p.to_bytes() for p in T.packetize_tokens(m)]
+    assert wire == O.packetize(O.KIND_I, 5, vals, np.ones((h, w), bool), 1)
+
+
+def test_empty_and_all_dropped_rows(rng):
+    m = C.TokenMatrix("P", np.zeros((3, 5, 12)), np.zeros((3, 5), bool))
+    pk = T.packetize_tokens(m)
+    assert all(p.payload == b"" and p.quant_range == 0.0 for p in pk)
+    back = T.reassemble(T.parse_packets([p.to_bytes() for p in pk]), (3, 5, 12), "P")
+    assert not back.mask.any() and not back.values.any()
+    assert T.packetize_tokens(C.TokenMatrix("I", np.zeros((0, 4, 12)), np.zeros((0, 4), bool))) == []
