@@ -145,9 +145,10 @@ SST_API int sst_decode(const double* i_tok, const double* p_tok, int64_t tok_str
 SST_API int sst_similarity(const double* p, const double* i, int64_t n, int C, double* sim, void* stream);
 
 /* top_k_drop_mask (selection.py:55-67): per map g, mark the k[g] largest
- * similarities (ties: lower row-major index first).  k is a DEVICE int32[G]. */
+ * similarities (ties: lower row-major index first).  k is a DEVICE int32[G];
+ * kth (DEVICE double[G] or NULL) receives the k-th largest value. */
 SST_API int sst_topk_mask(const double* sim, int G, int64_t n, const int32_t* k, uint8_t* drop,
-                  void* stream);
+                          double* kth, void* stream);
 
 /* apply_token_mask (codec.py:189-196) in place: mask &= ~drop, values of
  * invalid positions set to 0.0. */
@@ -217,6 +218,55 @@ SST_API int sst_unpack_decode(const uint8_t* buf, const int64_t* off, SstPacketI
  *   out: [G][9][H][W][3]. */
 SST_API int sst_upscale_blend(const float* img, int G, int h, int w, int s, int H, int W,
                       const SstPrevDesc* prev, int blend_n, float* out, void* stream);
+
+/* ---- residual enhancement layer and range coder (f2) ------- */
+
+/* compute_residual + aggregate_residual + sparsify_quantize
+ * (residual.py:62-105) for G GoPs at working resolution:
+ *   work [G][9][h][w][3] source frames, img [G][2][h][w][3] reconstruction
+ *   (I frame, shared P frame); avg [G][n] float64 (or NULL); dense [G][n] int16
+ *   quantised residual where kept else 0; mags [G][n] |avg| where kept else
+ *   -1 (or NULL; the fit_to_budget ranking key); count int32[G] kept entries.
+ *   n = h*w*3. */
+SST_API int sst_residual(const float* work, const float* img, int G, int h, int w, double theta,
+                         double step, double* avg, int16_t* dense, double* mags, int32_t* count,
+                         void* stream);
+
+/* sparsify_quantize (residual.py:86-105) of given float64 averages [G][n]. */
+SST_API int sst_sparsify(const double* avg, int G, int64_t n, double theta, double step,
+                         int16_t* dense, double* mags, int32_t* count, void* stream);
+
+/* apply_residual (residual.py:108-127): img[g][0..1] = clip(img + dense*step)
+ * unless count[g] == 0 (reconstruction left untouched). */
+SST_API int sst_apply_residual(float* img, const int16_t* dense, const int32_t* count, int G,
+                               int h, int w, double step, void* stream);
+
+/* out[e] = keep[e] ? dense[e] : 0 (fit_to_budget candidate scan). */
+SST_API int sst_mask_scan(const int16_t* dense, const uint8_t* keep, int64_t total, int16_t* out,
+                          void* stream);
+
+/* rangecoder.encode_scan (rangecoder.py:75-94,155-185,238-239) for G scans of
+ * n int16 samples: bytes to out + g*cap, length to out_len[g] (negative =
+ * -(needed bytes) when cap is too small).  idx_ws: int64 [G][n] workspace. */
+SST_API int sst_rc_encode(const int16_t* scans, int G, int64_t n, int64_t* idx_ws, uint8_t* out,
+                          int64_t cap, int64_t* out_len, void* stream);
+
+/* rangecoder.decode_scan (rangecoder.py:97-116,188-243): status[g] 0 ok,
+ * 1 truncated, 2 zero run overruns, 3 value overruns, 4 symbol budget. */
+SST_API int sst_rc_decode(const uint8_t* data, const int64_t* off, const int64_t* len, int G,
+                          int64_t n, int16_t* scans, int32_t* status, void* stream);
+
+/* rangecoder.encode_stream for explicit symbol lists (rangecoder.py:155-185):
+ * stream g = syms[off[g] .. off[g]+len[g]); bytes to out + g*cap. */
+SST_API int sst_rc_encode_symbols(const int32_t* syms, const int64_t* off, const int64_t* len,
+                                  int G, uint8_t* out, int64_t cap, int64_t* out_len,
+                                  void* stream);
+
+/* rangecoder.decode_stream (rangecoder.py:188-235): symbols to syms (<= cap),
+ * count to *nsym; status 0 ok, 1 truncated, 4 symbol budget, 7 capacity. */
+SST_API int sst_rc_decode_symbols(const uint8_t* data, int64_t nbytes, int64_t max_symbols,
+                                  int64_t cap, int32_t* syms, int64_t* nsym, int32_t* status,
+                                  void* stream);
 
 /* ---- metrics ------------------------------------------------------------ */
 

@@ -21,6 +21,8 @@ from .transport import (PacketFormatError, TokenPacket, packetize_tokens, parse_
 from .video import (GOP_SIZE, Frame, GoP, QualityReport, boundary_flicker, gop_psnr, mse, psnr,
                     segment_gops)
 from .plugin import tokenizer_decode, tokenizer_encode
+from .residual import (SparseResidual, aggregate_residual, apply_residual, compute_residual,
+                       fit_to_budget, raw_residual_rate, sparsify_quantize)
 
 __all__ = [
     "__version__",
@@ -31,5 +33,6 @@ __all__ = [
     "gop_psnr", "mse", "packetize_tokens", "parse_packet", "parse_packets", "psnr",
     "reassemble", "scale_gop", "segment_gops", "token_grid_shape", "token_packet_wire_size",
     "token_similarity", "tokenizer_decode", "tokenizer_encode", "top_k_drop_mask",
-    "upscale_frame",
+    "upscale_frame", "SparseResidual", "aggregate_residual", "apply_residual",
+    "compute_residual", "fit_to_budget", "raw_residual_rate", "sparsify_quantize",
 ]

@@ -21,7 +21,7 @@ BUILD = PKG.parent / "build" / "csrc"
 LIB = PKG / "libsemstream_b200.so"
 
 SOURCES = ["capi.cu", "tma_host.cu", "encode.cu", "select.cu", "packet.cu", "decode.cu",
-           "upscale.cu"]
+           "upscale.cu", "residual.cu"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -57,7 +57,7 @@ SIGNATURES = {
     "sst_encode": (_I, [_P, _I, _I, _I, _I, _P, _P, _P]),
     "sst_decode": (_I, [_P, _P, _L, _P, _I, _I, _I, _I, _I, _P, _P]),
     "sst_similarity": (_I, [_P, _P, _L, _I, _P, _P]),
-    "sst_topk_mask": (_I, [_P, _I, _L, _P, _P, _P]),
+    "sst_topk_mask": (_I, [_P, _I, _L, _P, _P, _P, _P]),
     "sst_apply_mask": (_I, [_P, _P, _P, _L, _I, _P]),
     "sst_select_drop": (_I, [_P, _P, _P, _I, _I, _I, _P, _P, _P]),
     "sst_packetize": (_I, [_P, _P, _I, _I, _I, _I, _P, _P, _P, _P, _L, _P, _P]),
@@ -67,6 +67,14 @@ SIGNATURES = {
     "sst_unpack_decode": (_I, [_P, _P, _P, _P, _L, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
     "sst_upscale_blend": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P]),
     "sst_mse": (_I, [_P, _P, _L, _L, _P, _P]),
+    "sst_residual": (_I, [_P, _P, _I, _I, _I, C.c_double, C.c_double, _P, _P, _P, _P, _P]),
+    "sst_sparsify": (_I, [_P, _I, _L, C.c_double, C.c_double, _P, _P, _P, _P]),
+    "sst_apply_residual": (_I, [_P, _P, _P, _I, _I, _I, C.c_double, _P]),
+    "sst_mask_scan": (_I, [_P, _P, _L, _P, _P]),
+    "sst_rc_encode": (_I, [_P, _I, _L, _P, _P, _L, _P, _P]),
+    "sst_rc_decode": (_I, [_P, _P, _P, _I, _L, _P, _P, _P]),
+    "sst_rc_encode_symbols": (_I, [_P, _P, _P, _I, _P, _L, _P, _P]),
+    "sst_rc_decode_symbols": (_I, [_P, _L, _L, _L, _P, _P, _P, _P]),
 }
 
 _lock = threading.Lock()

@@ -1,0 +1,471 @@
+// Residual enhancement layer and its adaptive range coder
+// (§8 f2).
+//
+//   k_residual      compute_residual + aggregate_residual + sparsify_quantize
+//                   (residual.py:62-105): per working-resolution sample, the
+//                   float64 temporal mean of x(t) - x_hat(t) (sequential sum
+//                   from 0.0, / 9), rint-quantised to int16 on the 1/127 grid
+//                   and thresholded; also the |avg| ranking key used by
+//                   fit_to_budget and the kept-entry count.
+//   k_apply_residual apply_residual (residual.py:108-127) on the two unique
+//                   reconstructions (I frame, shared P frame).
+//   k_rc_encode / k_rc_decode
+//                   rangecoder.py:75-243: zero-run symbolisation, order-0
+//                   adaptive model (counts start at 1, halved at total 2^16)
+//                   and the carry-less 32-bit range coder.  The coder is
+//                   serial per stream (adaptive model), so one CTA owns one
+//                   stream: all its threads first compact the non-zero
+//                   positions of the scan (ballot/popc, index order), then one
+//                   thread codes them with a Fenwick tree for the cumulative
+//                   frequencies (O(log 510) instead of the reference's O(510)).
+#include "common.cuh"
+
+namespace sst {
+
+// ---------------------------------------------------------------------------
+// residual
+
+__global__ void k_residual(const float* __restrict__ work, const float* __restrict__ img,
+                           int64_t n, double theta, double step, double* __restrict__ avg_out,
+                           int16_t* __restrict__ dense, double* __restrict__ mags,
+                           int32_t* __restrict__ count) {
+  // grid.y = GoP
+  const int g = blockIdx.y;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool kept = false;
+  if (e < n) {
+    const float* x = work + (int64_t)g * kGop * n;
+    const double ii = (double)img[(int64_t)g * 2 * n + e];
+    const double pp = (double)img[((int64_t)g * 2 + 1) * n + e];
+    double acc = 0.0 + ((double)x[e] - ii);                 // frame 0 vs I reconstruction
+#pragma unroll
+    for (int t = 1; t < kGop; ++t) acc = acc + ((double)x[(int64_t)t * n + e] - pp);
+    const double avg = acc / 9.0;
+    if (avg_out) avg_out[(int64_t)g * n + e] = avg;
+    double q = rint(avg / step);
+    q = q < -127.0 ? -127.0 : (q > 127.0 ? 127.0 : q);
+    const int16_t qv = (int16_t)(int)q;
+    const double mag = fabs(avg);
+    const int aq = qv < 0 ? -qv : qv;
+    kept = mag >= theta && qv != 0 && (double)aq * step >= theta;
+    dense[(int64_t)g * n + e] = kept ? qv : (int16_t)0;
+    if (mags) mags[(int64_t)g * n + e] = kept ? mag : -1.0;
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, kept);
+  if ((threadIdx.x & 31) == 0 && bal) atomicAdd(&count[g], __popc(bal));
+}
+
+// sparsify_quantize from a given float64 average (residual.py:86-105)
+__global__ void k_sparsify(const double* __restrict__ avg, int64_t n, double theta, double step,
+                           int16_t* __restrict__ dense, double* __restrict__ mags,
+                           int32_t* __restrict__ count) {
+  const int g = blockIdx.y;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool kept = false;
+  if (e < n) {
+    const double a = avg[(int64_t)g * n + e];
+    double q = rint(a / step);
+    q = q < -127.0 ? -127.0 : (q > 127.0 ? 127.0 : q);
+    const int16_t qv = (int16_t)(int)q;
+    const double mag = fabs(a);
+    const int aq = qv < 0 ? -qv : qv;
+    kept = mag >= theta && qv != 0 && (double)aq * step >= theta;
+    dense[(int64_t)g * n + e] = kept ? qv : (int16_t)0;
+    if (mags) mags[(int64_t)g * n + e] = kept ? mag : -1.0;
+  }
+  const unsigned bal = __ballot_sync(0xffffffffu, kept);
+  if ((threadIdx.x & 31) == 0 && bal) atomicAdd(&count[g], __popc(bal));
+}
+
+__global__ void k_apply_residual(float* __restrict__ img, const int16_t* __restrict__ dense,
+                                 const int32_t* __restrict__ count, int64_t n, double step) {
+  const int g = blockIdx.y;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n || count[g] == 0) return;           // empty residual: recon unchanged
+  const double delta = (double)dense[(int64_t)g * n + e] * step;
+#pragma unroll
+  for (int im = 0; im < 2; ++im) {
+    float* p = img + ((int64_t)g * 2 + im) * n + e;
+    *p = (float)clip01((double)*p + delta);
+  }
+}
+
+// keep only the chosen entries of a dense scan (fit_to_budget candidates)
+__global__ void k_mask_scan(const int16_t* __restrict__ dense, const uint8_t* __restrict__ keep,
+                            int64_t total, int16_t* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e < total) out[e] = keep[e] ? dense[e] : (int16_t)0;
+}
+
+// ---------------------------------------------------------------------------
+// range coder
+
+constexpr int kAlpha = 510;
+constexpr int kFen = 512;                         // Fenwick size (power of two >= 510)
+constexpr uint64_t kMask32 = 0xFFFFFFFFull;
+constexpr uint64_t kTop = 1ull << 24;
+constexpr uint64_t kBottom = 1ull << 16;
+constexpr int kRcThreads = 1024;
+
+struct Model {
+  uint32_t fen[kFen + 1];                         // 1-based Fenwick tree of counts
+  uint32_t cnt[kFen];
+  uint32_t total;
+};
+
+__device__ void model_build(Model& m) {
+  for (int i = 0; i <= kFen; ++i) m.fen[i] = 0;
+  uint32_t tot = 0;
+  for (int s = 0; s < kAlpha; ++s) {
+    tot += m.cnt[s];
+    for (int i = s + 1; i <= kFen; i += i & -i) m.fen[i] += m.cnt[s];
+  }
+  m.total = tot;
+}
+
+__device__ __forceinline__ uint32_t model_cum(const Model& m, int s) {   // sum cnt[0..s)
+  uint32_t c = 0;
+  for (int i = s; i > 0; i -= i & -i) c += m.fen[i];
+  return c;
+}
+
+__device__ __forceinline__ void model_update(Model& m, int s) {
+  m.cnt[s] += 1;
+  for (int i = s + 1; i <= kFen; i += i & -i) m.fen[i] += 1;
+  m.total += 1;
+  if (m.total >= (uint32_t)kBottom) {              // rangecoder.py:147-149
+    for (int t = 0; t < kAlpha; ++t) m.cnt[t] = (m.cnt[t] + 1) / 2;
+    model_build(m);
+  }
+}
+
+// largest symbol whose cumulative low is <= target; returns its low in *lo
+__device__ __forceinline__ int model_find(const Model& m, uint32_t target, uint32_t* lo) {
+  int pos = 0;
+  uint32_t acc = 0;
+  for (int step = kFen; step > 0; step >>= 1) {
+    const int nxt = pos + step;
+    if (nxt <= kFen && acc + m.fen[nxt] <= target) {
+      pos = nxt;
+      acc += m.fen[nxt];
+    }
+  }
+  *lo = acc;
+  return pos;                                      // symbol index (0-based) = pos
+}
+
+struct Enc {
+  uint64_t low, range;
+  uint8_t* out;
+  int64_t pos, cap;
+  bool overflow;
+};
+
+__device__ __forceinline__ void enc_symbol(Enc& e, Model& m, int sym) {
+  const uint64_t c = model_cum(m, sym);
+  const uint64_t d = c + m.cnt[sym];
+  const uint64_t r = e.range / m.total;
+  e.low += c * r;
+  e.range = (d - c) * r;
+  while ((e.low ^ (e.low + e.range)) < kTop || e.range < kBottom) {
+    if ((e.low ^ (e.low + e.range)) >= kTop) e.range = (kMask32 + 1 - e.low) & (kBottom - 1);
+    if (e.pos < e.cap) e.out[e.pos] = (uint8_t)((e.low >> 24) & 0xFF);
+    else e.overflow = true;
+    e.pos += 1;
+    e.low = (e.low << 8) & kMask32;
+    e.range <<= 8;
+  }
+  model_update(m, sym);
+}
+
+// Compact the non-zero positions of one stream's scan into idx (index order);
+// returns their count.  All threads of the CTA.
+__device__ int64_t compact_nonzero(const int16_t* scan, int64_t n, int64_t* idx, int* s_warp,
+                                   int64_t* s_base) {
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid == 0) *s_base = 0;
+  __syncthreads();
+  for (int64_t b = 0; b < n; b += kRcThreads) {
+    const int64_t j = b + tid;
+    const bool nz = j < n && scan[j] != 0;
+    const unsigned bal = __ballot_sync(0xffffffffu, nz);
+    if (lane == 0) s_warp[wid] = __popc(bal);
+    __syncthreads();
+    int off = 0;
+    for (int w = 0; w < wid; ++w) off += s_warp[w];
+    const int64_t base = *s_base;
+    if (nz) idx[base + off + __popc(bal & ((1u << lane) - 1u))] = j;
+    __syncthreads();
+    if (tid == 0) {
+      int tot = 0;
+      for (int w = 0; w < kRcThreads / 32; ++w) tot += s_warp[w];
+      *s_base = base + tot;
+    }
+    __syncthreads();
+  }
+  return *s_base;
+}
+
+// One CTA per stream: encode_scan(scan[g]) -> out[g*cap ...], len[g]
+// (len = -1 if the output would exceed cap).
+__global__ void __launch_bounds__(kRcThreads)
+    k_rc_encode(const int16_t* __restrict__ scans, int64_t n, int64_t* __restrict__ idx_ws,
+                uint8_t* __restrict__ out, int64_t cap, int64_t* __restrict__ out_len) {
+  __shared__ Model m;
+  __shared__ int s_warp[kRcThreads / 32];
+  __shared__ int64_t s_base;
+  const int g = blockIdx.x;
+  const int16_t* scan = scans + (int64_t)g * n;
+  int64_t* idx = idx_ws + (int64_t)g * n;
+  const int64_t nnz = compact_nonzero(scan, n, idx, s_warp, &s_base);
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < kFen; ++s) m.cnt[s] = s < kAlpha ? 1u : 0u;
+  model_build(m);
+  Enc e{0, kMask32, out + (int64_t)g * cap, 0, cap, false};
+  int64_t pos = 0;
+  for (int64_t i = 0; i < nnz; ++i) {              // rangecoder.py:75-94
+    const int64_t j = idx[i];
+    int64_t gap = j - pos;
+    while (gap > 255) {
+      enc_symbol(e, m, 255);
+      gap -= 255;
+    }
+    if (gap) enc_symbol(e, m, (int)gap);
+    const int v = scan[j];
+    enc_symbol(e, m, v < 0 ? v + 383 : v + 382);
+    pos = j + 1;
+  }
+  enc_symbol(e, m, 0);                              // EOS
+  for (int k = 0; k < 4; ++k) {                     // rangecoder.py:182-184
+    if (e.pos < e.cap) e.out[e.pos] = (uint8_t)((e.low >> 24) & 0xFF);
+    else e.overflow = true;
+    e.pos += 1;
+    e.low = (e.low << 8) & kMask32;
+  }
+  out_len[g] = e.overflow ? -e.pos : e.pos;
+}
+
+// One CTA per stream: decode_scan(data[g], n) -> scan[g]; status[g]:
+// 0 ok, 1 truncated, 2 zero run overruns, 3 value overruns, 4 symbol budget
+__global__ void __launch_bounds__(kRcThreads)
+    k_rc_decode(const uint8_t* __restrict__ data, const int64_t* __restrict__ off,
+                const int64_t* __restrict__ len, int64_t n, int16_t* __restrict__ scans,
+                int32_t* __restrict__ status) {
+  __shared__ Model m;
+  const int g = blockIdx.x;
+  int16_t* scan = scans + (int64_t)g * n;
+  for (int64_t j = threadIdx.x; j < n; j += kRcThreads) scan[j] = 0;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  const uint8_t* src = data + off[g];
+  const int64_t nb = len[g];
+  int64_t p = 0;
+  int st = 0;
+  for (int s = 0; s < kFen; ++s) m.cnt[s] = s < kAlpha ? 1u : 0u;
+  model_build(m);
+  uint64_t state = 0;
+  for (int k = 0; k < 4; ++k) {
+    if (p >= nb) { st = 1; break; }
+    state = (state << 8) | src[p++];
+  }
+  uint64_t low = 0, range = kMask32;
+  int64_t pos = 0, nsym = 0;
+  while (st == 0) {
+    const uint64_t total = m.total;
+    const uint64_t r = range / total;
+    uint64_t val = (state - low) / r;              // rangecoder.py:217-219
+    if (val >= total) val = total - 1;
+    uint32_t c32;
+    const int sym = model_find(m, (uint32_t)val, &c32);
+    const uint64_t c = c32, d = c + m.cnt[sym];
+    low += c * r;
+    range = (d - c) * r;
+    while ((low ^ (low + range)) < kTop || range < kBottom) {
+      if ((low ^ (low + range)) >= kTop) range = (kMask32 + 1 - low) & (kBottom - 1);
+      if (p >= nb) { st = 1; break; }
+      state = ((state << 8) | src[p++]) & kMask32;
+      low = (low << 8) & kMask32;
+      range <<= 8;
+    }
+    if (st) break;
+    model_update(m, sym);
+    ++nsym;
+    if (sym == 0) break;                            // EOS
+    if (sym <= 255) {                               // zero run (rangecoder.py:107-110)
+      pos += sym;
+      if (pos > n) { st = 2; break; }
+    } else {
+      if (pos >= n) { st = 3; break; }
+      scan[pos++] = (int16_t)(sym <= 382 ? sym - 383 : sym - 382);
+    }
+    if (nsym >= (1 << 24)) { st = 4; break; }
+  }
+  status[g] = st;
+}
+
+// encode_stream for explicit symbol lists (one CTA / thread per stream)
+__global__ void k_rc_encode_symbols(const int32_t* __restrict__ syms, const int64_t* __restrict__ off,
+                                    const int64_t* __restrict__ len, uint8_t* __restrict__ out,
+                                    int64_t cap, int64_t* __restrict__ out_len) {
+  __shared__ Model m;
+  if (threadIdx.x != 0) return;
+  const int g = blockIdx.x;
+  for (int s = 0; s < kFen; ++s) m.cnt[s] = s < kAlpha ? 1u : 0u;
+  model_build(m);
+  Enc e{0, kMask32, out + (int64_t)g * cap, 0, cap, false};
+  const int32_t* src = syms + off[g];
+  for (int64_t i = 0; i < len[g]; ++i) enc_symbol(e, m, src[i]);
+  for (int k = 0; k < 4; ++k) {
+    if (e.pos < e.cap) e.out[e.pos] = (uint8_t)((e.low >> 24) & 0xFF);
+    else e.overflow = true;
+    e.pos += 1;
+    e.low = (e.low << 8) & kMask32;
+  }
+  out_len[g] = e.overflow ? -e.pos : e.pos;
+}
+
+// decode_stream to a symbol list (rangecoder.py:188-235); status 1 truncated,
+// 4 symbol budget exceeded, 7 output capacity exceeded
+__global__ void k_rc_decode_symbols(const uint8_t* __restrict__ src, int64_t nb, int64_t max_symbols,
+                                    int64_t cap, int32_t* __restrict__ syms, int64_t* __restrict__ nsym,
+                                    int32_t* __restrict__ status) {
+  __shared__ Model m;
+  if (threadIdx.x != 0) return;
+  for (int s = 0; s < kFen; ++s) m.cnt[s] = s < kAlpha ? 1u : 0u;
+  model_build(m);
+  int64_t p = 0, count = 0;
+  int st = 0;
+  uint64_t state = 0;
+  for (int k = 0; k < 4; ++k) {
+    if (p >= nb) { st = 1; break; }
+    state = (state << 8) | src[p++];
+  }
+  uint64_t low = 0, range = kMask32;
+  while (st == 0) {
+    const uint64_t total = m.total;
+    const uint64_t r = range / total;
+    uint64_t val = (state - low) / r;
+    if (val >= total) val = total - 1;
+    uint32_t c32;
+    const int sym = model_find(m, (uint32_t)val, &c32);
+    if (count >= cap) { st = 7; break; }
+    syms[count++] = sym;
+    const uint64_t c = c32, d = c + m.cnt[sym];
+    low += c * r;
+    range = (d - c) * r;
+    while ((low ^ (low + range)) < kTop || range < kBottom) {
+      if ((low ^ (low + range)) >= kTop) range = (kMask32 + 1 - low) & (kBottom - 1);
+      if (p >= nb) { st = 1; break; }
+      state = ((state << 8) | src[p++]) & kMask32;
+      low = (low << 8) & kMask32;
+      range <<= 8;
+    }
+    if (st) break;
+    model_update(m, sym);
+    if (sym == 0) break;
+    if (count >= max_symbols) { st = 4; break; }
+  }
+  *nsym = count;
+  *status = st;
+}
+
+}  // namespace sst
+
+using namespace sst;
+
+extern "C" int sst_rc_encode_symbols(const int32_t* syms, const int64_t* off, const int64_t* len,
+                                     int G, uint8_t* out, int64_t cap, int64_t* out_len,
+                                     void* stream) {
+  if (G < 0 || cap < 0) return SST_ERR_ARG;
+  if (G == 0) return SST_OK;
+  if (!syms || !off || !len || !out || !out_len) return SST_ERR_ARG;
+  k_rc_encode_symbols<<<G, 32, 0, static_cast<cudaStream_t>(stream)>>>(syms, off, len, out, cap,
+                                                                         out_len);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+extern "C" int sst_rc_decode_symbols(const uint8_t* data, int64_t nbytes, int64_t max_symbols,
+                                     int64_t cap, int32_t* syms, int64_t* nsym, int32_t* status,
+                                     void* stream) {
+  if (nbytes < 0 || cap < 0) return SST_ERR_ARG;
+  if (!data || !syms || !nsym || !status) return SST_ERR_ARG;
+  k_rc_decode_symbols<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(data, nbytes, max_symbols,
+                                                                         cap, syms, nsym, status);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+extern "C" int sst_residual(const float* work, const float* img, int G, int h, int w,
+                            double theta, double step, double* avg, int16_t* dense, double* mags,
+                            int32_t* count, void* stream) {
+  if (G < 0 || h <= 0 || w <= 0 || !(step > 0.0) || theta < 0.0) return SST_ERR_ARG;
+  if (G == 0) return SST_OK;
+  if (!work || !img || !dense || !count) return SST_ERR_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t n = (int64_t)h * w * 3;
+  SST_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int32_t) * G, st));
+  dim3 grid((unsigned)ceil_div64(n, 256), G);
+  k_residual<<<grid, 256, 0, st>>>(work, img, n, theta, step, avg, dense, mags, count);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+extern "C" int sst_sparsify(const double* avg, int G, int64_t n, double theta, double step,
+                            int16_t* dense, double* mags, int32_t* count, void* stream) {
+  if (G < 0 || n < 0 || !(step > 0.0) || theta < 0.0) return SST_ERR_ARG;
+  if (G == 0) return SST_OK;
+  if (!count || (n > 0 && (!avg || !dense))) return SST_ERR_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SST_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int32_t) * G, st));
+  if (n == 0) return SST_OK;
+  dim3 grid((unsigned)ceil_div64(n, 256), G);
+  k_sparsify<<<grid, 256, 0, st>>>(avg, n, theta, step, dense, mags, count);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+extern "C" int sst_apply_residual(float* img, const int16_t* dense, const int32_t* count, int G,
+                                  int h, int w, double step, void* stream) {
+  if (G < 0 || h <= 0 || w <= 0 || !(step > 0.0)) return SST_ERR_ARG;
+  if (G == 0) return SST_OK;
+  if (!img || !dense || !count) return SST_ERR_ARG;
+  const int64_t n = (int64_t)h * w * 3;
+  dim3 grid((unsigned)ceil_div64(n, 256), G);
+  k_apply_residual<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(img, dense, count, n, step);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+extern "C" int sst_mask_scan(const int16_t* dense, const uint8_t* keep, int64_t total, int16_t* out,
+                             void* stream) {
+  if (total < 0) return SST_ERR_ARG;
+  if (total == 0) return SST_OK;
+  if (!dense || !keep || !out) return SST_ERR_ARG;
+  k_mask_scan<<<(unsigned)ceil_div64(total, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      dense, keep, total, out);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+extern "C" int sst_rc_encode(const int16_t* scans, int G, int64_t n, int64_t* idx_ws, uint8_t* out,
+                             int64_t cap, int64_t* out_len, void* stream) {
+  if (G < 0 || n < 0 || cap < 0) return SST_ERR_ARG;
+  if (G == 0) return SST_OK;
+  if ((n > 0 && (!scans || !idx_ws)) || !out || !out_len) return SST_ERR_ARG;
+  k_rc_encode<<<G, kRcThreads, 0, static_cast<cudaStream_t>(stream)>>>(scans, n, idx_ws, out, cap,
+                                                                         out_len);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+extern "C" int sst_rc_decode(const uint8_t* data, const int64_t* off, const int64_t* len, int G,
+                             int64_t n, int16_t* scans, int32_t* status, void* stream) {
+  if (G < 0 || n < 0) return SST_ERR_ARG;
+  if (G == 0) return SST_OK;
+  if (!data || !off || !len || !status || (n > 0 && !scans)) return SST_ERR_ARG;
+  k_rc_decode<<<G, kRcThreads, 0, static_cast<cudaStream_t>(stream)>>>(data, off, len, n, scans,
+                                                                         status);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}

@@ -63,7 +63,7 @@ constexpr int kSelThreads = 1024;
 // token batch and its [G][2][n] mask (fused apply_token_mask).
 __global__ void __launch_bounds__(kSelThreads)
     k_topk(const double* __restrict__ sim, int64_t n, const int32_t* __restrict__ kk,
-           uint8_t* __restrict__ drop, double* tok, uint8_t* p_mask) {
+           uint8_t* __restrict__ drop, double* tok, uint8_t* p_mask, double* kth) {
   __shared__ uint32_t hist[256];
   __shared__ uint64_t s_prefix;
   __shared__ int64_t s_krem;
@@ -138,6 +138,10 @@ __global__ void __launch_bounds__(kSelThreads)
     // (in index order) are dropped.
   }
   if (tid == 0) s_running = 0;
+  if (tid == 0 && kth != nullptr && k > 0) {      // value of the k-th largest key
+    const uint64_t b = (prefix & 0x8000000000000000ull) ? (prefix & 0x7FFFFFFFFFFFFFFFull) : ~prefix;
+    kth[g] = __longlong_as_double((long long)b);
+  }
   __syncthreads();
   const uint64_t T = prefix;
   const int lane = tid & 31, wid = tid >> 5;
@@ -210,12 +214,12 @@ extern "C" int sst_similarity(const double* p, const double* i, int64_t n, int C
 }
 
 extern "C" int sst_topk_mask(const double* sim, int G, int64_t n, const int32_t* k, uint8_t* drop,
-                             void* stream) {
+                             double* kth, void* stream) {
   if (G < 0 || n < 0) return SST_ERR_ARG;
   if (G == 0 || n == 0) return SST_OK;
   if (!sim || !k || !drop) return SST_ERR_ARG;
   k_topk<<<G, kSelThreads, 0, static_cast<cudaStream_t>(stream)>>>(sim, n, k, drop, nullptr,
-                                                                    nullptr);
+                                                                    nullptr, kth);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }
@@ -238,7 +242,8 @@ extern "C" int sst_select_drop(const double* sim, double* tok, uint8_t* p_mask, 
   int64_t n = (int64_t)Ht * Wt;
   if (G == 0 || n == 0) return SST_OK;
   if (!sim || !tok || !p_mask || !k) return SST_ERR_ARG;
-  k_topk<<<G, kSelThreads, 0, static_cast<cudaStream_t>(stream)>>>(sim, n, k, drop, tok, p_mask);
+  k_topk<<<G, kSelThreads, 0, static_cast<cudaStream_t>(stream)>>>(sim, n, k, drop, tok, p_mask,
+                                                                    nullptr);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }

@@ -4,7 +4,7 @@
 mkdir -p gpurun_out
 TAG=${1:-r01}
 B="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:sst:: --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ --csv \
     --log-file gpurun_out/${TAG}_launches.csv $B > gpurun_out/${TAG}_launches.log 2>&1
 echo "launches rc=$?"
 for k in k_upscale_blend_tma k_encode k_decode k_packetize k_topk k_parse; do

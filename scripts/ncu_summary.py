@@ -72,10 +72,10 @@ def launches(path: Path):
     for r in rows[hdr + 1:]:
         if len(r) <= vi:
             continue
-        name = r[ki]
-        if not name.startswith("sst::") and "sst::k_" not in name:
+        name = r[ki].replace("void ", "").replace("sst::", "")
+        if not name.startswith("k_"):
             continue                                   # input generation etc.
-        short = name.split("(")[0].replace("void ", "")
+        short = name.split("(")[0]
         tot[short] += float(r[vi].replace(",", ""))
         cnt[short] += 1
     return tot, cnt
@@ -87,8 +87,10 @@ def main():
     md = [f"# ncu summary — {tag}", ""]
     tot, cnt = launches(lcsv)
     T = sum(tot.values())
-    md += ["## Launch list (our kernels only; `--metrics gpu__time_duration.sum "
-           "--clock-control none`, cold-cache and serialised: compare shares)", "",
+    md += ["## Launch list (our kernels only; `ncu --metrics gpu__time_duration.sum "
+           "--clock-control none -k regex:^k_` over `python bench.py --steps 2 --warmup 1 "
+           "--no-e2e --no-cpu-baseline`, i.e. the bench workload: 64 x 1080p streams, 32 GoPs "
+           "per launch; cold-cache and serialised, so compare shares)", "",
            "| kernel | launches | total µs | share |", "|---|---|---|---|"]
     for k, v in sorted(tot.items(), key=lambda x: -x[1]):
         md.append(f"| `{k}` | {cnt[k]} | {v / 1000:.1f} | {100 * v / T:.1f}% |")
