@@ -576,6 +576,33 @@ def cpu_baseline(a) -> dict:
                       f"wall {walls[0]:.1f} s"}
 
 
+def parity_sample(a, device) -> dict:
+    """PSNR delta vs the CPU reference algorithm on one full-size GoP: the same
+    synthetic 1080p GoP through the GPU path and through the oracle port."""
+    import numpy as np
+    import torch
+
+    from oracle import semstream_oracle as O
+    from oracle.synth import make_clip
+    from paper_2602_03529_b200.pipeline import StreamBank
+
+    src = make_clip("moving-square", a.width, a.height, GOP, seed=0).gop(0)
+    s = scale_of(0, 0)
+    bank = StreamBank(1, a.height, a.width, concurrent_groups=False)
+    fr = torch.from_numpy(src[None].copy()).to(device)
+    out = torch.empty_like(fr)
+    bank.step({s: fr}, {s: out}, {s: [0]}, {s: [0]}, drop_rate=a.drop)
+    gpu = out.cpu().numpy()[0]
+    ref = np.stack(O.pipeline_gop(src, s, gop_id=0, drop_rate=a.drop)["frames"])
+    p_gpu, _ = O.gop_psnr(list(src), list(gpu))
+    p_ref, _ = O.gop_psnr(list(src), list(ref))
+    return {"sample": f"moving-square {a.height}p GoP, s={s}, {int(a.drop * 100)}% drop",
+            "psnr_gpu_db": round(p_gpu, 6), "psnr_cpu_ref_db": round(p_ref, 6),
+            "psnr_delta_db": p_gpu - p_ref,
+            "max_abs_diff": float(np.abs(gpu.astype(np.float64) - ref).max()),
+            "bit_exact": bool(np.array_equal(gpu, ref))}
+
+
 # ---------------------------------------------------------------------------
 
 def main():
@@ -621,6 +648,7 @@ def main():
         line["e2e"] = res.get("e2e")
         if world == 1 and not a.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(a)
+            line["parity"] = parity_sample(a, torch.device("cuda", local_rank))
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -232,6 +232,10 @@ SST_API int sst_residual(const float* work, const float* img, int G, int h, int 
                          double step, double* avg, int16_t* dense, double* mags, int32_t* count,
                          void* stream);
 
+/* aggregate_residual (residual.py:76-83): out[e] = (sum_t res[t][e]) / T,
+ * summed sequentially from 0.0 in float64. */
+SST_API int sst_mean_axis0(const double* res, int T, int64_t n, double* out, void* stream);
+
 /* sparsify_quantize (residual.py:86-105) of given float64 averages [G][n]. */
 SST_API int sst_sparsify(const double* avg, int G, int64_t n, double theta, double step,
                          int16_t* dense, double* mags, int32_t* count, void* stream);

@@ -29,6 +29,8 @@ def ptr(t) -> int | None:
 
 def h2d(a: np.ndarray, dtype=None) -> torch.Tensor:
     arr = np.ascontiguousarray(a if dtype is None else np.asarray(a, dtype=dtype))
+    if not arr.flags.writeable:          # torch.from_numpy needs a writable buffer
+        arr = arr.copy()
     return torch.from_numpy(arr).to(device(), non_blocking=False)
 
 

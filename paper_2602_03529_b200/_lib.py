@@ -68,6 +68,7 @@ SIGNATURES = {
     "sst_upscale_blend": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P]),
     "sst_mse": (_I, [_P, _P, _L, _L, _P, _P]),
     "sst_residual": (_I, [_P, _P, _I, _I, _I, C.c_double, C.c_double, _P, _P, _P, _P, _P]),
+    "sst_mean_axis0": (_I, [_P, _I, _L, _P, _P]),
     "sst_sparsify": (_I, [_P, _I, _L, C.c_double, C.c_double, _P, _P, _P, _P]),
     "sst_apply_residual": (_I, [_P, _P, _P, _I, _I, _I, C.c_double, _P]),
     "sst_mask_scan": (_I, [_P, _P, _L, _P, _P]),

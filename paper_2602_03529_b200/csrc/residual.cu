@@ -55,6 +55,17 @@ __global__ void k_residual(const float* __restrict__ work, const float* __restri
   if ((threadIdx.x & 31) == 0 && bal) atomicAdd(&count[g], __popc(bal));
 }
 
+// aggregate_residual: mean over the window axis, sequential from 0.0, / T
+// (residual.py:76-83 -> numpy add.reduce over axis 0, then true_divide)
+__global__ void k_mean_axis0(const double* __restrict__ res, int T, int64_t n,
+                             double* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  double acc = 0.0 + res[e];
+  for (int t = 1; t < T; ++t) acc = acc + res[(int64_t)t * n + e];
+  out[e] = acc / (double)T;
+}
+
 // sparsify_quantize from a given float64 average (residual.py:86-105)
 __global__ void k_sparsify(const double* __restrict__ avg, int64_t n, double theta, double step,
                            int16_t* __restrict__ dense, double* __restrict__ mags,
@@ -407,6 +418,16 @@ extern "C" int sst_residual(const float* work, const float* img, int G, int h, i
   SST_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(int32_t) * G, st));
   dim3 grid((unsigned)ceil_div64(n, 256), G);
   k_residual<<<grid, 256, 0, st>>>(work, img, n, theta, step, avg, dense, mags, count);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+extern "C" int sst_mean_axis0(const double* res, int T, int64_t n, double* out, void* stream) {
+  if (T < 1 || n < 0) return SST_ERR_ARG;
+  if (n == 0) return SST_OK;
+  if (!res || !out) return SST_ERR_ARG;
+  k_mean_axis0<<<(unsigned)ceil_div64(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      res, T, n, out);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }
