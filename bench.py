@@ -56,6 +56,8 @@ def parse_args():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--streams", type=int, default=64, help="streams per GPU")
+    ap.add_argument("--lanes", type=int, default=2,
+                    help="independent StreamBanks, each on its own CUDA stream (even)")
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--drop", type=float, default=0.10)
@@ -231,7 +233,14 @@ def run_ours(a, rank, world, local_rank):
     ne = len(even)
     inputs = make_inputs([rank * S + i for i in even + odd], H, W, dev)
     out = torch.empty_like(inputs[0])
-    lanes = [dict(sl=slice(0, ne), phase=0, n=ne), dict(sl=slice(ne, S), phase=1, n=S - ne)]
+    lanes = []
+    per = max(1, a.lanes // 2)                  # lanes per phase
+    for phase, (lo, hi) in enumerate(((0, ne), (ne, S))):
+        cuts = [lo + (hi - lo) * j // per for j in range(per + 1)]
+        for j in range(per):
+            if cuts[j + 1] > cuts[j]:
+                lanes.append(dict(sl=slice(cuts[j], cuts[j + 1]), phase=phase,
+                                  n=cuts[j + 1] - cuts[j]))
     for ln in lanes:
         ln["bank"] = StreamBank(ln["n"], H, W, concurrent_groups=False)
         ln["stream"] = torch.cuda.Stream(device=dev)
@@ -326,7 +335,7 @@ def run_ours(a, rank, world, local_rank):
 
     res = dict(ms=ms_max, value=value, stages=stages, launches=launches,
                clocks=clocks.summary(), psnr=psnr)
-    res["roofline"] = roofline(a, stages, S // 2, a.roofline_steps * 2)
+    res["roofline"] = roofline(a, stages, S // len(lanes), a.roofline_steps * len(lanes))
     if not a.no_e2e:
         del inputs, out
         torch.cuda.empty_cache()
@@ -634,6 +643,7 @@ def main():
 
     import torch
     import torch.distributed as dist
+    torch.cuda.set_device(local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     res = run_ours(a, rank, world, local_rank)

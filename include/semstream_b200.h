@@ -201,11 +201,13 @@ SST_API int sst_reassemble(const uint8_t* buf, const int64_t* off, SstPacketInfo
 /* reassemble x2 + decode_gop fused: the mask-aware decoder reads each token
  * straight out of the winning packet (no token matrix in HBM).
  *   packets routed per GoP g as target[i] = 2*g + kind; exp_gop[G];
- *   out: [G][2][h][w][3] float32 (I image, concealed P image). */
+ *   ws: device workspace of sst_unpack_decode_workspace(G, H', W') bytes
+ *   (16-byte aligned); out: [G][2][h][w][3] float32 (I image, concealed P). */
+SST_API int64_t sst_unpack_decode_workspace(int G, int Ht, int Wt);
 SST_API int sst_unpack_decode(const uint8_t* buf, const int64_t* off, SstPacketInfo* info,
-                      const int32_t* target, int64_t n, int G, int Ht, int Wt, int h, int w,
-                      const uint32_t* exp_gop, uint32_t* winner, int32_t* stats, float* out,
-                      void* stream);
+                              const int32_t* target, int64_t n, int G, int Ht, int Wt, int h, int w,
+                              const uint32_t* exp_gop, uint32_t* winner, int32_t* stats, void* ws,
+                              float* out, void* stream);
 
 /* ---- reconstruction ----------------------------------------------------- */
 

@@ -64,7 +64,8 @@ SIGNATURES = {
     "sst_serialize": (_I, [_P, _P, _P, _P, _P, _L, _P, _P, _P]),
     "sst_parse": (_I, [_P, _P, _P, _P, _L, _P, _P]),
     "sst_reassemble": (_I, [_P, _P, _P, _P, _L, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
-    "sst_unpack_decode": (_I, [_P, _P, _P, _P, _L, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P]),
+    "sst_unpack_decode_workspace": (_L, [_I, _I, _I]),
+    "sst_unpack_decode": (_I, [_P, _P, _P, _P, _L, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     "sst_upscale_blend": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P]),
     "sst_mse": (_I, [_P, _P, _L, _L, _P, _P]),
     "sst_residual": (_I, [_P, _P, _I, _I, _I, C.c_double, C.c_double, _P, _P, _P, _P, _P]),

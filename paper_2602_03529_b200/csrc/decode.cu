@@ -14,6 +14,59 @@
 
 namespace sst {
 
+// Winning packet of one matrix row, resolved once by k_rowprep
+struct RowInfo {
+  int64_t payload;   // byte offset of the payload in the packet buffer
+  double qmin;       // quant_min
+  double step;       // quant_range / 255.0 (transport.py:199)
+  int32_t ok;
+  int32_t pad;
+};
+
+// One warp per matrix row: validate the winner's shape, count the row as
+// received, and turn its MSB-first mask into per-token payload slots.
+__global__ void __launch_bounds__(256)
+    k_rowprep(const int64_t* __restrict__ off, SstPacketInfo* info, const uint8_t* __restrict__ buf,
+              const uint32_t* __restrict__ winner, int64_t nrows, int Ht, int Wt,
+              RowInfo* __restrict__ rows, int32_t* __restrict__ tokoff, int32_t* stats) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (r >= nrows) return;
+  const uint32_t win = winner[r];
+  bool ok = win != 0xFFFFFFFFu;
+  RowInfo ri{0, 0.0, 0.0, 0, 0};
+  const uint8_t* mb = nullptr;
+  if (ok) {
+    SstPacketInfo& p = info[win];
+    const uint8_t* pkt = buf + off[win];
+    mb = pkt + p.mask_off;
+    // shape contract of the fused path: W' tokens of 12 channels
+    bool bad = p.channels != kChannels || p.width < Wt;
+    for (int x = Wt + lane; !bad && x < p.width; x += 32)
+      if ((mb[x >> 3] >> (7 - (x & 7))) & 1) bad = true;
+    bad = __any_sync(0xffffffffu, bad);
+    if (bad) {
+      if (lane == 0) p.status = SST_PKT_SHAPE;
+      ok = false;
+    } else {
+      ri.payload = off[win] + p.payload_off;
+      ri.qmin = p.dqmin;
+      ri.step = p.dqrange / 255.0;
+      ri.ok = 1;
+      if (lane == 0) atomicAdd(&stats[2 * (r / Ht) + 1], 1);   // rows_received
+    }
+  }
+  if (lane == 0) rows[r] = ri;
+  int running = 0;
+  for (int base = 0; base < Wt; base += 32) {
+    const int x = base + lane;
+    const bool v = ok && x < Wt && ((mb[x >> 3] >> (7 - (x & 7))) & 1);
+    const unsigned bal = __ballot_sync(0xffffffffu, v);
+    if (x < Wt) tokoff[r * Wt + x] = v ? running + __popc(bal & ((1u << lane) - 1u)) : -1;
+    running += __popc(bal);
+  }
+}
+
 constexpr int kDecTok = 16;     // tokens per CTA
 constexpr int kDecThreads = 384; // = kDecTok * 3 channels * 8 pixel rows
 
@@ -29,6 +82,8 @@ struct DecArgs {
   SstPacketInfo* info;
   const uint32_t* winner;      // [G*2][Ht]
   int32_t* stats;              // [G*2][2]
+  const struct RowInfo* rows;  // [G*2][Ht] winning packet per matrix row
+  const int32_t* tokoff;       // [G*2][Ht][Wt] payload slot of each token or -1
   int G, Ht, Wt, h, w;
   float* out;                  // [G][2][h][w][3]
 };
@@ -37,7 +92,9 @@ template <bool kFromPackets>
 __global__ void __launch_bounds__(kDecThreads) k_decode(DecArgs a) {
   __shared__ double tok[2][kDecTok][kChannels];
   __shared__ uint8_t valid[kDecTok];
-  __shared__ double s1[2][kDecTok][3][8][2];       // [img][tok][ch][y][x] for block columns 0, 1
+  // column-IDCT results for block columns 0, 1: [img][y][x][tok*3 + ch]
+  // (token/channel innermost so a warp's reads are consecutive: no conflicts)
+  __shared__ double s1[2][8][2][kDecTok * 3];
   __shared__ double zc[8];                         // column IDCT of an all-zero column
   __shared__ float pix[2][8][kDecTok * 8][3];      // output tile
 
@@ -48,59 +105,22 @@ __global__ void __launch_bounds__(kDecThreads) k_decode(DecArgs a) {
 
   // ---- 1. gather the tokens ----
   if (kFromPackets) {
-    // warp 0 -> I row, warp 1 -> P row
-    const int wid = tid >> 5, lane = tid & 31;
-    if (wid < 2) {
-      const int mat = g * 2 + wid;
-      const uint32_t win = a.winner[(int64_t)mat * a.Ht + ty];
-      bool ok = win != 0xFFFFFFFFu;
-      const uint8_t* pkt = nullptr;
-      SstPacketInfo* p = nullptr;
-      if (ok) {
-        p = &a.info[win];
-        pkt = a.buf + a.off[win];
-        // shape contract of the fused path: W' tokens of 12 channels
-        bool bad = p->channels != kChannels || p->width < a.Wt;
-        for (int x = a.Wt + lane; !bad && x < p->width; x += 32)
-          if ((pkt[p->mask_off + (x >> 3)] >> (7 - (x & 7))) & 1) bad = true;
-        bad = __any_sync(0xffffffffu, bad);
-        if (bad) {
-          if (lane == 0) p->status = SST_PKT_SHAPE;
-          ok = false;
-        } else if (lane == 0 && blockIdx.x == 0) {
-          atomicAdd(&a.stats[2 * mat + 1], 1);          // rows_received
-        }
+    // every thread dequantises one (layer, token, channel) straight from the
+    // winning packet's payload (transport.py:195-199, 296-305)
+    for (int e = tid; e < 2 * kDecTok * kChannels; e += kDecThreads) {
+      const int im = e / (kDecTok * kChannels);
+      const int t = (e / kChannels) % kDecTok;
+      const int c = e % kChannels;
+      const int tx = tx0 + t;
+      const int64_t r = ((int64_t)g * 2 + im) * a.Ht + ty;
+      const int slot = tx < a.Wt ? a.tokoff[r * a.Wt + tx] : -1;
+      double v = 0.0;
+      if (slot >= 0) {
+        const RowInfo& ri = a.rows[r];
+        v = ri.qmin + (double)a.buf[ri.payload + (int64_t)slot * kChannels + c] * ri.step;
       }
-      // prefix count of valid tokens left of this CTA's first token
-      // (popcount of the whole mask bytes before it), spread over the lanes
-      const uint8_t* mb = ok ? pkt + p->mask_off : nullptr;
-      int pre0 = 0;
-      if (ok)
-        for (int b = lane; b < (tx0 >> 3); b += 32) pre0 += __popc((uint32_t)mb[b]);
-      pre0 = __reduce_add_sync(0xffffffffu, pre0);
-      // lane t < kDecTok owns token tx0 + t (kDecTok is a multiple of 8, so
-      // the tokens before tx0 are exactly the whole bytes counted above)
-      const int tx = tx0 + lane;
-      const bool v = ok && lane < kDecTok && tx < a.Wt && ((mb[tx >> 3] >> (7 - (tx & 7))) & 1);
-      const unsigned bal = __ballot_sync(0xffffffffu, v);
-      if (lane < kDecTok) {
-        double* dst = tok[wid][lane];
-        if (v) {
-          const int pre = pre0 + __popc(bal & ((1u << lane) - 1u));
-          const uint8_t* src = pkt + p->payload_off + pre * kChannels;
-          uint8_t raw[kChannels];
-#pragma unroll
-          for (int c = 0; c < kChannels; ++c) raw[c] = src[c];
-          const double qmin = p->dqmin;
-          const double step = p->dqrange / 255.0;    // transport.py:199
-#pragma unroll
-          for (int c = 0; c < kChannels; ++c) dst[c] = qmin + (double)raw[c] * step;
-        } else {
-#pragma unroll
-          for (int c = 0; c < kChannels; ++c) dst[c] = 0.0;
-        }
-        if (wid == 1) valid[lane] = v ? 1 : 0;
-      }
+      tok[im][t][c] = v;
+      if (im == 1 && c == 0) valid[t] = slot >= 0 ? 1 : 0;
     }
   } else {
     for (int e = tid; e < 2 * kDecTok * kChannels; e += kDecThreads) {
@@ -144,18 +164,18 @@ __global__ void __launch_bounds__(kDecThreads) k_decode(DecArgs a) {
     else { c[0] = v[1]; }
     dct3_8<true>(c, 1.0 / 16.0);
 #pragma unroll
-    for (int y = 0; y < 8; ++y) s1[im][t][ch][y][x] = c[y];
+    for (int y = 0; y < 8; ++y) s1[im][y][x][t * 3 + ch] = c[y];
   }
   __syncthreads();
 
   // ---- 3. IDCT along x per pixel row, clip, conceal ----
   for (int it = tid; it < kDecTok * 3 * 8; it += kDecThreads) {
-    int t = it / 24;
-    int ch = (it / 8) % 3;
-    int y = it % 8;
+    const int y = it / (kDecTok * 3);
+    const int tc = it % (kDecTok * 3);
+    const int t = tc / 3, ch = tc % 3;
     double ci[8], cp[8];
-    ci[0] = s1[0][t][ch][y][0]; ci[1] = s1[0][t][ch][y][1];
-    cp[0] = s1[1][t][ch][y][0]; cp[1] = s1[1][t][ch][y][1];
+    ci[0] = s1[0][y][0][tc]; ci[1] = s1[0][y][1][tc];
+    cp[0] = s1[1][y][0][tc]; cp[1] = s1[1][y][1][tc];
     const double z = zc[y];
 #pragma unroll
     for (int x = 2; x < 8; ++x) { ci[x] = z; cp[x] = z; }
@@ -228,21 +248,34 @@ extern "C" int sst_decode(const double* i_tok, const double* p_tok, int64_t tok_
   return SST_OK;
 }
 
+extern "C" int64_t sst_unpack_decode_workspace(int G, int Ht, int Wt) {
+  const int64_t rows = 2 * (int64_t)G * Ht;
+  return rows * (int64_t)sizeof(RowInfo) + rows * Wt * 4;
+}
+
 extern "C" int sst_unpack_decode(const uint8_t* buf, const int64_t* off, SstPacketInfo* info,
                                  const int32_t* target, int64_t n, int G, int Ht, int Wt, int h,
                                  int w, const uint32_t* exp_gop, uint32_t* winner, int32_t* stats,
-                                 float* out, void* stream) {
+                                 void* ws, float* out, void* stream) {
   if (n < 0 || G < 0 || Ht <= 0 || Wt <= 0 || h <= 0 || w <= 0) return SST_ERR_ARG;
   if (h > Ht * 8 || w > Wt * 8) return SST_ERR_ARG;
   if (G == 0) return SST_OK;
-  if (!exp_gop || !winner || !stats || !out) return SST_ERR_ARG;
+  if (!exp_gop || !winner || !stats || !out || !ws) return SST_ERR_ARG;
   if (n > 0 && (!buf || !off || !info || !target)) return SST_ERR_ARG;
   if (Ht > 65535 || G > 65535) return SST_ERR_ARG;
+  if (reinterpret_cast<uintptr_t>(ws) & 15) return SST_ERR_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   int rc = route_packets(info, target, n, 2 * G, Ht, nullptr, exp_gop, winner, stats, st);
   if (rc != SST_OK) return rc;
+  const int64_t nrows = 2 * (int64_t)G * Ht;
+  RowInfo* rows = static_cast<RowInfo*>(ws);
+  int32_t* tokoff = reinterpret_cast<int32_t*>(rows + nrows);
+  k_rowprep<<<(unsigned)ceil_div64(nrows, 8), 256, 0, st>>>(off, info, buf, winner, nrows, Ht, Wt,
+                                                            rows, tokoff, stats);
+  SST_LAUNCH_CHECK();
   DecArgs a{};
   a.buf = buf; a.off = off; a.info = info; a.winner = winner; a.stats = stats;
+  a.rows = rows; a.tokoff = tokoff;
   a.G = G; a.Ht = Ht; a.Wt = Wt; a.h = h; a.w = w; a.out = out;
   dim3 grid(ceil_div(Wt, kDecTok), Ht, G);
   k_decode<true><<<grid, kDecThreads, 0, st>>>(a);

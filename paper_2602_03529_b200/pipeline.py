@@ -109,6 +109,8 @@ class GopCodec:
         self.exp_gop = torch.zeros((G,), dtype=torch.int32, device=dev)
         self.winner = torch.empty((2 * G * self.Ht,), dtype=torch.int32, device=dev)
         self.stats = torch.empty((2 * G * 2,), dtype=i32, device=dev)
+        ws = _lib.load().sst_unpack_decode_workspace(G, self.Ht, self.Wt)
+        self.dec_ws = torch.empty((ws,), dtype=u8, device=dev)
         # double-buffered working images so the next step can still read the
         # previous GoP's P image for boundary blending
         self.img = [torch.empty((G, 2, self.h, self.w, 3), dtype=torch.float32, device=dev)
@@ -142,12 +144,21 @@ class GopCodec:
     # -- sender --------------------------------------------------------
     def encode(self, frames: torch.Tensor, g: int, drop_k: int = 0) -> None:
         """K1 + K2 + K3 for frames[:g] ([g, 9, H, W, 3] float32, contiguous)."""
-        st = _dev.stream()
+        self.tokenize(frames, g)
+        self.select_and_pack(g, drop_k)
+
+    def tokenize(self, frames: torch.Tensor, g: int) -> None:
+        """K1: downscale + tokenize + similarity."""
         tm = self.timer
         tm.begin("K1_encode")
         _lib.call("sst_encode", frames.data_ptr(), g, self.H, self.W, self.s,
-                  self.tok.data_ptr(), self.sim.data_ptr(), st)
+                  self.tok.data_ptr(), self.sim.data_ptr(), _dev.stream())
         tm.end("K1_encode")
+
+    def select_and_pack(self, g: int, drop_k: int = 0) -> None:
+        """K2 (intelligent drop) + K3 (quantise, packetise, CRC)."""
+        st = _dev.stream()
+        tm = self.timer
         self.mask[:g].fill_(1)
         if drop_k > 0:
             self.k[:g].fill_(drop_k)
@@ -182,7 +193,7 @@ class GopCodec:
         _lib.call("sst_unpack_decode", arena.data_ptr(), self.offsets.data_ptr(),
                   self.info.data_ptr(), self.target.data_ptr(), npk, g, self.Ht, self.Wt, self.h,
                   self.w, self.exp_gop.data_ptr(), self.winner.data_ptr(), self.stats.data_ptr(),
-                  img.data_ptr(), st)
+                  self.dec_ws.data_ptr(), img.data_ptr(), st)
         tm.end("K4_unpack_decode")
         return img[:g]
 
@@ -237,7 +248,7 @@ class StreamBank:
     the stream's previous reconstruction, at whatever scale it was coded."""
 
     def __init__(self, n_streams: int, H: int, W: int, scales=(2, 3), blend_n: int = 2,
-                 concurrent_groups: bool = True):
+                 concurrent_groups: bool = True, priority_middle: bool = True):
         if blend_n > 4:
             raise ValueError("the fused reconstruction blends at most 4 frames")
         self.n, self.H, self.W, self.blend_n = n_streams, H, W, blend_n
@@ -248,6 +259,11 @@ class StreamBank:
         # middle kernels of one group overlap the HBM-bound K1/K5 of the other
         self.group_streams = ({s: torch.cuda.Stream(device=_dev.device()) for s in scales}
                               if concurrent_groups else None)
+        # the latency-bound middle kernels (drop, packetise, parse, decode) run
+        # on a high-priority stream so their few CTAs are scheduled ahead of
+        # other lanes' HBM-streaming K1/K5 CTAs instead of queueing behind them
+        self.mid_stream = (torch.cuda.Stream(device=_dev.device(), priority=-10)
+                           if priority_middle else None)
         self.step_idx = 0
         self.launches = 0          # kernels of this library launched by step()
         # where each stream's last P image lives: (scale, parity, slot) or None
@@ -275,11 +291,18 @@ class StreamBank:
                 joined.append(gs)
             with torch.cuda.stream(gs):
                 codec.set_gop_ids(gop_ids_by_scale[s])
-                codec.encode(frames, g, codec.drop_k(drop_rate))
+                codec.tokenize(frames, g)
                 present = None if present_by_scale is None else present_by_scale.get(s)
-                codec.decode(g, parity, present=present)
-                # K1 + K2 (if dropping) + K3 + K4 parse + 4 (init/route/dups/decode) + K5
-                self.launches += 1 + (1 if codec.drop_k(drop_rate) > 0 else 0) + 1 + 1 + 4 + 1
+                mid = self.mid_stream if self.mid_stream is not None else gs
+                if mid is not gs:
+                    mid.wait_stream(gs)
+                with torch.cuda.stream(mid):
+                    codec.select_and_pack(g, codec.drop_k(drop_rate))
+                    codec.decode(g, parity, present=present)
+                if mid is not gs:
+                    gs.wait_stream(mid)
+                # K1 + K2 (if dropping) + K3 + K4 parse + 5 (init/route/dups/rowprep/decode) + K5
+                self.launches += 1 + (1 if codec.drop_k(drop_rate) > 0 else 0) + 1 + 1 + 5 + 1
                 staged = self._prev_descs(s, ids)
                 codec.reconstruct(g, parity, out_by_scale[s],
                                   None if staged is None else staged[0])
