@@ -174,24 +174,26 @@ __global__ void __launch_bounds__(kUpThreads) k_upscale_blend(const __grid_const
 // ---- fused upscale + blend, TMA-store variant (aligned widths) ----
 //
 // A CTA owns a band of kBand output rows x kTQ output floats of one GoP
-// (kTQ threads, one output float column each).  Each thread walks its column
-// down the band.  The bilinear filter is separable in the reference's own
-// operation order: the horizontal pass a*(1-fx) + b*fx (codec.py:233) depends
-// only on (source row, output column), so each thread keeps the passes of the
-// two source rows it currently needs in registers and, one source row ahead,
-// prefetches the raw samples of the next row (L1/L2 resident: the working
-// images are 1/s^2 of a frame), which hides their latency behind s output rows
-// of work.  The vertical pass top*(1-fy) + bot*fy (codec.py:235), clip, float32
-// and the boundary blend (codec.py:289-293) write at most n+1 distinct smem
-// tiles per 8-row chunk, which leave through one TMA bulk tensor store per
-// output frame (frames n..8 share the P tile); TMA clips the crop edges.  No
-// smem is spent on source windows, so 8 CTAs (64 warps) fit per SM.
+// (kTQ threads, one output float column each).
+//   setup:  row taps of the band, the band's source windows (I, P, previous
+//           P; float32) copied to smem with one batch of coalesced loads;
+//   compute: each thread walks its column down the band: the horizontal pass
+//           a*(1-fx) + b*fx (codec.py:233) once per source row, cached in
+//           registers; the vertical pass top*(1-fy) + bot*fy (codec.py:235)
+//           per output row; clip, float32, blend (codec.py:289-293);
+//   store:  every kTR rows the n+1 distinct tiles (blended frames 0..n-1, P)
+//           leave through one TMA bulk tensor store per output frame (frames
+//           n..8 share the P tile); TMA clips the crop edges.
 constexpr int kTR = 8;                     // output rows per stored tile
 constexpr int kBand = 32;                  // output rows per CTA
 constexpr int kTQ = 256;                   // output floats per tile row (= threads)
+constexpr int kWR = kBand / 2 + 2;         // max source rows per band (s >= 2)
+constexpr int kWF = (kTQ / 6 + 3) * 3 + 3; // max source floats per window row (s >= 2)
 
 struct UpTmaSmem {
+  float win[3][kWR][kWF];                  // I, P, previous P windows
   AxisTap ty_c[kBand], ty_p[kBand];
+  int wx0[2], wx1[2];                      // window column range (source px) cur / prev
 };
 typedef float UpTile[kTR][kTQ];
 constexpr int kTileOff = (int)((sizeof(UpTmaSmem) + 127) / 128 * 128);   // TMA needs 128-B
@@ -200,55 +202,18 @@ __host__ __device__ constexpr int up_tma_smem(int ntiles) {
   return kTileOff + ntiles * (int)sizeof(UpTile);
 }
 
-// Horizontal-pass walker over the source rows of one image (or an I/P pair
-// sharing geometry): h0/h1 = passes at rows lo and min(lo+1, h-1); raw = the
-// prefetched taps of row min(lo+2, h-1).
-template <int NI>
-struct RowWalker {
-  const float* img[NI];
-  int64_t xl, xh;        // element offsets of the two horizontal taps within a row
-  int64_t rowstride;     // w*3
-  int hmax;              // h - 1
-  double fx, gx;
-  int lo;
-  double h0[NI], h1[NI];
-  float pa[NI], pb[NI];
-
-  __device__ __forceinline__ void fetch(int y, float* a, float* b) const {
-    const int64_t r = (int64_t)y * rowstride;
+__device__ __forceinline__ void load_window(float* win, const float* img, int w, int r0, int r1,
+                                           int c0f, int c1f, int tid) {
+  const int ncol = c1f - c0f;
+  const int lane = tid & 31, wid = tid >> 5;
+  for (int j = wid; j <= r1 - r0; j += kTQ / 32) {
+    const float* src = img + ((int64_t)(r0 + j) * w) * 3 + c0f;
+    float* dst = win + j * kWF;
 #pragma unroll
-    for (int i = 0; i < NI; ++i) {
-      a[i] = __ldg(img[i] + r + xl);
-      b[i] = __ldg(img[i] + r + xh);
-    }
+    for (int c = lane; c < kWF; c += 32)
+      if (c < ncol) dst[c] = __ldg(src + c);
   }
-  __device__ __forceinline__ double hp(float a, float b) const {
-    return (double)a * gx + (double)b * fx;                       // codec.py:233
-  }
-  __device__ __forceinline__ void start(int y) {
-    lo = y;
-    float a0[NI], b0[NI], a1[NI], b1[NI];
-    fetch(y, a0, b0);
-    fetch(min(y + 1, hmax), a1, b1);
-    fetch(min(y + 2, hmax), pa, pb);
-#pragma unroll
-    for (int i = 0; i < NI; ++i) {
-      h0[i] = hp(a0[i], b0[i]);
-      h1[i] = hp(a1[i], b1[i]);
-    }
-  }
-  // advance to row y (y == lo or lo + 1)
-  __device__ __forceinline__ void advance(int y) {
-    if (y == lo) return;
-    lo = y;
-#pragma unroll
-    for (int i = 0; i < NI; ++i) {
-      h0[i] = h1[i];
-      h1[i] = hp(pa[i], pb[i]);
-    }
-    fetch(min(y + 2, hmax), pa, pb);
-  }
-};
+}
 
 template <bool kPrev, int kN>
 __global__ void __launch_bounds__(kTQ)
@@ -266,41 +231,47 @@ __global__ void __launch_bounds__(kTQ)
   if (kPrev) pd = a.prev[g];
   const bool has_prev = kPrev && pd.p_img != nullptr;
   const int rows = min(kBand, a.H - oy0);
+  const int qlast = min(q0 + kTQ, a.W * 3) - 1;
   if (tid < kBand) S.ty_c[tid] = axis_tap(oy0 + min(tid, rows - 1), a.h, a.s);
-  else if (tid < 2 * kBand && has_prev)
-    S.ty_p[tid - kBand] = axis_tap(oy0 + min(tid - kBand, rows - 1), pd.h, pd.s);
+  else if (tid < 2 * kBand) {
+    if (has_prev) S.ty_p[tid - kBand] = axis_tap(oy0 + min(tid - kBand, rows - 1), pd.h, pd.s);
+  } else if (tid == 2 * kBand) {
+    S.wx0[0] = axis_tap(q0 / 3, a.w, a.s).lo;
+    S.wx1[0] = axis_tap(qlast / 3, a.w, a.s).hi;
+  } else if (tid == 2 * kBand + 32 && has_prev) {
+    S.wx0[1] = axis_tap(q0 / 3, pd.w, pd.s).lo;
+    S.wx1[1] = axis_tap(qlast / 3, pd.w, pd.s).hi;
+  }
+  __syncthreads();
+
+  const float* iimg = a.img + (int64_t)g * 2 * a.h * a.w * 3;
+  const float* pimg = iimg + (int64_t)a.h * a.w * 3;
+  const int r0 = S.ty_c[0].lo;
+  const int pr0 = has_prev ? S.ty_p[0].lo : 0;
+  {
+    const int r1 = S.ty_c[rows - 1].hi;
+    load_window(&S.win[0][0][0], iimg, a.w, r0, r1, S.wx0[0] * 3, S.wx1[0] * 3 + 3, tid);
+    load_window(&S.win[1][0][0], pimg, a.w, r0, r1, S.wx0[0] * 3, S.wx1[0] * 3 + 3, tid);
+    if (has_prev)
+      load_window(&S.win[2][0][0], pd.p_img, pd.w, pr0, S.ty_p[rows - 1].hi, S.wx0[1] * 3,
+                  S.wx1[1] * 3 + 3, tid);
+  }
   __syncthreads();
 
   const int q = min(q0 + tid, a.W * 3 - 1);       // columns past the crop are clipped by TMA
   const int ox = q / 3, ch = q - ox * 3;
   const int nb = has_prev ? kN : 1;                // tiles 0..nb-1: frames 0..nb-1; tile nb: P
-
-  RowWalker<2> cw;
-  cw.img[0] = a.img + (int64_t)g * 2 * a.h * a.w * 3;
-  cw.img[1] = cw.img[0] + (int64_t)a.h * a.w * 3;
-  {
-    const AxisTap tx = axis_tap(ox, a.w, a.s);
-    cw.xl = (int64_t)tx.lo * 3 + ch;
-    cw.xh = (int64_t)tx.hi * 3 + ch;
-    cw.fx = tx.f;
-    cw.gx = tx.g;
-  }
-  cw.rowstride = (int64_t)a.w * 3;
-  cw.hmax = a.h - 1;
-  cw.start(S.ty_c[0].lo);
-  RowWalker<1> pw;
+  const AxisTap tx = axis_tap(ox, a.w, a.s);
+  const int xl = (tx.lo - S.wx0[0]) * 3 + ch, xh = (tx.hi - S.wx0[0]) * 3 + ch;
+  AxisTap txp = tx;
+  int pxl = 0, pxh = 0;
   if (has_prev) {
-    pw.img[0] = pd.p_img;
-    const AxisTap tx = axis_tap(ox, pd.w, pd.s);
-    pw.xl = (int64_t)tx.lo * 3 + ch;
-    pw.xh = (int64_t)tx.hi * 3 + ch;
-    pw.fx = tx.f;
-    pw.gx = tx.g;
-    pw.rowstride = (int64_t)pd.w * 3;
-    pw.hmax = pd.h - 1;
-    pw.start(S.ty_p[0].lo);
+    txp = axis_tap(ox, pd.w, pd.s);
+    pxl = (txp.lo - S.wx0[1]) * 3 + ch;
+    pxh = (txp.hi - S.wx0[1]) * 3 + ch;
   }
-
+  int ya = -1, yb = -1, qa = -1, qb = -1;
+  double ia = 0, pa = 0, ib = 0, pb = 0, qva = 0, qvb = 0;   // horizontal taps at cached rows
   const int z0 = g * kGop;
   for (int c0 = 0; c0 < rows; c0 += kTR) {
     if (c0 > 0) {                                  // tiles free again once TMA has read them
@@ -310,15 +281,49 @@ __global__ void __launch_bounds__(kTQ)
     const int cend = min(c0 + kTR, rows);
     for (int r = c0; r < cend; ++r) {
       const AxisTap ty = S.ty_c[r];
-      cw.advance(ty.lo);
-      const float ui = (float)clip_hi1(cw.h0[0] * ty.g + cw.h1[0] * ty.f);   // codec.py:235
-      const float up = (float)clip_hi1(cw.h0[1] * ty.g + cw.h1[1] * ty.f);
+      if (ty.lo != ya) {
+        if (ty.lo == yb) { ia = ib; pa = pb; }
+        else {
+          const float* wi = &S.win[0][ty.lo - r0][0];
+          const float* wp = &S.win[1][ty.lo - r0][0];
+          ia = (double)wi[xl] * tx.g + (double)wi[xh] * tx.f;
+          pa = (double)wp[xl] * tx.g + (double)wp[xh] * tx.f;
+        }
+        ya = ty.lo;
+      }
+      if (ty.hi != yb) {
+        if (ty.hi == ya) { ib = ia; pb = pa; }
+        else {
+          const float* wi = &S.win[0][ty.hi - r0][0];
+          const float* wp = &S.win[1][ty.hi - r0][0];
+          ib = (double)wi[xl] * tx.g + (double)wi[xh] * tx.f;
+          pb = (double)wp[xl] * tx.g + (double)wp[xh] * tx.f;
+        }
+        yb = ty.hi;
+      }
+      const float ui = (float)clip_hi1(ia * ty.g + ib * ty.f);
+      const float up = (float)clip_hi1(pa * ty.g + pb * ty.f);
       const int rr = r - c0;
       tile[nb][rr][tid] = up;
       if (has_prev) {
         const AxisTap tp = S.ty_p[r];
-        pw.advance(tp.lo);
-        const double dq = (double)(float)clip_hi1(pw.h0[0] * tp.g + pw.h1[0] * tp.f);
+        if (tp.lo != qa) {
+          if (tp.lo == qb) qva = qvb;
+          else {
+            const float* wq = &S.win[2][tp.lo - pr0][0];
+            qva = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
+          }
+          qa = tp.lo;
+        }
+        if (tp.hi != qb) {
+          if (tp.hi == qa) qvb = qva;
+          else {
+            const float* wq = &S.win[2][tp.hi - pr0][0];
+            qvb = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
+          }
+          qb = tp.hi;
+        }
+        const double dq = (double)(float)clip_hi1(qva * tp.g + qvb * tp.f);
         tile[0][rr][tid] = (float)clip_hi1(a.alpha[0] * dq + a.beta[0] * (double)ui);
         const double dp = (double)up;
 #pragma unroll
