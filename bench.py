@@ -413,26 +413,25 @@ def run_e2e(a, rank, world, local_rank) -> dict:
     lanes = max(1, min(4, E))
     per = [list(range(E))[i::lanes] for i in range(lanes)]
     src_dev = make_inputs([rank * E + i for i in range(E)], H, W, dev, n_sets=1)[0]
-    host_in = torch.empty(src_dev.shape, dtype=torch.float32, pin_memory=True)
-    host_in.copy_(src_dev)
-    host_out = torch.empty_like(host_in, pin_memory=True)
-    del src_dev
-    torch.cuda.empty_cache()
+    fshape = tuple(src_dev.shape[1:])
     L = []
     for ids in per:
         g = len(ids)
         bank = StreamBank(g, H, W)
-        idx = torch.tensor(ids)
+        # pinned host frames of this lane's streams (one copy per lane only)
+        h_in = torch.empty((g,) + fshape, dtype=torch.float32, pin_memory=True)
+        h_in.copy_(src_dev[torch.tensor(ids, device=dev)])
         L.append(dict(
             ids=ids, bank=bank, stream=torch.cuda.Stream(device=dev),
-            h_in=host_in[idx].pin_memory(), h_out=torch.empty((g,) + tuple(host_in.shape[1:]),
-                                                             dtype=torch.float32).pin_memory(),
-            d_in=torch.empty((g,) + tuple(host_in.shape[1:]), dtype=torch.float32, device=dev),
-            d_out=torch.empty((g,) + tuple(host_in.shape[1:]), dtype=torch.float32, device=dev),
+            h_in=h_in, h_out=torch.empty((g,) + fshape, dtype=torch.float32, pin_memory=True),
+            d_in=torch.empty((g,) + fshape, dtype=torch.float32, device=dev),
+            d_out=torch.empty((g,) + fshape, dtype=torch.float32, device=dev),
             pk={s: torch.empty(c.arena.shape, dtype=torch.uint8).pin_memory()
                 for s, c in bank.codecs.items()},
             ln={s: torch.empty(c.lengths.shape, dtype=torch.int32).pin_memory()
                 for s, c in bank.codecs.items()}))
+    del src_dev
+    torch.cuda.empty_cache()
     counters = {"h2d": 0, "d2h": 0}
 
     def one(k):

@@ -185,21 +185,25 @@ __global__ void __launch_bounds__(kUpThreads) k_upscale_blend(const __grid_const
 //           leave through one TMA bulk tensor store per output frame (frames
 //           n..8 share the P tile); TMA clips the crop edges.
 constexpr int kTR = 8;                     // output rows per stored tile
-constexpr int kBand = 32;                  // output rows per CTA
 constexpr int kTQ = 256;                   // output floats per tile row (= threads)
-constexpr int kWR = kBand / 2 + 2;         // max source rows per band (s >= 2)
 constexpr int kWF = (kTQ / 6 + 3) * 3 + 3; // max source floats per window row (s >= 2)
 
+template <int BAND>
 struct UpTmaSmem {
+  static constexpr int kWR = BAND / 2 + 2;   // max source rows per band (s >= 2)
   float win[3][kWR][kWF];                  // I, P, previous P windows
-  AxisTap ty_c[kBand], ty_p[kBand];
+  AxisTap ty_c[BAND], ty_p[BAND];
   int wx0[2], wx1[2];                      // window column range (source px) cur / prev
 };
 typedef float UpTile[kTR][kTQ];
-constexpr int kTileOff = (int)((sizeof(UpTmaSmem) + 127) / 128 * 128);   // TMA needs 128-B
-// dynamic smem when `ntiles` output tiles are used (n blended frames + P)
+template <int BAND>
+__host__ __device__ constexpr int tile_off() {
+  return (int)((sizeof(UpTmaSmem<BAND>) + 127) / 128 * 128);
+}
+// dynamic smem: windows + NBUF sets of `ntiles` output tiles (n blended + P)
+template <int BAND, int NBUF>
 __host__ __device__ constexpr int up_tma_smem(int ntiles) {
-  return kTileOff + ntiles * (int)sizeof(UpTile);
+  return tile_off<BAND>() + NBUF * ntiles * (int)sizeof(UpTile);
 }
 
 __device__ __forceinline__ void load_window(float* win, const float* img, int w, int r0, int r1,
@@ -215,12 +219,12 @@ __device__ __forceinline__ void load_window(float* win, const float* img, int w,
   }
 }
 
-template <bool kPrev, int kN>
+template <int kBand, int NBUF, bool kPrev, int kN>
 __global__ void __launch_bounds__(kTQ)
     k_upscale_blend_tma(const __grid_constant__ CUtensorMap omap, const __grid_constant__ UpArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  UpTmaSmem& S = *reinterpret_cast<UpTmaSmem*>(smem_raw);
-  UpTile* tile = reinterpret_cast<UpTile*>(smem_raw + kTileOff);
+  UpTmaSmem<kBand>& S = *reinterpret_cast<UpTmaSmem<kBand>*>(smem_raw);
+  UpTile* tiles = reinterpret_cast<UpTile*>(smem_raw + tile_off<kBand>());
   const int tid = threadIdx.x;
   const int q0 = blockIdx.x * kTQ;
   const int oy0 = blockIdx.y * kBand;
@@ -273,9 +277,15 @@ __global__ void __launch_bounds__(kTQ)
   int ya = -1, yb = -1, qa = -1, qb = -1;
   double ia = 0, pa = 0, ib = 0, pb = 0, qva = 0, qvb = 0;   // horizontal taps at cached rows
   const int z0 = g * kGop;
-  for (int c0 = 0; c0 < rows; c0 += kTR) {
-    if (c0 > 0) {                                  // tiles free again once TMA has read them
-      if (tid == 0) tma_store_wait_read();
+  for (int c0 = 0, ci = 0; c0 < rows; c0 += kTR, ++ci) {
+    // NBUF tile sets rotate; a set is reused once the TMA store issued NBUF
+    // chunks ago has finished reading it
+    UpTile* tile = tiles + (ci % NBUF) * (nb + 1);
+    if (ci >= NBUF) {
+      if (tid == 0) {
+        if (NBUF == 1) tma_store_wait_read();
+        else tma_store_wait_read_1();
+      }
       __syncthreads();
     }
     const int cend = min(c0 + kTR, rows);
@@ -410,6 +420,27 @@ __global__ void __launch_bounds__(kMseThreads)
 
 using namespace sst;
 
+template <int BAND, int NBUF>
+static int launch_k5(const CUtensorMap& omap, const UpArgs& a, const SstPrevDesc* prev,
+                     int blend_n, cudaStream_t st) {
+  dim3 grid(ceil_div(a.W * 3, kTQ), ceil_div(a.H, BAND), a.G);
+  if (grid.y > 65535) return SST_ERR_ARG;
+  const int smem = up_tma_smem<BAND, NBUF>((prev ? blend_n : 1) + 1);
+  auto kern = k_upscale_blend_tma<BAND, NBUF, false, 1>;
+  if (prev) {
+    switch (blend_n) {
+      case 1: kern = k_upscale_blend_tma<BAND, NBUF, true, 1>; break;
+      case 2: kern = k_upscale_blend_tma<BAND, NBUF, true, 2>; break;
+      case 3: kern = k_upscale_blend_tma<BAND, NBUF, true, 3>; break;
+      default: kern = k_upscale_blend_tma<BAND, NBUF, true, 4>; break;
+    }
+  }
+  SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<grid, kTQ, smem, st>>>(omap, a);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
 extern "C" int sst_upscale_blend(const float* img, int G, int h, int w, int s, int H, int W,
                                  const SstPrevDesc* prev, int blend_n, float* out, void* stream) {
   if (G < 0 || h <= 0 || w <= 0 || H <= 0 || W <= 0) return SST_ERR_ARG;
@@ -434,22 +465,14 @@ extern "C" int sst_upscale_blend(const float* img, int G, int h, int w, int s, i
   const bool want_tma = !(var && var[0] == '2');
   if (want_tma &&
       make_tmap_f32_3d(&omap, out, (uint64_t)W * 3, (uint64_t)H, (uint64_t)G * kGop, kTQ, kTR)) {
-    dim3 grid(ceil_div(W * 3, kTQ), ceil_div(H, kBand), G);
-    if (grid.y > 65535) return SST_ERR_ARG;
-    const int smem = up_tma_smem((prev ? blend_n : 1) + 1);
-    auto kern = k_upscale_blend_tma<false, 1>;
-    if (prev) {
-      switch (blend_n) {
-        case 1: kern = k_upscale_blend_tma<true, 1>; break;
-        case 2: kern = k_upscale_blend_tma<true, 2>; break;
-        case 3: kern = k_upscale_blend_tma<true, 3>; break;
-        default: kern = k_upscale_blend_tma<true, 4>; break;
-      }
-    }
-    SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    kern<<<grid, kTQ, smem, st>>>(omap, a);
-    SST_LAUNCH_CHECK();
-    return SST_OK;
+    const char* eb = getenv("SST_K5_BAND");       // A/B switches for profiling
+    const char* en = getenv("SST_K5_NBUF");
+    const int band = (eb && atoi(eb) == 16) ? 16 : 32;
+    const int nbuf = (en && atoi(en) == 1) ? 1 : 2;
+    return band == 16 ? (nbuf == 1 ? launch_k5<16, 1>(omap, a, prev, blend_n, st)
+                                   : launch_k5<16, 2>(omap, a, prev, blend_n, st))
+                      : (nbuf == 1 ? launch_k5<32, 1>(omap, a, prev, blend_n, st)
+                                   : launch_k5<32, 2>(omap, a, prev, blend_n, st));
   }
   dim3 grid(ceil_div(W * 3, kUpThreads), ceil_div(H, kUpRows), G);
   if (grid.y > 65535) return SST_ERR_ARG;

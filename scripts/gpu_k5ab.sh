@@ -1,10 +1,7 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests -m gpu -x -q 2>&1 | tail -2
-B="python bench.py --steps 20 --warmup 3 --streams 64 --no-cpu-baseline --no-e2e"
-SST_K5_VARIANT=2 timeout 600 $B 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('v2', d['value'], d['stages'], d['roofline']['frac'])"
-timeout 600 $B 2>&1 | tail -1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('v3d', d['value'], d['stages'], d['roofline']['frac'])"
-for k in k_upscale_blend_tma k_decode; do
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 2 -c 1 \
-      -o gpurun_out/prof2_$k python bench.py --steps 2 --warmup 1 --streams 16 --no-e2e --no-cpu-baseline > /dev/null 2>&1
-echo "ncu $k rc=$?"
+timeout 900 python -m pytest tests/test_gpu_pipeline.py tests/test_gpu_golden.py -x -q 2>&1 | tail -2
+for cfg in "32 1" "32 2" "16 1" "16 2"; do
+set -- $cfg
+SST_K5_BAND=$1 SST_K5_NBUF=$2 timeout 600 python bench.py --no-cpu-baseline --no-e2e 2>&1 | tail -1 > gpurun_out/bench_ab.json
+python -c "import json; d=json.load(open('gpurun_out/bench_ab.json')); print('band $1 nbuf $2', d['value'], d['stages']['K5_upscale_blend'], d['roofline']['frac'], d['path_roofline']['frac'])"
 done
