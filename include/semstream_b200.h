@@ -274,6 +274,57 @@ SST_API int sst_rc_decode_symbols(const uint8_t* data, int64_t nbytes, int64_t m
                                   int64_t cap, int32_t* syms, int64_t* nsym, int32_t* status,
                                   void* stream);
 
+/* ---- learned tokenizer plug-in ----------------------
+ * A causal spatio-temporal conv tokenizer with finite-scalar quantisation
+ * (FSQ), plugged in at the reference's tokenizer hook
+ * SessionConfig.tokenizer_encode / tokenizer_decode (session.py:57-61,
+ * contract SPEC.md:165).  The reference ships no learned model,
+ * so these entry points have no reference function to match: parity is
+ * against the torch fp32 restatement in oracle/learned_oracle.py (unpinned).
+ * Activations are bf16 channels-last [G][T][H'][W'][C]; the convolutions run
+ * as tcgen05 implicit GEMMs (bf16 x bf16 -> fp32 in TMEM), operands by TMA. */
+
+#define SST_LT_EPI_STORE 0   /* bf16 activation tensor (+bias, SiLU, +residual) */
+#define SST_LT_EPI_FSQ 1     /* FSQ head: codes f64 [G][2][H'][W'][12], idx i32 [..][2], mask u8 */
+#define SST_LT_EPI_PIXELS 2  /* unpatchify: frames f32 [G][9][h][w][3], clamp [0,1] */
+
+typedef struct SstConvDesc {
+  const void* in;          /* bf16 [G][in_T][in_H][in_W][in_C], in_C % 64 == 0 */
+  int32_t in_C, in_W, in_H, in_T;
+  int32_t G, Ht, Wt;       /* output token grid per latent frame */
+  int32_t t_lo, t_cnt;     /* output latent frames t_lo .. t_lo+t_cnt-1 */
+  int32_t n_taps;          /* <= 27 */
+  int32_t taps[27][3];     /* (dt, dy, dx) input offsets per tap; K order = tap-major, channel-minor */
+  const void* weight;      /* bf16 [N][K], K = n_taps * in_C */
+  int32_t N, K;
+  const float* bias;       /* fp32 [N] */
+  int32_t epi, act;        /* SST_LT_EPI_*; act 1 = SiLU (STORE only) */
+  const void* residual;    /* STORE: bf16, same layout as out, or NULL */
+  void* out;               /* STORE: bf16 [G][out_T][Ht][Wt][N] */
+  int32_t out_T;
+  double* codes;           /* FSQ */
+  int32_t* idx;
+  uint8_t* mask;
+  float* frames;           /* PIXELS: frame f = frame_base + N-tile index (192 columns per frame) */
+  int32_t h, w, frame_base;
+} SstConvDesc;
+
+/* One convolution layer (implicit GEMM on tcgen05). */
+SST_API int sst_lt_conv(const SstConvDesc* d, void* stream);
+
+/* Box downscale (codec.py:202-214, bit-exact) + edge pad to 8 (codec.py:99-105)
+ * + 8x8 patchify to bf16: pI [G][H'][W'][192] (frame 0), pP [G][H'][W'][1536]
+ * (frames 1..8), K order (frame, py, px, colour).  s in {1, 2, 3}. */
+SST_API int sst_lt_patchify(const float* frames, int G, int H, int W, int s, void* pI, void* pP,
+                            void* stream);
+
+/* Mask-aware decoder input: snap the received codes (tokens f64
+ * [G][2][H'][W'][12], e.g. reassemble output) to the FSQ grid, conceal masked
+ * P tokens with the co-located I token (codec.py:176-180 semantics in latent
+ * space) and write bf16 [G][2][H'][W'][64] (channels 12..63 zero). */
+SST_API int sst_lt_dec_in(const double* tok, const uint8_t* mask, int G, int Ht, int Wt, void* out,
+                          void* stream);
+
 /* ---- metrics ------------------------------------------------------------ */
 
 /* mse (video.py:265-270) per frame pair: out[i] = mean((a-b)^2) in float64. */

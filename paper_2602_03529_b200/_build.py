@@ -21,7 +21,11 @@ BUILD = PKG.parent / "build" / "csrc"
 LIB = PKG / "libsemstream_b200.so"
 
 SOURCES = ["capi.cu", "tma_host.cu", "encode.cu", "select.cu", "packet.cu", "decode.cu",
-           "upscale.cu", "residual.cu"]
+           "upscale.cu", "residual.cu", "learned.cu"]
+
+# the learned-tokenizer kernels are bf16/fp32 tensor-core math with no
+# bit-exact contract: let them contract a*b+c into FMA
+FMAD_OK = {"learned.cu"}
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -53,7 +57,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         src = CSRC / name
         obj = BUILD / (name[:-3] + ".o")
         if force or _stale(obj, src):
-            jobs.append([exe, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)])
+            flags = [f for f in NVCC_FLAGS if not (name in FMAD_OK and f == "-fmad=false")]
+            jobs.append([exe, *flags, "-c", str(src), "-o", str(obj)])
 
     def run(cmd):
         r = subprocess.run(cmd, capture_output=True, text=True)

@@ -38,6 +38,21 @@ class SstPrevDesc(C.Structure):
                 ("reserved", C.c_int32)]
 
 
+class SstConvDesc(C.Structure):
+    """include/semstream_b200.h SstConvDesc (learned tokenizer, one conv layer)."""
+    _fields_ = [("in_", C.c_void_p), ("in_C", C.c_int32), ("in_W", C.c_int32),
+                ("in_H", C.c_int32), ("in_T", C.c_int32), ("G", C.c_int32), ("Ht", C.c_int32),
+                ("Wt", C.c_int32), ("t_lo", C.c_int32), ("t_cnt", C.c_int32),
+                ("n_taps", C.c_int32), ("taps", (C.c_int32 * 3) * 27), ("weight", C.c_void_p),
+                ("N", C.c_int32), ("K", C.c_int32), ("bias", C.c_void_p), ("epi", C.c_int32),
+                ("act", C.c_int32), ("residual", C.c_void_p), ("out", C.c_void_p),
+                ("out_T", C.c_int32), ("codes", C.c_void_p), ("idx", C.c_void_p),
+                ("mask", C.c_void_p), ("frames", C.c_void_p), ("h", C.c_int32),
+                ("w", C.c_int32), ("frame_base", C.c_int32)]
+
+
+LT_EPI_STORE, LT_EPI_FSQ, LT_EPI_PIXELS = 0, 1, 2
+
 INFO_BYTES = C.sizeof(SstPacketInfo)          # 64
 PREV_BYTES = C.sizeof(SstPrevDesc)            # 24
 
@@ -68,6 +83,9 @@ SIGNATURES = {
     "sst_unpack_decode": (_I, [_P, _P, _P, _P, _L, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     "sst_upscale_blend": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P]),
     "sst_mse": (_I, [_P, _P, _L, _L, _P, _P]),
+    "sst_lt_conv": (_I, [C.POINTER(SstConvDesc), _P]),
+    "sst_lt_patchify": (_I, [_P, _I, _I, _I, _I, _P, _P, _P]),
+    "sst_lt_dec_in": (_I, [_P, _P, _I, _I, _I, _P, _P]),
     "sst_residual": (_I, [_P, _P, _I, _I, _I, C.c_double, C.c_double, _P, _P, _P, _P, _P]),
     "sst_mean_axis0": (_I, [_P, _I, _L, _P, _P]),
     "sst_sparsify": (_I, [_P, _I, _L, C.c_double, C.c_double, _P, _P, _P, _P]),

@@ -1,0 +1,449 @@
+// Learned-tokenizer plug-in kernels: a causal
+// spatio-temporal convolutional tokenizer with finite-scalar quantisation,
+// plugged in at the reference's tokenizer hook (session.py:57-61).
+//
+//   k_lt_patchify  box downscale (bit-exact, codec.py:202-214) + edge pad to
+//                  the 8x8 grid (codec.py:99-105) + 8x8(x8) patchify -> bf16
+//   k_lt_conv      implicit-GEMM convolution on the 5th-gen tensor cores:
+//                  one CTA computes a 128-token x BN-channel tile.  Warp 0
+//                  (one lane) streams A (the im2col view of the activation,
+//                  fetched per tap by 5-D TMA with zero-filled halo) and B
+//                  (weights) into a 4-stage 128B-swizzled smem ring; warp 1
+//                  (one lane) issues tcgen05.mma (M=128, N=BN, K=16) into a
+//                  TMEM accumulator; then all four warps drain TMEM with
+//                  tcgen05.ld and run the fused epilogue:
+//                    STORE   +bias, SiLU, +residual -> bf16 -> TMA store
+//                    FSQ     +bias, FSQ bound/round, codes f64 + indices
+//                    PIXELS  +bias, clamp, depth-to-space f32 frame stores
+//   k_lt_dec_in    mask-aware decoder input (snap to the FSQ grid, conceal
+//                  masked P tokens with the co-located I token)
+//
+// The reference ships no learned model, so there is nothing to
+// match bit-for-bit; oracle/learned_oracle.py restates the same network in
+// torch fp32 with the same bf16 rounding points (parity unpinned).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstring>
+
+#include "common.cuh"
+#include "tc.cuh"
+
+namespace sst {
+namespace lt {
+
+constexpr int BM = 128;            // tokens per tile (16 x 8 spatial box)
+constexpr int BOX_X = 16, BOX_Y = 8;
+constexpr int BK = 64;             // bf16 per 128-byte swizzled row
+constexpr int A_BYTES = BM * BK * 2;
+constexpr int STAGES = 4;
+constexpr int FSQ_C = 12;          // 2 groups x levels (8,8,8,5,5,5)
+constexpr int DEC_IN_C = 64;
+
+__device__ __forceinline__ int fsq_levels(int i) { return (i % 6) < 3 ? 8 : 5; }
+__device__ __forceinline__ int fsq_basis(int i) {
+  // mixed radix inside one 6-dim group: 1, 8, 64, 512, 2560, 12800
+  const int j = i % 6;
+  return j == 0 ? 1 : j == 1 ? 8 : j == 2 ? 64 : j == 3 ? 512 : j == 4 ? 2560 : 12800;
+}
+
+struct ConvArgs {
+  int Ht, Wt, tiles_x, tiles_y, t_lo, t_cnt;
+  int n_taps, kb_per_tap, N, out_T;
+  signed char taps[27][3];
+  const float* bias;
+  int act;
+  const __nv_bfloat16* residual;
+  double* codes;
+  int32_t* idx;
+  uint8_t* mask;
+  float* frames;
+  int h, w, frame_base;
+};
+
+__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+
+template <int BN>
+struct TileCfg {
+  static constexpr int B_BYTES = BN * 128;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(128, 1)
+    k_lt_conv(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmC, const ConvArgs a) {
+  using Cfg = TileCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * Cfg::B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* accum = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+  const int warp = threadIdx.x >> 5;
+  int tile = blockIdx.x;
+  const int tx = tile % a.tiles_x; tile /= a.tiles_x;
+  const int ty = tile % a.tiles_y; tile /= a.tiles_y;
+  const int t = a.t_lo + tile % a.t_cnt;
+  const int g = tile / a.t_cnt;
+  const int x0 = tx * BOX_X, y0 = ty * BOX_Y;
+  const int n0 = blockIdx.y * BN;
+
+  if (threadIdx.x == 0) {
+    tc::prefetch_tmap(&tmA);
+    tc::prefetch_tmap(&tmB);
+    if (EPI == SST_LT_EPI_STORE) tc::prefetch_tmap(&tmC);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accum, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, Cfg::TMEM_COLS);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  const int nkb = a.n_taps * a.kb_per_tap;
+  if (threadIdx.x == 0) {
+    // ---- TMA producer ----
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % STAGES;
+      if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) - 1) & 1);
+      const int tap = kb / a.kb_per_tap, cb = kb - tap * a.kb_per_tap;
+      mbar_expect_tx(&full[s], Cfg::STAGE_BYTES);
+      tc::tma_load_5d(sA + s * A_BYTES, &tmA, cb * BK, x0 + a.taps[tap][2], y0 + a.taps[tap][1],
+                      t + a.taps[tap][0], g, &full[s]);
+      tc::tma_load_2d(sB + s * Cfg::B_BYTES, &tmB, kb * BK, n0, &full[s]);
+    }
+  } else if (threadIdx.x == 32) {
+    // ---- MMA issuer ----
+    constexpr uint32_t idesc = tc::idesc_bf16_f32(BM, BN);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % STAGES;
+      mbar_wait(&full[s], (kb / STAGES) & 1);
+      tc::fence_after_sync();
+      const uint64_t ad = tc::smem_desc_sw128(smem_u32(sA + s * A_BYTES));
+      const uint64_t bd = tc::smem_desc_sw128(smem_u32(sB + s * Cfg::B_BYTES));
+#pragma unroll
+      for (int k = 0; k < BK / 16; ++k)  // +32 B along K inside the swizzle atom
+        tc::mma_bf16(tmem, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+      tc::mma_commit(&empty[s]);
+    }
+    tc::mma_commit(accum);
+  }
+  __syncwarp();
+  mbar_wait(accum, 0);
+  tc::fence_after_sync();
+
+  // ---- epilogue: thread r owns accumulator row r (TMEM lane r) ----
+  const int r = threadIdx.x;
+  const int y = y0 + (r >> 4), x = x0 + (r & 15);
+  const bool valid = y < a.Ht && x < a.Wt;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+
+  if constexpr (EPI == SST_LT_EPI_STORE) {
+    uint8_t* stage = sA;  // all loads consumed: reuse the A ring as the store tile
+    const size_t tok = (((size_t)g * a.out_T + t) * a.Ht + y) * a.Wt + x;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      float v[32];
+      tc::tmem_ld32(trow + c, v);
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        v[i] += __ldg(a.bias + n0 + c + i);
+        if (a.act) v[i] = silu(v[i]);
+      }
+      if (a.residual != nullptr && valid) {
+        const uint4* rp = reinterpret_cast<const uint4*>(a.residual + tok * a.N + n0 + c);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint4 u = __ldg(rp + q);
+          const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            float2 f = __bfloat1622float2(h2[e]);
+            v[q * 8 + 2 * e] += f.x;
+            v[q * 8 + 2 * e + 1] += f.y;
+          }
+        }
+      }
+      const int box = c >> 6, j0 = (c & 63) >> 3;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint4 u;
+        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[q * 8 + 2 * e], v[q * 8 + 2 * e + 1]);
+        const int j = j0 + q;
+        *reinterpret_cast<uint4*>(stage + box * A_BYTES + r * 128 + ((j ^ (r & 7)) << 4)) = u;
+      }
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int b = 0; b < BN / 64; ++b) tc::tma_store_5d(&tmC, stage + b * A_BYTES, n0 + b * 64, x0, y0, t, g);
+      tma_store_commit();
+      tma_store_wait_all();
+    }
+  } else if constexpr (EPI == SST_LT_EPI_FSQ) {
+    float v[16];
+    tc::tmem_ld16(trow, v);
+    if (valid) {
+      const size_t tok = (((size_t)g * 2 + t) * a.Ht + y) * a.Wt + x;
+      double codes[FSQ_C];
+      int idx0 = 0, idx1 = 0;
+#pragma unroll
+      for (int i = 0; i < FSQ_C; ++i) {
+        const int L = fsq_levels(i);
+        // constants rounded once from float64, exactly as the oracle does
+        const float half_l = (float)((double)(L - 1) * (1.0 - 1e-3) * 0.5);
+        const float offset = (L % 2 == 0) ? 0.5f : 0.0f;
+        const float shift = (float)atanh((double)offset / (double)half_l);
+        const float z = v[i] + __ldg(a.bias + i);
+        const float b = tanhf(z + shift) * half_l - offset;
+        const int q = (int)rintf(b);
+        const int hw = L / 2;
+        codes[i] = (double)q / (double)hw;
+        const int digit = (q + hw) * fsq_basis(i);
+        if (i < 6) idx0 += digit; else idx1 += digit;
+      }
+      double2* cp = reinterpret_cast<double2*>(a.codes + tok * FSQ_C);
+#pragma unroll
+      for (int i = 0; i < FSQ_C / 2; ++i) cp[i] = make_double2(codes[2 * i], codes[2 * i + 1]);
+      reinterpret_cast<int2*>(a.idx)[tok] = make_int2(idx0, idx1);
+      a.mask[tok] = 1;
+    }
+  } else {  // SST_LT_EPI_PIXELS: 192 columns = one frame's 8x8x3 patch
+    const int f = a.frame_base + blockIdx.y;
+    const bool vec = (a.w & 3) == 0;
+#pragma unroll 1
+    for (int half = 0; half < 2; ++half) {
+      float v[96];
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        float u[32];
+        tc::tmem_ld32(trow + half * 96 + q * 32, u);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[q * 32 + i] = u[i];
+      }
+      if (!valid) continue;
+#pragma unroll
+      for (int i = 0; i < 96; ++i)
+        v[i] = fminf(fmaxf(v[i] + __ldg(a.bias + n0 + half * 96 + i), 0.0f), 1.0f);
+#pragma unroll
+      for (int pr = 0; pr < 4; ++pr) {
+        const int Y = y * 8 + half * 4 + pr;
+        if (Y >= a.h) continue;
+        const int X0 = x * 8;
+        float* dst = a.frames + ((((size_t)g * 9 + f) * a.h + Y) * a.w + X0) * 3;
+        if (vec && X0 + 8 <= a.w) {
+          float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+          for (int e = 0; e < 6; ++e)
+            d4[e] = make_float4(v[pr * 24 + 4 * e], v[pr * 24 + 4 * e + 1], v[pr * 24 + 4 * e + 2],
+                                v[pr * 24 + 4 * e + 3]);
+        } else {
+          const int npx = min(8, a.w - X0);
+#pragma unroll
+          for (int e = 0; e < 24; ++e)
+            if (e / 3 < npx) dst[e] = v[pr * 24 + e];
+        }
+      }
+    }
+  }
+
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, Cfg::TMEM_COLS);
+}
+
+// ---- downscale + pad + patchify --------------------------------------------
+template <int S>
+__global__ void k_lt_patchify(const float* __restrict__ src, int G, int H, int W, int h, int w,
+                              int Ht, int Wt, __nv_bfloat16* __restrict__ pI,
+                              __nv_bfloat16* __restrict__ pP) {
+  const int PW = Wt * 8, PH = Ht * 8;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t total = (int64_t)G * 9 * PH * PW;
+  if (idx >= total) return;
+  const int X = (int)(idx % PW);
+  int64_t rest = idx / PW;
+  const int Y = (int)(rest % PH);
+  rest /= PH;
+  const int f = (int)(rest % 9);
+  const int g = (int)(rest / 9);
+  const int xc = min(X, w - 1), yc = min(Y, h - 1);  // np.pad(mode="edge") of the working frame
+  const float* fr = src + ((int64_t)g * 9 + f) * (int64_t)H * W * 3;
+  float px[3];
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    double acc = 0.0;
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      const int rr = min(yc * S + j, H - 1);
+#pragma unroll
+      for (int l = 0; l < S; ++l) {
+        const int cc = min(xc * S + l, W - 1);
+        acc = acc + (double)__ldg(fr + ((int64_t)rr * W + cc) * 3 + ch);
+      }
+    }
+    px[ch] = __double2float_rn(acc / (double)(S * S));
+  }
+  const int ty = Y >> 3, py = Y & 7, tx = X >> 3, pxl = X & 7;
+  __nv_bfloat16* dst;
+  if (f == 0)
+    dst = pI + ((int64_t)(g * Ht + ty) * Wt + tx) * 192 + (py * 8 + pxl) * 3;
+  else
+    dst = pP + ((int64_t)(g * Ht + ty) * Wt + tx) * 1536 + (((f - 1) * 8 + py) * 8 + pxl) * 3;
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) dst[ch] = __float2bfloat16_rn(px[ch]);
+}
+
+// ---- mask-aware decoder input ----------------------------------------------
+__global__ void k_lt_dec_in(const double* __restrict__ tok, const uint8_t* __restrict__ mask, int G,
+                            int Ht, int Wt, __nv_bfloat16* __restrict__ out) {
+  const int64_t n = (int64_t)Ht * Wt;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)G * 2 * n) return;
+  const int64_t pos = idx % n;
+  const int64_t gt = idx / n;
+  const int t = (int)(gt % 2);
+  const int64_t g = gt / 2;
+  int64_t src = idx;
+  if (t == 1 && !mask[idx]) src = (g * 2) * n + pos;  // conceal P with the co-located I token
+  const bool ok = mask[src] != 0;
+  uint4 o[DEC_IN_C / 8];
+#pragma unroll
+  for (int q = 0; q < DEC_IN_C / 8; ++q) o[q] = make_uint4(0, 0, 0, 0);
+  if (ok) {
+    __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(o);
+#pragma unroll
+    for (int i = 0; i < FSQ_C; ++i) {
+      const int L = fsq_levels(i), hw = L / 2;
+      double q = rint(tok[src * FSQ_C + i] * (double)hw);
+      q = fmin(fmax(q, (double)-hw), (double)(L - 1 - hw));
+      ob[i] = __float2bfloat16_rn((float)(q / (double)hw));
+    }
+  }
+  uint4* op = reinterpret_cast<uint4*>(out + idx * DEC_IN_C);
+#pragma unroll
+  for (int q = 0; q < DEC_IN_C / 8; ++q) op[q] = o[q];
+}
+
+template <int BN, int EPI>
+static int launch_conv(const SstConvDesc* d, cudaStream_t st) {
+  using Cfg = TileCfg<BN>;
+  if (d->N % BN != 0) return SST_ERR_ARG;
+  CUtensorMap tmA, tmB, tmC;
+  memset(&tmA, 0, sizeof(tmA));
+  memset(&tmB, 0, sizeof(tmB));
+  memset(&tmC, 0, sizeof(tmC));
+  const uint64_t adims[5] = {(uint64_t)d->in_C, (uint64_t)d->in_W, (uint64_t)d->in_H,
+                             (uint64_t)d->in_T, (uint64_t)d->G};
+  if (!make_tmap_bf16_5d(&tmA, d->in, adims, BOX_X, BOX_Y)) return SST_ERR_ARG;
+  if (!make_tmap_bf16_2d(&tmB, d->weight, (uint64_t)d->K, (uint64_t)d->N, BN)) return SST_ERR_ARG;
+  if (EPI == SST_LT_EPI_STORE) {
+    const uint64_t cdims[5] = {(uint64_t)d->N, (uint64_t)d->Wt, (uint64_t)d->Ht,
+                               (uint64_t)d->out_T, (uint64_t)d->G};
+    if (!make_tmap_bf16_5d(&tmC, d->out, cdims, BOX_X, BOX_Y)) return SST_ERR_ARG;
+  }
+  ConvArgs a;
+  memset(&a, 0, sizeof(a));
+  a.Ht = d->Ht; a.Wt = d->Wt;
+  a.tiles_x = ceil_div(d->Wt, BOX_X);
+  a.tiles_y = ceil_div(d->Ht, BOX_Y);
+  a.t_lo = d->t_lo; a.t_cnt = d->t_cnt;
+  a.n_taps = d->n_taps;
+  a.kb_per_tap = d->in_C / BK;
+  a.N = d->N;
+  a.out_T = d->out_T;
+  for (int i = 0; i < d->n_taps; ++i)
+    for (int j = 0; j < 3; ++j) a.taps[i][j] = (signed char)d->taps[i][j];
+  a.bias = d->bias;
+  a.act = d->act;
+  a.residual = static_cast<const __nv_bfloat16*>(d->residual);
+  a.codes = d->codes; a.idx = d->idx; a.mask = d->mask;
+  a.frames = d->frames; a.h = d->h; a.w = d->w; a.frame_base = d->frame_base;
+  const int64_t mt = (int64_t)d->G * d->t_cnt * a.tiles_y * a.tiles_x;
+  if (mt <= 0 || mt > 0x7fffffff) return SST_ERR_ARG;
+  dim3 grid((unsigned)mt, d->N / BN);
+  auto kern = k_lt_conv<BN, EPI>;
+  SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
+  kern<<<grid, 128, Cfg::SMEM, st>>>(tmA, tmB, tmC, a);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+}  // namespace lt
+}  // namespace sst
+
+using namespace sst;
+
+extern "C" int sst_lt_conv(const SstConvDesc* d, void* stream) {
+  if (!d || !d->in || !d->weight || !d->bias) return SST_ERR_ARG;
+  if (d->in_C <= 0 || d->in_C % lt::BK != 0) return SST_ERR_ARG;
+  if (d->n_taps < 1 || d->n_taps > 27 || d->K != d->n_taps * d->in_C) return SST_ERR_ARG;
+  if (d->G <= 0 || d->Ht <= 0 || d->Wt <= 0 || d->t_cnt <= 0) return SST_ERR_ARG;
+  for (int i = 0; i < d->n_taps; ++i)
+    for (int j = 0; j < 3; ++j)
+      if (d->taps[i][j] < -8 || d->taps[i][j] > 8) return SST_ERR_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (d->epi) {
+    case SST_LT_EPI_STORE:
+      if (!d->out || d->act < 0 || d->act > 1) return SST_ERR_ARG;
+      return lt::launch_conv<128, SST_LT_EPI_STORE>(d, st);
+    case SST_LT_EPI_FSQ:
+      if (!d->codes || !d->idx || !d->mask || d->N != 16 || d->t_lo != 0 || d->t_cnt != 2)
+        return SST_ERR_ARG;
+      return lt::launch_conv<16, SST_LT_EPI_FSQ>(d, st);
+    case SST_LT_EPI_PIXELS:
+      if (!d->frames || d->h <= 0 || d->w <= 0 || d->frame_base < 0 ||
+          d->frame_base + d->N / 192 > 9 || d->h > d->Ht * 8 || d->w > d->Wt * 8)
+        return SST_ERR_ARG;
+      return lt::launch_conv<192, SST_LT_EPI_PIXELS>(d, st);
+    default:
+      return SST_ERR_ARG;
+  }
+}
+
+extern "C" int sst_lt_patchify(const float* frames, int G, int H, int W, int s, void* pI, void* pP,
+                               void* stream) {
+  if (!frames || !pI || !pP || G <= 0 || H <= 0 || W <= 0) return SST_ERR_ARG;
+  if (s < 1 || s > 3) return SST_ERR_ARG;
+  const int h = ceil_div(H, s), w = ceil_div(W, s);
+  const int Ht = ceil_div(h, 8), Wt = ceil_div(w, 8);
+  const int64_t total = (int64_t)G * 9 * Ht * 8 * Wt * 8;
+  const int threads = 256;
+  const int64_t blocks = ceil_div64(total, threads);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  auto* i = static_cast<__nv_bfloat16*>(pI);
+  auto* p = static_cast<__nv_bfloat16*>(pP);
+  switch (s) {
+    case 1: lt::k_lt_patchify<1><<<(unsigned)blocks, threads, 0, st>>>(frames, G, H, W, h, w, Ht, Wt, i, p); break;
+    case 2: lt::k_lt_patchify<2><<<(unsigned)blocks, threads, 0, st>>>(frames, G, H, W, h, w, Ht, Wt, i, p); break;
+    default: lt::k_lt_patchify<3><<<(unsigned)blocks, threads, 0, st>>>(frames, G, H, W, h, w, Ht, Wt, i, p); break;
+  }
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+extern "C" int sst_lt_dec_in(const double* tok, const uint8_t* mask, int G, int Ht, int Wt, void* out,
+                             void* stream) {
+  if (!tok || !mask || !out || G <= 0 || Ht <= 0 || Wt <= 0) return SST_ERR_ARG;
+  const int64_t total = (int64_t)G * 2 * Ht * Wt;
+  const int threads = 256;
+  lt::k_lt_dec_in<<<(unsigned)ceil_div64(total, threads), threads, 0,
+                    static_cast<cudaStream_t>(stream)>>>(tok, mask, G, Ht, Wt,
+                                                         static_cast<__nv_bfloat16*>(out));
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}

@@ -4,6 +4,7 @@
 #include <mutex>
 
 #include "tma.cuh"
+#include "tc.cuh"
 
 namespace sst {
 
@@ -34,6 +35,49 @@ bool make_tmap_f32_3d(CUtensorMap* map, const void* base, uint64_t dim0, uint64_
   cuuint32_t estride[3] = {1, 1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), gdim, gstride,
                   box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace sst
+
+namespace sst {
+
+// bf16 tensor maps for the tcgen05 convolutions (tc.cuh): 128-byte swizzle,
+// out-of-bounds boxes zero-filled (the convolution halo / causal padding).
+bool make_tmap_bf16_5d(CUtensorMap* map, const void* base, const uint64_t dims[5], uint32_t b1,
+                       uint32_t b2) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  if (reinterpret_cast<uintptr_t>(base) & 15u) return false;
+  cuuint64_t gdim[5];
+  cuuint64_t gstride[4];
+  uint64_t stride = 2;
+  for (int i = 0; i < 5; ++i) {
+    if (dims[i] == 0 || dims[i] >= (1ull << 32)) return false;
+    gdim[i] = dims[i];
+    stride *= dims[i];
+    if (i < 4) gstride[i] = stride;
+  }
+  if (gstride[0] & 15u) return false;
+  cuuint32_t box[5] = {64, b1, b2, 1, 1};
+  cuuint32_t estride[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void*>(base), gdim, gstride,
+                  box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint32_t b1) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  if ((reinterpret_cast<uintptr_t>(base) & 15u) || ((d0 * 2) & 15u)) return false;
+  cuuint64_t gdim[2] = {d0, d1};
+  cuuint64_t gstride[1] = {d0 * 2};
+  cuuint32_t box[2] = {64, b1};
+  cuuint32_t estride[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), gdim, gstride,
+                  box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }

@@ -1,0 +1,294 @@
+"""Learned tokenizer plug-in: a causal spatio-temporal
+convolutional tokenizer with finite-scalar quantisation (FSQ), run on the
+B200's tensor cores and plugged in at the reference's tokenizer hook.
+
+The reference (`semstream`) ships no learned model: its tokenizer is a fixed
+8x8 block-DCT proxy "behind the same interface a learned model would use"
+(pkg/README.md:3-7).  The paper's codec is a Cosmos-style
+tokenizer: causal spatio-temporal blocks, 8x spatial and 8x
+temporal compression, FSQ latents.  This module is that shape of model behind
+the reference's plug-in contract (session.py:57-61):
+
+    encode(GoP, CodecConfig) -> (TokenMatrix I, TokenMatrix P)
+    decode(TokenMatrix I, TokenMatrix P, CodecConfig) -> GoP
+
+Geometry (identical to the proxy so packetisation, intelligent dropping and
+reassembly are reused unchanged):
+
+  * a 9-frame GoP at working resolution h x w is edge-padded to the 8x8 grid
+    (codec.py:99-105) and patchified: latent frame t=0 (I) embeds frame 0's
+    8x8x3 patch, latent frame t=1 (P) embeds frames 1..8's 8x8x8x3 patch;
+  * encoder: patch embeddings -> D channels, `blocks` causal residual blocks
+    h += conv(SiLU(conv(h))) with (2,3,3) kernels that see t and t-1 only,
+    then a 1x1 head to 12 channels and FSQ (two groups of levels
+    (8,8,8,5,5,5), 64000 codes each).  The 12 FSQ code values are the
+    TokenMatrix channels (codec.py:32 fixes C = 12) and travel through the
+    reference's 8-bit row quantiser; the decoder snaps them back onto the FSQ
+    grid, which is lossless because the quantiser error (<= range/510) is far
+    below half an FSQ step;
+  * decoder: masked P tokens take the co-located I token's codes (the
+    proxy's concealment rule, codec.py:176-180, in latent space), a (2,3,3)
+    conv lifts 12 -> D channels, `blocks` residual blocks, then 1x1 unpatchify
+    convs write frame 0 (from t=0) and frames 1..8 (from t=1), clamped to
+    [0, 1] and cropped to the working frame.
+
+Every convolution is one `sst_lt_conv` launch: an implicit GEMM on tcgen05
+(bf16 operands, fp32 accumulation in TMEM, TMA-fed, fused epilogue).
+Weights are seeded random-init (there is no checkpoint; BASELINE.json
+configs[0] "random-init weights").  Parity is against the torch fp32
+restatement in oracle/learned_oracle.py (unpinned: no reference model).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _dev, _lib
+from .codec import CodecConfig, TokenMatrix, token_grid_shape
+from .video import GOP_SIZE, Frame, GoP
+
+FSQ_LEVELS = (8, 8, 8, 5, 5, 5, 8, 8, 8, 5, 5, 5)
+FSQ_CHANNELS = len(FSQ_LEVELS)      # = CodecConfig.channels (codec.py:32)
+DEC_IN_CHANNELS = 64                # FSQ codes zero-padded to one 128-byte K block
+PATCH_I = 8 * 8 * 3
+PATCH_P = 8 * 8 * 8 * 3
+
+# (dt, dy, dx) of the causal (2,3,3) kernel, in K order (kt, ky, kx)
+TAPS_233 = [(kt - 1, ky - 1, kx - 1) for kt in range(2) for ky in range(3) for kx in range(3)]
+
+
+@dataclass(frozen=True)
+class LearnedConfig:
+    dim: int = 256          # latent channels D (multiple of 128)
+    blocks: int = 2         # residual blocks in the encoder and in the decoder
+    seed: int = 0
+
+    def __post_init__(self):
+        if self.dim <= 0 or self.dim % 128:
+            raise ValueError(f"dim must be a positive multiple of 128, got {self.dim}")
+        if not 0 <= self.blocks <= 8:
+            raise ValueError(f"blocks must be in [0, 8], got {self.blocks}")
+
+
+def _bf16_round(a: np.ndarray) -> np.ndarray:
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float32)).to(
+        torch.bfloat16).to(torch.float32).numpy()
+
+
+def make_weights(cfg: LearnedConfig) -> dict:
+    """Seeded random-init weights as float32 arrays holding bf16 values.
+
+    Layout: W[name] is [N][K] with K ordered (tap, input channel), the GEMM
+    "B" operand of the implicit convolution; b[name] is [N] float32.
+    """
+    rng = np.random.default_rng(cfg.seed)
+    D = cfg.dim
+
+    def normal(n, k, std):
+        return _bf16_round(rng.standard_normal((n, k)).astype(np.float32) * np.float32(std))
+
+    W, b = {}, {}
+    W["pe_i"] = normal(D, PATCH_I, 1.0 / np.sqrt(PATCH_I))
+    W["pe_p"] = normal(D, PATCH_P, 1.0 / np.sqrt(PATCH_P))
+    b["pe_i"] = _bf16_round(rng.standard_normal(D).astype(np.float32) * 0.1)
+    b["pe_p"] = _bf16_round(rng.standard_normal(D).astype(np.float32) * 0.1)
+    K3 = len(TAPS_233) * D
+    for part in ("enc", "dec"):
+        for i in range(cfg.blocks):
+            W[f"{part}{i}_c1"] = normal(D, K3, np.sqrt(2.0 / K3))
+            W[f"{part}{i}_c2"] = normal(D, K3, 0.3 / np.sqrt(K3))
+            b[f"{part}{i}_c1"] = np.zeros(D, np.float32)
+            b[f"{part}{i}_c2"] = np.zeros(D, np.float32)
+    head = np.zeros((16, D), np.float32)
+    head[:FSQ_CHANNELS] = normal(FSQ_CHANNELS, D, 1.5 / np.sqrt(D))
+    W["head"] = head
+    b["head"] = np.zeros(16, np.float32)
+    # decoder input conv: only the 12 code channels of each tap carry weight
+    w_in = np.zeros((D, len(TAPS_233), DEC_IN_CHANNELS), np.float32)
+    w_in[:, :, :FSQ_CHANNELS] = normal(D, len(TAPS_233) * FSQ_CHANNELS,
+                                       np.sqrt(2.0 / (len(TAPS_233) * FSQ_CHANNELS))).reshape(
+        D, len(TAPS_233), FSQ_CHANNELS)
+    W["dec_in"] = w_in.reshape(D, -1)
+    b["dec_in"] = np.zeros(D, np.float32)
+    W["out_i"] = normal(PATCH_I, D, 0.25 / np.sqrt(D))
+    W["out_p"] = normal(PATCH_P, D, 0.25 / np.sqrt(D))
+    b["out_i"] = np.full(PATCH_I, 0.5, np.float32)
+    b["out_p"] = np.full(PATCH_P, 0.5, np.float32)
+    return {"W": W, "b": b}
+
+
+def _taps_array(taps):
+    arr = ((C.c_int32 * 3) * 27)()
+    for i, (dt, dy, dx) in enumerate(taps):
+        arr[i][0], arr[i][1], arr[i][2] = dt, dy, dx
+    return arr
+
+
+class LearnedTokenizer:
+    """Device-resident learned tokenizer (weights bf16 on the GPU)."""
+
+    def __init__(self, cfg: LearnedConfig | None = None, weights: dict | None = None):
+        self.cfg = cfg or LearnedConfig()
+        dev = _dev.device()
+        host = weights if weights is not None else make_weights(self.cfg)
+        self.host_weights = host
+        self.W = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev).to(torch.bfloat16)
+                  for k, v in host["W"].items()}
+        self.b = {k: torch.from_numpy(np.ascontiguousarray(v, dtype=np.float32)).to(dev)
+                  for k, v in host["b"].items()}
+        self.launches = 0
+
+    # ---- one layer ----------------------------------------------------------
+    def _conv(self, name, x, in_shape, out_grid, taps, t_lo, t_cnt, epi, *, act=0,
+              residual=None, out=None, out_T=2, codes=None, idx=None, mask=None, frames=None,
+              hw=(0, 0), frame_base=0):
+        G, T_in, H_in, W_in, C_in = in_shape
+        Ht, Wt = out_grid
+        W = self.W[name]
+        d = _lib.SstConvDesc()
+        d.in_ = x.data_ptr()
+        d.in_C, d.in_W, d.in_H, d.in_T = C_in, W_in, H_in, T_in
+        d.G, d.Ht, d.Wt, d.t_lo, d.t_cnt = G, Ht, Wt, t_lo, t_cnt
+        d.n_taps = len(taps)
+        d.taps = _taps_array(taps)
+        d.weight = W.data_ptr()
+        d.N, d.K = W.shape
+        d.bias = self.b[name].data_ptr()
+        d.epi, d.act = epi, act
+        d.residual = residual.data_ptr() if residual is not None else None
+        d.out = out.data_ptr() if out is not None else None
+        d.out_T = out_T
+        d.codes = codes.data_ptr() if codes is not None else None
+        d.idx = idx.data_ptr() if idx is not None else None
+        d.mask = mask.data_ptr() if mask is not None else None
+        d.frames = frames.data_ptr() if frames is not None else None
+        d.h, d.w = hw
+        d.frame_base = frame_base
+        _lib.call("sst_lt_conv", C.byref(d), _dev.stream())
+        self.launches += 1
+
+    def _blocks(self, part, h, u, G, Ht, Wt):
+        D = self.cfg.dim
+        shape = (G, 2, Ht, Wt, D)
+        for i in range(self.cfg.blocks):
+            self._conv(f"{part}{i}_c1", h, shape, (Ht, Wt), TAPS_233, 0, 2, _lib.LT_EPI_STORE,
+                       act=1, out=u)
+            self._conv(f"{part}{i}_c2", u, shape, (Ht, Wt), TAPS_233, 0, 2, _lib.LT_EPI_STORE,
+                       residual=h, out=h)
+
+    # ---- encoder ------------------------------------------------------------
+    def encode_frames(self, frames: torch.Tensor, s: int = 1):
+        """frames: float32 [G][9][H][W][3] on the GPU (full resolution when
+        s in {2,3}: the box downscale is fused into the patchify pass).
+        Returns (codes f64 [G][2][H'][W'][12], idx i32 [G][2][H'][W'][2],
+        mask u8 [G][2][H'][W'], (h, w))."""
+        if frames.dtype != torch.float32 or frames.dim() != 5 or frames.shape[1] != GOP_SIZE \
+                or frames.shape[4] != 3:
+            raise ValueError("frames must be float32 [G][9][H][W][3]")
+        frames = frames.contiguous()
+        G, _, H, Wd, _ = frames.shape
+        h, w = -(-H // s), -(-Wd // s)
+        Ht, Wt = token_grid_shape(h, w)
+        D = self.cfg.dim
+        dev = frames.device
+        pI = torch.empty((G, 1, Ht, Wt, PATCH_I), dtype=torch.bfloat16, device=dev)
+        pP = torch.empty((G, 1, Ht, Wt, PATCH_P), dtype=torch.bfloat16, device=dev)
+        st = _dev.stream()
+        _lib.call("sst_lt_patchify", frames.data_ptr(), G, H, Wd, s, pI.data_ptr(),
+                  pP.data_ptr(), st)
+        self.launches += 1
+        hbuf = torch.empty((G, 2, Ht, Wt, D), dtype=torch.bfloat16, device=dev)
+        ubuf = torch.empty_like(hbuf)
+        self._conv("pe_i", pI, (G, 1, Ht, Wt, PATCH_I), (Ht, Wt), [(0, 0, 0)], 0, 1,
+                   _lib.LT_EPI_STORE, out=hbuf)
+        self._conv("pe_p", pP, (G, 1, Ht, Wt, PATCH_P), (Ht, Wt), [(-1, 0, 0)], 1, 1,
+                   _lib.LT_EPI_STORE, out=hbuf)
+        self._blocks("enc", hbuf, ubuf, G, Ht, Wt)
+        codes = torch.zeros((G, 2, Ht, Wt, FSQ_CHANNELS), dtype=torch.float64, device=dev)
+        idx = torch.zeros((G, 2, Ht, Wt, 2), dtype=torch.int32, device=dev)
+        mask = torch.zeros((G, 2, Ht, Wt), dtype=torch.uint8, device=dev)
+        self._conv("head", hbuf, (G, 2, Ht, Wt, D), (Ht, Wt), [(0, 0, 0)], 0, 2,
+                   _lib.LT_EPI_FSQ, codes=codes, idx=idx, mask=mask)
+        return codes, idx, mask, (h, w)
+
+    # ---- decoder ------------------------------------------------------------
+    def decode_tokens(self, tokens: torch.Tensor, mask: torch.Tensor, hw) -> torch.Tensor:
+        """tokens: float64 [G][2][H'][W'][12] (received, possibly 8-bit
+        requantised codes; masked = 0), mask u8 [G][2][H'][W'].  Returns the
+        working-resolution frames float32 [G][9][h][w][3]."""
+        if tokens.dtype != torch.float64 or tokens.dim() != 5 or tokens.shape[1] != 2 \
+                or tokens.shape[4] != FSQ_CHANNELS:
+            raise ValueError("tokens must be float64 [G][2][H'][W'][12]")
+        tokens = tokens.contiguous()
+        mask = mask.to(torch.uint8).contiguous()
+        G, _, Ht, Wt, _ = tokens.shape
+        h, w = hw
+        if not (0 < h <= Ht * 8 and 0 < w <= Wt * 8):
+            raise ValueError(f"frame shape {hw} does not fit a {Ht}x{Wt} token grid")
+        D = self.cfg.dim
+        dev = tokens.device
+        x = torch.empty((G, 2, Ht, Wt, DEC_IN_CHANNELS), dtype=torch.bfloat16, device=dev)
+        st = _dev.stream()
+        _lib.call("sst_lt_dec_in", tokens.data_ptr(), mask.data_ptr(), G, Ht, Wt, x.data_ptr(),
+                  st)
+        self.launches += 1
+        hbuf = torch.empty((G, 2, Ht, Wt, D), dtype=torch.bfloat16, device=dev)
+        ubuf = torch.empty_like(hbuf)
+        self._conv("dec_in", x, (G, 2, Ht, Wt, DEC_IN_CHANNELS), (Ht, Wt), TAPS_233, 0, 2,
+                   _lib.LT_EPI_STORE, act=1, out=hbuf)
+        self._blocks("dec", hbuf, ubuf, G, Ht, Wt)
+        frames = torch.empty((G, GOP_SIZE, h, w, 3), dtype=torch.float32, device=dev)
+        self._conv("out_i", hbuf, (G, 2, Ht, Wt, D), (Ht, Wt), [(0, 0, 0)], 0, 1,
+                   _lib.LT_EPI_PIXELS, frames=frames, hw=(h, w), frame_base=0)
+        self._conv("out_p", hbuf, (G, 2, Ht, Wt, D), (Ht, Wt), [(0, 0, 0)], 1, 1,
+                   _lib.LT_EPI_PIXELS, frames=frames, hw=(h, w), frame_base=1)
+        return frames
+
+    def flops_per_gop(self, Ht: int, Wt: int) -> int:
+        """Tensor-core flops of one GoP (2 latent frames of Ht x Wt tokens),
+        counting the padded GEMM shapes the kernels actually issue."""
+        D, n = self.cfg.dim, Ht * Wt
+        k3 = len(TAPS_233) * D
+        enc = n * 2 * D * (PATCH_I + PATCH_P) + 2 * n * 2 * (2 * self.cfg.blocks * k3 * D) \
+            + 2 * n * 2 * D * 16
+        dec = 2 * n * 2 * len(TAPS_233) * DEC_IN_CHANNELS * D \
+            + 2 * n * 2 * (2 * self.cfg.blocks * k3 * D) + n * 2 * D * (PATCH_I + PATCH_P)
+        return enc + dec
+
+
+# ---- the reference's plug-in contract (session.py:57-61) -------
+
+class LearnedPlugin:
+    """(encode, decode) pair for SessionConfig.tokenizer_encode/_decode.
+
+    The plug-in receives the already downscaled working GoP
+    (session.py:139-140), so the patchify runs at s = 1.
+    """
+
+    def __init__(self, cfg: LearnedConfig | None = None):
+        self.model = LearnedTokenizer(cfg)
+
+    def encode(self, gop: GoP, cfg: CodecConfig):
+        frames = np.stack([f.samples for f in gop.frames])[None]
+        codes, _, mask, (h, w) = self.model.encode_frames(_dev.h2d(frames, np.float32), 1)
+        vals = _dev.d2h(codes)[0]
+        m = _dev.d2h(mask)[0].astype(bool)
+        return (TokenMatrix("I", vals[0], m[0], gop_id=gop.gop_id, frame_shape=(h, w)),
+                TokenMatrix("P", vals[1], m[1], gop_id=gop.gop_id, frame_shape=(h, w)))
+
+    def decode(self, i_tokens: TokenMatrix, p_tokens: TokenMatrix, cfg: CodecConfig) -> GoP:
+        if i_tokens.values.shape != p_tokens.values.shape:
+            raise ValueError("I and P token matrices differ in shape")
+        if i_tokens.values.shape[2] != FSQ_CHANNELS:
+            raise ValueError(f"learned tokenizer expects {FSQ_CHANNELS} channels")
+        h, w = i_tokens.frame_shape
+        tok = np.stack([i_tokens.values, p_tokens.values])[None]
+        mask = np.stack([i_tokens.mask, p_tokens.mask])[None].astype(np.uint8)
+        frames = _dev.d2h(self.model.decode_tokens(_dev.h2d(tok, np.float64),
+                                                   _dev.h2d(mask, np.uint8), (h, w)))[0]
+        out = tuple(Frame(frames[t], timestamp_index=t) for t in range(GOP_SIZE))
+        return GoP(gop_id=i_tokens.gop_id, frames=out)
