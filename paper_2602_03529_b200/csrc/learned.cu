@@ -60,7 +60,7 @@ struct ConvArgs {
   int h, w, frame_base;
 };
 
-__device__ __forceinline__ float silu(float x) { return x / (1.0f + __expf(-x)); }
+__device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 
 template <int BN>
 struct TileCfg {
@@ -266,6 +266,178 @@ __global__ void __launch_bounds__(128, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, Cfg::TMEM_COLS);
 }
 
+// ---- causal (2,3,3) convolution with halo reuse ----------------------------
+// A CTA computes 256 tokens (a 16 x 16 spatial tile of one latent frame) x 256
+// output channels as two M=128 tcgen05 accumulators (TMEM columns 0..255 and
+// 256..511).  For each (temporal tap, 64-channel block) ONE 5-D TMA box brings
+// the tile's 18 x 18 halo (zero-filled outside the frame and
+// before t=0) into shared memory; the nine spatial taps are then nine UMMA
+// descriptors into that halo (start row (1+dy)*18 + (1+dx) [+ 8 for the right
+// half], 8-row groups 18 rows apart), so A is fetched once per 9 taps instead
+// of 9 times.  The 128-byte swizzle is a function of the absolute shared
+// address for both TMA and UMMA, so descriptors may start on any 128-byte row
+// (base offset 0) and the group stride need not be a multiple of 1024 B.  The weights stream through a 3-stage ring, each B stage feeding
+// 2 x 4 MMAs.  L2->SM traffic per 256 tokens: 8 halos x 41 KB + the weights
+// once (2.36 MB), vs 2 x 18 x 16 KB x 4 + 2 x 2.36 MB for the generic kernel.
+namespace c233 {
+constexpr int TILE = 16;                // 16 x 16 output tokens
+constexpr int PITCH = 18;               // halo row pitch in tokens (dense: the swizzle is on absolute smem addresses)
+constexpr int HROWS = 18;               // halo rows
+constexpr int HALO_BYTES = PITCH * HROWS * 128;   // 41472
+constexpr int BN = 256;
+constexpr int B_BYTES = BN * 128;       // 32768
+constexpr int HALO_STRIDE = (HALO_BYTES + 1023) / 1024 * 1024;  // slots stay 1024-B aligned
+constexpr int HSLOTS = 2, BSTAGES = 4;
+constexpr int SMEM = HSLOTS * HALO_STRIDE + BSTAGES * B_BYTES + 1024 + 256;
+constexpr int THREADS = 256;
+}  // namespace c233
+
+__device__ __forceinline__ uint64_t halo_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((c233::PITCH * 128) >> 4) << 32;   // 8-row groups are PITCH rows apart
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__global__ void __launch_bounds__(c233::THREADS, 1)
+    k_lt_conv233(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                 const ConvArgs a) {
+  using namespace c233;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sH = smem;
+  uint8_t* sB = smem + HSLOTS * HALO_STRIDE;
+  uint64_t* hfull = reinterpret_cast<uint64_t*>(sB + BSTAGES * B_BYTES);
+  uint64_t* hempty = hfull + HSLOTS;
+  uint64_t* bfull = hempty + HSLOTS;
+  uint64_t* bempty = bfull + BSTAGES;
+  uint64_t* accum = bempty + BSTAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accum + 1);
+
+  const int warp = threadIdx.x >> 5;
+  int tile = blockIdx.x;
+  const int tx = tile % a.tiles_x; tile /= a.tiles_x;
+  const int ty = tile % a.tiles_y; tile /= a.tiles_y;
+  const int t = a.t_lo + tile % a.t_cnt;
+  const int g = tile / a.t_cnt;
+  const int x0 = tx * TILE, y0 = ty * TILE;
+  const int n0 = blockIdx.y * BN;
+
+  if (threadIdx.x == 0) {
+    tc::prefetch_tmap(&tmA);
+    tc::prefetch_tmap(&tmB);
+    for (int i = 0; i < HSLOTS; ++i) { mbar_init(&hfull[i], 1); mbar_init(&hempty[i], 1); }
+    for (int i = 0; i < BSTAGES; ++i) { mbar_init(&bfull[i], 1); mbar_init(&bempty[i], 1); }
+    mbar_init(accum, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  const int nh = 2 * a.kb_per_tap;   // (temporal tap, channel block) pairs
+  const int C = a.kb_per_tap * BK;
+  if (threadIdx.x == 0) {
+    // ---- TMA producer: halos and weight k-blocks in consumption order ----
+    int kb = 0;
+    for (int hi = 0; hi < nh; ++hi) {
+      const int kt = hi / a.kb_per_tap, cb = hi - kt * a.kb_per_tap;
+      const int hs = hi % HSLOTS;
+      if (hi >= HSLOTS) mbar_wait(&hempty[hs], ((hi / HSLOTS) - 1) & 1);
+      mbar_expect_tx(&hfull[hs], HALO_BYTES);
+      tc::tma_load_5d(sH + hs * HALO_STRIDE, &tmA, cb * BK, x0 - 1, y0 - 1, t + kt - 1, g, &hfull[hs]);
+      for (int sp = 0; sp < 9; ++sp, ++kb) {
+        const int bs = kb % BSTAGES;
+        if (kb >= BSTAGES) mbar_wait(&bempty[bs], ((kb / BSTAGES) - 1) & 1);
+        mbar_expect_tx(&bfull[bs], B_BYTES);
+        const int tap = kt * 9 + sp;
+        tc::tma_load_2d(sB + bs * B_BYTES, &tmB, tap * C + cb * BK, n0, &bfull[bs]);
+      }
+    }
+  } else if (threadIdx.x == 32) {
+    // ---- MMA issuer ----
+    constexpr uint32_t idesc = tc::idesc_bf16_f32(128, BN);
+    int kb = 0;
+    for (int hi = 0; hi < nh; ++hi) {
+      const int hs = hi % HSLOTS;
+      mbar_wait(&hfull[hs], (hi / HSLOTS) & 1);
+      const uint32_t hbase = smem_u32(sH + hs * HALO_STRIDE);
+      for (int sp = 0; sp < 9; ++sp, ++kb) {
+        const int bs = kb % BSTAGES;
+        mbar_wait(&bfull[bs], (kb / BSTAGES) & 1);
+        tc::fence_after_sync();
+        const int dy = sp / 3, dx = sp % 3;   // halo offsets (1+dy', 1+dx')
+        const uint64_t bd = tc::smem_desc_sw128(smem_u32(sB + bs * B_BYTES));
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          const uint64_t ad = halo_desc(hbase + (uint32_t)((dy * PITCH + dx + 8 * half) * 128));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            tc::mma_bf16(tmem + half * BN, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+        }
+        tc::mma_commit(&bempty[bs]);
+      }
+      tc::mma_commit(&hempty[hs]);
+    }
+    tc::mma_commit(accum);
+  }
+  __syncwarp();
+  mbar_wait(accum, 0);
+  tc::fence_after_sync();
+
+  // ---- epilogue: 8 warps; warp w drains half (w >> 2), TMEM lanes 32*(w & 3) ----
+  const int half = warp >> 2, q = warp & 3;
+  const int m = q * 32 + (threadIdx.x & 31);        // accumulator row
+  const int y = y0 + (m >> 3), x = x0 + half * 8 + (m & 7);
+  const bool valid = y < a.Ht && x < a.Wt;
+  const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + half * BN;
+  const size_t tok = (((size_t)g * a.out_T + t) * a.Ht + y) * a.Wt + x;
+  __nv_bfloat16* outp = reinterpret_cast<__nv_bfloat16*>(a.frames) + tok * a.N + n0;  // out tensor
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 32) {
+    float v[32];
+    tc::tmem_ld32(trow + c, v);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      v[i] += __ldg(a.bias + n0 + c + i);
+      if (a.act) v[i] = silu(v[i]);
+    }
+    if (!valid) continue;
+    if (a.residual != nullptr) {
+      const uint4* rp = reinterpret_cast<const uint4*>(a.residual + tok * a.N + n0 + c);
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) {
+        uint4 u = __ldg(rp + qq);
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float2 f = __bfloat1622float2(h2[e]);
+          v[qq * 8 + 2 * e] += f.x;
+          v[qq * 8 + 2 * e + 1] += f.y;
+        }
+      }
+    }
+    uint4* op = reinterpret_cast<uint4*>(outp + c);
+#pragma unroll
+    for (int qq = 0; qq < 4; ++qq) {
+      uint4 u;
+      __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[qq * 8 + 2 * e], v[qq * 8 + 2 * e + 1]);
+      op[qq] = u;
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) tc::tmem_dealloc(tmem, 512);
+}
+
 // ---- downscale + pad + patchify --------------------------------------------
 template <int S>
 __global__ void k_lt_patchify(const float* __restrict__ src, int G, int H, int W, int h, int w,
@@ -383,8 +555,54 @@ static int launch_conv(const SstConvDesc* d, cudaStream_t st) {
   return SST_OK;
 }
 
+static bool is_taps233(const SstConvDesc* d) {
+  if (d->n_taps != 18) return false;
+  for (int i = 0; i < 18; ++i) {
+    const int kt = i / 9, ky = (i / 3) % 3, kx = i % 3;
+    if (d->taps[i][0] != kt - 1 || d->taps[i][1] != ky - 1 || d->taps[i][2] != kx - 1) return false;
+  }
+  return true;
+}
+
+static int launch_conv233(const SstConvDesc* d, cudaStream_t st) {
+  if (d->N % c233::BN != 0 || d->t_lo != 0 || d->t_cnt != d->in_T || d->in_T != d->out_T ||
+      d->in_W != d->Wt || d->in_H != d->Ht)
+    return SST_ERR_ARG;
+  CUtensorMap tmA, tmB;
+  memset(&tmA, 0, sizeof(tmA));
+  memset(&tmB, 0, sizeof(tmB));
+  const uint64_t adims[5] = {(uint64_t)d->in_C, (uint64_t)d->in_W, (uint64_t)d->in_H,
+                             (uint64_t)d->in_T, (uint64_t)d->G};
+  if (!make_tmap_bf16_5d(&tmA, d->in, adims, c233::PITCH, c233::HROWS)) return SST_ERR_ARG;
+  if (!make_tmap_bf16_2d(&tmB, d->weight, (uint64_t)d->K, (uint64_t)d->N, c233::BN)) return SST_ERR_ARG;
+  ConvArgs a;
+  memset(&a, 0, sizeof(a));
+  a.Ht = d->Ht; a.Wt = d->Wt;
+  a.tiles_x = ceil_div(d->Wt, c233::TILE);
+  a.tiles_y = ceil_div(d->Ht, c233::TILE);
+  a.t_lo = 0; a.t_cnt = d->t_cnt;
+  a.n_taps = 18;
+  a.kb_per_tap = d->in_C / BK;
+  a.N = d->N;
+  a.out_T = d->out_T;
+  a.bias = d->bias;
+  a.act = d->act;
+  a.residual = static_cast<const __nv_bfloat16*>(d->residual);
+  a.frames = static_cast<float*>(d->out);   // carries the bf16 output pointer
+  const int64_t mt = (int64_t)d->G * d->t_cnt * a.tiles_y * a.tiles_x;
+  if (mt <= 0 || mt > 0x7fffffff) return SST_ERR_ARG;
+  dim3 grid((unsigned)mt, d->N / c233::BN);
+  SST_CUDA_TRY(cudaFuncSetAttribute(k_lt_conv233, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    c233::SMEM));
+  k_lt_conv233<<<grid, c233::THREADS, c233::SMEM, st>>>(tmA, tmB, a);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
 }  // namespace lt
 }  // namespace sst
+
+#include <cstdlib>
 
 using namespace sst;
 
@@ -398,9 +616,14 @@ extern "C" int sst_lt_conv(const SstConvDesc* d, void* stream) {
       if (d->taps[i][j] < -8 || d->taps[i][j] > 8) return SST_ERR_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   switch (d->epi) {
-    case SST_LT_EPI_STORE:
+    case SST_LT_EPI_STORE: {
       if (!d->out || d->act < 0 || d->act > 1) return SST_ERR_ARG;
+      // SST_LT_CONV=generic forces the per-tap kernel (A/B comparisons)
+      const char* mode = getenv("SST_LT_CONV");
+      const bool generic = mode && mode[0] == 'g';
+      if (!generic && lt::is_taps233(d) && d->N % lt::c233::BN == 0) return lt::launch_conv233(d, st);
       return lt::launch_conv<128, SST_LT_EPI_STORE>(d, st);
+    }
     case SST_LT_EPI_FSQ:
       if (!d->codes || !d->idx || !d->mask || d->N != 16 || d->t_lo != 0 || d->t_cnt != 2)
         return SST_ERR_ARG;

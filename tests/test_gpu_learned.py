@@ -102,6 +102,29 @@ def test_conv233_store_matches_oracle(shape, cin, act, res):
     _assert_bf16_close(got, want)
 
 
+@pytest.mark.parametrize("shape,cin", [
+    ((2, 2, 16, 16, 64), 64),                # one exact 16x16 tile, decoder-input width
+    ((1, 2, 45, 80, 256), 256),              # 1080p s=3 token grid, ragged last tile row
+    ((2, 2, 13, 37, 64), 64),                # ragged in both dimensions
+])
+def test_conv233_halo_kernel(shape, cin, monkeypatch):
+    """N = 256 runs the halo-reuse kernel (one TMA box per 9 spatial taps,
+    UMMA descriptors starting mid swizzle atom); it must match the oracle and
+    the generic per-tap kernel."""
+    rng = np.random.default_rng(11)
+    G, Tn, H, Wd, _ = shape
+    x = _bf(rng.standard_normal(shape))
+    W = _bf(rng.standard_normal((256, 18 * cin)) / np.sqrt(18 * cin)).numpy()
+    b = _bf(rng.standard_normal(256) * 0.1).numpy()
+    resid = _bf(rng.standard_normal((G, Tn, H, Wd, 256)))
+    want = LO.conv233(x, W, b, act=True, residual=resid)
+    halo = _conv_gpu(x, W, b, TAPS_233, 0, 2, _lib.LT_EPI_STORE, act=1, residual=resid)["out"]
+    _assert_bf16_close(halo, want)
+    monkeypatch.setenv("SST_LT_CONV", "generic")
+    gen = _conv_gpu(x, W, b, TAPS_233, 0, 2, _lib.LT_EPI_STORE, act=1, residual=resid)["out"]
+    _assert_bf16_close(gen, want)
+
+
 def test_conv_causal_first_frame_sees_no_past():
     # t=0 output must not depend on t=1 input (causal temporal kernel)
     rng = np.random.default_rng(2)
