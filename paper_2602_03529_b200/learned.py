@@ -49,6 +49,7 @@ import torch
 
 from . import _dev, _lib
 from .codec import CodecConfig, TokenMatrix, token_grid_shape
+from .pipeline import CHANNELS, GopCodec
 from .video import GOP_SIZE, Frame, GoP
 
 FSQ_LEVELS = (8, 8, 8, 5, 5, 5, 8, 8, 8, 5, 5, 5)
@@ -181,11 +182,13 @@ class LearnedTokenizer:
                        residual=h, out=h)
 
     # ---- encoder ------------------------------------------------------------
-    def encode_frames(self, frames: torch.Tensor, s: int = 1):
+    def encode_frames(self, frames: torch.Tensor, s: int = 1, codes: torch.Tensor | None = None,
+                      mask: torch.Tensor | None = None, idx: torch.Tensor | None = None):
         """frames: float32 [G][9][H][W][3] on the GPU (full resolution when
         s in {2,3}: the box downscale is fused into the patchify pass).
         Returns (codes f64 [G][2][H'][W'][12], idx i32 [G][2][H'][W'][2],
-        mask u8 [G][2][H'][W'], (h, w))."""
+        mask u8 [G][2][H'][W'], (h, w)); codes / mask / idx may be passed in
+        (contiguous, G leading) to be written in place."""
         if frames.dtype != torch.float32 or frames.dim() != 5 or frames.shape[1] != GOP_SIZE \
                 or frames.shape[4] != 3:
             raise ValueError("frames must be float32 [G][9][H][W][3]")
@@ -208,15 +211,23 @@ class LearnedTokenizer:
         self._conv("pe_p", pP, (G, 1, Ht, Wt, PATCH_P), (Ht, Wt), [(-1, 0, 0)], 1, 1,
                    _lib.LT_EPI_STORE, out=hbuf)
         self._blocks("enc", hbuf, ubuf, G, Ht, Wt)
-        codes = torch.zeros((G, 2, Ht, Wt, FSQ_CHANNELS), dtype=torch.float64, device=dev)
-        idx = torch.zeros((G, 2, Ht, Wt, 2), dtype=torch.int32, device=dev)
-        mask = torch.zeros((G, 2, Ht, Wt), dtype=torch.uint8, device=dev)
+        if codes is None:
+            codes = torch.zeros((G, 2, Ht, Wt, FSQ_CHANNELS), dtype=torch.float64, device=dev)
+        if idx is None:
+            idx = torch.zeros((G, 2, Ht, Wt, 2), dtype=torch.int32, device=dev)
+        if mask is None:
+            mask = torch.zeros((G, 2, Ht, Wt), dtype=torch.uint8, device=dev)
+        for t_, shp in ((codes, (G, 2, Ht, Wt, FSQ_CHANNELS)), (idx, (G, 2, Ht, Wt, 2)),
+                        (mask, (G, 2, Ht, Wt))):
+            if tuple(t_.shape) != shp or not t_.is_contiguous():
+                raise ValueError(f"output buffer must be a contiguous {shp} tensor")
         self._conv("head", hbuf, (G, 2, Ht, Wt, D), (Ht, Wt), [(0, 0, 0)], 0, 2,
                    _lib.LT_EPI_FSQ, codes=codes, idx=idx, mask=mask)
         return codes, idx, mask, (h, w)
 
     # ---- decoder ------------------------------------------------------------
-    def decode_tokens(self, tokens: torch.Tensor, mask: torch.Tensor, hw) -> torch.Tensor:
+    def decode_tokens(self, tokens: torch.Tensor, mask: torch.Tensor, hw,
+                      frames: torch.Tensor | None = None) -> torch.Tensor:
         """tokens: float64 [G][2][H'][W'][12] (received, possibly 8-bit
         requantised codes; masked = 0), mask u8 [G][2][H'][W'].  Returns the
         working-resolution frames float32 [G][9][h][w][3]."""
@@ -241,7 +252,10 @@ class LearnedTokenizer:
         self._conv("dec_in", x, (G, 2, Ht, Wt, DEC_IN_CHANNELS), (Ht, Wt), TAPS_233, 0, 2,
                    _lib.LT_EPI_STORE, act=1, out=hbuf)
         self._blocks("dec", hbuf, ubuf, G, Ht, Wt)
-        frames = torch.empty((G, GOP_SIZE, h, w, 3), dtype=torch.float32, device=dev)
+        if frames is None:
+            frames = torch.empty((G, GOP_SIZE, h, w, 3), dtype=torch.float32, device=dev)
+        elif tuple(frames.shape) != (G, GOP_SIZE, h, w, 3) or not frames.is_contiguous():
+            raise ValueError("frames buffer must be a contiguous [G][9][h][w][3] tensor")
         self._conv("out_i", hbuf, (G, 2, Ht, Wt, D), (Ht, Wt), [(0, 0, 0)], 0, 1,
                    _lib.LT_EPI_PIXELS, frames=frames, hw=(h, w), frame_base=0)
         self._conv("out_p", hbuf, (G, 2, Ht, Wt, D), (Ht, Wt), [(0, 0, 0)], 1, 1,
@@ -292,3 +306,92 @@ class LearnedPlugin:
                                                    _dev.h2d(mask, np.uint8), (h, w)))[0]
         out = tuple(Frame(frames[t], timestamp_index=t) for t in range(GOP_SIZE))
         return GoP(gop_id=i_tokens.gop_id, frames=out)
+
+
+# ---- the batched device pipeline with the learned tokenizer ------------------
+
+class LearnedGopCodec(GopCodec):
+    """``pipeline.GopCodec`` with the learned tokenizer in place of the DCT
+    proxy: the sender, transport and receiver stages are the reference's
+    (session.py:134-170, 323-348) and reuse the proxy path's kernels:
+
+      encode      learned encoder + FSQ (tcgen05) -> tokens [G][2][H'][W'][12]
+      similarity  sst_similarity on the FSQ codes (selection.py:33-52)
+      K2 / K3     intelligent drop + 8-bit packetisation with CRC (unchanged)
+      K4          sst_parse + sst_reassemble (first-wins, zero-fill)
+      decode      mask-aware learned decoder (tcgen05), 9 distinct frames
+      K5          sst_upscale (bilinear x s, crop) + sst_blend (Eq. 2)
+    """
+
+    def __init__(self, g_max: int, H: int, W: int, s: int, blend_n: int = 2,
+                 model: LearnedTokenizer | None = None, cfg: LearnedConfig | None = None):
+        super().__init__(g_max, H, W, s, blend_n)
+        self.model = model if model is not None else LearnedTokenizer(cfg)
+        dev = self.tok.device
+        self.idx = torch.empty((g_max, 2, self.Ht, self.Wt, 2), dtype=torch.int32, device=dev)
+        self.rx_tok = torch.empty_like(self.tok)
+        self.rx_mask = torch.empty_like(self.mask)
+        self.frames9 = torch.empty((g_max, GOP_SIZE, self.h, self.w, 3), dtype=torch.float32,
+                                   device=dev)
+
+    def tokenize(self, frames: torch.Tensor, g: int) -> None:
+        tm = self.timer
+        tm.begin("L_encode")
+        self.model.encode_frames(frames[:g], self.s, codes=self.tok[:g], mask=self.mask[:g],
+                                 idx=self.idx[:g])
+        tm.end("L_encode")
+        tm.begin("L_similarity")
+        n, st = self.n, _dev.stream()
+        stride = 2 * n * CHANNELS * 8
+        base = self.tok.data_ptr()
+        for j in range(g):
+            _lib.call("sst_similarity", base + j * stride + n * CHANNELS * 8, base + j * stride,
+                      n, CHANNELS, self.sim.data_ptr() + j * n * 8, st)
+        tm.end("L_similarity")
+
+    def decode(self, g: int, parity: int, arena: torch.Tensor | None = None,
+               present: torch.Tensor | None = None) -> torch.Tensor:
+        """K4 parse + reassemble, then the learned decoder; returns the
+        [g, 9, h, w, 3] working-resolution frames."""
+        st = _dev.stream()
+        arena = self.arena if arena is None else arena
+        npk = g * self.n_pkt_per_gop
+        tm = self.timer
+        tm.begin("K4_parse")
+        _lib.call("sst_parse", arena.data_ptr(), self.offsets.data_ptr(),
+                  self.lengths.data_ptr(), None if present is None else present.data_ptr(), npk,
+                  self.info.data_ptr(), st)
+        tm.end("K4_parse")
+        tm.begin("K4_reassemble")
+        _lib.call("sst_reassemble", arena.data_ptr(), self.offsets.data_ptr(),
+                  self.info.data_ptr(), self.target.data_ptr(), npk, 2 * g, self.Ht, self.Wt,
+                  CHANNELS, self.kind.data_ptr(), self.gop_id.data_ptr(), self.winner.data_ptr(),
+                  self.rx_tok.data_ptr(), self.rx_mask.data_ptr(), self.stats.data_ptr(), st)
+        tm.end("K4_reassemble")
+        tm.begin("L_decode")
+        self.model.decode_tokens(self.rx_tok[:g], self.rx_mask[:g], (self.h, self.w),
+                                 frames=self.frames9[:g])
+        tm.end("L_decode")
+        return self.frames9[:g]
+
+    def reconstruct(self, g: int, parity: int, out: torch.Tensor,
+                    prev: torch.Tensor | None = None) -> None:
+        """Upscale the 9 decoded frames of g GoPs to [g, 9, H, W, 3] and blend
+        frames 0..n-1 with ``prev`` (the previous GoPs' output frames, same
+        shape) when given."""
+        st = _dev.stream()
+        self.timer.begin("K5_upscale_blend")
+        _lib.call("sst_upscale", self.frames9.data_ptr(), g * GOP_SIZE, self.h, self.w, self.s,
+                  self.H, self.W, out.data_ptr(), st)
+        if prev is not None:
+            _lib.call("sst_blend", prev.data_ptr(), out.data_ptr(), g, self.H, self.W,
+                      self.blend_n, out.data_ptr(), st)
+        self.timer.end("K5_upscale_blend")
+
+    def step(self, frames: torch.Tensor, out: torch.Tensor, g: int, drop_k: int = 0,
+             present: torch.Tensor | None = None, prev: torch.Tensor | None = None) -> None:
+        """One pass of the learned codec over g GoPs: sender then receiver."""
+        self.tokenize(frames, g)
+        self.select_and_pack(g, drop_k)
+        self.decode(g, 0, present=present)
+        self.reconstruct(g, 0, out, prev)

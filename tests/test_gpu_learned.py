@@ -284,3 +284,55 @@ def test_plugin_through_packet_transport():
     for a, b in zip(direct.frames, via.frames):
         assert np.array_equal(a.samples, b.samples)
     assert len(direct.frames) == 9 and direct.frames[0].samples.shape == (64, 96, 3)
+
+
+def test_learned_gop_codec_stages_bit_exact():
+    """LearnedGopCodec: the transport stages around the learned tokenizer are
+    the reference's, bit-exact given the GPU's FSQ codes (similarity, drop
+    mask, packet bytes, reassembly), then the learned decoder, upscale and
+    blend."""
+    from paper_2602_03529_b200.learned import LearnedGopCodec
+
+    H, W, s, g = 72, 100, 2, 2
+    cfg = LearnedConfig(dim=128, blocks=1, seed=4)
+    codec = LearnedGopCodec(g, H, W, s, cfg=cfg)
+    clip = make_clip("moving-square", W, H, 18, seed=2)
+    fr = np.stack([clip.gop(0), clip.gop(1)])
+    dev = _dev.device()
+    frames = torch.from_numpy(fr).to(dev)
+    codec.set_gop_ids([7, 8])
+    drop_k = codec.drop_k(0.25)
+    out = torch.empty_like(frames)
+    prev = torch.rand_like(frames)
+    codec.step(frames, out, g, drop_k=drop_k, prev=prev)
+    torch.cuda.synchronize()
+    codes, _, _, hw = codec.model.encode_frames(frames, s)
+    codes = codes.cpu().numpy()
+    arena, lengths = codec.arena.cpu().numpy(), codec.lengths.cpu().numpy()
+    Ht, Wt = codec.Ht, codec.Wt
+    rx = np.zeros((g, 2, Ht, Wt, 12))
+    rxm = np.zeros((g, 2, Ht, Wt), np.uint8)
+    for j in range(g):
+        sim = O.similarity(codes[j, 1], codes[j, 0])
+        assert np.array_equal(codec.sim[j].cpu().numpy(), sim)
+        drop = O.top_k_mask(sim, drop_k)
+        pv, pm = O.apply_mask(codes[j, 1], np.ones((Ht, Wt), bool), drop)
+        wire = O.packetize(0, 7 + j, codes[j, 0], np.ones((Ht, Wt), bool), s) + \
+            O.packetize(1, 7 + j, pv, pm, s)
+        base = j * codec.n_pkt_per_gop
+        got = [arena[base + i, :lengths[base + i]].tobytes() for i in range(codec.n_pkt_per_gop)]
+        assert got == wire
+        parsed = [O.parse(d) for d in wire]
+        for kind in (0, 1):
+            v, m = O.reassemble([q for q in parsed if q["kind"] == kind], (Ht, Wt, 12))
+            rx[j, kind], rxm[j, kind] = v, m
+    assert np.array_equal(codec.rx_tok[:g].cpu().numpy(), rx)
+    assert np.array_equal(codec.rx_mask[:g].cpu().numpy(), rxm)
+    dec = codec.model.decode_tokens(_dev.h2d(rx, np.float64), _dev.h2d(rxm, np.uint8), hw)
+    assert torch.equal(dec, codec.frames9[:g])
+    d9 = dec.cpu().numpy()
+    pv_ = prev.cpu().numpy()
+    for j in range(g):
+        up = [O.upscale(d9[j, t], s, crop=(H, W)) for t in range(9)]
+        want = O.blend(list(pv_[j]), up, 2)
+        assert np.array_equal(out[j].cpu().numpy(), np.stack(want))
