@@ -65,6 +65,9 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-workers", type=int, default=0, help="0 = auto")
+    ap.add_argument("--no-learned", action="store_true",
+                    help="skip the learned-tokenizer leg (SURVEY f4, tensor-core path)")
+    ap.add_argument("--learned-gops", type=int, default=32)
     ap.add_argument("--roofline-steps", type=int, default=3,
                     help="extra serialised steps timing each kernel alone")
     return ap.parse_args()
@@ -612,6 +615,90 @@ def parity_sample(a, device) -> dict:
 
 
 # ---------------------------------------------------------------------------
+# learned tokenizer leg: tcgen05 implicit-GEMM convs
+
+def measured_bf16_peak():
+    try:
+        d = json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
+        return float(d["bf16_tflops"]), "measured burst (MEASURED_PEAKS.json bf16_tflops)"
+    except Exception:
+        return 2250.0, "nominal dense bf16 (no MEASURED_PEAKS.json)"
+
+
+def run_learned(a, device) -> dict:
+    """G 1080p GoPs per step through LearnedGopCodec (learned encoder + FSQ ->
+    similarity -> 10% drop -> packetise -> parse/reassemble -> learned
+    decoder -> upscale + blend), device-resident, CUDA-event timed; plus one
+    serialised step timing every convolution for the tensor-core roofline."""
+    import torch
+    from paper_2602_03529_b200.learned import LearnedConfig, LearnedGopCodec
+    G, s, H, W = a.learned_gops, 3, a.height, a.width
+    cfg = LearnedConfig()
+    codec = LearnedGopCodec(G, H, W, s, cfg=cfg)
+    gen = torch.Generator(device=device).manual_seed(0)
+    frames = [torch.rand((G, GOP, H, W, 3), generator=gen, device=device) for _ in range(2)]
+    outs = [torch.empty_like(frames[0]) for _ in range(2)]
+    drop_k = codec.drop_k(a.drop)
+    codec.set_gop_ids(list(range(G)))
+
+    def step(k):
+        codec.step(frames[k % 2], outs[k % 2], G, drop_k=drop_k)
+
+    for k in range(max(a.warmup, 3)):
+        step(k)
+    torch.cuda.synchronize()
+    K = max(a.steps // 2, 5)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for k in range(K):
+        step(k + 1)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / K
+    # serialised pass: time every conv launch on its stream
+    model = codec.model
+    times = []
+    orig = model._conv
+
+    def timed(name, x, in_shape, out_grid, taps, t_lo, t_cnt, epi, **kw):
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record()
+        orig(name, x, in_shape, out_grid, taps, t_lo, t_cnt, epi, **kw)
+        b1.record()
+        N, Kd = model.W[name].shape
+        flops = 2 * in_shape[0] * t_cnt * out_grid[0] * out_grid[1] * N * Kd
+        times.append((name, len(taps), b0, b1, flops))
+
+    model._conv = timed
+    try:
+        step(1)
+        torch.cuda.synchronize()
+    finally:
+        model._conv = orig
+    per = [(n, nt, b0.elapsed_time(b1), fl) for n, nt, b0, b1, fl in times]
+    halo = [(ms_, fl) for n, nt, ms_, fl in per if nt == 18 and model.W[n].shape[0] % 256 == 0]
+    conv_ms = sum(ms_ for _, _, ms_, _ in per)
+    peak, src = measured_bf16_peak()
+    achieved = sum(fl for _, fl in halo) / sum(m for m, _ in halo) / 1e9
+    flops_step = model.flops_per_gop(codec.Ht, codec.Wt) * G
+    return {
+        "workload": f"{G} x 1080p GoPs per step, s=3, learned causal conv tokenizer "
+                    f"(D={cfg.dim}, {cfg.blocks} residual blocks per side, FSQ 2x(8,8,8,5,5,5)), "
+                    f"{int(a.drop * 100)}% intelligent drop, blend n=2; random-init weights",
+        "value": round(G * GOP / ms * 1e3, 1), "unit": UNIT, "ms_per_step": round(ms, 3),
+        "tensor_tflops_path": round(flops_step / ms / 1e9, 1),
+        "roofline": {"kernel": "k_lt_conv233 (causal (2,3,3) conv, halo-reuse tcgen05 implicit GEMM)",
+                     "bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
+                     "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "peak_source": src,
+                     "flops_per_launch": halo and int(sum(fl for _, fl in halo) / len(halo)),
+                     "avg_launch_ms": round(sum(m for m, _ in halo) / len(halo), 4),
+                     "launches_per_step": len(halo)},
+        "conv_share_of_serialised_step": round(conv_ms / max(ms, 1e-9), 3),
+        "gpu_launches_per_step": len(per) + 4 + G,
+        "dtype": "bf16 operands, fp32 accumulate (TMEM)",
+        "parity": "tests/test_gpu_learned.py vs oracle/learned_oracle.py (torch fp32, unpinned)",
+    }
+
 
 def main():
     a = parse_args()
@@ -658,6 +745,8 @@ def main():
         if world == 1 and not a.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(a)
             line["parity"] = parity_sample(a, torch.device("cuda", local_rank))
+        if world == 1 and not a.no_learned:
+            line["learned_tokenizer"] = run_learned(a, torch.device("cuda", local_rank))
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -120,6 +120,14 @@ SST_API int sst_clip_cast(const double* x, int64_t count, float* out, void* stre
 SST_API int sst_blend(const float* prev, const float* curr, int G, int H, int W, int n, float* out,
               void* stream);
 
+/* K5 for GoPs whose 9 frames are all distinct (learned-tokenizer decoder):
+ * img [G][9][h][w][3] -> out [G][9][H][W][3] (bilinear x s, clip, crop),
+ * frames 0..n-1 blended with the previous GoP's frames 9-n..8 upscaled from
+ * prev[g].p_img = that GoP's [9][h'][w'][3] working frames (blend_n <= 4).
+ * Requires W*3*4 % 16 == 0 (TMA store). */
+SST_API int sst_upscale_blend9(const float* img, int G, int h, int w, int s, int H, int W,
+                               const SstPrevDesc* prev, int blend_n, float* out, void* stream);
+
 /* ---- tokenizer ---------------------------------------------------------- */
 
 /* scale_gop(down) (codec.py:248-254) fused with encode_gop (codec.py:143-157)

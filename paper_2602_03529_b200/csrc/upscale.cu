@@ -353,6 +353,131 @@ __global__ void __launch_bounds__(kTQ)
   if (tid == 0) tma_store_wait_read();
 }
 
+// ---- K5 for 9 distinct frames (learned decoder output) ----
+// Same band / window / TMA-store scheme as k_upscale_blend_tma, but every
+// frame of the GoP has its own working image: the CTA walks the 9 frames of
+// its (column tile, band), loading one source window per frame.  Boundary
+// frames f < n are blended with the previous GoP's frame 9-n+f, upscaled
+// from that GoP's working frames (prev[g].p_img = its [9][h][w][3] block):
+// for n <= 4 those tail frames are unblended reconstructions, so recomputing
+// them is exact and saves reading two full-resolution frames.
+template <int kBand, bool kPrev, int kN>
+__global__ void __launch_bounds__(kTQ)
+    k_upscale9_tma(const __grid_constant__ CUtensorMap omap, const __grid_constant__ UpArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  UpTmaSmem<kBand>& S = *reinterpret_cast<UpTmaSmem<kBand>*>(smem_raw);
+  UpTile* tiles = reinterpret_cast<UpTile*>(smem_raw + tile_off<kBand>());
+  const int tid = threadIdx.x;
+  const int q0 = blockIdx.x * kTQ;
+  const int oy0 = blockIdx.y * kBand;
+  const int g = blockIdx.z;
+  SstPrevDesc pd;
+  pd.p_img = nullptr;
+  pd.h = pd.w = pd.s = 1;
+  if (kPrev) pd = a.prev[g];
+  const bool has_prev = kPrev && pd.p_img != nullptr;
+  const int rows = min(kBand, a.H - oy0);
+  const int qlast = min(q0 + kTQ, a.W * 3) - 1;
+  if (tid < kBand) S.ty_c[tid] = axis_tap(oy0 + min(tid, rows - 1), a.h, a.s);
+  else if (tid < 2 * kBand) {
+    if (has_prev) S.ty_p[tid - kBand] = axis_tap(oy0 + min(tid - kBand, rows - 1), pd.h, pd.s);
+  } else if (tid == 2 * kBand) {
+    S.wx0[0] = axis_tap(q0 / 3, a.w, a.s).lo;
+    S.wx1[0] = axis_tap(qlast / 3, a.w, a.s).hi;
+  } else if (tid == 2 * kBand + 32 && has_prev) {
+    S.wx0[1] = axis_tap(q0 / 3, pd.w, pd.s).lo;
+    S.wx1[1] = axis_tap(qlast / 3, pd.w, pd.s).hi;
+  }
+  __syncthreads();
+
+  const int q = min(q0 + tid, a.W * 3 - 1);       // columns past the crop are clipped by TMA
+  const int ox = q / 3, ch = q - ox * 3;
+  const AxisTap tx = axis_tap(ox, a.w, a.s);
+  const int xl = (tx.lo - S.wx0[0]) * 3 + ch, xh = (tx.hi - S.wx0[0]) * 3 + ch;
+  AxisTap txp = tx;
+  int pxl = 0, pxh = 0;
+  if (has_prev) {
+    txp = axis_tap(ox, pd.w, pd.s);
+    pxl = (txp.lo - S.wx0[1]) * 3 + ch;
+    pxh = (txp.hi - S.wx0[1]) * 3 + ch;
+  }
+  const int r0 = S.ty_c[0].lo, r1 = S.ty_c[rows - 1].hi;
+  const int pr0 = has_prev ? S.ty_p[0].lo : 0;
+  const int64_t fimg = (int64_t)a.h * a.w * 3;
+  const int z0 = g * kGop;
+  int ci = 0;   // tile-set counter across frames (2 sets rotate)
+  for (int f = 0; f < kGop; ++f) {
+    const bool blend = has_prev && f < kN;
+    if (f > 0) __syncthreads();                   // everyone done with the previous windows
+    load_window(&S.win[0][0][0], a.img + ((int64_t)g * kGop + f) * fimg, a.w, r0, r1,
+                S.wx0[0] * 3, S.wx1[0] * 3 + 3, tid);
+    if (blend)
+      load_window(&S.win[2][0][0], pd.p_img + (int64_t)(kGop - kN + f) * pd.h * pd.w * 3, pd.w,
+                  pr0, S.ty_p[rows - 1].hi, S.wx0[1] * 3, S.wx1[1] * 3 + 3, tid);
+    __syncthreads();
+    int ya = -1, yb = -1, qa = -1, qb = -1;
+    double ia = 0, ib = 0, qva = 0, qvb = 0;
+    for (int c0 = 0; c0 < rows; c0 += kTR, ++ci) {
+      UpTile* tile = tiles + (ci & 1);
+      if (ci >= 2) {
+        if (tid == 0) tma_store_wait_read_1();
+        __syncthreads();
+      }
+      const int cend = min(c0 + kTR, rows);
+      for (int r = c0; r < cend; ++r) {
+        const AxisTap ty = S.ty_c[r];
+        if (ty.lo != ya) {
+          if (ty.lo == yb) ia = ib;
+          else {
+            const float* wi = &S.win[0][ty.lo - r0][0];
+            ia = (double)wi[xl] * tx.g + (double)wi[xh] * tx.f;
+          }
+          ya = ty.lo;
+        }
+        if (ty.hi != yb) {
+          if (ty.hi == ya) ib = ia;
+          else {
+            const float* wi = &S.win[0][ty.hi - r0][0];
+            ib = (double)wi[xl] * tx.g + (double)wi[xh] * tx.f;
+          }
+          yb = ty.hi;
+        }
+        const float ui = (float)clip_hi1(ia * ty.g + ib * ty.f);
+        float v = ui;
+        if (blend) {
+          const AxisTap tp = S.ty_p[r];
+          if (tp.lo != qa) {
+            if (tp.lo == qb) qva = qvb;
+            else {
+              const float* wq = &S.win[2][tp.lo - pr0][0];
+              qva = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
+            }
+            qa = tp.lo;
+          }
+          if (tp.hi != qb) {
+            if (tp.hi == qa) qvb = qva;
+            else {
+              const float* wq = &S.win[2][tp.hi - pr0][0];
+              qvb = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
+            }
+            qb = tp.hi;
+          }
+          const double dq = (double)(float)clip_hi1(qva * tp.g + qvb * tp.f);
+          v = (float)clip_hi1(a.alpha[f] * dq + a.beta[f] * (double)ui);
+        }
+        (*tile)[r - c0][tid] = v;
+      }
+      fence_proxy_async_smem();
+      __syncthreads();
+      if (tid == 0) {
+        tma_store_3d(&omap, &(*tile)[0][0], q0, oy0 + c0, z0 + f);
+        tma_store_commit();
+      }
+    }
+  }
+  if (tid == 0) tma_store_wait_read();
+}
+
 // ---- standalone kernels ----
 template <typename Tin, typename Tout, bool kClip>
 __global__ void k_upscale(const Tin* __restrict__ img, int64_t n, int h, int w, int s, int ch_out,
@@ -479,6 +604,50 @@ extern "C" int sst_upscale_blend(const float* img, int G, int h, int w, int s, i
   k_upscale_blend<<<grid, kUpThreads, 0, st>>>(a);
   SST_LAUNCH_CHECK();
   return SST_OK;
+}
+
+template <int BAND>
+static int launch_k5_9(const CUtensorMap& omap, const UpArgs& a, const SstPrevDesc* prev,
+                       int blend_n, cudaStream_t st) {
+  dim3 grid(ceil_div(a.W * 3, kTQ), ceil_div(a.H, BAND), a.G);
+  if (grid.y > 65535) return SST_ERR_ARG;
+  const int smem = up_tma_smem<BAND, 1>(2);
+  auto kern = k_upscale9_tma<BAND, false, 1>;
+  if (prev) {
+    switch (blend_n) {
+      case 1: kern = k_upscale9_tma<BAND, true, 1>; break;
+      case 2: kern = k_upscale9_tma<BAND, true, 2>; break;
+      case 3: kern = k_upscale9_tma<BAND, true, 3>; break;
+      default: kern = k_upscale9_tma<BAND, true, 4>; break;
+    }
+  }
+  SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<grid, kTQ, smem, st>>>(omap, a);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+extern "C" int sst_upscale_blend9(const float* img, int G, int h, int w, int s, int H, int W,
+                                  const SstPrevDesc* prev, int blend_n, float* out, void* stream) {
+  if (G < 0 || h <= 0 || w <= 0 || H <= 0 || W <= 0) return SST_ERR_ARG;
+  if (s != 2 && s != 3) return SST_ERR_ARG;
+  if (H > h * s || W > w * s) return SST_ERR_ARG;
+  if (blend_n < 1 || blend_n > 8) return SST_ERR_ARG;
+  if (prev && blend_n > 4) return SST_ERR_UNSUPPORTED;
+  if (G == 0) return SST_OK;
+  if (!img || !out || G > 65535) return SST_ERR_ARG;
+  UpArgs a{};
+  a.img = img; a.G = G; a.h = h; a.w = w; a.s = s; a.H = H; a.W = W;
+  a.prev = prev; a.n = blend_n; a.out = out;
+  for (int i = 1; i <= 4; ++i) {
+    a.alpha[i - 1] = (double)(blend_n - i) / (double)blend_n;
+    a.beta[i - 1] = 1.0 - a.alpha[i - 1];
+  }
+  CUtensorMap omap;
+  memset(&omap, 0, sizeof(omap));
+  if (!make_tmap_f32_3d(&omap, out, (uint64_t)W * 3, (uint64_t)H, (uint64_t)G * kGop, kTQ, kTR))
+    return SST_ERR_UNSUPPORTED;   // TMA alignment: W*3*4 bytes must be a multiple of 16
+  return launch_k5_9<32>(omap, a, prev, blend_n, static_cast<cudaStream_t>(stream));
 }
 
 extern "C" int sst_upscale(const float* img, int64_t n, int h, int w, int s, int crop_h, int crop_w,

@@ -331,8 +331,21 @@ class LearnedGopCodec(GopCodec):
         self.idx = torch.empty((g_max, 2, self.Ht, self.Wt, 2), dtype=torch.int32, device=dev)
         self.rx_tok = torch.empty_like(self.tok)
         self.rx_mask = torch.empty_like(self.mask)
-        self.frames9 = torch.empty((g_max, GOP_SIZE, self.h, self.w, 3), dtype=torch.float32,
-                                   device=dev)
+        # double-buffered decoded frames: step k decodes into parity k % 2 while
+        # boundary blending reads the previous step's frames from the other
+        self.frames9 = [torch.empty((g_max, GOP_SIZE, self.h, self.w, 3), dtype=torch.float32,
+                                    device=dev) for _ in range(2)]
+        # SstPrevDesc[g_max] per parity: slot j's previous GoP = slot j of the other buffer
+        self.prev_desc = []
+        for par in range(2):
+            d = np.zeros(g_max, dtype=_lib.PREV_DTYPE)
+            src = self.frames9[1 - par]
+            d["p_img"] = src.data_ptr() + np.arange(g_max, dtype=np.uint64) * np.uint64(
+                src[0].numel() * 4)
+            d["h"], d["w"], d["s"] = self.h, self.w, s
+            self.prev_desc.append(torch.from_numpy(d.view(np.uint8).copy()).to(dev))
+        self.parity = 0
+        self.primed = False
 
     def tokenize(self, frames: torch.Tensor, g: int) -> None:
         tm = self.timer
@@ -370,28 +383,29 @@ class LearnedGopCodec(GopCodec):
         tm.end("K4_reassemble")
         tm.begin("L_decode")
         self.model.decode_tokens(self.rx_tok[:g], self.rx_mask[:g], (self.h, self.w),
-                                 frames=self.frames9[:g])
+                                 frames=self.frames9[parity][:g])
         tm.end("L_decode")
-        return self.frames9[:g]
+        return self.frames9[parity][:g]
 
-    def reconstruct(self, g: int, parity: int, out: torch.Tensor,
-                    prev: torch.Tensor | None = None) -> None:
-        """Upscale the 9 decoded frames of g GoPs to [g, 9, H, W, 3] and blend
-        frames 0..n-1 with ``prev`` (the previous GoPs' output frames, same
-        shape) when given."""
-        st = _dev.stream()
+    def reconstruct(self, g: int, parity: int, out: torch.Tensor, blend: bool = True) -> None:
+        """K5 for 9 distinct frames: upscale frames9[parity][:g] to
+        [g, 9, H, W, 3] and, when ``blend``, mix frames 0..n-1 with the
+        previous step's GoP in the same slot (frames9[1 - parity])."""
         self.timer.begin("K5_upscale_blend")
-        _lib.call("sst_upscale", self.frames9.data_ptr(), g * GOP_SIZE, self.h, self.w, self.s,
-                  self.H, self.W, out.data_ptr(), st)
-        if prev is not None:
-            _lib.call("sst_blend", prev.data_ptr(), out.data_ptr(), g, self.H, self.W,
-                      self.blend_n, out.data_ptr(), st)
+        prev = self.prev_desc[parity].data_ptr() if blend else None
+        _lib.call("sst_upscale_blend9", self.frames9[parity].data_ptr(), g, self.h, self.w,
+                  self.s, self.H, self.W, prev, self.blend_n, out.data_ptr(), _dev.stream())
         self.timer.end("K5_upscale_blend")
 
     def step(self, frames: torch.Tensor, out: torch.Tensor, g: int, drop_k: int = 0,
-             present: torch.Tensor | None = None, prev: torch.Tensor | None = None) -> None:
-        """One pass of the learned codec over g GoPs: sender then receiver."""
+             present: torch.Tensor | None = None) -> None:
+        """One GoP of each of g streams (slot j = stream j) through the learned
+        codec: sender, then receiver; from the second step on, frames 0..n-1
+        blend with the stream's previous GoP (codec.py:278-296)."""
+        par = self.parity
         self.tokenize(frames, g)
         self.select_and_pack(g, drop_k)
-        self.decode(g, 0, present=present)
-        self.reconstruct(g, 0, out, prev)
+        self.decode(g, par, present=present)
+        self.reconstruct(g, par, out, blend=self.primed)
+        self.parity ^= 1
+        self.primed = True

@@ -293,19 +293,28 @@ def test_learned_gop_codec_stages_bit_exact():
     blend."""
     from paper_2602_03529_b200.learned import LearnedGopCodec
 
-    H, W, s, g = 72, 100, 2, 2
+    H, W, s, g = 72, 100, 2, 2       # W*3*4 % 16 == 0 for the TMA store
     cfg = LearnedConfig(dim=128, blocks=1, seed=4)
     codec = LearnedGopCodec(g, H, W, s, cfg=cfg)
     clip = make_clip("moving-square", W, H, 18, seed=2)
     fr = np.stack([clip.gop(0), clip.gop(1)])
     dev = _dev.device()
     frames = torch.from_numpy(fr).to(dev)
-    codec.set_gop_ids([7, 8])
     drop_k = codec.drop_k(0.25)
     out = torch.empty_like(frames)
-    prev = torch.rand_like(frames)
-    codec.step(frames, out, g, drop_k=drop_k, prev=prev)
+    # step 1 primes the blend history with a different GoP pair
+    frames0 = torch.from_numpy(np.stack([clip.gop(1), clip.gop(0)])).to(dev)
+    out0 = torch.empty_like(frames0)
+    codec.set_gop_ids([5, 6])
+    codec.step(frames0, out0, g, drop_k=drop_k)
+    prev9 = codec.frames9[0][:g].cpu().numpy()
+    codec.set_gop_ids([7, 8])
+    codec.step(frames, out, g, drop_k=drop_k)
     torch.cuda.synchronize()
+    # first step: no blend
+    for j in range(g):
+        want0 = np.stack([O.upscale(prev9[j, t], s, crop=(H, W)) for t in range(9)])
+        assert np.array_equal(out0[j].cpu().numpy(), want0)
     codes, _, _, hw = codec.model.encode_frames(frames, s)
     codes = codes.cpu().numpy()
     arena, lengths = codec.arena.cpu().numpy(), codec.lengths.cpu().numpy()
@@ -329,10 +338,10 @@ def test_learned_gop_codec_stages_bit_exact():
     assert np.array_equal(codec.rx_tok[:g].cpu().numpy(), rx)
     assert np.array_equal(codec.rx_mask[:g].cpu().numpy(), rxm)
     dec = codec.model.decode_tokens(_dev.h2d(rx, np.float64), _dev.h2d(rxm, np.uint8), hw)
-    assert torch.equal(dec, codec.frames9[:g])
+    assert torch.equal(dec, codec.frames9[1][:g])
     d9 = dec.cpu().numpy()
-    pv_ = prev.cpu().numpy()
     for j in range(g):
         up = [O.upscale(d9[j, t], s, crop=(H, W)) for t in range(9)]
-        want = O.blend(list(pv_[j]), up, 2)
+        prev_up = [O.upscale(prev9[j, t], s, crop=(H, W)) for t in range(9)]
+        want = O.blend(prev_up, up, 2)
         assert np.array_equal(out[j].cpu().numpy(), np.stack(want))
