@@ -152,6 +152,9 @@ SST_API int sst_decode(const double* i_tok, const double* p_tok, int64_t tok_str
 /* token_similarity (selection.py:33-52) for n token pairs with C channels. */
 SST_API int sst_similarity(const double* p, const double* i, int64_t n, int C, double* sim, void* stream);
 
+/* token_similarity for a GoP batch: tok [G][2][n][C] (I then P), sim [G][n]. */
+SST_API int sst_similarity_gop(const double* tok, int G, int64_t n, int C, double* sim, void* stream);
+
 /* top_k_drop_mask (selection.py:55-67): per map g, mark the k[g] largest
  * similarities (ties: lower row-major index first).  k is a DEVICE int32[G];
  * kth (DEVICE double[G] or NULL) receives the k-th largest value. */

@@ -30,12 +30,16 @@ __device__ double np_sum(const double* x, int n) {
 
 constexpr int kMaxSimC = 128;
 
+// blockIdx.y = GoP g of a [G][2][n][C] token batch (pair stride gs doubles,
+// sim stride n); gs = 0 for a single pair of matrices
 __global__ void k_similarity(const double* __restrict__ p, const double* __restrict__ iv,
-                             int64_t n, int C, double* __restrict__ sim) {
+                             int64_t n, int C, double* __restrict__ sim, int64_t gs) {
   int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= n) return;
-  const double* pp = p + t * C;
-  const double* ii = iv + t * C;
+  const int64_t g = blockIdx.y;
+  sim += g * n;
+  const double* pp = p + g * gs + t * C;
+  const double* ii = iv + g * gs + t * C;
   double a[kMaxSimC];
   for (int k = 0; k < C; ++k) a[k] = pp[k] * ii[k];
   double dot = np_sum(a, C);
@@ -208,7 +212,21 @@ extern "C" int sst_similarity(const double* p, const double* i, int64_t n, int C
   if (C > kMaxSimC) return SST_ERR_UNSUPPORTED;
   int threads = 128;
   k_similarity<<<(unsigned)ceil_div64(n, threads), threads, 0, static_cast<cudaStream_t>(stream)>>>(
-      p, i, n, C, sim);
+      p, i, n, C, sim, 0);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+extern "C" int sst_similarity_gop(const double* tok, int G, int64_t n, int C, double* sim,
+                                  void* stream) {
+  if (G < 0 || n < 0 || C < 0 || G > 65535) return SST_ERR_ARG;
+  if (G == 0 || n == 0) return SST_OK;
+  if (!tok || !sim) return SST_ERR_ARG;
+  if (C > kMaxSimC) return SST_ERR_UNSUPPORTED;
+  int threads = 128;
+  dim3 grid((unsigned)ceil_div64(n, threads), G);
+  k_similarity<<<grid, threads, 0, static_cast<cudaStream_t>(stream)>>>(tok + n * C, tok, n, C, sim,
+                                                                       2 * n * C);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }

@@ -353,6 +353,37 @@ __global__ void __launch_bounds__(kTQ)
   if (tid == 0) tma_store_wait_read();
 }
 
+// Window rows/columns striped over the CTA's threads, held in registers
+// between fetch() (global loads issued) and commit() (shared stores).
+template <int kPF>
+struct WinFetch {
+  float v[kPF];
+  int ncol, total, tid;
+  __device__ __forceinline__ void setup(int nrow, int nc, int t) {
+    ncol = nc; total = nrow * nc; tid = t;
+  }
+  __device__ __forceinline__ void fetch(const float* img, int w, int row0, int c0f) {
+#pragma unroll
+    for (int i = 0; i < kPF; ++i) {
+      const int e = tid + i * kTQ;
+      if (e < total) {
+        const int r = e / ncol, c = e - r * ncol;
+        v[i] = __ldg(img + ((int64_t)(row0 + r) * w) * 3 + c0f + c);
+      }
+    }
+  }
+  __device__ __forceinline__ void commit(float* win) const {
+#pragma unroll
+    for (int i = 0; i < kPF; ++i) {
+      const int e = tid + i * kTQ;
+      if (e < total) {
+        const int r = e / ncol, c = e - r * ncol;
+        win[r * kWF + c] = v[i];
+      }
+    }
+  }
+};
+
 // ---- K5 for 9 distinct frames (learned decoder output) ----
 // Same band / window / TMA-store scheme as k_upscale_blend_tma, but every
 // frame of the GoP has its own working image: the CTA walks the 9 frames of
@@ -361,7 +392,7 @@ __global__ void __launch_bounds__(kTQ)
 // from that GoP's working frames (prev[g].p_img = its [9][h][w][3] block):
 // for n <= 4 those tail frames are unblended reconstructions, so recomputing
 // them is exact and saves reading two full-resolution frames.
-template <int kBand, bool kPrev, int kN>
+template <int kBand, bool kPrev, int kN, int kSlots, bool kPre>
 __global__ void __launch_bounds__(kTQ)
     k_upscale9_tma(const __grid_constant__ CUtensorMap omap, const __grid_constant__ UpArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -402,25 +433,45 @@ __global__ void __launch_bounds__(kTQ)
     pxh = (txp.hi - S.wx0[1]) * 3 + ch;
   }
   const int r0 = S.ty_c[0].lo, r1 = S.ty_c[rows - 1].hi;
-  const int pr0 = has_prev ? S.ty_p[0].lo : 0;
+  const int pr0 = has_prev ? S.ty_p[0].lo : 0, pr1 = has_prev ? S.ty_p[rows - 1].hi : 0;
   const int64_t fimg = (int64_t)a.h * a.w * 3;
+  const int64_t pimg = (int64_t)pd.h * pd.w * 3;
+  const float* cur_base = a.img + (int64_t)g * kGop * fimg;
   const int z0 = g * kGop;
-  int ci = 0;   // tile-set counter across frames (2 sets rotate)
+  // register prefetch of the next frame's source windows: the loads for
+  // frame f+1 are in flight while frame f is interpolated and stored
+  constexpr int kPF = ((kBand / 2 + 2) * kWF + kTQ - 1) / kTQ;
+  WinFetch<kPF> fc, fp;
+  fc.setup(r1 - r0 + 1, (S.wx1[0] - S.wx0[0] + 1) * 3, tid);
+  if (has_prev) fp.setup(pr1 - pr0 + 1, (S.wx1[1] - S.wx0[1] + 1) * 3, tid);
+  if (kPre) {
+    fc.fetch(cur_base, a.w, r0, S.wx0[0] * 3);
+    if (has_prev) fp.fetch(pd.p_img + (int64_t)(kGop - kN) * pimg, pd.w, pr0, S.wx0[1] * 3);
+  }
+  int ci = 0;   // tile counter across frames (kSlots tiles rotate)
   for (int f = 0; f < kGop; ++f) {
     const bool blend = has_prev && f < kN;
     if (f > 0) __syncthreads();                   // everyone done with the previous windows
-    load_window(&S.win[0][0][0], a.img + ((int64_t)g * kGop + f) * fimg, a.w, r0, r1,
-                S.wx0[0] * 3, S.wx1[0] * 3 + 3, tid);
-    if (blend)
-      load_window(&S.win[2][0][0], pd.p_img + (int64_t)(kGop - kN + f) * pd.h * pd.w * 3, pd.w,
-                  pr0, S.ty_p[rows - 1].hi, S.wx0[1] * 3, S.wx1[1] * 3 + 3, tid);
+    if (kPre) {
+      fc.commit(&S.win[0][0][0]);
+      if (blend) fp.commit(&S.win[2][0][0]);
+    } else {
+      load_window(&S.win[0][0][0], cur_base + (int64_t)f * fimg, a.w, r0, r1, S.wx0[0] * 3,
+                  S.wx1[0] * 3 + 3, tid);
+      if (blend)
+        load_window(&S.win[2][0][0], pd.p_img + (int64_t)(kGop - kN + f) * pimg, pd.w, pr0, pr1,
+                    S.wx0[1] * 3, S.wx1[1] * 3 + 3, tid);
+    }
     __syncthreads();
+    if (kPre && f + 1 < kGop) fc.fetch(cur_base + (int64_t)(f + 1) * fimg, a.w, r0, S.wx0[0] * 3);
+    if (kPre && has_prev && f + 1 < kN)
+      fp.fetch(pd.p_img + (int64_t)(kGop - kN + f + 1) * pimg, pd.w, pr0, S.wx0[1] * 3);
     int ya = -1, yb = -1, qa = -1, qb = -1;
     double ia = 0, ib = 0, qva = 0, qvb = 0;
     for (int c0 = 0; c0 < rows; c0 += kTR, ++ci) {
-      UpTile* tile = tiles + (ci & 1);
-      if (ci >= 2) {
-        if (tid == 0) tma_store_wait_read_1();
+      UpTile* tile = tiles + (ci % kSlots);
+      if (ci >= kSlots) {
+        if (tid == 0) tma_store_wait_read_n<kSlots - 1>();
         __syncthreads();
       }
       const int cend = min(c0 + kTR, rows);
@@ -606,19 +657,19 @@ extern "C" int sst_upscale_blend(const float* img, int G, int h, int w, int s, i
   return SST_OK;
 }
 
-template <int BAND>
+template <int BAND, int SLOTS, bool PRE>
 static int launch_k5_9(const CUtensorMap& omap, const UpArgs& a, const SstPrevDesc* prev,
                        int blend_n, cudaStream_t st) {
   dim3 grid(ceil_div(a.W * 3, kTQ), ceil_div(a.H, BAND), a.G);
   if (grid.y > 65535) return SST_ERR_ARG;
-  const int smem = up_tma_smem<BAND, 1>(2);
-  auto kern = k_upscale9_tma<BAND, false, 1>;
+  const int smem = up_tma_smem<BAND, 1>(SLOTS);
+  auto kern = k_upscale9_tma<BAND, false, 1, SLOTS, PRE>;
   if (prev) {
     switch (blend_n) {
-      case 1: kern = k_upscale9_tma<BAND, true, 1>; break;
-      case 2: kern = k_upscale9_tma<BAND, true, 2>; break;
-      case 3: kern = k_upscale9_tma<BAND, true, 3>; break;
-      default: kern = k_upscale9_tma<BAND, true, 4>; break;
+      case 1: kern = k_upscale9_tma<BAND, true, 1, SLOTS, PRE>; break;
+      case 2: kern = k_upscale9_tma<BAND, true, 2, SLOTS, PRE>; break;
+      case 3: kern = k_upscale9_tma<BAND, true, 3, SLOTS, PRE>; break;
+      default: kern = k_upscale9_tma<BAND, true, 4, SLOTS, PRE>; break;
     }
   }
   SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -647,7 +698,15 @@ extern "C" int sst_upscale_blend9(const float* img, int G, int h, int w, int s, 
   memset(&omap, 0, sizeof(omap));
   if (!make_tmap_f32_3d(&omap, out, (uint64_t)W * 3, (uint64_t)H, (uint64_t)G * kGop, kTQ, kTR))
     return SST_ERR_UNSUPPORTED;   // TMA alignment: W*3*4 bytes must be a multiple of 16
-  return launch_k5_9<32>(omap, a, prev, blend_n, static_cast<cudaStream_t>(stream));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // A/B switch for profiling: SST_K5_9=6 (six store tiles: fewer CTAs per
+  // SM), "p" suffix = register prefetch of the next frame's window.  Measured
+  // at 32 x 1080p GoPs: 2 tiles / no prefetch 3.15 ms, 2p 4.17, 6 5.02, 6p 6.77.
+  const char* v = getenv("SST_K5_9");
+  if (v && v[0] == '6') return v[1] == 'p' ? launch_k5_9<32, 6, true>(omap, a, prev, blend_n, st)
+                                           : launch_k5_9<32, 6, false>(omap, a, prev, blend_n, st);
+  if (v && v[1] == 'p') return launch_k5_9<32, 2, true>(omap, a, prev, blend_n, st);
+  return launch_k5_9<32, 2, false>(omap, a, prev, blend_n, st);
 }
 
 extern "C" int sst_upscale(const float* img, int64_t n, int h, int w, int s, int crop_h, int crop_w,

@@ -354,12 +354,8 @@ class LearnedGopCodec(GopCodec):
                                  idx=self.idx[:g])
         tm.end("L_encode")
         tm.begin("L_similarity")
-        n, st = self.n, _dev.stream()
-        stride = 2 * n * CHANNELS * 8
-        base = self.tok.data_ptr()
-        for j in range(g):
-            _lib.call("sst_similarity", base + j * stride + n * CHANNELS * 8, base + j * stride,
-                      n, CHANNELS, self.sim.data_ptr() + j * n * 8, st)
+        _lib.call("sst_similarity_gop", self.tok.data_ptr(), g, self.n, CHANNELS,
+                  self.sim.data_ptr(), _dev.stream())
         tm.end("L_similarity")
 
     def decode(self, g: int, parity: int, arena: torch.Tensor | None = None,
