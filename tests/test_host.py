@@ -152,3 +152,20 @@ def test_public_names_mirror_reference_hot_path():
         for n in names:
             assert hasattr(mod, n), n
     assert issubclass(T.PacketFormatError, ValueError)
+
+
+def test_residual_packet_header_roundtrip():
+    """Stream-file residual packets (transport.py:116-127,186-194): host-side
+    header + CRC framing round trip and validation."""
+    from paper_2602_03529_b200 import streamfile as SF
+    pkt = SF.ResidualPacket(gop_id=7, theta=0.02, quant_step=1 / 127, window_length=9,
+                            payload=b"\x01\x02\x03")
+    data = pkt.to_bytes()
+    assert data[:4] == b"\x4d\x53\x01\x02" and len(data) == 22 + 3 + 4
+    back = SF._parse_residual(data)
+    assert back.gop_id == 7 and back.window_length == 9 and back.payload == b"\x01\x02\x03"
+    bad = bytearray(data)
+    bad[-5] ^= 1
+    import pytest as _pt
+    with _pt.raises(ValueError, match="crc"):
+        SF._parse_residual(bytes(bad))
