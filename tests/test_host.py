@@ -161,7 +161,7 @@ def test_residual_packet_header_roundtrip():
     pkt = SF.ResidualPacket(gop_id=7, theta=0.02, quant_step=1 / 127, window_length=9,
                             payload=b"\x01\x02\x03")
     data = pkt.to_bytes()
-    assert data[:4] == b"\x4d\x53\x01\x02" and len(data) == 22 + 3 + 4
+    assert data[:4] == b"\x4d\x53\x01\x02" and len(data) == 21 + 3 + 4   # >HBBIffBI = 21 B
     back = SF._parse_residual(data)
     assert back.gop_id == 7 and back.window_length == 9 and back.payload == b"\x01\x02\x03"
     bad = bytearray(data)
