@@ -314,7 +314,7 @@ def run_ours(a, rank, world, local_rank):
     # Per-kernel roofline: a few extra steps with the lanes serialised on one
     # stream so that every kernel's CUDA-event duration is its own (in the
     # timed run the two lanes overlap and each kernel shares the HBM).
-    timer = StageTimer()
+    timer = StageTimer(lead_cycles=2_000_000)     # ~1 ms spin ahead of every stage
     bank.set_timer(timer)
     for k in range(a.warmup + a.steps, a.warmup + a.steps + a.roofline_steps):
         fr = inputs[k % 2]

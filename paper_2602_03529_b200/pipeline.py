@@ -38,11 +38,17 @@ def _cdiv(a: int, b: int) -> int:
 class StageTimer:
     """CUDA-event timing of each kernel stage on the launching (current) stream."""
 
-    def __init__(self):
+    def __init__(self, lead_cycles: int = 0):
         self.pairs: dict = {}
         self._open: dict = {}
+        # lead_cycles > 0: enqueue a GPU spin of that many cycles before each
+        # begin event so the host runs ahead and the event pair brackets the
+        # kernel alone (no launch / host gap inside the measured interval)
+        self.lead_cycles = lead_cycles
 
     def begin(self, name: str) -> None:
+        if self.lead_cycles:
+            torch.cuda._sleep(self.lead_cycles)
         ev = torch.cuda.Event(enable_timing=True)
         ev.record()
         self._open[name] = ev
