@@ -670,11 +670,15 @@ def run_learned(a, device) -> dict:
         times.append((name, len(taps), b0, b1, flops))
 
     model._conv = timed
+    l0 = model.launches
     try:
         step(1)
         torch.cuda.synchronize()
     finally:
         model._conv = orig
+    # tokenizer kernels (convs, patchify, decoder input) + similarity, top-k,
+    # packetize, parse, 4 reassembly kernels, K5-9
+    launches_step = (model.launches - l0) + (1 if drop_k else 0) + 8
     per = [(n, nt, b0.elapsed_time(b1), fl) for n, nt, b0, b1, fl in times]
     halo = [(ms_, fl) for n, nt, ms_, fl in per if nt == 18 and model.W[n].shape[0] % 256 == 0]
     conv_ms = sum(ms_ for _, _, ms_, _ in per)
@@ -694,7 +698,7 @@ def run_learned(a, device) -> dict:
                      "avg_launch_ms": round(sum(m for m, _ in halo) / len(halo), 4),
                      "launches_per_step": len(halo)},
         "conv_share_of_serialised_step": round(conv_ms / max(ms, 1e-9), 3),
-        "gpu_launches_per_step": len(per) + 4 + G,
+        "gpu_launches_per_step": launches_step,
         "dtype": "bf16 operands, fp32 accumulate (TMEM)",
         "parity": "tests/test_gpu_learned.py vs oracle/learned_oracle.py (torch fp32, unpinned)",
     }
