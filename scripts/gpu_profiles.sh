@@ -3,7 +3,7 @@
 #   2. --set full capture of one launch of each pipeline kernel
 mkdir -p gpurun_out
 TAG=${1:-r01}
-B="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
+B="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-learned"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_ --csv \
     --log-file gpurun_out/${TAG}_launches.csv $B > gpurun_out/${TAG}_launches.log 2>&1
 echo "launches rc=$?"
