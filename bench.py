@@ -68,6 +68,7 @@ def parse_args():
     ap.add_argument("--no-learned", action="store_true",
                     help="skip the learned-tokenizer leg (SURVEY f4, tensor-core path)")
     ap.add_argument("--learned-gops", type=int, default=32)
+    ap.add_argument("--learned-lanes", type=int, default=1)
     ap.add_argument("--roofline-steps", type=int, default=3,
                     help="extra serialised steps timing each kernel alone")
     return ap.parse_args()
@@ -634,29 +635,57 @@ def run_learned(a, device) -> dict:
     from paper_2602_03529_b200.learned import LearnedConfig, LearnedGopCodec
     G, s, H, W = a.learned_gops, 3, a.height, a.width
     cfg = LearnedConfig()
-    codec = LearnedGopCodec(G, H, W, s, cfg=cfg)
+    codec = LearnedGopCodec(G, H, W, s, cfg=cfg)        # full batch: serialised roofline pass
+    model = codec.model
     gen = torch.Generator(device=device).manual_seed(0)
     frames = [torch.rand((G, GOP, H, W, 3), generator=gen, device=device) for _ in range(2)]
     outs = [torch.empty_like(frames[0]) for _ in range(2)]
     drop_k = codec.drop_k(a.drop)
     codec.set_gop_ids(list(range(G)))
+    # timed run: the batch split into lanes on their own CUDA streams (one
+    # model, shared weights) so one lane's tensor-bound convolutions overlap
+    # the other lane's HBM-bound patchify / reconstruction
+    nl = max(1, a.learned_lanes)
+    cuts = [G * j // nl for j in range(nl + 1)]
+    lanes = []
+    for j in range(nl):
+        n = cuts[j + 1] - cuts[j]
+        c = LearnedGopCodec(n, H, W, s, model=model)
+        c.set_gop_ids(list(range(cuts[j], cuts[j + 1])))
+        lanes.append(dict(codec=c, sl=slice(cuts[j], cuts[j + 1]), n=n,
+                          stream=torch.cuda.Stream(device=device)))
 
     def step(k):
         codec.step(frames[k % 2], outs[k % 2], G, drop_k=drop_k)
 
+    def lanes_step(k):
+        for ln in lanes:
+            with torch.cuda.stream(ln["stream"]):
+                ln["codec"].step(frames[k % 2][ln["sl"]], outs[k % 2][ln["sl"]], ln["n"],
+                                 drop_k=drop_k)
+
+    main = torch.cuda.current_stream()
+    for ln in lanes:
+        ln["stream"].wait_stream(main)
     for k in range(max(a.warmup, 3)):
-        step(k)
+        lanes_step(k)
+    for ln in lanes:
+        main.wait_stream(ln["stream"])
+    step(0)
     torch.cuda.synchronize()
     K = max(a.steps // 2, 5)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
+    for ln in lanes:
+        ln["stream"].wait_stream(main)
     for k in range(K):
-        step(k + 1)
+        lanes_step(k + 1)
+    for ln in lanes:
+        main.wait_stream(ln["stream"])
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / K
-    # serialised pass: time every conv launch on its stream
-    model = codec.model
+    # serialised pass (full batch, one stream): time every conv launch
     times = []
     orig = model._conv
 
@@ -686,6 +715,7 @@ def run_learned(a, device) -> dict:
     achieved = sum(fl for _, fl in halo) / sum(m for m, _ in halo) / 1e9
     flops_step = model.flops_per_gop(codec.Ht, codec.Wt) * G
     return {
+        "lanes": nl,
         "workload": f"{G} x 1080p GoPs per step, s=3, learned causal conv tokenizer "
                     f"(D={cfg.dim}, {cfg.blocks} residual blocks per side, FSQ 2x(8,8,8,5,5,5)), "
                     f"{int(a.drop * 100)}% intelligent drop, blend n=2; random-init weights",

@@ -438,6 +438,196 @@ __global__ void __launch_bounds__(c233::THREADS, 1)
   if (warp == 1) tc::tmem_dealloc(tmem, 512);
 }
 
+// ---- persistent, warp-specialised causal (2,3,3) convolution ---------------
+// Work unit = 256 tokens (16x16 tile) x 128 output channels; units are dealt
+// round-robin to one persistent CTA per SM (2 N-halves per tile double the
+// number of units, so the tail wave is ~1/13 instead of ~1/2 of a wave).
+// Roles: warp 0 lane 0 = TMA producer (halos + weight k-blocks, running ahead
+// across units), warp 1 lane 0 = MMA issuer, warps 2..9 = epilogue.  The two
+// M=128 accumulators of a unit take 256 TMEM columns; units alternate between
+// columns 0..255 and 256..511, so the epilogue of unit i (tcgen05.ld, bias,
+// SiLU, residual, bf16 stores) runs while the MMAs of unit i+1 issue.
+namespace c233p {
+constexpr int TILE = 16, PITCH = 18, HROWS = 18;
+constexpr int HALO_BYTES = PITCH * HROWS * 128;
+constexpr int HALO_STRIDE = (HALO_BYTES + 1023) / 1024 * 1024;
+constexpr int BN = 128;
+constexpr int B_BYTES = BN * 128;
+constexpr int HSLOTS = 2, BSTAGES = 8;
+constexpr int SMEM = HSLOTS * HALO_STRIDE + BSTAGES * B_BYTES + 1024 + 512;
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 64 + EPI_WARPS * 32;
+}  // namespace c233p
+
+__global__ void __launch_bounds__(c233p::THREADS, 1)
+    k_lt_conv233p(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  const ConvArgs a, int n_units, int n_halves) {
+  using namespace c233p;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sH = smem;
+  uint8_t* sB = smem + HSLOTS * HALO_STRIDE;
+  uint64_t* hfull = reinterpret_cast<uint64_t*>(sB + BSTAGES * B_BYTES);
+  uint64_t* hempty = hfull + HSLOTS;
+  uint64_t* bfull = hempty + HSLOTS;
+  uint64_t* bempty = bfull + BSTAGES;
+  uint64_t* afull = bempty + BSTAGES;    // [2] accumulator ready (MMA -> epilogue)
+  uint64_t* aempty = afull + 2;          // [2] accumulator drained (epilogue -> MMA)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    tc::prefetch_tmap(&tmA);
+    tc::prefetch_tmap(&tmB);
+    for (int i = 0; i < HSLOTS; ++i) { mbar_init(&hfull[i], 1); mbar_init(&hempty[i], 1); }
+    for (int i = 0; i < BSTAGES; ++i) { mbar_init(&bfull[i], 1); mbar_init(&bempty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&afull[i], 1); mbar_init(&aempty[i], EPI_WARPS); }
+    fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc(tmem_slot, 512);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  const int nh = 2 * a.kb_per_tap;   // halos per unit: (temporal tap, channel block)
+  const int C = a.kb_per_tap * BK;
+  auto decode = [&](int u, int& g, int& t, int& x0, int& y0, int& n0) {
+    int tile = u / n_halves;
+    n0 = (u - tile * n_halves) * BN;
+    const int tx = tile % a.tiles_x; tile /= a.tiles_x;
+    const int ty = tile % a.tiles_y; tile /= a.tiles_y;
+    t = a.t_lo + tile % a.t_cnt;
+    g = tile / a.t_cnt;
+    x0 = tx * TILE; y0 = ty * TILE;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer ----
+      int hc = 0, bc = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+        int g, t, x0, y0, n0;
+        decode(u, g, t, x0, y0, n0);
+        for (int hi = 0; hi < nh; ++hi, ++hc) {
+          const int kt = hi / a.kb_per_tap, cb = hi - kt * a.kb_per_tap;
+          const int hs = hc % HSLOTS;
+          if (hc >= HSLOTS) mbar_wait(&hempty[hs], ((hc / HSLOTS) - 1) & 1);
+          mbar_expect_tx(&hfull[hs], HALO_BYTES);
+          tc::tma_load_5d(sH + hs * HALO_STRIDE, &tmA, cb * BK, x0 - 1, y0 - 1, t + kt - 1, g,
+                          &hfull[hs]);
+          for (int sp = 0; sp < 9; ++sp, ++bc) {
+            const int bs = bc % BSTAGES;
+            if (bc >= BSTAGES) mbar_wait(&bempty[bs], ((bc / BSTAGES) - 1) & 1);
+            mbar_expect_tx(&bfull[bs], B_BYTES);
+            tc::tma_load_2d(sB + bs * B_BYTES, &tmB, (kt * 9 + sp) * C + cb * BK, n0, &bfull[bs]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---- MMA issuer ----
+      constexpr uint32_t idesc = tc::idesc_bf16_f32(128, BN);
+      int hc = 0, bc = 0, it = 0;
+      for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
+        const int ab = it & 1;
+        if (it >= 2) mbar_wait(&aempty[ab], ((it >> 1) - 1) & 1);
+        tc::fence_after_sync();
+        const uint32_t acc = tmem + ab * 256;
+        for (int hi = 0; hi < nh; ++hi, ++hc) {
+          const int hs = hc % HSLOTS;
+          mbar_wait(&hfull[hs], (hc / HSLOTS) & 1);
+          const uint32_t hbase = smem_u32(sH + hs * HALO_STRIDE);
+          for (int sp = 0; sp < 9; ++sp, ++bc) {
+            const int bs = bc % BSTAGES;
+            mbar_wait(&bfull[bs], (bc / BSTAGES) & 1);
+            tc::fence_after_sync();
+            const int dy = sp / 3, dx = sp % 3;
+            const uint64_t bd = tc::smem_desc_sw128(smem_u32(sB + bs * B_BYTES));
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+              const uint64_t ad = halo_desc(hbase + (uint32_t)((dy * PITCH + dx + 8 * half) * 128));
+#pragma unroll
+              for (int k = 0; k < BK / 16; ++k)
+                tc::mma_bf16(acc + half * BN, ad + 2 * k, bd + 2 * k, idesc, (hi | sp | k) != 0);
+            }
+            tc::mma_commit(&bempty[bs]);
+          }
+          tc::mma_commit(&hempty[hs]);
+        }
+        tc::mma_commit(&afull[ab]);
+      }
+    }
+  } else {
+    // ---- epilogue warps: warp w drains half (w-2)/4, TMEM lanes 32*(w%4) ----
+    const int e = warp - 2;
+    const int half = e >> 2, q = warp & 3;
+    const int m = q * 32 + lane;
+    int it = 0;
+    for (int u = blockIdx.x; u < n_units; u += gridDim.x, ++it) {
+      int g, t, x0, y0, n0;
+      decode(u, g, t, x0, y0, n0);
+      const int ab = it & 1;
+      mbar_wait(&afull[ab], (it >> 1) & 1);
+      tc::fence_after_sync();
+      const int y = y0 + (m >> 3), x = x0 + half * 8 + (m & 7);
+      const bool valid = y < a.Ht && x < a.Wt;
+      const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + ab * 256 + half * BN;
+      const size_t tok = (((size_t)g * a.out_T + t) * a.Ht + y) * a.Wt + x;
+      __nv_bfloat16* outp = reinterpret_cast<__nv_bfloat16*>(a.frames) + tok * a.N + n0;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tc::tmem_ld32(trow + c, v);
+        if (c + 32 == BN) {
+          // last TMEM read of this accumulator by this warp: release it early
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&aempty[ab]);
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          v[i] += __ldg(a.bias + n0 + c + i);
+          if (a.act) v[i] = silu(v[i]);
+        }
+        if (!valid) continue;
+        if (a.residual != nullptr) {
+          const uint4* rp = reinterpret_cast<const uint4*>(a.residual + tok * a.N + n0 + c);
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            uint4 uu = __ldg(rp + qq);
+            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&uu);
+#pragma unroll
+            for (int e2 = 0; e2 < 4; ++e2) {
+              float2 f = __bfloat1622float2(h2[e2]);
+              v[qq * 8 + 2 * e2] += f.x;
+              v[qq * 8 + 2 * e2 + 1] += f.y;
+            }
+          }
+        }
+        uint4* op = reinterpret_cast<uint4*>(outp + c);
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+          uint4 uu;
+          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&uu);
+#pragma unroll
+          for (int e2 = 0; e2 < 4; ++e2)
+            h2[e2] = __floats2bfloat162_rn(v[qq * 8 + 2 * e2], v[qq * 8 + 2 * e2 + 1]);
+          op[qq] = uu;
+        }
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) {
+    __syncwarp();
+    tc::tmem_dealloc(tmem, 512);
+  }
+}
+
 // ---- downscale + pad + patchify --------------------------------------------
 template <int S>
 __global__ void k_lt_patchify(const float* __restrict__ src, int G, int H, int W, int h, int w,
@@ -564,6 +754,49 @@ static bool is_taps233(const SstConvDesc* d) {
   return true;
 }
 
+static int launch_conv233p(const SstConvDesc* d, cudaStream_t st) {
+  if (d->N % c233p::BN != 0 || d->t_lo != 0 || d->t_cnt != d->in_T || d->in_T != d->out_T ||
+      d->in_W != d->Wt || d->in_H != d->Ht)
+    return SST_ERR_ARG;
+  CUtensorMap tmA, tmB;
+  memset(&tmA, 0, sizeof(tmA));
+  memset(&tmB, 0, sizeof(tmB));
+  const uint64_t adims[5] = {(uint64_t)d->in_C, (uint64_t)d->in_W, (uint64_t)d->in_H,
+                             (uint64_t)d->in_T, (uint64_t)d->G};
+  if (!make_tmap_bf16_5d(&tmA, d->in, adims, c233p::PITCH, c233p::HROWS)) return SST_ERR_ARG;
+  if (!make_tmap_bf16_2d(&tmB, d->weight, (uint64_t)d->K, (uint64_t)d->N, c233p::BN))
+    return SST_ERR_ARG;
+  ConvArgs a;
+  memset(&a, 0, sizeof(a));
+  a.Ht = d->Ht; a.Wt = d->Wt;
+  a.tiles_x = ceil_div(d->Wt, c233p::TILE);
+  a.tiles_y = ceil_div(d->Ht, c233p::TILE);
+  a.t_lo = 0; a.t_cnt = d->t_cnt;
+  a.n_taps = 18;
+  a.kb_per_tap = d->in_C / BK;
+  a.N = d->N;
+  a.out_T = d->out_T;
+  a.bias = d->bias;
+  a.act = d->act;
+  a.residual = static_cast<const __nv_bfloat16*>(d->residual);
+  a.frames = static_cast<float*>(d->out);   // carries the bf16 output pointer
+  const int n_halves = d->N / c233p::BN;
+  const int64_t units = (int64_t)d->G * d->t_cnt * a.tiles_y * a.tiles_x * n_halves;
+  if (units <= 0 || units > 0x7fffffff) return SST_ERR_ARG;
+  static int n_sm = 0;
+  if (n_sm == 0) {
+    int dev = 0;
+    SST_CUDA_TRY(cudaGetDevice(&dev));
+    SST_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int grid = (int)(units < n_sm ? units : n_sm);
+  SST_CUDA_TRY(cudaFuncSetAttribute(k_lt_conv233p, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    c233p::SMEM));
+  k_lt_conv233p<<<grid, c233p::THREADS, c233p::SMEM, st>>>(tmA, tmB, a, (int)units, n_halves);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
 static int launch_conv233(const SstConvDesc* d, cudaStream_t st) {
   if (d->N % c233::BN != 0 || d->t_lo != 0 || d->t_cnt != d->in_T || d->in_T != d->out_T ||
       d->in_W != d->Wt || d->in_H != d->Ht)
@@ -618,10 +851,13 @@ extern "C" int sst_lt_conv(const SstConvDesc* d, void* stream) {
   switch (d->epi) {
     case SST_LT_EPI_STORE: {
       if (!d->out || d->act < 0 || d->act > 1) return SST_ERR_ARG;
-      // SST_LT_CONV=generic forces the per-tap kernel (A/B comparisons)
+      // SST_LT_CONV=generic forces the per-tap kernel, =halo the
+      // non-persistent halo kernel (A/B comparisons)
       const char* mode = getenv("SST_LT_CONV");
       const bool generic = mode && mode[0] == 'g';
-      if (!generic && lt::is_taps233(d) && d->N % lt::c233::BN == 0) return lt::launch_conv233(d, st);
+      const bool halo1 = mode && mode[0] == 'h';
+      if (!generic && lt::is_taps233(d) && d->N % lt::c233::BN == 0)
+        return halo1 ? lt::launch_conv233(d, st) : lt::launch_conv233p(d, st);
       return lt::launch_conv<128, SST_LT_EPI_STORE>(d, st);
     }
     case SST_LT_EPI_FSQ:
