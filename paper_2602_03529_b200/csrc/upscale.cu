@@ -703,14 +703,30 @@ extern "C" int sst_upscale_blend9(const float* img, int G, int h, int w, int s, 
   if (!make_tmap_f32_3d(&omap, out, (uint64_t)W * 3, (uint64_t)H, (uint64_t)G * kGop, kTQ, kTR))
     return SST_ERR_UNSUPPORTED;   // TMA alignment: W*3*4 bytes must be a multiple of 16
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  // A/B switch for profiling: SST_K5_9=6 (six store tiles: fewer CTAs per
-  // SM), "p" suffix = register prefetch of the next frame's window.  Measured
-  // at 32 x 1080p GoPs: 2 tiles / no prefetch 3.15 ms, 2p 4.17, 6 5.02, 6p 6.77.
-  const char* v = getenv("SST_K5_9");
-  if (v && v[0] == '6') return v[1] == 'p' ? launch_k5_9<32, 6, true>(omap, a, prev, blend_n, st)
-                                           : launch_k5_9<32, 6, false>(omap, a, prev, blend_n, st);
-  if (v && v[1] == 'p') return launch_k5_9<32, 2, true>(omap, a, prev, blend_n, st);
-  return launch_k5_9<32, 2, false>(omap, a, prev, blend_n, st);
+  // A/B switch for profiling: SST_K5_9="<band>,<tiles>[p]" (band 16 | 32,
+  // tiles 1 | 2 | 6, p = register prefetch of the next frame's window).
+  int band = 32, slots = 2;
+  bool pre = false;
+  // default 32-row bands, one tile set (k5_9_micro: 2.37 / 2.88 ms per
+  // 32-GoP launch at s=3 without / with blend; a column-private variant with
+  // per-thread horizontal taps and direct stores measured 3.0 / 4.1 ms)
+  slots = 1;
+  if (const char* v = getenv("SST_K5_9")) {
+    band = atoi(v) == 16 ? 16 : 32;
+    const char* c = strchr(v, ',');
+    if (c) { slots = atoi(c + 1); pre = strchr(c, 'p') != nullptr; }
+  }
+  if (band == 16) {
+    if (slots == 1) return pre ? launch_k5_9<16, 1, true>(omap, a, prev, blend_n, st)
+                               : launch_k5_9<16, 1, false>(omap, a, prev, blend_n, st);
+    return pre ? launch_k5_9<16, 2, true>(omap, a, prev, blend_n, st)
+               : launch_k5_9<16, 2, false>(omap, a, prev, blend_n, st);
+  }
+  if (slots == 6) return pre ? launch_k5_9<32, 6, true>(omap, a, prev, blend_n, st)
+                             : launch_k5_9<32, 6, false>(omap, a, prev, blend_n, st);
+  if (slots == 1) return launch_k5_9<32, 1, false>(omap, a, prev, blend_n, st);
+  return pre ? launch_k5_9<32, 2, true>(omap, a, prev, blend_n, st)
+             : launch_k5_9<32, 2, false>(omap, a, prev, blend_n, st);
 }
 
 extern "C" int sst_upscale(const float* img, int64_t n, int h, int w, int s, int crop_h, int crop_w,

@@ -1,1 +1,2 @@
-for v in 2n 2p 6n 6p; do echo "== $v"; SST_K5_9=$v timeout -s KILL 300 python scripts/diag_learned_stages.py | grep K5; done
+for v in c16 c32 "32,1"; do echo "== $v"; SST_K5_9=$v timeout -s KILL 200 python scripts/k5_9_micro.py; done
+timeout -s KILL 300 python -m pytest tests/test_gpu_learned.py -q -k gop_codec 2>&1 | tail -2
