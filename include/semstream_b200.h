@@ -336,6 +336,13 @@ SST_API int sst_lt_patchify(const float* frames, int G, int H, int W, int s, voi
 SST_API int sst_lt_dec_in(const double* tok, const uint8_t* mask, int G, int Ht, int Wt, void* out,
                           void* stream);
 
+/* Causal spatio-temporal window attention core of the learned tokenizer:
+ * qkv bf16 [G][2][H'][W'][3D] (Q | K | V, head-major 64-dim heads, from one
+ * 1x1 sst_lt_conv), out bf16 [G][2][H'][W'][D].  Each query attends to the
+ * valid tokens of its 8x8 window in latent frames <= its own (softmax in
+ * fp32, scale 1/8). */
+SST_API int sst_lt_attn(const void* qkv, int G, int Ht, int Wt, int D, void* out, void* stream);
+
 /* ---- metrics ------------------------------------------------------------ */
 
 /* mse (video.py:265-270) per frame pair: out[i] = mean((a-b)^2) in float64. */

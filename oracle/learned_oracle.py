@@ -101,6 +101,42 @@ def fsq(z: torch.Tensor):
     return torch.stack(codes, -1), torch.stack(idx, -1)
 
 
+def window_attention(qkv: torch.Tensor) -> torch.Tensor:
+    """Causal spatio-temporal 8x8-window attention (sst_lt_attn): qkv
+    [G][2][H][W][3D] bf16 values -> [G][2][H][W][D] bf16 values.  Keys: the
+    valid tokens of the query's window in latent frames <= its own; softmax
+    in fp32 with scale 1/sqrt(64)."""
+    G, T, H, W, C3 = qkv.shape
+    D = C3 // 3
+    nh = D // 64
+    Hp, Wp = -(-H // 8) * 8, -(-W // 8) * 8
+    x = F.pad(qkv, (0, 0, 0, Wp - W, 0, Hp - H))
+    valid = torch.zeros((Hp, Wp), dtype=torch.bool)
+    valid[:H, :W] = True
+    # [G][T][wy][8][wx][8][3][nh][64] -> [G][wy][wx][3][nh][T*64][64]
+    x = x.reshape(G, T, Hp // 8, 8, Wp // 8, 8, 3, nh, 64)
+    x = x.permute(0, 2, 4, 6, 7, 1, 3, 5, 8).reshape(G, Hp // 8, Wp // 8, 3, nh, T * 64, 64)
+    q, k, v = x[:, :, :, 0], x[:, :, :, 1], x[:, :, :, 2]
+    scores = (q @ k.transpose(-1, -2)) * 0.125
+    kv = valid.reshape(Hp // 8, 8, Wp // 8, 8).permute(0, 2, 1, 3).reshape(Hp // 8, Wp // 8, 64)
+    kv = kv.repeat(1, 1, T)                                    # [wy][wx][T*64] key validity
+    frame = torch.arange(T * 64) // 64
+    causal = frame[None, :] <= frame[:, None]                  # [query][key]
+    allow = causal[None, None] & kv[:, :, None, :]             # [wy][wx][q][k]
+    scores = scores.masked_fill(~allow[None, :, :, None], float("-inf"))
+    p = torch.softmax(scores, dim=-1)
+    o = torch.nan_to_num(p) @ v                                # [G][wy][wx][nh][T*64][64]
+    o = o.reshape(G, Hp // 8, Wp // 8, nh, T, 8, 8, 64).permute(0, 4, 1, 5, 2, 6, 3, 7)
+    o = o.reshape(G, T, Hp, Wp, D)[:, :, :H, :W]
+    return bf(o)
+
+
+def attention_block(h: torch.Tensor, Wm: dict, bm: dict, part: str) -> torch.Tensor:
+    qkv = bf(linear(h, Wm[f"{part}_qkv"], bm[f"{part}_qkv"]))
+    o = window_attention(qkv)
+    return bf(linear(o, Wm[f"{part}_proj"], bm[f"{part}_proj"]) + h)
+
+
 def encode(frames: np.ndarray, s: int, weights: dict, blocks: int):
     """-> (codes f64 [G][2][H'][W'][12], idx [G][2][H'][W'][2], (h, w), latent before FSQ)."""
     Wm, bm = weights["W"], weights["b"]
@@ -111,6 +147,8 @@ def encode(frames: np.ndarray, s: int, weights: dict, blocks: int):
     for i in range(blocks):
         u = conv233(h, Wm[f"enc{i}_c1"], bm[f"enc{i}_c1"], act=True)
         h = conv233(u, Wm[f"enc{i}_c2"], bm[f"enc{i}_c2"], residual=h)
+    if "enc_qkv" in Wm:
+        h = attention_block(h, Wm, bm, "enc")
     z = linear(h, Wm["head"], bm["head"])[..., :12]
     codes, idx = fsq(z)
     return codes.numpy(), idx.numpy(), hw, z
@@ -139,6 +177,8 @@ def decode(tokens: np.ndarray, mask: np.ndarray, hw, weights: dict, blocks: int)
     Wm, bm = weights["W"], weights["b"]
     x = dec_in(tokens, mask)
     h = conv233(x, Wm["dec_in"], bm["dec_in"], act=True)
+    if "dec_qkv" in Wm:
+        h = attention_block(h, Wm, bm, "dec")
     for i in range(blocks):
         u = conv233(h, Wm[f"dec{i}_c1"], bm[f"dec{i}_c1"], act=True)
         h = conv233(u, Wm[f"dec{i}_c2"], bm[f"dec{i}_c2"], residual=h)

@@ -628,6 +628,116 @@ __global__ void __launch_bounds__(c233p::THREADS, 1)
   }
 }
 
+// ---- causal spatio-temporal window attention (the attention core) ---------
+// Q, K, V come from one tcgen05 1x1 projection (qkv [G][2][H'][W'][3D], channel
+// = part*D + head*64 + d).  A CTA owns one 8x8 token window of one GoP and one
+// 64-dim head: 128 threads = 2 latent frames x 64 query tokens.  Keys/values of
+// the window's two frames are staged in shared memory as fp32; a query of frame
+// t attends to the window's valid tokens of frames <= t (causal in time), with
+// a one-pass online softmax in fp32.  The core is ~0.5 % of the tokenizer's
+// flops (64-128 keys per query), so it is plain SIMT; the projections around
+// it are the tensor-core GEMMs.
+constexpr int ATT_WIN = 8, ATT_HD = 64;
+
+__global__ void __launch_bounds__(128)
+    k_lt_attn(const __nv_bfloat16* __restrict__ qkv, int G, int Ht, int Wt, int D,
+              __nv_bfloat16* __restrict__ out) {
+  extern __shared__ float4 att_smem[];      // K [128][16], V [128][16] float4, kval[128]
+  float4 (*Ks)[ATT_HD / 4] = reinterpret_cast<float4 (*)[ATT_HD / 4]>(att_smem);
+  float4 (*Vs)[ATT_HD / 4] = reinterpret_cast<float4 (*)[ATT_HD / 4]>(att_smem + 128 * (ATT_HD / 4));
+  int* kval = reinterpret_cast<int*>(att_smem + 2 * 128 * (ATT_HD / 4));
+  const int wins_x = ceil_div(Wt, ATT_WIN);
+  const int wy = blockIdx.x / wins_x, wx = blockIdx.x - wy * wins_x;
+  const int head = blockIdx.y, g = blockIdx.z;
+  const int t = threadIdx.x;
+  const int ft = t >> 6, lt = t & 63;
+  const int y = wy * ATT_WIN + (lt >> 3), x = wx * ATT_WIN + (lt & 7);
+  const bool valid = y < Ht && x < Wt;
+  const size_t tok = (((size_t)g * 2 + ft) * Ht + y) * Wt + x;
+  const int C3 = 3 * D;
+  // stage this thread's key / value row (token t of the window) as fp32
+  kval[t] = valid;
+  {
+    float4* kd = Ks[t];
+    float4* vd = Vs[t];
+    if (valid) {
+      const uint4* kp = reinterpret_cast<const uint4*>(qkv + tok * C3 + D + head * ATT_HD);
+      const uint4* vp = reinterpret_cast<const uint4*>(qkv + tok * C3 + 2 * D + head * ATT_HD);
+#pragma unroll
+      for (int i = 0; i < ATT_HD / 8; ++i) {
+        uint4 ku = __ldg(kp + i), vu = __ldg(vp + i);
+        const __nv_bfloat162* k2 = reinterpret_cast<const __nv_bfloat162*>(&ku);
+        const __nv_bfloat162* v2 = reinterpret_cast<const __nv_bfloat162*>(&vu);
+        float2 a0 = __bfloat1622float2(k2[0]), a1 = __bfloat1622float2(k2[1]);
+        float2 a2 = __bfloat1622float2(k2[2]), a3 = __bfloat1622float2(k2[3]);
+        kd[2 * i] = make_float4(a0.x, a0.y, a1.x, a1.y);
+        kd[2 * i + 1] = make_float4(a2.x, a2.y, a3.x, a3.y);
+        a0 = __bfloat1622float2(v2[0]); a1 = __bfloat1622float2(v2[1]);
+        a2 = __bfloat1622float2(v2[2]); a3 = __bfloat1622float2(v2[3]);
+        vd[2 * i] = make_float4(a0.x, a0.y, a1.x, a1.y);
+        vd[2 * i + 1] = make_float4(a2.x, a2.y, a3.x, a3.y);
+      }
+    }
+  }
+  float q[ATT_HD];
+  if (valid) {
+    const uint4* qp = reinterpret_cast<const uint4*>(qkv + tok * C3 + head * ATT_HD);
+#pragma unroll
+    for (int i = 0; i < ATT_HD / 8; ++i) {
+      uint4 u = __ldg(qp + i);
+      const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        float2 f = __bfloat1622float2(h2[e]);
+        q[8 * i + 2 * e] = f.x * 0.125f;          // 1/sqrt(64), exact
+        q[8 * i + 2 * e + 1] = f.y * 0.125f;
+      }
+    }
+  }
+  __syncthreads();
+  if (!valid) return;
+  float acc[ATT_HD];
+#pragma unroll
+  for (int d = 0; d < ATT_HD; ++d) acc[d] = 0.0f;
+  float m = -INFINITY, l = 0.0f;
+  const int nkeys = (ft + 1) * ATT_WIN * ATT_WIN;   // causal: frames 0..ft
+  for (int j = 0; j < nkeys; ++j) {
+    if (!kval[j]) continue;
+    float sdot = 0.0f;
+#pragma unroll
+    for (int i = 0; i < ATT_HD / 4; ++i) {
+      const float4 k4 = Ks[j][i];
+      sdot = fmaf(q[4 * i], k4.x, sdot);
+      sdot = fmaf(q[4 * i + 1], k4.y, sdot);
+      sdot = fmaf(q[4 * i + 2], k4.z, sdot);
+      sdot = fmaf(q[4 * i + 3], k4.w, sdot);
+    }
+    const float mn = fmaxf(m, sdot);
+    const float c = __expf(m - mn), p = __expf(sdot - mn);
+    l = l * c + p;
+#pragma unroll
+    for (int i = 0; i < ATT_HD / 4; ++i) {
+      const float4 v4 = Vs[j][i];
+      acc[4 * i] = fmaf(p, v4.x, acc[4 * i] * c);
+      acc[4 * i + 1] = fmaf(p, v4.y, acc[4 * i + 1] * c);
+      acc[4 * i + 2] = fmaf(p, v4.z, acc[4 * i + 2] * c);
+      acc[4 * i + 3] = fmaf(p, v4.w, acc[4 * i + 3] * c);
+    }
+    m = mn;
+  }
+  const float inv = 1.0f / l;
+  uint4* op = reinterpret_cast<uint4*>(out + tok * D + head * ATT_HD);
+#pragma unroll
+  for (int i = 0; i < ATT_HD / 8; ++i) {
+    uint4 u;
+    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      h2[e] = __floats2bfloat162_rn(acc[8 * i + 2 * e] * inv, acc[8 * i + 2 * e + 1] * inv);
+    op[i] = u;
+  }
+}
+
 // ---- downscale + pad + patchify --------------------------------------------
 template <int S>
 __global__ void k_lt_patchify(const float* __restrict__ src, int G, int H, int W, int h, int w,
@@ -903,6 +1013,20 @@ extern "C" int sst_lt_dec_in(const double* tok, const uint8_t* mask, int G, int 
   lt::k_lt_dec_in<<<(unsigned)ceil_div64(total, threads), threads, 0,
                     static_cast<cudaStream_t>(stream)>>>(tok, mask, G, Ht, Wt,
                                                          static_cast<__nv_bfloat16*>(out));
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+extern "C" int sst_lt_attn(const void* qkv, int G, int Ht, int Wt, int D, void* out, void* stream) {
+  if (!qkv || !out || G <= 0 || Ht <= 0 || Wt <= 0 || D <= 0 || D % lt::ATT_HD) return SST_ERR_ARG;
+  if (G > 65535 || D / lt::ATT_HD > 65535) return SST_ERR_ARG;
+  const int64_t wins = (int64_t)ceil_div(Ht, lt::ATT_WIN) * ceil_div(Wt, lt::ATT_WIN);
+  if (wins > 0x7fffffff) return SST_ERR_ARG;
+  dim3 grid((unsigned)wins, D / lt::ATT_HD, G);
+  const int smem = 2 * 128 * lt::ATT_HD * 4 + 128 * 4;
+  SST_CUDA_TRY(cudaFuncSetAttribute(lt::k_lt_attn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  lt::k_lt_attn<<<grid, 128, smem, static_cast<cudaStream_t>(stream)>>>(
+      static_cast<const __nv_bfloat16*>(qkv), G, Ht, Wt, D, static_cast<__nv_bfloat16*>(out));
   SST_LAUNCH_CHECK();
   return SST_OK;
 }

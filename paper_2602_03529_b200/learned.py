@@ -20,7 +20,9 @@ reassembly are reused unchanged):
     8x8x3 patch, latent frame t=1 (P) embeds frames 1..8's 8x8x8x3 patch;
   * encoder: patch embeddings -> D channels, `blocks` causal residual blocks
     h += conv(SiLU(conv(h))) with (2,3,3) kernels that see t and t-1 only,
-    then a 1x1 head to 12 channels and FSQ (two groups of levels
+    a causal spatio-temporal attention block h += proj(attn(qkv(h))) (8x8
+    token windows, 64-dim heads, frame t attends to frames <= t), then a 1x1
+    head to 12 channels and FSQ (two groups of levels
     (8,8,8,5,5,5), 64000 codes each).  The 12 FSQ code values are the
     TokenMatrix channels (codec.py:32 fixes C = 12) and travel through the
     reference's 8-bit row quantiser; the decoder snaps them back onto the FSQ
@@ -28,7 +30,8 @@ reassembly are reused unchanged):
     below half an FSQ step;
   * decoder: masked P tokens take the co-located I token's codes (the
     proxy's concealment rule, codec.py:176-180, in latent space), a (2,3,3)
-    conv lifts 12 -> D channels, `blocks` residual blocks, then 1x1 unpatchify
+    conv lifts 12 -> D channels, an attention block, `blocks` residual
+    blocks, then 1x1 unpatchify
     convs write frame 0 (from t=0) and frames 1..8 (from t=1), clamped to
     [0, 1] and cropped to the working frame.
 
@@ -67,6 +70,7 @@ class LearnedConfig:
     dim: int = 256          # latent channels D (multiple of 128)
     blocks: int = 2         # residual blocks in the encoder and in the decoder
     seed: int = 0
+    attn: bool = True       # one causal spatio-temporal window-attention block per side
 
     def __post_init__(self):
         if self.dim <= 0 or self.dim % 128:
@@ -119,6 +123,12 @@ def make_weights(cfg: LearnedConfig) -> dict:
     W["out_p"] = normal(PATCH_P, D, 0.25 / np.sqrt(D))
     b["out_i"] = np.full(PATCH_I, 0.5, np.float32)
     b["out_p"] = np.full(PATCH_P, 0.5, np.float32)
+    if cfg.attn:     # drawn last: the weights above do not depend on cfg.attn
+        for part in ("enc", "dec"):
+            W[f"{part}_qkv"] = normal(3 * D, D, 1.0 / np.sqrt(D))
+            b[f"{part}_qkv"] = np.zeros(3 * D, np.float32)
+            W[f"{part}_proj"] = normal(D, D, 0.5 / np.sqrt(D))
+            b[f"{part}_proj"] = np.zeros(D, np.float32)
     return {"W": W, "b": b}
 
 
@@ -181,6 +191,22 @@ class LearnedTokenizer:
             self._conv(f"{part}{i}_c2", u, shape, (Ht, Wt), TAPS_233, 0, 2, _lib.LT_EPI_STORE,
                        residual=h, out=h)
 
+    def _attention(self, part, h, G, Ht, Wt):
+        """h += proj(WindowAttention(qkv(h))): the projections are tcgen05
+        1x1 GEMMs, the 8x8-window causal attention core is sst_lt_attn."""
+        if not self.cfg.attn:
+            return
+        D = self.cfg.dim
+        shape = (G, 2, Ht, Wt, D)
+        qkv = torch.empty((G, 2, Ht, Wt, 3 * D), dtype=torch.bfloat16, device=h.device)
+        o = torch.empty_like(h)
+        self._conv(f"{part}_qkv", h, shape, (Ht, Wt), [(0, 0, 0)], 0, 2, _lib.LT_EPI_STORE,
+                   out=qkv)
+        _lib.call("sst_lt_attn", qkv.data_ptr(), G, Ht, Wt, D, o.data_ptr(), _dev.stream())
+        self.launches += 1
+        self._conv(f"{part}_proj", o, shape, (Ht, Wt), [(0, 0, 0)], 0, 2, _lib.LT_EPI_STORE,
+                   residual=h, out=h)
+
     # ---- encoder ------------------------------------------------------------
     def encode_frames(self, frames: torch.Tensor, s: int = 1, codes: torch.Tensor | None = None,
                       mask: torch.Tensor | None = None, idx: torch.Tensor | None = None):
@@ -211,6 +237,7 @@ class LearnedTokenizer:
         self._conv("pe_p", pP, (G, 1, Ht, Wt, PATCH_P), (Ht, Wt), [(-1, 0, 0)], 1, 1,
                    _lib.LT_EPI_STORE, out=hbuf)
         self._blocks("enc", hbuf, ubuf, G, Ht, Wt)
+        self._attention("enc", hbuf, G, Ht, Wt)
         if codes is None:
             codes = torch.zeros((G, 2, Ht, Wt, FSQ_CHANNELS), dtype=torch.float64, device=dev)
         if idx is None:
@@ -251,6 +278,7 @@ class LearnedTokenizer:
         ubuf = torch.empty_like(hbuf)
         self._conv("dec_in", x, (G, 2, Ht, Wt, DEC_IN_CHANNELS), (Ht, Wt), TAPS_233, 0, 2,
                    _lib.LT_EPI_STORE, act=1, out=hbuf)
+        self._attention("dec", hbuf, G, Ht, Wt)
         self._blocks("dec", hbuf, ubuf, G, Ht, Wt)
         if frames is None:
             frames = torch.empty((G, GOP_SIZE, h, w, 3), dtype=torch.float32, device=dev)
@@ -271,7 +299,8 @@ class LearnedTokenizer:
             + 2 * n * 2 * D * 16
         dec = 2 * n * 2 * len(TAPS_233) * DEC_IN_CHANNELS * D \
             + 2 * n * 2 * (2 * self.cfg.blocks * k3 * D) + n * 2 * D * (PATCH_I + PATCH_P)
-        return enc + dec
+        attn = 2 * (2 * n * 2 * D * 4 * D) if self.cfg.attn else 0   # qkv + proj, both sides
+        return enc + dec + attn
 
 
 # ---- the reference's plug-in contract (session.py:57-61) -------

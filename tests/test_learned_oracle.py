@@ -107,3 +107,29 @@ def test_oracle_end_to_end_small():
     assert hw == (10, 14) and codes.shape == (1, 2, 2, 2, 12)
     out = LO.decode(codes, np.ones(codes.shape[:-1], np.uint8), hw, w, cfg.blocks)
     assert out.shape == (1, 9, 10, 14, 3) and out.min() >= 0 and out.max() <= 1
+
+
+def test_window_attention_matches_bruteforce():
+    """The oracle's batched window attention vs a per-query loop (causal in
+    latent time, keys restricted to the query's 8x8 window)."""
+    rng = np.random.default_rng(9)
+    G, T, H, W, D = 1, 2, 10, 11, 128
+    qkv = LO.bf(torch.from_numpy(rng.standard_normal((G, T, H, W, 3 * D)).astype(np.float32)))
+    got = LO.window_attention(qkv).numpy()
+    x = qkv.numpy().astype(np.float64)
+    for t in range(T):
+        for y in range(H):
+            for xx in range(W):
+                for hd in range(D // 64):
+                    q = x[0, t, y, xx, hd * 64:(hd + 1) * 64] * 0.125
+                    keys, vals = [], []
+                    for tk in range(t + 1):
+                        for yk in range((y // 8) * 8, min(H, (y // 8) * 8 + 8)):
+                            for xk in range((xx // 8) * 8, min(W, (xx // 8) * 8 + 8)):
+                                keys.append(x[0, tk, yk, xk, D + hd * 64:D + (hd + 1) * 64])
+                                vals.append(x[0, tk, yk, xk, 2 * D + hd * 64:2 * D + (hd + 1) * 64])
+                    sc = np.array(keys) @ q
+                    p = np.exp(sc - sc.max())
+                    o = (p / p.sum()) @ np.array(vals)
+                    np.testing.assert_allclose(got[0, t, y, xx, hd * 64:(hd + 1) * 64], o,
+                                               rtol=2 ** -7, atol=1e-3)
