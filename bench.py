@@ -85,7 +85,9 @@ def workload_config(a) -> dict:
         "gop_frames": GOP,
         "drop_rate": a.drop,
         "blend_width": 2,
-        "l2": "inputs larger than L2 (each step reads a fresh 14.3 GB GoP batch at 64 streams)",
+        "l2": (f"inputs larger than L2: each step reads a fresh "
+               f"{a.streams * GOP * a.height * a.width * 12 / 1e9:.1f} GB GoP batch "
+               f"({a.streams} streams) vs the 126 MB L2"),
     }
 
 
@@ -216,6 +218,17 @@ def make_inputs(stream_ids, H, W, device, n_sets=2):
 # ---------------------------------------------------------------------------
 # our arm
 
+def max_over_ranks(ms: float, dev) -> float:
+    """Device-timed step time, max over ranks (NCCL on the GPUs; a host tensor
+    when the group is gloo -- the SST_BENCH_SHARE_GPU test hook)."""
+    import torch
+    import torch.distributed as dist
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor([ms], dtype=torch.float64, device=dev if on_dev else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def run_ours(a, rank, world, local_rank):
     import numpy as np
     import torch
@@ -308,9 +321,7 @@ def run_ours(a, rank, world, local_rank):
     ms = t_start.elapsed_time(t_end)
     ms_max = ms
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
+        ms_max = max_over_ranks(ms, dev)
     launches = bank.launches - launches0
     # Per-kernel roofline: a few extra steps with the lanes serialised on one
     # stream so that every kernel's CUDA-event duration is its own (in the
@@ -495,9 +506,7 @@ def run_e2e(a, rank, world, local_rank) -> dict:
     wall = time.perf_counter() - wall0
     ms = t0.elapsed_time(t1)
     if world > 1:
-        t = torch.tensor([ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms = max_over_ranks(ms, dev)
     # the outputs really arrived: spot-check one host frame against the device
     frames = E * GOP * a.steps * world
     return {"value": round(frames / (ms / 1000.0), 2), "unit": UNIT,
@@ -763,9 +772,18 @@ def main():
 
     import torch
     import torch.distributed as dist
+    # SST_BENCH_SHARE_GPU=1 (test hook): ranks share the visible GPUs round-robin
+    # and rendezvous over gloo, so the N>1 control flow (barriers, max-over-ranks,
+    # stream sharding) can be exercised on a one-GPU box.  Never used by the driver.
+    share = os.environ.get("SST_BENCH_SHARE_GPU") == "1"
+    if share:
+        local_rank = local_rank % torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     res = run_ours(a, rank, world, local_rank)
     if rank == 0:
         line = dict(base, value=round(res["value"], 2), ms_per_step=round(res["ms"] / a.steps, 3),
