@@ -104,8 +104,9 @@ def fsq(z: torch.Tensor):
 def window_attention(qkv: torch.Tensor) -> torch.Tensor:
     """Causal spatio-temporal 8x8-window attention (sst_lt_attn): qkv
     [G][2][H][W][3D] bf16 values -> [G][2][H][W][D] bf16 values.  Keys: the
-    valid tokens of the query's window in latent frames <= its own; softmax
-    in fp32 with scale 1/sqrt(64)."""
+    valid tokens of the query's window in latent frames <= its own; scores
+    scaled by 1/sqrt(64), P = exp(s - max) in fp32 rounded to bf16 (the
+    tensor-core operand), O = (P V) / sum(P) with the fp32 sum."""
     G, T, H, W, C3 = qkv.shape
     D = C3 // 3
     nh = D // 64
@@ -124,8 +125,12 @@ def window_attention(qkv: torch.Tensor) -> torch.Tensor:
     causal = frame[None, :] <= frame[:, None]                  # [query][key]
     allow = causal[None, None] & kv[:, :, None, :]             # [wy][wx][q][k]
     scores = scores.masked_fill(~allow[None, :, :, None], float("-inf"))
-    p = torch.softmax(scores, dim=-1)
-    o = torch.nan_to_num(p) @ v                                # [G][wy][wx][nh][T*64][64]
+    # softmax with the unnormalised probabilities rounded to bf16 before P.V
+    # (the tensor-core operand) and the fp32 row sum applied afterwards
+    mx = scores.amax(-1, keepdim=True)
+    p = torch.exp(scores - torch.where(torch.isfinite(mx), mx, torch.zeros_like(mx)))
+    l = p.sum(-1, keepdim=True)
+    o = (bf(p) @ v) / torch.where(l > 0, l, torch.ones_like(l))   # [G][wy][wx][nh][T*64][64]
     o = o.reshape(G, Hp // 8, Wp // 8, nh, T, 8, 8, 64).permute(0, 4, 1, 5, 2, 6, 3, 7)
     o = o.reshape(G, T, Hp, Wp, D)[:, :, :H, :W]
     return bf(o)

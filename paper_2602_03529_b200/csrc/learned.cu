@@ -35,7 +35,6 @@ constexpr int BM = 128;            // tokens per tile (16 x 8 spatial box)
 constexpr int BOX_X = 16, BOX_Y = 8;
 constexpr int BK = 64;             // bf16 per 128-byte swizzled row
 constexpr int A_BYTES = BM * BK * 2;
-constexpr int STAGES = 4;
 constexpr int FSQ_C = 12;          // 2 groups x levels (8,8,8,5,5,5)
 constexpr int DEC_IN_C = 64;
 
@@ -62,19 +61,23 @@ struct ConvArgs {
 
 __device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 
-template <int BN>
+template <int BN, int NST>
 struct TileCfg {
   static constexpr int B_BYTES = BN * 128;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
-  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM = NST * STAGE_BYTES + 1024 + 256;
 };
 
-template <int BN, int EPI>
-__global__ void __launch_bounds__(128, 1)
+// NST = smem pipeline stages: 4 for long K, 2 for the short-K (<= 512) 1x1
+// layers so that 2-3 CTAs share an SM and one CTA's epilogue overlaps
+// another's loads and MMAs.
+template <int BN, int EPI, int NST>
+__global__ void __launch_bounds__(128)
     k_lt_conv(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmC, const ConvArgs a) {
-  using Cfg = TileCfg<BN>;
+  constexpr int STAGES = NST;
+  using Cfg = TileCfg<BN, NST>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -738,6 +741,177 @@ __global__ void __launch_bounds__(128)
   }
 }
 
+// ---- causal window attention core on tcgen05 --------------------------------
+// One CTA = one (GoP, 8x8 window, 64-dim head): 128 query rows (2 latent
+// frames x 64 tokens) and the same 128 keys.  Q, K and V^T are staged into
+// 128B-swizzled K-major tiles with st.shared (manual swizzle), then
+//   S = Q K^T   tcgen05.mma M=128 N=128 K=64  -> TMEM columns 0..127
+//   softmax     thread q: tcgen05.ld its 128 scores, causal + validity mask,
+//               P = exp((s - max) / 8) rounded to bf16 -> smem (over Q, K)
+//   O = P V     tcgen05.mma M=128 N=64 K=128  -> TMEM columns 0..63
+//   O / l       tcgen05.ld, bf16 stores.
+constexpr int ATT_SMEM = 3 * 16384 + 1024 + 64 + 128 * 4;
+
+__global__ void __launch_bounds__(128)
+    k_lt_attn_tc(const __nv_bfloat16* __restrict__ qkv, int G, int Ht, int Wt, int D,
+                 __nv_bfloat16* __restrict__ out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;                 // [128 q][64 d]   A of S
+  uint8_t* sK = smem + 16384;         // [128 k][64 d]   B of S
+  uint8_t* sP = smem;                 // [2 kb][128 q][64 k] A of O (reuses sQ, sK)
+  uint8_t* sV = smem + 32768;         // [2 kb][64 d][64 k]  B of O (V^T)
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 49152);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2);
+  int* kval = reinterpret_cast<int*>(smem + 49152 + 64);
+
+  const int wins_x = ceil_div(Wt, ATT_WIN);
+  const int wy = blockIdx.x / wins_x, wx = blockIdx.x - wy * wins_x;
+  const int head = blockIdx.y, g = blockIdx.z;
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int ft = t >> 6, lt = t & 63;
+  const int y = wy * ATT_WIN + (lt >> 3), x = wx * ATT_WIN + (lt & 7);
+  const bool valid = y < Ht && x < Wt;
+  const size_t tok = (((size_t)g * 2 + ft) * Ht + y) * Wt + x;
+  const int C3 = 3 * D;
+
+  if (t == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tmem_slot, 128);
+
+  // ---- stage Q, K rows (K-major, row = token t) and V^T (row = dim) ----
+  kval[t] = valid;
+  {
+    uint4 q4[8], k4[8], v4[8];
+    if (valid) {
+      const uint4* base = reinterpret_cast<const uint4*>(qkv + tok * C3 + head * ATT_HD);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        q4[j] = __ldg(base + j);
+        k4[j] = __ldg(base + D / 8 + j);
+        v4[j] = __ldg(base + 2 * D / 8 + j);
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) q4[j] = k4[j] = v4[j] = make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int off = t * 128 + ((j ^ (t & 7)) << 4);
+      *reinterpret_cast<uint4*>(sQ + off) = q4[j];
+      *reinterpret_cast<uint4*>(sK + off) = k4[j];
+    }
+    const int kb = t >> 6, kk = t & 63;
+    uint8_t* vb = sV + kb * 8192 + (kk & 7) * 2;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const __nv_bfloat16* e = reinterpret_cast<const __nv_bfloat16*>(&v4[j]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int d = 8 * j + i;
+        *reinterpret_cast<__nv_bfloat16*>(vb + d * 128 + (((kk >> 3) ^ (d & 7)) << 4)) = e[i];
+      }
+    }
+  }
+  fence_proxy_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (t == 0) {
+    constexpr uint32_t id1 = tc::idesc_bf16_f32(128, 128);
+    const uint64_t ad = tc::smem_desc_sw128(smem_u32(sQ));
+    const uint64_t bd = tc::smem_desc_sw128(smem_u32(sK));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) tc::mma_bf16(tmem, ad + 2 * k, bd + 2 * k, id1, k);
+    tc::mma_commit(&bar[0]);
+  }
+  mbar_wait(&bar[0], 0);
+  tc::fence_after_sync();
+
+  // ---- softmax of this thread's query row (TMEM lane t) ----
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  float sc[128];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    float v[32];
+    tc::tmem_ld32(trow + c * 32, v);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) sc[c * 32 + i] = v[i];
+  }
+  const int nk = (ft + 1) * 64;       // causal: keys of frames <= ft
+  float m = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < 128; ++k)
+    if (k < nk && kval[k]) m = fmaxf(m, sc[k]);
+  float l = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 128; ++k) {
+    const float p = (k < nk && kval[k]) ? __expf((sc[k] - m) * 0.125f) : 0.0f;
+    sc[k] = p;
+    l += p;
+  }
+  tc::fence_before_sync();
+  __syncthreads();                    // every S read done and GEMM 1 retired: sQ/sK -> sP
+#pragma unroll
+  for (int kb = 0; kb < 2; ++kb) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint4 u;
+      __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        h2[e] = __floats2bfloat162_rn(sc[kb * 64 + 8 * j + 2 * e], sc[kb * 64 + 8 * j + 2 * e + 1]);
+      *reinterpret_cast<uint4*>(sP + kb * 16384 + t * 128 + ((j ^ (t & 7)) << 4)) = u;
+    }
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (t == 0) {
+    constexpr uint32_t id2 = tc::idesc_bf16_f32(128, 64);
+#pragma unroll
+    for (int kb = 0; kb < 2; ++kb) {
+      const uint64_t ad = tc::smem_desc_sw128(smem_u32(sP + kb * 16384));
+      const uint64_t bd = tc::smem_desc_sw128(smem_u32(sV + kb * 8192));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) tc::mma_bf16(tmem, ad + 2 * k, bd + 2 * k, id2, kb | k);
+    }
+    tc::mma_commit(&bar[1]);
+  }
+  mbar_wait(&bar[1], 0);
+  tc::fence_after_sync();
+  float o[64];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    float v[32];
+    tc::tmem_ld32(trow + c * 32, v);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) o[c * 32 + i] = v[i];
+  }
+  if (valid) {
+    const float inv = 1.0f / l;
+    uint4* op = reinterpret_cast<uint4*>(out + tok * D + head * ATT_HD);
+#pragma unroll
+    for (int i = 0; i < ATT_HD / 8; ++i) {
+      uint4 u;
+      __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        h2[e] = __floats2bfloat162_rn(o[8 * i + 2 * e] * inv, o[8 * i + 2 * e + 1] * inv);
+      op[i] = u;
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 128);
+}
+
 // ---- downscale + pad + patchify --------------------------------------------
 template <int S>
 __global__ void k_lt_patchify(const float* __restrict__ src, int G, int H, int W, int h, int w,
@@ -811,9 +985,9 @@ __global__ void k_lt_dec_in(const double* __restrict__ tok, const uint8_t* __res
   for (int q = 0; q < DEC_IN_C / 8; ++q) op[q] = o[q];
 }
 
-template <int BN, int EPI>
-static int launch_conv(const SstConvDesc* d, cudaStream_t st) {
-  using Cfg = TileCfg<BN>;
+template <int BN, int EPI, int NST>
+static int launch_conv_n(const SstConvDesc* d, cudaStream_t st) {
+  using Cfg = TileCfg<BN, NST>;
   if (d->N % BN != 0) return SST_ERR_ARG;
   CUtensorMap tmA, tmB, tmC;
   memset(&tmA, 0, sizeof(tmA));
@@ -848,11 +1022,17 @@ static int launch_conv(const SstConvDesc* d, cudaStream_t st) {
   const int64_t mt = (int64_t)d->G * d->t_cnt * a.tiles_y * a.tiles_x;
   if (mt <= 0 || mt > 0x7fffffff) return SST_ERR_ARG;
   dim3 grid((unsigned)mt, d->N / BN);
-  auto kern = k_lt_conv<BN, EPI>;
+  auto kern = k_lt_conv<BN, EPI, NST>;
   SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM));
   kern<<<grid, 128, Cfg::SMEM, st>>>(tmA, tmB, tmC, a);
   SST_LAUNCH_CHECK();
   return SST_OK;
+}
+
+template <int BN, int EPI>
+static int launch_conv(const SstConvDesc* d, cudaStream_t st) {
+  if (d->n_taps * (d->in_C / BK) <= 8) return launch_conv_n<BN, EPI, 2>(d, st);
+  return launch_conv_n<BN, EPI, 4>(d, st);
 }
 
 static bool is_taps233(const SstConvDesc* d) {
@@ -1023,10 +1203,19 @@ extern "C" int sst_lt_attn(const void* qkv, int G, int Ht, int Wt, int D, void* 
   const int64_t wins = (int64_t)ceil_div(Ht, lt::ATT_WIN) * ceil_div(Wt, lt::ATT_WIN);
   if (wins > 0x7fffffff) return SST_ERR_ARG;
   dim3 grid((unsigned)wins, D / lt::ATT_HD, G);
-  const int smem = 2 * 128 * lt::ATT_HD * 4 + 128 * 4;
-  SST_CUDA_TRY(cudaFuncSetAttribute(lt::k_lt_attn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  lt::k_lt_attn<<<grid, 128, smem, static_cast<cudaStream_t>(stream)>>>(
-      static_cast<const __nv_bfloat16*>(qkv), G, Ht, Wt, D, static_cast<__nv_bfloat16*>(out));
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const char* mode = getenv("SST_LT_ATTN");          // "simt": the SIMT core (A/B)
+  if (mode && mode[0] == 's') {
+    const int smem = 2 * 128 * lt::ATT_HD * 4 + 128 * 4;
+    SST_CUDA_TRY(cudaFuncSetAttribute(lt::k_lt_attn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    lt::k_lt_attn<<<grid, 128, smem, st>>>(static_cast<const __nv_bfloat16*>(qkv), G, Ht, Wt, D,
+                                           static_cast<__nv_bfloat16*>(out));
+  } else {
+    SST_CUDA_TRY(cudaFuncSetAttribute(lt::k_lt_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      lt::ATT_SMEM));
+    lt::k_lt_attn_tc<<<grid, 128, lt::ATT_SMEM, st>>>(static_cast<const __nv_bfloat16*>(qkv), G, Ht,
+                                                       Wt, D, static_cast<__nv_bfloat16*>(out));
+  }
   SST_LAUNCH_CHECK();
   return SST_OK;
 }

@@ -77,10 +77,10 @@ def _conv_gpu(x, W, b, taps, t_lo, t_cnt, epi, out_T=2, act=0, residual=None, hw
     return {k: v.float().cpu() if v.dtype == torch.bfloat16 else v.cpu() for k, v in out.items()}
 
 
-def _assert_bf16_close(got, want, min_exact=0.97):
+def _assert_bf16_close(got, want, min_exact=0.97, atol=0.0):
     got, want = got.numpy(), want.numpy()
     err = np.abs(got - want)
-    tol = 2 * BF16_ULP * np.maximum(np.abs(want), 1e-3)
+    tol = 2 * BF16_ULP * np.maximum(np.abs(want), 1e-3) + atol
     assert (err <= tol).all(), f"max err {err.max()} (worst rel {(err / tol).max():.2f} of 2 ulp)"
     assert (got == want).mean() >= min_exact
 
@@ -135,7 +135,10 @@ def test_window_attention_core(H, W, D):
     out = torch.full((G, 2, H, W, D), 7.0, dtype=torch.bfloat16, device=dev)
     _lib.call("sst_lt_attn", qd.data_ptr(), G, H, W, D, out.data_ptr(), _dev.stream())
     torch.cuda.synchronize()
-    _assert_bf16_close(out.float().cpu(), LO.window_attention(qkv), min_exact=0.95)
+    # attention outputs are convex mixes of V rows (|o| <~ 1); near-zero
+    # results from cancellation carry the absolute rounding error of the
+    # bf16 probabilities, hence the 2e-3 absolute floor
+    _assert_bf16_close(out.float().cpu(), LO.window_attention(qkv), min_exact=0.95, atol=2e-3)
 
 
 def test_conv_causal_first_frame_sees_no_past():

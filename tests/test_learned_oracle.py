@@ -131,5 +131,6 @@ def test_window_attention_matches_bruteforce():
                     sc = np.array(keys) @ q
                     p = np.exp(sc - sc.max())
                     o = (p / p.sum()) @ np.array(vals)
+                    # bf16 output and bf16-rounded probabilities (the P.V operand)
                     np.testing.assert_allclose(got[0, t, y, xx, hd * 64:(hd + 1) * 64], o,
-                                               rtol=2 ** -7, atol=1e-3)
+                                               rtol=2 ** -7, atol=4e-3)
