@@ -1,4 +1,5 @@
-"""Where does end-to-end FSQ divergence come from?  Compare GPU vs oracle z
+"""(Experiment record: written against the reverted fp32-residual-stream variant,
+which exposed an `out32` conv output.)  Where does end-to-end FSQ divergence come from?  Compare GPU vs oracle z
 (pre-FSQ) and the stream after each encoder stage, e2e (no isolation)."""
 import sys
 sys.path.insert(0, ".")
