@@ -52,7 +52,7 @@ import torch
 
 from . import _dev, _lib
 from .codec import CodecConfig, TokenMatrix, token_grid_shape
-from .pipeline import CHANNELS, GopCodec
+from .pipeline import CHANNELS, GopCodec, check_gop_tensor
 from .video import GOP_SIZE, Frame, GoP
 
 FSQ_LEVELS = (8, 8, 8, 5, 5, 5, 8, 8, 8, 5, 5, 5)
@@ -416,6 +416,7 @@ class LearnedGopCodec(GopCodec):
         """K5 for 9 distinct frames: upscale frames9[parity][:g] to
         [g, 9, H, W, 3] and, when ``blend``, mix frames 0..n-1 with the
         previous step's GoP in the same slot (frames9[1 - parity])."""
+        check_gop_tensor(out, g, self.H, self.W, "out")
         self.timer.begin("K5_upscale_blend")
         prev = self.prev_desc[parity].data_ptr() if blend else None
         _lib.call("sst_upscale_blend9", self.frames9[parity].data_ptr(), g, self.h, self.w,

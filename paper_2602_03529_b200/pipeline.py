@@ -35,6 +35,20 @@ def _cdiv(a: int, b: int) -> int:
     return -(-a // b)
 
 
+def check_gop_tensor(t: torch.Tensor, g: int, H: int, W: int, what: str) -> None:
+    """The kernels address [g][9][H][W][3] float32 by raw pointer: reject
+    anything else (a non-contiguous view, e.g. a transposed numpy array
+    wrapped by torch.from_numpy, would otherwise be read in the wrong order)."""
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise ValueError(f"{what} must be a CUDA tensor")
+    if t.dtype != torch.float32:
+        raise ValueError(f"{what} must be float32, got {t.dtype}")
+    if t.dim() != 5 or tuple(t.shape[1:]) != (GOP, H, W, 3) or t.shape[0] < g:
+        raise ValueError(f"{what} must be [>= {g}, {GOP}, {H}, {W}, 3], got {tuple(t.shape)}")
+    if not t.is_contiguous():
+        raise ValueError(f"{what} must be contiguous (call .contiguous())")
+
+
 class StageTimer:
     """CUDA-event timing of each kernel stage on the launching (current) stream."""
 
@@ -156,6 +170,7 @@ class GopCodec:
     def tokenize(self, frames: torch.Tensor, g: int) -> None:
         """K1: downscale + tokenize + similarity."""
         tm = self.timer
+        check_gop_tensor(frames, g, self.H, self.W, "frames")
         tm.begin("K1_encode")
         _lib.call("sst_encode", frames.data_ptr(), g, self.H, self.W, self.s,
                   self.tok.data_ptr(), self.sim.data_ptr(), _dev.stream())
@@ -208,6 +223,7 @@ class GopCodec:
                     prev: torch.Tensor | None = None) -> None:
         """K5: [g, 9, H, W, 3] float32 output frames; prev = device
         SstPrevDesc[g] as uint8 bytes (or None: no blending)."""
+        check_gop_tensor(out, g, self.H, self.W, "out")
         self.timer.begin("K5_upscale_blend")
         _lib.call("sst_upscale_blend", self.img[parity].data_ptr(), g, self.h, self.w, self.s,
                   self.H, self.W, None if prev is None else prev.data_ptr(), self.blend_n,

@@ -114,3 +114,51 @@ def test_1080p_properties_and_determinism():
         assert torch.equal(o[0, f], o[0, 1])               # P reconstruction materialised 8x
     mse = ((o.double() - src.double()) ** 2).mean().item()
     assert 20.0 < 10 * np.log10(1 / mse) < 40.0
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_configuration_sweep(seed):
+    """Seeded random geometry / scale / drop / loss / content / GoP batch:
+    packet bytes, working images and the 9 reconstructed frames of every GoP
+    bit-identical to the oracle (which is pinned to the live reference)."""
+    rng = np.random.default_rng(1000 + seed)
+    H, W = int(rng.integers(42, 181)), int(rng.integers(42, 261))   # static-detail needs >= 42
+    s = int(rng.choice([2, 3]))
+    g = int(rng.integers(1, 4))
+    drop = float(rng.choice([0.0, 0.05, 0.1, 0.25, 0.3]))
+    kinds = ["moving-square", "noisy-motion", "static-detail", "noise-field", "static-gradient"]
+    srcs = [make_clip(kinds[int(rng.integers(len(kinds)))], W, H, 9, seed=int(rng.integers(99))).gop(0)
+            for _ in range(g)]
+    c = GopCodec(g, H, W, s)
+    gop_ids = [int(x) for x in rng.integers(0, 2 ** 32 - 1, size=g, dtype=np.uint64)]
+    c.set_gop_ids(gop_ids)
+    # np.stack keeps the memory order of a transposed clip view: make it C order
+    frames = torch.from_numpy(np.ascontiguousarray(np.stack(srcs))).cuda()
+    c.encode(frames, g, c.drop_k(drop))
+    torch.cuda.synchronize()
+    wires = _wire(c, g)
+    npk = c.n_pkt_per_gop
+    loss = float(rng.choice([0.0, 0.1, 0.3]))
+    lost = [set(int(j) for j in np.flatnonzero(rng.random(npk) < loss)) for _ in range(g)]
+    present = torch.tensor([0 if j in lost[i] else 1 for i in range(g) for j in range(npk)],
+                           dtype=torch.uint8, device="cuda")
+    img = c.decode(g, 0, present=present)
+    out = torch.empty_like(frames)
+    c.reconstruct(g, 0, out)
+    torch.cuda.synchronize()
+    img, out = img.cpu().numpy(), out.cpu().numpy()
+    for i in range(g):
+        ref = O.pipeline_gop(srcs[i], s, gop_id=gop_ids[i], drop_rate=drop, lost=lost[i])
+        assert wires[i] == ref["wire"], (seed, i)
+        assert np.array_equal(img[i, 0], ref["i_img"]) and np.array_equal(img[i, 1], ref["p_img"])
+        assert np.array_equal(out[i], np.stack(ref["frames"])), (seed, i, H, W, s)
+
+
+def test_non_contiguous_frames_are_rejected():
+    H, W = 32, 40
+    c = GopCodec(1, H, W, 2)
+    src = torch.rand((1, 9, W, H, 3), device="cuda").transpose(2, 3)   # [1][9][H][W][3] view
+    with pytest.raises(ValueError, match="contiguous"):
+        c.encode(src, 1)
+    with pytest.raises(ValueError, match="float32"):
+        c.encode(src.contiguous().double(), 1)
