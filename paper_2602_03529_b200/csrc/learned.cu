@@ -631,6 +631,210 @@ __global__ void __launch_bounds__(c233p::THREADS, 1)
   }
 }
 
+// ---- causal (2,3,3) convolution on CTA pairs (cta_group::2) ----------------
+// A cluster of 2 CTAs on one TPC computes a unit of 256 tokens (16x16) x 256
+// output channels with tcgen05.mma.cta_group::2 (M=256, N=256, K=16): CTA r
+// owns the tokens of x-half r (its own 10x18 halo and its 128 accumulator rows)
+// and loads weight rows n = 128r..128r+127 of every k-block; the MMA reads A
+// and B from both CTAs' shared memory at the same offsets.  Per SM and k-step
+// that is 128x256x16 of work for 4 KB of A and 4 KB of B shared-memory reads
+// (the single-CTA kernel needs 8 KB for 128x128x16).  The leader's warp 1 lane
+// 0 issues all MMAs; both CTAs' TMA bytes complete on the leader's barriers
+// (peer bit cleared); commits multicast to both CTAs; the 8 epilogue warps of
+// each CTA drain their own TMEM and arrive on the leader's accumulator-empty
+// barrier through the cluster window.  Two 256-column accumulators per CTA.
+namespace c233c {
+constexpr int TILE = 16, PITCH = 10, HROWS = 18;
+constexpr int HALO_BYTES = PITCH * HROWS * 128;                   // 23040
+constexpr int HALO_STRIDE = (HALO_BYTES + 1023) / 1024 * 1024;    // 23552
+constexpr int BNH = 128;                                          // weight rows per CTA
+constexpr int B_BYTES = BNH * 128;
+constexpr int HSLOTS = 3, BSTAGES = 8;
+constexpr int SMEM = HSLOTS * HALO_STRIDE + BSTAGES * B_BYTES + 1024 + 512;
+constexpr int EPI_WARPS = 8;
+constexpr int THREADS = 64 + EPI_WARPS * 32;
+}  // namespace c233c
+
+__device__ __forceinline__ uint64_t halo_desc_pitch(uint32_t saddr, int pitch) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr & 0x3FFFFu) >> 4);
+  d |= (uint64_t)1 << 16;
+  d |= (uint64_t)((pitch * 128) >> 4) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
+    k_lt_conv233c(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  const ConvArgs a, int n_units) {
+  using namespace c233c;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sH = smem;
+  uint8_t* sB = smem + HSLOTS * HALO_STRIDE;
+  uint64_t* hfull = reinterpret_cast<uint64_t*>(sB + BSTAGES * B_BYTES);
+  uint64_t* hempty = hfull + HSLOTS;
+  uint64_t* bfull = hempty + HSLOTS;
+  uint64_t* bempty = bfull + BSTAGES;
+  uint64_t* afull = bempty + BSTAGES;
+  uint64_t* aempty = afull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(aempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = tc::cluster_ctarank();
+  const bool leader = rank == 0;
+  if (threadIdx.x == 0) {
+    tc::prefetch_tmap(&tmA);
+    tc::prefetch_tmap(&tmB);
+    for (int i = 0; i < HSLOTS; ++i) { mbar_init(&hfull[i], 1); mbar_init(&hempty[i], 1); }
+    for (int i = 0; i < BSTAGES; ++i) { mbar_init(&bfull[i], 1); mbar_init(&bempty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&afull[i], 1); mbar_init(&aempty[i], 2 * EPI_WARPS); }
+    fence_mbar_init();
+  }
+  if (warp == 1) tc::tmem_alloc_pair(tmem_slot, 512);
+  tc::fence_before_sync();
+  tc::cluster_sync();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  const int nh = 2 * a.kb_per_tap;
+  const int C = a.kb_per_tap * BK;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  auto decode = [&](int u, int& g, int& t, int& x0, int& y0) {
+    int tile = u;
+    const int tx = tile % a.tiles_x; tile /= a.tiles_x;
+    const int ty = tile % a.tiles_y; tile /= a.tiles_y;
+    t = a.t_lo + tile % a.t_cnt;
+    g = tile / a.t_cnt;
+    x0 = tx * TILE; y0 = ty * TILE;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---- TMA producer (both CTAs): own halo, own half of the weights ----
+      int hc = 0, bc = 0;
+      for (int u = pair; u < n_units; u += npairs) {
+        int g, t, x0, y0;
+        decode(u, g, t, x0, y0);
+        for (int hi = 0; hi < nh; ++hi, ++hc) {
+          const int kt = hi / a.kb_per_tap, cb = hi - kt * a.kb_per_tap;
+          const int hs = hc % HSLOTS;
+          if (hc >= HSLOTS) mbar_wait(&hempty[hs], ((hc / HSLOTS) - 1) & 1);
+          if (leader) mbar_expect_tx(&hfull[hs], 2 * HALO_BYTES);
+          tc::tma_load_5d_pair(sH + hs * HALO_STRIDE, &tmA, cb * BK, x0 + 8 * (int)rank - 1,
+                               y0 - 1, t + kt - 1, g, &hfull[hs]);
+          for (int sp = 0; sp < 9; ++sp, ++bc) {
+            const int bs = bc % BSTAGES;
+            if (bc >= BSTAGES) mbar_wait(&bempty[bs], ((bc / BSTAGES) - 1) & 1);
+            if (leader) mbar_expect_tx(&bfull[bs], 2 * B_BYTES);
+            tc::tma_load_2d_pair(sB + bs * B_BYTES, &tmB, (kt * 9 + sp) * C + cb * BK,
+                                 (int)rank * BNH, &bfull[bs]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {
+      // ---- MMA issuer (leader only): M=256 across the pair, N=256 ----
+      constexpr uint32_t idesc = tc::idesc_bf16_f32(256, 256);
+      int hc = 0, bc = 0, it = 0;
+      for (int u = pair; u < n_units; u += npairs, ++it) {
+        const int ab = it & 1;
+        if (it >= 2) mbar_wait(&aempty[ab], ((it >> 1) - 1) & 1);
+        tc::fence_after_sync();
+        const uint32_t acc = tmem + ab * 256;
+        for (int hi = 0; hi < nh; ++hi, ++hc) {
+          const int hs = hc % HSLOTS;
+          mbar_wait(&hfull[hs], (hc / HSLOTS) & 1);
+          const uint32_t hbase = smem_u32(sH + hs * HALO_STRIDE);
+          for (int sp = 0; sp < 9; ++sp, ++bc) {
+            const int bs = bc % BSTAGES;
+            mbar_wait(&bfull[bs], (bc / BSTAGES) & 1);
+            tc::fence_after_sync();
+            const int dy = sp / 3, dx = sp % 3;
+            const uint64_t bd = tc::smem_desc_sw128(smem_u32(sB + bs * B_BYTES));
+            const uint64_t ad = halo_desc_pitch(hbase + (uint32_t)((dy * PITCH + dx) * 128), PITCH);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              tc::mma_bf16_pair(acc, ad + 2 * k, bd + 2 * k, idesc, (hi | sp | k) != 0);
+            tc::mma_commit_pair(&bempty[bs]);
+          }
+          tc::mma_commit_pair(&hempty[hs]);
+        }
+        tc::mma_commit_pair(&afull[ab]);
+      }
+    }
+  } else {
+    // ---- epilogue (both CTAs): warp w drains columns 128*((w-2)/4).., lanes 32*(w%4) ----
+    const int e = warp - 2;
+    const int half = e >> 2, q = warp & 3;
+    const int m = q * 32 + lane;
+    const uint32_t aempty_leader = tc::mapa(smem_u32(&aempty[0]), 0);
+    int it = 0;
+    for (int u = pair; u < n_units; u += npairs, ++it) {
+      int g, t, x0, y0;
+      decode(u, g, t, x0, y0);
+      const int ab = it & 1;
+      mbar_wait(&afull[ab], (it >> 1) & 1);
+      tc::fence_after_sync();
+      const int y = y0 + (m >> 3), x = x0 + 8 * (int)rank + (m & 7);
+      const bool valid = y < a.Ht && x < a.Wt;
+      const int n0 = half * 128;
+      const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + ab * 256 + n0;
+      const size_t tok = (((size_t)g * a.out_T + t) * a.Ht + y) * a.Wt + x;
+      __nv_bfloat16* outp = reinterpret_cast<__nv_bfloat16*>(a.frames) + tok * a.N + n0;
+#pragma unroll 1
+      for (int c = 0; c < 128; c += 32) {
+        float v[32];
+        tc::tmem_ld32(trow + c, v);
+        if (c + 32 == 128) {
+          tc::fence_before_sync();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive_cluster(aempty_leader + ab * 8);
+        }
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          v[i] += __ldg(a.bias + n0 + c + i);
+          if (a.act) v[i] = silu(v[i]);
+        }
+        if (!valid) continue;
+        if (a.residual != nullptr) {
+          const uint4* rp = reinterpret_cast<const uint4*>(a.residual + tok * a.N + n0 + c);
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            uint4 uu = __ldg(rp + qq);
+            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&uu);
+#pragma unroll
+            for (int e2 = 0; e2 < 4; ++e2) {
+              float2 f = __bfloat1622float2(h2[e2]);
+              v[qq * 8 + 2 * e2] += f.x;
+              v[qq * 8 + 2 * e2 + 1] += f.y;
+            }
+          }
+        }
+        uint4* op = reinterpret_cast<uint4*>(outp + c);
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+          uint4 uu;
+          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&uu);
+#pragma unroll
+          for (int e2 = 0; e2 < 4; ++e2)
+            h2[e2] = __floats2bfloat162_rn(v[qq * 8 + 2 * e2], v[qq * 8 + 2 * e2 + 1]);
+          op[qq] = uu;
+        }
+      }
+    }
+  }
+  tc::fence_before_sync();
+  tc::cluster_sync();
+  if (warp == 1) {
+    __syncwarp();
+    tc::tmem_dealloc_pair(tmem, 512);
+  }
+}
+
 // ---- causal spatio-temporal window attention (the attention core) ---------
 // Q, K, V come from one tcgen05 1x1 projection (qkv [G][2][H'][W'][3D], channel
 // = part*D + head*64 + d).  A CTA owns one 8x8 token window of one GoP and one
@@ -1087,6 +1291,48 @@ static int launch_conv233p(const SstConvDesc* d, cudaStream_t st) {
   return SST_OK;
 }
 
+static int launch_conv233c(const SstConvDesc* d, cudaStream_t st) {
+  if (d->N != 256 || d->t_lo != 0 || d->t_cnt != d->in_T || d->in_T != d->out_T ||
+      d->in_W != d->Wt || d->in_H != d->Ht)
+    return SST_ERR_ARG;
+  CUtensorMap tmA, tmB;
+  memset(&tmA, 0, sizeof(tmA));
+  memset(&tmB, 0, sizeof(tmB));
+  const uint64_t adims[5] = {(uint64_t)d->in_C, (uint64_t)d->in_W, (uint64_t)d->in_H,
+                             (uint64_t)d->in_T, (uint64_t)d->G};
+  if (!make_tmap_bf16_5d(&tmA, d->in, adims, c233c::PITCH, c233c::HROWS)) return SST_ERR_ARG;
+  if (!make_tmap_bf16_2d(&tmB, d->weight, (uint64_t)d->K, (uint64_t)d->N, c233c::BNH))
+    return SST_ERR_ARG;
+  ConvArgs a;
+  memset(&a, 0, sizeof(a));
+  a.Ht = d->Ht; a.Wt = d->Wt;
+  a.tiles_x = ceil_div(d->Wt, c233c::TILE);
+  a.tiles_y = ceil_div(d->Ht, c233c::TILE);
+  a.t_lo = 0; a.t_cnt = d->t_cnt;
+  a.n_taps = 18;
+  a.kb_per_tap = d->in_C / BK;
+  a.N = d->N;
+  a.out_T = d->out_T;
+  a.bias = d->bias;
+  a.act = d->act;
+  a.residual = static_cast<const __nv_bfloat16*>(d->residual);
+  a.frames = static_cast<float*>(d->out);
+  const int64_t units = (int64_t)d->G * d->t_cnt * a.tiles_y * a.tiles_x;
+  if (units <= 0 || units > 0x7fffffff) return SST_ERR_ARG;
+  static int n_sm = 0;
+  if (n_sm == 0) {
+    int dev = 0;
+    SST_CUDA_TRY(cudaGetDevice(&dev));
+    SST_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int64_t pairs = units < n_sm / 2 ? units : n_sm / 2;
+  SST_CUDA_TRY(cudaFuncSetAttribute(k_lt_conv233c, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    c233c::SMEM));
+  k_lt_conv233c<<<(unsigned)(2 * pairs), c233c::THREADS, c233c::SMEM, st>>>(tmA, tmB, a, (int)units);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
 static int launch_conv233(const SstConvDesc* d, cudaStream_t st) {
   if (d->N % c233::BN != 0 || d->t_lo != 0 || d->t_cnt != d->in_T || d->in_T != d->out_T ||
       d->in_W != d->Wt || d->in_H != d->Ht)
@@ -1141,13 +1387,17 @@ extern "C" int sst_lt_conv(const SstConvDesc* d, void* stream) {
   switch (d->epi) {
     case SST_LT_EPI_STORE: {
       if (!d->out || d->act < 0 || d->act > 1) return SST_ERR_ARG;
-      // SST_LT_CONV=generic forces the per-tap kernel, =halo the
-      // non-persistent halo kernel (A/B comparisons)
+      // Default for the causal (2,3,3) convs: the CTA-pair kernel (N = 256) or
+      // the persistent single-CTA kernel (other N).  A/B switches:
+      // SST_LT_CONV=persistent / halo (non-persistent) / generic (per-tap loads)
       const char* mode = getenv("SST_LT_CONV");
       const bool generic = mode && mode[0] == 'g';
       const bool halo1 = mode && mode[0] == 'h';
-      if (!generic && lt::is_taps233(d) && d->N % lt::c233::BN == 0)
+      const bool single = mode && mode[0] == 'p';
+      if (!generic && lt::is_taps233(d) && d->N % lt::c233::BN == 0) {
+        if (!single && !halo1 && d->N == 256) return lt::launch_conv233c(d, st);
         return halo1 ? lt::launch_conv233(d, st) : lt::launch_conv233p(d, st);
+      }
       return lt::launch_conv<128, SST_LT_EPI_STORE>(d, st);
     }
     case SST_LT_EPI_FSQ:

@@ -13,8 +13,8 @@ for shape, cin in [((2, 2, 16, 16, 64), 64), ((1, 2, 45, 80, 256), 256), ((2, 2,
     b = _bf(rng.standard_normal(256) * 0.1).numpy()
     resid = _bf(rng.standard_normal((G, Tn, H, Wd, 256)))
     want = LO.conv233(x, W, b, act=True, residual=resid)
-    for mode in ("g", "h", "p"):
-        os.environ["SST_LT_CONV"] = {"g": "generic", "h": "halo", "p": "persistent"}[mode]
+    for mode in ("p", "c"):
+        os.environ["SST_LT_CONV"] = {"g": "generic", "h": "halo", "p": "persistent", "c": "cluster"}[mode]
         got = _conv_gpu(x, W, b, TAPS_233, 0, 2, _lib.LT_EPI_STORE, act=1, residual=resid)["out"]
         err = (got - want).abs()
         print(shape, "mode", mode, "exact", (got == want).float().mean().item(), "max err", err.max().item())

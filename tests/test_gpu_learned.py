@@ -108,9 +108,11 @@ def test_conv233_store_matches_oracle(shape, cin, act, res):
     ((2, 2, 13, 37, 64), 64),                # ragged in both dimensions
 ])
 def test_conv233_halo_kernel(shape, cin, monkeypatch):
-    """N = 256 runs the halo-reuse kernel (one TMA box per 9 spatial taps,
-    UMMA descriptors starting mid swizzle atom); it must match the oracle and
-    the generic per-tap kernel."""
+    """N = 256 runs the CTA-pair halo kernel (cta_group::2, one TMA box per 9
+    spatial taps, UMMA descriptors starting mid swizzle atom); it must match
+    the oracle, and the persistent single-CTA and non-persistent halo kernels
+    bit for bit (same MMA order per output), and the per-tap kernel to the
+    oracle tolerance."""
     rng = np.random.default_rng(11)
     G, Tn, H, Wd, _ = shape
     x = _bf(rng.standard_normal(shape))
@@ -118,11 +120,13 @@ def test_conv233_halo_kernel(shape, cin, monkeypatch):
     b = _bf(rng.standard_normal(256) * 0.1).numpy()
     resid = _bf(rng.standard_normal((G, Tn, H, Wd, 256)))
     want = LO.conv233(x, W, b, act=True, residual=resid)
-    halo = _conv_gpu(x, W, b, TAPS_233, 0, 2, _lib.LT_EPI_STORE, act=1, residual=resid)["out"]
-    _assert_bf16_close(halo, want)
-    monkeypatch.setenv("SST_LT_CONV", "generic")
-    gen = _conv_gpu(x, W, b, TAPS_233, 0, 2, _lib.LT_EPI_STORE, act=1, residual=resid)["out"]
-    _assert_bf16_close(gen, want)
+    pair = _conv_gpu(x, W, b, TAPS_233, 0, 2, _lib.LT_EPI_STORE, act=1, residual=resid)["out"]
+    _assert_bf16_close(pair, want)                       # default: CTA-pair kernel
+    for mode in ("persistent", "halo", "generic"):
+        monkeypatch.setenv("SST_LT_CONV", mode)
+        got = _conv_gpu(x, W, b, TAPS_233, 0, 2, _lib.LT_EPI_STORE, act=1, residual=resid)["out"]
+        _assert_bf16_close(got, want)
+        assert torch.equal(got, pair) or mode == "generic"
 
 
 @pytest.mark.parametrize("H,W,D", [(8, 8, 128), (13, 21, 256), (45, 80, 256)])
