@@ -730,7 +730,7 @@ def run_learned(a, device) -> dict:
                     f"{int(a.drop * 100)}% intelligent drop, blend n=2; random-init weights",
         "value": round(G * GOP / ms * 1e3, 1), "unit": UNIT, "ms_per_step": round(ms, 3),
         "tensor_tflops_path": round(flops_step / ms / 1e9, 1),
-        "roofline": {"kernel": "k_lt_conv233c (causal (2,3,3) conv, CTA-pair tcgen05 implicit GEMM)",
+        "roofline": {"kernel": "k_lt_convpair<true> (causal (2,3,3) conv, CTA-pair tcgen05 implicit GEMM)",
                      "bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
                      "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "peak_source": src,
                      "flops_per_launch": halo and int(sum(fl for _, fl in halo) / len(halo)),

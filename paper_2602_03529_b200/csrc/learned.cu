@@ -645,7 +645,7 @@ __global__ void __launch_bounds__(c233p::THREADS, 1)
 // barrier through the cluster window.  Two 256-column accumulators per CTA.
 namespace c233c {
 constexpr int TILE = 16, PITCH = 10, HROWS = 18;
-constexpr int HALO_BYTES = PITCH * HROWS * 128;                   // 23040
+constexpr int HALO_BYTES = PITCH * HROWS * 128;                   // 23040 (1x1: 8x16 box, 16384)
 constexpr int HALO_STRIDE = (HALO_BYTES + 1023) / 1024 * 1024;    // 23552
 constexpr int BNH = 128;                                          // weight rows per CTA
 constexpr int B_BYTES = BNH * 128;
@@ -665,10 +665,17 @@ __device__ __forceinline__ uint64_t halo_desc_pitch(uint32_t saddr, int pitch) {
   return d;
 }
 
+// kHalo = true: causal (2,3,3) conv (2 temporal taps x 9 spatial taps per
+// halo); false: 1x1 conv / GEMM (one tap, an 8x16 token box per CTA, temporal
+// offset taps[0][0]).  A unit covers 256 output channels n_blk*256..+255.
+template <bool kHalo>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
-    k_lt_conv233c(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                  const ConvArgs a, int n_units) {
+    k_lt_convpair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  const ConvArgs a, int n_units, int n_blocks) {
   using namespace c233c;
+  constexpr int kPitch = kHalo ? PITCH : 8;
+  constexpr int kBoxBytes = kHalo ? HALO_BYTES : 8 * 16 * 128;
+  constexpr int kSpatial = kHalo ? 9 : 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -699,11 +706,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
 
-  const int nh = 2 * a.kb_per_tap;
+  const int nh = (kHalo ? 2 : 1) * a.kb_per_tap;
   const int C = a.kb_per_tap * BK;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
-  auto decode = [&](int u, int& g, int& t, int& x0, int& y0) {
-    int tile = u;
+  auto decode = [&](int u, int& g, int& t, int& x0, int& y0, int& nb) {
+    int tile = u / n_blocks;
+    nb = u - tile * n_blocks;
     const int tx = tile % a.tiles_x; tile /= a.tiles_x;
     const int ty = tile % a.tiles_y; tile /= a.tiles_y;
     t = a.t_lo + tile % a.t_cnt;
@@ -716,21 +724,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
       // ---- TMA producer (both CTAs): own halo, own half of the weights ----
       int hc = 0, bc = 0;
       for (int u = pair; u < n_units; u += npairs) {
-        int g, t, x0, y0;
-        decode(u, g, t, x0, y0);
+        int g, t, x0, y0, nb;
+        decode(u, g, t, x0, y0, nb);
         for (int hi = 0; hi < nh; ++hi, ++hc) {
           const int kt = hi / a.kb_per_tap, cb = hi - kt * a.kb_per_tap;
           const int hs = hc % HSLOTS;
           if (hc >= HSLOTS) mbar_wait(&hempty[hs], ((hc / HSLOTS) - 1) & 1);
-          if (leader) mbar_expect_tx(&hfull[hs], 2 * HALO_BYTES);
-          tc::tma_load_5d_pair(sH + hs * HALO_STRIDE, &tmA, cb * BK, x0 + 8 * (int)rank - 1,
-                               y0 - 1, t + kt - 1, g, &hfull[hs]);
-          for (int sp = 0; sp < 9; ++sp, ++bc) {
+          if (leader) mbar_expect_tx(&hfull[hs], 2 * kBoxBytes);
+          if (kHalo)
+            tc::tma_load_5d_pair(sH + hs * HALO_STRIDE, &tmA, cb * BK, x0 + 8 * (int)rank - 1,
+                                 y0 - 1, t + kt - 1, g, &hfull[hs]);
+          else
+            tc::tma_load_5d_pair(sH + hs * HALO_STRIDE, &tmA, cb * BK, x0 + 8 * (int)rank, y0,
+                                 t + a.taps[0][0], g, &hfull[hs]);
+          for (int sp = 0; sp < kSpatial; ++sp, ++bc) {
             const int bs = bc % BSTAGES;
             if (bc >= BSTAGES) mbar_wait(&bempty[bs], ((bc / BSTAGES) - 1) & 1);
             if (leader) mbar_expect_tx(&bfull[bs], 2 * B_BYTES);
-            tc::tma_load_2d_pair(sB + bs * B_BYTES, &tmB, (kt * 9 + sp) * C + cb * BK,
-                                 (int)rank * BNH, &bfull[bs]);
+            tc::tma_load_2d_pair(sB + bs * B_BYTES, &tmB, (kt * kSpatial + sp) * C + cb * BK,
+                                 nb * 256 + (int)rank * BNH, &bfull[bs]);
           }
         }
       }
@@ -749,13 +761,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
           const int hs = hc % HSLOTS;
           mbar_wait(&hfull[hs], (hc / HSLOTS) & 1);
           const uint32_t hbase = smem_u32(sH + hs * HALO_STRIDE);
-          for (int sp = 0; sp < 9; ++sp, ++bc) {
+          for (int sp = 0; sp < kSpatial; ++sp, ++bc) {
             const int bs = bc % BSTAGES;
             mbar_wait(&bfull[bs], (bc / BSTAGES) & 1);
             tc::fence_after_sync();
             const int dy = sp / 3, dx = sp % 3;
             const uint64_t bd = tc::smem_desc_sw128(smem_u32(sB + bs * B_BYTES));
-            const uint64_t ad = halo_desc_pitch(hbase + (uint32_t)((dy * PITCH + dx) * 128), PITCH);
+            const uint64_t ad = halo_desc_pitch(hbase + (uint32_t)((dy * kPitch + dx) * 128), kPitch);
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
               tc::mma_bf16_pair(acc, ad + 2 * k, bd + 2 * k, idesc, (hi | sp | k) != 0);
@@ -774,15 +786,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
     const uint32_t aempty_leader = tc::mapa(smem_u32(&aempty[0]), 0);
     int it = 0;
     for (int u = pair; u < n_units; u += npairs, ++it) {
-      int g, t, x0, y0;
-      decode(u, g, t, x0, y0);
+      int g, t, x0, y0, nb;
+      decode(u, g, t, x0, y0, nb);
       const int ab = it & 1;
       mbar_wait(&afull[ab], (it >> 1) & 1);
       tc::fence_after_sync();
       const int y = y0 + (m >> 3), x = x0 + 8 * (int)rank + (m & 7);
       const bool valid = y < a.Ht && x < a.Wt;
-      const int n0 = half * 128;
-      const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + ab * 256 + n0;
+      const int n0 = nb * 256 + half * 128;
+      const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + ab * 256 + half * 128;
       const size_t tok = (((size_t)g * a.out_T + t) * a.Ht + y) * a.Wt + x;
       __nv_bfloat16* outp = reinterpret_cast<__nv_bfloat16*>(a.frames) + tok * a.N + n0;
 #pragma unroll 1
@@ -1291,16 +1303,17 @@ static int launch_conv233p(const SstConvDesc* d, cudaStream_t st) {
   return SST_OK;
 }
 
-static int launch_conv233c(const SstConvDesc* d, cudaStream_t st) {
-  if (d->N != 256 || d->t_lo != 0 || d->t_cnt != d->in_T || d->in_T != d->out_T ||
-      d->in_W != d->Wt || d->in_H != d->Ht)
-    return SST_ERR_ARG;
+static int launch_convpair(const SstConvDesc* d, cudaStream_t st, bool halo) {
+  if (d->N % 256 != 0 || d->in_W != d->Wt || d->in_H != d->Ht) return SST_ERR_ARG;
+  if (halo && (d->t_lo != 0 || d->t_cnt != d->in_T || d->in_T != d->out_T)) return SST_ERR_ARG;
+  if (!halo && (d->n_taps != 1 || d->taps[0][1] != 0 || d->taps[0][2] != 0)) return SST_ERR_ARG;
   CUtensorMap tmA, tmB;
   memset(&tmA, 0, sizeof(tmA));
   memset(&tmB, 0, sizeof(tmB));
   const uint64_t adims[5] = {(uint64_t)d->in_C, (uint64_t)d->in_W, (uint64_t)d->in_H,
                              (uint64_t)d->in_T, (uint64_t)d->G};
-  if (!make_tmap_bf16_5d(&tmA, d->in, adims, c233c::PITCH, c233c::HROWS)) return SST_ERR_ARG;
+  if (!make_tmap_bf16_5d(&tmA, d->in, adims, halo ? c233c::PITCH : 8, halo ? c233c::HROWS : 16))
+    return SST_ERR_ARG;
   if (!make_tmap_bf16_2d(&tmB, d->weight, (uint64_t)d->K, (uint64_t)d->N, c233c::BNH))
     return SST_ERR_ARG;
   ConvArgs a;
@@ -1308,8 +1321,10 @@ static int launch_conv233c(const SstConvDesc* d, cudaStream_t st) {
   a.Ht = d->Ht; a.Wt = d->Wt;
   a.tiles_x = ceil_div(d->Wt, c233c::TILE);
   a.tiles_y = ceil_div(d->Ht, c233c::TILE);
-  a.t_lo = 0; a.t_cnt = d->t_cnt;
-  a.n_taps = 18;
+  a.t_lo = d->t_lo; a.t_cnt = d->t_cnt;
+  a.n_taps = d->n_taps;
+  for (int i = 0; i < d->n_taps; ++i)
+    for (int j = 0; j < 3; ++j) a.taps[i][j] = (signed char)d->taps[i][j];
   a.kb_per_tap = d->in_C / BK;
   a.N = d->N;
   a.out_T = d->out_T;
@@ -1317,7 +1332,8 @@ static int launch_conv233c(const SstConvDesc* d, cudaStream_t st) {
   a.act = d->act;
   a.residual = static_cast<const __nv_bfloat16*>(d->residual);
   a.frames = static_cast<float*>(d->out);
-  const int64_t units = (int64_t)d->G * d->t_cnt * a.tiles_y * a.tiles_x;
+  const int n_blocks = d->N / 256;
+  const int64_t units = (int64_t)d->G * d->t_cnt * a.tiles_y * a.tiles_x * n_blocks;
   if (units <= 0 || units > 0x7fffffff) return SST_ERR_ARG;
   static int n_sm = 0;
   if (n_sm == 0) {
@@ -1326,9 +1342,10 @@ static int launch_conv233c(const SstConvDesc* d, cudaStream_t st) {
     SST_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
   }
   const int64_t pairs = units < n_sm / 2 ? units : n_sm / 2;
-  SST_CUDA_TRY(cudaFuncSetAttribute(k_lt_conv233c, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    c233c::SMEM));
-  k_lt_conv233c<<<(unsigned)(2 * pairs), c233c::THREADS, c233c::SMEM, st>>>(tmA, tmB, a, (int)units);
+  auto kern = halo ? k_lt_convpair<true> : k_lt_convpair<false>;
+  SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, c233c::SMEM));
+  kern<<<(unsigned)(2 * pairs), c233c::THREADS, c233c::SMEM, st>>>(tmA, tmB, a, (int)units,
+                                                                   n_blocks);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }
@@ -1395,8 +1412,17 @@ extern "C" int sst_lt_conv(const SstConvDesc* d, void* stream) {
       const bool halo1 = mode && mode[0] == 'h';
       const bool single = mode && mode[0] == 'p';
       if (!generic && lt::is_taps233(d) && d->N % lt::c233::BN == 0) {
-        if (!single && !halo1 && d->N == 256) return lt::launch_conv233c(d, st);
+        if (!single && !halo1 && d->N % 256 == 0) return lt::launch_convpair(d, st, true);
         return halo1 ? lt::launch_conv233(d, st) : lt::launch_conv233p(d, st);
+      }
+      // long-K 1x1 layers (K >= 1024: the P patch embedding) with N % 256 == 0:
+      // the CTA-pair kernel without halo.  Short-K 1x1 layers (qkv / proj,
+      // K = 256) are store-bound and keep the tile kernel's swizzled TMA-store
+      // epilogue (measured: qkv 0.30 ms tile kernel vs 0.46 ms pair kernel).
+      if (!generic && d->n_taps == 1 && d->taps[0][1] == 0 && d->taps[0][2] == 0 &&
+          d->N % 256 == 0 && d->in_C >= 1024 && d->in_W == d->Wt && d->in_H == d->Ht) {
+        const char* m1 = getenv("SST_LT_GEMM");
+        if (!(m1 && m1[0] == 't')) return lt::launch_convpair(d, st, false);
       }
       return lt::launch_conv<128, SST_LT_EPI_STORE>(d, st);
     }
