@@ -52,6 +52,7 @@ struct ConvArgs {
   const float* bias;
   int act;
   const __nv_bfloat16* residual;
+  __nv_bfloat16* out;          // STORE output of the halo / CTA-pair kernels (direct stores)
   double* codes;
   int32_t* idx;
   uint8_t* mask;
@@ -401,7 +402,7 @@ __global__ void __launch_bounds__(c233::THREADS, 1)
   const bool valid = y < a.Ht && x < a.Wt;
   const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + half * BN;
   const size_t tok = (((size_t)g * a.out_T + t) * a.Ht + y) * a.Wt + x;
-  __nv_bfloat16* outp = reinterpret_cast<__nv_bfloat16*>(a.frames) + tok * a.N + n0;  // out tensor
+  __nv_bfloat16* outp = a.out + tok * a.N + n0;
 #pragma unroll 1
   for (int c = 0; c < BN; c += 32) {
     float v[32];
@@ -579,7 +580,7 @@ __global__ void __launch_bounds__(c233p::THREADS, 1)
       const bool valid = y < a.Ht && x < a.Wt;
       const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + ab * 256 + half * BN;
       const size_t tok = (((size_t)g * a.out_T + t) * a.Ht + y) * a.Wt + x;
-      __nv_bfloat16* outp = reinterpret_cast<__nv_bfloat16*>(a.frames) + tok * a.N + n0;
+      __nv_bfloat16* outp = a.out + tok * a.N + n0;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         float v[32];
@@ -796,7 +797,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
       const int n0 = nb * 256 + half * 128;
       const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + ab * 256 + half * 128;
       const size_t tok = (((size_t)g * a.out_T + t) * a.Ht + y) * a.Wt + x;
-      __nv_bfloat16* outp = reinterpret_cast<__nv_bfloat16*>(a.frames) + tok * a.N + n0;
+      __nv_bfloat16* outp = a.out + tok * a.N + n0;
 #pragma unroll 1
       for (int c = 0; c < 128; c += 32) {
         float v[32];
@@ -1285,7 +1286,7 @@ static int launch_conv233p(const SstConvDesc* d, cudaStream_t st) {
   a.bias = d->bias;
   a.act = d->act;
   a.residual = static_cast<const __nv_bfloat16*>(d->residual);
-  a.frames = static_cast<float*>(d->out);   // carries the bf16 output pointer
+  a.out = static_cast<__nv_bfloat16*>(d->out);
   const int n_halves = d->N / c233p::BN;
   const int64_t units = (int64_t)d->G * d->t_cnt * a.tiles_y * a.tiles_x * n_halves;
   if (units <= 0 || units > 0x7fffffff) return SST_ERR_ARG;
@@ -1331,7 +1332,7 @@ static int launch_convpair(const SstConvDesc* d, cudaStream_t st, bool halo) {
   a.bias = d->bias;
   a.act = d->act;
   a.residual = static_cast<const __nv_bfloat16*>(d->residual);
-  a.frames = static_cast<float*>(d->out);
+  a.out = static_cast<__nv_bfloat16*>(d->out);
   const int n_blocks = d->N / 256;
   const int64_t units = (int64_t)d->G * d->t_cnt * a.tiles_y * a.tiles_x * n_blocks;
   if (units <= 0 || units > 0x7fffffff) return SST_ERR_ARG;
@@ -1374,7 +1375,7 @@ static int launch_conv233(const SstConvDesc* d, cudaStream_t st) {
   a.bias = d->bias;
   a.act = d->act;
   a.residual = static_cast<const __nv_bfloat16*>(d->residual);
-  a.frames = static_cast<float*>(d->out);   // carries the bf16 output pointer
+  a.out = static_cast<__nv_bfloat16*>(d->out);
   const int64_t mt = (int64_t)d->G * d->t_cnt * a.tiles_y * a.tiles_x;
   if (mt <= 0 || mt > 0x7fffffff) return SST_ERR_ARG;
   dim3 grid((unsigned)mt, d->N / c233::BN);
