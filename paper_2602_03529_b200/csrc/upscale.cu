@@ -529,6 +529,195 @@ __global__ void __launch_bounds__(kTQ)
   if (tid == 0) tma_store_wait_read();
 }
 
+// ---- K5-9, kF frames per pass, direct stores ----
+// The CTA loads the source windows of kF frames (and the previous GoP's
+// frames for blended ones) in ONE load phase -- kF x the bytes in flight of
+// the one-frame-per-pass kernel -- then interpolates the kF frames with shared
+// row-cache control and writes rows with coalesced streaming stores.
+template <int kBand, int kF>
+struct Up9fSmem {
+  static constexpr int kWR = kBand / 2 + 2;
+  float win[kF][kWR][kWF];
+  float winp[4][kWR][kWF];          // previous GoP's frames 9-n+f, f < n <= 4
+  AxisTap ty_c[kBand], ty_p[kBand];
+  int wx0[2], wx1[2];
+};
+
+// One pass over NF consecutive frames f0..f0+NF-1 of the CTA's (column tile,
+// band): load their windows (and, when BLEND, the previous GoP's frames
+// 9-n+f) in one phase, then interpolate all NF frames per output row with the
+// row-cache control shared, and stream the rows out.
+template <int kBand, int kF, int NF, bool BLEND, int kN>
+__device__ __forceinline__ void k5_9_pass(Up9fSmem<kBand, kF>& S, const UpArgs& a,
+                                          const SstPrevDesc& pd, int g, int f0, int q0, int oy0,
+                                          int rows, const AxisTap& tx, int xl, int xh,
+                                          const AxisTap& txp, int pxl, int pxh, bool col_ok) {
+  const int tid = threadIdx.x;
+  const int r0 = S.ty_c[0].lo, r1 = S.ty_c[rows - 1].hi;
+  const int pr0 = BLEND ? S.ty_p[0].lo : 0, pr1 = BLEND ? S.ty_p[rows - 1].hi : 0;
+  const int64_t fimg = (int64_t)a.h * a.w * 3;
+  const float* cur = a.img + ((int64_t)g * kGop + f0) * fimg;
+  __syncthreads();                                  // previous pass done with the windows
+#pragma unroll
+  for (int j = 0; j < NF; ++j)
+    load_window(&S.win[j][0][0], cur + (int64_t)j * fimg, a.w, r0, r1, S.wx0[0] * 3,
+                S.wx1[0] * 3 + 3, tid);
+  if (BLEND) {
+    const int64_t pimg = (int64_t)pd.h * pd.w * 3;
+#pragma unroll
+    for (int j = 0; j < NF; ++j)
+      load_window(&S.winp[j][0][0], pd.p_img + (int64_t)(kGop - kN + f0 + j) * pimg, pd.w, pr0,
+                  pr1, S.wx0[1] * 3, S.wx1[1] * 3 + 3, tid);
+  }
+  __syncthreads();
+  if (!col_ok) return;
+  const int64_t orow = (int64_t)a.W * 3;
+  int ya = -1, yb = -1, qa = -1, qb = -1;
+  double ia[NF], ib[NF], qva[BLEND ? NF : 1], qvb[BLEND ? NF : 1];
+#pragma unroll
+  for (int j = 0; j < NF; ++j) ia[j] = ib[j] = 0.0;
+  for (int r = 0; r < rows; ++r) {
+    const AxisTap ty = S.ty_c[r];
+    if (ty.lo != ya) {
+      if (ty.lo == yb) {
+#pragma unroll
+        for (int j = 0; j < NF; ++j) ia[j] = ib[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+          const float* wr = &S.win[j][ty.lo - r0][0];
+          ia[j] = (double)wr[xl] * tx.g + (double)wr[xh] * tx.f;
+        }
+      }
+      ya = ty.lo;
+    }
+    if (ty.hi != yb) {
+      if (ty.hi == ya) {
+#pragma unroll
+        for (int j = 0; j < NF; ++j) ib[j] = ia[j];
+      } else {
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+          const float* wr = &S.win[j][ty.hi - r0][0];
+          ib[j] = (double)wr[xl] * tx.g + (double)wr[xh] * tx.f;
+        }
+      }
+      yb = ty.hi;
+    }
+    AxisTap tp = ty;
+    if (BLEND) {
+      tp = S.ty_p[r];
+      if (tp.lo != qa) {
+        if (tp.lo == qb) {
+#pragma unroll
+          for (int j = 0; j < NF; ++j) qva[j] = qvb[j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < NF; ++j) {
+            const float* wq = &S.winp[j][tp.lo - pr0][0];
+            qva[j] = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
+          }
+        }
+        qa = tp.lo;
+      }
+      if (tp.hi != qb) {
+        if (tp.hi == qa) {
+#pragma unroll
+          for (int j = 0; j < NF; ++j) qvb[j] = qva[j];
+        } else {
+#pragma unroll
+          for (int j = 0; j < NF; ++j) {
+            const float* wq = &S.winp[j][tp.hi - pr0][0];
+            qvb[j] = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
+          }
+        }
+        qb = tp.hi;
+      }
+    }
+    float* op = a.out + ((int64_t)(g * kGop + f0) * a.H + oy0 + r) * orow + q0 + tid;
+#pragma unroll
+    for (int j = 0; j < NF; ++j) {
+      const float ui = (float)clip_hi1(ia[j] * ty.g + ib[j] * ty.f);
+      float v = ui;
+      if (BLEND) {
+        const double dq = (double)(float)clip_hi1(qva[j] * tp.g + qvb[j] * tp.f);
+        v = (float)clip_hi1(a.alpha[f0 + j] * dq + a.beta[f0 + j] * (double)ui);
+      }
+      __stcs(op + (int64_t)j * a.H * orow, v);
+    }
+  }
+}
+
+template <int kBand, int kF, bool kPrev, int kN>
+__global__ void __launch_bounds__(kTQ)
+    k_upscale9f(const __grid_constant__ UpArgs a) {
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  Up9fSmem<kBand, kF>& S = *reinterpret_cast<Up9fSmem<kBand, kF>*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int q0 = blockIdx.x * kTQ;
+  const int oy0 = blockIdx.y * kBand;
+  const int g = blockIdx.z;
+  SstPrevDesc pd;
+  pd.p_img = nullptr;
+  pd.h = pd.w = pd.s = 1;
+  if (kPrev) pd = a.prev[g];
+  const bool has_prev = kPrev && pd.p_img != nullptr;
+  const int rows = min(kBand, a.H - oy0);
+  const int qlast = min(q0 + kTQ, a.W * 3) - 1;
+  if (tid < kBand) S.ty_c[tid] = axis_tap(oy0 + min(tid, rows - 1), a.h, a.s);
+  else if (tid < 2 * kBand) {
+    if (has_prev) S.ty_p[tid - kBand] = axis_tap(oy0 + min(tid - kBand, rows - 1), pd.h, pd.s);
+  } else if (tid == 2 * kBand) {
+    S.wx0[0] = axis_tap(q0 / 3, a.w, a.s).lo;
+    S.wx1[0] = axis_tap(qlast / 3, a.w, a.s).hi;
+  } else if (tid == 2 * kBand + 32 && has_prev) {
+    S.wx0[1] = axis_tap(q0 / 3, pd.w, pd.s).lo;
+    S.wx1[1] = axis_tap(qlast / 3, pd.w, pd.s).hi;
+  }
+  __syncthreads();
+  const int q = min(q0 + tid, a.W * 3 - 1);
+  const int ox = q / 3, ch = q - ox * 3;
+  const AxisTap tx = axis_tap(ox, a.w, a.s);
+  const int xl = (tx.lo - S.wx0[0]) * 3 + ch, xh = (tx.hi - S.wx0[0]) * 3 + ch;
+  AxisTap txp = tx;
+  int pxl = 0, pxh = 0;
+  if (has_prev) {
+    txp = axis_tap(ox, pd.w, pd.s);
+    pxl = (txp.lo - S.wx0[1]) * 3 + ch;
+    pxh = (txp.hi - S.wx0[1]) * 3 + ch;
+  }
+  const bool col_ok = q0 + tid < a.W * 3;
+  if (kPrev && has_prev) {
+    k5_9_pass<kBand, kF, kN, true, kN>(S, a, pd, g, 0, q0, oy0, rows, tx, xl, xh, txp, pxl, pxh,
+                                       col_ok);
+    k5_9_pass<kBand, kF, kGop - kN, false, kN>(S, a, pd, g, kN, q0, oy0, rows, tx, xl, xh, txp,
+                                               pxl, pxh, col_ok);
+  } else {
+    k5_9_pass<kBand, kF, kGop, false, kN>(S, a, pd, g, 0, q0, oy0, rows, tx, xl, xh, txp, pxl, pxh,
+                                          col_ok);
+  }
+}
+
+template <int BAND, int F>
+static int launch_k5_9f(const UpArgs& a, const SstPrevDesc* prev, int blend_n, cudaStream_t st) {
+  dim3 grid(ceil_div(a.W * 3, kTQ), ceil_div(a.H, BAND), a.G);
+  if (grid.y > 65535) return SST_ERR_ARG;
+  const int smem = (int)sizeof(Up9fSmem<BAND, F>);
+  auto kern = k_upscale9f<BAND, F, false, 1>;
+  if (prev) {
+    switch (blend_n) {
+      case 1: kern = k_upscale9f<BAND, F, true, 1>; break;
+      case 2: kern = k_upscale9f<BAND, F, true, 2>; break;
+      case 3: kern = k_upscale9f<BAND, F, true, 3>; break;
+      default: kern = k_upscale9f<BAND, F, true, 4>; break;
+    }
+  }
+  SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<grid, kTQ, smem, st>>>(a);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
 // ---- standalone kernels ----
 template <typename Tin, typename Tout, bool kClip>
 __global__ void k_upscale(const Tin* __restrict__ img, int64_t n, int h, int w, int s, int ch_out,
@@ -707,11 +896,19 @@ extern "C" int sst_upscale_blend9(const float* img, int G, int h, int w, int s, 
   // tiles 1 | 2 | 6, p = register prefetch of the next frame's window).
   int band = 32, slots = 2;
   bool pre = false;
-  // default 32-row bands, one tile set (k5_9_micro: 2.37 / 2.88 ms per
-  // 32-GoP launch at s=3 without / with blend; a column-private variant with
-  // per-thread horizontal taps and direct stores measured 3.0 / 4.1 ms)
+  // Measured (k5_9_micro, 32 x 1080p GoPs, s=3, without / with blend):
+  // nine frames per CTA with 16-row bands and direct stores 1.89 / 2.62 ms
+  // (default); the one-frame-per-pass TMA-store kernel ("32,1") 2.37 / 2.88;
+  // a column-private variant 3.0 / 4.1; nine frames with 32-row bands 3.5 / 4.8.
   slots = 1;
-  if (const char* v = getenv("SST_K5_9")) {
+  const char* v9 = getenv("SST_K5_9");
+  if (!v9 || v9[0] == 'f') {    // default: all 9 frames per CTA ("f9[,band]"), direct stores
+    const char* c = v9 ? strchr(v9, ',') : nullptr;
+    const int B = c ? atoi(c + 1) : 16;
+    return B == 32 ? launch_k5_9f<32, 9>(a, prev, blend_n, st)
+                   : launch_k5_9f<16, 9>(a, prev, blend_n, st);
+  }
+  if (const char* v = v9) {
     band = atoi(v) == 16 ? 16 : 32;
     const char* c = strchr(v, ',');
     if (c) { slots = atoi(c + 1); pre = strchr(c, 'p') != nullptr; }
