@@ -88,3 +88,40 @@ def test_sass_is_sm100a_with_tma(lib):
     sass = subprocess.run([cuobjdump, "-sass", str(_lib.LIB_PATH)], capture_output=True,
                           text=True).stdout
     assert "UTMALDG" in sass           # cp.async.bulk.tensor loads in the encoder
+
+
+def test_learned_entry_point_argument_errors(lib):
+    """sst_lt_* validate their descriptors before any CUDA call."""
+    from paper_2602_03529_b200 import _lib
+    d = _lib.SstConvDesc()
+    assert lib.sst_lt_conv(ctypes.byref(d), None) == -1               # null pointers
+    d.in_, d.weight, d.bias = 16, 16, 16
+    d.in_C, d.n_taps, d.K, d.G, d.Ht, d.Wt, d.t_cnt = 48, 1, 48, 1, 4, 4, 1
+    assert lib.sst_lt_conv(ctypes.byref(d), None) == -1               # in_C not a multiple of 64
+    d.in_C, d.K = 64, 128
+    assert lib.sst_lt_conv(ctypes.byref(d), None) == -1               # K != n_taps * in_C
+    d.K, d.epi = 64, 7
+    assert lib.sst_lt_conv(ctypes.byref(d), None) == -1               # unknown epilogue
+    d.epi, d.N = 1, 12
+    assert lib.sst_lt_conv(ctypes.byref(d), None) == -1               # FSQ head needs N == 16
+    assert lib.sst_lt_patchify(None, 1, 8, 8, 1, None, None, None) == -1
+    assert lib.sst_lt_patchify(ctypes.c_void_p(16), 1, 8, 8, 4, ctypes.c_void_p(16),
+                               ctypes.c_void_p(16), None) == -1        # s not in {1,2,3}
+    assert lib.sst_lt_dec_in(None, None, 1, 1, 1, None, None) == -1
+    assert lib.sst_lt_attn(ctypes.c_void_p(16), 1, 8, 8, 100, ctypes.c_void_p(16), None) == -1
+    assert lib.sst_upscale_blend9(ctypes.c_void_p(16), 1, 8, 8, 2, 16, 16, ctypes.c_void_p(16), 5,
+                                  ctypes.c_void_p(16), None) == -4   # blend width > 4 with prev
+    assert lib.sst_similarity_gop(None, 1, 4, 12, None, None) == -1
+
+
+def test_sass_has_tcgen05_and_cluster_mma(lib):
+    """The learned-tokenizer kernels issue 5th-gen tensor-core MMAs (UTCHMMA),
+    TMEM loads and 2-SM (CTA-pair) MMAs."""
+    from paper_2602_03529_b200 import _lib
+    cuobjdump = "/usr/local/cuda/bin/cuobjdump"
+    if not Path(cuobjdump).exists():
+        pytest.skip("cuobjdump missing")
+    sass = subprocess.run([cuobjdump, "-sass", str(_lib.LIB_PATH)], capture_output=True,
+                          text=True).stdout
+    assert "UTCHMMA" in sass and "LDTM" in sass and "UTMALDG.5D" in sass
+    assert "UTCHMMA.2CTA" in sass and "UTCBAR.2CTA.MULTICAST" in sass
