@@ -62,6 +62,23 @@ struct ConvArgs {
 
 __device__ __forceinline__ float silu(float x) { return __fdividef(x, 1.0f + __expf(-x)); }
 
+// +bf16 residual for 32 channels at element offset off (STORE epilogues)
+__device__ __forceinline__ void epi_add_residual(float (&v)[32], const ConvArgs& a, size_t off) {
+  if (a.residual == nullptr) return;
+  const uint4* rp = reinterpret_cast<const uint4*>(a.residual + off);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint4 u = __ldg(rp + q);
+    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float2 f = __bfloat1622float2(h2[e]);
+      v[q * 8 + 2 * e] += f.x;
+      v[q * 8 + 2 * e + 1] += f.y;
+    }
+  }
+}
+
 template <int BN, int NST>
 struct TileCfg {
   static constexpr int B_BYTES = BN * 128;
@@ -669,20 +686,38 @@ __device__ __forceinline__ uint64_t halo_desc_pitch(uint32_t saddr, int pitch) {
 // kHalo = true: causal (2,3,3) conv (2 temporal taps x 9 spatial taps per
 // halo); false: 1x1 conv / GEMM (one tap, an 8x16 token box per CTA, temporal
 // offset taps[0][0]).  A unit covers 256 output channels n_blk*256..+255.
-template <bool kHalo>
+// kTma: STORE epilogue through a swizzled smem staging tile + 5-D TMA store
+// (short-K 1x1 GEMMs, whose cost is the output write); otherwise direct
+// 16-byte stores from registers.
+template <bool kTma>
+__host__ __device__ constexpr int pair_bstages() { return kTma ? 4 : c233c::BSTAGES; }
+template <bool kTma>
+__host__ __device__ constexpr int pair_smem() {
+  return c233c::HSLOTS * c233c::HALO_STRIDE + pair_bstages<kTma>() * c233c::B_BYTES +
+         (kTma ? 2 * 2 * 16384 : 0) + 1024 + 512;
+}
+
+__device__ __forceinline__ void named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+template <bool kHalo, bool kTma>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
     k_lt_convpair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                  const ConvArgs a, int n_units, int n_blocks) {
+                  const __grid_constant__ CUtensorMap tmC, const ConvArgs a, int n_units,
+                  int n_blocks) {
   using namespace c233c;
   constexpr int kPitch = kHalo ? PITCH : 8;
   constexpr int kBoxBytes = kHalo ? HALO_BYTES : 8 * 16 * 128;
   constexpr int kSpatial = kHalo ? 9 : 1;
+  constexpr int BSTAGES = pair_bstages<kTma>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sH = smem;
   uint8_t* sB = smem + HSLOTS * HALO_STRIDE;
-  uint64_t* hfull = reinterpret_cast<uint64_t*>(sB + BSTAGES * B_BYTES);
+  uint8_t* sStage = sB + BSTAGES * B_BYTES;            // kTma: [2 halves][2 boxes][128 rows][128 B]
+  uint64_t* hfull = reinterpret_cast<uint64_t*>(sStage + (kTma ? 2 * 2 * 16384 : 0));
   uint64_t* hempty = hfull + HSLOTS;
   uint64_t* bfull = hempty + HSLOTS;
   uint64_t* bempty = bfull + BSTAGES;
@@ -696,6 +731,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
   if (threadIdx.x == 0) {
     tc::prefetch_tmap(&tmA);
     tc::prefetch_tmap(&tmB);
+    if (kTma) tc::prefetch_tmap(&tmC);
     for (int i = 0; i < HSLOTS; ++i) { mbar_init(&hfull[i], 1); mbar_init(&hempty[i], 1); }
     for (int i = 0; i < BSTAGES; ++i) { mbar_init(&bfull[i], 1); mbar_init(&bempty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&afull[i], 1); mbar_init(&aempty[i], 2 * EPI_WARPS); }
@@ -785,6 +821,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
     const int half = e >> 2, q = warp & 3;
     const int m = q * 32 + lane;
     const uint32_t aempty_leader = tc::mapa(smem_u32(&aempty[0]), 0);
+    const bool issuer = kTma && (e & 3) == 0 && lane == 0;     // first warp of each half
     int it = 0;
     for (int u = pair; u < n_units; u += npairs, ++it) {
       int g, t, x0, y0, nb;
@@ -798,6 +835,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
       const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + ab * 256 + half * 128;
       const size_t tok = (((size_t)g * a.out_T + t) * a.Ht + y) * a.Wt + x;
       __nv_bfloat16* outp = a.out + tok * a.N + n0;
+      uint8_t* stage = sStage + half * 2 * 16384;
+      if (kTma) named_bar(1 + half, 128);    // the previous unit's TMA store has read the tile
 #pragma unroll 1
       for (int c = 0; c < 128; c += 32) {
         float v[32];
@@ -811,6 +850,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
         for (int i = 0; i < 32; ++i) {
           v[i] += __ldg(a.bias + n0 + c + i);
           if (a.act) v[i] = silu(v[i]);
+        }
+        if (kTma) {
+          if (valid) epi_add_residual(v, a, tok * a.N + n0 + c);
+          const int box = c >> 6, j0 = (c & 63) >> 3;
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            uint4 uu;
+            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&uu);
+#pragma unroll
+            for (int e2 = 0; e2 < 4; ++e2)
+              h2[e2] = __floats2bfloat162_rn(v[qq * 8 + 2 * e2], v[qq * 8 + 2 * e2 + 1]);
+            const int j = j0 + qq;
+            *reinterpret_cast<uint4*>(stage + box * 16384 + m * 128 + ((j ^ (m & 7)) << 4)) = uu;
+          }
+          continue;
         }
         if (!valid) continue;
         if (a.residual != nullptr) {
@@ -838,7 +892,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
           op[qq] = uu;
         }
       }
+      if (kTma) {
+        fence_proxy_async_smem();
+        named_bar(1 + half, 128);
+        if (issuer) {
+#pragma unroll
+          for (int b = 0; b < 2; ++b)
+            tc::tma_store_5d(&tmC, stage + b * 16384, n0 + b * 64, x0 + 8 * (int)rank, y0, t, g);
+          tma_store_commit();
+          tma_store_wait_read();           // staging reusable once the bulk store read it
+        }
+      }
     }
+    if (issuer) tma_store_wait_all();
   }
   tc::fence_before_sync();
   tc::cluster_sync();
@@ -1343,10 +1409,18 @@ static int launch_convpair(const SstConvDesc* d, cudaStream_t st, bool halo) {
     SST_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
   }
   const int64_t pairs = units < n_sm / 2 ? units : n_sm / 2;
-  auto kern = halo ? k_lt_convpair<true> : k_lt_convpair<false>;
-  SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, c233c::SMEM));
-  kern<<<(unsigned)(2 * pairs), c233c::THREADS, c233c::SMEM, st>>>(tmA, tmB, a, (int)units,
-                                                                   n_blocks);
+  CUtensorMap tmC;
+  memset(&tmC, 0, sizeof(tmC));
+  const bool tma_store = !halo;
+  if (tma_store) {
+    const uint64_t cdims[5] = {(uint64_t)d->N, (uint64_t)d->Wt, (uint64_t)d->Ht,
+                               (uint64_t)d->out_T, (uint64_t)d->G};
+    if (!make_tmap_bf16_5d(&tmC, d->out, cdims, 8, 16)) return SST_ERR_ARG;
+  }
+  auto kern = halo ? k_lt_convpair<true, false> : k_lt_convpair<false, true>;
+  const int smem = halo ? pair_smem<false>() : pair_smem<true>();
+  SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<(unsigned)(2 * pairs), c233c::THREADS, smem, st>>>(tmA, tmB, tmC, a, (int)units, n_blocks);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }
@@ -1421,7 +1495,7 @@ extern "C" int sst_lt_conv(const SstConvDesc* d, void* stream) {
       // K = 256) are store-bound and keep the tile kernel's swizzled TMA-store
       // epilogue (measured: qkv 0.30 ms tile kernel vs 0.46 ms pair kernel).
       if (!generic && d->n_taps == 1 && d->taps[0][1] == 0 && d->taps[0][2] == 0 &&
-          d->N % 256 == 0 && d->in_C >= 1024 && d->in_W == d->Wt && d->in_H == d->Ht) {
+          d->N % 256 == 0 && d->in_W == d->Wt && d->in_H == d->Ht) {
         const char* m1 = getenv("SST_LT_GEMM");
         if (!(m1 && m1[0] == 't')) return lt::launch_convpair(d, st, false);
       }
