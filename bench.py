@@ -597,6 +597,36 @@ def cpu_baseline(a) -> dict:
                       f"wall {walls[0]:.1f} s"}
 
 
+def single_stream_latency(a, device) -> dict:
+    """Real-time view (north_star: >= 30 fps per 1080p stream): ONE stream,
+    one GoP at a time (each GoP blends with the previous one), variable scale
+    3,3,2,2; device time per GoP (encode .. reconstruct, 9 frames) with the
+    GoP resident in HBM, and the frame rate that implies for a single stream."""
+    import torch
+    from paper_2602_03529_b200.pipeline import StreamBank
+    H, W = a.height, a.width
+    bank = StreamBank(1, H, W)
+    fr = make_inputs([0], H, W, device, n_sets=1)[0]
+    out = torch.empty_like(fr)
+    n, warm = 24, 4
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(n)]
+    for k in range(warm + n):
+        s = SCALE_PATTERN[k % len(SCALE_PATTERN)]
+        if k >= warm:
+            ev[k - warm][0].record()
+        bank.step({s: fr}, {s: out}, {s: [0]}, {s: [k]}, drop_rate=a.drop)
+        if k >= warm:
+            ev[k - warm][1].record()
+            torch.cuda.synchronize()          # one GoP in flight: latency, not throughput
+    ms = sorted(b.elapsed_time(e) for b, e in ev)
+    med = ms[len(ms) // 2]
+    return {"stream": f"1 x {H}p, scales {SCALE_PATTERN}, {int(a.drop * 100)}% drop, blend n=2",
+            "gop_ms_median": round(med, 3), "gop_ms_max": round(ms[-1], 3),
+            "frames_per_s_single_stream": round(GOP / med * 1e3, 1),
+            "realtime_30fps_budget_ms_per_gop": round(GOP / 30 * 1e3, 1)}
+
+
 def parity_sample(a, device) -> dict:
     """PSNR delta vs the CPU reference algorithm on one full-size GoP: the same
     synthetic 1080p GoP through the GPU path and through the oracle port."""
@@ -797,6 +827,7 @@ def main():
         if world == 1 and not a.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(a)
             line["parity"] = parity_sample(a, torch.device("cuda", local_rank))
+            line["single_stream"] = single_stream_latency(a, torch.device("cuda", local_rank))
         if world == 1 and not a.no_learned:
             line["learned_tokenizer"] = run_learned(a, torch.device("cuda", local_rank))
         print(json.dumps(line), flush=True)
