@@ -336,6 +336,14 @@ SST_API int sst_lt_patchify(const float* frames, int G, int H, int W, int s, voi
 SST_API int sst_lt_dec_in(const double* tok, const uint8_t* mask, int G, int Ht, int Wt, void* out,
                           void* stream);
 
+/* reassemble x2 fused with the learned decoder's input stage: packets routed
+ * as for sst_unpack_decode (ws = sst_unpack_decode_workspace bytes); writes
+ * the snapped, concealed bf16 [G][2][H'][W'][64] decoder input directly. */
+SST_API int sst_lt_unpack_dec_in(const uint8_t* buf, const int64_t* off, SstPacketInfo* info,
+                                 const int32_t* target, int64_t n, int G, int Ht, int Wt,
+                                 const uint32_t* exp_gop, uint32_t* winner, int32_t* stats,
+                                 void* ws, void* out, void* stream);
+
 /* Causal spatio-temporal window attention core of the learned tokenizer:
  * qkv bf16 [G][2][H'][W'][3D] (Q | K | V, head-major 64-dim heads, from one
  * 1x1 sst_lt_conv), out bf16 [G][2][H'][W'][D].  Each query attends to the

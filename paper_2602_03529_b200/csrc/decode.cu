@@ -9,6 +9,8 @@
 //   -> IDCT along x per pixel row, clip to [0,1]
 //   -> temporal-reference concealment (invalid P block <- I block)
 //   -> float32 working-resolution I and P images, cropped to (h, w).
+#include <cuda_bf16.h>
+
 #include "common.cuh"
 #include "dct8.cuh"
 
@@ -279,6 +281,81 @@ extern "C" int sst_unpack_decode(const uint8_t* buf, const int64_t* off, SstPack
   a.G = G; a.Ht = Ht; a.Wt = Wt; a.h = h; a.w = w; a.out = out;
   dim3 grid(ceil_div(Wt, kDecTok), Ht, G);
   k_decode<true><<<grid, kDecThreads, 0, st>>>(a);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+// ---- learned tokenizer: packets -> decoder input ----------------
+// The mask-aware learned decoder's input stage fused with reassembly: one
+// thread per latent token dequantises its 12 FSQ-code channels straight out of
+// the winning row packet (transport.py:108-112: qmin + raw * (qrange / 255)),
+// conceals a missing P token with the co-located I token, snaps the values
+// back onto the FSQ grid and writes the bf16 [G][2][H'][W'][64] input of the
+// first decoder convolution -- no token matrix is materialised.
+namespace sst {
+__device__ __forceinline__ int lt_levels(int i) { return (i % 6) < 3 ? 8 : 5; }
+
+__global__ void k_lt_unpack_dec_in(const uint8_t* __restrict__ buf, const RowInfo* __restrict__ rows,
+                                   const int32_t* __restrict__ tokoff, int G, int Ht, int Wt,
+                                   __nv_bfloat16* __restrict__ out) {
+  const int64_t n = (int64_t)Ht * Wt;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)G * 2 * n) return;
+  const int64_t pos = idx % n;
+  const int64_t gt = idx / n;
+  const int t = (int)(gt % 2);
+  const int64_t g = gt / 2;
+  const int y = (int)(pos / Wt), x = (int)(pos % Wt);
+  int64_t r = (g * 2 + t) * Ht + y;
+  int slot = tokoff[r * Wt + x];
+  if (t == 1 && slot < 0) {               // conceal with the co-located I token
+    r = (g * 2) * Ht + y;
+    slot = tokoff[r * Wt + x];
+  }
+  uint4 o[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) o[q] = make_uint4(0, 0, 0, 0);
+  if (slot >= 0) {
+    const RowInfo ri = rows[r];
+    const uint8_t* p = buf + ri.payload + (int64_t)slot * kChannels;
+    __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(o);
+#pragma unroll
+    for (int i = 0; i < kChannels; ++i) {
+      const double v = ri.qmin + (double)p[i] * ri.step;
+      const int L = lt_levels(i), hw = L / 2;
+      double q = rint(v * (double)hw);
+      q = fmin(fmax(q, (double)-hw), (double)(L - 1 - hw));
+      ob[i] = __float2bfloat16_rn((float)(q / (double)hw));
+    }
+  }
+  uint4* op = reinterpret_cast<uint4*>(out + idx * 64);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) op[q] = o[q];
+}
+}  // namespace sst
+
+extern "C" int sst_lt_unpack_dec_in(const uint8_t* buf, const int64_t* off, SstPacketInfo* info,
+                                    const int32_t* target, int64_t n, int G, int Ht, int Wt,
+                                    const uint32_t* exp_gop, uint32_t* winner, int32_t* stats,
+                                    void* ws, void* out, void* stream) {
+  if (n < 0 || G < 0 || Ht <= 0 || Wt <= 0) return SST_ERR_ARG;
+  if (G == 0) return SST_OK;
+  if (!exp_gop || !winner || !stats || !out || !ws) return SST_ERR_ARG;
+  if (n > 0 && (!buf || !off || !info || !target)) return SST_ERR_ARG;
+  if (Ht > 65535 || G > 65535) return SST_ERR_ARG;
+  if (reinterpret_cast<uintptr_t>(ws) & 15) return SST_ERR_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = route_packets(info, target, n, 2 * G, Ht, nullptr, exp_gop, winner, stats, st);
+  if (rc != SST_OK) return rc;
+  const int64_t nrows = 2 * (int64_t)G * Ht;
+  RowInfo* rows = static_cast<RowInfo*>(ws);
+  int32_t* tokoff = reinterpret_cast<int32_t*>(rows + nrows);
+  k_rowprep<<<(unsigned)ceil_div64(nrows, 8), 256, 0, st>>>(off, info, buf, winner, nrows, Ht, Wt,
+                                                            rows, tokoff, stats);
+  SST_LAUNCH_CHECK();
+  const int64_t total = nrows * Wt;
+  k_lt_unpack_dec_in<<<(unsigned)ceil_div64(total, 256), 256, 0, st>>>(
+      buf, rows, tokoff, G, Ht, Wt, static_cast<__nv_bfloat16*>(out));
   SST_LAUNCH_CHECK();
   return SST_OK;
 }

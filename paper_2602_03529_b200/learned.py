@@ -267,13 +267,21 @@ class LearnedTokenizer:
         h, w = hw
         if not (0 < h <= Ht * 8 and 0 < w <= Wt * 8):
             raise ValueError(f"frame shape {hw} does not fit a {Ht}x{Wt} token grid")
-        D = self.cfg.dim
         dev = tokens.device
         x = torch.empty((G, 2, Ht, Wt, DEC_IN_CHANNELS), dtype=torch.bfloat16, device=dev)
-        st = _dev.stream()
         _lib.call("sst_lt_dec_in", tokens.data_ptr(), mask.data_ptr(), G, Ht, Wt, x.data_ptr(),
-                  st)
+                  _dev.stream())
         self.launches += 1
+        return self.decode_inputs(x, hw, frames)
+
+    def decode_inputs(self, x: torch.Tensor, hw, frames: torch.Tensor | None = None
+                      ) -> torch.Tensor:
+        """Decoder from its prepared input (bf16 [G][2][H'][W'][64]: snapped,
+        concealed FSQ codes, e.g. sst_lt_unpack_dec_in straight from packets)."""
+        G, _, Ht, Wt, _ = x.shape
+        h, w = hw
+        D = self.cfg.dim
+        dev = x.device
         hbuf = torch.empty((G, 2, Ht, Wt, D), dtype=torch.bfloat16, device=dev)
         ubuf = torch.empty_like(hbuf)
         self._conv("dec_in", x, (G, 2, Ht, Wt, DEC_IN_CHANNELS), (Ht, Wt), TAPS_233, 0, 2,
@@ -347,7 +355,9 @@ class LearnedGopCodec(GopCodec):
       encode      learned encoder + FSQ (tcgen05) -> tokens [G][2][H'][W'][12]
       similarity  sst_similarity on the FSQ codes (selection.py:33-52)
       K2 / K3     intelligent drop + 8-bit packetisation with CRC (unchanged)
-      K4          sst_parse + sst_reassemble (first-wins, zero-fill)
+      K4          sst_parse + sst_lt_unpack_dec_in (first-wins routing; tokens
+                  dequantised from the winning packets, concealed and snapped
+                  straight into the first decoder conv's bf16 input)
       decode      mask-aware learned decoder (tcgen05), 9 distinct frames
       K5          sst_upscale (bilinear x s, crop) + sst_blend (Eq. 2)
     """
@@ -360,6 +370,8 @@ class LearnedGopCodec(GopCodec):
         self.idx = torch.empty((g_max, 2, self.Ht, self.Wt, 2), dtype=torch.int32, device=dev)
         self.rx_tok = torch.empty_like(self.tok)
         self.rx_mask = torch.empty_like(self.mask)
+        self.dec_x = torch.empty((g_max, 2, self.Ht, self.Wt, DEC_IN_CHANNELS),
+                                 dtype=torch.bfloat16, device=dev)
         # double-buffered decoded frames: step k decodes into parity k % 2 while
         # boundary blending reads the previous step's frames from the other
         self.frames9 = [torch.empty((g_max, GOP_SIZE, self.h, self.w, 3), dtype=torch.float32,
@@ -400,15 +412,16 @@ class LearnedGopCodec(GopCodec):
                   self.lengths.data_ptr(), None if present is None else present.data_ptr(), npk,
                   self.info.data_ptr(), st)
         tm.end("K4_parse")
-        tm.begin("K4_reassemble")
-        _lib.call("sst_reassemble", arena.data_ptr(), self.offsets.data_ptr(),
-                  self.info.data_ptr(), self.target.data_ptr(), npk, 2 * g, self.Ht, self.Wt,
-                  CHANNELS, self.kind.data_ptr(), self.gop_id.data_ptr(), self.winner.data_ptr(),
-                  self.rx_tok.data_ptr(), self.rx_mask.data_ptr(), self.stats.data_ptr(), st)
-        tm.end("K4_reassemble")
+        # reassembly fused with the decoder's input stage: tokens go from the
+        # winning packets straight to the bf16 input of the first conv
+        tm.begin("K4_unpack_dec_in")
+        _lib.call("sst_lt_unpack_dec_in", arena.data_ptr(), self.offsets.data_ptr(),
+                  self.info.data_ptr(), self.target.data_ptr(), npk, g, self.Ht, self.Wt,
+                  self.exp_gop.data_ptr(), self.winner.data_ptr(), self.stats.data_ptr(),
+                  self.dec_ws.data_ptr(), self.dec_x.data_ptr(), st)
+        tm.end("K4_unpack_dec_in")
         tm.begin("L_decode")
-        self.model.decode_tokens(self.rx_tok[:g], self.rx_mask[:g], (self.h, self.w),
-                                 frames=self.frames9[parity][:g])
+        self.model.decode_inputs(self.dec_x[:g], (self.h, self.w), frames=self.frames9[parity][:g])
         tm.end("L_decode")
         return self.frames9[parity][:g]
 

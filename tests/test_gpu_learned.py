@@ -355,8 +355,8 @@ def test_learned_gop_codec_stages_bit_exact():
         for kind in (0, 1):
             v, m = O.reassemble([q for q in parsed if q["kind"] == kind], (Ht, Wt, 12))
             rx[j, kind], rxm[j, kind] = v, m
-    assert np.array_equal(codec.rx_tok[:g].cpu().numpy(), rx)
-    assert np.array_equal(codec.rx_mask[:g].cpu().numpy(), rxm)
+    # the fused packets -> decoder-input stage equals reassemble + dec_in
+    assert torch.equal(codec.dec_x[:g].float().cpu(), LO.dec_in(rx, rxm))
     dec = codec.model.decode_tokens(_dev.h2d(rx, np.float64), _dev.h2d(rxm, np.uint8), hw)
     assert torch.equal(dec, codec.frames9[1][:g])
     d9 = dec.cpu().numpy()
@@ -365,3 +365,41 @@ def test_learned_gop_codec_stages_bit_exact():
         prev_up = [O.upscale(prev9[j, t], s, crop=(H, W)) for t in range(9)]
         want = O.blend(prev_up, up, 2)
         assert np.array_equal(out[j].cpu().numpy(), np.stack(want))
+
+
+def test_learned_decoder_input_from_lossy_packets():
+    """Packets -> decoder input with network loss: first-wins routing, lost I
+    rows -> zero codes, lost P rows -> the co-located I codes; equal to the
+    reference's reassemble (oracle) followed by the snap / conceal stage."""
+    from paper_2602_03529_b200.learned import LearnedGopCodec
+
+    H, W, s, g = 64, 96, 2, 2
+    codec = LearnedGopCodec(g, H, W, s, cfg=LearnedConfig(dim=128, blocks=1, seed=6))
+    clip = make_clip("noisy-motion", W, H, 9, seed=4)
+    frames = torch.from_numpy(np.stack([clip.gop(0)] * g)).cuda()
+    codec.set_gop_ids([3, 4])
+    codec.tokenize(frames, g)
+    codec.select_and_pack(g, codec.drop_k(0.1))
+    torch.cuda.synchronize()
+    npk = codec.n_pkt_per_gop
+    rng = np.random.default_rng(9)
+    lost = [set(int(j) for j in np.flatnonzero(rng.random(npk) < 0.3)) for _ in range(g)]
+    present = torch.tensor([0 if j in lost[i] else 1 for i in range(g) for j in range(npk)],
+                           dtype=torch.uint8, device="cuda")
+    codec.decode(g, 0, present=present)
+    torch.cuda.synchronize()
+    arena, lengths = codec.arena.cpu().numpy(), codec.lengths.cpu().numpy()
+    rx = np.zeros((g, 2, codec.Ht, codec.Wt, 12))
+    rxm = np.zeros((g, 2, codec.Ht, codec.Wt), np.uint8)
+    for i in range(g):
+        wire = [arena[i * npk + j, :lengths[i * npk + j]].tobytes() for j in range(npk)
+                if j not in lost[i]]
+        parsed = [O.parse(d) for d in wire]
+        for kind in (0, 1):
+            v, m = O.reassemble([q for q in parsed if q["kind"] == kind], (codec.Ht, codec.Wt, 12))
+            rx[i, kind], rxm[i, kind] = v, m
+    assert torch.equal(codec.dec_x[:g].float().cpu(), LO.dec_in(rx, rxm))
+    st = codec.stats[:4 * g].cpu().numpy().reshape(g, 2, 2)
+    for i in range(g):
+        lost_i = sum(1 for j in lost[i] if j < codec.Ht)
+        assert st[i, 0, 1] == codec.Ht - lost_i                      # I rows received
