@@ -8,7 +8,7 @@ for k in k_lt_convpair k_lt_attn_tc; do
       -o gpurun_out/${TAG}_$k python scripts/learned_step.py 32 2 > gpurun_out/${TAG}_ncu_$k.log 2>&1
   echo "$k rc=$?"
 done
-for k in k_lt_patchify k_upscale9_tma; do
+for k in k_lt_patchify k_upscale9f; do
   timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:$k -s 1 -c 1 \
       -o gpurun_out/${TAG}_$k python scripts/learned_step.py 32 2 > gpurun_out/${TAG}_ncu_$k.log 2>&1
   echo "$k rc=$?"
