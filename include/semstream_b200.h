@@ -351,6 +351,13 @@ SST_API int sst_lt_unpack_dec_in(const uint8_t* buf, const int64_t* off, SstPack
  * fp32, scale 1/8). */
 SST_API int sst_lt_attn(const void* qkv, int G, int Ht, int Wt, int D, void* out, void* stream);
 
+/* qkv projection fused with the attention core: h bf16 [G][2][H'][W'][D]
+ * (the block input), w_qkv bf16 [3D][D], b_qkv fp32 [3D] -> out bf16
+ * [G][2][H'][W'][D]; same result definition as a 1x1 sst_lt_conv (bf16 qkv)
+ * followed by sst_lt_attn. */
+SST_API int sst_lt_attn_fused(const void* h, const void* w_qkv, const float* b_qkv, int G, int Ht,
+                              int Wt, int D, void* out, void* stream);
+
 /* ---- metrics ------------------------------------------------------------ */
 
 /* mse (video.py:265-270) per frame pair: out[i] = mean((a-b)^2) in float64. */

@@ -89,6 +89,7 @@ SIGNATURES = {
     "sst_lt_patchify": (_I, [_P, _I, _I, _I, _I, _P, _P, _P]),
     "sst_lt_dec_in": (_I, [_P, _P, _I, _I, _I, _P, _P]),
     "sst_lt_attn": (_I, [_P, _I, _I, _I, _I, _P, _P]),
+    "sst_lt_attn_fused": (_I, [_P, _P, _P, _I, _I, _I, _I, _P, _P]),
     "sst_lt_unpack_dec_in": (_I, [_P, _P, _P, _P, _L, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     "sst_residual": (_I, [_P, _P, _I, _I, _I, C.c_double, C.c_double, _P, _P, _P, _P, _P]),
     "sst_mean_axis0": (_I, [_P, _I, _L, _P, _P]),

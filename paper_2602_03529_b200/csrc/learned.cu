@@ -1195,6 +1195,214 @@ __global__ void __launch_bounds__(128)
   if (warp == 0) tc::tmem_dealloc(tmem, 128);
 }
 
+// ---- fused qkv projection + causal window attention (tcgen05) -------------
+// One CTA = (GoP, 8x8 window, 64-dim head).  The qkv projection of the
+// window's 128 tokens for this head is a third tcgen05 GEMM inside the CTA:
+//   QKV = H W_h^T   M=128 (2 frames x 64 tokens), N=192 (q|k|v), K=D,
+// A = the window's tokens of the residual stream (two 5-D TMA boxes per
+// 64-channel block, zero-filled outside the frame), B = the head's 192 rows of
+// W_qkv, through a 2-stage TMA ring; the epilogue (+bias, bf16) writes Q, K
+// and V^T straight into the swizzled operand tiles of S = QK^T, then the
+// softmax / P V steps of k_lt_attn_tc follow.  The qkv tensor never exists.
+constexpr int AF_STAGE = 16384 + 24576;                 // A (128 x 64) + B (192 x 64) bf16
+constexpr int AF_SMEM = 2 * AF_STAGE + 1024 + 128 + 128 * 4;
+
+__global__ void __launch_bounds__(128)
+    k_lt_attn_fused(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW,
+                    const float* __restrict__ bqkv, int G, int Ht, int Wt, int D,
+                    __nv_bfloat16* __restrict__ out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;                 // after the projection: [128 q][64 d]
+  uint8_t* sK = smem + 16384;         // [128 k][64 d]
+  uint8_t* sP = smem;                 // [2 kb][128 q][64 k]
+  uint8_t* sV = smem + 32768;         // [2 kb][64 d][64 k]  (V^T)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * AF_STAGE);
+  uint64_t* empty = full + 2;
+  uint64_t* bar = empty + 2;          // [0] qkv, [1] S, [2] O
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 3);
+  int* kval = reinterpret_cast<int*>(smem + 2 * AF_STAGE + 128);
+
+  const int wins_x = ceil_div(Wt, ATT_WIN);
+  const int wy = blockIdx.x / wins_x, wx = blockIdx.x - wy * wins_x;
+  const int head = blockIdx.y, g = blockIdx.z;
+  const int t = threadIdx.x, warp = t >> 5;
+  const int ft = t >> 6, lt = t & 63;
+  const int y = wy * ATT_WIN + (lt >> 3), x = wx * ATT_WIN + (lt & 7);
+  const bool valid = y < Ht && x < Wt;
+  const size_t tok = (((size_t)g * 2 + ft) * Ht + y) * Wt + x;
+  const int ncb = D / BK;
+
+  if (t == 0) {
+    tc::prefetch_tmap(&tmH);
+    tc::prefetch_tmap(&tmW);
+    for (int i = 0; i < 2; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < 3; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tmem_slot, 256);
+  kval[t] = valid;
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  // ---- QKV projection (thread 0 streams the operands and issues the MMAs) ----
+  if (t == 0) {
+    auto load = [&](int cb, int s) {
+      uint8_t* st = smem + s * AF_STAGE;
+      mbar_expect_tx(&full[s], AF_STAGE);
+      tc::tma_load_5d(st, &tmH, cb * BK, wx * ATT_WIN, wy * ATT_WIN, 0, g, &full[s]);
+      tc::tma_load_5d(st + 8192, &tmH, cb * BK, wx * ATT_WIN, wy * ATT_WIN, 1, g, &full[s]);
+      for (int part = 0; part < 3; ++part)
+        tc::tma_load_2d(st + 16384 + part * 8192, &tmW, cb * BK, part * D + head * ATT_HD, &full[s]);
+    };
+    for (int cb = 0; cb < ncb && cb < 2; ++cb) load(cb, cb);
+    constexpr uint32_t id0 = tc::idesc_bf16_f32(128, 192);
+    for (int cb = 0; cb < ncb; ++cb) {
+      const int s = cb & 1;
+      mbar_wait(&full[s], (cb >> 1) & 1);
+      tc::fence_after_sync();
+      const uint64_t ad = tc::smem_desc_sw128(smem_u32(smem + s * AF_STAGE));
+      const uint64_t bd = tc::smem_desc_sw128(smem_u32(smem + s * AF_STAGE + 16384));
+#pragma unroll
+      for (int k = 0; k < BK / 16; ++k) tc::mma_bf16(tmem, ad + 2 * k, bd + 2 * k, id0, cb | k);
+      tc::mma_commit(&empty[s]);
+      if (cb + 2 < ncb) {
+        mbar_wait(&empty[s], (cb >> 1) & 1);
+        load(cb + 2, s);
+      }
+    }
+    tc::mma_commit(&bar[0]);
+  }
+  mbar_wait(&bar[0], 0);
+  tc::fence_after_sync();
+
+  // ---- +bias, bf16: Q and K rows into their tiles, V transposed ----
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+#pragma unroll 1
+  for (int c = 0; c < 6; ++c) {
+    float v[32];
+    tc::tmem_ld32(trow + c * 32, v);
+    const int part = c >> 1;                       // 0 q, 1 k, 2 v
+    const int d0 = (c & 1) * 32;
+    const float* bp = bqkv + part * D + head * ATT_HD + d0;
+#pragma unroll
+    for (int i = 0; i < 32; ++i) v[i] = valid ? v[i] + __ldg(bp + i) : 0.0f;
+    if (part < 2) {
+      uint8_t* base = part == 0 ? sQ : sK;
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) {
+        uint4 u;
+        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[qq * 8 + 2 * e], v[qq * 8 + 2 * e + 1]);
+        const int j = (d0 >> 3) + qq;
+        *reinterpret_cast<uint4*>(base + t * 128 + ((j ^ (t & 7)) << 4)) = u;
+      }
+    } else {
+      const int kb = t >> 6, kk = t & 63;
+      uint8_t* vb = sV + kb * 8192 + (kk & 7) * 2;
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int d = d0 + i;
+        *reinterpret_cast<__nv_bfloat16*>(vb + d * 128 + (((kk >> 3) ^ (d & 7)) << 4)) =
+            __float2bfloat16_rn(v[i]);
+      }
+    }
+  }
+  fence_proxy_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+
+  if (t == 0) {
+    constexpr uint32_t id1 = tc::idesc_bf16_f32(128, 128);
+    const uint64_t ad = tc::smem_desc_sw128(smem_u32(sQ));
+    const uint64_t bd = tc::smem_desc_sw128(smem_u32(sK));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) tc::mma_bf16(tmem, ad + 2 * k, bd + 2 * k, id1, k);
+    tc::mma_commit(&bar[1]);
+  }
+  mbar_wait(&bar[1], 0);
+  tc::fence_after_sync();
+  float sc[128];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    float v[32];
+    tc::tmem_ld32(trow + c * 32, v);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) sc[c * 32 + i] = v[i];
+  }
+  const int nk = (ft + 1) * 64;
+  float m = -INFINITY;
+#pragma unroll
+  for (int k = 0; k < 128; ++k)
+    if (k < nk && kval[k]) m = fmaxf(m, sc[k]);
+  float l = 0.0f;
+#pragma unroll
+  for (int k = 0; k < 128; ++k) {
+    const float p = (k < nk && kval[k]) ? __expf((sc[k] - m) * 0.125f) : 0.0f;
+    sc[k] = p;
+    l += p;
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+#pragma unroll
+  for (int kb = 0; kb < 2; ++kb) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      uint4 u;
+      __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        h2[e] = __floats2bfloat162_rn(sc[kb * 64 + 8 * j + 2 * e], sc[kb * 64 + 8 * j + 2 * e + 1]);
+      *reinterpret_cast<uint4*>(sP + kb * 16384 + t * 128 + ((j ^ (t & 7)) << 4)) = u;
+    }
+  }
+  fence_proxy_async_smem();
+  __syncthreads();
+  tc::fence_after_sync();
+  if (t == 0) {
+    constexpr uint32_t id2 = tc::idesc_bf16_f32(128, 64);
+#pragma unroll
+    for (int kb = 0; kb < 2; ++kb) {
+      const uint64_t ad = tc::smem_desc_sw128(smem_u32(sP + kb * 16384));
+      const uint64_t bd = tc::smem_desc_sw128(smem_u32(sV + kb * 8192));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) tc::mma_bf16(tmem, ad + 2 * k, bd + 2 * k, id2, kb | k);
+    }
+    tc::mma_commit(&bar[2]);
+  }
+  mbar_wait(&bar[2], 0);
+  tc::fence_after_sync();
+  float o[64];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    float v[32];
+    tc::tmem_ld32(trow + c * 32, v);
+#pragma unroll
+    for (int i = 0; i < 32; ++i) o[c * 32 + i] = v[i];
+  }
+  if (valid) {
+    const float inv = 1.0f / l;
+    uint4* op = reinterpret_cast<uint4*>(out + tok * D + head * ATT_HD);
+#pragma unroll
+    for (int i = 0; i < ATT_HD / 8; ++i) {
+      uint4 u;
+      __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        h2[e] = __floats2bfloat162_rn(o[8 * i + 2 * e] * inv, o[8 * i + 2 * e + 1] * inv);
+      op[i] = u;
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 256);
+}
+
 // ---- downscale + pad + patchify --------------------------------------------
 template <int S>
 __global__ void k_lt_patchify(const float* __restrict__ src, int G, int H, int W, int h, int w,
@@ -1567,6 +1775,28 @@ extern "C" int sst_lt_attn(const void* qkv, int G, int Ht, int Wt, int D, void* 
     lt::k_lt_attn_tc<<<grid, 128, lt::ATT_SMEM, st>>>(static_cast<const __nv_bfloat16*>(qkv), G, Ht,
                                                        Wt, D, static_cast<__nv_bfloat16*>(out));
   }
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+extern "C" int sst_lt_attn_fused(const void* h, const void* w_qkv, const float* b_qkv, int G, int Ht,
+                                 int Wt, int D, void* out, void* stream) {
+  if (!h || !w_qkv || !b_qkv || !out || G <= 0 || Ht <= 0 || Wt <= 0 || D <= 0) return SST_ERR_ARG;
+  if (D % lt::ATT_HD || G > 65535 || D / lt::ATT_HD > 65535) return SST_ERR_ARG;
+  const int64_t wins = (int64_t)ceil_div(Ht, lt::ATT_WIN) * ceil_div(Wt, lt::ATT_WIN);
+  if (wins > 0x7fffffff) return SST_ERR_ARG;
+  CUtensorMap tmH, tmW;
+  memset(&tmH, 0, sizeof(tmH));
+  memset(&tmW, 0, sizeof(tmW));
+  const uint64_t hdims[5] = {(uint64_t)D, (uint64_t)Wt, (uint64_t)Ht, 2, (uint64_t)G};
+  if (!make_tmap_bf16_5d(&tmH, h, hdims, lt::ATT_WIN, lt::ATT_WIN)) return SST_ERR_ARG;
+  if (!make_tmap_bf16_2d(&tmW, w_qkv, (uint64_t)D, (uint64_t)(3 * D), lt::ATT_HD)) return SST_ERR_ARG;
+  dim3 grid((unsigned)wins, D / lt::ATT_HD, G);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SST_CUDA_TRY(cudaFuncSetAttribute(lt::k_lt_attn_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    lt::AF_SMEM));
+  lt::k_lt_attn_fused<<<grid, 128, lt::AF_SMEM, st>>>(tmH, tmW, b_qkv, G, Ht, Wt, D,
+                                                      static_cast<__nv_bfloat16*>(out));
   SST_LAUNCH_CHECK();
   return SST_OK;
 }

@@ -45,6 +45,7 @@ restatement in oracle/learned_oracle.py (unpinned: no reference model).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -192,18 +193,26 @@ class LearnedTokenizer:
                        residual=h, out=h)
 
     def _attention(self, part, h, G, Ht, Wt):
-        """h += proj(WindowAttention(qkv(h))): the projections are tcgen05
-        1x1 GEMMs, the 8x8-window causal attention core is sst_lt_attn."""
+        """h += proj(WindowAttention(qkv(h))): the qkv projection and the
+        8x8-window causal attention run in one tcgen05 kernel per (window,
+        head) (sst_lt_attn_fused; SST_LT_ATTN=unfused: a 1x1 GEMM writing qkv,
+        then sst_lt_attn), proj is a tcgen05 1x1 GEMM with the residual add."""
         if not self.cfg.attn:
             return
         D = self.cfg.dim
         shape = (G, 2, Ht, Wt, D)
-        qkv = torch.empty((G, 2, Ht, Wt, 3 * D), dtype=torch.bfloat16, device=h.device)
         o = torch.empty_like(h)
-        self._conv(f"{part}_qkv", h, shape, (Ht, Wt), [(0, 0, 0)], 0, 2, _lib.LT_EPI_STORE,
-                   out=qkv)
-        _lib.call("sst_lt_attn", qkv.data_ptr(), G, Ht, Wt, D, o.data_ptr(), _dev.stream())
-        self.launches += 1
+        if os.environ.get("SST_LT_ATTN", "fused") == "fused":
+            # qkv projection inside the attention kernel (no qkv tensor)
+            _lib.call("sst_lt_attn_fused", h.data_ptr(), self.W[f"{part}_qkv"].data_ptr(),
+                      self.b[f"{part}_qkv"].data_ptr(), G, Ht, Wt, D, o.data_ptr(), _dev.stream())
+            self.launches += 1
+        else:
+            qkv = torch.empty((G, 2, Ht, Wt, 3 * D), dtype=torch.bfloat16, device=h.device)
+            self._conv(f"{part}_qkv", h, shape, (Ht, Wt), [(0, 0, 0)], 0, 2, _lib.LT_EPI_STORE,
+                       out=qkv)
+            _lib.call("sst_lt_attn", qkv.data_ptr(), G, Ht, Wt, D, o.data_ptr(), _dev.stream())
+            self.launches += 1
         self._conv(f"{part}_proj", o, shape, (Ht, Wt), [(0, 0, 0)], 0, 2, _lib.LT_EPI_STORE,
                    residual=h, out=h)
 

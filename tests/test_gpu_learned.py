@@ -145,6 +145,26 @@ def test_window_attention_core(H, W, D):
     _assert_bf16_close(out.float().cpu(), LO.window_attention(qkv), min_exact=0.95, atol=2e-3)
 
 
+@pytest.mark.parametrize("H,W,D", [(8, 8, 128), (13, 21, 256), (45, 80, 256)])
+def test_fused_qkv_attention(H, W, D):
+    """qkv projection inside the attention kernel == 1x1 GEMM + attention core."""
+    rng = np.random.default_rng(13)
+    G = 2
+    h = _bf(rng.standard_normal((G, 2, H, W, D)) * 0.5)
+    Wq = _bf(rng.standard_normal((3 * D, D)) / np.sqrt(D)).numpy()
+    bq = _bf(rng.standard_normal(3 * D) * 0.1).numpy()
+    dev = _dev.device()
+    hd = h.to(dev, torch.bfloat16).contiguous()
+    wd = torch.from_numpy(Wq).to(dev, torch.bfloat16).contiguous()
+    bd = torch.from_numpy(bq).to(dev)
+    out = torch.full((G, 2, H, W, D), 7.0, dtype=torch.bfloat16, device=dev)
+    _lib.call("sst_lt_attn_fused", hd.data_ptr(), wd.data_ptr(), bd.data_ptr(), G, H, W, D,
+              out.data_ptr(), _dev.stream())
+    torch.cuda.synchronize()
+    want = LO.window_attention(LO.bf(LO.linear(h, Wq, bq)))
+    _assert_bf16_close(out.float().cpu(), want, min_exact=0.9, atol=4e-3)
+
+
 def test_conv_causal_first_frame_sees_no_past():
     # t=0 output must not depend on t=1 input (causal temporal kernel)
     rng = np.random.default_rng(2)
