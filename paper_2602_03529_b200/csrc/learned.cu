@@ -1564,12 +1564,9 @@ static int launch_conv233p(const SstConvDesc* d, cudaStream_t st) {
   const int n_halves = d->N / c233p::BN;
   const int64_t units = (int64_t)d->G * d->t_cnt * a.tiles_y * a.tiles_x * n_halves;
   if (units <= 0 || units > 0x7fffffff) return SST_ERR_ARG;
-  static int n_sm = 0;
-  if (n_sm == 0) {
-    int dev = 0;
-    SST_CUDA_TRY(cudaGetDevice(&dev));
-    SST_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-  }
+  int n_sm = 0, dev = 0;                     // the current device's SM count (per call:
+  SST_CUDA_TRY(cudaGetDevice(&dev));         // a process may drive several devices)
+  SST_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
   const int grid = (int)(units < n_sm ? units : n_sm);
   SST_CUDA_TRY(cudaFuncSetAttribute(k_lt_conv233p, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     c233p::SMEM));
@@ -1610,12 +1607,9 @@ static int launch_convpair(const SstConvDesc* d, cudaStream_t st, bool halo) {
   const int n_blocks = d->N / 256;
   const int64_t units = (int64_t)d->G * d->t_cnt * a.tiles_y * a.tiles_x * n_blocks;
   if (units <= 0 || units > 0x7fffffff) return SST_ERR_ARG;
-  static int n_sm = 0;
-  if (n_sm == 0) {
-    int dev = 0;
-    SST_CUDA_TRY(cudaGetDevice(&dev));
-    SST_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
-  }
+  int n_sm = 0, dev = 0;                     // the current device's SM count (per call:
+  SST_CUDA_TRY(cudaGetDevice(&dev));         // a process may drive several devices)
+  SST_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
   const int64_t pairs = units < n_sm / 2 ? units : n_sm / 2;
   CUtensorMap tmC;
   memset(&tmC, 0, sizeof(tmC));
