@@ -627,6 +627,65 @@ def single_stream_latency(a, device) -> dict:
             "realtime_30fps_budget_ms_per_gop": round(GOP / 30 * 1e3, 1)}
 
 
+def loss_legs(a, device) -> dict:
+    """BASELINE.json configs[3]: 1080p, s=3, 32 GoPs per
+    launch with (a) intelligent P-token dropping at 10 % / 30 % and (b) seeded
+    Bernoulli packet loss at 10 % / 30 % on the I+P packet list, decoder
+    zero-fill + I-block concealment.  Device-resident frames/s, and for GoP 0
+    the PSNR of the GPU reconstruction vs the CPU reference algorithm on the
+    same lost-packet set (bit-exact expected)."""
+    import numpy as np
+    import torch
+
+    from oracle import semstream_oracle as O
+    from paper_2602_03529_b200.pipeline import GopCodec
+    H, W, s, G = a.height, a.width, 3, 32
+    frames = make_inputs(list(range(G)), H, W, device, n_sets=1)[0]
+    out = torch.empty_like(frames)
+    codec = GopCodec(G, H, W, s)
+    codec.set_gop_ids([0] * G)
+    npk = codec.n_pkt_per_gop
+    res = {}
+    for kind, rate in (("drop", 0.10), ("drop", 0.30), ("loss", 0.10), ("loss", 0.30)):
+        drop_k = codec.drop_k(rate) if kind == "drop" else 0
+        present, lost0 = None, None
+        if kind == "loss":
+            rng = np.random.default_rng(int(rate * 100))
+            keep = (rng.random(G * npk) >= rate).astype(np.uint8)
+            present = torch.from_numpy(keep).to(device)
+            lost0 = set(int(j) for j in np.flatnonzero(keep[:npk] == 0))
+
+        def step():
+            codec.encode(frames, G, drop_k)
+            codec.decode(G, 0, present=present)
+            codec.reconstruct(G, 0, out)
+
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n = 5
+        e0.record()
+        for _ in range(n):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / n
+        src = frames[0].cpu().numpy()
+        ref = O.pipeline_gop(src, s, gop_id=0, drop_rate=rate if kind == "drop" else 0.0,
+                             lost=lost0)
+        gpu = out[0].cpu().numpy()
+        p_gpu, _ = O.gop_psnr(list(src), list(gpu))
+        p_ref, _ = O.gop_psnr(list(src), list(ref["frames"]))
+        res[f"{kind}_{int(rate * 100)}pct"] = {
+            "frames_per_s": round(G * GOP / ms * 1e3, 1),
+            "psnr_gpu_db": round(p_gpu, 4), "psnr_cpu_ref_db": round(p_ref, 4),
+            "bit_exact": bool(np.array_equal(gpu, np.stack(ref["frames"])))}
+    return {"workload": f"{G} x {H}p GoPs per launch, s=3, no blending (first GoP of each "
+                        "stream); drop = intelligent P-token dropping, loss = Bernoulli packet "
+                        "loss with zero-fill + I concealment", **res}
+
+
 def parity_sample(a, device) -> dict:
     """PSNR delta vs the CPU reference algorithm on one full-size GoP: the same
     synthetic 1080p GoP through the GPU path and through the oracle port."""
@@ -828,6 +887,7 @@ def main():
             line["cpu_baseline"] = cpu_baseline(a)
             line["parity"] = parity_sample(a, torch.device("cuda", local_rank))
             line["single_stream"] = single_stream_latency(a, torch.device("cuda", local_rank))
+            line["loss_recovery"] = loss_legs(a, torch.device("cuda", local_rank))
         if world == 1 and not a.no_learned:
             line["learned_tokenizer"] = run_learned(a, torch.device("cuda", local_rank))
         print(json.dumps(line), flush=True)
