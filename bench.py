@@ -686,6 +686,91 @@ def loss_legs(a, device) -> dict:
                         "loss with zero-fill + I concealment", **res}
 
 
+def small_configs(a, device) -> dict:
+    """BASELINE.json configs[0] and configs[1] on the GPU:
+    [0] the 17-frame 256x256 clip (2 GoPs, the last one tail-padded) through
+        the learned tokenizer (random-init weights, encode -> FSQ -> packetise
+        -> decode -> upscale, tcgen05) at s=2, and through the reference proxy
+        path at s=2 (bit-exact vs the CPU reference);
+    [1] a 720p 33-frame clip (4 GoPs) through the proxy path, no loss:
+        frames/s for 64 such streams per launch (device-resident) and GoP-0
+        parity."""
+    import numpy as np
+    import torch
+
+    from oracle import learned_oracle as LO
+    from oracle import semstream_oracle as O
+    from oracle.synth import make_clip
+    from paper_2602_03529_b200.learned import LearnedConfig, LearnedGopCodec
+    from paper_2602_03529_b200.pipeline import GopCodec, StreamBank
+
+    out = {}
+    # ---- configs[0]
+    clip = make_clip("moving-square", 256, 256, 17, seed=0)
+    gops = np.stack([clip.gop(0), clip.gop(1)])
+    fr = torch.from_numpy(gops).to(device)
+    cfg = LearnedConfig()
+    lc = LearnedGopCodec(2, 256, 256, 2, cfg=cfg)
+    o = torch.empty_like(fr)
+    lc.set_gop_ids([0, 1])
+    for _ in range(3):
+        lc.step(fr, o, 2)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        lc.step(fr, o, 2)
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 10
+    codes, idx, _, hw = lc.model.encode_frames(fr, 2)
+    oc, oi, _, _ = LO.encode(gops, 2, lc.model.host_weights, cfg.blocks)
+    agree = float((idx.cpu().numpy() == oi).mean())
+    bank = StreamBank(1, 256, 256)
+    po = torch.empty_like(fr[:1])
+    prev, exact = None, True
+    for k in range(2):
+        bank.step({2: fr[k:k + 1].contiguous()}, {2: po}, {2: [0]}, {2: [k]})
+        ref = O.pipeline_gop(gops[k], 2, gop_id=k, prev_out=prev)
+        prev = ref["frames"]
+        exact &= bool(np.array_equal(po[0].cpu().numpy(), np.stack(ref["frames"])))
+    out["c0_tiny_256x256x17"] = {
+        "learned_gop_ms": round(ms, 3),
+        "learned_frames_per_s": round(17 / (ms / 1e3), 1),
+        "learned_fsq_index_agreement_vs_oracle": round(agree, 5),
+        "proxy_s2_bit_exact_vs_cpu_reference": exact,
+        "note": "one clip (2 GoPs per launch): launch-latency bound, not a throughput config"}
+    # ---- configs[1]
+    H, W, S = 720, 1280, 64
+    frames = make_inputs(list(range(S)), H, W, device, n_sets=1)[0]
+    res = {}
+    for s in (2, 3):
+        c = GopCodec(S, H, W, s)
+        c.set_gop_ids([0] * S)
+        o2 = torch.empty_like(frames)
+
+        def step():
+            c.encode(frames, S, 0)
+            c.decode(S, 0)
+            c.reconstruct(S, 0, o2)
+
+        for _ in range(2):
+            step()
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(5):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 5
+        ref = O.pipeline_gop(frames[0].cpu().numpy(), s, gop_id=0)
+        res[f"s{s}"] = {"frames_per_s": round(S * GOP / ms * 1e3, 1),
+                        "bit_exact_gop0": bool(np.array_equal(o2[0].cpu().numpy(),
+                                                              np.stack(ref["frames"])))}
+    out["c1_720p_x64_streams"] = res
+    return out
+
+
 def parity_sample(a, device) -> dict:
     """PSNR delta vs the CPU reference algorithm on one full-size GoP: the same
     synthetic 1080p GoP through the GPU path and through the oracle port."""
@@ -888,6 +973,8 @@ def main():
             line["parity"] = parity_sample(a, torch.device("cuda", local_rank))
             line["single_stream"] = single_stream_latency(a, torch.device("cuda", local_rank))
             line["loss_recovery"] = loss_legs(a, torch.device("cuda", local_rank))
+            if a.height == 1080 and a.width == 1920:
+                line["small_configs"] = small_configs(a, torch.device("cuda", local_rank))
         if world == 1 and not a.no_learned:
             line["learned_tokenizer"] = run_learned(a, torch.device("cuda", local_rank))
         print(json.dumps(line), flush=True)
