@@ -691,9 +691,13 @@ __device__ __forceinline__ uint64_t halo_desc_pitch(uint32_t saddr, int pitch) {
 // 16-byte stores from registers.
 template <bool kTma>
 __host__ __device__ constexpr int pair_bstages() { return kTma ? 4 : c233c::BSTAGES; }
-template <bool kTma>
+// kPix: PIXELS epilogue (unpatchify), units of 192 output channels (one frame's
+// 8x8x3 patch), 96 weight rows per CTA
+template <bool kPix>
+__host__ __device__ constexpr int pair_bbytes() { return (kPix ? 96 : c233c::BNH) * 128; }
+template <bool kTma, bool kPix = false>
 __host__ __device__ constexpr int pair_smem() {
-  return c233c::HSLOTS * c233c::HALO_STRIDE + pair_bstages<kTma>() * c233c::B_BYTES +
+  return c233c::HSLOTS * c233c::HALO_STRIDE + pair_bstages<kTma>() * pair_bbytes<kPix>() +
          (kTma ? 2 * 2 * 16384 : 0) + 1024 + 512;
 }
 
@@ -701,7 +705,7 @@ __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <bool kHalo, bool kTma>
+template <bool kHalo, bool kTma, bool kPix = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
     k_lt_convpair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                   const __grid_constant__ CUtensorMap tmC, const ConvArgs a, int n_units,
@@ -711,6 +715,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
   constexpr int kBoxBytes = kHalo ? HALO_BYTES : 8 * 16 * 128;
   constexpr int kSpatial = kHalo ? 9 : 1;
   constexpr int BSTAGES = pair_bstages<kTma>();
+  constexpr int kNU = kPix ? 192 : 256;          // output channels per unit
+  constexpr int kBNH = kNU / 2;                  // weight rows per CTA
+  constexpr int B_BYTES = pair_bbytes<kPix>();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
@@ -779,7 +786,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
             if (bc >= BSTAGES) mbar_wait(&bempty[bs], ((bc / BSTAGES) - 1) & 1);
             if (leader) mbar_expect_tx(&bfull[bs], 2 * B_BYTES);
             tc::tma_load_2d_pair(sB + bs * B_BYTES, &tmB, (kt * kSpatial + sp) * C + cb * BK,
-                                 nb * 256 + (int)rank * BNH, &bfull[bs]);
+                                 nb * kNU + (int)rank * kBNH, &bfull[bs]);
           }
         }
       }
@@ -787,7 +794,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0 && leader) {
       // ---- MMA issuer (leader only): M=256 across the pair, N=256 ----
-      constexpr uint32_t idesc = tc::idesc_bf16_f32(256, 256);
+      constexpr uint32_t idesc = tc::idesc_bf16_f32(256, kNU);
       int hc = 0, bc = 0, it = 0;
       for (int u = pair; u < n_units; u += npairs, ++it) {
         const int ab = it & 1;
@@ -831,6 +838,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
       tc::fence_after_sync();
       const int y = y0 + (m >> 3), x = x0 + 8 * (int)rank + (m & 7);
       const bool valid = y < a.Ht && x < a.Wt;
+      if (kPix) {
+        // ---- unpatchify: columns half*96 .. +95 = pixel rows py = 4*half .. +3 of frame f ----
+        const uint32_t trp = tmem + ((uint32_t)(q * 32) << 16) + ab * 256 + half * 96;
+        float v[96];
+#pragma unroll
+        for (int cc = 0; cc < 3; ++cc) {
+          float u32[32];
+          tc::tmem_ld32(trp + cc * 32, u32);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[cc * 32 + i] = u32[i];
+        }
+        tc::fence_before_sync();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive_cluster(aempty_leader + ab * 8);
+        if (!valid) continue;
+        const int f = a.frame_base + nb;
+        const int nb0 = nb * kNU + half * 96;
+#pragma unroll
+        for (int i = 0; i < 96; ++i) v[i] = fminf(fmaxf(v[i] + __ldg(a.bias + nb0 + i), 0.0f), 1.0f);
+        const bool vec = (a.w & 3) == 0;
+#pragma unroll
+        for (int pr = 0; pr < 4; ++pr) {
+          const int Y = y * 8 + half * 4 + pr;
+          if (Y >= a.h) continue;
+          const int X0 = x * 8;
+          float* dst = a.frames + ((((size_t)g * 9 + f) * a.h + Y) * a.w + X0) * 3;
+          if (vec && X0 + 8 <= a.w) {
+            float4* d4 = reinterpret_cast<float4*>(dst);
+#pragma unroll
+            for (int e4 = 0; e4 < 6; ++e4)
+              d4[e4] = make_float4(v[pr * 24 + 4 * e4], v[pr * 24 + 4 * e4 + 1],
+                                   v[pr * 24 + 4 * e4 + 2], v[pr * 24 + 4 * e4 + 3]);
+          } else {
+            const int npx = min(8, a.w - X0);
+#pragma unroll
+            for (int e4 = 0; e4 < 24; ++e4)
+              if (e4 / 3 < npx) dst[e4] = v[pr * 24 + e4];
+          }
+        }
+        continue;
+      }
       const int n0 = nb * 256 + half * 128;
       const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + ab * 256 + half * 128;
       const size_t tok = (((size_t)g * a.out_T + t) * a.Ht + y) * a.Wt + x;
@@ -1575,6 +1623,46 @@ static int launch_conv233p(const SstConvDesc* d, cudaStream_t st) {
   return SST_OK;
 }
 
+static int launch_convpair_pixels(const SstConvDesc* d, cudaStream_t st) {
+  if (d->N % 192 != 0 || d->n_taps != 1 || d->taps[0][1] != 0 || d->taps[0][2] != 0 ||
+      d->in_W != d->Wt || d->in_H != d->Ht)
+    return SST_ERR_ARG;
+  CUtensorMap tmA, tmB, tmC;
+  memset(&tmA, 0, sizeof(tmA));
+  memset(&tmB, 0, sizeof(tmB));
+  memset(&tmC, 0, sizeof(tmC));
+  const uint64_t adims[5] = {(uint64_t)d->in_C, (uint64_t)d->in_W, (uint64_t)d->in_H,
+                             (uint64_t)d->in_T, (uint64_t)d->G};
+  if (!make_tmap_bf16_5d(&tmA, d->in, adims, 8, 16)) return SST_ERR_ARG;
+  if (!make_tmap_bf16_2d(&tmB, d->weight, (uint64_t)d->K, (uint64_t)d->N, 96)) return SST_ERR_ARG;
+  ConvArgs a;
+  memset(&a, 0, sizeof(a));
+  a.Ht = d->Ht; a.Wt = d->Wt;
+  a.tiles_x = ceil_div(d->Wt, c233c::TILE);
+  a.tiles_y = ceil_div(d->Ht, c233c::TILE);
+  a.t_lo = d->t_lo; a.t_cnt = d->t_cnt;
+  a.n_taps = 1;
+  for (int j = 0; j < 3; ++j) a.taps[0][j] = (signed char)d->taps[0][j];
+  a.kb_per_tap = d->in_C / BK;
+  a.N = d->N;
+  a.out_T = d->out_T;
+  a.bias = d->bias;
+  a.frames = d->frames; a.h = d->h; a.w = d->w; a.frame_base = d->frame_base;
+  const int n_blocks = d->N / 192;
+  const int64_t units = (int64_t)d->G * d->t_cnt * a.tiles_y * a.tiles_x * n_blocks;
+  if (units <= 0 || units > 0x7fffffff) return SST_ERR_ARG;
+  int n_sm = 0, dev = 0;
+  SST_CUDA_TRY(cudaGetDevice(&dev));
+  SST_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
+  const int64_t pairs = units < n_sm / 2 ? units : n_sm / 2;
+  auto kern = k_lt_convpair<false, false, true>;
+  const int smem = pair_smem<false, true>();
+  SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<(unsigned)(2 * pairs), c233c::THREADS, smem, st>>>(tmA, tmB, tmC, a, (int)units, n_blocks);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
 static int launch_convpair(const SstConvDesc* d, cudaStream_t st, bool halo) {
   if (d->N % 256 != 0 || d->in_W != d->Wt || d->in_H != d->Ht) return SST_ERR_ARG;
   if (halo && (d->t_lo != 0 || d->t_cnt != d->in_T || d->in_T != d->out_T)) return SST_ERR_ARG;
@@ -1707,11 +1795,16 @@ extern "C" int sst_lt_conv(const SstConvDesc* d, void* stream) {
       if (!d->codes || !d->idx || !d->mask || d->N != 16 || d->t_lo != 0 || d->t_cnt != 2)
         return SST_ERR_ARG;
       return lt::launch_conv<16, SST_LT_EPI_FSQ>(d, st);
-    case SST_LT_EPI_PIXELS:
+    case SST_LT_EPI_PIXELS: {
       if (!d->frames || d->h <= 0 || d->w <= 0 || d->frame_base < 0 ||
           d->frame_base + d->N / 192 > 9 || d->h > d->Ht * 8 || d->w > d->Wt * 8)
         return SST_ERR_ARG;
+      const char* m2 = getenv("SST_LT_GEMM");          // "tile": the per-tile kernel (A/B)
+      if (!(m2 && m2[0] == 't') && d->N % 192 == 0 && d->n_taps == 1 && d->taps[0][1] == 0 &&
+          d->taps[0][2] == 0 && d->in_W == d->Wt && d->in_H == d->Ht)
+        return lt::launch_convpair_pixels(d, st);
       return lt::launch_conv<192, SST_LT_EPI_PIXELS>(d, st);
+    }
     default:
       return SST_ERR_ARG;
   }
