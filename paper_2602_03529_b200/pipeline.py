@@ -356,3 +356,56 @@ class StreamBank:
             rec[j]["p_img"] = img.data_ptr() + ((slot * 2 + 1) * c.h * c.w * 3) * 4
             rec[j]["h"], rec[j]["w"], rec[j]["s"] = c.h, c.w, s
         return self.rings[s].stage(rec)
+
+
+class GraphedGopCodec:
+    """CUDA-graph replay of one GopCodec step (encode, drop, packetise, parse,
+    decode, reconstruct + blend) for a fixed batch, fixed device buffers and
+    one geometry -- the launch-bound regime (a single stream, one GoP in
+    flight).  Three graphs are captured: the first GoP (no blending) and the
+    two parities of the steady state (each blends with the working images
+    the other parity wrote).  Per step the host only refreshes the GoP ids
+    (device fills) and replays one graph."""
+
+    def __init__(self, codec: GopCodec, g: int, frames: torch.Tensor, out: torch.Tensor,
+                 drop_k: int = 0):
+        check_gop_tensor(frames, g, codec.H, codec.W, "frames")
+        check_gop_tensor(out, g, codec.H, codec.W, "out")
+        self.codec, self.g, self.frames, self.out, self.drop_k = codec, g, frames, out, drop_k
+        dev = frames.device
+        self.prev = []
+        for par in range(2):
+            d = np.zeros(g, dtype=_lib.PREV_DTYPE)
+            img = codec.img[1 - par]
+            for j in range(g):
+                d[j]["p_img"] = img.data_ptr() + ((j * 2 + 1) * codec.h * codec.w * 3) * 4
+                d[j]["h"], d[j]["w"], d[j]["s"] = codec.h, codec.w, codec.s
+            self.prev.append(torch.from_numpy(d.view(np.uint8).copy()).to(dev))
+        codec.set_gop_ids([0] * g)
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):                # warm-up outside capture
+            for par, prev in ((0, None), (1, self.prev[1]), (0, self.prev[0])):
+                self._body(par, prev)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.graphs = []
+        for par, prev in ((0, None), (1, self.prev[1]), (0, self.prev[0])):
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                self._body(par, prev)
+            self.graphs.append(gr)
+        self.k = 0
+
+    def _body(self, parity: int, prev) -> None:
+        c = self.codec
+        c.tokenize(self.frames, self.g)
+        c.select_and_pack(self.g, self.drop_k)
+        c.decode(self.g, parity)
+        c.reconstruct(self.g, parity, self.out, prev)
+
+    def step(self, gop_ids) -> None:
+        self.codec.set_gop_ids(gop_ids)
+        idx = 0 if self.k == 0 else (1 if self.k % 2 == 1 else 2)
+        self.graphs[idx].replay()
+        self.k += 1

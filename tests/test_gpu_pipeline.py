@@ -162,3 +162,23 @@ def test_non_contiguous_frames_are_rejected():
         c.encode(src, 1)
     with pytest.raises(ValueError, match="float32"):
         c.encode(src.contiguous().double(), 1)
+
+
+def test_graphed_codec_matches_eager():
+    """CUDA-graph replay of the GoP step == the eager launches (3 GoPs:
+    first without blending, then both parities with blending)."""
+    from paper_2602_03529_b200.pipeline import GraphedGopCodec
+    H, W, s = 72, 96, 3
+    clip = make_clip("noisy-motion", W, H, 27, seed=8)
+    c = GopCodec(1, H, W, s)
+    fr = torch.empty((1, 9, H, W, 3), device="cuda")
+    out = torch.empty_like(fr)
+    gr = GraphedGopCodec(c, 1, fr, out, drop_k=c.drop_k(0.2))
+    prev = None
+    for k in range(3):
+        fr.copy_(torch.from_numpy(clip.gop(k)[None].copy()))
+        gr.step([k])
+        torch.cuda.synchronize()
+        ref = O.pipeline_gop(clip.gop(k), s, gop_id=k, drop_rate=0.2, prev_out=prev)
+        prev = ref["frames"]
+        assert np.array_equal(out[0].cpu().numpy(), np.stack(ref["frames"])), k
