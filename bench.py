@@ -425,7 +425,7 @@ def run_e2e(a, rank, world, local_rank) -> dict:
 
     dev = torch.device("cuda", local_rank)
     E, H, W = a.e2e_streams, a.height, a.width
-    lanes = max(1, min(4, E))
+    lanes = max(1, min(int(os.environ.get("SST_E2E_LANES", "8")), E))   # one stream per lane
     per = [list(range(E))[i::lanes] for i in range(lanes)]
     src_dev = make_inputs([rank * E + i for i in range(E)], H, W, dev, n_sets=1)[0]
     fshape = tuple(src_dev.shape[1:])
