@@ -175,7 +175,10 @@ struct Enc {
 __device__ __forceinline__ void enc_symbol(Enc& e, Model& m, int sym) {
   const uint64_t c = model_cum(m, sym);
   const uint64_t d = c + m.cnt[sym];
-  const uint64_t r = e.range / m.total;
+  // range < 2^32 and total < 2^16: a 32-bit division gives the same quotient
+  // as the reference's arbitrary-precision one at a fraction of the cost of
+  // the 64-bit software division
+  const uint64_t r = (uint64_t)((uint32_t)e.range / m.total);
   e.low += c * r;
   e.range = (d - c) * r;
   while ((e.low ^ (e.low + e.range)) < kTop || e.range < kBottom) {
@@ -283,8 +286,10 @@ __global__ void __launch_bounds__(kRcThreads)
   int64_t pos = 0, nsym = 0;
   while (st == 0) {
     const uint64_t total = m.total;
-    const uint64_t r = range / total;
-    uint64_t val = (state - low) / r;              // rangecoder.py:217-219
+    const uint64_t r = (uint64_t)((uint32_t)range / (uint32_t)total);   // range < 2^32
+    const uint64_t diff = state - low;
+    uint64_t val = (diff >> 32) == 0 ? (uint64_t)((uint32_t)diff / (uint32_t)r)
+                                     : diff / r;   // rangecoder.py:217-219 (wrapped: 64-bit)
     if (val >= total) val = total - 1;
     uint32_t c32;
     const int sym = model_find(m, (uint32_t)val, &c32);
