@@ -18,6 +18,8 @@
 //                   positions of the scan (ballot/popc, index order), then one
 //                   thread codes them with a Fenwick tree for the cumulative
 //                   frequencies (O(log 510) instead of the reference's O(510)).
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace sst {
@@ -319,6 +321,236 @@ __global__ void __launch_bounds__(kRcThreads)
   status[g] = st;
 }
 
+// ---- warp-cooperative coder -------------------------------------------------
+// The same adaptive model and coder, but the model lives in the registers of
+// one warp: lane l owns the counts of symbols 16l .. 16l+15.  cum(s) is a warp
+// sum of per-lane partials (5 shuffles), the decoder's symbol search a warp
+// prefix scan + ballot, the halving is lane-parallel; the coder state is kept
+// uniform across the warp (every lane runs the same arithmetic), lane 0 writes.
+struct WarpModel {
+  uint32_t c[16];
+  uint32_t lsum;
+  uint32_t total;
+};
+
+__device__ __forceinline__ uint32_t warp_sum_u32(uint32_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ void wm_init(WarpModel& m, int lane) {
+  m.lsum = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    m.c[k] = (16 * lane + k) < kAlpha ? 1u : 0u;
+    m.lsum += m.c[k];
+  }
+  m.total = warp_sum_u32(m.lsum);
+}
+
+__device__ __forceinline__ void wm_lookup(const WarpModel& m, int lane, int sym, uint32_t& cum,
+                                          uint32_t& cnt) {
+  const int owner = sym >> 4, off = sym & 15;
+  uint32_t part = 0, mine = 0;
+  if (lane < owner) {
+    part = m.lsum;
+  } else if (lane == owner) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      if (k < off) part += m.c[k];
+      if (k == off) mine = m.c[k];
+    }
+  }
+  cum = warp_sum_u32(part);
+  cnt = __shfl_sync(0xffffffffu, mine, owner);
+}
+
+__device__ __forceinline__ void wm_update(WarpModel& m, int lane, int sym) {
+  const int owner = sym >> 4, off = sym & 15;
+  if (lane == owner) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (k == off) m.c[k] += 1;
+    m.lsum += 1;
+  }
+  m.total += 1;
+  if (m.total >= (uint32_t)kBottom) {               // rangecoder.py:147-149
+    m.lsum = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      m.c[k] = (m.c[k] + 1) / 2;                    // 0 stays 0 for s >= 510
+      m.lsum += m.c[k];
+    }
+    m.total = warp_sum_u32(m.lsum);
+  }
+}
+
+struct WEnc {
+  uint64_t low, range;
+  int64_t pos;
+};
+
+__device__ __forceinline__ void wenc_symbol(WEnc& e, WarpModel& m, int lane, int sym,
+                                            uint8_t* out, int64_t cap) {
+  uint32_t c32, n32;
+  wm_lookup(m, lane, sym, c32, n32);
+  const uint64_t r = (uint64_t)((uint32_t)e.range / m.total);
+  e.low += (uint64_t)c32 * r;
+  e.range = (uint64_t)n32 * r;
+  while ((e.low ^ (e.low + e.range)) < kTop || e.range < kBottom) {
+    if ((e.low ^ (e.low + e.range)) >= kTop) e.range = (kMask32 + 1 - e.low) & (kBottom - 1);
+    if (lane == 0 && e.pos < cap) out[e.pos] = (uint8_t)((e.low >> 24) & 0xFF);
+    e.pos += 1;
+    e.low = (e.low << 8) & kMask32;
+    e.range <<= 8;
+  }
+  wm_update(m, lane, sym);
+}
+
+__global__ void __launch_bounds__(kRcThreads)
+    k_rc_encode_w(const int16_t* __restrict__ scans, int64_t n, int64_t* __restrict__ idx_ws,
+                  uint8_t* __restrict__ out, int64_t cap, int64_t* __restrict__ out_len) {
+  __shared__ int s_warp[kRcThreads / 32];
+  __shared__ int64_t s_base;
+  const int g = blockIdx.x;
+  const int16_t* scan = scans + (int64_t)g * n;
+  int64_t* idx = idx_ws + (int64_t)g * n;
+  const int64_t nnz = compact_nonzero(scan, n, idx, s_warp, &s_base);
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  WarpModel m;
+  wm_init(m, lane);
+  uint8_t* o = out + (int64_t)g * cap;
+  WEnc e{0, kMask32, 0};
+  int64_t pos = 0;
+  // the non-zero positions and values are fetched 32 at a time (one per lane,
+  // coalesced) and handed to the serial coder by shuffles, so the coder never
+  // waits on a dependent global load
+  for (int64_t base = 0; base < nnz; base += 32) {
+    const int64_t ii = base + lane;
+    const int64_t jl = ii < nnz ? idx[ii] : 0;
+    const int vl = ii < nnz ? (int)scan[jl] : 0;
+    const int nb32 = (int)min((int64_t)32, nnz - base);
+    for (int t = 0; t < nb32; ++t) {                // rangecoder.py:75-94
+      const int64_t j = __shfl_sync(0xffffffffu, jl, t);
+      const int v = __shfl_sync(0xffffffffu, vl, t);
+      int64_t gap = j - pos;
+      while (gap > 255) {
+        wenc_symbol(e, m, lane, 255, o, cap);
+        gap -= 255;
+      }
+      if (gap) wenc_symbol(e, m, lane, (int)gap, o, cap);
+      wenc_symbol(e, m, lane, v < 0 ? v + 383 : v + 382, o, cap);
+      pos = j + 1;
+    }
+  }
+  wenc_symbol(e, m, lane, 0, o, cap);                // EOS
+  for (int k = 0; k < 4; ++k) {                      // rangecoder.py:182-184
+    if (lane == 0 && e.pos < cap) o[e.pos] = (uint8_t)((e.low >> 24) & 0xFF);
+    e.pos += 1;
+    e.low = (e.low << 8) & kMask32;
+  }
+  if (lane == 0) out_len[g] = e.pos > cap ? -e.pos : e.pos;
+}
+
+__global__ void __launch_bounds__(kRcThreads)
+    k_rc_decode_w(const uint8_t* __restrict__ data, const int64_t* __restrict__ off,
+                  const int64_t* __restrict__ len, int64_t n, int16_t* __restrict__ scans,
+                  int32_t* __restrict__ status) {
+  const int g = blockIdx.x;
+  int16_t* scan = scans + (int64_t)g * n;
+  for (int64_t j = threadIdx.x; j < n; j += kRcThreads) scan[j] = 0;
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  const uint8_t* src = data + off[g];
+  const int64_t nb = len[g];
+  int64_t p = 0;
+  int st = 0;
+  WarpModel m;
+  wm_init(m, lane);
+  // 32-byte window of the payload held one byte per lane (coalesced refill)
+  int64_t wbase = 0;
+  uint32_t wbyte = lane < nb ? src[lane] : 0;
+  auto next_byte = [&]() -> uint32_t {
+    if (p - wbase >= 32) {
+      wbase = p;
+      wbyte = wbase + lane < nb ? src[wbase + lane] : 0;
+    }
+    const uint32_t b = __shfl_sync(0xffffffffu, wbyte, (int)(p - wbase));
+    ++p;
+    return b;
+  };
+  uint64_t state = 0;
+  for (int k = 0; k < 4; ++k) {
+    if (p >= nb) { st = 1; break; }
+    state = (state << 8) | next_byte();
+  }
+  uint64_t low = 0, range = kMask32;
+  int64_t pos = 0, nsym = 0;
+  while (st == 0) {
+    const uint64_t total = m.total;
+    const uint64_t r = (uint64_t)((uint32_t)range / (uint32_t)total);
+    const uint64_t diff = state - low;
+    uint64_t val = (diff >> 32) == 0 ? (uint64_t)((uint32_t)diff / (uint32_t)r) : diff / r;
+    if (val >= total) val = total - 1;
+    // symbol search: lane prefix sums, then the owner lane scans its 16 counts
+    uint32_t incl = m.lsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += t;
+    }
+    const uint32_t excl = incl - m.lsum;
+    const unsigned bal = __ballot_sync(0xffffffffu, (uint64_t)excl <= val);
+    const int owner = 31 - __clz(bal);
+    int soff = 0;
+    uint32_t lo = 0, cnt = 0;
+    if (lane == owner) {
+      uint32_t acc = excl;
+      bool found = false;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        if (!found && (uint64_t)(acc + m.c[k]) > val) {
+          found = true;
+          soff = k;
+          lo = acc;
+          cnt = m.c[k];
+        }
+        acc += m.c[k];
+      }
+    }
+    soff = __shfl_sync(0xffffffffu, soff, owner);
+    lo = __shfl_sync(0xffffffffu, lo, owner);
+    cnt = __shfl_sync(0xffffffffu, cnt, owner);
+    const int sym = owner * 16 + soff;
+    low += (uint64_t)lo * r;
+    range = (uint64_t)cnt * r;
+    while ((low ^ (low + range)) < kTop || range < kBottom) {
+      if ((low ^ (low + range)) >= kTop) range = (kMask32 + 1 - low) & (kBottom - 1);
+      if (p >= nb) { st = 1; break; }
+      state = ((state << 8) | next_byte()) & kMask32;
+      low = (low << 8) & kMask32;
+      range <<= 8;
+    }
+    if (st) break;
+    wm_update(m, lane, sym);
+    ++nsym;
+    if (sym == 0) break;                            // EOS
+    if (sym <= 255) {                               // zero run (rangecoder.py:107-110)
+      pos += sym;
+      if (pos > n) { st = 2; break; }
+    } else {
+      if (pos >= n) { st = 3; break; }
+      if (lane == 0) scan[pos] = (int16_t)(sym <= 382 ? sym - 383 : sym - 382);
+      ++pos;
+    }
+    if (nsym >= (1 << 24)) { st = 4; break; }
+  }
+  if (lane == 0) status[g] = st;
+}
+
 // encode_stream for explicit symbol lists (one CTA / thread per stream)
 __global__ void k_rc_encode_symbols(const int32_t* __restrict__ syms, const int64_t* __restrict__ off,
                                     const int64_t* __restrict__ len, uint8_t* __restrict__ out,
@@ -479,8 +711,13 @@ extern "C" int sst_rc_encode(const int16_t* scans, int G, int64_t n, int64_t* id
   if (G < 0 || n < 0 || cap < 0) return SST_ERR_ARG;
   if (G == 0) return SST_OK;
   if ((n > 0 && (!scans || !idx_ws)) || !out || !out_len) return SST_ERR_ARG;
-  k_rc_encode<<<G, kRcThreads, 0, static_cast<cudaStream_t>(stream)>>>(scans, n, idx_ws, out, cap,
-                                                                         out_len);
+  const char* mode = getenv("SST_RC");            // "fenwick": single-thread model (A/B)
+  if (mode && mode[0] == 'f')
+    k_rc_encode<<<G, kRcThreads, 0, static_cast<cudaStream_t>(stream)>>>(scans, n, idx_ws, out, cap,
+                                                                           out_len);
+  else
+    k_rc_encode_w<<<G, kRcThreads, 0, static_cast<cudaStream_t>(stream)>>>(scans, n, idx_ws, out,
+                                                                             cap, out_len);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }
@@ -490,8 +727,13 @@ extern "C" int sst_rc_decode(const uint8_t* data, const int64_t* off, const int6
   if (G < 0 || n < 0) return SST_ERR_ARG;
   if (G == 0) return SST_OK;
   if (!data || !off || !len || !status || (n > 0 && !scans)) return SST_ERR_ARG;
-  k_rc_decode<<<G, kRcThreads, 0, static_cast<cudaStream_t>(stream)>>>(data, off, len, n, scans,
-                                                                         status);
+  const char* mode = getenv("SST_RC");
+  if (mode && mode[0] == 'f')
+    k_rc_decode<<<G, kRcThreads, 0, static_cast<cudaStream_t>(stream)>>>(data, off, len, n, scans,
+                                                                           status);
+  else
+    k_rc_decode_w<<<G, kRcThreads, 0, static_cast<cudaStream_t>(stream)>>>(data, off, len, n, scans,
+                                                                             status);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }
