@@ -219,7 +219,11 @@ __device__ __forceinline__ void load_window(float* win, const float* img, int w,
   }
 }
 
-template <int kBand, int NBUF, bool kPrev, int kN>
+// kDirect: the 9 frame values of each output float leave as coalesced
+// streaming stores straight from registers (a warp writes 128 contiguous bytes
+// of a frame row) instead of smem tiles + TMA bulk stores: no tile barrier,
+// no store-read wait, and no tile smem (more CTAs per SM).
+template <int kBand, int NBUF, bool kPrev, int kN, bool kDirect = false>
 __global__ void __launch_bounds__(kTQ)
     k_upscale_blend_tma(const __grid_constant__ CUtensorMap omap, const __grid_constant__ UpArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -277,11 +281,12 @@ __global__ void __launch_bounds__(kTQ)
   int ya = -1, yb = -1, qa = -1, qb = -1;
   double ia = 0, pa = 0, ib = 0, pb = 0, qva = 0, qvb = 0;   // horizontal taps at cached rows
   const int z0 = g * kGop;
+  const bool col_ok = q0 + tid < a.W * 3;
   for (int c0 = 0, ci = 0; c0 < rows; c0 += kTR, ++ci) {
     // NBUF tile sets rotate; a set is reused once the TMA store issued NBUF
     // chunks ago has finished reading it
     UpTile* tile = tiles + (ci % NBUF) * (nb + 1);
-    if (ci >= NBUF) {
+    if (!kDirect && ci >= NBUF) {
       if (tid == 0) {
         if (NBUF == 1) tma_store_wait_read();
         else tma_store_wait_read_1();
@@ -314,6 +319,43 @@ __global__ void __launch_bounds__(kTQ)
       const float ui = (float)clip_hi1(ia * ty.g + ib * ty.f);
       const float up = (float)clip_hi1(pa * ty.g + pb * ty.f);
       const int rr = r - c0;
+      if (kDirect) {
+        float fv[kN];
+        float f0 = ui;
+        if (has_prev) {
+          const AxisTap tp = S.ty_p[r];
+          if (tp.lo != qa) {
+            if (tp.lo == qb) qva = qvb;
+            else {
+              const float* wq = &S.win[2][tp.lo - pr0][0];
+              qva = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
+            }
+            qa = tp.lo;
+          }
+          if (tp.hi != qb) {
+            if (tp.hi == qa) qvb = qva;
+            else {
+              const float* wq = &S.win[2][tp.hi - pr0][0];
+              qvb = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
+            }
+            qb = tp.hi;
+          }
+          const double dq = (double)(float)clip_hi1(qva * tp.g + qvb * tp.f);
+          f0 = (float)clip_hi1(a.alpha[0] * dq + a.beta[0] * (double)ui);
+          const double dp = (double)up;
+#pragma unroll
+          for (int f = 1; f < kN; ++f) fv[f] = (float)clip_hi1(a.alpha[f] * dq + a.beta[f] * dp);
+        }
+        if (col_ok) {
+          const int64_t fstride = (int64_t)a.H * a.W * 3;
+          float* o = a.out + ((int64_t)z0 * a.H + oy0 + r) * (int64_t)a.W * 3 + q0 + tid;
+          __stcs(o, f0);
+#pragma unroll
+          for (int f = 1; f < kGop; ++f)
+            __stcs(o + f * fstride, (has_prev && f < kN) ? fv[f] : up);
+        }
+        continue;
+      }
       tile[nb][rr][tid] = up;
       if (has_prev) {
         const AxisTap tp = S.ty_p[r];
@@ -342,6 +384,7 @@ __global__ void __launch_bounds__(kTQ)
         tile[0][rr][tid] = ui;
       }
     }
+    if (kDirect) continue;
     fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
@@ -350,7 +393,7 @@ __global__ void __launch_bounds__(kTQ)
       tma_store_commit();
     }
   }
-  if (tid == 0) tma_store_wait_read();
+  if (!kDirect && tid == 0) tma_store_wait_read();
 }
 
 // Window rows/columns striped over the CTA's threads, held in registers
@@ -785,19 +828,19 @@ __global__ void __launch_bounds__(kMseThreads)
 
 using namespace sst;
 
-template <int BAND, int NBUF>
+template <int BAND, int NBUF, bool DIRECT = false>
 static int launch_k5(const CUtensorMap& omap, const UpArgs& a, const SstPrevDesc* prev,
                      int blend_n, cudaStream_t st) {
   dim3 grid(ceil_div(a.W * 3, kTQ), ceil_div(a.H, BAND), a.G);
   if (grid.y > 65535) return SST_ERR_ARG;
-  const int smem = up_tma_smem<BAND, NBUF>((prev ? blend_n : 1) + 1);
-  auto kern = k_upscale_blend_tma<BAND, NBUF, false, 1>;
+  const int smem = DIRECT ? tile_off<BAND>() : up_tma_smem<BAND, NBUF>((prev ? blend_n : 1) + 1);
+  auto kern = k_upscale_blend_tma<BAND, NBUF, false, 1, DIRECT>;
   if (prev) {
     switch (blend_n) {
-      case 1: kern = k_upscale_blend_tma<BAND, NBUF, true, 1>; break;
-      case 2: kern = k_upscale_blend_tma<BAND, NBUF, true, 2>; break;
-      case 3: kern = k_upscale_blend_tma<BAND, NBUF, true, 3>; break;
-      default: kern = k_upscale_blend_tma<BAND, NBUF, true, 4>; break;
+      case 1: kern = k_upscale_blend_tma<BAND, NBUF, true, 1, DIRECT>; break;
+      case 2: kern = k_upscale_blend_tma<BAND, NBUF, true, 2, DIRECT>; break;
+      case 3: kern = k_upscale_blend_tma<BAND, NBUF, true, 3, DIRECT>; break;
+      default: kern = k_upscale_blend_tma<BAND, NBUF, true, 4, DIRECT>; break;
     }
   }
   SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -838,6 +881,9 @@ extern "C" int sst_upscale_blend(const float* img, int G, int h, int w, int s, i
     const char* en = getenv("SST_K5_NBUF");
     const int band = (eb && atoi(eb) == 32) ? 32 : 16;
     const int nbuf = (en && atoi(en) == 2) ? 2 : 1;
+    if (var && var[0] == 'd')                     // "direct": streaming stores, no TMA tiles
+      return band == 16 ? launch_k5<16, 1, true>(omap, a, prev, blend_n, st)
+                        : launch_k5<32, 1, true>(omap, a, prev, blend_n, st);
     return band == 16 ? (nbuf == 1 ? launch_k5<16, 1>(omap, a, prev, blend_n, st)
                                    : launch_k5<16, 2>(omap, a, prev, blend_n, st))
                       : (nbuf == 1 ? launch_k5<32, 1>(omap, a, prev, blend_n, st)
