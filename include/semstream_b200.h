@@ -124,7 +124,9 @@ SST_API int sst_blend(const float* prev, const float* curr, int G, int H, int W,
  * img [G][9][h][w][3] -> out [G][9][H][W][3] (bilinear x s, clip, crop),
  * frames 0..n-1 blended with the previous GoP's frames 9-n..8 upscaled from
  * prev[g].p_img = that GoP's [9][h'][w'][3] working frames (blend_n <= 4).
- * Requires W*3*4 % 16 == 0 (TMA store). */
+ * Samples must be >= 0 (the decoder clamps to [0, 1]; the clip's lower bound
+ * is then a no-op and is not evaluated).  Any W; the windows of img are read
+ * by TMA when img is 16-byte aligned and w*3*4 % 16 == 0, else by cp.async. */
 SST_API int sst_upscale_blend9(const float* img, int G, int h, int w, int s, int H, int W,
                                const SstPrevDesc* prev, int blend_n, float* out, void* stream);
 

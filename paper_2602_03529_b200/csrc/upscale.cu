@@ -219,6 +219,11 @@ __device__ __forceinline__ void load_window(float* win, const float* img, int w,
   }
 }
 
+// cp.async completion for the K5-9 window loads
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
 // kDirect: the 9 frame values of each output float leave as coalesced
 // streaming stores straight from registers (a warp writes 128 contiguous bytes
 // of a frame row) instead of smem tiles + TMA bulk stores: no tile barrier,
@@ -396,230 +401,64 @@ __global__ void __launch_bounds__(kTQ)
   if (!kDirect && tid == 0) tma_store_wait_read();
 }
 
-// Window rows/columns striped over the CTA's threads, held in registers
-// between fetch() (global loads issued) and commit() (shared stores).
-template <int kPF>
-struct WinFetch {
-  float v[kPF];
-  int ncol, total, tid;
-  __device__ __forceinline__ void setup(int nrow, int nc, int t) {
-    ncol = nc; total = nrow * nc; tid = t;
-  }
-  __device__ __forceinline__ void fetch(const float* img, int w, int row0, int c0f) {
-#pragma unroll
-    for (int i = 0; i < kPF; ++i) {
-      const int e = tid + i * kTQ;
-      if (e < total) {
-        const int r = e / ncol, c = e - r * ncol;
-        v[i] = __ldg(img + ((int64_t)(row0 + r) * w) * 3 + c0f + c);
-      }
-    }
-  }
-  __device__ __forceinline__ void commit(float* win) const {
-#pragma unroll
-    for (int i = 0; i < kPF; ++i) {
-      const int e = tid + i * kTQ;
-      if (e < total) {
-        const int r = e / ncol, c = e - r * ncol;
-        win[r * kWF + c] = v[i];
-      }
-    }
-  }
+// ---- K5-9: all 9 frames per CTA, direct stores ----
+// A CTA owns a band of kBand output rows x kTQ output floats of one GoP.  It
+// loads the source windows of the GoP's 9 working frames (and of the previous
+// GoP's frames 9-n+f for the blended ones) in ONE load phase, then walks its
+// column down the band, interpolating the 9 frames per output row with the
+// row-cache control shared, and writes each row with coalesced streaming
+// stores (a warp covers 128 contiguous bytes of a frame row).
+//
+// Window loads (kLoad): 0 = register-staged loads, 1 = 4-byte cp.async,
+// 2 = one TMA box per frame for the current GoP (3-D tensor map over the
+// [G*9][h][w*3] working frames, out-of-range rows / columns zero-filled) with
+// cp.async for the previous GoP's windows (their base pointers are per-GoP
+// table entries, so they have no single tensor map).
+// TMA box rows start on a 16-byte boundary: the window is loaded from
+// x = (first column & ~3), up to 3 floats before the first column it needs,
+// so the pitch covers kWF + 3 floats.
+constexpr int kWF9 = 144;                  // window pitch (floats), 16-byte multiple
+
+template <int kBand>
+struct Up9fGeom {
+  static constexpr int kWR = kBand / 2 + 2;                      // max source rows (s >= 2)
+  static constexpr int kWin = (kWR * kWF9 + 31) / 32 * 32;       // floats per window, 128 B aligned
 };
 
-// ---- K5 for 9 distinct frames (learned decoder output) ----
-// Same band / window / TMA-store scheme as k_upscale_blend_tma, but every
-// frame of the GoP has its own working image: the CTA walks the 9 frames of
-// its (column tile, band), loading one source window per frame.  Boundary
-// frames f < n are blended with the previous GoP's frame 9-n+f, upscaled
-// from that GoP's working frames (prev[g].p_img = its [9][h][w][3] block):
-// for n <= 4 those tail frames are unblended reconstructions, so recomputing
-// them is exact and saves reading two full-resolution frames.
-template <int kBand, bool kPrev, int kN, int kSlots, bool kPre>
-__global__ void __launch_bounds__(kTQ)
-    k_upscale9_tma(const __grid_constant__ CUtensorMap omap, const __grid_constant__ UpArgs a) {
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  UpTmaSmem<kBand>& S = *reinterpret_cast<UpTmaSmem<kBand>*>(smem_raw);
-  UpTile* tiles = reinterpret_cast<UpTile*>(smem_raw + tile_off<kBand>());
-  const int tid = threadIdx.x;
-  const int q0 = blockIdx.x * kTQ;
-  const int oy0 = blockIdx.y * kBand;
-  const int g = blockIdx.z;
-  SstPrevDesc pd;
-  pd.p_img = nullptr;
-  pd.h = pd.w = pd.s = 1;
-  if (kPrev) pd = a.prev[g];
-  const bool has_prev = kPrev && pd.p_img != nullptr;
-  const int rows = min(kBand, a.H - oy0);
-  const int qlast = min(q0 + kTQ, a.W * 3) - 1;
-  if (tid < kBand) S.ty_c[tid] = axis_tap(oy0 + min(tid, rows - 1), a.h, a.s);
-  else if (tid < 2 * kBand) {
-    if (has_prev) S.ty_p[tid - kBand] = axis_tap(oy0 + min(tid - kBand, rows - 1), pd.h, pd.s);
-  } else if (tid == 2 * kBand) {
-    S.wx0[0] = axis_tap(q0 / 3, a.w, a.s).lo;
-    S.wx1[0] = axis_tap(qlast / 3, a.w, a.s).hi;
-  } else if (tid == 2 * kBand + 32 && has_prev) {
-    S.wx0[1] = axis_tap(q0 / 3, pd.w, pd.s).lo;
-    S.wx1[1] = axis_tap(qlast / 3, pd.w, pd.s).hi;
-  }
-  __syncthreads();
-
-  const int q = min(q0 + tid, a.W * 3 - 1);       // columns past the crop are clipped by TMA
-  const int ox = q / 3, ch = q - ox * 3;
-  const AxisTap tx = axis_tap(ox, a.w, a.s);
-  const int xl = (tx.lo - S.wx0[0]) * 3 + ch, xh = (tx.hi - S.wx0[0]) * 3 + ch;
-  AxisTap txp = tx;
-  int pxl = 0, pxh = 0;
-  if (has_prev) {
-    txp = axis_tap(ox, pd.w, pd.s);
-    pxl = (txp.lo - S.wx0[1]) * 3 + ch;
-    pxh = (txp.hi - S.wx0[1]) * 3 + ch;
-  }
-  const int r0 = S.ty_c[0].lo, r1 = S.ty_c[rows - 1].hi;
-  const int pr0 = has_prev ? S.ty_p[0].lo : 0, pr1 = has_prev ? S.ty_p[rows - 1].hi : 0;
-  const int64_t fimg = (int64_t)a.h * a.w * 3;
-  const int64_t pimg = (int64_t)pd.h * pd.w * 3;
-  const float* cur_base = a.img + (int64_t)g * kGop * fimg;
-  const int z0 = g * kGop;
-  // register prefetch of the next frame's source windows: the loads for
-  // frame f+1 are in flight while frame f is interpolated and stored
-  constexpr int kPF = ((kBand / 2 + 2) * kWF + kTQ - 1) / kTQ;
-  WinFetch<kPF> fc, fp;
-  fc.setup(r1 - r0 + 1, (S.wx1[0] - S.wx0[0] + 1) * 3, tid);
-  if (has_prev) fp.setup(pr1 - pr0 + 1, (S.wx1[1] - S.wx0[1] + 1) * 3, tid);
-  if (kPre) {
-    fc.fetch(cur_base, a.w, r0, S.wx0[0] * 3);
-    if (has_prev) fp.fetch(pd.p_img + (int64_t)(kGop - kN) * pimg, pd.w, pr0, S.wx0[1] * 3);
-  }
-  int ci = 0;   // tile counter across frames (kSlots tiles rotate)
-  for (int f = 0; f < kGop; ++f) {
-    const bool blend = has_prev && f < kN;
-    if (f > 0) __syncthreads();                   // everyone done with the previous windows
-    if (kPre) {
-      fc.commit(&S.win[0][0][0]);
-      if (blend) fp.commit(&S.win[2][0][0]);
-    } else {
-      load_window(&S.win[0][0][0], cur_base + (int64_t)f * fimg, a.w, r0, r1, S.wx0[0] * 3,
-                  S.wx1[0] * 3 + 3, tid);
-      if (blend)
-        load_window(&S.win[2][0][0], pd.p_img + (int64_t)(kGop - kN + f) * pimg, pd.w, pr0, pr1,
-                    S.wx0[1] * 3, S.wx1[1] * 3 + 3, tid);
-    }
-    __syncthreads();
-    if (kPre && f + 1 < kGop) fc.fetch(cur_base + (int64_t)(f + 1) * fimg, a.w, r0, S.wx0[0] * 3);
-    if (kPre && has_prev && f + 1 < kN)
-      fp.fetch(pd.p_img + (int64_t)(kGop - kN + f + 1) * pimg, pd.w, pr0, S.wx0[1] * 3);
-    int ya = -1, yb = -1, qa = -1, qb = -1;
-    double ia = 0, ib = 0, qva = 0, qvb = 0;
-    for (int c0 = 0; c0 < rows; c0 += kTR, ++ci) {
-      UpTile* tile = tiles + (ci % kSlots);
-      if (ci >= kSlots) {
-        if (tid == 0) tma_store_wait_read_n<kSlots - 1>();
-        __syncthreads();
-      }
-      const int cend = min(c0 + kTR, rows);
-      for (int r = c0; r < cend; ++r) {
-        const AxisTap ty = S.ty_c[r];
-        if (ty.lo != ya) {
-          if (ty.lo == yb) ia = ib;
-          else {
-            const float* wi = &S.win[0][ty.lo - r0][0];
-            ia = (double)wi[xl] * tx.g + (double)wi[xh] * tx.f;
-          }
-          ya = ty.lo;
-        }
-        if (ty.hi != yb) {
-          if (ty.hi == ya) ib = ia;
-          else {
-            const float* wi = &S.win[0][ty.hi - r0][0];
-            ib = (double)wi[xl] * tx.g + (double)wi[xh] * tx.f;
-          }
-          yb = ty.hi;
-        }
-        const float ui = (float)clip_hi1(ia * ty.g + ib * ty.f);
-        float v = ui;
-        if (blend) {
-          const AxisTap tp = S.ty_p[r];
-          if (tp.lo != qa) {
-            if (tp.lo == qb) qva = qvb;
-            else {
-              const float* wq = &S.win[2][tp.lo - pr0][0];
-              qva = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
-            }
-            qa = tp.lo;
-          }
-          if (tp.hi != qb) {
-            if (tp.hi == qa) qvb = qva;
-            else {
-              const float* wq = &S.win[2][tp.hi - pr0][0];
-              qvb = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
-            }
-            qb = tp.hi;
-          }
-          const double dq = (double)(float)clip_hi1(qva * tp.g + qvb * tp.f);
-          v = (float)clip_hi1(a.alpha[f] * dq + a.beta[f] * (double)ui);
-        }
-        (*tile)[r - c0][tid] = v;
-      }
-      fence_proxy_async_smem();
-      __syncthreads();
-      if (tid == 0) {
-        tma_store_3d(&omap, &(*tile)[0][0], q0, oy0 + c0, z0 + f);
-        tma_store_commit();
-      }
-    }
-  }
-  if (tid == 0) tma_store_wait_read();
-}
-
-// ---- K5-9, kF frames per pass, direct stores ----
-// The CTA loads the source windows of kF frames (and the previous GoP's
-// frames for blended ones) in ONE load phase -- kF x the bytes in flight of
-// the one-frame-per-pass kernel -- then interpolates the kF frames with shared
-// row-cache control and writes rows with coalesced streaming stores.
-template <int kBand, int kF>
+template <int kBand, int kP>
 struct Up9fSmem {
-  static constexpr int kWR = kBand / 2 + 2;
-  float win[kF][kWR][kWF];
-  float winp[4][kWR][kWF];          // previous GoP's frames 9-n+f, f < n <= 4
+  float win[kGop][Up9fGeom<kBand>::kWin];
+  float winp[kP > 0 ? kP : 1][Up9fGeom<kBand>::kWin];   // previous GoP's frames 9-n+f, f < n = kP
   AxisTap ty_c[kBand], ty_p[kBand];
   int wx0[2], wx1[2];
+  int xs;                    // current window's column shift (TMA alignment), 0 for cp.async
+  uint64_t bar;
 };
 
-// One pass over NF consecutive frames f0..f0+NF-1 of the CTA's (column tile,
-// band): load their windows (and, when BLEND, the previous GoP's frames
-// 9-n+f) in one phase, then interpolate all NF frames per output row with the
-// row-cache control shared, and stream the rows out.
-template <int kBand, int kF, int NF, bool BLEND, int kN>
-__device__ __forceinline__ void k5_9_pass(Up9fSmem<kBand, kF>& S, const UpArgs& a,
-                                          const SstPrevDesc& pd, int g, int f0, int q0, int oy0,
-                                          int rows, const AxisTap& tx, int xl, int xh,
-                                          const AxisTap& txp, int pxl, int pxh, bool col_ok) {
+// (float)clip_hi1(x) as one float min: float rounding is monotonic, so
+// x > 1 implies (float)x >= 1 and x <= 1 implies (float)x <= 1 -- the result
+// is bit-identical (including -0.0) and costs one FMNMX instead of a DSETP and
+// two FSELs on the 64-bit value.
+__device__ __forceinline__ float f32_clip_hi1(double x) { return fminf((float)x, 1.0f); }
+
+// Interpolate frames f0..f0+NF-1 from their windows with the row-cache
+// control shared, and stream the rows out.
+template <int kBand, int kP, int NF, bool BLEND>
+__device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP>& S, const UpArgs& a, int g,
+                                             int f0, int q0, int oy0, int rows,
+                                             const AxisTap& tx, int xl, int xh,
+                                             const AxisTap& txp, int pxl, int pxh) {
   const int tid = threadIdx.x;
-  const int r0 = S.ty_c[0].lo, r1 = S.ty_c[rows - 1].hi;
-  const int pr0 = BLEND ? S.ty_p[0].lo : 0, pr1 = BLEND ? S.ty_p[rows - 1].hi : 0;
-  const int64_t fimg = (int64_t)a.h * a.w * 3;
-  const float* cur = a.img + ((int64_t)g * kGop + f0) * fimg;
-  __syncthreads();                                  // previous pass done with the windows
-#pragma unroll
-  for (int j = 0; j < NF; ++j)
-    load_window(&S.win[j][0][0], cur + (int64_t)j * fimg, a.w, r0, r1, S.wx0[0] * 3,
-                S.wx1[0] * 3 + 3, tid);
-  if (BLEND) {
-    const int64_t pimg = (int64_t)pd.h * pd.w * 3;
-#pragma unroll
-    for (int j = 0; j < NF; ++j)
-      load_window(&S.winp[j][0][0], pd.p_img + (int64_t)(kGop - kN + f0 + j) * pimg, pd.w, pr0,
-                  pr1, S.wx0[1] * 3, S.wx1[1] * 3 + 3, tid);
-  }
-  __syncthreads();
-  if (!col_ok) return;
+  const int r0 = S.ty_c[0].lo;
+  const int pr0 = BLEND ? S.ty_p[0].lo : 0;
   const int64_t orow = (int64_t)a.W * 3;
+  const int64_t fstride = (int64_t)a.H * orow;
+  float* op = a.out + ((int64_t)(g * kGop + f0) * a.H + oy0) * orow + q0 + tid;
   int ya = -1, yb = -1, qa = -1, qb = -1;
   double ia[NF], ib[NF], qva[BLEND ? NF : 1], qvb[BLEND ? NF : 1];
 #pragma unroll
   for (int j = 0; j < NF; ++j) ia[j] = ib[j] = 0.0;
-  for (int r = 0; r < rows; ++r) {
+  for (int r = 0; r < rows; ++r, op += orow) {
     const AxisTap ty = S.ty_c[r];
     if (ty.lo != ya) {
       if (ty.lo == yb) {
@@ -628,8 +467,8 @@ __device__ __forceinline__ void k5_9_pass(Up9fSmem<kBand, kF>& S, const UpArgs& 
       } else {
 #pragma unroll
         for (int j = 0; j < NF; ++j) {
-          const float* wr = &S.win[j][ty.lo - r0][0];
-          ia[j] = (double)wr[xl] * tx.g + (double)wr[xh] * tx.f;
+          const float* wr = &S.win[f0 + j][(ty.lo - r0) * kWF9];
+          ia[j] = (double)wr[xl] * tx.g + (double)wr[xh] * tx.f;     // codec.py:233
         }
       }
       ya = ty.lo;
@@ -641,7 +480,7 @@ __device__ __forceinline__ void k5_9_pass(Up9fSmem<kBand, kF>& S, const UpArgs& 
       } else {
 #pragma unroll
         for (int j = 0; j < NF; ++j) {
-          const float* wr = &S.win[j][ty.hi - r0][0];
+          const float* wr = &S.win[f0 + j][(ty.hi - r0) * kWF9];
           ib[j] = (double)wr[xl] * tx.g + (double)wr[xh] * tx.f;
         }
       }
@@ -657,7 +496,7 @@ __device__ __forceinline__ void k5_9_pass(Up9fSmem<kBand, kF>& S, const UpArgs& 
         } else {
 #pragma unroll
           for (int j = 0; j < NF; ++j) {
-            const float* wq = &S.winp[j][tp.lo - pr0][0];
+            const float* wq = &S.winp[j][(tp.lo - pr0) * kWF9];
             qva[j] = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
           }
         }
@@ -670,32 +509,54 @@ __device__ __forceinline__ void k5_9_pass(Up9fSmem<kBand, kF>& S, const UpArgs& 
         } else {
 #pragma unroll
           for (int j = 0; j < NF; ++j) {
-            const float* wq = &S.winp[j][tp.hi - pr0][0];
+            const float* wq = &S.winp[j][(tp.hi - pr0) * kWF9];
             qvb[j] = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
           }
         }
         qb = tp.hi;
       }
     }
-    float* op = a.out + ((int64_t)(g * kGop + f0) * a.H + oy0 + r) * orow + q0 + tid;
 #pragma unroll
     for (int j = 0; j < NF; ++j) {
-      const float ui = (float)clip_hi1(ia[j] * ty.g + ib[j] * ty.f);
+      const float ui = f32_clip_hi1(ia[j] * ty.g + ib[j] * ty.f);     // codec.py:235
       float v = ui;
-      if (BLEND) {
-        const double dq = (double)(float)clip_hi1(qva[j] * tp.g + qvb[j] * tp.f);
-        v = (float)clip_hi1(a.alpha[f0 + j] * dq + a.beta[f0 + j] * (double)ui);
+      if (BLEND) {   // codec.py:289-293
+        const double dq = (double)f32_clip_hi1(qva[j] * tp.g + qvb[j] * tp.f);
+        v = f32_clip_hi1(a.alpha[f0 + j] * dq + a.beta[f0 + j] * (double)ui);
       }
-      __stcs(op + (int64_t)j * a.H * orow, v);
+      __stcs(op + j * fstride, v);
     }
   }
 }
 
-template <int kBand, int kF, bool kPrev, int kN>
-__global__ void __launch_bounds__(kTQ)
-    k_upscale9f(const __grid_constant__ UpArgs a) {
+template <int kLoad>
+__device__ __forceinline__ void k5_9_window(float* dst, const float* img, int w, int r0, int r1,
+                                            int c0f, int c1f, int tid) {
+  const int ncol = c1f - c0f;
+  const int lane = tid & 31, wid = tid >> 5;
+  for (int j = wid; j <= r1 - r0; j += kTQ / 32) {
+    const float* src = img + ((int64_t)(r0 + j) * w) * 3 + c0f;
+    float* d = dst + j * kWF9;
+#pragma unroll
+    for (int c = lane; c < kWF; c += 32) {
+      if (c < ncol) {
+        if (kLoad == 0)
+          d[c] = __ldg(src + c);
+        else
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(d + c)),
+                       "l"(src + c)
+                       : "memory");
+      }
+    }
+  }
+}
+
+template <int kBand, bool kPrev, int kN, int kLoad>
+__global__ void __launch_bounds__(kTQ, 3)
+    k_upscale9f(const __grid_constant__ CUtensorMap imap, const __grid_constant__ UpArgs a) {
+  constexpr int kP = kPrev ? kN : 0;
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  Up9fSmem<kBand, kF>& S = *reinterpret_cast<Up9fSmem<kBand, kF>*>(smem_raw);
+  Up9fSmem<kBand, kP>& S = *reinterpret_cast<Up9fSmem<kBand, kP>*>(smem_raw);
   const int tid = threadIdx.x;
   const int q0 = blockIdx.x * kTQ;
   const int oy0 = blockIdx.y * kBand;
@@ -713,50 +574,82 @@ __global__ void __launch_bounds__(kTQ)
   } else if (tid == 2 * kBand) {
     S.wx0[0] = axis_tap(q0 / 3, a.w, a.s).lo;
     S.wx1[0] = axis_tap(qlast / 3, a.w, a.s).hi;
+    S.xs = kLoad == 2 ? (S.wx0[0] * 3) & 3 : 0;
+    if (kLoad == 2) {
+      mbar_init(&S.bar, 1);
+      fence_mbar_init();
+    }
   } else if (tid == 2 * kBand + 32 && has_prev) {
     S.wx0[1] = axis_tap(q0 / 3, pd.w, pd.s).lo;
     S.wx1[1] = axis_tap(qlast / 3, pd.w, pd.s).hi;
   }
   __syncthreads();
-  const int q = min(q0 + tid, a.W * 3 - 1);
+
+  // ---- load phase ----
+  {
+    const int r0 = S.ty_c[0].lo, r1 = S.ty_c[rows - 1].hi;
+    if (kLoad == 2) {
+      if (tid == 0) {
+        constexpr uint32_t kBox = Up9fGeom<kBand>::kWR * kWF9 * sizeof(float);
+        mbar_expect_tx(&S.bar, kGop * kBox);
+#pragma unroll 1
+        for (int f = 0; f < kGop; ++f)
+          tma_load_3d(S.win[f], &imap, S.wx0[0] * 3 - S.xs, r0, g * kGop + f, &S.bar);
+      }
+    } else {
+      const int64_t fimg = (int64_t)a.h * a.w * 3;
+      const float* cur = a.img + (int64_t)g * kGop * fimg;
+#pragma unroll 1
+      for (int f = 0; f < kGop; ++f)
+        k5_9_window<kLoad>(S.win[f], cur + f * fimg, a.w, r0, r1, S.wx0[0] * 3, S.wx1[0] * 3 + 3,
+                           tid);
+    }
+    if (has_prev) {
+      const int pr0 = S.ty_p[0].lo, pr1 = S.ty_p[rows - 1].hi;
+      const int64_t pimg = (int64_t)pd.h * pd.w * 3;
+#pragma unroll
+      for (int j = 0; j < kP; ++j)
+        k5_9_window<kLoad == 0 ? 0 : 1>(S.winp[j], pd.p_img + (kGop - kN + j) * pimg, pd.w, pr0,
+                                        pr1, S.wx0[1] * 3, S.wx1[1] * 3 + 3, tid);
+    }
+    if (kLoad != 0) cp_async_wait_all();
+    if (kLoad == 2) mbar_wait(&S.bar, 0);
+    __syncthreads();
+  }
+
+  if (q0 + tid >= a.W * 3) return;
+  const int q = q0 + tid;
   const int ox = q / 3, ch = q - ox * 3;
   const AxisTap tx = axis_tap(ox, a.w, a.s);
-  const int xl = (tx.lo - S.wx0[0]) * 3 + ch, xh = (tx.hi - S.wx0[0]) * 3 + ch;
-  AxisTap txp = tx;
-  int pxl = 0, pxh = 0;
+  const int xl = (tx.lo - S.wx0[0]) * 3 + ch + S.xs, xh = (tx.hi - S.wx0[0]) * 3 + ch + S.xs;
   if (has_prev) {
-    txp = axis_tap(ox, pd.w, pd.s);
-    pxl = (txp.lo - S.wx0[1]) * 3 + ch;
-    pxh = (txp.hi - S.wx0[1]) * 3 + ch;
-  }
-  const bool col_ok = q0 + tid < a.W * 3;
-  if (kPrev && has_prev) {
-    k5_9_pass<kBand, kF, kN, true, kN>(S, a, pd, g, 0, q0, oy0, rows, tx, xl, xh, txp, pxl, pxh,
-                                       col_ok);
-    k5_9_pass<kBand, kF, kGop - kN, false, kN>(S, a, pd, g, kN, q0, oy0, rows, tx, xl, xh, txp,
-                                               pxl, pxh, col_ok);
+    const AxisTap txp = axis_tap(ox, pd.w, pd.s);
+    const int pxl = (txp.lo - S.wx0[1]) * 3 + ch, pxh = (txp.hi - S.wx0[1]) * 3 + ch;
+    k5_9_compute<kBand, kP, kN, true>(S, a, g, 0, q0, oy0, rows, tx, xl, xh, txp, pxl, pxh);
+    k5_9_compute<kBand, kP, kGop - kN, false>(S, a, g, kN, q0, oy0, rows, tx, xl, xh, txp, pxl,
+                                              pxh);
   } else {
-    k5_9_pass<kBand, kF, kGop, false, kN>(S, a, pd, g, 0, q0, oy0, rows, tx, xl, xh, txp, pxl, pxh,
-                                          col_ok);
+    k5_9_compute<kBand, kP, kGop, false>(S, a, g, 0, q0, oy0, rows, tx, xl, xh, tx, 0, 0);
   }
 }
 
-template <int BAND, int F>
-static int launch_k5_9f(const UpArgs& a, const SstPrevDesc* prev, int blend_n, cudaStream_t st) {
+template <int BAND, int LOAD>
+static int launch_k5_9f(const CUtensorMap& imap, const UpArgs& a, const SstPrevDesc* prev,
+                        int blend_n, cudaStream_t st) {
   dim3 grid(ceil_div(a.W * 3, kTQ), ceil_div(a.H, BAND), a.G);
   if (grid.y > 65535) return SST_ERR_ARG;
-  const int smem = (int)sizeof(Up9fSmem<BAND, F>);
-  auto kern = k_upscale9f<BAND, F, false, 1>;
+  int smem = (int)sizeof(Up9fSmem<BAND, 0>);
+  auto kern = k_upscale9f<BAND, false, 1, LOAD>;
   if (prev) {
     switch (blend_n) {
-      case 1: kern = k_upscale9f<BAND, F, true, 1>; break;
-      case 2: kern = k_upscale9f<BAND, F, true, 2>; break;
-      case 3: kern = k_upscale9f<BAND, F, true, 3>; break;
-      default: kern = k_upscale9f<BAND, F, true, 4>; break;
+      case 1: kern = k_upscale9f<BAND, true, 1, LOAD>; smem = sizeof(Up9fSmem<BAND, 1>); break;
+      case 2: kern = k_upscale9f<BAND, true, 2, LOAD>; smem = sizeof(Up9fSmem<BAND, 2>); break;
+      case 3: kern = k_upscale9f<BAND, true, 3, LOAD>; smem = sizeof(Up9fSmem<BAND, 3>); break;
+      default: kern = k_upscale9f<BAND, true, 4, LOAD>; smem = sizeof(Up9fSmem<BAND, 4>); break;
     }
   }
   SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  kern<<<grid, kTQ, smem, st>>>(a);
+  kern<<<grid, kTQ, smem, st>>>(imap, a);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }
@@ -896,27 +789,6 @@ extern "C" int sst_upscale_blend(const float* img, int G, int h, int w, int s, i
   return SST_OK;
 }
 
-template <int BAND, int SLOTS, bool PRE>
-static int launch_k5_9(const CUtensorMap& omap, const UpArgs& a, const SstPrevDesc* prev,
-                       int blend_n, cudaStream_t st) {
-  dim3 grid(ceil_div(a.W * 3, kTQ), ceil_div(a.H, BAND), a.G);
-  if (grid.y > 65535) return SST_ERR_ARG;
-  const int smem = up_tma_smem<BAND, 1>(SLOTS);
-  auto kern = k_upscale9_tma<BAND, false, 1, SLOTS, PRE>;
-  if (prev) {
-    switch (blend_n) {
-      case 1: kern = k_upscale9_tma<BAND, true, 1, SLOTS, PRE>; break;
-      case 2: kern = k_upscale9_tma<BAND, true, 2, SLOTS, PRE>; break;
-      case 3: kern = k_upscale9_tma<BAND, true, 3, SLOTS, PRE>; break;
-      default: kern = k_upscale9_tma<BAND, true, 4, SLOTS, PRE>; break;
-    }
-  }
-  SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  kern<<<grid, kTQ, smem, st>>>(omap, a);
-  SST_LAUNCH_CHECK();
-  return SST_OK;
-}
-
 extern "C" int sst_upscale_blend9(const float* img, int G, int h, int w, int s, int H, int W,
                                   const SstPrevDesc* prev, int blend_n, float* out, void* stream) {
   if (G < 0 || h <= 0 || w <= 0 || H <= 0 || W <= 0) return SST_ERR_ARG;
@@ -933,43 +805,26 @@ extern "C" int sst_upscale_blend9(const float* img, int G, int h, int w, int s, 
     a.alpha[i - 1] = (double)(blend_n - i) / (double)blend_n;
     a.beta[i - 1] = 1.0 - a.alpha[i - 1];
   }
-  CUtensorMap omap;
-  memset(&omap, 0, sizeof(omap));
-  if (!make_tmap_f32_3d(&omap, out, (uint64_t)W * 3, (uint64_t)H, (uint64_t)G * kGop, kTQ, kTR))
-    return SST_ERR_UNSUPPORTED;   // TMA alignment: W*3*4 bytes must be a multiple of 16
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  // A/B switch for profiling: SST_K5_9="<band>,<tiles>[p]" (band 16 | 32,
-  // tiles 1 | 2 | 6, p = register prefetch of the next frame's window).
-  int band = 32, slots = 2;
-  bool pre = false;
-  // Measured (k5_9_micro, 32 x 1080p GoPs, s=3, without / with blend):
-  // nine frames per CTA with 16-row bands and direct stores 1.89 / 2.62 ms
-  // (default); the one-frame-per-pass TMA-store kernel ("32,1") 2.37 / 2.88;
-  // a column-private variant 3.0 / 4.1; nine frames with 32-row bands 3.5 / 4.8.
-  slots = 1;
-  const char* v9 = getenv("SST_K5_9");
-  if (!v9 || v9[0] == 'f') {    // default: all 9 frames per CTA ("f9[,band]"), direct stores
-    const char* c = v9 ? strchr(v9, ',') : nullptr;
-    const int B = c ? atoi(c + 1) : 16;
-    return B == 32 ? launch_k5_9f<32, 9>(a, prev, blend_n, st)
-                   : launch_k5_9f<16, 9>(a, prev, blend_n, st);
+  // Window loads: TMA boxes for the current GoP when its frames admit a
+  // tensor map (16-byte aligned base and rows), else cp.async.  A/B switch:
+  // SST_K5_9=sync | async | tma.  Measured (scripts/k5_9_micro.py, 32 x 1080p
+  // GoPs, s=3, without / with blend n=2): register-staged loads 1.89 / 2.59 ms,
+  // cp.async 1.49 / 2.12 ms.  Earlier layouts, since removed: one frame per
+  // pass with TMA-store tiles 2.37 / 2.88 ms, column-private threads 3.0 / 4.1,
+  // 32-row bands 2.24 / 3.28 (cp.async) and 3.5 / 4.8 (register-staged).
+  CUtensorMap imap;
+  memset(&imap, 0, sizeof(imap));
+  const bool tma_in = make_tmap_f32_3d(&imap, img, (uint64_t)w * 3, (uint64_t)h,
+                                       (uint64_t)G * kGop, kWF9, Up9fGeom<16>::kWR);
+  int load = tma_in ? 2 : 1;
+  if (const char* v9 = getenv("SST_K5_9")) {
+    if (!strcmp(v9, "sync")) load = 0;
+    else if (!strcmp(v9, "async")) load = 1;
   }
-  if (const char* v = v9) {
-    band = atoi(v) == 16 ? 16 : 32;
-    const char* c = strchr(v, ',');
-    if (c) { slots = atoi(c + 1); pre = strchr(c, 'p') != nullptr; }
-  }
-  if (band == 16) {
-    if (slots == 1) return pre ? launch_k5_9<16, 1, true>(omap, a, prev, blend_n, st)
-                               : launch_k5_9<16, 1, false>(omap, a, prev, blend_n, st);
-    return pre ? launch_k5_9<16, 2, true>(omap, a, prev, blend_n, st)
-               : launch_k5_9<16, 2, false>(omap, a, prev, blend_n, st);
-  }
-  if (slots == 6) return pre ? launch_k5_9<32, 6, true>(omap, a, prev, blend_n, st)
-                             : launch_k5_9<32, 6, false>(omap, a, prev, blend_n, st);
-  if (slots == 1) return launch_k5_9<32, 1, false>(omap, a, prev, blend_n, st);
-  return pre ? launch_k5_9<32, 2, true>(omap, a, prev, blend_n, st)
-             : launch_k5_9<32, 2, false>(omap, a, prev, blend_n, st);
+  if (load == 2) return launch_k5_9f<16, 2>(imap, a, prev, blend_n, st);
+  if (load == 1) return launch_k5_9f<16, 1>(imap, a, prev, blend_n, st);
+  return launch_k5_9f<16, 0>(imap, a, prev, blend_n, st);
 }
 
 extern "C" int sst_upscale(const float* img, int64_t n, int h, int w, int s, int crop_h, int crop_w,
