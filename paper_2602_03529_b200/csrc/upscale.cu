@@ -56,6 +56,12 @@ __device__ __forceinline__ double bilerp(const T* img, int w, const AxisTap& ty,
 // the lower bound never triggers and -0.0 passes through exactly as in numpy.
 __device__ __forceinline__ double clip_hi1(double x) { return x > 1.0 ? 1.0 : x; }
 
+// f32_clip_hi1(x) as one float min: float rounding is monotonic, so
+// x > 1 implies (float)x >= 1 and x <= 1 implies (float)x <= 1 -- the result
+// is bit-identical (including -0.0) and costs one FMNMX instead of a DSETP and
+// two FSELs on the 64-bit value.
+__device__ __forceinline__ float f32_clip_hi1(double x) { return fminf((float)x, 1.0f); }
+
 __device__ __forceinline__ float blend_px(float prev, float curr, double alpha) {
   double v = alpha * (double)prev + (1.0 - alpha) * (double)curr;   // codec.py:293
   return (float)clip01(v);
@@ -187,13 +193,20 @@ __global__ void __launch_bounds__(kUpThreads) k_upscale_blend(const __grid_const
 constexpr int kTR = 8;                     // output rows per stored tile
 constexpr int kTQ = 256;                   // output floats per tile row (= threads)
 constexpr int kWF = (kTQ / 6 + 3) * 3 + 3; // max source floats per window row (s >= 2)
+// TMA box rows start on a 16-byte boundary: the window is loaded from
+// x = (first column & ~3), up to 3 floats before the first column it needs,
+// so the pitch covers kWF + 3 floats.
+constexpr int kWF9 = 144;                  // window pitch (floats), 16-byte multiple
 
 template <int BAND>
 struct UpTmaSmem {
   static constexpr int kWR = BAND / 2 + 2;   // max source rows per band (s >= 2)
-  float win[3][kWR][kWF];                  // I, P, previous P windows
+  static constexpr int kWin = (kWR * kWF9 + 31) / 32 * 32;   // floats per window, 128 B aligned
+  float win[3][kWin];                      // I, P, previous P windows (row pitch kWF9)
   AxisTap ty_c[BAND], ty_p[BAND];
   int wx0[2], wx1[2];                      // window column range (source px) cur / prev
+  int xs;                                  // I/P window column shift (TMA alignment)
+  uint64_t bar;                            // TMA window loads
 };
 typedef float UpTile[kTR][kTQ];
 template <int BAND>
@@ -212,7 +225,7 @@ __device__ __forceinline__ void load_window(float* win, const float* img, int w,
   const int lane = tid & 31, wid = tid >> 5;
   for (int j = wid; j <= r1 - r0; j += kTQ / 32) {
     const float* src = img + ((int64_t)(r0 + j) * w) * 3 + c0f;
-    float* dst = win + j * kWF;
+    float* dst = win + j * kWF9;
 #pragma unroll
     for (int c = lane; c < kWF; c += 32)
       if (c < ncol) dst[c] = __ldg(src + c);
@@ -228,9 +241,10 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // streaming stores straight from registers (a warp writes 128 contiguous bytes
 // of a frame row) instead of smem tiles + TMA bulk stores: no tile barrier,
 // no store-read wait, and no tile smem (more CTAs per SM).
-template <int kBand, int NBUF, bool kPrev, int kN, bool kDirect = false>
+template <int kBand, int NBUF, bool kPrev, int kN, bool kDirect = false, bool kTmaIn = false>
 __global__ void __launch_bounds__(kTQ)
-    k_upscale_blend_tma(const __grid_constant__ CUtensorMap omap, const __grid_constant__ UpArgs a) {
+    k_upscale_blend_tma(const __grid_constant__ CUtensorMap omap, const __grid_constant__ CUtensorMap imap,
+                        const __grid_constant__ UpArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   UpTmaSmem<kBand>& S = *reinterpret_cast<UpTmaSmem<kBand>*>(smem_raw);
   UpTile* tiles = reinterpret_cast<UpTile*>(smem_raw + tile_off<kBand>());
@@ -251,6 +265,11 @@ __global__ void __launch_bounds__(kTQ)
   } else if (tid == 2 * kBand) {
     S.wx0[0] = axis_tap(q0 / 3, a.w, a.s).lo;
     S.wx1[0] = axis_tap(qlast / 3, a.w, a.s).hi;
+    S.xs = kTmaIn ? (S.wx0[0] * 3) & 3 : 0;
+    if (kTmaIn) {
+      mbar_init(&S.bar, 1);
+      fence_mbar_init();
+    }
   } else if (tid == 2 * kBand + 32 && has_prev) {
     S.wx0[1] = axis_tap(q0 / 3, pd.w, pd.s).lo;
     S.wx1[1] = axis_tap(qlast / 3, pd.w, pd.s).hi;
@@ -263,11 +282,22 @@ __global__ void __launch_bounds__(kTQ)
   const int pr0 = has_prev ? S.ty_p[0].lo : 0;
   {
     const int r1 = S.ty_c[rows - 1].hi;
-    load_window(&S.win[0][0][0], iimg, a.w, r0, r1, S.wx0[0] * 3, S.wx1[0] * 3 + 3, tid);
-    load_window(&S.win[1][0][0], pimg, a.w, r0, r1, S.wx0[0] * 3, S.wx1[0] * 3 + 3, tid);
+    if (kTmaIn) {
+      // I and P windows: one TMA box each from the [G*2][h][w*3] tensor map
+      if (tid == 0) {
+        constexpr uint32_t kBox = UpTmaSmem<kBand>::kWR * kWF9 * sizeof(float);
+        mbar_expect_tx(&S.bar, 2 * kBox);
+        tma_load_3d(S.win[0], &imap, S.wx0[0] * 3 - S.xs, r0, 2 * g, &S.bar);
+        tma_load_3d(S.win[1], &imap, S.wx0[0] * 3 - S.xs, r0, 2 * g + 1, &S.bar);
+      }
+    } else {
+      load_window(S.win[0], iimg, a.w, r0, r1, S.wx0[0] * 3, S.wx1[0] * 3 + 3, tid);
+      load_window(S.win[1], pimg, a.w, r0, r1, S.wx0[0] * 3, S.wx1[0] * 3 + 3, tid);
+    }
     if (has_prev)
-      load_window(&S.win[2][0][0], pd.p_img, pd.w, pr0, S.ty_p[rows - 1].hi, S.wx0[1] * 3,
+      load_window(S.win[2], pd.p_img, pd.w, pr0, S.ty_p[rows - 1].hi, S.wx0[1] * 3,
                   S.wx1[1] * 3 + 3, tid);
+    if (kTmaIn) mbar_wait(&S.bar, 0);
   }
   __syncthreads();
 
@@ -275,7 +305,7 @@ __global__ void __launch_bounds__(kTQ)
   const int ox = q / 3, ch = q - ox * 3;
   const int nb = has_prev ? kN : 1;                // tiles 0..nb-1: frames 0..nb-1; tile nb: P
   const AxisTap tx = axis_tap(ox, a.w, a.s);
-  const int xl = (tx.lo - S.wx0[0]) * 3 + ch, xh = (tx.hi - S.wx0[0]) * 3 + ch;
+  const int xl = (tx.lo - S.wx0[0]) * 3 + ch + S.xs, xh = (tx.hi - S.wx0[0]) * 3 + ch + S.xs;
   AxisTap txp = tx;
   int pxl = 0, pxh = 0;
   if (has_prev) {
@@ -304,8 +334,8 @@ __global__ void __launch_bounds__(kTQ)
       if (ty.lo != ya) {
         if (ty.lo == yb) { ia = ib; pa = pb; }
         else {
-          const float* wi = &S.win[0][ty.lo - r0][0];
-          const float* wp = &S.win[1][ty.lo - r0][0];
+          const float* wi = &S.win[0][(ty.lo - r0) * kWF9];
+          const float* wp = &S.win[1][(ty.lo - r0) * kWF9];
           ia = (double)wi[xl] * tx.g + (double)wi[xh] * tx.f;
           pa = (double)wp[xl] * tx.g + (double)wp[xh] * tx.f;
         }
@@ -314,15 +344,15 @@ __global__ void __launch_bounds__(kTQ)
       if (ty.hi != yb) {
         if (ty.hi == ya) { ib = ia; pb = pa; }
         else {
-          const float* wi = &S.win[0][ty.hi - r0][0];
-          const float* wp = &S.win[1][ty.hi - r0][0];
+          const float* wi = &S.win[0][(ty.hi - r0) * kWF9];
+          const float* wp = &S.win[1][(ty.hi - r0) * kWF9];
           ib = (double)wi[xl] * tx.g + (double)wi[xh] * tx.f;
           pb = (double)wp[xl] * tx.g + (double)wp[xh] * tx.f;
         }
         yb = ty.hi;
       }
-      const float ui = (float)clip_hi1(ia * ty.g + ib * ty.f);
-      const float up = (float)clip_hi1(pa * ty.g + pb * ty.f);
+      const float ui = f32_clip_hi1(ia * ty.g + ib * ty.f);
+      const float up = f32_clip_hi1(pa * ty.g + pb * ty.f);
       const int rr = r - c0;
       if (kDirect) {
         float fv[kN];
@@ -332,7 +362,7 @@ __global__ void __launch_bounds__(kTQ)
           if (tp.lo != qa) {
             if (tp.lo == qb) qva = qvb;
             else {
-              const float* wq = &S.win[2][tp.lo - pr0][0];
+              const float* wq = &S.win[2][(tp.lo - pr0) * kWF9];
               qva = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
             }
             qa = tp.lo;
@@ -340,16 +370,16 @@ __global__ void __launch_bounds__(kTQ)
           if (tp.hi != qb) {
             if (tp.hi == qa) qvb = qva;
             else {
-              const float* wq = &S.win[2][tp.hi - pr0][0];
+              const float* wq = &S.win[2][(tp.hi - pr0) * kWF9];
               qvb = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
             }
             qb = tp.hi;
           }
-          const double dq = (double)(float)clip_hi1(qva * tp.g + qvb * tp.f);
-          f0 = (float)clip_hi1(a.alpha[0] * dq + a.beta[0] * (double)ui);
+          const double dq = (double)f32_clip_hi1(qva * tp.g + qvb * tp.f);
+          f0 = f32_clip_hi1(a.alpha[0] * dq + a.beta[0] * (double)ui);
           const double dp = (double)up;
 #pragma unroll
-          for (int f = 1; f < kN; ++f) fv[f] = (float)clip_hi1(a.alpha[f] * dq + a.beta[f] * dp);
+          for (int f = 1; f < kN; ++f) fv[f] = f32_clip_hi1(a.alpha[f] * dq + a.beta[f] * dp);
         }
         if (col_ok) {
           const int64_t fstride = (int64_t)a.H * a.W * 3;
@@ -367,7 +397,7 @@ __global__ void __launch_bounds__(kTQ)
         if (tp.lo != qa) {
           if (tp.lo == qb) qva = qvb;
           else {
-            const float* wq = &S.win[2][tp.lo - pr0][0];
+            const float* wq = &S.win[2][(tp.lo - pr0) * kWF9];
             qva = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
           }
           qa = tp.lo;
@@ -375,16 +405,16 @@ __global__ void __launch_bounds__(kTQ)
         if (tp.hi != qb) {
           if (tp.hi == qa) qvb = qva;
           else {
-            const float* wq = &S.win[2][tp.hi - pr0][0];
+            const float* wq = &S.win[2][(tp.hi - pr0) * kWF9];
             qvb = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
           }
           qb = tp.hi;
         }
-        const double dq = (double)(float)clip_hi1(qva * tp.g + qvb * tp.f);
-        tile[0][rr][tid] = (float)clip_hi1(a.alpha[0] * dq + a.beta[0] * (double)ui);
+        const double dq = (double)f32_clip_hi1(qva * tp.g + qvb * tp.f);
+        tile[0][rr][tid] = f32_clip_hi1(a.alpha[0] * dq + a.beta[0] * (double)ui);
         const double dp = (double)up;
 #pragma unroll
-        for (int f = 1; f < kN; ++f) tile[f][rr][tid] = (float)clip_hi1(a.alpha[f] * dq + a.beta[f] * dp);
+        for (int f = 1; f < kN; ++f) tile[f][rr][tid] = f32_clip_hi1(a.alpha[f] * dq + a.beta[f] * dp);
       } else {
         tile[0][rr][tid] = ui;
       }
@@ -414,11 +444,6 @@ __global__ void __launch_bounds__(kTQ)
 // [G*9][h][w*3] working frames, out-of-range rows / columns zero-filled) with
 // cp.async for the previous GoP's windows (their base pointers are per-GoP
 // table entries, so they have no single tensor map).
-// TMA box rows start on a 16-byte boundary: the window is loaded from
-// x = (first column & ~3), up to 3 floats before the first column it needs,
-// so the pitch covers kWF + 3 floats.
-constexpr int kWF9 = 144;                  // window pitch (floats), 16-byte multiple
-
 template <int kBand>
 struct Up9fGeom {
   static constexpr int kWR = kBand / 2 + 2;                      // max source rows (s >= 2)
@@ -434,12 +459,6 @@ struct Up9fSmem {
   int xs;                    // current window's column shift (TMA alignment), 0 for cp.async
   uint64_t bar;
 };
-
-// (float)clip_hi1(x) as one float min: float rounding is monotonic, so
-// x > 1 implies (float)x >= 1 and x <= 1 implies (float)x <= 1 -- the result
-// is bit-identical (including -0.0) and costs one FMNMX instead of a DSETP and
-// two FSELs on the 64-bit value.
-__device__ __forceinline__ float f32_clip_hi1(double x) { return fminf((float)x, 1.0f); }
 
 // Interpolate frames f0..f0+NF-1 from their windows with the row-cache
 // control shared, and stream the rows out.
@@ -721,23 +740,23 @@ __global__ void __launch_bounds__(kMseThreads)
 
 using namespace sst;
 
-template <int BAND, int NBUF, bool DIRECT = false>
-static int launch_k5(const CUtensorMap& omap, const UpArgs& a, const SstPrevDesc* prev,
-                     int blend_n, cudaStream_t st) {
+template <int BAND, int NBUF, bool DIRECT = false, bool TMAIN = false>
+static int launch_k5(const CUtensorMap& omap, const CUtensorMap& imap, const UpArgs& a,
+                     const SstPrevDesc* prev, int blend_n, cudaStream_t st) {
   dim3 grid(ceil_div(a.W * 3, kTQ), ceil_div(a.H, BAND), a.G);
   if (grid.y > 65535) return SST_ERR_ARG;
   const int smem = DIRECT ? tile_off<BAND>() : up_tma_smem<BAND, NBUF>((prev ? blend_n : 1) + 1);
-  auto kern = k_upscale_blend_tma<BAND, NBUF, false, 1, DIRECT>;
+  auto kern = k_upscale_blend_tma<BAND, NBUF, false, 1, DIRECT, TMAIN>;
   if (prev) {
     switch (blend_n) {
-      case 1: kern = k_upscale_blend_tma<BAND, NBUF, true, 1, DIRECT>; break;
-      case 2: kern = k_upscale_blend_tma<BAND, NBUF, true, 2, DIRECT>; break;
-      case 3: kern = k_upscale_blend_tma<BAND, NBUF, true, 3, DIRECT>; break;
-      default: kern = k_upscale_blend_tma<BAND, NBUF, true, 4, DIRECT>; break;
+      case 1: kern = k_upscale_blend_tma<BAND, NBUF, true, 1, DIRECT, TMAIN>; break;
+      case 2: kern = k_upscale_blend_tma<BAND, NBUF, true, 2, DIRECT, TMAIN>; break;
+      case 3: kern = k_upscale_blend_tma<BAND, NBUF, true, 3, DIRECT, TMAIN>; break;
+      default: kern = k_upscale_blend_tma<BAND, NBUF, true, 4, DIRECT, TMAIN>; break;
     }
   }
   SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  kern<<<grid, kTQ, smem, st>>>(omap, a);
+  kern<<<grid, kTQ, smem, st>>>(omap, imap, a);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }
@@ -775,12 +794,23 @@ extern "C" int sst_upscale_blend(const float* img, int G, int h, int w, int s, i
     const int band = (eb && atoi(eb) == 32) ? 32 : 16;
     const int nbuf = (en && atoi(en) == 2) ? 2 : 1;
     if (var && var[0] == 'd')                     // "direct": streaming stores, no TMA tiles
-      return band == 16 ? launch_k5<16, 1, true>(omap, a, prev, blend_n, st)
-                        : launch_k5<32, 1, true>(omap, a, prev, blend_n, st);
-    return band == 16 ? (nbuf == 1 ? launch_k5<16, 1>(omap, a, prev, blend_n, st)
-                                   : launch_k5<16, 2>(omap, a, prev, blend_n, st))
-                      : (nbuf == 1 ? launch_k5<32, 1>(omap, a, prev, blend_n, st)
-                                   : launch_k5<32, 2>(omap, a, prev, blend_n, st));
+      return band == 16 ? launch_k5<16, 1, true>(omap, omap, a, prev, blend_n, st)
+                        : launch_k5<32, 1, true>(omap, omap, a, prev, blend_n, st);
+    // I/P windows by TMA when img admits a tensor map ([G*2][h][w*3]; the
+    // register-staged loads otherwise, or with SST_K5_LOAD=sync).  Same time
+    // either way (1.17 ms per 32-GoP launch, scripts/k5_ab.sh): K5 is bound
+    // by its 7.2 GB of writes, the load phase is hidden by the other CTAs.
+    const char* el = getenv("SST_K5_LOAD");
+    CUtensorMap imap;
+    memset(&imap, 0, sizeof(imap));
+    if (band == 16 && nbuf == 1 && !(var && var[0] == 'd') && !(el && !strcmp(el, "sync")) &&
+        make_tmap_f32_3d(&imap, img, (uint64_t)w * 3, (uint64_t)h, (uint64_t)G * 2, kWF9,
+                         UpTmaSmem<16>::kWR))
+      return launch_k5<16, 1, false, true>(omap, imap, a, prev, blend_n, st);
+    return band == 16 ? (nbuf == 1 ? launch_k5<16, 1>(omap, imap, a, prev, blend_n, st)
+                                   : launch_k5<16, 2>(omap, imap, a, prev, blend_n, st))
+                      : (nbuf == 1 ? launch_k5<32, 1>(omap, imap, a, prev, blend_n, st)
+                                   : launch_k5<32, 2>(omap, imap, a, prev, blend_n, st));
   }
   dim3 grid(ceil_div(W * 3, kUpThreads), ceil_div(H, kUpRows), G);
   if (grid.y > 65535) return SST_ERR_ARG;
