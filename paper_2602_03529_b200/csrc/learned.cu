@@ -1451,6 +1451,320 @@ __global__ void __launch_bounds__(128)
   if (warp == 0) tc::tmem_dealloc(tmem, 256);
 }
 
+// ---- persistent, warp-specialised fused qkv + window attention ------------
+// The same math as k_lt_attn_fused (identical MMA order per output element,
+// so bit-identical results), restructured so the tensor core never waits on
+// the SIMT phases of one work item (= GoP, 8x8 window, 64-dim head):
+//   warp 0      TMA producer: per item 4 k-blocks of (2 token boxes of the
+//               window + the head's 3 x 64 W_qkv rows) through a 2-stage ring;
+//   warp 1      qkv GEMM issuer (runs up to two items ahead of the softmax);
+//   warp 10     S = Q K^T / O = P V issuer (separate thread: neither issue
+//               stream blocks the other);
+//   warps 2-5,  two epilogue groups of 128 threads (one TMEM lane = one query
+//   warps 6-9   row each); group b handles the items of parity b with its own
+//               TMEM half (256 columns: qkv 0..191, S 0..127, O 128..191) and
+//               its own operand tiles (Q, K, V^T; P over Q and K).
+// TMEM per group: qkv columns 0..191, S 0..127 (over q|k, once they are in
+// smem), O 192..255 -- so the projection of the group's next item only has
+// to wait until this item's scores are consumed (p_ready), not for its O.
+// Hand-offs are mbarriers: qkv_full / s_full / o_full (MMA commits),
+// ops_ready / p_ready (128 epilogue arrivals each).
+constexpr int AP_RING = 2 * AF_STAGE;                         // 80 KB
+constexpr int AP_OPS = 3 * 16384;                             // Q, K, V^T per group
+constexpr int AP_SMEM = AP_RING + 2 * AP_OPS + 256 + 1024;
+
+__global__ void __launch_bounds__(352, 1)
+    k_lt_attn_persist(const __grid_constant__ CUtensorMap tmH, const __grid_constant__ CUtensorMap tmW,
+                      const float* __restrict__ bqkv, int G, int Ht, int Wt, int D,
+                      __nv_bfloat16* __restrict__ out) {
+  extern __shared__ uint8_t smem_raw[];
+  // 1024-byte alignment by offset from smem_raw (keeps the shared address
+  // space visible to the compiler: st.shared, not generic stores)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* ops = smem + AP_RING;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ops + 2 * AP_OPS);
+  uint64_t* empty = full + 2;
+  uint64_t* qkv_full = empty + 2;     // [2] per group
+  uint64_t* ops_ready = qkv_full + 2;
+  uint64_t* s_full = ops_ready + 2;
+  uint64_t* p_ready = s_full + 2;
+  uint64_t* o_full = p_ready + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_full + 2);
+
+  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int wins_x = ceil_div(Wt, ATT_WIN);
+  const int wins = ceil_div(Ht, ATT_WIN) * wins_x;
+  const int heads = D / ATT_HD;
+  const int n_items = G * wins * heads;
+  // contiguous chunk of items per CTA (the 4 heads of a window back to back)
+  const int per = ceil_div(n_items, (int)gridDim.x);
+  const int it0 = blockIdx.x * per;
+  const int n_my = max(0, min(n_items, it0 + per) - it0);
+  const int ncb = D / BK;
+
+  if (t == 0) {
+    tc::prefetch_tmap(&tmH);
+    tc::prefetch_tmap(&tmW);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+      mbar_init(&qkv_full[i], 1);
+      mbar_init(&s_full[i], 1);
+      mbar_init(&o_full[i], 1);
+      mbar_init(&ops_ready[i], 128);
+      mbar_init(&p_ready[i], 128);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tmem_slot, 512);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  struct Item { int g, wy, wx, head; };
+  auto item_coords = [=](int it) {
+    Item c;
+    c.head = it % heads;
+    const int r = it / heads;
+    const int win = r % wins;
+    c.g = r / wins;
+    c.wy = win / wins_x;
+    c.wx = win - c.wy * wins_x;
+    return c;
+  };
+
+  if (warp == 0) {
+    // ---- TMA producer ----
+    if (lane == 0) {
+      int kb = 0;
+      for (int i = 0; i < n_my; ++i) {
+        const Item c = item_coords(it0 + i);
+        const int g = c.g, wy = c.wy, wx = c.wx, head = c.head;
+        for (int cb = 0; cb < ncb; ++cb, ++kb) {
+          const int s = kb & 1;
+          if (kb >= 2) mbar_wait(&empty[s], ((kb >> 1) - 1) & 1);
+          uint8_t* st = smem + s * AF_STAGE;
+          mbar_expect_tx(&full[s], AF_STAGE);
+          tc::tma_load_5d(st, &tmH, cb * BK, wx * ATT_WIN, wy * ATT_WIN, 0, g, &full[s]);
+          tc::tma_load_5d(st + 8192, &tmH, cb * BK, wx * ATT_WIN, wy * ATT_WIN, 1, g, &full[s]);
+          for (int part = 0; part < 3; ++part)
+            tc::tma_load_2d(st + 16384 + part * 8192, &tmW, cb * BK, part * D + head * ATT_HD,
+                            &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---- qkv projection issuer ----
+    if (lane == 0) {
+      constexpr uint32_t id0 = tc::idesc_bf16_f32(128, 192);
+      int kb = 0;
+      for (int i = 0; i < n_my; ++i) {
+        const int b = i & 1;
+        // TMEM columns 0..191 of group b are free once S(i-2) has been read
+        // (p_ready(i-2)); O(i-2) lives in columns 192..255
+        if (i >= 2) {
+          mbar_wait(&p_ready[b], ((i >> 1) - 1) & 1);
+          tc::fence_after_sync();
+        }
+        for (int cb = 0; cb < ncb; ++cb, ++kb) {
+          const int s = kb & 1;
+          mbar_wait(&full[s], (kb >> 1) & 1);
+          tc::fence_after_sync();
+          const uint64_t ad = tc::smem_desc_sw128(smem_u32(smem + s * AF_STAGE));
+          const uint64_t bd = tc::smem_desc_sw128(smem_u32(smem + s * AF_STAGE + 16384));
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            tc::mma_bf16(tmem + b * 256, ad + 2 * k, bd + 2 * k, id0, cb | k);
+          tc::mma_commit(&empty[s]);
+        }
+        tc::mma_commit(&qkv_full[b]);
+      }
+    }
+  } else if (warp == 10) {
+    // ---- S = Q K^T and O = P V issuer ----
+    if (lane == 0) {
+      for (int i = 0; i < n_my; ++i) {
+        const int b = i & 1, u = i >> 1;
+        uint8_t* o = ops + b * AP_OPS;
+        mbar_wait(&ops_ready[b], u & 1);
+        tc::fence_after_sync();
+        {
+          constexpr uint32_t id1 = tc::idesc_bf16_f32(128, 128);
+          const uint64_t ad = tc::smem_desc_sw128(smem_u32(o));
+          const uint64_t bd = tc::smem_desc_sw128(smem_u32(o + 16384));
+#pragma unroll
+          for (int k = 0; k < 4; ++k) tc::mma_bf16(tmem + b * 256, ad + 2 * k, bd + 2 * k, id1, k);
+          tc::mma_commit(&s_full[b]);
+        }
+        mbar_wait(&p_ready[b], u & 1);
+        tc::fence_after_sync();
+        {
+          constexpr uint32_t id2 = tc::idesc_bf16_f32(128, 64);
+#pragma unroll
+          for (int kbk = 0; kbk < 2; ++kbk) {
+            const uint64_t ad = tc::smem_desc_sw128(smem_u32(o + kbk * 16384));
+            const uint64_t bd = tc::smem_desc_sw128(smem_u32(o + 32768 + kbk * 8192));
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              tc::mma_bf16(tmem + b * 256 + 192, ad + 2 * k, bd + 2 * k, id2, kbk | k);
+          }
+          tc::mma_commit(&o_full[b]);
+        }
+      }
+    }
+  } else {
+    // ---- epilogue groups ----
+    const int grp = (warp - 2) >> 2;
+    const int q = ((warp & 3) << 5) | lane;          // TMEM lane = query / token row
+    const int ft = q >> 6, lt = q & 63;
+    uint8_t* o = ops + grp * AP_OPS;
+    uint8_t* sQ = o;
+    uint8_t* sK = o + 16384;
+    uint8_t* sV = o + 32768;
+    const uint32_t tb = tmem + grp * 256 + ((uint32_t)((warp & 3) * 32) << 16);
+    for (int i = grp; i < n_my; i += 2) {
+      const int u = i >> 1;
+      const Item c = item_coords(it0 + i);
+      const int g = c.g, wy = c.wy, wx = c.wx, head = c.head;
+      const int y = wy * ATT_WIN + (lt >> 3), x = wx * ATT_WIN + (lt & 7);
+      const bool valid = y < Ht && x < Wt;
+      // -- qkv: +bias, bf16; Q and K rows into their tiles, V transposed --
+      mbar_wait(&qkv_full[grp], u & 1);
+      tc::fence_after_sync();
+#pragma unroll 1
+      for (int c = 0; c < 6; ++c) {
+        float v[32];
+        tc::tmem_ld32(tb + c * 32, v);
+        const int part = c >> 1;
+        const int d0 = (c & 1) * 32;
+        const float4* bp = reinterpret_cast<const float4*>(bqkv + part * D + head * ATT_HD + d0);
+#pragma unroll
+        for (int e4 = 0; e4 < 8; ++e4) {
+          const float4 bb = __ldg(bp + e4);
+          v[4 * e4 + 0] = valid ? v[4 * e4 + 0] + bb.x : 0.0f;
+          v[4 * e4 + 1] = valid ? v[4 * e4 + 1] + bb.y : 0.0f;
+          v[4 * e4 + 2] = valid ? v[4 * e4 + 2] + bb.z : 0.0f;
+          v[4 * e4 + 3] = valid ? v[4 * e4 + 3] + bb.w : 0.0f;
+        }
+        if (part < 2) {
+          uint8_t* base = part == 0 ? sQ : sK;
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            uint4 w4;
+            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w4);
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              h2[e] = __floats2bfloat162_rn(v[qq * 8 + 2 * e], v[qq * 8 + 2 * e + 1]);
+            const int j = (d0 >> 3) + qq;
+            *reinterpret_cast<uint4*>(base + q * 128 + ((j ^ (q & 7)) << 4)) = w4;
+          }
+        } else {
+          const int kbk = q >> 6, kk = q & 63;
+          uint8_t* vb = sV + kbk * 8192 + (kk & 7) * 2;
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const int d = d0 + e;
+            *reinterpret_cast<__nv_bfloat16*>(vb + d * 128 + (((kk >> 3) ^ (d & 7)) << 4)) =
+                __float2bfloat16_rn(v[e]);
+          }
+        }
+      }
+      fence_proxy_async_smem();
+      tc::fence_before_sync();
+      tc::mbar_arrive(&ops_ready[grp]);
+      // -- softmax of this query row --
+      mbar_wait(&s_full[grp], u & 1);
+      tc::fence_after_sync();
+      // two passes over the scores in TMEM (32 columns at a time, so the
+      // 128 scores never sit in registers): row max, then exp / sum / P.
+      // Keys of the later frame are skipped for frame-0 queries; the sum
+      // order is k = 0..127 as in k_lt_attn_fused (skipped terms are +0).
+      const int nk = (ft + 1) * 64;
+      const int nch = nk >> 5;
+      const uint32_t vrow = (1u << min(8, Ht - wy * ATT_WIN)) - 1u;
+      const uint32_t vcol = (1u << min(8, Wt - wx * ATT_WIN)) - 1u;
+      const bool interior = vrow == 0xffu && vcol == 0xffu;
+      float m = -INFINITY;
+#pragma unroll 1
+      for (int c = 0; c < nch; ++c) {
+        float v[32];
+        tc::tmem_ld32(tb + c * 32, v);
+        if (interior) {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) m = fmaxf(m, v[e]);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const int kl = (c * 32 + e) & 63;
+            if ((vrow >> (kl >> 3)) & (vcol >> (kl & 7)) & 1u) m = fmaxf(m, v[e]);
+          }
+        }
+      }
+      float l = 0.0f;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        float v[32];
+        if (c < nch) {
+          tc::tmem_ld32(tb + c * 32, v);
+#pragma unroll
+          for (int e = 0; e < 32; ++e) {
+            const int kl = (c * 32 + e) & 63;
+            const bool ok = interior || ((vrow >> (kl >> 3)) & (vcol >> (kl & 7)) & 1u);
+            v[e] = ok ? __expf((v[e] - m) * 0.125f) : 0.0f;
+            l += v[e];
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 32; ++e) v[e] = 0.0f;
+        }
+        // P over Q and K (the S GEMM that read them has completed: s_full)
+        uint8_t* pb = o + (c >> 1) * 16384 + q * 128;
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) {
+          uint4 w4;
+          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w4);
+#pragma unroll
+          for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[8 * jj + 2 * e], v[8 * jj + 2 * e + 1]);
+          const int jc = (c & 1) * 4 + jj;
+          *reinterpret_cast<uint4*>(pb + ((jc ^ (q & 7)) << 4)) = w4;
+        }
+      }
+      fence_proxy_async_smem();
+      tc::fence_before_sync();
+      tc::mbar_arrive(&p_ready[grp]);
+      // -- O / l --
+      mbar_wait(&o_full[grp], u & 1);
+      tc::fence_after_sync();
+      float ov[64];
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float v[32];
+        tc::tmem_ld32(tb + 192 + c * 32, v);
+#pragma unroll
+        for (int e = 0; e < 32; ++e) ov[c * 32 + e] = v[e];
+      }
+      if (valid) {
+        const size_t tok = (((size_t)g * 2 + ft) * Ht + y) * Wt + x;
+        const float inv = 1.0f / l;
+        uint4* op = reinterpret_cast<uint4*>(out + tok * D + head * ATT_HD);
+#pragma unroll
+        for (int j = 0; j < ATT_HD / 8; ++j) {
+          uint4 w4;
+          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w4);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            h2[e] = __floats2bfloat162_rn(ov[8 * j + 2 * e] * inv, ov[8 * j + 2 * e + 1] * inv);
+          op[j] = w4;
+        }
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 512);
+}
+
 // ---- downscale + pad + patchify --------------------------------------------
 template <int S>
 __global__ void k_lt_patchify(const float* __restrict__ src, int G, int H, int W, int h, int w,
@@ -1878,8 +2192,29 @@ extern "C" int sst_lt_attn_fused(const void* h, const void* w_qkv, const float* 
   const uint64_t hdims[5] = {(uint64_t)D, (uint64_t)Wt, (uint64_t)Ht, 2, (uint64_t)G};
   if (!make_tmap_bf16_5d(&tmH, h, hdims, lt::ATT_WIN, lt::ATT_WIN)) return SST_ERR_ARG;
   if (!make_tmap_bf16_2d(&tmW, w_qkv, (uint64_t)D, (uint64_t)(3 * D), lt::ATT_HD)) return SST_ERR_ARG;
-  dim3 grid((unsigned)wins, D / lt::ATT_HD, G);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // default: one CTA per (GoP, window, head), two CTAs per SM.
+  // SST_LT_ATTN=persistent: the warp-specialised persistent kernel --
+  // bit-identical, but measured slower at the learned leg's shape (32 x 1080p
+  // GoPs, D=256: 0.48 vs 0.41 ms, scripts/attn_micro.py): both are bound by
+  // the SIMT epilogue (bias, V transpose, softmax) with 8 epilogue warps per
+  // SM, and the persistent kernel's hand-offs add latency to that chain.
+  const char* ea = getenv("SST_LT_ATTN");
+  if (ea && !strcmp(ea, "persistent")) {
+    const int64_t items = wins * (D / lt::ATT_HD) * (int64_t)G;
+    if (items > 0x7fffffff) return SST_ERR_ARG;
+    int dev = 0, sms = 148;
+    SST_CUDA_TRY(cudaGetDevice(&dev));
+    SST_CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    const int grid = (int)(items < sms ? items : sms);
+    SST_CUDA_TRY(cudaFuncSetAttribute(lt::k_lt_attn_persist,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, lt::AP_SMEM));
+    lt::k_lt_attn_persist<<<grid, 352, lt::AP_SMEM, st>>>(tmH, tmW, b_qkv, G, Ht, Wt, D,
+                                                          static_cast<__nv_bfloat16*>(out));
+    SST_LAUNCH_CHECK();
+    return SST_OK;
+  }
+  dim3 grid((unsigned)wins, D / lt::ATT_HD, G);
   SST_CUDA_TRY(cudaFuncSetAttribute(lt::k_lt_attn_fused, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     lt::AF_SMEM));
   lt::k_lt_attn_fused<<<grid, 128, lt::AF_SMEM, st>>>(tmH, tmW, b_qkv, G, Ht, Wt, D,

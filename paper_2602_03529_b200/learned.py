@@ -194,15 +194,17 @@ class LearnedTokenizer:
 
     def _attention(self, part, h, G, Ht, Wt):
         """h += proj(WindowAttention(qkv(h))): the qkv projection and the
-        8x8-window causal attention run in one tcgen05 kernel per (window,
-        head) (sst_lt_attn_fused; SST_LT_ATTN=unfused: a 1x1 GEMM writing qkv,
-        then sst_lt_attn), proj is a tcgen05 1x1 GEMM with the residual add."""
+        8x8-window causal attention run in one tcgen05 kernel, one CTA per
+        (window, head) (sst_lt_attn_fused; SST_LT_ATTN=persistent: the
+        warp-specialised persistent variant; SST_LT_ATTN=unfused: a 1x1 GEMM
+        writing qkv, then sst_lt_attn), proj is a tcgen05 1x1 GEMM with the
+        residual add."""
         if not self.cfg.attn:
             return
         D = self.cfg.dim
         shape = (G, 2, Ht, Wt, D)
         o = torch.empty_like(h)
-        if os.environ.get("SST_LT_ATTN", "fused") == "fused":
+        if os.environ.get("SST_LT_ATTN") != "unfused":
             # qkv projection inside the attention kernel (no qkv tensor)
             _lib.call("sst_lt_attn_fused", h.data_ptr(), self.W[f"{part}_qkv"].data_ptr(),
                       self.b[f"{part}_qkv"].data_ptr(), G, Ht, Wt, D, o.data_ptr(), _dev.stream())

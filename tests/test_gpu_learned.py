@@ -165,6 +165,34 @@ def test_fused_qkv_attention(H, W, D):
     _assert_bf16_close(out.float().cpu(), want, min_exact=0.9, atol=4e-3)
 
 
+@pytest.mark.parametrize("H,W,D,G", [(8, 8, 128, 1), (13, 21, 256, 3), (45, 80, 256, 4),
+                                     (3, 5, 64, 1)])
+def test_persistent_attention_equals_one_cta_per_item(H, W, D, G, monkeypatch):
+    """The persistent warp-specialised attention kernel (SST_LT_ATTN=persistent)
+    and the one-CTA-per-(window, head) kernel (default) issue the same MMAs
+    in the same order: bit-identical outputs, including item counts that do
+    not divide the grid and fewer items than SMs."""
+    rng = np.random.default_rng(14 + D + G)
+    h = _bf(rng.standard_normal((G, 2, H, W, D)) * 0.5)
+    Wq = _bf(rng.standard_normal((3 * D, D)) / np.sqrt(D)).numpy()
+    bq = _bf(rng.standard_normal(3 * D) * 0.1).numpy()
+    dev = _dev.device()
+    hd = h.to(dev, torch.bfloat16).contiguous()
+    wd = torch.from_numpy(Wq).to(dev, torch.bfloat16).contiguous()
+    bd = torch.from_numpy(bq).to(dev)
+    outs = []
+    for mode in ("fused", "persistent"):
+        monkeypatch.setenv("SST_LT_ATTN", mode)
+        out = torch.full((G, 2, H, W, D), 7.0, dtype=torch.bfloat16, device=dev)
+        _lib.call("sst_lt_attn_fused", hd.data_ptr(), wd.data_ptr(), bd.data_ptr(), G, H, W, D,
+                  out.data_ptr(), _dev.stream())
+        torch.cuda.synchronize()
+        outs.append(out)
+    assert torch.equal(outs[0], outs[1])
+    want = LO.window_attention(LO.bf(LO.linear(h, Wq, bq)))
+    _assert_bf16_close(outs[1].float().cpu(), want, min_exact=0.9, atol=4e-3)
+
+
 def test_conv_causal_first_frame_sees_no_past():
     # t=0 output must not depend on t=1 input (causal temporal kernel)
     rng = np.random.default_rng(2)
