@@ -1243,6 +1243,144 @@ __global__ void __launch_bounds__(128)
   if (warp == 0) tc::tmem_dealloc(tmem, 128);
 }
 
+// ---- attention epilogue helpers (k_lt_attn_fused, k_lt_attn_persist) -----
+// Thread = TMEM lane = token row q of the window (q = frame * 64 + 8y + x).
+
+// qkv accumulator row (192 TMEM columns at tq) + bias -> bf16 Q and K rows
+// into their 128B-swizzled K-major tiles, V transposed into V^T's tile.
+__device__ __forceinline__ void att_qkv_epilogue(uint32_t tq, const float* __restrict__ bqkv, int D,
+                                                 int head, bool valid, int q, uint8_t* sQ,
+                                                 uint8_t* sK, uint8_t* sV) {
+#pragma unroll 1
+  for (int c = 0; c < 6; ++c) {
+    float v[32];
+    tc::tmem_ld32(tq + c * 32, v);
+    const int part = c >> 1;                       // 0 q, 1 k, 2 v
+    const int d0 = (c & 1) * 32;
+    const float4* bp = reinterpret_cast<const float4*>(bqkv + part * D + head * ATT_HD + d0);
+#pragma unroll
+    for (int e4 = 0; e4 < 8; ++e4) {
+      const float4 bb = __ldg(bp + e4);
+      v[4 * e4 + 0] += bb.x;
+      v[4 * e4 + 1] += bb.y;
+      v[4 * e4 + 2] += bb.z;
+      v[4 * e4 + 3] += bb.w;
+    }
+    if (!valid) {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) v[e] = 0.0f;
+    }
+    if (part < 2) {
+      uint8_t* base = part == 0 ? sQ : sK;
+#pragma unroll
+      for (int qq = 0; qq < 4; ++qq) {
+        uint4 w4;
+        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w4);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[qq * 8 + 2 * e], v[qq * 8 + 2 * e + 1]);
+        const int j = (d0 >> 3) + qq;
+        *reinterpret_cast<uint4*>(base + q * 128 + ((j ^ (q & 7)) << 4)) = w4;
+      }
+    } else {
+      const int kbk = q >> 6, kk = q & 63;
+      uint8_t* vb = sV + kbk * 8192 + (kk & 7) * 2;
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const int d = d0 + e;
+        *reinterpret_cast<__nv_bfloat16*>(vb + d * 128 + (((kk >> 3) ^ (d & 7)) << 4)) =
+            __float2bfloat16_rn(v[e]);
+      }
+    }
+  }
+}
+
+// Causal window softmax of query row q from its 128 scores in TMEM (tS), two
+// passes of 32 columns (row max; then exp, sum, bf16 P into the two
+// 128B-swizzled K-major tiles at sP).  Key k is valid when k < 64 * (frame
+// of q + 1) and its (y, x) is inside the frame (vrow / vcol: the window's
+// valid rows / columns as bit masks).  p = 2^((s - m) * log2(e) / 8) with
+// one FFMA + ex2.approx; keys of the later frame are skipped for frame-0
+// queries (the sum order stays k = 0..127: skipped terms are +0).
+// Returns the row sum l.
+__device__ __forceinline__ float att_softmax_p(uint32_t tS, uint8_t* sP, int q, uint32_t vrow,
+                                               uint32_t vcol) {
+  constexpr float kC = 0.125f * 1.4426950408889634f;
+  const int nch = ((q >> 6) + 1) * 2;              // 32-key chunks in the causal range
+  const bool interior = vrow == 0xffu && vcol == 0xffu;
+  float m = -INFINITY;
+#pragma unroll 1
+  for (int c = 0; c < nch; ++c) {
+    float v[32];
+    tc::tmem_ld32(tS + c * 32, v);
+    if (interior) {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) m = fmaxf(m, v[e]);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const int kl = (c * 32 + e) & 63;
+        if ((vrow >> (kl >> 3)) & (vcol >> (kl & 7)) & 1u) m = fmaxf(m, v[e]);
+      }
+    }
+  }
+  const float mc = m * kC;
+  float l = 0.0f;
+#pragma unroll 1
+  for (int c = 0; c < 4; ++c) {
+    float v[32];
+    if (c < nch) {
+      tc::tmem_ld32(tS + c * 32, v);
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const int kl = (c * 32 + e) & 63;
+        const bool ok = interior || ((vrow >> (kl >> 3)) & (vcol >> (kl & 7)) & 1u);
+        float y;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(fmaf(v[e], kC, -mc)));
+        v[e] = ok ? y : 0.0f;
+        l += v[e];
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 32; ++e) v[e] = 0.0f;
+    }
+    uint8_t* pb = sP + (c >> 1) * 16384 + q * 128;
+#pragma unroll
+    for (int jj = 0; jj < 4; ++jj) {
+      uint4 w4;
+      __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w4);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[8 * jj + 2 * e], v[8 * jj + 2 * e + 1]);
+      const int jc = (c & 1) * 4 + jj;
+      *reinterpret_cast<uint4*>(pb + ((jc ^ (q & 7)) << 4)) = w4;
+    }
+  }
+  return l;
+}
+
+// O row (64 TMEM columns at tO) / l -> bf16 output row.  Called by every
+// thread of the warp (tcgen05.ld is warp-collective); only valid rows store.
+__device__ __forceinline__ void att_store_o(uint32_t tO, float l, bool valid, __nv_bfloat16* orow) {
+  float ov[64];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    float v[32];
+    tc::tmem_ld32(tO + c * 32, v);
+#pragma unroll
+    for (int e = 0; e < 32; ++e) ov[c * 32 + e] = v[e];
+  }
+  if (!valid) return;
+  const float inv = 1.0f / l;
+  uint4* op = reinterpret_cast<uint4*>(orow);
+#pragma unroll
+  for (int j = 0; j < ATT_HD / 8; ++j) {
+    uint4 w4;
+    __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w4);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(ov[8 * j + 2 * e] * inv, ov[8 * j + 2 * e + 1] * inv);
+    op[j] = w4;
+  }
+}
+
 // ---- fused qkv projection + causal window attention (tcgen05) -------------
 // One CTA = (GoP, 8x8 window, 64-dim head).  The qkv projection of the
 // window's 128 tokens for this head is a third tcgen05 GEMM inside the CTA:
@@ -1260,8 +1398,7 @@ __global__ void __launch_bounds__(128)
                     const float* __restrict__ bqkv, int G, int Ht, int Wt, int D,
                     __nv_bfloat16* __restrict__ out) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* sQ = smem;                 // after the projection: [128 q][64 d]
   uint8_t* sK = smem + 16384;         // [128 k][64 d]
   uint8_t* sP = smem;                 // [2 kb][128 q][64 k]
@@ -1270,7 +1407,6 @@ __global__ void __launch_bounds__(128)
   uint64_t* empty = full + 2;
   uint64_t* bar = empty + 2;          // [0] qkv, [1] S, [2] O
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 3);
-  int* kval = reinterpret_cast<int*>(smem + 2 * AF_STAGE + 128);
 
   const int wins_x = ceil_div(Wt, ATT_WIN);
   const int wy = blockIdx.x / wins_x, wx = blockIdx.x - wy * wins_x;
@@ -1290,7 +1426,6 @@ __global__ void __launch_bounds__(128)
     fence_mbar_init();
   }
   if (warp == 0) tc::tmem_alloc(tmem_slot, 256);
-  kval[t] = valid;
   tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
@@ -1329,37 +1464,7 @@ __global__ void __launch_bounds__(128)
 
   // ---- +bias, bf16: Q and K rows into their tiles, V transposed ----
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-#pragma unroll 1
-  for (int c = 0; c < 6; ++c) {
-    float v[32];
-    tc::tmem_ld32(trow + c * 32, v);
-    const int part = c >> 1;                       // 0 q, 1 k, 2 v
-    const int d0 = (c & 1) * 32;
-    const float* bp = bqkv + part * D + head * ATT_HD + d0;
-#pragma unroll
-    for (int i = 0; i < 32; ++i) v[i] = valid ? v[i] + __ldg(bp + i) : 0.0f;
-    if (part < 2) {
-      uint8_t* base = part == 0 ? sQ : sK;
-#pragma unroll
-      for (int qq = 0; qq < 4; ++qq) {
-        uint4 u;
-        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-        for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[qq * 8 + 2 * e], v[qq * 8 + 2 * e + 1]);
-        const int j = (d0 >> 3) + qq;
-        *reinterpret_cast<uint4*>(base + t * 128 + ((j ^ (t & 7)) << 4)) = u;
-      }
-    } else {
-      const int kb = t >> 6, kk = t & 63;
-      uint8_t* vb = sV + kb * 8192 + (kk & 7) * 2;
-#pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int d = d0 + i;
-        *reinterpret_cast<__nv_bfloat16*>(vb + d * 128 + (((kk >> 3) ^ (d & 7)) << 4)) =
-            __float2bfloat16_rn(v[i]);
-      }
-    }
-  }
+  att_qkv_epilogue(trow, bqkv, D, head, valid, t, sQ, sK, sV);
   fence_proxy_async_smem();
   tc::fence_before_sync();
   __syncthreads();
@@ -1375,41 +1480,14 @@ __global__ void __launch_bounds__(128)
   }
   mbar_wait(&bar[1], 0);
   tc::fence_after_sync();
-  float sc[128];
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    float v[32];
-    tc::tmem_ld32(trow + c * 32, v);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) sc[c * 32 + i] = v[i];
-  }
-  const int nk = (ft + 1) * 64;
-  float m = -INFINITY;
-#pragma unroll
-  for (int k = 0; k < 128; ++k)
-    if (k < nk && kval[k]) m = fmaxf(m, sc[k]);
-  float l = 0.0f;
-#pragma unroll
-  for (int k = 0; k < 128; ++k) {
-    const float p = (k < nk && kval[k]) ? __expf((sc[k] - m) * 0.125f) : 0.0f;
-    sc[k] = p;
-    l += p;
-  }
-  tc::fence_before_sync();
-  __syncthreads();
-#pragma unroll
-  for (int kb = 0; kb < 2; ++kb) {
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      uint4 u;
-      __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        h2[e] = __floats2bfloat162_rn(sc[kb * 64 + 8 * j + 2 * e], sc[kb * 64 + 8 * j + 2 * e + 1]);
-      *reinterpret_cast<uint4*>(sP + kb * 16384 + t * 128 + ((j ^ (t & 7)) << 4)) = u;
-    }
-  }
+  const uint32_t vrow = (1u << min(8, Ht - wy * ATT_WIN)) - 1u;
+  const uint32_t vcol = (1u << min(8, Wt - wx * ATT_WIN)) - 1u;
+  // P overwrites Q and K: every thread's S reads and GEMM 1 (s barrier) are
+  // done before any P store -- the S GEMM completed (bar[1]) and P rows are
+  // per-thread, while S lives in TMEM
+  const float l = att_softmax_p(trow, sP, t, vrow, vcol);
   fence_proxy_async_smem();
+  tc::fence_before_sync();
   __syncthreads();
   tc::fence_after_sync();
   if (t == 0) {
@@ -1425,27 +1503,7 @@ __global__ void __launch_bounds__(128)
   }
   mbar_wait(&bar[2], 0);
   tc::fence_after_sync();
-  float o[64];
-#pragma unroll
-  for (int c = 0; c < 2; ++c) {
-    float v[32];
-    tc::tmem_ld32(trow + c * 32, v);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) o[c * 32 + i] = v[i];
-  }
-  if (valid) {
-    const float inv = 1.0f / l;
-    uint4* op = reinterpret_cast<uint4*>(out + tok * D + head * ATT_HD);
-#pragma unroll
-    for (int i = 0; i < ATT_HD / 8; ++i) {
-      uint4 u;
-      __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-      for (int e = 0; e < 4; ++e)
-        h2[e] = __floats2bfloat162_rn(o[8 * i + 2 * e] * inv, o[8 * i + 2 * e + 1] * inv);
-      op[i] = u;
-    }
-  }
+  att_store_o(trow, l, valid, out + tok * D + head * ATT_HD);
   tc::fence_before_sync();
   __syncthreads();
   if (warp == 0) tc::tmem_dealloc(tmem, 256);
@@ -1632,132 +1690,25 @@ __global__ void __launch_bounds__(352, 1)
       // -- qkv: +bias, bf16; Q and K rows into their tiles, V transposed --
       mbar_wait(&qkv_full[grp], u & 1);
       tc::fence_after_sync();
-#pragma unroll 1
-      for (int c = 0; c < 6; ++c) {
-        float v[32];
-        tc::tmem_ld32(tb + c * 32, v);
-        const int part = c >> 1;
-        const int d0 = (c & 1) * 32;
-        const float4* bp = reinterpret_cast<const float4*>(bqkv + part * D + head * ATT_HD + d0);
-#pragma unroll
-        for (int e4 = 0; e4 < 8; ++e4) {
-          const float4 bb = __ldg(bp + e4);
-          v[4 * e4 + 0] = valid ? v[4 * e4 + 0] + bb.x : 0.0f;
-          v[4 * e4 + 1] = valid ? v[4 * e4 + 1] + bb.y : 0.0f;
-          v[4 * e4 + 2] = valid ? v[4 * e4 + 2] + bb.z : 0.0f;
-          v[4 * e4 + 3] = valid ? v[4 * e4 + 3] + bb.w : 0.0f;
-        }
-        if (part < 2) {
-          uint8_t* base = part == 0 ? sQ : sK;
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq) {
-            uint4 w4;
-            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w4);
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              h2[e] = __floats2bfloat162_rn(v[qq * 8 + 2 * e], v[qq * 8 + 2 * e + 1]);
-            const int j = (d0 >> 3) + qq;
-            *reinterpret_cast<uint4*>(base + q * 128 + ((j ^ (q & 7)) << 4)) = w4;
-          }
-        } else {
-          const int kbk = q >> 6, kk = q & 63;
-          uint8_t* vb = sV + kbk * 8192 + (kk & 7) * 2;
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const int d = d0 + e;
-            *reinterpret_cast<__nv_bfloat16*>(vb + d * 128 + (((kk >> 3) ^ (d & 7)) << 4)) =
-                __float2bfloat16_rn(v[e]);
-          }
-        }
-      }
+      att_qkv_epilogue(tb, bqkv, D, head, valid, q, sQ, sK, sV);
       fence_proxy_async_smem();
       tc::fence_before_sync();
       tc::mbar_arrive(&ops_ready[grp]);
       // -- softmax of this query row --
       mbar_wait(&s_full[grp], u & 1);
       tc::fence_after_sync();
-      // two passes over the scores in TMEM (32 columns at a time, so the
-      // 128 scores never sit in registers): row max, then exp / sum / P.
-      // Keys of the later frame are skipped for frame-0 queries; the sum
-      // order is k = 0..127 as in k_lt_attn_fused (skipped terms are +0).
-      const int nk = (ft + 1) * 64;
-      const int nch = nk >> 5;
       const uint32_t vrow = (1u << min(8, Ht - wy * ATT_WIN)) - 1u;
       const uint32_t vcol = (1u << min(8, Wt - wx * ATT_WIN)) - 1u;
-      const bool interior = vrow == 0xffu && vcol == 0xffu;
-      float m = -INFINITY;
-#pragma unroll 1
-      for (int c = 0; c < nch; ++c) {
-        float v[32];
-        tc::tmem_ld32(tb + c * 32, v);
-        if (interior) {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) m = fmaxf(m, v[e]);
-        } else {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const int kl = (c * 32 + e) & 63;
-            if ((vrow >> (kl >> 3)) & (vcol >> (kl & 7)) & 1u) m = fmaxf(m, v[e]);
-          }
-        }
-      }
-      float l = 0.0f;
-#pragma unroll 1
-      for (int c = 0; c < 4; ++c) {
-        float v[32];
-        if (c < nch) {
-          tc::tmem_ld32(tb + c * 32, v);
-#pragma unroll
-          for (int e = 0; e < 32; ++e) {
-            const int kl = (c * 32 + e) & 63;
-            const bool ok = interior || ((vrow >> (kl >> 3)) & (vcol >> (kl & 7)) & 1u);
-            v[e] = ok ? __expf((v[e] - m) * 0.125f) : 0.0f;
-            l += v[e];
-          }
-        } else {
-#pragma unroll
-          for (int e = 0; e < 32; ++e) v[e] = 0.0f;
-        }
-        // P over Q and K (the S GEMM that read them has completed: s_full)
-        uint8_t* pb = o + (c >> 1) * 16384 + q * 128;
-#pragma unroll
-        for (int jj = 0; jj < 4; ++jj) {
-          uint4 w4;
-          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w4);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[8 * jj + 2 * e], v[8 * jj + 2 * e + 1]);
-          const int jc = (c & 1) * 4 + jj;
-          *reinterpret_cast<uint4*>(pb + ((jc ^ (q & 7)) << 4)) = w4;
-        }
-      }
+      // P over Q and K (the S GEMM that read them has completed: s_full)
+      const float l = att_softmax_p(tb, o, q, vrow, vcol);
       fence_proxy_async_smem();
       tc::fence_before_sync();
       tc::mbar_arrive(&p_ready[grp]);
       // -- O / l --
       mbar_wait(&o_full[grp], u & 1);
       tc::fence_after_sync();
-      float ov[64];
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        float v[32];
-        tc::tmem_ld32(tb + 192 + c * 32, v);
-#pragma unroll
-        for (int e = 0; e < 32; ++e) ov[c * 32 + e] = v[e];
-      }
-      if (valid) {
-        const size_t tok = (((size_t)g * 2 + ft) * Ht + y) * Wt + x;
-        const float inv = 1.0f / l;
-        uint4* op = reinterpret_cast<uint4*>(out + tok * D + head * ATT_HD);
-#pragma unroll
-        for (int j = 0; j < ATT_HD / 8; ++j) {
-          uint4 w4;
-          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w4);
-#pragma unroll
-          for (int e = 0; e < 4; ++e)
-            h2[e] = __floats2bfloat162_rn(ov[8 * j + 2 * e] * inv, ov[8 * j + 2 * e + 1] * inv);
-          op[j] = w4;
-        }
-      }
+      const size_t tok = (((size_t)g * 2 + ft) * Ht + y) * Wt + x;
+      att_store_o(tb + 192, l, valid, out + tok * D + head * ATT_HD);
     }
   }
   tc::fence_before_sync();
@@ -2193,14 +2144,13 @@ extern "C" int sst_lt_attn_fused(const void* h, const void* w_qkv, const float* 
   if (!make_tmap_bf16_5d(&tmH, h, hdims, lt::ATT_WIN, lt::ATT_WIN)) return SST_ERR_ARG;
   if (!make_tmap_bf16_2d(&tmW, w_qkv, (uint64_t)D, (uint64_t)(3 * D), lt::ATT_HD)) return SST_ERR_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  // default: one CTA per (GoP, window, head), two CTAs per SM.
-  // SST_LT_ATTN=persistent: the warp-specialised persistent kernel --
-  // bit-identical, but measured slower at the learned leg's shape (32 x 1080p
-  // GoPs, D=256: 0.48 vs 0.41 ms, scripts/attn_micro.py): both are bound by
-  // the SIMT epilogue (bias, V transpose, softmax) with 8 epilogue warps per
-  // SM, and the persistent kernel's hand-offs add latency to that chain.
+  // default: the persistent warp-specialised kernel (0.221 ms at the learned
+  // leg's shape, 32 x 1080p GoPs, D=256; scripts/attn_micro.py).
+  // SST_LT_ATTN=fused: one CTA per (GoP, window, head), two CTAs per SM
+  // (0.264 ms) -- bit-identical.  Both are bound by the SIMT epilogue; the
+  // persistent kernel overlaps it with the next item's qkv GEMM.
   const char* ea = getenv("SST_LT_ATTN");
-  if (ea && !strcmp(ea, "persistent")) {
+  if (!(ea && !strcmp(ea, "fused"))) {
     const int64_t items = wins * (D / lt::ATT_HD) * (int64_t)G;
     if (items > 0x7fffffff) return SST_ERR_ARG;
     int dev = 0, sms = 148;

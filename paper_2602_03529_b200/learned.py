@@ -194,11 +194,10 @@ class LearnedTokenizer:
 
     def _attention(self, part, h, G, Ht, Wt):
         """h += proj(WindowAttention(qkv(h))): the qkv projection and the
-        8x8-window causal attention run in one tcgen05 kernel, one CTA per
-        (window, head) (sst_lt_attn_fused; SST_LT_ATTN=persistent: the
-        warp-specialised persistent variant; SST_LT_ATTN=unfused: a 1x1 GEMM
-        writing qkv, then sst_lt_attn), proj is a tcgen05 1x1 GEMM with the
-        residual add."""
+        8x8-window causal attention run in one persistent, warp-specialised
+        tcgen05 kernel (sst_lt_attn_fused; SST_LT_ATTN=fused: one CTA per
+        (window, head); SST_LT_ATTN=unfused: a 1x1 GEMM writing qkv, then
+        sst_lt_attn), proj is a tcgen05 1x1 GEMM with the residual add."""
         if not self.cfg.attn:
             return
         D = self.cfg.dim

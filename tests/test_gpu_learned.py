@@ -168,8 +168,8 @@ def test_fused_qkv_attention(H, W, D):
 @pytest.mark.parametrize("H,W,D,G", [(8, 8, 128, 1), (13, 21, 256, 3), (45, 80, 256, 4),
                                      (3, 5, 64, 1)])
 def test_persistent_attention_equals_one_cta_per_item(H, W, D, G, monkeypatch):
-    """The persistent warp-specialised attention kernel (SST_LT_ATTN=persistent)
-    and the one-CTA-per-(window, head) kernel (default) issue the same MMAs
+    """The persistent warp-specialised attention kernel (default) and the
+    one-CTA-per-(window, head) kernel (SST_LT_ATTN=fused) issue the same MMAs
     in the same order: bit-identical outputs, including item counts that do
     not divide the grid and fewer items than SMs."""
     rng = np.random.default_rng(14 + D + G)
