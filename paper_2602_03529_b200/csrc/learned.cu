@@ -1246,8 +1246,8 @@ __global__ void __launch_bounds__(128)
 // ---- attention epilogue helpers (k_lt_attn_fused, k_lt_attn_persist) -----
 // Thread = TMEM lane = token row q of the window (q = frame * 64 + 8y + x).
 
-// qkv accumulator row (192 TMEM columns at tq) + bias -> bf16 Q and K rows
-// into their 128B-swizzled K-major tiles, V transposed into V^T's tile.
+// qkv accumulator row (192 TMEM columns at tq) + bias -> bf16 Q, K and V rows
+// into their 128B-swizzled tiles.
 __device__ __forceinline__ void att_qkv_epilogue(uint32_t tq, const float* __restrict__ bqkv, int D,
                                                  int head, bool valid, int q, uint8_t* sQ,
                                                  uint8_t* sK, uint8_t* sV) {
@@ -1270,27 +1270,31 @@ __device__ __forceinline__ void att_qkv_epilogue(uint32_t tq, const float* __res
 #pragma unroll
       for (int e = 0; e < 32; ++e) v[e] = 0.0f;
     }
-    if (part < 2) {
-      uint8_t* base = part == 0 ? sQ : sK;
+    // Q, K: K-major A / B of S = Q K^T; V: MN-major B of O = P V (row =
+    // key, d contiguous) -- all three are plain swizzled 128-byte rows
+    uint8_t* base = part == 0 ? sQ : (part == 1 ? sK : sV);
 #pragma unroll
-      for (int qq = 0; qq < 4; ++qq) {
-        uint4 w4;
-        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w4);
+    for (int qq = 0; qq < 4; ++qq) {
+      uint4 w4;
+      __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&w4);
 #pragma unroll
-        for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[qq * 8 + 2 * e], v[qq * 8 + 2 * e + 1]);
-        const int j = (d0 >> 3) + qq;
-        *reinterpret_cast<uint4*>(base + q * 128 + ((j ^ (q & 7)) << 4)) = w4;
-      }
-    } else {
-      const int kbk = q >> 6, kk = q & 63;
-      uint8_t* vb = sV + kbk * 8192 + (kk & 7) * 2;
-#pragma unroll
-      for (int e = 0; e < 32; ++e) {
-        const int d = d0 + e;
-        *reinterpret_cast<__nv_bfloat16*>(vb + d * 128 + (((kk >> 3) ^ (d & 7)) << 4)) =
-            __float2bfloat16_rn(v[e]);
-      }
+      for (int e = 0; e < 4; ++e) h2[e] = __floats2bfloat162_rn(v[qq * 8 + 2 * e], v[qq * 8 + 2 * e + 1]);
+      const int j = (d0 >> 3) + qq;
+      *reinterpret_cast<uint4*>(base + q * 128 + ((j ^ (q & 7)) << 4)) = w4;
     }
+  }
+}
+
+// O = P V: A = P (K-major, two 64-key tiles at sP), B = V (MN-major [128
+// keys][64 d] at sV); 8 MMAs of K = 16 keys.
+__device__ __forceinline__ void att_issue_pv(uint32_t tmem_o, uint8_t* sP, uint8_t* sV) {
+  constexpr uint32_t id2 = tc::idesc_bf16_f32_bmn(128, 64);
+#pragma unroll
+  for (int kb = 0; kb < 2; ++kb) {
+    const uint64_t ad = tc::smem_desc_sw128(smem_u32(sP + kb * 16384));
+    const uint64_t bd = tc::smem_desc_sw128(smem_u32(sV + kb * 8192));
+#pragma unroll
+    for (int k = 0; k < 4; ++k) tc::mma_bf16(tmem_o, ad + 2 * k, bd + 128 * k, id2, kb | k);
   }
 }
 
@@ -1388,7 +1392,7 @@ __device__ __forceinline__ void att_store_o(uint32_t tO, float l, bool valid, __
 // A = the window's tokens of the residual stream (two 5-D TMA boxes per
 // 64-channel block, zero-filled outside the frame), B = the head's 192 rows of
 // W_qkv, through a 2-stage TMA ring; the epilogue (+bias, bf16) writes Q, K
-// and V^T straight into the swizzled operand tiles of S = QK^T, then the
+// and V straight into the swizzled operand tiles of S = QK^T and O = PV, then the
 // softmax / P V steps of k_lt_attn_tc follow.  The qkv tensor never exists.
 constexpr int AF_STAGE = 16384 + 24576;                 // A (128 x 64) + B (192 x 64) bf16
 constexpr int AF_SMEM = 2 * AF_STAGE + 1024 + 128 + 128 * 4;
@@ -1402,7 +1406,7 @@ __global__ void __launch_bounds__(128)
   uint8_t* sQ = smem;                 // after the projection: [128 q][64 d]
   uint8_t* sK = smem + 16384;         // [128 k][64 d]
   uint8_t* sP = smem;                 // [2 kb][128 q][64 k]
-  uint8_t* sV = smem + 32768;         // [2 kb][64 d][64 k]  (V^T)
+  uint8_t* sV = smem + 32768;         // [128 k][64 d]  (MN-major B of O = P V)
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * AF_STAGE);
   uint64_t* empty = full + 2;
   uint64_t* bar = empty + 2;          // [0] qkv, [1] S, [2] O
@@ -1462,7 +1466,7 @@ __global__ void __launch_bounds__(128)
   mbar_wait(&bar[0], 0);
   tc::fence_after_sync();
 
-  // ---- +bias, bf16: Q and K rows into their tiles, V transposed ----
+  // ---- +bias, bf16: Q, K and V rows into their tiles ----
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   att_qkv_epilogue(trow, bqkv, D, head, valid, t, sQ, sK, sV);
   fence_proxy_async_smem();
@@ -1491,14 +1495,7 @@ __global__ void __launch_bounds__(128)
   __syncthreads();
   tc::fence_after_sync();
   if (t == 0) {
-    constexpr uint32_t id2 = tc::idesc_bf16_f32(128, 64);
-#pragma unroll
-    for (int kb = 0; kb < 2; ++kb) {
-      const uint64_t ad = tc::smem_desc_sw128(smem_u32(sP + kb * 16384));
-      const uint64_t bd = tc::smem_desc_sw128(smem_u32(sV + kb * 8192));
-#pragma unroll
-      for (int k = 0; k < 4; ++k) tc::mma_bf16(tmem, ad + 2 * k, bd + 2 * k, id2, kb | k);
-    }
+    att_issue_pv(tmem, sP, sV);
     tc::mma_commit(&bar[2]);
   }
   mbar_wait(&bar[2], 0);
@@ -1521,14 +1518,14 @@ __global__ void __launch_bounds__(128)
 //   warps 2-5,  two epilogue groups of 128 threads (one TMEM lane = one query
 //   warps 6-9   row each); group b handles the items of parity b with its own
 //               TMEM half (256 columns: qkv 0..191, S 0..127, O 128..191) and
-//               its own operand tiles (Q, K, V^T; P over Q and K).
+//               its own operand tiles (Q, K, V; P over Q and K).
 // TMEM per group: qkv columns 0..191, S 0..127 (over q|k, once they are in
 // smem), O 192..255 -- so the projection of the group's next item only has
 // to wait until this item's scores are consumed (p_ready), not for its O.
 // Hand-offs are mbarriers: qkv_full / s_full / o_full (MMA commits),
 // ops_ready / p_ready (128 epilogue arrivals each).
 constexpr int AP_RING = 2 * AF_STAGE;                         // 80 KB
-constexpr int AP_OPS = 3 * 16384;                             // Q, K, V^T per group
+constexpr int AP_OPS = 3 * 16384;                             // Q, K, V per group
 constexpr int AP_SMEM = AP_RING + 2 * AP_OPS + 256 + 1024;
 
 __global__ void __launch_bounds__(352, 1)
@@ -1657,18 +1654,8 @@ __global__ void __launch_bounds__(352, 1)
         }
         mbar_wait(&p_ready[b], u & 1);
         tc::fence_after_sync();
-        {
-          constexpr uint32_t id2 = tc::idesc_bf16_f32(128, 64);
-#pragma unroll
-          for (int kbk = 0; kbk < 2; ++kbk) {
-            const uint64_t ad = tc::smem_desc_sw128(smem_u32(o + kbk * 16384));
-            const uint64_t bd = tc::smem_desc_sw128(smem_u32(o + 32768 + kbk * 8192));
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              tc::mma_bf16(tmem + b * 256 + 192, ad + 2 * k, bd + 2 * k, id2, kbk | k);
-          }
-          tc::mma_commit(&o_full[b]);
-        }
+        att_issue_pv(tmem + b * 256 + 192, o, o + 32768);
+        tc::mma_commit(&o_full[b]);
       }
     }
   } else {
@@ -1687,7 +1674,7 @@ __global__ void __launch_bounds__(352, 1)
       const int g = c.g, wy = c.wy, wx = c.wx, head = c.head;
       const int y = wy * ATT_WIN + (lt >> 3), x = wx * ATT_WIN + (lt & 7);
       const bool valid = y < Ht && x < Wt;
-      // -- qkv: +bias, bf16; Q and K rows into their tiles, V transposed --
+      // -- qkv: +bias, bf16; Q, K and V rows into their tiles --
       mbar_wait(&qkv_full[grp], u & 1);
       tc::fence_after_sync();
       att_qkv_epilogue(tb, bqkv, D, head, valid, q, sQ, sK, sV);
@@ -2144,10 +2131,10 @@ extern "C" int sst_lt_attn_fused(const void* h, const void* w_qkv, const float* 
   if (!make_tmap_bf16_5d(&tmH, h, hdims, lt::ATT_WIN, lt::ATT_WIN)) return SST_ERR_ARG;
   if (!make_tmap_bf16_2d(&tmW, w_qkv, (uint64_t)D, (uint64_t)(3 * D), lt::ATT_HD)) return SST_ERR_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
-  // default: the persistent warp-specialised kernel (0.221 ms at the learned
+  // default: the persistent warp-specialised kernel (0.211 ms at the learned
   // leg's shape, 32 x 1080p GoPs, D=256; scripts/attn_micro.py).
   // SST_LT_ATTN=fused: one CTA per (GoP, window, head), two CTAs per SM
-  // (0.264 ms) -- bit-identical.  Both are bound by the SIMT epilogue; the
+  // (0.257 ms) -- bit-identical.  Both are bound by the SIMT epilogue; the
   // persistent kernel overlaps it with the next item's qkv GEMM.
   const char* ea = getenv("SST_LT_ATTN");
   if (!(ea && !strcmp(ea, "fused"))) {

@@ -39,6 +39,14 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
          ((uint32_t)(M >> 4) << 24);
 }
 
+// Same with B MN-major (transpose-B bit 16): B stored as [K rows][N] with N
+// contiguous, 128-byte rows swizzled in 8-row atoms exactly like a K-major
+// tile -- the smem descriptor is unchanged (SBO = 1024 B between 8-row groups
+// along K), and a K step of 16 advances its start address by 2 x 1024 B.
+__host__ __device__ constexpr uint32_t idesc_bf16_f32_bmn(int M, int N) {
+  return idesc_bf16_f32(M, N) | (1u << 16);
+}
+
 __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                          uint32_t idesc, uint32_t accumulate) {
   asm volatile(
