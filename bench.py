@@ -892,6 +892,23 @@ def run_learned(a, device) -> dict:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / K
+    # one stream alone (G = 1, blend on): GoP latency vs the real-time budget
+    c1 = LearnedGopCodec(1, H, W, s, model=model)
+    c1.set_gop_ids([0])
+    k1 = c1.drop_k(a.drop)
+    for k in range(3):
+        c1.step(frames[k % 2][:1], outs[k % 2][:1], 1, drop_k=k1)
+    torch.cuda.synchronize()
+    single = []
+    for k in range(10):
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record()
+        c1.step(frames[k % 2][:1], outs[k % 2][:1], 1, drop_k=k1)
+        b1.record()
+        torch.cuda.synchronize()
+        single.append(b0.elapsed_time(b1))
+    single.sort()
+    del c1
     # serialised pass (full batch, one stream): time every conv launch
     times = []
     orig = model._conv
@@ -935,6 +952,10 @@ def run_learned(a, device) -> dict:
                      "avg_launch_ms": round(sum(m for m, _ in halo) / len(halo), 4),
                      "launches_per_step": len(halo)},
         "conv_share_of_serialised_step": round(conv_ms / max(ms, 1e-9), 3),
+        "single_stream": {"stream": "1 x 1080p, s=3, learned tokenizer, 10% drop, blend n=2",
+                          "gop_ms_median": round(single[len(single) // 2], 3),
+                          "gop_ms_max": round(single[-1], 3),
+                          "realtime_30fps_budget_ms_per_gop": round(GOP / 30 * 1e3, 1)},
         "gpu_launches_per_step": launches_step,
         "dtype": "bf16 operands, fp32 accumulate (TMEM)",
         "parity": "tests/test_gpu_learned.py vs oracle/learned_oracle.py (torch fp32, unpinned)",
