@@ -310,7 +310,7 @@ typedef struct SstConvDesc {
   int32_t taps[27][3];     /* (dt, dy, dx) input offsets per tap; K order = tap-major, channel-minor */
   const void* weight;      /* bf16 [N][K], K = n_taps * in_C */
   int32_t N, K;
-  const float* bias;       /* fp32 [N] */
+  const float* bias;       /* fp32 [N], 16-byte aligned */
   int32_t epi, act;        /* SST_LT_EPI_*; act 1 = SiLU (STORE only) */
   const void* residual;    /* STORE: bf16, same layout as out, or NULL */
   void* out;               /* STORE: bf16 [G][out_T][Ht][Wt][N] */
@@ -354,7 +354,7 @@ SST_API int sst_lt_unpack_dec_in(const uint8_t* buf, const int64_t* off, SstPack
 SST_API int sst_lt_attn(const void* qkv, int G, int Ht, int Wt, int D, void* out, void* stream);
 
 /* qkv projection fused with the attention core: h bf16 [G][2][H'][W'][D]
- * (the block input), w_qkv bf16 [3D][D], b_qkv fp32 [3D] -> out bf16
+ * (the block input), w_qkv bf16 [3D][D], b_qkv fp32 [3D] (16-byte aligned) -> out bf16
  * [G][2][H'][W'][D]; same result definition as a 1x1 sst_lt_conv (bf16 qkv)
  * followed by sst_lt_attn. */
 SST_API int sst_lt_attn_fused(const void* h, const void* w_qkv, const float* b_qkv, int G, int Ht,

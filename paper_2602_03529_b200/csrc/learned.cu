@@ -689,17 +689,29 @@ __device__ __forceinline__ uint64_t halo_desc_pitch(uint32_t saddr, int pitch) {
 // kTma: STORE epilogue through a swizzled smem staging tile + 5-D TMA store
 // (short-K 1x1 GEMMs, whose cost is the output write); otherwise direct
 // 16-byte stores from registers.
-template <bool kTma>
-__host__ __device__ constexpr int pair_bstages() { return kTma ? 4 : c233c::BSTAGES; }
+// Operand ring depths.  Halo convs: 3 halo slots (23 KB) x 8 weight stages.
+// 1x1 GEMMs (a 16 KB token box per k-block, K = 4..24 k-blocks): 5 + 5
+// (TMA-store epilogue, whose 64 KB staging tile takes the rest) or 5 + 8
+// (pixels) -- the producer runs a whole 4-k-block unit ahead, which the
+// short-K, HBM-bound GEMMs need to keep enough bytes in flight.
+template <bool kHalo, bool kTma>
+__host__ __device__ constexpr int pair_bstages() { return kHalo ? c233c::BSTAGES : (kTma ? 5 : 8); }
+template <bool kHalo>
+__host__ __device__ constexpr int pair_hslots() { return kHalo ? c233c::HSLOTS : 5; }
+template <bool kHalo>
+__host__ __device__ constexpr int pair_hstride() { return kHalo ? c233c::HALO_STRIDE : 16384; }
 // kPix: PIXELS epilogue (unpatchify), units of 192 output channels (one frame's
 // 8x8x3 patch), 96 weight rows per CTA
 template <bool kPix>
 __host__ __device__ constexpr int pair_bbytes() { return (kPix ? 96 : c233c::BNH) * 128; }
-template <bool kTma, bool kPix = false>
+template <bool kHalo, bool kTma, bool kPix = false>
 __host__ __device__ constexpr int pair_smem() {
-  return c233c::HSLOTS * c233c::HALO_STRIDE + pair_bstages<kTma>() * pair_bbytes<kPix>() +
+  return pair_hslots<kHalo>() * pair_hstride<kHalo>() + pair_bstages<kHalo, kTma>() * pair_bbytes<kPix>() +
          (kTma ? 2 * 2 * 16384 : 0) + 1024 + 512;
 }
+static_assert(pair_smem<true, false>() <= 232448, "halo conv smem");
+static_assert(pair_smem<false, true>() <= 232448, "1x1 conv smem");
+static_assert(pair_smem<false, false, true>() <= 232448, "pixel conv smem");
 
 __device__ __forceinline__ void named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -714,7 +726,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
   constexpr int kPitch = kHalo ? PITCH : 8;
   constexpr int kBoxBytes = kHalo ? HALO_BYTES : 8 * 16 * 128;
   constexpr int kSpatial = kHalo ? 9 : 1;
-  constexpr int BSTAGES = pair_bstages<kTma>();
+  constexpr int BSTAGES = pair_bstages<kHalo, kTma>();
+  constexpr int HSLOTS = pair_hslots<kHalo>();
+  constexpr int HALO_STRIDE = pair_hstride<kHalo>();
   constexpr int kNU = kPix ? 192 : 256;          // output channels per unit
   constexpr int kBNH = kNU / 2;                  // weight rows per CTA
   constexpr int B_BYTES = pair_bbytes<kPix>();
@@ -855,8 +869,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
         if (!valid) continue;
         const int f = a.frame_base + nb;
         const int nb0 = nb * kNU + half * 96;
+        const float4* bp4 = reinterpret_cast<const float4*>(a.bias + nb0);
 #pragma unroll
-        for (int i = 0; i < 96; ++i) v[i] = fminf(fmaxf(v[i] + __ldg(a.bias + nb0 + i), 0.0f), 1.0f);
+        for (int i4 = 0; i4 < 24; ++i4) {
+          const float4 bb = __ldg(bp4 + i4);
+          v[4 * i4 + 0] = fminf(fmaxf(v[4 * i4 + 0] + bb.x, 0.0f), 1.0f);
+          v[4 * i4 + 1] = fminf(fmaxf(v[4 * i4 + 1] + bb.y, 0.0f), 1.0f);
+          v[4 * i4 + 2] = fminf(fmaxf(v[4 * i4 + 2] + bb.z, 0.0f), 1.0f);
+          v[4 * i4 + 3] = fminf(fmaxf(v[4 * i4 + 3] + bb.w, 0.0f), 1.0f);
+        }
         const bool vec = (a.w & 3) == 0;
 #pragma unroll
         for (int pr = 0; pr < 4; ++pr) {
@@ -883,8 +904,81 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
       const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + ab * 256 + half * 128;
       const size_t tok = (((size_t)g * a.out_T + t) * a.Ht + y) * a.Wt + x;
       __nv_bfloat16* outp = a.out + tok * a.N + n0;
-      uint8_t* stage = sStage + half * 2 * 16384;
-      if (kTma) named_bar(1 + half, 128);    // the previous unit's TMA store has read the tile
+      if (kTma) {
+        // ---- short-K GEMM epilogue (HBM-bound): this row's 128 residual
+        // values are fetched up front (one memory latency per unit, not one
+        // per 32-column chunk), and the wait for the previous unit's TMA
+        // store to release the staging tile is deferred to the first
+        // staging write, so it overlaps the TMEM drain and the loads ----
+        uint8_t* stage = sStage + half * 2 * 16384;
+        uint4 res[16];
+        const bool has_res = valid && a.residual != nullptr;
+        if (has_res) {
+          const uint4* rp = reinterpret_cast<const uint4*>(a.residual + tok * a.N + n0);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) res[i] = __ldg(rp + i);
+        }
+#pragma unroll
+        for (int c = 0; c < 128; c += 32) {
+          float v[32];
+          tc::tmem_ld32(trow + c, v);
+          if (c + 32 == 128) {
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive_cluster(aempty_leader + ab * 8);
+          }
+          const float4* bp = reinterpret_cast<const float4*>(a.bias + n0 + c);
+#pragma unroll
+          for (int i4 = 0; i4 < 8; ++i4) {
+            const float4 bb = __ldg(bp + i4);
+            v[4 * i4 + 0] += bb.x;
+            v[4 * i4 + 1] += bb.y;
+            v[4 * i4 + 2] += bb.z;
+            v[4 * i4 + 3] += bb.w;
+          }
+          if (a.act) {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = silu(v[i]);
+          }
+          if (has_res) {
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&res[(c >> 3) + qq]);
+#pragma unroll
+              for (int e2 = 0; e2 < 4; ++e2) {
+                float2 f = __bfloat1622float2(h2[e2]);
+                v[qq * 8 + 2 * e2] += f.x;
+                v[qq * 8 + 2 * e2 + 1] += f.y;
+              }
+            }
+          }
+          if (c == 0) {
+            // the previous unit's TMA store has read the staging tile
+            if (issuer) tma_store_wait_read();
+            named_bar(1 + half, 128);
+          }
+          const int box = c >> 6, j0 = (c & 63) >> 3;
+#pragma unroll
+          for (int qq = 0; qq < 4; ++qq) {
+            uint4 uu;
+            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&uu);
+#pragma unroll
+            for (int e2 = 0; e2 < 4; ++e2)
+              h2[e2] = __floats2bfloat162_rn(v[qq * 8 + 2 * e2], v[qq * 8 + 2 * e2 + 1]);
+            const int j = j0 + qq;
+            *reinterpret_cast<uint4*>(stage + box * 16384 + m * 128 + ((j ^ (m & 7)) << 4)) = uu;
+          }
+        }
+        fence_proxy_async_smem();
+        named_bar(1 + half, 128);
+        if (issuer) {
+#pragma unroll
+          for (int b = 0; b < 2; ++b)
+            tc::tma_store_5d(&tmC, stage + b * 16384, n0 + b * 64, x0 + 8 * (int)rank, y0, t, g);
+          tma_store_commit();
+        }
+        continue;
+      }
 #pragma unroll 1
       for (int c = 0; c < 128; c += 32) {
         float v[32];
@@ -898,21 +992,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
         for (int i = 0; i < 32; ++i) {
           v[i] += __ldg(a.bias + n0 + c + i);
           if (a.act) v[i] = silu(v[i]);
-        }
-        if (kTma) {
-          if (valid) epi_add_residual(v, a, tok * a.N + n0 + c);
-          const int box = c >> 6, j0 = (c & 63) >> 3;
-#pragma unroll
-          for (int qq = 0; qq < 4; ++qq) {
-            uint4 uu;
-            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&uu);
-#pragma unroll
-            for (int e2 = 0; e2 < 4; ++e2)
-              h2[e2] = __floats2bfloat162_rn(v[qq * 8 + 2 * e2], v[qq * 8 + 2 * e2 + 1]);
-            const int j = j0 + qq;
-            *reinterpret_cast<uint4*>(stage + box * 16384 + m * 128 + ((j ^ (m & 7)) << 4)) = uu;
-          }
-          continue;
         }
         if (!valid) continue;
         if (a.residual != nullptr) {
@@ -938,17 +1017,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
           for (int e2 = 0; e2 < 4; ++e2)
             h2[e2] = __floats2bfloat162_rn(v[qq * 8 + 2 * e2], v[qq * 8 + 2 * e2 + 1]);
           op[qq] = uu;
-        }
-      }
-      if (kTma) {
-        fence_proxy_async_smem();
-        named_bar(1 + half, 128);
-        if (issuer) {
-#pragma unroll
-          for (int b = 0; b < 2; ++b)
-            tc::tma_store_5d(&tmC, stage + b * 16384, n0 + b * 64, x0 + 8 * (int)rank, y0, t, g);
-          tma_store_commit();
-          tma_store_wait_read();           // staging reusable once the bulk store read it
         }
       }
     }
@@ -1908,7 +1976,7 @@ static int launch_convpair_pixels(const SstConvDesc* d, cudaStream_t st) {
   SST_CUDA_TRY(cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev));
   const int64_t pairs = units < n_sm / 2 ? units : n_sm / 2;
   auto kern = k_lt_convpair<false, false, true>;
-  const int smem = pair_smem<false, true>();
+  const int smem = pair_smem<false, false, true>();
   SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   kern<<<(unsigned)(2 * pairs), c233c::THREADS, smem, st>>>(tmA, tmB, tmC, a, (int)units, n_blocks);
   SST_LAUNCH_CHECK();
@@ -1960,7 +2028,7 @@ static int launch_convpair(const SstConvDesc* d, cudaStream_t st, bool halo) {
     if (!make_tmap_bf16_5d(&tmC, d->out, cdims, 8, 16)) return SST_ERR_ARG;
   }
   auto kern = halo ? k_lt_convpair<true, false> : k_lt_convpair<false, true>;
-  const int smem = halo ? pair_smem<false>() : pair_smem<true>();
+  const int smem = halo ? pair_smem<true, false>() : pair_smem<false, true>();
   SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   kern<<<(unsigned)(2 * pairs), c233c::THREADS, smem, st>>>(tmA, tmB, tmC, a, (int)units, n_blocks);
   SST_LAUNCH_CHECK();
@@ -2011,6 +2079,7 @@ using namespace sst;
 
 extern "C" int sst_lt_conv(const SstConvDesc* d, void* stream) {
   if (!d || !d->in || !d->weight || !d->bias) return SST_ERR_ARG;
+  if (reinterpret_cast<uintptr_t>(d->bias) & 15u) return SST_ERR_ARG;   // float4 bias loads
   if (d->in_C <= 0 || d->in_C % lt::BK != 0) return SST_ERR_ARG;
   if (d->n_taps < 1 || d->n_taps > 27 || d->K != d->n_taps * d->in_C) return SST_ERR_ARG;
   if (d->G <= 0 || d->Ht <= 0 || d->Wt <= 0 || d->t_cnt <= 0) return SST_ERR_ARG;
@@ -2121,6 +2190,7 @@ extern "C" int sst_lt_attn(const void* qkv, int G, int Ht, int Wt, int D, void* 
 extern "C" int sst_lt_attn_fused(const void* h, const void* w_qkv, const float* b_qkv, int G, int Ht,
                                  int Wt, int D, void* out, void* stream) {
   if (!h || !w_qkv || !b_qkv || !out || G <= 0 || Ht <= 0 || Wt <= 0 || D <= 0) return SST_ERR_ARG;
+  if (reinterpret_cast<uintptr_t>(b_qkv) & 15u) return SST_ERR_ARG;   // float4 bias loads
   if (D % lt::ATT_HD || G > 65535 || D / lt::ATT_HD > 65535) return SST_ERR_ARG;
   const int64_t wins = (int64_t)ceil_div(Ht, lt::ATT_WIN) * ceil_div(Wt, lt::ATT_WIN);
   if (wins > 0x7fffffff) return SST_ERR_ARG;

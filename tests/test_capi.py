@@ -95,8 +95,11 @@ def test_learned_entry_point_argument_errors(lib):
     from paper_2602_03529_b200 import _lib
     d = _lib.SstConvDesc()
     assert lib.sst_lt_conv(ctypes.byref(d), None) == -1               # null pointers
-    d.in_, d.weight, d.bias = 16, 16, 16
-    d.in_C, d.n_taps, d.K, d.G, d.Ht, d.Wt, d.t_cnt = 48, 1, 48, 1, 4, 4, 1
+    d.in_, d.weight, d.bias = 16, 16, 20
+    d.in_C, d.n_taps, d.K, d.G, d.Ht, d.Wt, d.t_cnt = 64, 1, 64, 1, 4, 4, 1
+    assert lib.sst_lt_conv(ctypes.byref(d), None) == -1               # bias not 16-byte aligned
+    d.bias = 16
+    d.in_C, d.K = 48, 48
     assert lib.sst_lt_conv(ctypes.byref(d), None) == -1               # in_C not a multiple of 64
     d.in_C, d.K = 64, 128
     assert lib.sst_lt_conv(ctypes.byref(d), None) == -1               # K != n_taps * in_C
@@ -109,6 +112,8 @@ def test_learned_entry_point_argument_errors(lib):
                                ctypes.c_void_p(16), None) == -1        # s not in {1,2,3}
     assert lib.sst_lt_dec_in(None, None, 1, 1, 1, None, None) == -1
     assert lib.sst_lt_attn(ctypes.c_void_p(16), 1, 8, 8, 100, ctypes.c_void_p(16), None) == -1
+    assert lib.sst_lt_attn_fused(ctypes.c_void_p(16), ctypes.c_void_p(16), ctypes.c_void_p(20), 1,
+                                 8, 8, 128, ctypes.c_void_p(16), None) == -1   # misaligned bias
     assert lib.sst_upscale_blend9(ctypes.c_void_p(16), 1, 8, 8, 2, 16, 16, ctypes.c_void_p(16), 5,
                                   ctypes.c_void_p(16), None) == -4   # blend width > 4 with prev
     assert lib.sst_similarity_gop(None, 1, 4, 12, None, None) == -1
