@@ -704,10 +704,14 @@ __host__ __device__ constexpr int pair_hstride() { return kHalo ? c233c::HALO_ST
 // 8x8x3 patch), 96 weight rows per CTA
 template <bool kPix>
 __host__ __device__ constexpr int pair_bbytes() { return (kPix ? 96 : c233c::BNH) * 128; }
+// epilogue staging: TMA-store tiles (kTma) or per-warp pixel rows (kPix:
+// 8 warps x 4 rows x 768 B, for coalesced frame stores)
+template <bool kTma, bool kPix>
+__host__ __device__ constexpr int pair_stage() { return kTma ? 2 * 2 * 16384 : (kPix ? 8 * 3072 : 0); }
 template <bool kHalo, bool kTma, bool kPix = false>
 __host__ __device__ constexpr int pair_smem() {
   return pair_hslots<kHalo>() * pair_hstride<kHalo>() + pair_bstages<kHalo, kTma>() * pair_bbytes<kPix>() +
-         (kTma ? 2 * 2 * 16384 : 0) + 1024 + 512;
+         pair_stage<kTma, kPix>() + 1024 + 512;
 }
 static_assert(pair_smem<true, false>() <= 232448, "halo conv smem");
 static_assert(pair_smem<false, true>() <= 232448, "1x1 conv smem");
@@ -738,7 +742,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
   uint8_t* sH = smem;
   uint8_t* sB = smem + HSLOTS * HALO_STRIDE;
   uint8_t* sStage = sB + BSTAGES * B_BYTES;            // kTma: [2 halves][2 boxes][128 rows][128 B]
-  uint64_t* hfull = reinterpret_cast<uint64_t*>(sStage + (kTma ? 2 * 2 * 16384 : 0));
+  uint64_t* hfull = reinterpret_cast<uint64_t*>(sStage + pair_stage<kTma, kPix>());
   uint64_t* hempty = hfull + HSLOTS;
   uint64_t* bfull = hempty + HSLOTS;
   uint64_t* bempty = bfull + BSTAGES;
@@ -866,7 +870,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
         tc::fence_before_sync();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive_cluster(aempty_leader + ab * 8);
-        if (!valid) continue;
         const int f = a.frame_base + nb;
         const int nb0 = nb * kNU + half * 96;
         const float4* bp4 = reinterpret_cast<const float4*>(a.bias + nb0);
@@ -879,6 +882,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
           v[4 * i4 + 3] = fminf(fmaxf(v[4 * i4 + 3] + bb.w, 0.0f), 1.0f);
         }
         const bool vec = (a.w & 3) == 0;
+        // warp = 4 token rows x the pair-half's 8 tokens: each pixel row of it
+        // is 8 x 8 px x 3 = 192 contiguous floats when all 8 tokens are inside
+        const int xs = x0 + 8 * (int)rank;                 // first token of the warp's rows
+        const bool seg = vec && xs + 8 <= a.Wt && xs * 8 + 64 <= a.w;
+        if (seg) {
+          float* srow = reinterpret_cast<float*>(sStage) + (warp - 2) * 768;   // [4][192]
+#pragma unroll
+          for (int pr = 0; pr < 4; ++pr) {
+            float4* s4 = reinterpret_cast<float4*>(srow + (lane >> 3) * 192 + (lane & 7) * 24);
+#pragma unroll
+            for (int e4 = 0; e4 < 6; ++e4)
+              s4[e4] = make_float4(v[pr * 24 + 4 * e4], v[pr * 24 + 4 * e4 + 1],
+                                   v[pr * 24 + 4 * e4 + 2], v[pr * 24 + 4 * e4 + 3]);
+            __syncwarp();
+#pragma unroll
+            for (int i = 0; i < 6; ++i) {
+              const int idx = i * 32 + lane, r = idx / 48, c4 = idx - r * 48;
+              const int yr = y0 + q * 4 + r;                 // token row of staged row r
+              const int Y = yr * 8 + half * 4 + pr;
+              if (yr < a.Ht && Y < a.h) {
+                float4* d4 = reinterpret_cast<float4*>(
+                    a.frames + ((((size_t)g * 9 + f) * a.h + Y) * a.w + xs * 8) * 3);
+                d4[c4] = reinterpret_cast<const float4*>(srow + r * 192)[c4];
+              }
+            }
+            __syncwarp();
+          }
+          continue;
+        }
+        if (!valid) continue;
 #pragma unroll
         for (int pr = 0; pr < 4; ++pr) {
           const int Y = y * 8 + half * 4 + pr;
