@@ -244,13 +244,18 @@ def test_fsq_head_indices():
     assert out["idx"].min() >= 0 and out["idx"].max() < 64000
 
 
-def test_pixels_unpatchify():
+@pytest.mark.parametrize("Ht,Wt,crop", [
+    (5, 7, (3, 5)),      # cropped, odd width: scalar store path
+    (21, 24, (5, 0)),    # width % 4 == 0: warp-staged coalesced rows, ragged last token rows
+    (19, 21, (2, 4)),    # staged interior segments + per-thread edge segment
+])
+def test_pixels_unpatchify(Ht, Wt, crop):
     rng = np.random.default_rng(5)
-    G, Ht, Wt = 2, 5, 7
+    G = 2
     h = _bf(rng.standard_normal((G, 2, Ht, Wt, 256)))
     W = _bf(rng.standard_normal((1536, 256)) / 16).numpy()
     b = np.full(1536, 0.5, np.float32)
-    hw = (Ht * 8 - 3, Wt * 8 - 5)            # cropped, odd width (scalar store path)
+    hw = (Ht * 8 - crop[0], Wt * 8 - crop[1])
     fr = _conv_gpu(h, W, b, [(0, 0, 0)], 1, 1, _lib.LT_EPI_PIXELS, hw=hw, frame_base=1)["frames"]
     op = LO.linear(h[:, 1], W, b).clamp(0, 1).reshape(G, Ht, Wt, 8, 8, 8, 3)
     want = op.permute(0, 3, 1, 4, 2, 5, 6).reshape(G, 8, Ht * 8, Wt * 8, 3)[:, :, :hw[0], :hw[1]]
