@@ -290,6 +290,7 @@ class StreamBank:
         self.launches = 0          # kernels of this library launched by step()
         # where each stream's last P image lives: (scale, parity, slot) or None
         self.last = [None] * n_streams
+        self._pending = None       # (frames, ids, gop_ids, drop_rate) between send / receive
 
     def step(self, frames_by_scale: dict, out_by_scale: dict, stream_ids_by_scale: dict,
              gop_ids_by_scale: dict, drop_rate: float = 0.0, present_by_scale: dict | None = None
@@ -298,6 +299,30 @@ class StreamBank:
         the streams coded at scale s this step ([g, 9, H, W, 3]); outputs go to
         ``out_by_scale[s]`` in the same order.  ``present_by_scale[s]`` (uint8
         per packet slot, I rows then P rows per GoP) simulates network loss."""
+        self._run(frames_by_scale, out_by_scale, stream_ids_by_scale, gop_ids_by_scale,
+                  drop_rate, present_by_scale, send=True, receive=True)
+
+    def send(self, frames_by_scale: dict, stream_ids_by_scale: dict, gop_ids_by_scale: dict,
+             drop_rate: float = 0.0) -> None:
+        """Sender half of ``step``: encode, drop and packetise one GoP per
+        stream into the packet arena.  ``receive`` must follow before the
+        next ``send`` (it consumes the arena); in between, other work may run
+        on the stream -- e.g. a pipelined caller receives GoP k, then sends
+        GoP k + 1, so its HBM-bound encode / reconstruction kernels sit on
+        either side of the latency-bound middle ones."""
+        self._run(frames_by_scale, None, stream_ids_by_scale, gop_ids_by_scale, drop_rate,
+                  None, send=True, receive=False)
+
+    def receive(self, out_by_scale: dict, present_by_scale: dict | None = None) -> None:
+        """Receiver half of ``step`` for the GoPs of the last ``send``."""
+        if self._pending is None:
+            raise RuntimeError("receive() without a pending send()")
+        frames_by_scale, ids, gop_ids, drop_rate = self._pending
+        self._run(frames_by_scale, out_by_scale, ids, gop_ids, drop_rate, present_by_scale,
+                  send=False, receive=True)
+
+    def _run(self, frames_by_scale, out_by_scale, stream_ids_by_scale, gop_ids_by_scale,
+             drop_rate, present_by_scale, send: bool, receive: bool) -> None:
         parity = self.step_idx & 1
         main = torch.cuda.current_stream()
         joined = []
@@ -312,26 +337,39 @@ class StreamBank:
                 gs.wait_stream(main)
                 joined.append(gs)
             with torch.cuda.stream(gs):
-                codec.set_gop_ids(gop_ids_by_scale[s])
-                codec.tokenize(frames, g)
-                present = None if present_by_scale is None else present_by_scale.get(s)
                 mid = self.mid_stream if self.mid_stream is not None else gs
-                if mid is not gs:
-                    mid.wait_stream(gs)
-                with torch.cuda.stream(mid):
-                    codec.select_and_pack(g, codec.drop_k(drop_rate))
-                    codec.decode(g, parity, present=present)
-                if mid is not gs:
+                if send:
+                    codec.set_gop_ids(gop_ids_by_scale[s])
+                    codec.tokenize(frames, g)
+                    if mid is not gs:
+                        mid.wait_stream(gs)
+                    with torch.cuda.stream(mid):
+                        codec.select_and_pack(g, codec.drop_k(drop_rate))
+                    # K1 + K2 (if dropping) + K3
+                    self.launches += 1 + (1 if codec.drop_k(drop_rate) > 0 else 0) + 1
+                if receive:
+                    present = None if present_by_scale is None else present_by_scale.get(s)
+                    if mid is not gs:
+                        mid.wait_stream(gs)
+                    with torch.cuda.stream(mid):
+                        codec.decode(g, parity, present=present)
+                    if mid is not gs:
+                        gs.wait_stream(mid)
+                    # K4 parse + 5 (init/route/dups/rowprep/decode) + K5
+                    self.launches += 1 + 5 + 1
+                    staged = self._prev_descs(s, ids)
+                    codec.reconstruct(g, parity, out_by_scale[s],
+                                      None if staged is None else staged[0])
+                    if staged is not None:
+                        self.rings[s].release(staged[1])
+                elif mid is not gs:
                     gs.wait_stream(mid)
-                # K1 + K2 (if dropping) + K3 + K4 parse + 5 (init/route/dups/rowprep/decode) + K5
-                self.launches += 1 + (1 if codec.drop_k(drop_rate) > 0 else 0) + 1 + 1 + 5 + 1
-                staged = self._prev_descs(s, ids)
-                codec.reconstruct(g, parity, out_by_scale[s],
-                                  None if staged is None else staged[0])
-                if staged is not None:
-                    self.rings[s].release(staged[1])
         for gs in joined:
             main.wait_stream(gs)
+        if not receive:
+            self._pending = (frames_by_scale, stream_ids_by_scale, gop_ids_by_scale, drop_rate)
+            return
+        self._pending = None
         for s, ids in stream_ids_by_scale.items():
             for slot, sid in enumerate(ids):
                 self.last[sid] = (s, parity, slot)

@@ -52,6 +52,45 @@ def test_multistream_variable_scale_matches_oracle(blend_n, HW):
                 assert np.array_equal(got[j], np.stack(ref["frames"])), (k, i, s)
 
 
+def test_send_receive_split_equals_step():
+    """StreamBank.send + receive (the sender and receiver halves, which a
+    pipelined caller can interleave: receive GoP k, then send GoP k + 1) give
+    the same packets and frames as step(), bit for bit."""
+    H, W = 72, 96
+    n_streams, n_gops = 3, 3
+    clips = [make_clip("noisy-motion" if i % 2 else "moving-square", W, H, 9 * n_gops, seed=i)
+             for i in range(n_streams)]
+    sched = [(3, 2, 3), (2, 2, 3), (3, 3, 2)]
+    a, b = StreamBank(n_streams, H, W), StreamBank(n_streams, H, W)
+    pending = None
+    outs_b = {}
+    for k in range(n_gops + 1):
+        if k < n_gops:
+            by_s = {}
+            for i in range(n_streams):
+                by_s.setdefault(sched[i][k], []).append(i)
+            frames = {s: torch.from_numpy(np.stack([clips[i].gop(k) for i in ids])).cuda()
+                      for s, ids in by_s.items()}
+            gids = {s: [k] * len(ids) for s, ids in by_s.items()}
+            outs_a = {s: torch.empty_like(f) for s, f in frames.items()}
+            a.step(frames, outs_a, by_s, gids, drop_rate=0.2)
+        if pending is not None:                      # pipelined: receive k-1 ...
+            pk, p_outs_a = pending
+            outs_b = {s: torch.empty_like(o) for s, o in p_outs_a.items()}
+            b.receive(outs_b)
+            torch.cuda.synchronize()
+            for s in outs_b:
+                assert torch.equal(outs_b[s], p_outs_a[s]), (pk, s)
+        if k < n_gops:                               # ... then send k
+            b.send(frames, by_s, gids, drop_rate=0.2)
+            torch.cuda.synchronize()
+            for s, ids in by_s.items():
+                assert _wire(a.codecs[s], len(ids)) == _wire(b.codecs[s], len(ids)), (k, s)
+            pending = (k, {s: o.clone() for s, o in outs_a.items()})
+    with pytest.raises(RuntimeError):
+        b.receive(outs_b)                            # nothing pending
+
+
 def test_loss_and_duplicate_packets_first_wins():
     H, W = 48, 64
     clip = make_clip("moving-square", W, H, 9, seed=3)
