@@ -909,6 +909,23 @@ def run_learned(a, device) -> dict:
         single.append(b0.elapsed_time(b1))
     single.sort()
     del c1
+    # the same single stream replayed as CUDA graphs (GraphedLearnedGopCodec)
+    from paper_2602_03529_b200.learned import GraphedLearnedGopCodec
+    c1g = LearnedGopCodec(1, H, W, s, model=model)
+    gr = GraphedLearnedGopCodec(c1g, 1, frames[0][:1], outs[0][:1], drop_k=k1)
+    for k in range(3):
+        gr.step([k])
+    torch.cuda.synchronize()
+    single_g = []
+    for k in range(10):
+        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        b0.record()
+        gr.step([k])
+        b1.record()
+        torch.cuda.synchronize()
+        single_g.append(b0.elapsed_time(b1))
+    single_g.sort()
+    del gr, c1g
     # serialised pass (full batch, one stream): time every conv launch
     times = []
     orig = model._conv
@@ -955,6 +972,7 @@ def run_learned(a, device) -> dict:
         "single_stream": {"stream": "1 x 1080p, s=3, learned tokenizer, 10% drop, blend n=2",
                           "gop_ms_median": round(single[len(single) // 2], 3),
                           "gop_ms_max": round(single[-1], 3),
+                          "graph_gop_ms_median": round(single_g[len(single_g) // 2], 3),
                           "realtime_30fps_budget_ms_per_gop": round(GOP / 30 * 1e3, 1)},
         "gpu_launches_per_step": launches_step,
         "dtype": "bf16 operands, fp32 accumulate (TMEM)",

@@ -458,3 +458,49 @@ class LearnedGopCodec(GopCodec):
         self.reconstruct(g, par, out, blend=self.primed)
         self.parity ^= 1
         self.primed = True
+
+
+class GraphedLearnedGopCodec:
+    """CUDA-graph replay of one LearnedGopCodec step (learned encode + FSQ,
+    similarity, drop, packetise, parse, packets -> decoder input, learned
+    decode, K5-9) for a fixed batch, fixed device buffers and one geometry --
+    the single-stream, one-GoP-in-flight regime, where ~30 launches per GoP
+    are host-bound.  Three graphs, as in ``pipeline.GraphedGopCodec``: the
+    first GoP (no blending) and the two steady-state parities (each blends
+    with the decoded frames the other parity wrote)."""
+
+    def __init__(self, codec: LearnedGopCodec, g: int, frames: torch.Tensor, out: torch.Tensor,
+                 drop_k: int = 0):
+        check_gop_tensor(frames, g, codec.H, codec.W, "frames")
+        check_gop_tensor(out, g, codec.H, codec.W, "out")
+        self.codec, self.g, self.frames, self.out, self.drop_k = codec, g, frames, out, drop_k
+        codec.set_gop_ids([0] * g)
+        plan = ((0, False), (1, True), (0, True))
+        side = torch.cuda.Stream(device=frames.device)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):                # warm-up outside capture
+            for par, blend in plan:
+                self._body(par, blend)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.graphs = []
+        for par, blend in plan:
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                self._body(par, blend)
+            self.graphs.append(gr)
+        self.k = 0
+
+    def _body(self, parity: int, blend: bool) -> None:
+        c = self.codec
+        c.tokenize(self.frames, self.g)
+        c.select_and_pack(self.g, self.drop_k)
+        c.decode(self.g, parity)
+        c.reconstruct(self.g, parity, self.out, blend=blend)
+
+    def step(self, gop_ids) -> None:
+        """Encode ... reconstruct the GoPs currently in ``frames`` into ``out``."""
+        self.codec.set_gop_ids(gop_ids)
+        idx = 0 if self.k == 0 else (1 if self.k % 2 == 1 else 2)
+        self.graphs[idx].replay()
+        self.k += 1

@@ -456,3 +456,30 @@ def test_learned_decoder_input_from_lossy_packets():
     for i in range(g):
         lost_i = sum(1 for j in lost[i] if j < codec.Ht)
         assert st[i, 0, 1] == codec.Ht - lost_i                      # I rows received
+
+
+def test_graphed_learned_codec_matches_eager():
+    """GraphedLearnedGopCodec replays the same launches as LearnedGopCodec.step:
+    bit-identical frames over a first GoP and both blend parities."""
+    from paper_2602_03529_b200.learned import GraphedLearnedGopCodec, LearnedGopCodec
+
+    H, W, s, g = 72, 96, 2, 1
+    cfg = LearnedConfig(dim=128, blocks=1, seed=6)
+    eager = LearnedGopCodec(g, H, W, s, cfg=cfg)
+    graphed = LearnedGopCodec(g, H, W, s, model=eager.model)
+    clip = make_clip("moving-square", W, H, 36, seed=4)
+    dev = _dev.device()
+    frames = torch.empty((g, 9, H, W, 3), device=dev)
+    out_g = torch.empty_like(frames)
+    drop_k = eager.drop_k(0.2)
+    gr = None
+    for k in range(4):
+        frames.copy_(torch.from_numpy(np.ascontiguousarray(clip.gop(k)[None])))
+        out_e = torch.empty_like(frames)
+        eager.set_gop_ids([k])
+        eager.step(frames, out_e, g, drop_k=drop_k)
+        if gr is None:
+            gr = GraphedLearnedGopCodec(graphed, g, frames, out_g, drop_k=drop_k)
+        gr.step([k])
+        torch.cuda.synchronize()
+        assert torch.equal(out_g, out_e), k
