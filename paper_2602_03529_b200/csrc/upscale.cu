@@ -646,9 +646,10 @@ __global__ void __launch_bounds__(kTQ, 3)
   if (has_prev) {
     const AxisTap txp = axis_tap(ox, pd.w, pd.s);
     const int pxl = (txp.lo - S.wx0[1]) * 3 + ch, pxh = (txp.hi - S.wx0[1]) * 3 + ch;
-    // frames 0..4 (the n <= 4 blended ones first), then 5..8.  One 9-frame
-    // pass measured slower (2.07 vs 1.77 ms per 32 GoPs: register spills),
-    // and so did a 2 + 7 split (1.79 ms)
+    // frames 0..4 (the n <= 4 blended ones first), then 5..8.  Measured
+    // slower (32 x 1080p GoPs, s=3, n=2; 1.77 ms here): one 9-frame pass at
+    // 3 CTAs/SM 2.07 ms (spills), at 2 CTAs/SM 1.93 ms; this split at 2
+    // CTAs/SM 2.10 ms; a 2 + 7 split 1.79 ms
     k5_9_compute<kBand, kP, 5, kN>(S, a, g, 0, q0, oy0, rows, tx, xl, xh, txp, pxl, pxh);
     k5_9_compute<kBand, kP, kGop - 5, 0>(S, a, g, 5, q0, oy0, rows, tx, xl, xh, txp, pxl, pxh);
   } else {
