@@ -470,13 +470,17 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP>& S, const UpArg
                                              const AxisTap& txp, int pxl, int pxh) {
   const int tid = threadIdx.x;
   const int r0 = S.ty_c[0].lo;
-  constexpr bool BLEND = NB > 0;
+  // blended frames f < NB = n: alpha_f = (n - 1 - f) / n; the last one has
+  // alpha = 0, i.e. clip(0 * prev + 1 * cur) = cur + 0.0 (exact: prev is
+  // finite and >= 0), so only the first n - 1 need the previous GoP
+  constexpr int NQ = NB > 0 ? NB - 1 : 0;
+  constexpr bool BLEND = NQ > 0;
   const int pr0 = BLEND ? S.ty_p[0].lo : 0;
   const int64_t orow = (int64_t)a.W * 3;
   const int64_t fstride = (int64_t)a.H * orow;
   float* op = a.out + ((int64_t)(g * kGop + f0) * a.H + oy0) * orow + q0 + tid;
   int ya = -1, yb = -1, qa = -1, qb = -1;
-  double ia[NF], ib[NF], qva[BLEND ? NB : 1], qvb[BLEND ? NB : 1];
+  double ia[NF], ib[NF], qva[BLEND ? NQ : 1], qvb[BLEND ? NQ : 1];
 #pragma unroll
   for (int j = 0; j < NF; ++j) ia[j] = ib[j] = 0.0;
   for (int r = 0; r < rows; ++r, op += orow) {
@@ -513,10 +517,10 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP>& S, const UpArg
       if (tp.lo != qa) {
         if (tp.lo == qb) {
 #pragma unroll
-          for (int j = 0; j < NB; ++j) qva[j] = qvb[j];
+          for (int j = 0; j < NQ; ++j) qva[j] = qvb[j];
         } else {
 #pragma unroll
-          for (int j = 0; j < NB; ++j) {
+          for (int j = 0; j < NQ; ++j) {
             const float* wq = &S.winp[j][(tp.lo - pr0) * kWF9];
             qva[j] = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
           }
@@ -526,10 +530,10 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP>& S, const UpArg
       if (tp.hi != qb) {
         if (tp.hi == qa) {
 #pragma unroll
-          for (int j = 0; j < NB; ++j) qvb[j] = qva[j];
+          for (int j = 0; j < NQ; ++j) qvb[j] = qva[j];
         } else {
 #pragma unroll
-          for (int j = 0; j < NB; ++j) {
+          for (int j = 0; j < NQ; ++j) {
             const float* wq = &S.winp[j][(tp.hi - pr0) * kWF9];
             qvb[j] = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
           }
@@ -541,9 +545,11 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP>& S, const UpArg
     for (int j = 0; j < NF; ++j) {
       const float ui = f32_clip_hi1(ia[j] * ty.g + ib[j] * ty.f);     // codec.py:235
       float v = ui;
-      if (j < NB) {   // codec.py:289-293
+      if (j < NQ) {   // codec.py:289-293
         const double dq = (double)f32_clip_hi1(qva[j] * tp.g + qvb[j] * tp.f);
         v = f32_clip_hi1(a.alpha[f0 + j] * dq + a.beta[f0 + j] * (double)ui);
+      } else if (j < NB) {
+        v = ui + 0.0f;   // alpha = 0: -0.0 becomes +0.0 as in 0 * prev + cur
       }
       __stcs(op + j * fstride, v);
     }
@@ -575,7 +581,7 @@ __device__ __forceinline__ void k5_9_window(float* dst, const float* img, int w,
 template <int kBand, bool kPrev, int kN, int kLoad>
 __global__ void __launch_bounds__(kTQ, 3)
     k_upscale9f(const __grid_constant__ CUtensorMap imap, const __grid_constant__ UpArgs a) {
-  constexpr int kP = kPrev ? kN : 0;
+  constexpr int kP = kPrev ? kN - 1 : 0;      // previous-GoP windows (alpha > 0 frames)
   extern __shared__ __align__(128) uint8_t smem_raw[];
   Up9fSmem<kBand, kP>& S = *reinterpret_cast<Up9fSmem<kBand, kP>*>(smem_raw);
   const int tid = threadIdx.x;
@@ -666,10 +672,10 @@ static int launch_k5_9f(const CUtensorMap& imap, const UpArgs& a, const SstPrevD
   auto kern = k_upscale9f<BAND, false, 1, LOAD>;
   if (prev) {
     switch (blend_n) {
-      case 1: kern = k_upscale9f<BAND, true, 1, LOAD>; smem = sizeof(Up9fSmem<BAND, 1>); break;
-      case 2: kern = k_upscale9f<BAND, true, 2, LOAD>; smem = sizeof(Up9fSmem<BAND, 2>); break;
-      case 3: kern = k_upscale9f<BAND, true, 3, LOAD>; smem = sizeof(Up9fSmem<BAND, 3>); break;
-      default: kern = k_upscale9f<BAND, true, 4, LOAD>; smem = sizeof(Up9fSmem<BAND, 4>); break;
+      case 1: kern = k_upscale9f<BAND, true, 1, LOAD>; smem = sizeof(Up9fSmem<BAND, 0>); break;
+      case 2: kern = k_upscale9f<BAND, true, 2, LOAD>; smem = sizeof(Up9fSmem<BAND, 1>); break;
+      case 3: kern = k_upscale9f<BAND, true, 3, LOAD>; smem = sizeof(Up9fSmem<BAND, 2>); break;
+      default: kern = k_upscale9f<BAND, true, 4, LOAD>; smem = sizeof(Up9fSmem<BAND, 3>); break;
     }
   }
   SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

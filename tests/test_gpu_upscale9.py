@@ -121,3 +121,21 @@ def test_upscale9_load_modes_identical(mode, monkeypatch):
     got = _run(img, s, H, W, prev, 2)
     for g in range(2):
         assert np.array_equal(got[g], _want(img[g], s, H, W, prev[g], 2))
+
+
+@pytest.mark.parametrize("n", [1, 2, 3])
+def test_upscale9_negative_zero_samples(n):
+    """-0.0 samples (allowed: >= 0) keep the reference's signs bit for bit:
+    bilinear of -0.0 neighbourhoods gives -0.0, and the alpha = 0 blend frame
+    turns it into +0.0 (0 * prev + cur)."""
+    H, W, s = 48, 64, 2
+    rng = np.random.default_rng(20 + n)
+    img = _frames(rng, 1, 24, 32)
+    img[0, :, :6, :8] = -0.0                   # whole bilinear neighbourhoods of -0.0
+    prev = [(_frames(rng, 1, 24, 32)[0], 2)]
+    prev[0][0][:, :6, :8] = 0.0
+    got = _run(img, s, H, W, prev, n)[0]
+    want = _want(img[0], s, H, W, prev[0], n)
+    assert np.array_equal(got, want)
+    assert np.array_equal(np.signbit(got), np.signbit(want))
+    assert np.signbit(want).any()              # the case is exercised
