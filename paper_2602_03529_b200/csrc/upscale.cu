@@ -804,9 +804,6 @@ extern "C" int sst_upscale_blend(const float* img, int G, int h, int w, int s, i
     const char* en = getenv("SST_K5_NBUF");
     const int band = (eb && atoi(eb) == 32) ? 32 : 16;
     const int nbuf = (en && atoi(en) == 2) ? 2 : 1;
-    if (var && var[0] == 'd')                     // "direct": streaming stores, no TMA tiles
-      return band == 16 ? launch_k5<16, 1, true>(omap, omap, a, prev, blend_n, st)
-                        : launch_k5<32, 1, true>(omap, omap, a, prev, blend_n, st);
     // I/P windows by TMA when img admits a tensor map ([G*2][h][w*3]; the
     // register-staged loads otherwise, or with SST_K5_LOAD=sync).  Same time
     // either way (1.17 ms per 32-GoP launch, scripts/k5_ab.sh): K5 is bound
@@ -814,10 +811,20 @@ extern "C" int sst_upscale_blend(const float* img, int G, int h, int w, int s, i
     const char* el = getenv("SST_K5_LOAD");
     CUtensorMap imap;
     memset(&imap, 0, sizeof(imap));
-    if (band == 16 && nbuf == 1 && !(var && var[0] == 'd') && !(el && !strcmp(el, "sync")) &&
-        make_tmap_f32_3d(&imap, img, (uint64_t)w * 3, (uint64_t)h, (uint64_t)G * 2, kWF9,
-                         UpTmaSmem<16>::kWR))
-      return launch_k5<16, 1, false, true>(omap, imap, a, prev, blend_n, st);
+    const bool tma_in = band == 16 && nbuf == 1 && !(el && !strcmp(el, "sync")) &&
+                        make_tmap_f32_3d(&imap, img, (uint64_t)w * 3, (uint64_t)h,
+                                         (uint64_t)G * 2, kWF9, UpTmaSmem<16>::kWR);
+    // Default: the direct-store variant with TMA window loads (s=3 with
+    // blend: 1.13 ms per 32-GoP launch vs 1.17 ms for TMA-store tiles; a
+    // write-only kernel with the same band pattern and no compute reaches
+    // 1.03 ms, scripts/diag/write_pattern.py).  SST_K5_VARIANT=tiles: the
+    // TMA-store tile variant.
+    if (!(var && !strcmp(var, "tiles"))) {        // "direct": streaming stores, no TMA tiles
+      if (tma_in) return launch_k5<16, 1, true, true>(omap, imap, a, prev, blend_n, st);
+      return band == 16 ? launch_k5<16, 1, true>(omap, omap, a, prev, blend_n, st)
+                        : launch_k5<32, 1, true>(omap, omap, a, prev, blend_n, st);
+    }
+    if (tma_in) return launch_k5<16, 1, false, true>(omap, imap, a, prev, blend_n, st);
     return band == 16 ? (nbuf == 1 ? launch_k5<16, 1>(omap, imap, a, prev, blend_n, st)
                                    : launch_k5<16, 2>(omap, imap, a, prev, blend_n, st))
                       : (nbuf == 1 ? launch_k5<32, 1>(omap, imap, a, prev, blend_n, st)
