@@ -666,9 +666,7 @@ constexpr int TILE = 16, PITCH = 10, HROWS = 18;
 constexpr int HALO_BYTES = PITCH * HROWS * 128;                   // 23040 (1x1: 8x16 box, 16384)
 constexpr int HALO_STRIDE = (HALO_BYTES + 1023) / 1024 * 1024;    // 23552
 constexpr int BNH = 128;                                          // weight rows per CTA
-constexpr int B_BYTES = BNH * 128;
 constexpr int HSLOTS = 3, BSTAGES = 8;
-constexpr int SMEM = HSLOTS * HALO_STRIDE + BSTAGES * B_BYTES + 1024 + 512;
 constexpr int EPI_WARPS = 8;
 constexpr int THREADS = 64 + EPI_WARPS * 32;
 }  // namespace c233c
@@ -937,7 +935,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
       const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + ab * 256 + half * 128;
       const size_t tok = (((size_t)g * a.out_T + t) * a.Ht + y) * a.Wt + x;
       __nv_bfloat16* outp = a.out + tok * a.N + n0;
-      if (kTma) {
+      if constexpr (kTma) {
         // ---- short-K GEMM epilogue (HBM-bound): this row's 128 residual
         // values are fetched up front (one memory latency per unit, not one
         // per 32-column chunk), and the wait for the previous unit's TMA
@@ -1010,46 +1008,46 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
             tc::tma_store_5d(&tmC, stage + b * 16384, n0 + b * 64, x0 + 8 * (int)rank, y0, t, g);
           tma_store_commit();
         }
-        continue;
-      }
+      } else {
 #pragma unroll 1
-      for (int c = 0; c < 128; c += 32) {
-        float v[32];
-        tc::tmem_ld32(trow + c, v);
-        if (c + 32 == 128) {
-          tc::fence_before_sync();
-          __syncwarp();
-          if (lane == 0) tc::mbar_arrive_cluster(aempty_leader + ab * 8);
-        }
+        for (int c = 0; c < 128; c += 32) {
+          float v[32];
+          tc::tmem_ld32(trow + c, v);
+          if (c + 32 == 128) {
+            tc::fence_before_sync();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive_cluster(aempty_leader + ab * 8);
+          }
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          v[i] += __ldg(a.bias + n0 + c + i);
-          if (a.act) v[i] = silu(v[i]);
-        }
-        if (!valid) continue;
-        if (a.residual != nullptr) {
-          const uint4* rp = reinterpret_cast<const uint4*>(a.residual + tok * a.N + n0 + c);
+          for (int i = 0; i < 32; ++i) {
+            v[i] += __ldg(a.bias + n0 + c + i);
+            if (a.act) v[i] = silu(v[i]);
+          }
+          if (!valid) continue;
+          if (a.residual != nullptr) {
+            const uint4* rp = reinterpret_cast<const uint4*>(a.residual + tok * a.N + n0 + c);
 #pragma unroll
-          for (int qq = 0; qq < 4; ++qq) {
-            uint4 uu = __ldg(rp + qq);
-            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&uu);
+            for (int qq = 0; qq < 4; ++qq) {
+              uint4 uu = __ldg(rp + qq);
+              const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&uu);
 #pragma unroll
-            for (int e2 = 0; e2 < 4; ++e2) {
-              float2 f = __bfloat1622float2(h2[e2]);
-              v[qq * 8 + 2 * e2] += f.x;
-              v[qq * 8 + 2 * e2 + 1] += f.y;
+              for (int e2 = 0; e2 < 4; ++e2) {
+                float2 f = __bfloat1622float2(h2[e2]);
+                v[qq * 8 + 2 * e2] += f.x;
+                v[qq * 8 + 2 * e2 + 1] += f.y;
+              }
             }
           }
-        }
-        uint4* op = reinterpret_cast<uint4*>(outp + c);
+          uint4* op = reinterpret_cast<uint4*>(outp + c);
 #pragma unroll
-        for (int qq = 0; qq < 4; ++qq) {
-          uint4 uu;
-          __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&uu);
+          for (int qq = 0; qq < 4; ++qq) {
+            uint4 uu;
+            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&uu);
 #pragma unroll
-          for (int e2 = 0; e2 < 4; ++e2)
-            h2[e2] = __floats2bfloat162_rn(v[qq * 8 + 2 * e2], v[qq * 8 + 2 * e2 + 1]);
-          op[qq] = uu;
+            for (int e2 = 0; e2 < 4; ++e2)
+              h2[e2] = __floats2bfloat162_rn(v[qq * 8 + 2 * e2], v[qq * 8 + 2 * e2 + 1]);
+            op[qq] = uu;
+          }
         }
       }
     }
@@ -1201,7 +1199,7 @@ __global__ void __launch_bounds__(128)
   const int wins_x = ceil_div(Wt, ATT_WIN);
   const int wy = blockIdx.x / wins_x, wx = blockIdx.x - wy * wins_x;
   const int head = blockIdx.y, g = blockIdx.z;
-  const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+  const int t = threadIdx.x, warp = t >> 5;
   const int ft = t >> 6, lt = t & 63;
   const int y = wy * ATT_WIN + (lt >> 3), x = wx * ATT_WIN + (lt & 7);
   const bool valid = y < Ht && x < Wt;
