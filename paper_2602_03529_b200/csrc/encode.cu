@@ -25,7 +25,10 @@ struct EncCfg {
   static constexpr int R = 8 * S;                   // full-res rows per tile
   static constexpr int IN = TPB * 8 * S * 3;        // floats per tile row
   static constexpr int NT = 64 * TPB;               // one thread per working pixel
-  static constexpr int NST = 4;                     // TMA ring depth
+  // TMA ring depth: s=3 tiles are 20 KB, and a 4-deep ring (83 KB) capped
+  // residency at 2 CTAs / SM; 3 deep (62 KB, 3 CTAs) runs K1 at 7.2 instead
+  // of 6.75 TB/s (scripts/k1_micro.py: 0.99 vs 1.06 ms per 32 GoPs)
+  static constexpr int NST = (S == 3) ? 3 : 4;
   static constexpr int TILE = R * IN;               // floats per tile
   static constexpr int RING_BYTES = NST * TILE * 4;
   static constexpr int IMG_D = 2 * 8 * 8 * TPB * 3;            // imgbuf doubles
