@@ -1807,16 +1807,14 @@ template <int S>
 __global__ void k_lt_patchify(const float* __restrict__ src, int G, int H, int W, int h, int w,
                               int Ht, int Wt, __nv_bfloat16* __restrict__ pI,
                               __nv_bfloat16* __restrict__ pP) {
-  const int PW = Wt * 8, PH = Ht * 8;
-  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t total = (int64_t)G * 9 * PH * PW;
-  if (idx >= total) return;
-  const int X = (int)(idx % PW);
-  int64_t rest = idx / PW;
-  const int Y = (int)(rest % PH);
-  rest /= PH;
-  const int f = (int)(rest % 9);
-  const int g = (int)(rest / 9);
+  // grid: x = 256-pixel column tiles of a padded row, y = padded row,
+  // z = frame (g * 9 + f): no 64-bit index divisions per pixel
+  const int PW = Wt * 8;
+  const int X = blockIdx.x * blockDim.x + threadIdx.x;
+  if (X >= PW) return;
+  const int Y = blockIdx.y;
+  const int f = (int)(blockIdx.z % 9);
+  const int g = (int)(blockIdx.z / 9);
   const int xc = min(X, w - 1), yc = min(Y, h - 1);  // np.pad(mode="edge") of the working frame
   const float* fr = src + ((int64_t)g * 9 + f) * (int64_t)H * W * 3;
   float px[3];
@@ -2168,16 +2166,16 @@ extern "C" int sst_lt_patchify(const float* frames, int G, int H, int W, int s, 
   if (s < 1 || s > 3) return SST_ERR_ARG;
   const int h = ceil_div(H, s), w = ceil_div(W, s);
   const int Ht = ceil_div(h, 8), Wt = ceil_div(w, 8);
-  const int64_t total = (int64_t)G * 9 * Ht * 8 * Wt * 8;
   const int threads = 256;
-  const int64_t blocks = ceil_div64(total, threads);
+  if ((int64_t)G * 9 > 65535 || Ht * 8 > 65535) return SST_ERR_ARG;
+  const dim3 blocks(ceil_div(Wt * 8, threads), Ht * 8, G * 9);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   auto* i = static_cast<__nv_bfloat16*>(pI);
   auto* p = static_cast<__nv_bfloat16*>(pP);
   switch (s) {
-    case 1: lt::k_lt_patchify<1><<<(unsigned)blocks, threads, 0, st>>>(frames, G, H, W, h, w, Ht, Wt, i, p); break;
-    case 2: lt::k_lt_patchify<2><<<(unsigned)blocks, threads, 0, st>>>(frames, G, H, W, h, w, Ht, Wt, i, p); break;
-    default: lt::k_lt_patchify<3><<<(unsigned)blocks, threads, 0, st>>>(frames, G, H, W, h, w, Ht, Wt, i, p); break;
+    case 1: lt::k_lt_patchify<1><<<blocks, threads, 0, st>>>(frames, G, H, W, h, w, Ht, Wt, i, p); break;
+    case 2: lt::k_lt_patchify<2><<<blocks, threads, 0, st>>>(frames, G, H, W, h, w, Ht, Wt, i, p); break;
+    default: lt::k_lt_patchify<3><<<blocks, threads, 0, st>>>(frames, G, H, W, h, w, Ht, Wt, i, p); break;
   }
   SST_LAUNCH_CHECK();
   return SST_OK;
