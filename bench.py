@@ -54,7 +54,14 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--streams", type=int, default=64, help="streams per GPU")
+    ap.add_argument("--streams", type=int, default=64,
+                    help="streams per GPU (--scaling weak) or in total (--scaling strong)")
+    ap.add_argument("--scaling", choices=("weak", "strong"), default="weak",
+                    help="weak: every GPU codes --streams streams (ids rank*S+i); strong: "
+                         "--streams streams in total, stream_id %% N == rank (BASELINE configs[4])")
+    ap.add_argument("--selftest-launcher", action="store_true",
+                    help="CPU test hook: run the N-rank launch / sharding / max-over-ranks / "
+                         "reporting path over gloo without GPU work")
     ap.add_argument("--lanes", type=int, default=2,
                     help="independent StreamBanks, each on its own CUDA stream (even)")
     ap.add_argument("--height", type=int, default=1080)
@@ -74,11 +81,13 @@ def parse_args():
 
 
 def workload_config(a) -> dict:
+    per = "per GPU" if a.scaling == "weak" else "in total, sharded stream_id % N"
     return {
-        "workload": f"{a.streams} concurrent {a.height}p streams per GPU, variable-resolution "
+        "workload": f"{a.streams} concurrent {a.height}p streams {per}, variable-resolution "
                     f"(scales {SCALE_PATTERN} per stream, half the streams at each scale), "
                     f"{int(a.drop * 100)}% intelligent P-token drop, blend n=2, no network loss",
-        "streams_per_gpu": a.streams,
+        "streams": a.streams,
+        "streams_are": "per GPU" if a.scaling == "weak" else "total",
         "frame": [a.height, a.width, 3],
         "frame_dtype": "float32 in / float32 out (reference Frame dtype)",
         "gop_frames": GOP,
@@ -217,15 +226,48 @@ def make_inputs(stream_ids, H, W, device, n_sets=2):
 # ---------------------------------------------------------------------------
 # our arm
 
+def _coll_device(dev):
+    """Collectives run on the GPU under NCCL, on host tensors under gloo (the
+    SST_BENCH_SHARE_GPU hook and the CPU launcher self-test)."""
+    import torch.distributed as dist
+    return dev if dist.get_backend() == "nccl" else "cpu"
+
+
 def max_over_ranks(ms: float, dev) -> float:
-    """Device-timed step time, max over ranks (NCCL on the GPUs; a host tensor
-    when the group is gloo -- the SST_BENCH_SHARE_GPU test hook)."""
+    """Device-timed step time, max over ranks (paper_2602_03529_b200.shard)."""
+    from paper_2602_03529_b200.shard import max_over_ranks as _max
+    return _max(ms, _coll_device(dev))
+
+
+def gather_ranks(values, dev) -> list:
+    """Every rank's small float vector (per-rank timing / stream counts), for
+    the report only -- no collective touches the data path."""
     import torch
     import torch.distributed as dist
-    on_dev = dist.get_backend() == "nccl"
-    t = torch.tensor([ms], dtype=torch.float64, device=dev if on_dev else "cpu")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return [list(values)]
+    t = torch.tensor(list(values), dtype=torch.float64, device=_coll_device(dev))
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return [[float(v) for v in o.cpu()] for o in out]
+
+
+def my_streams(a, rank: int, world: int, per: int | None = None) -> list:
+    """This rank's stream ids: weak scaling = its own
+    ``per`` streams (rank*per + i), strong = stream_id % world == rank out of
+    ``per`` in total."""
+    from paper_2602_03529_b200.shard import rank_streams, strong_streams
+    per = a.streams if per is None else per
+    if a.scaling == "weak":
+        return rank_streams(rank, world, per)
+    if per < world:
+        raise SystemExit(f"--scaling strong needs at least one stream per rank ({per} < {world})")
+    return strong_streams(rank, world, per)
+
+
+def total_streams(a, world: int, per: int | None = None) -> int:
+    per = a.streams if per is None else per
+    return per * world if a.scaling == "weak" else per
 
 
 def run_ours(a, rank, world, local_rank):
@@ -237,17 +279,20 @@ def run_ours(a, rank, world, local_rank):
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    S, H, W = a.streams, a.height, a.width
+    mine = my_streams(a, rank, world)
+    S, H, W = len(mine), a.height, a.width
     # Two lanes of streams: the even-phase streams and the odd-phase streams
     # (their scale patterns are offset by two GoPs, so at every step one lane
     # codes at s=3 and the other at s=2).  Each lane is an independent
     # StreamBank on its own CUDA stream: no dependency crosses lanes, so one
     # lane's latency-bound middle kernels overlap the other's HBM-bound
-    # encode / reconstruction, and lanes are only joined at the end.
+    # encode / reconstruction, and lanes are only joined at the end.  The
+    # phase alternates over the rank's own streams, so every GPU codes half
+    # of its streams at each scale in either scaling mode.
     even = [i for i in range(S) if i % 2 == 0]
     odd = [i for i in range(S) if i % 2 == 1]
     ne = len(even)
-    inputs = make_inputs([rank * S + i for i in even + odd], H, W, dev)
+    inputs = make_inputs([mine[i] for i in even + odd], H, W, dev)
     out = torch.empty_like(inputs[0])
     lanes = []
     per = max(1, a.lanes // 2)                  # lanes per phase
@@ -321,6 +366,7 @@ def run_ours(a, rank, world, local_rank):
     ms_max = ms
     if world > 1:
         ms_max = max_over_ranks(ms, dev)
+    per_rank = gather_ranks([ms, S], dev)
     launches = bank.launches - launches0
     # Per-kernel roofline: a few extra steps with the lanes serialised on one
     # stream so that every kernel's CUDA-event duration is its own (in the
@@ -336,7 +382,8 @@ def run_ours(a, rank, world, local_rank):
     torch.cuda.synchronize()
     bank.set_timer(None)
     stages = timer.summary()
-    frames_total = S * GOP * a.steps * world
+    frames_total = total_streams(a, world) * GOP * a.steps
+    assert frames_total == sum(int(n) for _, n in per_rank) * GOP * a.steps
     value = frames_total / (ms_max / 1000.0)
 
     # quality of one GoP per scale vs the source (device metric)
@@ -348,7 +395,10 @@ def run_ours(a, rank, world, local_rank):
         psnr[f"s{s}"] = 99.0 if mse <= 0 else min(99.0, 10 * np.log10(1.0 / mse))
 
     res = dict(ms=ms_max, value=value, stages=stages, launches=launches,
-               clocks=clocks.summary(), psnr=psnr)
+               clocks=clocks.summary(), psnr=psnr,
+               per_rank=[{"rank": r, "streams": int(n), "ms": round(m, 3),
+                          "frames_per_s": round(n * GOP * a.steps / (m / 1000.0), 1)}
+                         for r, (m, n) in enumerate(per_rank)])
     res["roofline"] = roofline(a, stages, S // len(lanes), a.roofline_steps * len(lanes))
     if not a.no_e2e:
         del inputs, out
@@ -423,10 +473,11 @@ def run_e2e(a, rank, world, local_rank) -> dict:
     from paper_2602_03529_b200.pipeline import StreamBank
 
     dev = torch.device("cuda", local_rank)
-    E, H, W = a.e2e_streams, a.height, a.width
+    mine = my_streams(a, rank, world, a.e2e_streams)
+    E, H, W = len(mine), a.height, a.width
     lanes = max(1, min(int(os.environ.get("SST_E2E_LANES", "8")), E))   # one stream per lane
     per = [list(range(E))[i::lanes] for i in range(lanes)]
-    src_dev = make_inputs([rank * E + i for i in range(E)], H, W, dev, n_sets=1)[0]
+    src_dev = make_inputs(mine, H, W, dev, n_sets=1)[0]
     fshape = tuple(src_dev.shape[1:])
     L = []
     for ids in per:
@@ -506,94 +557,199 @@ def run_e2e(a, rank, world, local_rank) -> dict:
     ms = t0.elapsed_time(t1)
     if world > 1:
         ms = max_over_ranks(ms, dev)
-    # the outputs really arrived: spot-check one host frame against the device
-    frames = E * GOP * a.steps * world
+    frames = total_streams(a, world, a.e2e_streams) * GOP * a.steps
     return {"value": round(frames / (ms / 1000.0), 2), "unit": UNIT,
             "h2d_bytes_per_step": int(counters["h2d"] // a.steps),
             "d2h_bytes_per_step": int(counters["d2h"] // a.steps),
-            "streams_per_gpu": E, "lanes": lanes, "wall_s": round(wall, 3),
+            "streams": total_streams(a, world, a.e2e_streams), "streams_this_rank": E,
+            "lanes": lanes, "wall_s": round(wall, 3),
             "path": "StreamBank public API on pinned host frames: frames H2D, packets D2H + "
                     "H2D (network boundary), frames D2H, all inside the timed region; "
                     f"{lanes} CUDA-stream lanes overlap PCIe directions with compute"}
 
 
 # ---------------------------------------------------------------------------
-# CPU reference (oracle port of the reference algorithm)
+# CPU reference: the UNMODIFIED reference package installed in baseline/_ref
+# (python -m pip install --no-index --no-build-isolation --no-deps --target
+# baseline/_ref <copy of /root/reference/pkg>; git-ignored, travels with the
+# snapshot) run through its own public API; the oracle port only when that
+# install is absent.
+
+REF_DIR = ROOT / "baseline" / "_ref"
+
+
+def reference_kind() -> str:
+    return "reference" if (REF_DIR / "semstream" / "__init__.py").is_file() else "port"
+
 
 def _init_worker():
     for v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
         os.environ[v] = "1"
+    if str(REF_DIR) not in sys.path:
+        sys.path.insert(0, str(REF_DIR))
 
 
 _CLIP_CACHE: dict = {}
+_PREV_OUT: dict = {}
 
 
-def _cpu_worker(job):
+def _ref_gop(H, W, sid, k, s, drop):
+    """One GoP through the stock reference composition (session.py:134-170
+    sender, 323-348 receiver, without the emulated network): scale_gop(down)
+    -> encode_gop -> token_similarity -> build_drop_mask -> apply_token_mask
+    -> packetize_tokens -> to_bytes -> parse_packet -> reassemble x2 ->
+    decode_gop -> scale_gop(up, crop) -> blend_boundary(n=2) against the
+    worker's previous output.  Returns (compute seconds, PSNR dB)."""
+    from semstream import codec, selection, synth, transport, video
+    key = ("ref", H, W, sid, k)
+    if key not in _CLIP_CACHE:          # clip generation is not part of the timed work
+        name = "moving-square" if sid % 2 == 0 else "noisy-motion"
+        _CLIP_CACHE.clear()
+        _CLIP_CACHE[key] = synth.make_clip(name, W, H, GOP * (k + 1), seed=sid).gop(k)
+    gop = _CLIP_CACHE[key]
+    t0 = time.perf_counter()
+    cfg = codec.CodecConfig()
+    working = codec.scale_gop(gop, s, "down")
+    i_tok, p_tok = codec.encode_gop(working, cfg)
+    if drop > 0.0:
+        sim = selection.token_similarity(p_tok, i_tok)
+        p_tok = codec.apply_token_mask(p_tok, selection.build_drop_mask(sim, drop))
+    wire = [p.to_bytes() for p in transport.packetize_tokens(i_tok, scale=s)
+            + transport.packetize_tokens(p_tok, scale=s)]
+    parsed = [transport.parse_packet(d) for d in wire]
+    shape = i_tok.values.shape
+    ri = transport.reassemble([p for p in parsed if p.kind == "I"], shape, "I", gop_id=k,
+                              frame_shape=i_tok.frame_shape)
+    rp = transport.reassemble([p for p in parsed if p.kind == "P"], shape, "P", gop_id=k,
+                              frame_shape=i_tok.frame_shape)
+    recon = codec.scale_gop(codec.decode_gop(ri, rp, cfg), s, "up", crop=(H, W))
+    prev = _PREV_OUT.get((H, W))
+    if prev is not None:
+        recon = codec.blend_boundary(prev, recon, 2)
+    dt = time.perf_counter() - t0
+    _PREV_OUT[(H, W)] = recon
+    return dt, video.gop_psnr(gop, recon)[0]
+
+
+def _port_gop(H, W, sid, k, s, drop):
     from oracle import semstream_oracle as O
     from oracle.synth import make_clip
-    H, W, sid, k, s, drop = job
-    key = (H, W, sid, k)
-    if key not in _CLIP_CACHE:          # clip generation is not part of the timed work
+    key = ("port", H, W, sid, k)
+    if key not in _CLIP_CACHE:
         name = "moving-square" if sid % 2 == 0 else "noisy-motion"
         _CLIP_CACHE.clear()
         _CLIP_CACHE[key] = make_clip(name, W, H, GOP * (k + 1), seed=sid).gop(k)
     frames = _CLIP_CACHE[key]
     t0 = time.perf_counter()
-    res = O.pipeline_gop(frames, s, gop_id=k, drop_rate=drop)
+    res = O.pipeline_gop(frames, s, gop_id=k, drop_rate=drop, prev_out=_PREV_OUT.get((H, W)))
     dt = time.perf_counter() - t0
-    psnr, _ = O.gop_psnr(list(frames), res["frames"])
-    return dt, psnr
+    _PREV_OUT[(H, W)] = res["frames"]
+    return dt, O.gop_psnr(list(frames), res["frames"])[0]
 
 
-def cpu_workers(a) -> int:
-    if a.cpu_workers:
-        return a.cpu_workers
-    n = os.cpu_count() or 1
+def _cpu_worker(job):
+    H, W, sid, k, s, drop, kind = job
+    return (_ref_gop if kind == "reference" else _port_gop)(H, W, sid, k, s, drop)
+
+
+def host_info() -> dict:
+    """What the CPU arm ran on (nproc, CPU model, library versions)."""
+    info = {"nproc": os.cpu_count()}
     try:
-        import psutil
-        mem = psutil.virtual_memory().available
-        n = min(n, max(1, int(mem // (3 * 1024 ** 3))))     # ~3 GB per 1080p GoP worker
+        info["affinity_cores"] = len(os.sched_getaffinity(0))
     except Exception:
         pass
-    return max(1, min(n, 64))
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                info["cpu_model"] = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    try:
+        import numpy
+        import scipy
+        info["numpy"], info["scipy"] = numpy.__version__, scipy.__version__
+    except Exception:
+        pass
+    try:
+        import psutil
+        info["mem_available_gb"] = round(psutil.virtual_memory().available / 1e9, 1)
+    except Exception:
+        pass
+    info["python"] = sys.version.split()[0]
+    return info
 
 
-def cpu_sample(a, steps: int, warm: int = 0):
-    """Time `steps` rounds of one GoP per worker; returns per-round wall times."""
+def cpu_workers(a) -> tuple:
+    """(workers, why): every host core the process may use, capped only by
+    memory (~1.2 GB peak RSS per 1080p GoP worker, measured: 0.66 GB for the
+    reference pipeline plus the cached clip) and 128."""
+    if a.cpu_workers:
+        return a.cpu_workers, "--cpu-workers"
+    try:
+        n = len(os.sched_getaffinity(0))
+    except Exception:
+        n = os.cpu_count() or 1
+    why = "all host cores"
+    try:
+        import psutil
+        per = 1.2e9 * (a.height * a.width) / (1080 * 1920)
+        cap = max(1, int(psutil.virtual_memory().available // max(per, 1e8)))
+        if cap < n:
+            n, why = cap, f"memory cap ({per / 1e9:.1f} GB per worker)"
+    except Exception:
+        pass
+    if n > 128:
+        n, why = 128, "capped at 128"
+    return max(1, n), why
+
+
+def cpu_sample(a, steps: int, warm: int = 0, kind: str | None = None):
+    """`steps` timed rounds of one GoP per worker process (pool wall clock per
+    round, clip generation excluded: every worker's clip is materialised by an
+    untimed round first).  Returns (workers, why, kind, round walls, psnrs)."""
     import multiprocessing as mp
-    n = cpu_workers(a)
+    kind = kind or reference_kind()
+    n, why = cpu_workers(a)
     ctx = mp.get_context("spawn")
-    walls = []
-    psnrs = []
+    walls, psnrs = [], []
     with ctx.Pool(n, initializer=_init_worker) as pool:
-        # one untimed round materialises every worker's input clip
-        pool.map(_cpu_worker, [(a.height, a.width, i, 0, scale_of(i, 0), a.drop) for i in range(n)],
-                 chunksize=1)
+        pool.map(_cpu_worker, [(a.height, a.width, i, 0, scale_of(i, 0), a.drop, kind)
+                               for i in range(n)], chunksize=1)
         for r in range(warm + steps):
-            jobs = [(a.height, a.width, i, 0, scale_of(i, r), a.drop) for i in range(n)]
+            jobs = [(a.height, a.width, i, 0, scale_of(i, r), a.drop, kind) for i in range(n)]
+            t0 = time.perf_counter()
             out = pool.map(_cpu_worker, jobs, chunksize=1)
+            wall = time.perf_counter() - t0
             if r >= warm:
-                # core-seconds spread over the n workers (each runs its GoP
-                # single-threaded; clip generation excluded)
-                walls.append(sum(dt for dt, _ in out) / n)
+                walls.append(wall)
                 psnrs.extend(p for _, p in out)
-    return n, walls, psnrs
+    return n, why, kind, walls, psnrs
+
+
+def _cpu_record(a, n, why, kind, walls) -> dict:
+    what = ("the unmodified reference package (baseline/_ref semstream, its public API)"
+            if kind == "reference" else "oracle/semstream_oracle.py (port; baseline/_ref absent)")
+    return {"value": round(n * GOP * len(walls) / sum(walls), 3), "unit": UNIT, "cores": n,
+            "kind": kind, "workers_why": why, "host": host_info(),
+            "sample": f"{len(walls)} round(s) x {n} worker processes x one {a.height}p GoP each "
+                      f"(9 frames, scales {sorted({scale_of(i, 0) for i in range(n)})}, "
+                      f"{int(a.drop * 100)}% drop, blend n=2), {what}; throughput from the "
+                      f"pool's wall clock per round ({sum(walls):.1f} s total), one thread per "
+                      f"worker (OMP/OPENBLAS/MKL_NUM_THREADS=1)"}
 
 
 def run_reference(a) -> dict:
-    n, walls, psnrs = cpu_sample(a, a.steps, a.warmup)
-    total = sum(walls)
-    value = n * GOP * a.steps / total
-    return dict(value=value, ms=1000 * total / a.steps, cores=n, psnr=statistics.mean(psnrs))
+    n, why, kind, walls, psnrs = cpu_sample(a, a.steps, a.warmup)
+    rec = _cpu_record(a, n, why, kind, walls)
+    return dict(value=rec["value"], ms=1000 * sum(walls) / len(walls), record=rec,
+                psnr=statistics.mean(psnrs))
 
 
 def cpu_baseline(a) -> dict:
-    n, walls, _ = cpu_sample(a, 1, 0)
-    return {"value": round(n * GOP / walls[0], 3), "unit": UNIT, "cores": n, "kind": "port",
-            "sample": f"{n} worker processes x one {a.height}p GoP each (9 frames, "
-                      f"scales {sorted({scale_of(i, 0) for i in range(n)})}, "
-                      f"{int(a.drop * 100)}% drop), oracle/semstream_oracle.py pipeline_gop, "
-                      f"wall {walls[0]:.1f} s"}
+    n, why, kind, walls, _ = cpu_sample(a, 1, 1)
+    return _cpu_record(a, n, why, kind, walls)
 
 
 def single_stream_latency(a, device) -> dict:
@@ -662,6 +818,7 @@ def loss_legs(a, device) -> dict:
 
     from oracle import semstream_oracle as O
     from paper_2602_03529_b200.pipeline import GopCodec
+    from paper_2602_03529_b200.video import gop_psnr_device
     H, W, s, G = a.height, a.width, 3, 32
     frames = make_inputs(list(range(G)), H, W, device, n_sets=1)[0]
     out = torch.empty_like(frames)
@@ -698,7 +855,7 @@ def loss_legs(a, device) -> dict:
         ref = O.pipeline_gop(src, s, gop_id=0, drop_rate=rate if kind == "drop" else 0.0,
                              lost=lost0)
         gpu = out[0].cpu().numpy()
-        p_gpu, _ = O.gop_psnr(list(src), list(gpu))
+        p_gpu, _ = gop_psnr_device(frames[0], out[0])          # GPU metric kernel
         p_ref, _ = O.gop_psnr(list(src), list(ref["frames"]))
         res[f"{kind}_{int(rate * 100)}pct"] = {
             "frames_per_s": round(G * GOP / ms * 1e3, 1),
@@ -794,15 +951,45 @@ def small_configs(a, device) -> dict:
     return out
 
 
+def cpu_reference_gop(src, s: int, drop: float, gop_id: int = 0):
+    """(frames [9,H,W,3], psnr_db, kind): one GoP through the unmodified
+    reference (baseline/_ref) when installed, else the oracle port; PSNR by
+    the reference's own gop_psnr."""
+    import numpy as np
+    if reference_kind() == "reference":
+        _init_worker()
+        from semstream import codec, selection, transport, video
+        gop = video.GoP(gop_id, tuple(video.Frame(f, timestamp_index=t) for t, f in enumerate(src)))
+        cfg = codec.CodecConfig()
+        working = codec.scale_gop(gop, s, "down")
+        i_tok, p_tok = codec.encode_gop(working, cfg)
+        if drop > 0.0:
+            p_tok = codec.apply_token_mask(p_tok, selection.build_drop_mask(
+                selection.token_similarity(p_tok, i_tok), drop))
+        parsed = [transport.parse_packet(p.to_bytes()) for p in
+                  transport.packetize_tokens(i_tok, scale=s) + transport.packetize_tokens(p_tok, scale=s)]
+        sh = i_tok.values.shape
+        ri = transport.reassemble([p for p in parsed if p.kind == "I"], sh, "I", gop_id=gop_id,
+                                  frame_shape=i_tok.frame_shape)
+        rp = transport.reassemble([p for p in parsed if p.kind == "P"], sh, "P", gop_id=gop_id,
+                                  frame_shape=i_tok.frame_shape)
+        rec = codec.scale_gop(codec.decode_gop(ri, rp, cfg), s, "up", crop=src.shape[1:3])
+        return np.stack([f.samples for f in rec.frames]), video.gop_psnr(gop, rec)[0], "reference"
+    from oracle import semstream_oracle as O
+    frames = np.stack(O.pipeline_gop(src, s, gop_id=gop_id, drop_rate=drop)["frames"])
+    return frames, O.gop_psnr(list(src), list(frames))[0], "port"
+
+
 def parity_sample(a, device) -> dict:
-    """PSNR delta vs the CPU reference algorithm on one full-size GoP: the same
-    synthetic 1080p GoP through the GPU path and through the oracle port."""
+    """PSNR delta vs the CPU reference on one full-size GoP: the same
+    synthetic 1080p GoP through the GPU path (PSNR by the GPU metric kernel,
+    csrc/metrics.cu) and through the reference (PSNR by its gop_psnr)."""
     import numpy as np
     import torch
 
-    from oracle import semstream_oracle as O
     from oracle.synth import make_clip
     from paper_2602_03529_b200.pipeline import StreamBank
+    from paper_2602_03529_b200.video import gop_psnr_device
 
     src = make_clip("moving-square", a.width, a.height, GOP, seed=0).gop(0)
     s = scale_of(0, 0)
@@ -810,12 +997,11 @@ def parity_sample(a, device) -> dict:
     fr = torch.from_numpy(src[None].copy()).to(device)
     out = torch.empty_like(fr)
     bank.step({s: fr}, {s: out}, {s: [0]}, {s: [0]}, drop_rate=a.drop)
+    p_gpu, _ = gop_psnr_device(fr[0], out[0])
     gpu = out.cpu().numpy()[0]
-    ref = np.stack(O.pipeline_gop(src, s, gop_id=0, drop_rate=a.drop)["frames"])
-    p_gpu, _ = O.gop_psnr(list(src), list(gpu))
-    p_ref, _ = O.gop_psnr(list(src), list(ref))
+    ref, p_ref, kind = cpu_reference_gop(src, s, a.drop)
     return {"sample": f"moving-square {a.height}p GoP, s={s}, {int(a.drop * 100)}% drop",
-            "psnr_gpu_db": round(p_gpu, 6), "psnr_cpu_ref_db": round(p_ref, 6),
+            "cpu_side": kind, "psnr_gpu_db": round(p_gpu, 6), "psnr_cpu_ref_db": round(p_ref, 6),
             "psnr_delta_db": p_gpu - p_ref,
             "max_abs_diff": float(np.abs(gpu.astype(np.float64) - ref).max()),
             "bit_exact": bool(np.array_equal(gpu, ref))}
@@ -979,30 +1165,96 @@ def run_learned(a, device) -> dict:
     }
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(a) -> int:
+    """`python bench.py --gpus N` (N > 1) without a torchrun environment:
+    re-execute this script under torch.distributed.run with N local ranks
+    (one process per GPU, rendezvous on 127.0.0.1) and pass its exit status
+    through.  Rank 0 prints the JSON line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={a.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", str(Path(__file__).resolve())] + sys.argv[1:]
+    print(f"[bench] launching {a.gpus} ranks: {' '.join(cmd[1:6])} ...", file=sys.stderr,
+          flush=True)
+    import subprocess
+    return subprocess.call(cmd, env=dict(os.environ, OMP_NUM_THREADS="1"))
+
+
+def comm_info(world: int, dev) -> dict:
+    import torch
+    import torch.distributed as dist
+    info = {"world_size": world, "backend": dist.get_backend() if world > 1 else None,
+            "data_path_collectives": 0,
+            "collectives": "barrier + max-over-ranks step time + per-rank timing gather"}
+    try:
+        v = torch.cuda.nccl.version()
+        info["nccl_version"] = ".".join(str(x) for x in v) if isinstance(v, tuple) else v
+    except Exception:
+        pass
+    return info
+
+
+def selftest_launcher(a, rank, world) -> None:
+    """CPU path of the N-rank bench (tests/test_bench_cpu.py): gloo rendezvous,
+    stream sharding, max-over-ranks of a synthetic per-rank step time, the
+    per-rank gather and the JSON line -- everything but the GPU work."""
+    import torch.distributed as dist
+    if world > 1:
+        dist.init_process_group("gloo")
+    mine = my_streams(a, rank, world)
+    ms = 10.0 + rank                                   # rank r "takes" 10 + r ms
+    ms_max = max_over_ranks(ms, "cpu") if world > 1 else ms
+    per_rank = gather_ranks([ms, len(mine), sum(mine)], "cpu")
+    if rank == 0:
+        frames = total_streams(a, world) * GOP * a.steps
+        line = {"metric": METRIC, "value": round(frames / (ms_max / 1000.0), 2), "unit": UNIT,
+                "n_gpus": world, "steps": a.steps, "warmup": a.warmup, "scaling": a.scaling,
+                "selftest": True, "ms_max": ms_max, "comm": comm_info(world, "cpu"),
+                "per_rank": [{"rank": r, "ms": v[0], "n_streams": int(v[1]),
+                              "stream_id_sum": int(v[2])} for r, v in enumerate(per_rank)]}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
 def main():
     a = parse_args()
+    in_launch = "WORLD_SIZE" in os.environ
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    base = {"metric": METRIC, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
-            "warmup": a.warmup, "higher_is_better": True, "scaling": "weak",
+    if a.gpus < 1:
+        raise SystemExit("--gpus must be >= 1")
+    if in_launch and world != a.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {a.gpus}: refusing to "
+                         f"report a {a.gpus}-GPU number from {world} rank(s)")
+    if a.gpus > 1 and not in_launch and a.impl == "ours":
+        sys.exit(self_launch(a))
+    if a.selftest_launcher:
+        return selftest_launcher(a, rank, world)
+    base = {"metric": METRIC, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "higher_is_better": True, "scaling": a.scaling,
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(a)}
 
     if a.impl == "reference":
+        # the reference is a CPU package: rank 0 alone runs it on the host cores
         if rank != 0:
             return
         r = run_reference(a)
-        line = dict(base, impl="reference", value=round(r["value"], 3),
-                    ms_per_step=round(r["ms"], 2),
-                    cpu_baseline={"value": round(r["value"], 3), "unit": UNIT,
-                                  "cores": r["cores"], "kind": "port",
-                                  "sample": f"{r['cores']} processes x one {a.height}p GoP per "
-                                            f"step, oracle port of the reference algorithm"},
-                    e2e={"value": round(r["value"], 3), "unit": UNIT,
+        rec = r["record"]
+        line = dict(base, impl="reference", value=rec["value"],
+                    ms_per_step=round(r["ms"], 2), cpu_baseline=rec,
+                    e2e={"value": rec["value"], "unit": UNIT,
                          "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
                     psnr_db=round(r["psnr"], 3))
-        line["config"] = dict(line["config"], streams_per_step=r["cores"])
         print(json.dumps(line), flush=True)
         return
 
@@ -1012,14 +1264,19 @@ def main():
     # and rendezvous over gloo, so the N>1 control flow (barriers, max-over-ranks,
     # stream sharding) can be exercised on a one-GPU box.  Never used by the driver.
     share = os.environ.get("SST_BENCH_SHARE_GPU") == "1"
+    ngpu = torch.cuda.device_count()
+    if not share and world > ngpu:
+        raise SystemExit(f"bench.py: {world} ranks but only {ngpu} visible GPU(s); "
+                         f"one process per GPU is required")
     if share:
-        local_rank = local_rank % torch.cuda.device_count()
+        local_rank = local_rank % ngpu
     torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
     if world > 1:
         if share:
             dist.init_process_group("gloo")
         else:
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+            dist.init_process_group("nccl", device_id=dev)
     res = run_ours(a, rank, world, local_rank)
     if rank == 0:
         line = dict(base, value=round(res["value"], 2), ms_per_step=round(res["ms"] / a.steps, 3),
@@ -1027,18 +1284,21 @@ def main():
                     clocks=res["clocks"],
                     stages={k: {"ms_per_launch": round(v[0] / v[1], 4), "launches": v[1]}
                             for k, v in res["stages"].items()},
-                    path_roofline=path_roofline(a, res["value"]),
-                    psnr_db=res["psnr"])
+                    path_roofline=path_roofline(a, res["value"] / world),
+                    psnr_db=res["psnr"], per_rank=res["per_rank"],
+                    comm=comm_info(world, dev))
+        if share and world > 1:
+            line["shared_gpu_test_hook"] = True
         line["e2e"] = res.get("e2e")
         if world == 1 and not a.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(a)
-            line["parity"] = parity_sample(a, torch.device("cuda", local_rank))
-            line["single_stream"] = single_stream_latency(a, torch.device("cuda", local_rank))
-            line["loss_recovery"] = loss_legs(a, torch.device("cuda", local_rank))
+            line["parity"] = parity_sample(a, dev)
+            line["single_stream"] = single_stream_latency(a, dev)
+            line["loss_recovery"] = loss_legs(a, dev)
             if a.height == 1080 and a.width == 1920:
-                line["small_configs"] = small_configs(a, torch.device("cuda", local_rank))
+                line["small_configs"] = small_configs(a, dev)
         if world == 1 and not a.no_learned:
-            line["learned_tokenizer"] = run_learned(a, torch.device("cuda", local_rank))
+            line["learned_tokenizer"] = run_learned(a, dev)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

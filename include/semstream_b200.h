@@ -44,11 +44,11 @@ extern "C" {
 /* call status */
 #define SST_OK 0
 #define SST_ERR_ARG (-1)         /* bad shape / scale / pointer */
-#define SST_ERR_ROWS_16BIT (-2)  /* > 65535 token rows: transport.py:331-333 "16-bit" */
+#define SST_ERR_ROWS_16BIT (-2)  /* > 65535 token rows: transport.py:245-246 "16-bit" */
 #define SST_ERR_CUDA (-3)        /* CUDA runtime / launch failure */
 #define SST_ERR_UNSUPPORTED (-4) /* e.g. channel count the kernel does not handle */
 
-/* per-packet status (parse_packet, transport.py:151-157, 241-271; reassemble, 274-305) */
+/* per-packet status (parse_packet, transport.py:154-218; reassemble, 274-305) */
 #define SST_PKT_OK 0
 #define SST_PKT_SHORT 1        /* "packet shorter than its checksum" */
 #define SST_PKT_CRC 2          /* "crc32 mismatch" */
@@ -66,7 +66,7 @@ extern "C" {
 #define SST_PKT_DUP 14         /* duplicate row: a packet that arrived earlier wins */
 #define SST_PKT_SHAPE 15       /* width / channel count incompatible with the matrix */
 
-/* Parsed token-packet header (TokenPacket fields, transport.py:82-95). */
+/* Parsed token-packet header (TokenPacket fields, transport.py:83-95). */
 typedef struct SstPacketInfo {
   int32_t status;      /* SST_PKT_* */
   int32_t kind;        /* 0 = I, 1 = P */
@@ -93,7 +93,7 @@ typedef struct SstPrevDesc {
 
 SST_API int sst_abi_version(void);
 
-/* Wire size of one token packet: transport.py:308-313 token_packet_wire_size. */
+/* Wire size of one token packet: transport.py:221-226 token_packet_wire_size. */
 SST_API int64_t sst_packet_wire_size(int width_tokens, int channels, int valid_count);
 
 /* ---- scaling ------------------------------------------------------------ */
@@ -177,7 +177,7 @@ SST_API int sst_select_drop(const double* sim, double* tok, uint8_t* mask, int G
 
 /* ---- wire format -------------------------------------------------------- */
 
-/* packetize_tokens + TokenPacket.to_bytes (transport.py:323-358, 184-189):
+/* packetize_tokens + TokenPacket.to_bytes (transport.py:236-271, 97-102):
  * one sealed packet per token row, written to arena[(m*Ht + row)*slot].
  *   values [m][H'][W'][C], mask [m][H'][W'] (NULL = all valid); kind/gop_id/
  *   scale per matrix (DEVICE arrays, length m); lengths: int32 [m*H'].
@@ -186,7 +186,7 @@ SST_API int sst_packetize(const double* values, const uint8_t* mask, int m, int 
                   const uint8_t* kind, const uint32_t* gop_id, const uint8_t* scale,
                   uint8_t* arena, int64_t slot, int32_t* lengths, void* stream);
 
-/* TokenPacket.to_bytes for packets given field-wise (transport.py:184-189):
+/* TokenPacket.to_bytes for packets given field-wise (transport.py:97-102):
  *   info[n] supplies kind/gop/row/width/channels/scale/qmin/qrange/valid;
  *   mask bits (ceil(width/8) bytes, MSB first) at masks + mask_off[i];
  *   payload (valid*channels bytes) at payload + payload_off[i];
@@ -195,7 +195,7 @@ SST_API int sst_serialize(const SstPacketInfo* info, const uint8_t* masks, const
                   const uint8_t* payload, const int64_t* payload_off, int64_t n, uint8_t* out,
                   const int64_t* out_off, void* stream);
 
-/* parse_packet (transport.py:151-157, 241-271) for n packets at buf+off[i]
+/* parse_packet (transport.py:154-218) for n packets at buf+off[i]
  * of len[i] bytes.  present (NULL = all) marks delivered packets. */
 SST_API int sst_parse(const uint8_t* buf, const int64_t* off, const int32_t* len, const uint8_t* present,
               int64_t n, SstPacketInfo* info, void* stream);
@@ -362,7 +362,16 @@ SST_API int sst_lt_attn_fused(const void* h, const void* w_qkv, const float* b_q
 
 /* ---- metrics ------------------------------------------------------------ */
 
-/* mse (video.py:265-270) per frame pair: out[i] = mean((a-b)^2) in float64. */
+/* np.mean over `elems` float64 per-pixel differences of n frame pairs
+ * a[i], b[i] (float32 [n][elems]): mode 0 = (a-b)^2 (mse, video.py:265-270;
+ * gop_psnr's per-frame errors, video.py:318-322; the l2 flicker norm),
+ * mode 1 = |a-b| (boundary_flicker l1, video.py:285-304;
+ * inter_frame_consistency, video.py:307-315).  Summed in numpy's pairwise
+ * order from 0.0, divided by elems: bit-identical to the reference. */
+SST_API int sst_mean_diff(const float* a, const float* b, int64_t n, int64_t elems, int mode,
+                          double* out, void* stream);
+
+/* mse (video.py:265-270) per frame pair = sst_mean_diff mode 0. */
 SST_API int sst_mse(const float* a, const float* b, int64_t n, int64_t elems, double* out, void* stream);
 
 #ifdef __cplusplus

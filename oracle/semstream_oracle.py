@@ -17,7 +17,7 @@ results are bit-identical, not merely close:
 * similarity: numpy's pairwise summation order for 12 channels (8-way
   unrolled block then sequential tail) (selection.py:44-46);
 * quantiser: float64 ``rint`` half-to-even on (v - qmin32) * (255/qrange32)
-  (transport.py:339-347);
+  (transport.py:248-266);
 * bilinear: half-pixel centres, separate mul/add in the reference's order
   (codec.py:217-235);
 * blend: alpha * prev + (1 - alpha) * curr in float64 (codec.py:289-293).
@@ -234,7 +234,7 @@ def _crc(data: bytes) -> int:
 
 
 def quantize_row(vals: np.ndarray):
-    """Per-row quantiser (transport.py:337-353): returns (qmin32, qrange32, payload)."""
+    """Per-row quantiser (transport.py:248-266): returns (qmin32, qrange32, payload)."""
     if vals.size == 0:
         return 0.0, 0.0, b""
     qmin, qmax = row_min_max(vals)
@@ -263,7 +263,7 @@ def pack_row(kind: int, gop_id: int, row: int, values_row: np.ndarray,
 
 def packetize(kind: int, gop_id: int, values: np.ndarray, mask: np.ndarray,
               scale: int = 1) -> list[bytes]:
-    """All rows of one token matrix (transport.py:323-358)."""
+    """All rows of one token matrix (transport.py:236-271)."""
     h = values.shape[0]
     if h > 0xFFFF:
         raise ValueError(f"matrix has {h} rows; the row index field is 16-bit")
@@ -271,14 +271,14 @@ def packetize(kind: int, gop_id: int, values: np.ndarray, mask: np.ndarray,
 
 
 def wire_size(width: int, channels: int, valid: int | None = None) -> int:
-    """transport.py:308-313."""
+    """transport.py:221-226."""
     if valid is None:
         valid = width
     return HDR_SIZE + (width + 7) // 8 + valid * channels + 4
 
 
 def parse(data: bytes) -> dict:
-    """Token-packet parse + validation (transport.py:151-157, 241-271)."""
+    """Token-packet parse + validation (transport.py:154-184, _check_seal 64-70)."""
     if len(data) < 4:
         raise OraclePacketError("packet shorter than its checksum")
     body = data[:-4]
@@ -436,6 +436,30 @@ def gop_psnr(ref9, test9) -> tuple[float, float]:
     errs = [mse(r, t) for r, t in zip(ref9, test9)]
     pooled = float(np.mean(errs))
     return psnr_from_mse(pooled), pooled           # video.py:318-322
+
+
+def boundary_flicker(prev9, curr9, n: int, norm: str = "l1") -> float:
+    """video.py:285-304 (frame i of the current GoP vs frame T-n+i of the previous)."""
+    total = 0.0
+    for i in range(1, n + 1):
+        a = np.asarray(curr9[i - 1], np.float64)
+        b = np.asarray(prev9[GOP_SIZE - n + i - 1], np.float64)
+        if norm == "l1":
+            total += float(np.mean(np.abs(a - b)))
+        else:
+            total += float(np.sqrt(np.mean((a - b) ** 2)))
+    return total / n
+
+
+def inter_frame_consistency(frames) -> float:
+    """video.py:307-315."""
+    frames = list(frames)
+    if len(frames) < 2:
+        return 0.0
+    deltas = [float(np.mean(np.abs(np.asarray(frames[i + 1], np.float64)
+                                   - np.asarray(frames[i], np.float64))))
+              for i in range(len(frames) - 1)]
+    return float(np.mean(deltas))
 
 
 # ---------------------------------------------------------------------------

@@ -83,6 +83,7 @@ SIGNATURES = {
     "sst_unpack_decode": (_I, [_P, _P, _P, _P, _L, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     "sst_upscale_blend": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P]),
     "sst_mse": (_I, [_P, _P, _L, _L, _P, _P]),
+    "sst_mean_diff": (_I, [_P, _P, _L, _L, _I, _P, _P]),
     "sst_similarity_gop": (_I, [_P, _I, _L, _I, _P, _P]),
     "sst_upscale_blend9": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P]),
     "sst_lt_conv": (_I, [C.POINTER(SstConvDesc), _P]),

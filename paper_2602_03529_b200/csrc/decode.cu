@@ -20,7 +20,7 @@ namespace sst {
 struct RowInfo {
   int64_t payload;   // byte offset of the payload in the packet buffer
   double qmin;       // quant_min
-  double step;       // quant_range / 255.0 (transport.py:199)
+  double step;       // quant_range / 255.0 (transport.py:112)
   int32_t ok;
   int32_t pad;
 };
@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(kDecThreads) k_decode(DecArgs a) {
   // ---- 1. gather the tokens ----
   if (kFromPackets) {
     // every thread dequantises one (layer, token, channel) straight from the
-    // winning packet's payload (transport.py:195-199, 296-305)
+    // winning packet's payload (transport.py:108-112, 296-302)
     for (int e = tid; e < 2 * kDecTok * kChannels; e += kDecThreads) {
       const int im = e / (kDecTok * kChannels);
       const int t = (e / kChannels) % kDecTok;

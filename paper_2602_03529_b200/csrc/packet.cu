@@ -1,7 +1,7 @@
 // K3 / K4a: the token wire format (transport.py).
 //
-//   packetize_tokens + TokenPacket.to_bytes  (transport.py:323-358, 184-189)
-//   parse_packet for token packets            (transport.py:151-157, 241-271)
+//   packetize_tokens + TokenPacket.to_bytes  (transport.py:236-271, 97-102)
+//   parse_packet for token packets            (transport.py:154-184)
 //   reassemble (first-wins, zero-fill)        (transport.py:274-305, 195-199)
 //
 // One warp builds (or validates) one row packet: a warp-wide masked min/max,
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kPackWarps * 32) k_packetize(PackArgs a) {
     buf[kHdr + b] = (uint8_t)byte;
   }
 
-  // 2) masked row min / max over the valid tokens (transport.py:337-340)
+  // 2) masked row min / max over the valid tokens (transport.py:249-253)
   double lo = 0.0, hi = 0.0;
   bool any = false;
   const int64_t nel = (int64_t)Wt * C;
@@ -145,7 +145,7 @@ __global__ void __launch_bounds__(kPackWarps * 32) k_packetize(PackArgs a) {
     }
     pay[pre[t] * C + c] = q;
   }
-  // 4) header (transport.py:131, 184-189)
+  // 4) header (transport.py:97-102)
   if (lane == 0) {
     write_token_header(buf, a.kind[mi], a.gop_id[mi], (uint32_t)row, (uint32_t)Wt, (uint32_t)C,
                        a.scale[mi], (float)qmin32, (float)qrange32);
@@ -189,7 +189,7 @@ __global__ void __launch_bounds__(kPackWarps * 32)
   for (int b = lane; b < body + 4; b += 32) dst[b] = buf[b];
 }
 
-// parse_packet (token kinds) -- validation order mirrors transport.py:151-157,241-271
+// parse_packet (token kinds) -- validation order mirrors transport.py:154-184
 __global__ void __launch_bounds__(kPackWarps * 32)
     k_parse(const uint8_t* __restrict__ buf, const int64_t* __restrict__ off,
             const int32_t* __restrict__ len, const uint8_t* __restrict__ present, int64_t n,
@@ -250,7 +250,7 @@ __global__ void k_mark_dups(SstPacketInfo* info, const int32_t* __restrict__ tar
   if (winner[(int64_t)target[i] * Ht + p.row] != (uint32_t)i) p.status = SST_PKT_DUP;
 }
 
-// one warp per matrix row: dequantise the winner's payload (transport.py:195-199,
+// one warp per matrix row: dequantise the winner's payload (transport.py:108-112,
 // 296-305), zero-fill everything else
 __global__ void __launch_bounds__(256)
     k_scatter(const uint8_t* __restrict__ buf, const int64_t* __restrict__ off,

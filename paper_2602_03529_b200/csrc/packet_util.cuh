@@ -9,7 +9,7 @@ namespace sst {
 constexpr uint32_t kMagic = 0x4D53;  // transport.py:32
 constexpr uint32_t kVersion = 1;     // transport.py:33
 
-// ">HBBIHHBBff" (transport.py:44, 184-187)
+// ">HBBIHHBBff" (transport.py:44, 97-102)
 __device__ __forceinline__ void write_token_header(uint8_t* b, uint32_t kind, uint32_t gop,
                                                    uint32_t row, uint32_t width, uint32_t channels,
                                                    uint32_t scale, float qmin, float qrange) {
@@ -26,7 +26,7 @@ __device__ __forceinline__ void write_token_header(uint8_t* b, uint32_t kind, ui
 }
 
 // parse_packet for token packets: the check order and messages follow
-// transport.py:151-157 (_check_seal) and 241-271.  Whole warp; control flow is
+// transport.py:64-70 (_check_seal) and 154-184.  Whole warp; control flow is
 // warp-uniform.  Result is valid in every lane.
 __device__ __forceinline__ void parse_token_packet(const uint8_t* pkt, int len, bool present,
                                                    const uint32_t* tab, const uint32_t* x2n,

@@ -724,29 +724,6 @@ __global__ void k_blend(const float* __restrict__ prev, const float* curr, int G
     for (int f = n; f < kGop; ++f) og[f * fe + q] = cg[f * fe + q];
 }
 
-constexpr int kMseThreads = 512;
-
-__global__ void __launch_bounds__(kMseThreads)
-    k_mse(const float* __restrict__ a, const float* __restrict__ b, int64_t elems, double* out) {
-  __shared__ double part[kMseThreads / 32];
-  const float* pa = a + (int64_t)blockIdx.x * elems;
-  const float* pb = b + (int64_t)blockIdx.x * elems;
-  double acc = 0.0;
-  for (int64_t e = threadIdx.x; e < elems; e += kMseThreads) {
-    double d = (double)pa[e] - (double)pb[e];
-    acc = acc + d * d;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < kMseThreads / 32; ++i) s += part[i];
-    out[blockIdx.x] = s / (double)elems;
-  }
-}
-
 }  // namespace sst
 
 using namespace sst;
@@ -922,16 +899,6 @@ extern "C" int sst_blend(const float* prev, const float* curr, int G, int H, int
   int64_t fe = (int64_t)H * W * 3;
   k_blend<<<(unsigned)ceil_div64(G * fe, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
       prev, curr, G, fe, n, out);
-  SST_LAUNCH_CHECK();
-  return SST_OK;
-}
-
-extern "C" int sst_mse(const float* a, const float* b, int64_t n, int64_t elems, double* out,
-                       void* stream) {
-  if (n < 0 || elems <= 0) return SST_ERR_ARG;
-  if (n == 0) return SST_OK;
-  if (!a || !b || !out) return SST_ERR_ARG;
-  k_mse<<<(unsigned)n, kMseThreads, 0, static_cast<cudaStream_t>(stream)>>>(a, b, elems, out);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }

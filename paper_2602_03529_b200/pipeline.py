@@ -271,10 +271,17 @@ class StreamBank:
 
     def __init__(self, n_streams: int, H: int, W: int, scales=(2, 3), blend_n: int = 2,
                  concurrent_groups: bool = True, priority_middle: bool = True):
-        if blend_n > 4:
-            raise ValueError("the fused reconstruction blends at most 4 frames")
+        if not 1 <= blend_n <= 8:                 # CodecConfig, codec.py:41-42
+            raise ValueError(f"blend width must be in [1, 8], got {blend_n}")
         self.n, self.H, self.W, self.blend_n = n_streams, H, W, blend_n
         self.codecs = {s: GopCodec(n_streams, H, W, s, blend_n) for s in scales}
+        # blend_n <= 4: K5 recomputes the previous GoP's (unblended) tail from
+        # its working image.  blend_n >= 5 reaches back into frames the
+        # previous blend already changed (frame 9-n+i-1 < n), so each stream
+        # keeps its last full-resolution output instead and blends after K5,
+        # sequentially per stream (codec.py:278-296).
+        self.prev_out = None
+        self.has_prev = [False] * n_streams
         self.prev_host = np.zeros(n_streams, dtype=_lib.PREV_DTYPE)
         self.rings = {s: _DescRing(n_streams * _lib.PREV_BYTES) for s in scales}
         # each scale group runs on its own CUDA stream so the latency-bound
@@ -357,11 +364,15 @@ class StreamBank:
                         gs.wait_stream(mid)
                     # K4 parse + 5 (init/route/dups/rowprep/decode) + K5
                     self.launches += 1 + 5 + 1
-                    staged = self._prev_descs(s, ids)
-                    codec.reconstruct(g, parity, out_by_scale[s],
-                                      None if staged is None else staged[0])
-                    if staged is not None:
-                        self.rings[s].release(staged[1])
+                    if self.blend_n <= 4:
+                        staged = self._prev_descs(s, ids)
+                        codec.reconstruct(g, parity, out_by_scale[s],
+                                          None if staged is None else staged[0])
+                        if staged is not None:
+                            self.rings[s].release(staged[1])
+                    else:
+                        codec.reconstruct(g, parity, out_by_scale[s], None)
+                        self._blend_wide(ids, out_by_scale[s])
                 elif mid is not gs:
                     gs.wait_stream(mid)
         for gs in joined:
@@ -374,6 +385,21 @@ class StreamBank:
             for slot, sid in enumerate(ids):
                 self.last[sid] = (s, parity, slot)
         self.step_idx += 1
+
+    def _blend_wide(self, ids, out: torch.Tensor) -> None:
+        """blend_boundary for n >= 5 against each stream's previous output,
+        then keep this output as the next GoP's previous (stream-ordered)."""
+        if self.prev_out is None:
+            self.prev_out = torch.empty((self.n, GOP, self.H, self.W, 3), dtype=torch.float32,
+                                        device=_dev.device())
+        st = _dev.stream()
+        for j, sid in enumerate(ids):
+            if self.has_prev[sid]:
+                _lib.call("sst_blend", self.prev_out[sid].data_ptr(), out[j].data_ptr(), 1,
+                          self.H, self.W, self.blend_n, out[j].data_ptr(), st)
+                self.launches += 1
+            self.prev_out[sid].copy_(out[j])
+            self.has_prev[sid] = True
 
     def set_timer(self, timer) -> None:
         for c in self.codecs.values():
@@ -388,11 +414,11 @@ class StreamBank:
             loc = self.last[sid]
             if loc is None:
                 continue
-            s, par, slot = loc
-            c = self.codecs[s]
+            ps, par, slot = loc             # the previous GoP's scale, not this one's
+            c = self.codecs[ps]
             img = c.img[par]
             rec[j]["p_img"] = img.data_ptr() + ((slot * 2 + 1) * c.h * c.w * 3) * 4
-            rec[j]["h"], rec[j]["w"], rec[j]["s"] = c.h, c.w, s
+            rec[j]["h"], rec[j]["w"], rec[j]["s"] = c.h, c.w, ps
         return self.rings[s].stage(rec)
 
 

@@ -179,28 +179,38 @@ def encode_symbol_streams(streams) -> list:
     offs = np.zeros(G, dtype=np.int64)
     offs[1:] = np.cumsum(lens)[:-1]
     d_syms = _dev.h2d(np.concatenate(streams) if G else np.zeros(1, np.int32))
-    cap = int(max(64, 2 * lens.max() + 64))
-    out = _dev.empty((G * cap,), torch.uint8)
-    olen = _dev.empty((G,), torch.int64)
+    cap = int(max(64, 2 * lens.max() + 64)) if G else 64
     d_off, d_len = _dev.h2d(offs), _dev.h2d(lens)
-    _lib.call("sst_rc_encode_symbols", _dev.ptr(d_syms), _dev.ptr(d_off), _dev.ptr(d_len), G,
-              _dev.ptr(out), cap, _dev.ptr(olen), _dev.stream())
-    ol = _dev.d2h(olen)
-    raw = _dev.d2h(out)
-    return [raw[g * cap:g * cap + int(ol[g])].tobytes() for g in range(G)]
+    while True:
+        out = _dev.empty((max(G * cap, 1),), torch.uint8)
+        olen = _dev.empty((max(G, 1),), torch.int64)
+        _lib.call("sst_rc_encode_symbols", _dev.ptr(d_syms), _dev.ptr(d_off), _dev.ptr(d_len), G,
+                  _dev.ptr(out), cap, _dev.ptr(olen), _dev.stream())
+        ol = _dev.d2h(olen)[:G]
+        if (ol >= 0).all():          # a negative length is the size the output needed
+            raw = _dev.d2h(out)
+            return [raw[g * cap:g * cap + int(ol[g])].tobytes() for g in range(G)]
+        cap = int(-ol.min()) + 64
 
 
 def decode_stream(data: bytes, max_symbols: int = 1 << 24) -> list:
     """Decode to the exact symbol list (rangecoder.py:188-235)."""
     data = bytes(data)
-    cap = min(max_symbols, max(16, 8 * len(data) + 16))
+    # The adaptive model can code a symbol in well under one bit, so the byte
+    # count does not bound the symbol count: start from a guess and grow the
+    # output on status 7 (capacity exceeded) up to the caller's budget.
+    cap = max(1, min(max_symbols, max(16, 8 * len(data) + 16)))
     buf = _dev.h2d(np.frombuffer(data or b"\0", dtype=np.uint8))
-    syms = _dev.empty((cap,), torch.int32)
     nsym = _dev.empty((1,), torch.int64)
     status = _dev.empty((1,), torch.int32)
-    _lib.call("sst_rc_decode_symbols", _dev.ptr(buf), len(data), max_symbols, cap,
-              _dev.ptr(syms), _dev.ptr(nsym), _dev.ptr(status), _dev.stream())
-    st = int(status.item())
+    while True:
+        syms = _dev.empty((cap,), torch.int32)
+        _lib.call("sst_rc_decode_symbols", _dev.ptr(buf), len(data), max_symbols, cap,
+                  _dev.ptr(syms), _dev.ptr(nsym), _dev.ptr(status), _dev.stream())
+        st = int(status.item())
+        if st != 7 or cap >= max_symbols:
+            break
+        cap = min(max_symbols, cap * 8)
     if st == 1:
         raise CorruptStreamError(f"compressed stream truncated ({len(data)} bytes)")
     if st == 4:

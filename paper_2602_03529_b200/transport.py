@@ -157,7 +157,7 @@ def serialize_packets(packets) -> list:
 # packetisation
 
 def packetize_tokens(m: TokenMatrix, scale: int = 1) -> list:
-    """One packet per token row, header-only rows included (transport.py:323-358)."""
+    """One packet per token row, header-only rows included (transport.py:236-271)."""
     h = m.height_tokens
     if h > 0xFFFF:
         raise ValueError(f"matrix has {h} rows; the row index field is 16-bit")
@@ -266,7 +266,7 @@ def parse_packets(datas, errors: str = "raise") -> list:
 
 def parse_packet(data: bytes):
     """Parse one wire packet, validating checksum, magic, version and
-    lengths (transport.py:151-157, 241-271)."""
+    lengths (transport.py:154-218)."""
     return parse_packets([data])[0]
 
 
@@ -282,6 +282,21 @@ def reassemble(packets, expected: tuple, kind: str, gop_id: int = 0,
         if pkt.kind != kind or pkt.gop_id != gop_id:
             raise ValueError(f"packet ({pkt.kind}, gop {pkt.gop_id}) does not belong to "
                              f"({kind}, gop {gop_id})")
+    # The rows the reference dequantises (in range, first arrival, any valid
+    # column) must carry popcount(mask) * C payload bytes: TokenPacket.dequantized
+    # reshapes the payload and raises ValueError otherwise (transport.py:108-112,
+    # 292-301).  The kernel trusts these lengths, so check them here.
+    seen = set()
+    for pkt in packets:
+        if pkt.row_index >= h or pkt.row_index in seen:
+            continue
+        seen.add(pkt.row_index)
+        pmask = np.asarray(pkt.mask, dtype=bool)
+        if pmask[:w].any():
+            need = int(np.count_nonzero(pmask)) * int(pkt.channels)
+            if len(pkt.payload) != need:
+                raise ValueError(f"cannot reshape array of size {len(pkt.payload)} into shape "
+                                 f"({int(np.count_nonzero(pmask))},{pkt.channels})")
     n = len(packets)
     values = _dev.empty((h, w, c), torch.float64)
     mask = _dev.empty((h, w), torch.uint8)

@@ -125,20 +125,43 @@ def concat_gops(gops, frame_count: int | None = None) -> list:
 # ---------------------------------------------------------------------------
 # metrics (device reductions)
 
-def _mse_many(refs, tests) -> np.ndarray:
-    refs = list(refs)
-    tests = list(tests)
+def _mean_diff(refs, tests, mode: int = 0) -> np.ndarray:
+    """np.mean of the float64 per-pixel (a-b)^2 (mode 0) or |a-b| (mode 1) of
+    each frame pair, on the GPU in numpy's pairwise summation order
+    (csrc/metrics.cu): bit-identical to the reference's metric arithmetic."""
+    refs = [np.asarray(getattr(r, "samples", r)) for r in refs]
+    tests = [np.asarray(getattr(t, "samples", t)) for t in tests]
     for r, t in zip(refs, tests):
-        if r.samples.shape != t.samples.shape:
-            raise ValueError(f"dimension mismatch: {r.samples.shape} vs {t.samples.shape}")
+        if r.shape != t.shape:
+            raise ValueError(f"dimension mismatch: {r.shape} vs {t.shape}")
     if not refs:
         return np.zeros(0)
-    a = _dev.h2d(np.stack([r.samples for r in refs]), np.float32)
-    b = _dev.h2d(np.stack([t.samples for t in tests]), np.float32)
+    a = _dev.h2d(np.stack(refs), np.float32)
+    b = _dev.h2d(np.stack(tests), np.float32)
     out = _dev.empty((len(refs),), torch.float64)
-    elems = int(np.prod(refs[0].samples.shape))
-    _lib.call("sst_mse", _dev.ptr(a), _dev.ptr(b), len(refs), elems, _dev.ptr(out), _dev.stream())
+    elems = int(np.prod(refs[0].shape))
+    _lib.call("sst_mean_diff", _dev.ptr(a), _dev.ptr(b), len(refs), elems, mode, _dev.ptr(out),
+              _dev.stream())
     return _dev.d2h(out)
+
+
+def _mse_many(refs, tests) -> np.ndarray:
+    return _mean_diff(refs, tests, 0)
+
+
+def gop_psnr_device(reference: torch.Tensor, test: torch.Tensor) -> tuple:
+    """gop_psnr (video.py:318-322) of device GoPs: float32 [9, H, W, 3] CUDA
+    tensors, reduced in place on the GPU (no host copy of the frames)."""
+    if reference.shape != test.shape or reference.dim() != 4:
+        raise ValueError(f"dimension mismatch: {tuple(reference.shape)} vs {tuple(test.shape)}")
+    if reference.dtype != torch.float32 or test.dtype != torch.float32:
+        raise ValueError("frames must be float32")
+    a, b = reference.contiguous(), test.contiguous()
+    out = torch.empty((a.shape[0],), dtype=torch.float64, device=a.device)
+    _lib.call("sst_mean_diff", a.data_ptr(), b.data_ptr(), a.shape[0], a[0].numel(), 0,
+              out.data_ptr(), _dev.stream())
+    pooled = float(np.mean(_dev.d2h(out)))
+    return psnr_from_mse(pooled), pooled
 
 
 def mse(reference: Frame, test: Frame) -> float:
@@ -171,23 +194,22 @@ def boundary_flicker(prev_gop_recon: GoP, curr_gop_recon: GoP, n: int, norm: str
         raise ValueError("GoP dimension mismatch")
     if norm not in ("l1", "l2"):
         raise ValueError(f"unknown norm {norm!r}")
-    a = _dev.h2d(np.stack([curr_gop_recon.frames[i - 1].samples for i in range(1, n + 1)]))
-    b = _dev.h2d(np.stack([prev_gop_recon.frames[GOP_SIZE - n + i - 1].samples
-                           for i in range(1, n + 1)]))
-    d = a.double() - b.double()
-    if norm == "l1":
-        per = d.abs().flatten(1).mean(dim=1)
-    else:
-        per = (d * d).flatten(1).mean(dim=1).sqrt()
-    return float(per.sum().item()) / n
+    per = _mean_diff([curr_gop_recon.frames[i - 1] for i in range(1, n + 1)],
+                     [prev_gop_recon.frames[GOP_SIZE - n + i - 1] for i in range(1, n + 1)],
+                     1 if norm == "l1" else 0)
+    total = 0.0
+    for v in per:                                    # video.py:294-303, in order
+        total += float(v) if norm == "l1" else float(np.sqrt(v))
+    return total / n
 
 
 def inter_frame_consistency(frames) -> float:
+    """Mean absolute inter-frame pixel difference (video.py:307-315)."""
     frames = list(frames)
     if len(frames) < 2:
         return 0.0
-    x = _dev.h2d(np.stack([f.samples for f in frames])).double()
-    return float((x[1:] - x[:-1]).abs().flatten(1).mean(dim=1).mean().item())
+    deltas = _mean_diff(frames[1:], frames[:-1], 1)
+    return float(np.mean([float(d) for d in deltas]))
 
 
 def quality_report(reference: GoP, test: GoP, prev_recon: GoP | None = None,

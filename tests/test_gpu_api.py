@@ -128,6 +128,17 @@ def test_blend_kats(rng):
         assert V.boundary_flicker(prev, C.blend_boundary(prev, curr, 2), 2) < before
 
 
+@pytest.mark.parametrize("n", range(1, 9))
+def test_blend_all_widths_match_oracle(rng, n):
+    # codec.py:41-42 allows n in 1..8; n >= 5 blends with frames of the
+    # previous GoP that were themselves blended
+    prev, curr = random_gop(rng, 20, 28), random_gop(rng, 20, 28)
+    out = C.blend_boundary(_gop(prev), _gop(curr, 1), n)
+    want = O.blend(list(prev), list(curr), n)
+    for a, b in zip(out.frames, want):
+        assert _bits(a.samples, b)
+
+
 def test_scale_gop_roundtrip_shapes(rng):
     g = _gop(random_gop(rng, 30, 30))
     down = C.scale_gop(g, 3, "down")
@@ -296,6 +307,18 @@ def test_reassembly_rules(rng):
     stats = {}
     out = T.reassemble(T.packetize_tokens(m) + [rogue], (2, 4, 3), "P", stats=stats)
     assert stats["corrupt"] == 1 and stats["rows_received"] == 2 and out.mask.all()
+    # caller-built packets whose payload does not hold popcount(mask)*C bytes:
+    # the reference's dequantized() reshape raises; a row that is never
+    # dequantised (duplicate) is ignored, as in the reference
+    good = first[0]
+    for pay in (good.payload[:-1], good.payload + b"\0"):
+        bad = T.TokenPacket(kind="P", gop_id=0, row_index=0, width_tokens=4, channels=3, scale=1,
+                            quant_min=good.quant_min, quant_range=good.quant_range,
+                            mask=good.mask, payload=pay)
+        with pytest.raises(ValueError):
+            T.reassemble([bad], (2, 4, 3), "P")
+        out = T.reassemble([good, bad, first[1]], (2, 4, 3), "P")
+        assert np.array_equal(out.values, T.reassemble(first, (2, 4, 3), "P").values)
 
 
 def test_sender_drop_equals_network_loss(rng):

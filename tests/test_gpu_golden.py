@@ -64,6 +64,12 @@ def test_api_pipeline_matches_reference(c):
         assert digest(r["dec"].frames[0].samples) == rec["i_img"]
         assert digest(r["dec"].frames[1].samples) == rec["p_img"]
         assert digest(r["out"]) == rec["out"]
+        # a19: the GPU metric path reproduces the reference's gop_psnr exactly
+        # (numpy pairwise summation order, csrc/metrics.cu)
+        from paper_2602_03529_b200 import video as V
+        src = V.GoP(0, tuple(V.Frame(f, timestamp_index=t) for t, f in enumerate(r["src"])))
+        out = V.GoP(0, tuple(V.Frame(f, timestamp_index=t) for t, f in enumerate(r["out"])))
+        assert V.gop_psnr(src, out) == (rec["psnr_db"], rec["mse"])
 
 
 BATCH_CASES = [c for c in CASES if all(g["scale"] in (2, 3) for g in c["gops"])]
@@ -98,5 +104,7 @@ def test_batched_pipeline_matches_reference(c):
         assert digest(img[0]) == rec["i_img"]
         assert digest(img[1]) == rec["p_img"]
         assert digest(out[0].cpu().numpy()) == rec["out"]
+        from paper_2602_03529_b200.video import gop_psnr_device
+        assert gop_psnr_device(frames[0], out[0]) == (rec["psnr_db"], rec["mse"])
         st = codec.stats[:4].cpu().numpy()
         assert [int(st[1]), int(st[3])] == rec["rows_received"]

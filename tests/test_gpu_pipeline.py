@@ -1,6 +1,6 @@
 """GPU: the fused batched path (StreamBank / GopCodec, kernels K1-K5) against
 the oracle -- many streams at once, variable scale per GoP, every blend width
-the fused kernel supports, network loss and duplicates -- plus full-size
+(1..4 fused into K5, 5..8 blended per stream after it), network loss and duplicates -- plus full-size
 (1080p) properties and determinism."""
 
 import numpy as np
@@ -21,7 +21,7 @@ def _wire(codec, g):
     return [[arena[i * n + j, :lengths[i * n + j]].tobytes() for j in range(n)] for i in range(g)]
 
 
-@pytest.mark.parametrize("blend_n", [1, 2, 3, 4])
+@pytest.mark.parametrize("blend_n", [1, 2, 3, 4, 5, 6, 7, 8])
 @pytest.mark.parametrize("HW", [(72, 96), (60, 70)])      # TMA-aligned and not
 def test_multistream_variable_scale_matches_oracle(blend_n, HW):
     H, W = HW

@@ -163,6 +163,19 @@ def test_compression_tracks_entropy(rng):
     assert RC.decode_stream(data) == syms
 
 
+def test_sub_bit_symbols_decode():
+    # the adaptive model codes a long constant run in far under one bit per
+    # symbol (20001 symbols in ~436 bytes): the decoder's output buffer must
+    # not be sized from the byte count
+    syms = [255] * 20000 + [RC.EOS]
+    data = RC.encode_stream(syms)
+    assert data == R.encode_stream(syms)
+    assert len(data) * 8 < len(syms)
+    assert RC.decode_stream(data) == syms
+    with pytest.raises(RC.CorruptStreamError):
+        RC.decode_stream(data, max_symbols=1000)
+
+
 # ---------------------------------------------------------------------------
 # pkg/tests/test_residual.py (core properties)
 

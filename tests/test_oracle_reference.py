@@ -134,3 +134,18 @@ def test_decode_upscale_blend(ref):
                 ours = O.blend([f.samples for f in prev.frames], [f.samples for f in up.frames], n)
                 for a, b in zip(ours, bl.frames):
                     assert _bits(a, b.samples)
+
+
+def test_metrics(ref):
+    C, S, T, V = ref
+    rng = np.random.default_rng(15)
+    for shape in ((16, 24, 3), (45, 80, 3), (1080, 1920, 3)):
+        a = _adversarial_frames(rng, 9, *shape[:2])
+        b = _adversarial_frames(rng, 9, *shape[:2])
+        ga = V.GoP(0, tuple(V.Frame(x, timestamp_index=t) for t, x in enumerate(a)))
+        gb = V.GoP(1, tuple(V.Frame(x, timestamp_index=t) for t, x in enumerate(b)))
+        assert O.gop_psnr(list(a), list(b)) == V.gop_psnr(ga, gb)
+        for n in (1, 2, 5, 9):
+            for norm in ("l1", "l2"):
+                assert O.boundary_flicker(a, b, n, norm) == V.boundary_flicker(ga, gb, n, norm)
+        assert O.inter_frame_consistency(b) == V.inter_frame_consistency(gb.frames)
