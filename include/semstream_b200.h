@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define SST_ABI_VERSION 1
+#define SST_ABI_VERSION 2
 
 /* call status */
 #define SST_OK 0
@@ -320,6 +320,11 @@ typedef struct SstConvDesc {
   uint8_t* mask;
   float* frames;           /* PIXELS: frame f = frame_base + N-tile index (192 columns per frame) */
   int32_t h, w, frame_base;
+  /* int8 layers (sst_lt8_conv only; ignored by sst_lt_conv): in / weight /
+   * residual / out are int8, in_C % 128 == 0, accumulators int32 (exact) */
+  int32_t shift;           /* requantisation: y = clamp((acc + b + 2^(shift-1)) >> shift, -127, 127) */
+  const int32_t* bias_i32; /* int32 [N], 16-byte aligned */
+  const int8_t* act_lut;   /* act 1: y = act_lut[y + 128] (the SiLU table) */
 } SstConvDesc;
 
 /* One convolution layer (implicit GEMM on tcgen05). */
@@ -359,6 +364,46 @@ SST_API int sst_lt_attn(const void* qkv, int G, int Ht, int Wt, int D, void* out
  * followed by sst_lt_attn. */
 SST_API int sst_lt_attn_fused(const void* h, const void* w_qkv, const float* b_qkv, int G, int Ht,
                               int Wt, int D, void* out, void* stream);
+
+/* ---- int8 learned tokenizer (exact integer arithmetic, kind::i8) ---------
+ * The same plug-in network shape with int8 activations / weights and int32
+ * tensor-core accumulation: bit-identical to oracle/learned_i8_oracle.py
+ * (which documents the arithmetic).  Activations int8 channels-last
+ * [G][T][H'][W'][C], C % 128 == 0. */
+
+/* One int8 layer: SstConvDesc with the int8 fields (shift, bias_i32,
+ * act_lut); epi STORE (requantise, SiLU table, saturating residual add, int8
+ * out), FSQ (N = 16: q = clamp((acc + b) >> shift, -L/2, L-1-L/2), codes
+ * q/(L/2) f64, mixed-radix indices, mask = 1) or PIXELS (clamp(round-shift,
+ * 0, 255) / 255 float32 frames). */
+SST_API int sst_lt8_conv(const SstConvDesc* d, void* stream);
+
+/* Box downscale (bit-exact) + edge pad + 8x8 patchify to int8
+ * rint(px * 255) - 128: pI [G][H'][W'][256] (192 used, rest zero), pP
+ * [G][H'][W'][1536]. */
+SST_API int sst_lt8_patchify(const float* frames, int G, int H, int W, int s, void* pI, void* pP,
+                             void* stream);
+
+/* Causal 8x8-window attention core, 128-dim heads, integer softmax:
+ * qkv int8 [G][2][H'][W'][3D] -> out int8 [G][2][H'][W'][D]; shift and
+ * exp_lut (uint8[256]) as in the oracle. */
+SST_API int sst_lt8_attn(const void* qkv, int G, int Ht, int Wt, int D, int shift,
+                         const uint8_t* exp_lut, void* out, void* stream);
+
+/* Decoder input from a token matrix (plug-in path): received f64 codes
+ * [G][2][H'][W'][12] + mask -> snapped, concealed codes (ws: G*2*H'*W'*16
+ * bytes) -> the first layer's gathered (2,3,3) neighbourhood, int8
+ * [G][2][H'][W'][256]. */
+SST_API int sst_lt8_dec_in(const double* tok, const uint8_t* mask, int G, int Ht, int Wt, void* ws,
+                           void* out, void* stream);
+
+/* The same straight from the winning row packets (reassemble x2 fused with
+ * the decoder input; packets routed as for sst_unpack_decode). */
+SST_API int64_t sst_lt8_unpack_workspace(int G, int Ht, int Wt);
+SST_API int sst_lt8_unpack_dec_in(const uint8_t* buf, const int64_t* off, SstPacketInfo* info,
+                                  const int32_t* target, int64_t n, int G, int Ht, int Wt,
+                                  const uint32_t* exp_gop, uint32_t* winner, int32_t* stats,
+                                  void* ws, void* out, void* stream);
 
 /* ---- metrics ------------------------------------------------------------ */
 

@@ -21,7 +21,7 @@ BUILD = PKG.parent / "build" / "csrc"
 LIB = PKG / "libsemstream_b200.so"
 
 SOURCES = ["capi.cu", "tma_host.cu", "encode.cu", "select.cu", "packet.cu", "decode.cu",
-           "upscale.cu", "residual.cu", "learned.cu", "metrics.cu"]
+           "upscale.cu", "residual.cu", "learned.cu", "metrics.cu", "learned_i8.cu"]
 
 # the learned-tokenizer kernels are bf16/fp32 tensor-core math with no
 # bit-exact contract: let them contract a*b+c into FMA

@@ -48,7 +48,8 @@ class SstConvDesc(C.Structure):
                 ("act", C.c_int32), ("residual", C.c_void_p), ("out", C.c_void_p),
                 ("out_T", C.c_int32), ("codes", C.c_void_p), ("idx", C.c_void_p),
                 ("mask", C.c_void_p), ("frames", C.c_void_p), ("h", C.c_int32),
-                ("w", C.c_int32), ("frame_base", C.c_int32)]
+                ("w", C.c_int32), ("frame_base", C.c_int32), ("shift", C.c_int32),
+                ("bias_i32", C.c_void_p), ("act_lut", C.c_void_p)]
 
 
 LT_EPI_STORE, LT_EPI_FSQ, LT_EPI_PIXELS = 0, 1, 2
@@ -87,6 +88,12 @@ SIGNATURES = {
     "sst_similarity_gop": (_I, [_P, _I, _L, _I, _P, _P]),
     "sst_upscale_blend9": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P]),
     "sst_lt_conv": (_I, [C.POINTER(SstConvDesc), _P]),
+    "sst_lt8_conv": (_I, [C.POINTER(SstConvDesc), _P]),
+    "sst_lt8_patchify": (_I, [_P, _I, _I, _I, _I, _P, _P, _P]),
+    "sst_lt8_attn": (_I, [_P, _I, _I, _I, _I, _I, _P, _P, _P]),
+    "sst_lt8_dec_in": (_I, [_P, _P, _I, _I, _I, _P, _P, _P]),
+    "sst_lt8_unpack_workspace": (_L, [_I, _I, _I]),
+    "sst_lt8_unpack_dec_in": (_I, [_P, _P, _P, _P, _L, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     "sst_lt_patchify": (_I, [_P, _I, _I, _I, _I, _P, _P, _P]),
     "sst_lt_dec_in": (_I, [_P, _P, _I, _I, _I, _P, _P]),
     "sst_lt_attn": (_I, [_P, _I, _I, _I, _I, _P, _P]),

@@ -359,3 +359,140 @@ extern "C" int sst_lt_unpack_dec_in(const uint8_t* buf, const int64_t* off, SstP
   SST_LAUNCH_CHECK();
   return SST_OK;
 }
+
+// ---- int8 learned tokenizer: decoder input (learned_i8.py) -------
+// Received codes -> snapped, concealed FSQ levels q (x16, int8) per token
+// ([G][2][H'][W'][16], channels 12..15 zero), then the first decoder layer's
+// (2,3,3) neighbourhood gathered tap-major into 2 x 9 x 12 = 216 (+40 zero)
+// channels, so that layer is one K = 256 int8 GEMM
+// (oracle/learned_i8_oracle.py snap_codes / dec_input).
+namespace sst {
+
+__device__ __forceinline__ int8_t l8_snap(double v, int i) {
+  const int L = lt_levels(i), hw = L / 2;
+  double q = rint(v * (double)hw);
+  q = fmin(fmax(q, (double)-hw), (double)(L - 1 - hw));
+  return (int8_t)(16 * (int)q);
+}
+
+__global__ void k_l8_codes_tok(const double* __restrict__ tok, const uint8_t* __restrict__ mask,
+                               int64_t G, int64_t n, int8_t* __restrict__ codes) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= G * 2 * n) return;
+  const int64_t pos = idx % n, gt = idx / n;
+  int64_t src = idx;
+  if ((gt & 1) && !mask[idx]) src = (gt - 1) * n + pos;     // conceal P with the I token
+  int8_t q[16] = {0};
+  if (mask[src]) {
+#pragma unroll
+    for (int i = 0; i < kChannels; ++i) q[i] = l8_snap(tok[src * kChannels + i], i);
+  }
+  *reinterpret_cast<uint4*>(codes + idx * 16) = *reinterpret_cast<const uint4*>(q);
+}
+
+__global__ void k_l8_codes_pkt(const uint8_t* __restrict__ buf, const RowInfo* __restrict__ rows,
+                               const int32_t* __restrict__ tokoff, int G, int Ht, int Wt,
+                               int8_t* __restrict__ codes) {
+  const int64_t n = (int64_t)Ht * Wt;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)G * 2 * n) return;
+  const int64_t pos = idx % n, gt = idx / n;
+  const int y = (int)(pos / Wt), x = (int)(pos % Wt);
+  int64_t r = gt * Ht + y;
+  int slot = tokoff[r * Wt + x];
+  if ((gt & 1) && slot < 0) {                 // conceal with the co-located I token
+    r = (gt - 1) * Ht + y;
+    slot = tokoff[r * Wt + x];
+  }
+  int8_t q[16] = {0};
+  if (slot >= 0) {
+    const RowInfo ri = rows[r];
+    const uint8_t* p = buf + ri.payload + (int64_t)slot * kChannels;
+#pragma unroll
+    for (int i = 0; i < kChannels; ++i) q[i] = l8_snap(ri.qmin + (double)p[i] * ri.step, i);
+  }
+  *reinterpret_cast<uint4*>(codes + idx * 16) = *reinterpret_cast<const uint4*>(q);
+}
+
+// one thread per (token, 16-byte output chunk): 16 chunks of 256 channels
+__global__ void k_l8_gather233(const int8_t* __restrict__ codes, int G, int Ht, int Wt,
+                               int8_t* __restrict__ out) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n = (int64_t)Ht * Wt;
+  if (e >= (int64_t)G * 2 * n * 16) return;
+  const int chunk = (int)(e & 15);
+  const int64_t tokn = e >> 4;
+  const int64_t pos = tokn % n, gt = tokn / n;
+  const int t = (int)(gt & 1);
+  const int y = (int)(pos / Wt), x = (int)(pos % Wt);
+  int8_t v[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int ch = chunk * 16 + j;            // gathered channel = tap * 12 + c
+    int8_t val = 0;
+    if (ch < 216) {
+      const int tap = ch / 12, c = ch - tap * 12;
+      const int tt = t + tap / 9 - 1, yy = y + (tap / 3) % 3 - 1, xx = x + tap % 3 - 1;
+      if (tt >= 0 && yy >= 0 && yy < Ht && xx >= 0 && xx < Wt)
+        val = codes[((((gt - t + tt) * Ht) + yy) * Wt + xx) * 16 + c];
+    }
+    v[j] = val;
+  }
+  *reinterpret_cast<uint4*>(out + e * 16) = *reinterpret_cast<const uint4*>(v);
+}
+
+static int l8_gather(const int8_t* codes, int G, int Ht, int Wt, void* out, cudaStream_t st) {
+  const int64_t total = (int64_t)G * 2 * Ht * Wt * 16;
+  k_l8_gather233<<<(unsigned)ceil_div64(total, 256), 256, 0, st>>>(codes, G, Ht, Wt,
+                                                                   static_cast<int8_t*>(out));
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+}  // namespace sst
+
+extern "C" int sst_lt8_dec_in(const double* tok, const uint8_t* mask, int G, int Ht, int Wt, void* ws,
+                              void* out, void* stream) {
+  if (!tok || !mask || !ws || !out || G <= 0 || Ht <= 0 || Wt <= 0) return SST_ERR_ARG;
+  if ((reinterpret_cast<uintptr_t>(ws) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
+    return SST_ERR_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int64_t n = (int64_t)Ht * Wt;
+  k_l8_codes_tok<<<(unsigned)ceil_div64((int64_t)G * 2 * n, 256), 256, 0, st>>>(
+      tok, mask, G, n, static_cast<int8_t*>(ws));
+  SST_LAUNCH_CHECK();
+  return l8_gather(static_cast<const int8_t*>(ws), G, Ht, Wt, out, st);
+}
+
+extern "C" int64_t sst_lt8_unpack_workspace(int G, int Ht, int Wt) {
+  const int64_t base = (sst_unpack_decode_workspace(G, Ht, Wt) + 15) / 16 * 16;
+  return base + 2 * (int64_t)G * Ht * Wt * 16;
+}
+
+extern "C" int sst_lt8_unpack_dec_in(const uint8_t* buf, const int64_t* off, SstPacketInfo* info,
+                                     const int32_t* target, int64_t n, int G, int Ht, int Wt,
+                                     const uint32_t* exp_gop, uint32_t* winner, int32_t* stats,
+                                     void* ws, void* out, void* stream) {
+  if (n < 0 || G < 0 || Ht <= 0 || Wt <= 0) return SST_ERR_ARG;
+  if (G == 0) return SST_OK;
+  if (!exp_gop || !winner || !stats || !out || !ws) return SST_ERR_ARG;
+  if (n > 0 && (!buf || !off || !info || !target)) return SST_ERR_ARG;
+  if (Ht > 65535 || G > 65535) return SST_ERR_ARG;
+  if ((reinterpret_cast<uintptr_t>(ws) & 15) || (reinterpret_cast<uintptr_t>(out) & 15))
+    return SST_ERR_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = route_packets(info, target, n, 2 * G, Ht, nullptr, exp_gop, winner, stats, st);
+  if (rc != SST_OK) return rc;
+  const int64_t nrows = 2 * (int64_t)G * Ht;
+  RowInfo* rows = static_cast<RowInfo*>(ws);
+  int32_t* tokoff = reinterpret_cast<int32_t*>(rows + nrows);
+  int8_t* codes = static_cast<int8_t*>(ws) + (sst_unpack_decode_workspace(G, Ht, Wt) + 15) / 16 * 16;
+  k_rowprep<<<(unsigned)ceil_div64(nrows, 8), 256, 0, st>>>(off, info, buf, winner, nrows, Ht, Wt,
+                                                            rows, tokoff, stats);
+  SST_LAUNCH_CHECK();
+  const int64_t total = nrows * Wt;
+  k_l8_codes_pkt<<<(unsigned)ceil_div64(total, 256), 256, 0, st>>>(buf, rows, tokoff, G, Ht, Wt,
+                                                                   codes);
+  SST_LAUNCH_CHECK();
+  return l8_gather(codes, G, Ht, Wt, out, st);
+}

@@ -47,6 +47,29 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32_bmn(int M, int N) {
   return idesc_bf16_f32(M, N) | (1u << 16);
 }
 
+// Instruction descriptor, kind::i8: D format s32 (2), A / B format 1 = s8,
+// 0 = u8, both operands K-major.  The smem layout of an int8 K-major tile is
+// byte-for-byte that of a bf16 one (128-byte swizzled rows, here 128 int8),
+// and one MMA consumes K = 32 int8 = 32 bytes, so the descriptors advance by
+// the same 32 bytes per instruction as for bf16.
+__host__ __device__ constexpr uint32_t idesc_i8_s32(int M, int N, bool a_signed = true,
+                                                     bool b_signed = true) {
+  return (2u << 4) | ((a_signed ? 1u : 0u) << 7) | ((b_signed ? 1u : 0u) << 10) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                       uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
 __device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
                                          uint32_t idesc, uint32_t accumulate) {
   asm volatile(
@@ -206,6 +229,17 @@ __device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t adesc, u
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+__device__ __forceinline__ void mma_i8_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 // commit to the barrier at the same smem offset in both CTAs of the pair
 __device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
   asm volatile(
@@ -234,5 +268,9 @@ __device__ __forceinline__ void tmem_dealloc_pair(uint32_t taddr, uint32_t ncols
 bool make_tmap_bf16_5d(CUtensorMap* map, const void* base, const uint64_t dims[5], uint32_t b1,
                        uint32_t b2);
 bool make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint32_t b1);
+// int8 / uint8 tensor maps, same 128-byte swizzle (box inner extent = 128 bytes)
+bool make_tmap_u8_5d(CUtensorMap* map, const void* base, const uint64_t dims[5], uint32_t b1,
+                     uint32_t b2);
+bool make_tmap_u8_2d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint32_t b1);
 
 }  // namespace sst

@@ -83,3 +83,46 @@ bool make_tmap_bf16_2d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t
 }
 
 }  // namespace sst
+
+namespace sst {
+
+// int8 activations / weights of the int8 learned tokenizer (learned_i8.cu):
+// the same 128-byte swizzled K-major tiles, 128 one-byte elements per row.
+bool make_tmap_u8_5d(CUtensorMap* map, const void* base, const uint64_t dims[5], uint32_t b1,
+                     uint32_t b2) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  if (reinterpret_cast<uintptr_t>(base) & 15u) return false;
+  cuuint64_t gdim[5];
+  cuuint64_t gstride[4];
+  uint64_t stride = 1;
+  for (int i = 0; i < 5; ++i) {
+    if (dims[i] == 0 || dims[i] >= (1ull << 32)) return false;
+    gdim[i] = dims[i];
+    stride *= dims[i];
+    if (i < 4) gstride[i] = stride;
+  }
+  if (gstride[0] & 15u) return false;
+  cuuint32_t box[5] = {128, b1, b2, 1, 1};
+  cuuint32_t estride[5] = {1, 1, 1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 5, const_cast<void*>(base), gdim, gstride,
+                  box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool make_tmap_u8_2d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d1, uint32_t b1) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  if ((reinterpret_cast<uintptr_t>(base) & 15u) || (d0 & 15u)) return false;
+  cuuint64_t gdim[2] = {d0, d1};
+  cuuint64_t gstride[1] = {d0};
+  cuuint32_t box[2] = {128, b1};
+  cuuint32_t estride[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), gdim, gstride,
+                  box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace sst

@@ -1,0 +1,423 @@
+"""Int8 learned tokenizer, exact by construction.
+
+The same plug-in and the same shape of network as ``learned.py`` (causal
+(2,3,3) conv residual blocks, a causal 8x8-window attention block, FSQ head,
+mask-aware decoder, 8x/8x compression behind the reference's tokenizer hook,
+session.py:57-61), but every layer is integer arithmetic on the B200's
+``tcgen05.mma .kind::i8`` tensor cores: int8 activations and weights, int32
+accumulators in TMEM (exact: |acc| <= 4608 * 127^2 < 2^31), integer
+requantisation with arithmetic shifts, and table lookups for SiLU and the
+attention softmax.  Results therefore do not depend on summation order, and
+the GPU agrees with the numpy oracle (``oracle/learned_i8_oracle.py``, which
+documents the arithmetic) bit for bit: 100 % FSQ index agreement and
+identical decoded frames -- the north star's ">= 99.9 % index agreement"
+met with no tolerance at all.  int8 also runs at twice the bf16 tensor rate.
+
+Weights are seeded random-init (BASELINE.json configs[0]); the per-layer
+shifts are fixed functions of the fan-in so activations use the int8 range.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+FSQ_LEVELS = (8, 8, 8, 5, 5, 5, 8, 8, 8, 5, 5, 5)
+FSQ_CHANNELS = len(FSQ_LEVELS)
+PATCH_I, PATCH_I_PAD, PATCH_P = 192, 256, 1536
+DEC_IN_K = 256                        # 2 x 9 x 12 = 216 gathered code channels + 40 zero
+HEAD_DIM = 128                        # one 128-byte swizzled row of int8 per head
+TAPS_233 = [(kt - 1, ky - 1, kx - 1) for kt in range(2) for ky in range(3) for kx in range(3)]
+ACT_SCALE = 32.0                      # int8 activation units per 1.0 (SiLU table)
+EXP_TEMP = 8.0                        # EXP[t] = rint(255 exp(-t / 8))
+
+
+@dataclass(frozen=True)
+class LearnedI8Config:
+    dim: int = 256          # latent channels D (multiple of 256)
+    blocks: int = 2         # residual blocks per side
+    seed: int = 0
+    attn: bool = True
+
+    def __post_init__(self):
+        if self.dim <= 0 or self.dim % 256:
+            raise ValueError(f"dim must be a positive multiple of 256, got {self.dim}")
+        if not 0 <= self.blocks <= 8:
+            raise ValueError(f"blocks must be in [0, 8], got {self.blocks}")
+
+
+def silu_table() -> np.ndarray:
+    x = (np.arange(256) - 128) / ACT_SCALE
+    y = x / (1.0 + np.exp(-x))
+    return np.clip(np.rint(y * ACT_SCALE), -127, 127).astype(np.int8)
+
+
+def exp_table() -> np.ndarray:
+    return np.rint(255.0 * np.exp(-np.arange(256) / EXP_TEMP)).astype(np.uint8)
+
+
+def _shift(k_eff: int, sx: float, sw: float, st: float) -> int:
+    return max(1, int(round(math.log2(math.sqrt(k_eff) * sx * sw / st))))
+
+
+def make_weights_i8(cfg: LearnedI8Config) -> dict:
+    """Seeded random-init int8 weights [N][K] (K = tap-major, channel-minor),
+    int32 biases and per-layer requantisation shifts."""
+    rng = np.random.default_rng(cfg.seed)
+    D = cfg.dim
+    SW = 24.0
+    W, b, sh = {}, {}, {}
+
+    def layer(name, n, k, k_eff, sx, st, bias_std=2.0, bias_mean=0.0, zero_from=None):
+        w = np.clip(np.rint(rng.standard_normal((n, k)) * SW), -127, 127).astype(np.int8)
+        if zero_from is not None:
+            w[:, zero_from:] = 0
+        s = _shift(k_eff, sx, SW, st)
+        W[name] = w
+        sh[name] = s
+        b[name] = np.rint((rng.standard_normal(n) * bias_std + bias_mean) * (1 << s)).astype(np.int32)
+
+    layer("pe_i", D, PATCH_I_PAD, PATCH_I, 60.0, 40.0, zero_from=PATCH_I)
+    layer("pe_p", D, PATCH_P, PATCH_P, 60.0, 40.0)
+    K3 = len(TAPS_233) * D
+    for part in ("enc", "dec"):
+        for i in range(cfg.blocks):
+            layer(f"{part}{i}_c1", D, K3, K3, 40.0, 40.0)
+            layer(f"{part}{i}_c2", D, K3, K3, 25.0, 16.0)
+    # FSQ head: z >> sh spans about +-4 FSQ steps
+    layer("head", 16, D, D, 40.0, 2.0, bias_std=0.25)
+    W["head"][FSQ_CHANNELS:] = 0
+    b["head"][FSQ_CHANNELS:] = 0
+    layer("dec_in", D, DEC_IN_K, 216, 37.0, 40.0, zero_from=216)
+    layer("out_i", PATCH_I, D, D, 40.0, 40.0, bias_std=4.0, bias_mean=128.0)
+    layer("out_p", PATCH_P, D, D, 40.0, 40.0, bias_std=4.0, bias_mean=128.0)
+    if cfg.attn:            # drawn last: the weights above do not depend on cfg.attn
+        for part in ("enc", "dec"):
+            layer(f"{part}_qkv", 3 * D, D, D, 40.0, 32.0)
+            layer(f"{part}_proj", D, D, D, 20.0, 16.0)
+    # attention logits: S = q.k over 128 dims, std ~ sqrt(128) 32^2; one
+    # EXP step = 1/8 nat, so (max - S) >> sh_s spans ~2 nats per S std
+    attn_shift = _shift(HEAD_DIM, 32.0, 32.0, 16.0 * 8.0 / 1.5)
+    return {"W": W, "b": b, "sh": sh, "silu": silu_table(), "exp": exp_table(),
+            "attn_shift": attn_shift, "head_dim": HEAD_DIM, "blocks": cfg.blocks,
+            "attn": cfg.attn, "dim": D}
+
+
+# ---------------------------------------------------------------------------
+# device model
+
+import ctypes as C            # noqa: E402
+
+import torch                  # noqa: E402
+
+from . import _dev, _lib      # noqa: E402
+from .codec import CodecConfig, TokenMatrix, token_grid_shape  # noqa: E402
+from .pipeline import CHANNELS, GopCodec, check_gop_tensor      # noqa: E402
+from .video import GOP_SIZE, Frame, GoP                          # noqa: E402
+
+
+def _taps_array(taps):
+    arr = ((C.c_int32 * 3) * 27)()
+    for i, (dt, dy, dx) in enumerate(taps):
+        arr[i][0], arr[i][1], arr[i][2] = dt, dy, dx
+    return arr
+
+
+_TAPS_233_ARR = _taps_array(TAPS_233)
+_TAP_0 = _taps_array([(0, 0, 0)])
+_TAP_M1 = _taps_array([(-1, 0, 0)])
+
+
+class LearnedTokenizerI8:
+    """Device-resident int8 learned tokenizer (weights int8 on the GPU); every
+    layer is one kind::i8 tcgen05 launch (``sst_lt8_conv``)."""
+
+    def __init__(self, cfg: LearnedI8Config | None = None, weights: dict | None = None):
+        self.cfg = cfg or LearnedI8Config()
+        dev = _dev.device()
+        host = weights if weights is not None else make_weights_i8(self.cfg)
+        self.host_weights = host
+        self.W = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in host["W"].items()}
+        self.b = {k: torch.from_numpy(np.ascontiguousarray(v, dtype=np.int32)).to(dev)
+                  for k, v in host["b"].items()}
+        self.sh = dict(host["sh"])
+        self.silu = torch.from_numpy(host["silu"].copy()).to(dev)
+        self.exp = torch.from_numpy(host["exp"].copy()).to(dev)
+        self.launches = 0
+
+    # ---- one layer ----------------------------------------------------------
+    def _conv(self, name, x, in_shape, out_grid, taps, t_lo, t_cnt, epi, *, act=0,
+              residual=None, out=None, out_T=2, codes=None, idx=None, mask=None, frames=None,
+              hw=(0, 0), frame_base=0):
+        G, T_in, H_in, W_in, C_in = in_shape
+        Ht, Wt = out_grid
+        W = self.W[name]
+        d = _lib.SstConvDesc()
+        d.in_ = x.data_ptr()
+        d.in_C, d.in_W, d.in_H, d.in_T = C_in, W_in, H_in, T_in
+        d.G, d.Ht, d.Wt, d.t_lo, d.t_cnt = G, Ht, Wt, t_lo, t_cnt
+        d.n_taps = taps[0]
+        d.taps = taps[1]
+        d.weight = W.data_ptr()
+        d.N, d.K = W.shape
+        d.bias = None
+        d.bias_i32 = self.b[name].data_ptr()
+        d.shift = self.sh[name]
+        d.epi, d.act = epi, act
+        d.act_lut = self.silu.data_ptr() if act else None
+        d.residual = residual.data_ptr() if residual is not None else None
+        d.out = out.data_ptr() if out is not None else None
+        d.out_T = out_T
+        d.codes = codes.data_ptr() if codes is not None else None
+        d.idx = idx.data_ptr() if idx is not None else None
+        d.mask = mask.data_ptr() if mask is not None else None
+        d.frames = frames.data_ptr() if frames is not None else None
+        d.h, d.w = hw
+        d.frame_base = frame_base
+        _lib.call("sst_lt8_conv", C.byref(d), _dev.stream())
+        self.launches += 1
+
+    def _blocks(self, part, h, u, G, Ht, Wt):
+        D = self.cfg.dim
+        shape = (G, 2, Ht, Wt, D)
+        t233 = (18, _TAPS_233_ARR)
+        for i in range(self.cfg.blocks):
+            self._conv(f"{part}{i}_c1", h, shape, (Ht, Wt), t233, 0, 2, _lib.LT_EPI_STORE,
+                       act=1, out=u)
+            self._conv(f"{part}{i}_c2", u, shape, (Ht, Wt), t233, 0, 2, _lib.LT_EPI_STORE,
+                       residual=h, out=h)
+
+    def _attention(self, part, h, G, Ht, Wt):
+        """h = sat(h + proj(WindowAttention(qkv(h)))): qkv and proj are 1x1
+        int8 GEMMs, the core (S = QK^T, integer softmax, O = PV) one
+        sst_lt8_attn launch."""
+        if not self.cfg.attn:
+            return
+        D = self.cfg.dim
+        shape = (G, 2, Ht, Wt, D)
+        qkv = torch.empty((G, 2, Ht, Wt, 3 * D), dtype=torch.int8, device=h.device)
+        self._conv(f"{part}_qkv", h, shape, (Ht, Wt), (1, _TAP_0), 0, 2, _lib.LT_EPI_STORE,
+                   out=qkv)
+        o = torch.empty_like(h)
+        _lib.call("sst_lt8_attn", qkv.data_ptr(), G, Ht, Wt, D, self.host_weights["attn_shift"],
+                  self.exp.data_ptr(), o.data_ptr(), _dev.stream())
+        self.launches += 1
+        self._conv(f"{part}_proj", o, shape, (Ht, Wt), (1, _TAP_0), 0, 2, _lib.LT_EPI_STORE,
+                   residual=h, out=h)
+
+    # ---- encoder ------------------------------------------------------------
+    def encode_frames(self, frames: torch.Tensor, s: int = 1, codes: torch.Tensor | None = None,
+                      mask: torch.Tensor | None = None, idx: torch.Tensor | None = None):
+        """frames float32 [G][9][H][W][3] on the GPU (full resolution for s in
+        {2,3}: the box downscale is fused into the patchify pass).  Returns
+        (codes f64 [G][2][H'][W'][12], idx i32 [G][2][H'][W'][2], mask u8
+        [G][2][H'][W'], (h, w))."""
+        if frames.dtype != torch.float32 or frames.dim() != 5 or frames.shape[1] != GOP_SIZE \
+                or frames.shape[4] != 3:
+            raise ValueError("frames must be float32 [G][9][H][W][3]")
+        frames = frames.contiguous()
+        G, _, H, Wd, _ = frames.shape
+        h, w = -(-H // s), -(-Wd // s)
+        Ht, Wt = token_grid_shape(h, w)
+        D = self.cfg.dim
+        dev = frames.device
+        pI = torch.empty((G, 1, Ht, Wt, PATCH_I_PAD), dtype=torch.int8, device=dev)
+        pP = torch.empty((G, 1, Ht, Wt, PATCH_P), dtype=torch.int8, device=dev)
+        _lib.call("sst_lt8_patchify", frames.data_ptr(), G, H, Wd, s, pI.data_ptr(),
+                  pP.data_ptr(), _dev.stream())
+        self.launches += 1
+        hbuf = torch.empty((G, 2, Ht, Wt, D), dtype=torch.int8, device=dev)
+        ubuf = torch.empty_like(hbuf)
+        self._conv("pe_i", pI, (G, 1, Ht, Wt, PATCH_I_PAD), (Ht, Wt), (1, _TAP_0), 0, 1,
+                   _lib.LT_EPI_STORE, out=hbuf)
+        self._conv("pe_p", pP, (G, 1, Ht, Wt, PATCH_P), (Ht, Wt), (1, _TAP_M1), 1, 1,
+                   _lib.LT_EPI_STORE, out=hbuf)
+        self._blocks("enc", hbuf, ubuf, G, Ht, Wt)
+        self._attention("enc", hbuf, G, Ht, Wt)
+        if codes is None:
+            codes = torch.zeros((G, 2, Ht, Wt, FSQ_CHANNELS), dtype=torch.float64, device=dev)
+        if idx is None:
+            idx = torch.zeros((G, 2, Ht, Wt, 2), dtype=torch.int32, device=dev)
+        if mask is None:
+            mask = torch.zeros((G, 2, Ht, Wt), dtype=torch.uint8, device=dev)
+        for t_, shp in ((codes, (G, 2, Ht, Wt, FSQ_CHANNELS)), (idx, (G, 2, Ht, Wt, 2)),
+                        (mask, (G, 2, Ht, Wt))):
+            if tuple(t_.shape) != shp or not t_.is_contiguous():
+                raise ValueError(f"output buffer must be a contiguous {shp} tensor")
+        self._conv("head", hbuf, (G, 2, Ht, Wt, D), (Ht, Wt), (1, _TAP_0), 0, 2,
+                   _lib.LT_EPI_FSQ, codes=codes, idx=idx, mask=mask)
+        return codes, idx, mask, (h, w)
+
+    # ---- decoder ------------------------------------------------------------
+    def decode_tokens(self, tokens: torch.Tensor, mask: torch.Tensor, hw,
+                      frames: torch.Tensor | None = None) -> torch.Tensor:
+        """tokens float64 [G][2][H'][W'][12] (received codes; masked = 0),
+        mask u8 [G][2][H'][W'] -> working-resolution frames f32 [G][9][h][w][3]."""
+        if tokens.dtype != torch.float64 or tokens.dim() != 5 or tokens.shape[1] != 2 \
+                or tokens.shape[4] != FSQ_CHANNELS:
+            raise ValueError("tokens must be float64 [G][2][H'][W'][12]")
+        tokens = tokens.contiguous()
+        mask = mask.to(torch.uint8).contiguous()
+        G, _, Ht, Wt, _ = tokens.shape
+        h, w = hw
+        if not (0 < h <= Ht * 8 and 0 < w <= Wt * 8):
+            raise ValueError(f"frame shape {hw} does not fit a {Ht}x{Wt} token grid")
+        dev = tokens.device
+        ws = torch.empty((G, 2, Ht, Wt, 16), dtype=torch.int8, device=dev)
+        x = torch.empty((G, 2, Ht, Wt, DEC_IN_K), dtype=torch.int8, device=dev)
+        _lib.call("sst_lt8_dec_in", tokens.data_ptr(), mask.data_ptr(), G, Ht, Wt, ws.data_ptr(),
+                  x.data_ptr(), _dev.stream())
+        self.launches += 2
+        return self.decode_inputs(x, hw, frames)
+
+    def decode_inputs(self, x: torch.Tensor, hw, frames: torch.Tensor | None = None
+                      ) -> torch.Tensor:
+        """Decoder from its gathered int8 input [G][2][H'][W'][256]."""
+        G, _, Ht, Wt, _ = x.shape
+        h, w = hw
+        D = self.cfg.dim
+        dev = x.device
+        hbuf = torch.empty((G, 2, Ht, Wt, D), dtype=torch.int8, device=dev)
+        ubuf = torch.empty_like(hbuf)
+        self._conv("dec_in", x, (G, 2, Ht, Wt, DEC_IN_K), (Ht, Wt), (1, _TAP_0), 0, 2,
+                   _lib.LT_EPI_STORE, act=1, out=hbuf)
+        self._attention("dec", hbuf, G, Ht, Wt)
+        self._blocks("dec", hbuf, ubuf, G, Ht, Wt)
+        if frames is None:
+            frames = torch.empty((G, GOP_SIZE, h, w, 3), dtype=torch.float32, device=dev)
+        elif tuple(frames.shape) != (G, GOP_SIZE, h, w, 3) or not frames.is_contiguous():
+            raise ValueError("frames buffer must be a contiguous [G][9][h][w][3] tensor")
+        self._conv("out_i", hbuf, (G, 2, Ht, Wt, D), (Ht, Wt), (1, _TAP_0), 0, 1,
+                   _lib.LT_EPI_PIXELS, frames=frames, hw=(h, w), frame_base=0)
+        self._conv("out_p", hbuf, (G, 2, Ht, Wt, D), (Ht, Wt), (1, _TAP_0), 1, 1,
+                   _lib.LT_EPI_PIXELS, frames=frames, hw=(h, w), frame_base=1)
+        return frames
+
+    def ops_per_gop(self, Ht: int, Wt: int) -> int:
+        """Useful int8 tensor-core ops of one GoP (2 latent frames of Ht x Wt
+        tokens): the padded K of the patch / decoder-input layers and the
+        t = 0 causal taps (skipped by the kernels) are not counted."""
+        D, n = self.cfg.dim, Ht * Wt
+        k3 = len(TAPS_233) * D
+        blocks = 2 * self.cfg.blocks * 2 * n * D * (k3 + k3 // 2)      # t=1: 18 taps, t=0: 9
+        enc = 2 * n * D * (PATCH_I + PATCH_P) + blocks + 2 * (2 * n) * FSQ_CHANNELS * D
+        dec = 2 * (2 * n) * 216 * D + blocks + 2 * n * D * (PATCH_I + PATCH_P)
+        attn = 0
+        if self.cfg.attn:
+            proj = 2 * (2 * n) * D * 4 * D                    # qkv (3D) + proj (D)
+            core = 2 * 2 * (2 * n) * 128 * D                  # S and PV over 128 keys
+            attn = 2 * (proj + core)
+        return enc + dec + attn
+
+
+class LearnedI8Plugin:
+    """(encode, decode) pair for SessionConfig.tokenizer_encode/_decode
+    (session.py:57-61): the int8 model on the already downscaled working GoP."""
+
+    def __init__(self, cfg: LearnedI8Config | None = None):
+        self.model = LearnedTokenizerI8(cfg)
+
+    def encode(self, gop: GoP, cfg: CodecConfig):
+        frames = np.stack([f.samples for f in gop.frames])[None]
+        codes, _, mask, (h, w) = self.model.encode_frames(_dev.h2d(frames, np.float32), 1)
+        vals = _dev.d2h(codes)[0]
+        m = _dev.d2h(mask)[0].astype(bool)
+        return (TokenMatrix("I", vals[0], m[0], gop_id=gop.gop_id, frame_shape=(h, w)),
+                TokenMatrix("P", vals[1], m[1], gop_id=gop.gop_id, frame_shape=(h, w)))
+
+    def decode(self, i_tokens: TokenMatrix, p_tokens: TokenMatrix, cfg: CodecConfig) -> GoP:
+        if i_tokens.values.shape != p_tokens.values.shape:
+            raise ValueError("I and P token matrices differ in shape")
+        if i_tokens.values.shape[2] != FSQ_CHANNELS:
+            raise ValueError(f"learned tokenizer expects {FSQ_CHANNELS} channels")
+        h, w = i_tokens.frame_shape
+        tok = np.stack([i_tokens.values, p_tokens.values])[None]
+        mask = np.stack([i_tokens.mask, p_tokens.mask])[None].astype(np.uint8)
+        frames = _dev.d2h(self.model.decode_tokens(_dev.h2d(tok, np.float64),
+                                                   _dev.h2d(mask, np.uint8), (h, w)))[0]
+        out = tuple(Frame(frames[t], timestamp_index=t) for t in range(GOP_SIZE))
+        return GoP(gop_id=i_tokens.gop_id, frames=out)
+
+
+class LearnedI8GopCodec(GopCodec):
+    """``pipeline.GopCodec`` with the int8 learned tokenizer: encoder + FSQ
+    (kind::i8), similarity, intelligent drop and 8-bit packetisation
+    (unchanged K2/K3), parse, reassembly fused with the decoder input
+    (sst_lt8_unpack_dec_in), the int8 decoder, and K5 for 9 distinct frames
+    with the boundary blend (sst_upscale_blend9)."""
+
+    def __init__(self, g_max: int, H: int, W: int, s: int, blend_n: int = 2,
+                 model: LearnedTokenizerI8 | None = None, cfg: LearnedI8Config | None = None):
+        super().__init__(g_max, H, W, s, blend_n)
+        self.model = model if model is not None else LearnedTokenizerI8(cfg)
+        dev = self.tok.device
+        self.idx = torch.empty((g_max, 2, self.Ht, self.Wt, 2), dtype=torch.int32, device=dev)
+        self.dec_x = torch.empty((g_max, 2, self.Ht, self.Wt, DEC_IN_K), dtype=torch.int8,
+                                 device=dev)
+        ws = _lib.load().sst_lt8_unpack_workspace(g_max, self.Ht, self.Wt)
+        self.dec_ws = torch.empty((ws,), dtype=torch.uint8, device=dev)
+        self.frames9 = [torch.empty((g_max, GOP_SIZE, self.h, self.w, 3), dtype=torch.float32,
+                                    device=dev) for _ in range(2)]
+        self.prev_desc = []
+        for par in range(2):
+            d = np.zeros(g_max, dtype=_lib.PREV_DTYPE)
+            src = self.frames9[1 - par]
+            d["p_img"] = src.data_ptr() + np.arange(g_max, dtype=np.uint64) * np.uint64(
+                src[0].numel() * 4)
+            d["h"], d["w"], d["s"] = self.h, self.w, s
+            self.prev_desc.append(torch.from_numpy(d.view(np.uint8).copy()).to(dev))
+        self.parity = 0
+        self.primed = False
+
+    def tokenize(self, frames: torch.Tensor, g: int) -> None:
+        tm = self.timer
+        tm.begin("L_encode")
+        self.model.encode_frames(frames[:g], self.s, codes=self.tok[:g], mask=self.mask[:g],
+                                 idx=self.idx[:g])
+        tm.end("L_encode")
+        tm.begin("L_similarity")
+        _lib.call("sst_similarity_gop", self.tok.data_ptr(), g, self.n, CHANNELS,
+                  self.sim.data_ptr(), _dev.stream())
+        tm.end("L_similarity")
+
+    def decode(self, g: int, parity: int, arena: torch.Tensor | None = None,
+               present: torch.Tensor | None = None) -> torch.Tensor:
+        st = _dev.stream()
+        arena = self.arena if arena is None else arena
+        npk = g * self.n_pkt_per_gop
+        tm = self.timer
+        tm.begin("K4_parse")
+        _lib.call("sst_parse", arena.data_ptr(), self.offsets.data_ptr(),
+                  self.lengths.data_ptr(), None if present is None else present.data_ptr(), npk,
+                  self.info.data_ptr(), st)
+        tm.end("K4_parse")
+        tm.begin("K4_unpack_dec_in")
+        _lib.call("sst_lt8_unpack_dec_in", arena.data_ptr(), self.offsets.data_ptr(),
+                  self.info.data_ptr(), self.target.data_ptr(), npk, g, self.Ht, self.Wt,
+                  self.exp_gop.data_ptr(), self.winner.data_ptr(), self.stats.data_ptr(),
+                  self.dec_ws.data_ptr(), self.dec_x.data_ptr(), st)
+        tm.end("K4_unpack_dec_in")
+        tm.begin("L_decode")
+        self.model.decode_inputs(self.dec_x[:g], (self.h, self.w), frames=self.frames9[parity][:g])
+        tm.end("L_decode")
+        return self.frames9[parity][:g]
+
+    def reconstruct(self, g: int, parity: int, out: torch.Tensor, blend: bool = True) -> None:
+        check_gop_tensor(out, g, self.H, self.W, "out")
+        self.timer.begin("K5_upscale_blend")
+        prev = self.prev_desc[parity].data_ptr() if blend else None
+        _lib.call("sst_upscale_blend9", self.frames9[parity].data_ptr(), g, self.h, self.w,
+                  self.s, self.H, self.W, prev, self.blend_n, out.data_ptr(), _dev.stream())
+        self.timer.end("K5_upscale_blend")
+
+    def step(self, frames: torch.Tensor, out: torch.Tensor, g: int, drop_k: int = 0,
+             present: torch.Tensor | None = None) -> None:
+        par = self.parity
+        self.tokenize(frames, g)
+        self.select_and_pack(g, drop_k)
+        self.decode(g, par, present=present)
+        self.reconstruct(g, par, out, blend=self.primed)
+        self.parity ^= 1
+        self.primed = True

@@ -1,0 +1,335 @@
+"""GPU: the int8 learned tokenizer (learned_i8.py) on
+tcgen05 .kind::i8 against the exact numpy oracle (oracle/learned_i8_oracle.py).
+
+All arithmetic is integer, so the bar is BIT-EXACT everywhere -- per layer
+(CTA-pair halo conv, CTA-pair 1x1 GEMM, generic tile kernel, FSQ head, pixel
+epilogue, attention core, patchify, decoder input) and end to end: FSQ
+indices 100 % equal to the oracle's (north_star: >= 99.9 %) and decoded
+frames identical (north_star: <= 1e-2 max abs in bf16 / 1e-4 in fp32)."""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import learned_i8_oracle as LO
+from oracle import semstream_oracle as O
+from oracle.synth import make_clip
+from paper_2602_03529_b200 import _dev, _lib
+from paper_2602_03529_b200 import codec as CC, transport as T, video as V
+from paper_2602_03529_b200.learned_i8 import (DEC_IN_K, PATCH_I_PAD, PATCH_P, TAPS_233,
+                                              LearnedI8Config, LearnedI8GopCodec, LearnedI8Plugin,
+                                              LearnedTokenizerI8, _taps_array, exp_table,
+                                              make_weights_i8, silu_table)
+
+pytestmark = pytest.mark.gpu
+
+SILU = silu_table()
+
+
+def _i8(rng, shape, lo=-127, hi=128):
+    return rng.integers(lo, hi, size=shape).astype(np.int8)
+
+
+def _conv_gpu(x, W, b, sh, taps, t_lo, t_cnt, epi, out_T=2, act=0, residual=None, hw=(0, 0),
+              frame_base=0):
+    """Raw sst_lt8_conv on int8 CUDA tensors; returns the epilogue outputs."""
+    G, T_in, H, Wd, Cin = x.shape
+    dev = _dev.device()
+    xd = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+    Wt = torch.from_numpy(np.ascontiguousarray(W)).to(dev)
+    bd = torch.from_numpy(np.ascontiguousarray(b, dtype=np.int32)).to(dev)
+    lut = torch.from_numpy(SILU.copy()).to(dev)
+    d = _lib.SstConvDesc()
+    d.in_ = xd.data_ptr()
+    d.in_C, d.in_W, d.in_H, d.in_T = Cin, Wd, H, T_in
+    d.G, d.Ht, d.Wt, d.t_lo, d.t_cnt = G, H, Wd, t_lo, t_cnt
+    d.n_taps = len(taps)
+    d.taps = _taps_array(taps)
+    d.weight = Wt.data_ptr()
+    d.N, d.K = W.shape
+    d.bias_i32 = bd.data_ptr()
+    d.shift = sh
+    d.act_lut = lut.data_ptr()
+    d.epi, d.act, d.out_T = epi, act, out_T
+    keep = [xd, Wt, bd, lut]
+    out = {}
+    if epi == _lib.LT_EPI_STORE:
+        o = torch.zeros((G, out_T, H, Wd, W.shape[0]), dtype=torch.int8, device=dev)
+        d.out = o.data_ptr()
+        if residual is not None:
+            r = torch.from_numpy(np.ascontiguousarray(residual)).to(dev)
+            keep.append(r)
+            d.residual = r.data_ptr()
+        out["out"] = o
+    elif epi == _lib.LT_EPI_FSQ:
+        codes = torch.zeros((G, 2, H, Wd, 12), dtype=torch.float64, device=dev)
+        idx = torch.zeros((G, 2, H, Wd, 2), dtype=torch.int32, device=dev)
+        mask = torch.zeros((G, 2, H, Wd), dtype=torch.uint8, device=dev)
+        d.codes, d.idx, d.mask = codes.data_ptr(), idx.data_ptr(), mask.data_ptr()
+        out.update(codes=codes, idx=idx, mask=mask)
+    else:
+        fr = torch.full((G, 9, hw[0], hw[1], 3), -1.0, dtype=torch.float32, device=dev)
+        d.frames, (d.h, d.w), d.frame_base = fr.data_ptr(), hw, frame_base
+        out["frames"] = fr
+    rc = _lib.load().sst_lt8_conv(C.byref(d), C.c_void_p(_dev.stream()))
+    assert rc == 0, rc
+    torch.cuda.synchronize()
+    return {k: v.cpu().numpy() for k, v in out.items()}
+
+
+def _w(rng, n, k):
+    return np.clip(np.rint(rng.standard_normal((n, k)) * 24), -127, 127).astype(np.int8)
+
+
+def _ref_store(x, W, b, sh, taps, act, residual):
+    cols = LO.im2col233(x) if len(taps) == 18 else x
+    return LO.requant(LO.gemm(cols, W), b, sh, SILU if act else None, residual)
+
+
+@pytest.mark.parametrize("mode", ["pair", "tile"])
+@pytest.mark.parametrize("shape,act,res", [
+    ((1, 2, 16, 16, 256), 1, False),      # one exact 16x16 tile
+    ((1, 2, 45, 80, 256), 0, True),       # 1080p s=3 token grid, ragged tiles, residual
+    ((2, 2, 13, 37, 256), 1, True),       # ragged both ways, act + residual
+])
+def test_conv233_bit_exact(shape, act, res, mode, monkeypatch):
+    if mode == "tile":
+        monkeypatch.setenv("SST_LT8_GEMM", "tile")
+    rng = np.random.default_rng(3)
+    G, Tn, H, Wd, Cin = shape
+    x = _i8(rng, shape)
+    W = _w(rng, 256, 18 * Cin)
+    b = rng.integers(-4000, 4000, 256).astype(np.int32)
+    resid = _i8(rng, (G, Tn, H, Wd, 256)) if res else None
+    got = _conv_gpu(x, W, b, 11, TAPS_233, 0, 2, _lib.LT_EPI_STORE, act=act, residual=resid)["out"]
+    want = _ref_store(x, W, b, 11, TAPS_233, act, resid)
+    assert np.array_equal(got, want)
+
+
+def test_conv233_first_frame_sees_no_past():
+    # the pair kernel skips the t-1 tap at t = 0; frame 0 must equal a conv of
+    # frame 0 alone, whatever frame 1 holds
+    rng = np.random.default_rng(4)
+    x = _i8(rng, (1, 2, 16, 24, 256))
+    W = _w(rng, 256, 18 * 256)
+    b = np.zeros(256, np.int32)
+    a = _conv_gpu(x, W, b, 11, TAPS_233, 0, 2, _lib.LT_EPI_STORE)["out"]
+    x2 = x.copy()
+    x2[:, 1] = _i8(rng, x2[:, 1].shape)
+    b2 = _conv_gpu(x2, W, b, 11, TAPS_233, 0, 2, _lib.LT_EPI_STORE)["out"]
+    assert np.array_equal(a[:, 0], b2[:, 0]) and not np.array_equal(a[:, 1], b2[:, 1])
+
+
+@pytest.mark.parametrize("mode", ["pair", "tile"])
+@pytest.mark.parametrize("cin,n,Tin,t_lo,tap", [
+    (256, 256, 1, 0, (0, 0, 0)),      # I patch embedding (t = 0 of a 1-frame input)
+    (1536, 256, 1, 1, (-1, 0, 0)),    # P patch embedding (output t = 1 reads input t = 0)
+    (256, 768, 2, 0, (0, 0, 0)),      # qkv projection
+])
+def test_one_by_one_bit_exact(cin, n, Tin, t_lo, tap, mode, monkeypatch):
+    if mode == "tile":
+        monkeypatch.setenv("SST_LT8_GEMM", "tile")
+    rng = np.random.default_rng(5)
+    Ht, Wt = 19, 35
+    x = _i8(rng, (2, Tin, Ht, Wt, cin))
+    W = _w(rng, n, cin)
+    b = rng.integers(-2000, 2000, n).astype(np.int32)
+    t_cnt = 2 if Tin == 2 else 1
+    got = _conv_gpu(x, W, b, 9, [tap], t_lo, t_cnt, _lib.LT_EPI_STORE)["out"]
+    want = LO.requant(LO.gemm(x, W), b, 9)
+    if Tin == 2:
+        assert np.array_equal(got, want)
+    else:
+        assert np.array_equal(got[:, t_lo], want[:, 0])
+
+
+def test_fsq_head_bit_exact():
+    rng = np.random.default_rng(6)
+    x = _i8(rng, (2, 2, 21, 30, 256))
+    W = np.zeros((16, 256), np.int8)
+    W[:12] = _w(rng, 12, 256)
+    b = np.zeros(16, np.int32)
+    b[:12] = rng.integers(-3000, 3000, 12)
+    got = _conv_gpu(x, W, b, 13, [(0, 0, 0)], 0, 2, _lib.LT_EPI_FSQ)
+    codes, idx = LO.fsq(LO.gemm(x, W), b, 13)
+    assert np.array_equal(got["codes"], codes) and np.array_equal(got["idx"], idx)
+    assert got["mask"].all()
+
+
+@pytest.mark.parametrize("mode", ["pair", "tile"])
+@pytest.mark.parametrize("Ht,Wt,crop", [(16, 16, (128, 128)), (23, 41, (180, 327))])
+def test_pixels_bit_exact(Ht, Wt, crop, mode, monkeypatch):
+    if mode == "tile":
+        monkeypatch.setenv("SST_LT8_GEMM", "tile")
+    rng = np.random.default_rng(7)
+    w = make_weights_i8(LearnedI8Config())
+    x = _i8(rng, (2, 2, Ht, Wt, 256), -60, 60)
+    wts = {"W": w["W"], "b": w["b"], "sh": w["sh"]}
+    got_i = _conv_gpu(x, wts["W"]["out_i"], wts["b"]["out_i"], wts["sh"]["out_i"], [(0, 0, 0)], 0,
+                      1, _lib.LT_EPI_PIXELS, hw=crop, frame_base=0)["frames"]
+    got_p = _conv_gpu(x, wts["W"]["out_p"], wts["b"]["out_p"], wts["sh"]["out_p"], [(0, 0, 0)], 1,
+                      1, _lib.LT_EPI_PIXELS, hw=crop, frame_base=1)["frames"]
+    # oracle decode tail with h given directly
+    ww = dict(w, blocks=0, attn=False)
+    pix_i = LO.gemm(x[:, 0], ww["W"]["out_i"])
+    q = np.clip(LO.rshift_round(pix_i + ww["b"]["out_i"].astype(np.int64), ww["sh"]["out_i"]), 0, 255)
+    fi = (q.astype(np.float32) / np.float32(255.0)).reshape(2, Ht, Wt, 8, 8, 3).transpose(
+        0, 1, 3, 2, 4, 5).reshape(2, Ht * 8, Wt * 8, 3)[:, :crop[0], :crop[1]]
+    assert np.array_equal(got_i[:, 0], fi)
+    pix_p = LO.gemm(x[:, 1], ww["W"]["out_p"])
+    q = np.clip(LO.rshift_round(pix_p + ww["b"]["out_p"].astype(np.int64), ww["sh"]["out_p"]), 0, 255)
+    fp = (q.astype(np.float32) / np.float32(255.0)).reshape(2, Ht, Wt, 8, 8, 8, 3).transpose(
+        0, 3, 1, 4, 2, 5, 6).reshape(2, 8, Ht * 8, Wt * 8, 3)[:, :, :crop[0], :crop[1]]
+    assert np.array_equal(got_p[:, 1:], fp)
+
+
+@pytest.mark.parametrize("Ht,Wt,D", [(8, 8, 256), (13, 21, 256), (45, 80, 512)])
+def test_attention_core_bit_exact(Ht, Wt, D):
+    rng = np.random.default_rng(8)
+    qkv = _i8(rng, (2, 2, Ht, Wt, 3 * D), -60, 60)
+    lut = exp_table()
+    sh = 8
+    dev = _dev.device()
+    qd = torch.from_numpy(qkv).to(dev)
+    ld = torch.from_numpy(lut.copy()).to(dev)
+    out = torch.zeros((2, 2, Ht, Wt, D), dtype=torch.int8, device=dev)
+    _lib.call("sst_lt8_attn", qd.data_ptr(), 2, Ht, Wt, D, sh, ld.data_ptr(), out.data_ptr(),
+              _dev.stream())
+    torch.cuda.synchronize()
+    want = LO.attention_core(qkv, D, 128, sh, lut)
+    assert np.array_equal(out.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("H,W,s", [(128, 128, 1), (256, 256, 2), (90, 170, 3), (1080, 1920, 3)])
+def test_patchify_bit_exact(H, W, s):
+    rng = np.random.default_rng(9)
+    fr = rng.random((2, 9, H, W, 3)).astype(np.float32)
+    fr[0, :, :5] = 0.0
+    fr[1, :, -3:] = 1.0
+    h, w = -(-H // s), -(-W // s)
+    Ht, Wt = -(-h // 8), -(-w // 8)
+    dev = _dev.device()
+    pI = torch.full((2, 1, Ht, Wt, PATCH_I_PAD), 55, dtype=torch.int8, device=dev)
+    pP = torch.empty((2, 1, Ht, Wt, PATCH_P), dtype=torch.int8, device=dev)
+    _lib.call("sst_lt8_patchify", torch.from_numpy(fr).to(dev).data_ptr(), 2, H, W, s,
+              pI.data_ptr(), pP.data_ptr(), _dev.stream())
+    torch.cuda.synchronize()
+    oi, op, _ = LO.patchify(fr, s)
+    assert np.array_equal(pI.cpu().numpy(), oi) and np.array_equal(pP.cpu().numpy(), op)
+
+
+def test_dec_in_snap_conceal_gather():
+    rng = np.random.default_rng(10)
+    G, Ht, Wt = 2, 9, 14
+    L = np.array(LO.FSQ_LEVELS)
+    hw = L // 2
+    q = rng.integers(-hw, L - hw, size=(G, 2, Ht, Wt, 12))
+    tok = q / hw + rng.uniform(-0.01, 0.01, q.shape)        # 8-bit wire error
+    mask = (rng.random((G, 2, Ht, Wt)) > 0.3).astype(np.uint8)
+    mask[0, 0, 0, :] = 0                                    # lost I row: P concealment finds nothing
+    tok = np.where(mask[..., None] > 0, tok, 0.0)
+    dev = _dev.device()
+    ws = torch.empty((G, 2, Ht, Wt, 16), dtype=torch.int8, device=dev)
+    out = torch.empty((G, 2, Ht, Wt, DEC_IN_K), dtype=torch.int8, device=dev)
+    _lib.call("sst_lt8_dec_in", torch.from_numpy(tok).to(dev).data_ptr(),
+              torch.from_numpy(mask).to(dev).data_ptr(), G, Ht, Wt, ws.data_ptr(), out.data_ptr(),
+              _dev.stream())
+    torch.cuda.synchronize()
+    want = LO.dec_input(LO.snap_codes(tok, mask))
+    assert np.array_equal(out.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("W,H,s,G", [(256, 256, 2, 2), (1280, 720, 3, 1)])
+def test_end_to_end_bit_exact(W, H, s, G):
+    """Encode (patchify -> embeddings -> 2 residual blocks -> attention ->
+    FSQ) and decode (gathered input -> attention -> blocks -> pixels) equal
+    the oracle exactly: 100 % FSQ index agreement, identical frames."""
+    clip = make_clip("moving-square", W, H, 9 * G, seed=3)
+    fr = np.stack([clip.gop(k) for k in range(G)])
+    model = LearnedTokenizerI8(LearnedI8Config())
+    codes, idx, mask, hw = model.encode_frames(torch.from_numpy(fr).cuda(), s)
+    ocodes, oidx, ohw = LO.encode(fr, s, model.host_weights)
+    assert hw == ohw
+    assert np.array_equal(idx.cpu().numpy(), oidx)            # 100 % index agreement
+    assert np.array_equal(codes.cpu().numpy(), ocodes)
+    dec = model.decode_tokens(codes, mask, hw)
+    odec = LO.decode(ocodes, np.ones(ocodes.shape[:-1], np.uint8), hw, model.host_weights)
+    assert np.array_equal(dec.cpu().numpy(), odec)
+
+
+def test_tile_and_pair_paths_identical(monkeypatch):
+    clip = make_clip("noisy-motion", 320, 240, 9, seed=4)
+    fr = torch.from_numpy(clip.gop(0)[None].copy()).cuda()
+    model = LearnedTokenizerI8(LearnedI8Config())
+    a = model.encode_frames(fr, 2)[1].cpu().numpy()
+    monkeypatch.setenv("SST_LT8_GEMM", "tile")
+    b = model.encode_frames(fr, 2)[1].cpu().numpy()
+    assert np.array_equal(a, b)
+
+
+def test_plugin_through_packet_transport():
+    """The plug-in pair with the reference transport in between (drop,
+    packetise, parse, reassemble): decoded frames equal the oracle decode of
+    the reassembled codes exactly."""
+    clip = make_clip("moving-square", 160, 128, 9, seed=2)
+    g = V.GoP(0, tuple(V.Frame(f, timestamp_index=t) for t, f in enumerate(clip.gop(0))))
+    plug = LearnedI8Plugin()
+    work = CC.scale_gop(g, 2, "down")
+    I, P = plug.encode(work, CC.CodecConfig())
+    from paper_2602_03529_b200 import selection as S
+    P = CC.apply_token_mask(P, S.build_drop_mask(S.token_similarity(P, I), 0.25))
+    pk = T.parse_packets([p.to_bytes() for p in T.packetize_tokens(I, 2) + T.packetize_tokens(P, 2)])
+    shp = I.values.shape
+    ri = T.reassemble([p for p in pk if p.kind == "I"], shp, "I", frame_shape=I.frame_shape)
+    rp = T.reassemble([p for p in pk if p.kind == "P"], shp, "P", frame_shape=I.frame_shape)
+    rec = plug.decode(ri, rp, CC.CodecConfig())
+    tok = np.stack([ri.values, rp.values])[None]
+    m = np.stack([ri.mask, rp.mask])[None].astype(np.uint8)
+    want = LO.decode(tok, m, I.frame_shape, plug.model.host_weights)[0]
+    assert np.array_equal(np.stack([f.samples for f in rec.frames]), want)
+
+
+def test_i8_gop_codec_stages_bit_exact():
+    """The batched pipeline (LearnedI8GopCodec): encode codes, packets
+    (8-bit quantiser + CRC on the codes), drop mask, the decoder fed straight
+    from the packets, and K5-9 (upscale + blend) -- every stage equal to the
+    oracles, two steps so the boundary blend runs."""
+    H, W, s, G = 270, 480, 3, 2
+    clips = [make_clip("moving-square" if i % 2 == 0 else "noisy-motion", W, H, 18, seed=i)
+             for i in range(G)]
+    codec = LearnedI8GopCodec(G, H, W, s)
+    w = codec.model.host_weights
+    prev = [None] * G
+    for k in range(2):
+        fr = np.stack([c.gop(k) for c in clips])
+        out = torch.empty((G, 9, H, W, 3), dtype=torch.float32, device="cuda")
+        codec.set_gop_ids([k] * G)
+        codec.step(torch.from_numpy(fr).cuda(), out, G, drop_k=codec.drop_k(0.2))
+        torch.cuda.synchronize()
+        ocodes, _, hw = LO.encode(fr, s, w)
+        arena, lengths = codec.arena.cpu().numpy(), codec.lengths.cpu().numpy()
+        frames9 = codec.frames9[(codec.parity ^ 1)][:G].cpu().numpy()
+        got = out.cpu().numpy()
+        for j in range(G):
+            iv, pv = ocodes[j, 0], ocodes[j, 1]
+            sim = O.similarity(pv, iv)
+            drop = O.top_k_mask(sim, O.drop_count(0.2, sim.size))
+            pv2, pm = O.apply_mask(pv, np.ones(sim.shape, bool), drop)
+            full = np.ones(sim.shape, bool)
+            wire = O.packetize(0, k, iv, full, s) + O.packetize(1, k, pv2, pm, s)
+            npk = codec.n_pkt_per_gop
+            gw = [arena[j * npk + r, :lengths[j * npk + r]].tobytes() for r in range(npk)]
+            assert gw == wire, (k, j)
+            parsed = [O.parse(d) for d in wire]
+            ri, mi = O.reassemble([q for q in parsed if q["kind"] == 0], iv.shape)
+            rp, mp = O.reassemble([q for q in parsed if q["kind"] == 1], iv.shape)
+            dec = LO.decode(np.stack([ri, rp])[None], np.stack([mi, mp])[None].astype(np.uint8),
+                            hw, w)[0]
+            assert np.array_equal(frames9[j], dec), (k, j)
+            up = [O.upscale(f, s, crop=(H, W)) for f in dec]
+            if prev[j] is not None:
+                up = O.blend(prev[j], up, 2)
+            prev[j] = up
+            assert np.array_equal(got[j], np.stack(up)), (k, j)
