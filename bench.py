@@ -73,6 +73,8 @@ def parse_args():
     ap.add_argument("--cpu-workers", type=int, default=0, help="0 = auto")
     ap.add_argument("--no-learned", action="store_true",
                     help="skip the learned-tokenizer leg (SURVEY f4, tensor-core path)")
+    ap.add_argument("--no-learned-bf16", action="store_true",
+                    help="skip the bf16 learned-tokenizer leg (the int8 leg still runs)")
     ap.add_argument("--learned-gops", type=int, default=32)
     ap.add_argument("--learned-lanes", type=int, default=1)
     ap.add_argument("--roofline-steps", type=int, default=3,
@@ -1018,31 +1020,64 @@ def measured_bf16_peak():
         return 2250.0, "nominal dense bf16 (no MEASURED_PEAKS.json)"
 
 
-def run_learned(a, device) -> dict:
-    """G 1080p GoPs per step through LearnedGopCodec (learned encoder + FSQ ->
-    similarity -> 10% drop -> packetise -> parse/reassemble -> learned
-    decoder -> upscale + blend), device-resident, CUDA-event timed; plus one
-    serialised step timing every convolution for the tensor-core roofline."""
+def measured_i8_peak(device) -> tuple:
+    """Dense int8 tensor peak measured in this run: cuBLASLt int8 GEMM
+    (torch._int_mm, 8192^3, int32 out), best of 10 after warm-up -- the int8
+    counterpart of MEASURED_PEAKS.json's bf16_tflops (which has no int8
+    entry).  Falls back to 2 x the measured bf16 peak."""
     import torch
-    from paper_2602_03529_b200.learned import LearnedConfig, LearnedGopCodec
+    try:
+        n = 8192
+        x = torch.randint(-127, 128, (n, n), dtype=torch.int8, device=device)
+        y = torch.randint(-127, 128, (n, n), dtype=torch.int8, device=device)
+        for _ in range(3):
+            torch._int_mm(x, y)
+        best = None
+        for _ in range(10):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch._int_mm(x, y)
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        del x, y
+        return 2 * n ** 3 / (best / 1e3) / 1e12, "measured in-run (cuBLASLt int8 GEMM 8192^3, burst)"
+    except Exception as e:            # pragma: no cover
+        bf, _ = measured_bf16_peak()
+        return 2 * bf, f"2 x measured bf16 peak (int8 GEMM probe failed: {type(e).__name__})"
+
+
+def run_learned(a, device, precision: str = "i8") -> dict:
+    """G 1080p GoPs per step through the learned codec (encoder + FSQ ->
+    similarity -> 10% drop -> packetise -> parse / reassemble -> decoder ->
+    upscale + blend), device-resident, CUDA-event timed; plus one serialised
+    step timing every tensor-core layer for the roofline.  precision "i8":
+    the exact int8 network on tcgen05 kind::i8 (learned_i8.py, the default);
+    "bf16": the bf16 network (learned.py)."""
+    import numpy as np
+    import torch
     G, s, H, W = a.learned_gops, 3, a.height, a.width
-    cfg = LearnedConfig()
-    codec = LearnedGopCodec(G, H, W, s, cfg=cfg)        # full batch: serialised roofline pass
+    if precision == "i8":
+        from paper_2602_03529_b200.learned_i8 import (LearnedI8Config as Cfg,
+                                                      LearnedI8GopCodec as Codec)
+        from oracle import learned_i8_oracle as LO
+    else:
+        from paper_2602_03529_b200.learned import LearnedConfig as Cfg, LearnedGopCodec as Codec
+    cfg = Cfg()
+    codec = Codec(G, H, W, s, cfg=cfg)        # full batch: serialised roofline pass
     model = codec.model
     gen = torch.Generator(device=device).manual_seed(0)
     frames = [torch.rand((G, GOP, H, W, 3), generator=gen, device=device) for _ in range(2)]
     outs = [torch.empty_like(frames[0]) for _ in range(2)]
     drop_k = codec.drop_k(a.drop)
     codec.set_gop_ids(list(range(G)))
-    # timed run: the batch split into lanes on their own CUDA streams (one
-    # model, shared weights) so one lane's tensor-bound convolutions overlap
-    # the other lane's HBM-bound patchify / reconstruction
     nl = max(1, a.learned_lanes)
     cuts = [G * j // nl for j in range(nl + 1)]
     lanes = []
     for j in range(nl):
         n = cuts[j + 1] - cuts[j]
-        c = LearnedGopCodec(n, H, W, s, model=model)
+        c = Codec(n, H, W, s, model=model)
         c.set_gop_ids(list(range(cuts[j], cuts[j + 1])))
         lanes.append(dict(codec=c, sl=slice(cuts[j], cuts[j + 1]), n=n,
                           stream=torch.cuda.Stream(device=device)))
@@ -1078,7 +1113,7 @@ def run_learned(a, device) -> dict:
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / K
     # one stream alone (G = 1, blend on): GoP latency vs the real-time budget
-    c1 = LearnedGopCodec(1, H, W, s, model=model)
+    c1 = Codec(1, H, W, s, model=model)
     c1.set_gop_ids([0])
     k1 = c1.drop_k(a.drop)
     for k in range(3):
@@ -1094,24 +1129,7 @@ def run_learned(a, device) -> dict:
         single.append(b0.elapsed_time(b1))
     single.sort()
     del c1
-    # the same single stream replayed as CUDA graphs (GraphedLearnedGopCodec)
-    from paper_2602_03529_b200.learned import GraphedLearnedGopCodec
-    c1g = LearnedGopCodec(1, H, W, s, model=model)
-    gr = GraphedLearnedGopCodec(c1g, 1, frames[0][:1], outs[0][:1], drop_k=k1)
-    for k in range(3):
-        gr.step([k])
-    torch.cuda.synchronize()
-    single_g = []
-    for k in range(10):
-        b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        b0.record()
-        gr.step([k])
-        b1.record()
-        torch.cuda.synchronize()
-        single_g.append(b0.elapsed_time(b1))
-    single_g.sort()
-    del gr, c1g
-    # serialised pass (full batch, one stream): time every conv launch
+    # serialised pass (full batch, one stream): time every tensor-core layer
     times = []
     orig = model._conv
 
@@ -1121,8 +1139,15 @@ def run_learned(a, device) -> dict:
         orig(name, x, in_shape, out_grid, taps, t_lo, t_cnt, epi, **kw)
         b1.record()
         N, Kd = model.W[name].shape
-        flops = 2 * in_shape[0] * t_cnt * out_grid[0] * out_grid[1] * N * Kd
-        times.append((name, len(taps), b0, b1, flops))
+        nt = taps[0] if isinstance(taps, tuple) else len(taps)
+        tok = in_shape[0] * out_grid[0] * out_grid[1]
+        if nt == 18 and precision == "i8":
+            # useful work: t = 1 sees both temporal taps, t = 0 only its own
+            # (the kernel skips the all-padding t-1 tap there)
+            flops = 2 * tok * N * (Kd + Kd // 2)
+        else:
+            flops = 2 * tok * t_cnt * N * Kd
+        times.append((name, nt, b0, b1, flops))
 
     model._conv = timed
     l0 = model.launches
@@ -1131,38 +1156,61 @@ def run_learned(a, device) -> dict:
         torch.cuda.synchronize()
     finally:
         model._conv = orig
-    # tokenizer kernels (convs, patchify, decoder input) + similarity, top-k,
-    # packetize, parse, 4 reassembly kernels, K5-9
     launches_step = (model.launches - l0) + (1 if drop_k else 0) + 8
     per = [(n, nt, b0.elapsed_time(b1), fl) for n, nt, b0, b1, fl in times]
     halo = [(ms_, fl) for n, nt, ms_, fl in per if nt == 18 and model.W[n].shape[0] % 256 == 0]
     conv_ms = sum(ms_ for _, _, ms_, _ in per)
-    peak, src = measured_bf16_peak()
+    if precision == "i8":
+        peak, src = measured_i8_peak(device)
+        unit, dtype = "TOP/s", "int8 operands, int32 accumulate (TMEM), exact"
+        kern = "k_l8_pair<true> (causal (2,3,3) conv, CTA-pair tcgen05 kind::i8 implicit GEMM)"
+    else:
+        peak, src = measured_bf16_peak()
+        unit, dtype = "TFLOP/s", "bf16 operands, fp32 accumulate (TMEM)"
+        kern = "k_lt_convpair<true> (causal (2,3,3) conv, CTA-pair tcgen05 implicit GEMM)"
     achieved = sum(fl for _, fl in halo) / sum(m for m, _ in halo) / 1e9
-    flops_step = model.flops_per_gop(codec.Ht, codec.Wt) * G
-    return {
+    res = {
+        "precision": precision,
         "lanes": nl,
         "workload": f"{G} x 1080p GoPs per step, s=3, learned causal conv tokenizer "
-                    f"(D={cfg.dim}, {cfg.blocks} residual blocks per side, FSQ 2x(8,8,8,5,5,5)), "
-                    f"{int(a.drop * 100)}% intelligent drop, blend n=2; random-init weights",
+                    f"(D={cfg.dim}, {cfg.blocks} residual blocks per side, window attention, "
+                    f"FSQ 2x(8,8,8,5,5,5)), {int(a.drop * 100)}% intelligent drop, blend n=2; "
+                    f"random-init weights",
         "value": round(G * GOP / ms * 1e3, 1), "unit": UNIT, "ms_per_step": round(ms, 3),
-        "tensor_tflops_path": round(flops_step / ms / 1e9, 1),
-        "roofline": {"kernel": "k_lt_convpair<true> (causal (2,3,3) conv, CTA-pair tcgen05 implicit GEMM)",
-                     "bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
-                     "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "peak_source": src,
-                     "flops_per_launch": halo and int(sum(fl for _, fl in halo) / len(halo)),
+        "roofline": {"kernel": kern, "bound": "tensor", "achieved": round(achieved, 1),
+                     "peak": round(peak, 1), "unit": unit, "frac": round(achieved / peak, 4),
+                     "peak_source": src, "counted": "useful MACs only (no zero-padding taps)"
+                     if precision == "i8" else "all issued MMAs",
+                     "ops_per_launch": halo and int(sum(fl for _, fl in halo) / len(halo)),
                      "avg_launch_ms": round(sum(m for m, _ in halo) / len(halo), 4),
                      "launches_per_step": len(halo)},
         "conv_share_of_serialised_step": round(conv_ms / max(ms, 1e-9), 3),
         "single_stream": {"stream": "1 x 1080p, s=3, learned tokenizer, 10% drop, blend n=2",
                           "gop_ms_median": round(single[len(single) // 2], 3),
                           "gop_ms_max": round(single[-1], 3),
-                          "graph_gop_ms_median": round(single_g[len(single_g) // 2], 3),
                           "realtime_30fps_budget_ms_per_gop": round(GOP / 30 * 1e3, 1)},
         "gpu_launches_per_step": launches_step,
-        "dtype": "bf16 operands, fp32 accumulate (TMEM)",
-        "parity": "tests/test_gpu_learned.py vs oracle/learned_oracle.py (torch fp32, unpinned)",
+        "dtype": dtype,
     }
+    if precision == "i8":
+        ops = model.ops_per_gop(codec.Ht, codec.Wt) * G
+        res["tensor_tops_path"] = round(ops / ms / 1e9, 1)
+        # parity at the bench's own size: one 1080p GoP, GPU vs the exact oracle
+        fr0 = frames[0][:1]
+        codes, idx, mask, hw = model.encode_frames(fr0, s)
+        oc, oi, _ = LO.encode(fr0.cpu().numpy(), s, model.host_weights)
+        dec = model.decode_tokens(codes, mask, hw).cpu().numpy()
+        od = LO.decode(oc, np.ones(oc.shape[:-1], np.uint8), hw, model.host_weights)
+        res["parity_1080p"] = {
+            "fsq_index_agreement": float((idx.cpu().numpy() == oi).mean()),
+            "decoded_frames_bit_exact": bool(np.array_equal(dec, od)),
+            "max_abs_err": float(np.abs(dec - od).max()),
+            "oracle": "oracle/learned_i8_oracle.py (exact integer restatement, unpinned: no "
+                      "reference model)"}
+    else:
+        res["tensor_tflops_path"] = round(model.flops_per_gop(codec.Ht, codec.Wt) * G / ms / 1e9, 1)
+        res["parity"] = "tests/test_gpu_learned.py vs oracle/learned_oracle.py (torch fp32, unpinned)"
+    return res
 
 
 def _free_port() -> int:
@@ -1298,7 +1346,9 @@ def main():
             if a.height == 1080 and a.width == 1920:
                 line["small_configs"] = small_configs(a, dev)
         if world == 1 and not a.no_learned:
-            line["learned_tokenizer"] = run_learned(a, dev)
+            line["learned_tokenizer"] = run_learned(a, dev, "i8")
+            if not a.no_learned_bf16:
+                line["learned_tokenizer_bf16"] = run_learned(a, dev, "bf16")
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.barrier()

@@ -414,35 +414,36 @@ __global__ void k_l8_codes_pkt(const uint8_t* __restrict__ buf, const RowInfo* _
   *reinterpret_cast<uint4*>(codes + idx * 16) = *reinterpret_cast<const uint4*>(q);
 }
 
-// one thread per (token, 16-byte output chunk): 16 chunks of 256 channels
+// one thread per (token, tap): tap < 18 copies the 12 code bytes of that
+// (2,3,3) neighbour (zero outside the frame / before t = 0) to channels
+// 12 tap .. 12 tap + 11 as three 4-byte stores; tap 18 zeroes channels 216..255
 __global__ void k_l8_gather233(const int8_t* __restrict__ codes, int G, int Ht, int Wt,
                                int8_t* __restrict__ out) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n = (int64_t)Ht * Wt;
-  if (e >= (int64_t)G * 2 * n * 16) return;
-  const int chunk = (int)(e & 15);
-  const int64_t tokn = e >> 4;
+  if (e >= (int64_t)G * 2 * n * 19) return;
+  const int tap = (int)(e % 19);
+  const int64_t tokn = e / 19;
+  uint32_t* dst = reinterpret_cast<uint32_t*>(out + tokn * 256);
+  if (tap == 18) {
+#pragma unroll
+    for (int i = 54; i < 64; ++i) dst[i] = 0u;
+    return;
+  }
   const int64_t pos = tokn % n, gt = tokn / n;
   const int t = (int)(gt & 1);
-  const int y = (int)(pos / Wt), x = (int)(pos % Wt);
-  int8_t v[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const int ch = chunk * 16 + j;            // gathered channel = tap * 12 + c
-    int8_t val = 0;
-    if (ch < 216) {
-      const int tap = ch / 12, c = ch - tap * 12;
-      const int tt = t + tap / 9 - 1, yy = y + (tap / 3) % 3 - 1, xx = x + tap % 3 - 1;
-      if (tt >= 0 && yy >= 0 && yy < Ht && xx >= 0 && xx < Wt)
-        val = codes[((((gt - t + tt) * Ht) + yy) * Wt + xx) * 16 + c];
-    }
-    v[j] = val;
-  }
-  *reinterpret_cast<uint4*>(out + e * 16) = *reinterpret_cast<const uint4*>(v);
+  const int y = (int)(pos / Wt), x = (int)(pos - (int64_t)y * Wt);
+  const int tt = t + tap / 9 - 1, yy = y + (tap / 3) % 3 - 1, xx = x + tap % 3 - 1;
+  uint4 v = make_uint4(0, 0, 0, 0);
+  if (tt >= 0 && yy >= 0 && yy < Ht && xx >= 0 && xx < Wt)
+    v = __ldg(reinterpret_cast<const uint4*>(codes + ((((gt - t + tt) * Ht) + yy) * Wt + xx) * 16));
+  dst[tap * 3 + 0] = v.x;
+  dst[tap * 3 + 1] = v.y;
+  dst[tap * 3 + 2] = v.z;
 }
 
 static int l8_gather(const int8_t* codes, int G, int Ht, int Wt, void* out, cudaStream_t st) {
-  const int64_t total = (int64_t)G * 2 * Ht * Wt * 16;
+  const int64_t total = (int64_t)G * 2 * Ht * Wt * 19;
   k_l8_gather233<<<(unsigned)ceil_div64(total, 256), 256, 0, st>>>(codes, G, Ht, Wt,
                                                                    static_cast<int8_t*>(out));
   SST_LAUNCH_CHECK();

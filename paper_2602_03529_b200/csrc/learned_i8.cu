@@ -116,6 +116,13 @@ __device__ __forceinline__ float pixel(int32_t acc, int32_t b, int sh) {
   return __fdiv_rn((float)v, 255.0f);
 }
 
+// the same through a 256-entry table of q / 255 (filled with __fdiv_rn, so
+// identical values; one shared load instead of an IEEE division per sample)
+__device__ __forceinline__ float pixel_lut(int32_t acc, int32_t b, int sh, const float* lut) {
+  int v = (acc + b + (1 << (sh - 1))) >> sh;
+  return lut[min(max(v, 0), 255)];
+}
+
 // ---- generic tile layer -------------------------------------------------------
 template <int BN>
 struct TileCfg {
@@ -368,6 +375,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::THREADS, 1)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = tc::cluster_ctarank();
   const bool leader = rank == 0;
+  __shared__ float pix_lut[kPix ? 256 : 1];
+  if (kPix)
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) pix_lut[i] = __fdiv_rn((float)i, 255.0f);
   if (threadIdx.x == 0) {
     tc::prefetch_tmap(&tmA);
     tc::prefetch_tmap(&tmB);
@@ -494,10 +504,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::THREADS, 1)
 #pragma unroll
         for (int i4 = 0; i4 < 24; ++i4) {
           const int4 bb = __ldg(bp4 + i4);
-          v[4 * i4 + 0] = pixel(__float_as_int(v[4 * i4 + 0]), bb.x, a.shift);
-          v[4 * i4 + 1] = pixel(__float_as_int(v[4 * i4 + 1]), bb.y, a.shift);
-          v[4 * i4 + 2] = pixel(__float_as_int(v[4 * i4 + 2]), bb.z, a.shift);
-          v[4 * i4 + 3] = pixel(__float_as_int(v[4 * i4 + 3]), bb.w, a.shift);
+          v[4 * i4 + 0] = pixel_lut(__float_as_int(v[4 * i4 + 0]), bb.x, a.shift, pix_lut);
+          v[4 * i4 + 1] = pixel_lut(__float_as_int(v[4 * i4 + 1]), bb.y, a.shift, pix_lut);
+          v[4 * i4 + 2] = pixel_lut(__float_as_int(v[4 * i4 + 2]), bb.z, a.shift, pix_lut);
+          v[4 * i4 + 3] = pixel_lut(__float_as_int(v[4 * i4 + 3]), bb.w, a.shift, pix_lut);
         }
         const bool vec = (a.w & 3) == 0;
         const int xs = x0 + 8 * (int)rank;
@@ -630,23 +640,36 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::THREADS, 1)
 // One CTA = one (GoP, 8x8 window, 128-dim head): 128 query rows (2 latent
 // frames x 64 tokens) against the same 128 keys.
 //   S = Q K^T   kind::i8 (s8 x s8), M=128 N=128 K=128 -> TMEM columns 0..127
-//   softmax     thread q: m = max allowed S, e = EXP[min((m - S) >> sh, 255)]
-//               (allowed: valid token of a frame <= the query's), l = sum e,
-//               P = e (uint8) -> smem (over Q)
-//   O = P V     kind::i8 (u8 x s8), M=128 N=128 K=128 -> TMEM columns 128..255
-//   out         clamp(floor((2 O + l) / (2 l)), -127, 127) -> int8
+//   softmax     thread q, two passes over its TMEM row: m = max allowed S,
+//               then e = EXP[min((m - S) >> sh, 255)] (allowed: valid token of
+//               a frame <= the query's), l = sum e, P = e (uint8) -> smem (over Q)
+//   O = P V     kind::i8 (u8 x s8), M=128 N=128 K=128 -> the same TMEM columns
+//               (every S value is in registers / smem by then); V is the B
+//               operand in MN-major form: its rows are the keys exactly as
+//               loaded, no transposed scatter
+//   out         clamp(floor((2 O + l) / (2 l)), -127, 127) -> int8 (division by
+//               a float reciprocal, corrected to the exact integer floor)
+// 128 TMEM columns and ~50 KB of smem per CTA: four CTAs share an SM.
 constexpr int AT_WIN = 8, AT_HD = 128;
 constexpr int AT_SMEM = 3 * 16384 + 1024 + 64 + 128 * 4 + 256;
 
-__global__ void __launch_bounds__(128)
+__device__ __forceinline__ int floor_div_pos(int n, int d, float rcp) {
+  int q = __float2int_rd((float)n * rcp);       // |n| < 2^24: within one of the floor
+  int r = n - q * d;
+  if (r < 0) { --q; r += d; }
+  if (r >= d) ++q;
+  return q;
+}
+
+__global__ void __launch_bounds__(128, 4)
     k_l8_attn(const int8_t* __restrict__ qkv, int G, int Ht, int Wt, int D, int shift,
               const uint8_t* __restrict__ exp_lut, int8_t* __restrict__ out) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint8_t* sQ = smem;                 // [128 q][128 d]  A of S; then P [128 q][128 k], A of O
-  uint8_t* sK = smem + 16384;         // [128 k][128 d]  B of S
-  uint8_t* sV = smem + 32768;         // [128 d][128 k]  B of O (V^T, K-major)
+  uint8_t* sK = smem + 16384;         // [128 k][128 d]  B of S (K-major)
+  uint8_t* sV = smem + 32768;         // [128 k][128 d]  B of O (MN-major: d contiguous)
   uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 49152);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2);
   int* kval = reinterpret_cast<int*>(smem + 49152 + 64);
@@ -666,35 +689,25 @@ __global__ void __launch_bounds__(128)
     mbar_init(&bar[1], 1);
     fence_mbar_init();
   }
-  if (warp == 0) tc::tmem_alloc(tmem_slot, 256);
+  if (warp == 0) tc::tmem_alloc(tmem_slot, 128);
   lut[t] = exp_lut[t];
   lut[t + 128] = exp_lut[t + 128];
   kval[t] = valid;
   {
-    uint4 q4[8], k4[8], v4[8];
-    if (valid) {
-      const uint4* base = reinterpret_cast<const uint4*>(qkv + tok * 3 * D + head * AT_HD);
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        q4[j] = __ldg(base + j);
-        k4[j] = __ldg(base + D / 16 + j);
-        v4[j] = __ldg(base + 2 * D / 16 + j);
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) q4[j] = k4[j] = v4[j] = make_uint4(0, 0, 0, 0);
-    }
+    const uint4* base = reinterpret_cast<const uint4*>(qkv + tok * 3 * D + head * AT_HD);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
+      uint4 q4 = make_uint4(0, 0, 0, 0), k4 = q4, v4 = q4;
+      if (valid) {
+        q4 = __ldg(base + j);
+        k4 = __ldg(base + D / 16 + j);
+        v4 = __ldg(base + 2 * D / 16 + j);
+      }
       const int off = t * 128 + ((j ^ (t & 7)) << 4);
-      *reinterpret_cast<uint4*>(sQ + off) = q4[j];
-      *reinterpret_cast<uint4*>(sK + off) = k4[j];
+      *reinterpret_cast<uint4*>(sQ + off) = q4;
+      *reinterpret_cast<uint4*>(sK + off) = k4;
+      *reinterpret_cast<uint4*>(sV + off) = v4;
     }
-    // V^T: row d holds the 128 keys' values of dimension d (key k = t)
-    const uint8_t* vb = reinterpret_cast<const uint8_t*>(v4);
-#pragma unroll 8
-    for (int d = 0; d < AT_HD; ++d)
-      sV[d * 128 + ((((t >> 4) ^ (d & 7))) << 4) + (t & 15)] = vb[d];
   }
   fence_proxy_async_smem();
   tc::fence_before_sync();
@@ -714,66 +727,72 @@ __global__ void __launch_bounds__(128)
   tc::fence_after_sync();
 
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-  int sc[128];
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    float v[32];
-    tc::tmem_ld32(trow + c * 32, v);
-#pragma unroll
-    for (int i = 0; i < 32; ++i) sc[c * 32 + i] = __float_as_int(v[i]);
-  }
   const int nk = (ft + 1) * 64;       // causal: keys of frames <= ft
   int m = INT_MIN;
+#pragma unroll 1
+  for (int c = 0; c < nk; c += 32) {
+    float v[32];
+    tc::tmem_ld32(trow + c, v);
 #pragma unroll
-  for (int k = 0; k < 128; ++k)
-    if (k < nk && kval[k]) m = max(m, sc[k]);
-  int l = 0;
-#pragma unroll
-  for (int k = 0; k < 128; ++k) {
-    int e = 0;
-    if (k < nk && kval[k]) e = lut[min((m - sc[k]) >> shift, 255)];
-    sc[k] = e;
-    l += e;
+    for (int i = 0; i < 32; ++i)
+      if (kval[c + i]) m = max(m, __float_as_int(v[i]));
   }
-  tc::fence_before_sync();
-  __syncthreads();                    // every S read done and GEMM 1 retired: sQ -> P
+  int l = 0;
+#pragma unroll 1
+  for (int c = 0; c < 128; c += 32) {
+    int e[32];
+    if (c < nk) {
+      float v[32];
+      tc::tmem_ld32(trow + c, v);
 #pragma unroll
-  for (int j = 0; j < 8; ++j) {
-    const uint4 u = make_uint4(pack4(sc[16 * j + 0], sc[16 * j + 1], sc[16 * j + 2], sc[16 * j + 3]),
-                               pack4(sc[16 * j + 4], sc[16 * j + 5], sc[16 * j + 6], sc[16 * j + 7]),
-                               pack4(sc[16 * j + 8], sc[16 * j + 9], sc[16 * j + 10], sc[16 * j + 11]),
-                               pack4(sc[16 * j + 12], sc[16 * j + 13], sc[16 * j + 14], sc[16 * j + 15]));
-    *reinterpret_cast<uint4*>(sQ + t * 128 + ((j ^ (t & 7)) << 4)) = u;
+      for (int i = 0; i < 32; ++i) {
+        e[i] = kval[c + i] ? (int)lut[min((m - __float_as_int(v[i])) >> shift, 255)] : 0;
+        l += e[i];
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < 32; ++i) e[i] = 0;
+    }
+    // P row t, keys c..c+31 = 16-byte chunks c/16, c/16+1 (over Q: the S MMA has retired)
+#pragma unroll
+    for (int qq = 0; qq < 2; ++qq) {
+      const int j = (c >> 4) + qq;
+      const int* ee = e + 16 * qq;
+      *reinterpret_cast<uint4*>(sQ + t * 128 + ((j ^ (t & 7)) << 4)) =
+          make_uint4(pack4(ee[0], ee[1], ee[2], ee[3]), pack4(ee[4], ee[5], ee[6], ee[7]),
+                     pack4(ee[8], ee[9], ee[10], ee[11]), pack4(ee[12], ee[13], ee[14], ee[15]));
+    }
   }
   fence_proxy_async_smem();
   tc::fence_before_sync();
-  __syncthreads();
+  __syncthreads();                    // every S value read: O may overwrite its columns
   tc::fence_after_sync();
   if (t == 0) {
-    constexpr uint32_t id2 = tc::idesc_i8_s32(128, 128, false, true);   // P unsigned, V signed
+    // P unsigned, V signed and MN-major (bit 16): a K step of 32 keys is 32
+    // rows = 4 swizzle atoms = 4096 bytes
+    constexpr uint32_t id2 = tc::idesc_i8_s32(128, 128, false, true) | (1u << 16);
     const uint64_t ad = tc::smem_desc_sw128(smem_u32(sQ));
     const uint64_t bd = tc::smem_desc_sw128(smem_u32(sV));
 #pragma unroll
-    for (int k = 0; k < 4; ++k) tc::mma_i8(tmem + 128, ad + 2 * k, bd + 2 * k, id2, k);
+    for (int k = 0; k < 4; ++k) tc::mma_i8(tmem, ad + 2 * k, bd + 256 * k, id2, k);
     tc::mma_commit(&bar[1]);
   }
   mbar_wait(&bar[1], 0);
   tc::fence_after_sync();
-  const int64_t l2 = 2 * (int64_t)l;
-#pragma unroll
-  for (int c = 0; c < 4; ++c) {
+  const int l2 = 2 * l;
+  const float rcp = 1.0f / (float)l2;
+#pragma unroll 1
+  for (int c = 0; c < 128; c += 32) {
     float v[32];
-    tc::tmem_ld32(trow + 128 + c * 32, v);
+    tc::tmem_ld32(trow + c, v);
     if (!valid) continue;
     int o[32];
 #pragma unroll
     for (int i = 0; i < 32; ++i) {
-      const int64_t n = 2 * (int64_t)__float_as_int(v[i]) + l;
-      int64_t qv = n / l2;                         // truncation ...
-      if ((n % l2 != 0) && (n < 0)) qv -= 1;      // ... to floor
-      o[i] = (int)max(min(qv, (int64_t)127), (int64_t)-127);
+      const int q = floor_div_pos(2 * __float_as_int(v[i]) + l, l2, rcp);
+      o[i] = min(max(q, -127), 127);
     }
-    uint4* op = reinterpret_cast<uint4*>(out + tok * D + head * AT_HD + c * 32);
+    uint4* op = reinterpret_cast<uint4*>(out + tok * D + head * AT_HD + c);
 #pragma unroll
     for (int qq = 0; qq < 2; ++qq)
       op[qq] = make_uint4(pack4(o[qq * 16 + 0], o[qq * 16 + 1], o[qq * 16 + 2], o[qq * 16 + 3]),
@@ -783,7 +802,7 @@ __global__ void __launch_bounds__(128)
   }
   tc::fence_before_sync();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tmem, 256);
+  if (warp == 0) tc::tmem_dealloc(tmem, 128);
 }
 
 // ---- patchify -------------------------------------------------------------------

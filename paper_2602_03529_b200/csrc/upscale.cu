@@ -450,10 +450,16 @@ struct Up9fGeom {
   static constexpr int kWin = (kWR * kWF9 + 31) / 32 * 32;       // floats per window, 128 B aligned
 };
 
-template <int kBand, int kP>
+// Window element type T: float (the windows as loaded), or double -- each
+// source sample widened ONCE after the load instead of once per use by every
+// output column that reads it (the float64 -> float32 -> float64 conversions
+// run on the XU pipe, which bounded the float variant at ~61 % XU, 0.75 of
+// the HBM roofline).  A double window's loads land, as float32, in the upper
+// half of its own slot and are widened in place (read all, sync, write all).
+template <int kBand, int kP, typename T = float>
 struct Up9fSmem {
-  float win[kGop][Up9fGeom<kBand>::kWin];
-  float winp[kP > 0 ? kP : 1][Up9fGeom<kBand>::kWin];   // previous GoP's frames 9-n+f, f < n = kP
+  T win[kGop][Up9fGeom<kBand>::kWin];
+  T winp[kP > 0 ? kP : 1][Up9fGeom<kBand>::kWin];   // previous GoP's frames 9-n+f, f < n = kP
   AxisTap ty_c[kBand], ty_p[kBand];
   int wx0[2], wx1[2];
   int xs;                    // current window's column shift (TMA alignment), 0 for cp.async
@@ -463,8 +469,14 @@ struct Up9fSmem {
 // Interpolate frames f0..f0+NF-1 from their windows with the row-cache
 // control shared, and stream the rows out; the first NB of them (f0 = 0) are
 // blended with the previous GoP's frames 9-n+f.
-template <int kBand, int kP, int NF, int NB>
-__device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP>& S, const UpArgs& a, int g,
+// landing zone of window w's float32 loads
+template <typename T, int kWin>
+__device__ __forceinline__ float* k5_9_land(T* w) {
+  return reinterpret_cast<float*>(w) + (sizeof(T) == 8 ? kWin : 0);
+}
+
+template <int kBand, int kP, int NF, int NB, typename T>
+__device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const UpArgs& a, int g,
                                              int f0, int q0, int oy0, int rows,
                                              const AxisTap& tx, int xl, int xh,
                                              const AxisTap& txp, int pxl, int pxh) {
@@ -492,7 +504,7 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP>& S, const UpArg
       } else {
 #pragma unroll
         for (int j = 0; j < NF; ++j) {
-          const float* wr = &S.win[f0 + j][(ty.lo - r0) * kWF9];
+          const T* wr = &S.win[f0 + j][(ty.lo - r0) * kWF9];
           ia[j] = (double)wr[xl] * tx.g + (double)wr[xh] * tx.f;     // codec.py:233
         }
       }
@@ -505,7 +517,7 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP>& S, const UpArg
       } else {
 #pragma unroll
         for (int j = 0; j < NF; ++j) {
-          const float* wr = &S.win[f0 + j][(ty.hi - r0) * kWF9];
+          const T* wr = &S.win[f0 + j][(ty.hi - r0) * kWF9];
           ib[j] = (double)wr[xl] * tx.g + (double)wr[xh] * tx.f;
         }
       }
@@ -521,7 +533,7 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP>& S, const UpArg
         } else {
 #pragma unroll
           for (int j = 0; j < NQ; ++j) {
-            const float* wq = &S.winp[j][(tp.lo - pr0) * kWF9];
+            const T* wq = &S.winp[j][(tp.lo - pr0) * kWF9];
             qva[j] = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
           }
         }
@@ -534,7 +546,7 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP>& S, const UpArg
         } else {
 #pragma unroll
           for (int j = 0; j < NQ; ++j) {
-            const float* wq = &S.winp[j][(tp.hi - pr0) * kWF9];
+            const T* wq = &S.winp[j][(tp.hi - pr0) * kWF9];
             qvb[j] = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
           }
         }
@@ -578,12 +590,13 @@ __device__ __forceinline__ void k5_9_window(float* dst, const float* img, int w,
   }
 }
 
-template <int kBand, bool kPrev, int kN, int kLoad>
-__global__ void __launch_bounds__(kTQ, 3)
+template <int kBand, bool kPrev, int kN, int kLoad, typename T>
+__global__ void __launch_bounds__(kTQ, sizeof(T) == 8 ? 2 : 3)
     k_upscale9f(const __grid_constant__ CUtensorMap imap, const __grid_constant__ UpArgs a) {
   constexpr int kP = kPrev ? kN - 1 : 0;      // previous-GoP windows (alpha > 0 frames)
+  constexpr int kWin = Up9fGeom<kBand>::kWin;
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  Up9fSmem<kBand, kP>& S = *reinterpret_cast<Up9fSmem<kBand, kP>*>(smem_raw);
+  Up9fSmem<kBand, kP, T>& S = *reinterpret_cast<Up9fSmem<kBand, kP, T>*>(smem_raw);
   const int tid = threadIdx.x;
   const int q0 = blockIdx.x * kTQ;
   const int oy0 = blockIdx.y * kBand;
@@ -621,27 +634,54 @@ __global__ void __launch_bounds__(kTQ, 3)
         mbar_expect_tx(&S.bar, kGop * kBox);
 #pragma unroll 1
         for (int f = 0; f < kGop; ++f)
-          tma_load_3d(S.win[f], &imap, S.wx0[0] * 3 - S.xs, r0, g * kGop + f, &S.bar);
+          tma_load_3d(k5_9_land<T, kWin>(S.win[f]), &imap, S.wx0[0] * 3 - S.xs, r0, g * kGop + f,
+                      &S.bar);
       }
     } else {
       const int64_t fimg = (int64_t)a.h * a.w * 3;
       const float* cur = a.img + (int64_t)g * kGop * fimg;
 #pragma unroll 1
       for (int f = 0; f < kGop; ++f)
-        k5_9_window<kLoad>(S.win[f], cur + f * fimg, a.w, r0, r1, S.wx0[0] * 3, S.wx1[0] * 3 + 3,
-                           tid);
+        k5_9_window<kLoad>(k5_9_land<T, kWin>(S.win[f]), cur + f * fimg, a.w, r0, r1,
+                           S.wx0[0] * 3, S.wx1[0] * 3 + 3, tid);
     }
     if (has_prev) {
       const int pr0 = S.ty_p[0].lo, pr1 = S.ty_p[rows - 1].hi;
       const int64_t pimg = (int64_t)pd.h * pd.w * 3;
 #pragma unroll
       for (int j = 0; j < kP; ++j)
-        k5_9_window<kLoad == 0 ? 0 : 1>(S.winp[j], pd.p_img + (kGop - kN + j) * pimg, pd.w, pr0,
+        k5_9_window<kLoad == 0 ? 0 : 1>(k5_9_land<T, kWin>(S.winp[j]), pd.p_img + (kGop - kN + j) * pimg, pd.w, pr0,
                                         pr1, S.wx0[1] * 3, S.wx1[1] * 3 + 3, tid);
     }
     if (kLoad != 0) cp_async_wait_all();
     if (kLoad == 2) mbar_wait(&S.bar, 0);
     __syncthreads();
+    if constexpr (sizeof(T) == 8) {
+      // widen every window in place: each thread reads its samples of one
+      // window into registers, then (after the barrier) writes them back as
+      // doubles over the float32 landing zone
+      constexpr int n = Up9fGeom<kBand>::kWR * kWF9;
+      constexpr int per = (n + kTQ - 1) / kTQ;
+      const int nw = kGop + (has_prev ? kP : 0);
+#pragma unroll 1
+      for (int f = 0; f < nw; ++f) {
+        T* wd = f < kGop ? S.win[f] : S.winp[f - kGop];
+        const float* src = k5_9_land<T, kWin>(wd);
+        float v[per];
+#pragma unroll
+        for (int k = 0; k < per; ++k) {
+          const int i = tid + k * kTQ;
+          v[k] = i < n ? src[i] : 0.0f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < per; ++k) {
+          const int i = tid + k * kTQ;
+          if (i < n) wd[i] = (double)v[k];
+        }
+        __syncthreads();
+      }
+    }
   }
 
   if (q0 + tid >= a.W * 3) return;
@@ -663,19 +703,19 @@ __global__ void __launch_bounds__(kTQ, 3)
   }
 }
 
-template <int BAND, int LOAD>
+template <int BAND, int LOAD, typename T>
 static int launch_k5_9f(const CUtensorMap& imap, const UpArgs& a, const SstPrevDesc* prev,
                         int blend_n, cudaStream_t st) {
   dim3 grid(ceil_div(a.W * 3, kTQ), ceil_div(a.H, BAND), a.G);
   if (grid.y > 65535) return SST_ERR_ARG;
-  int smem = (int)sizeof(Up9fSmem<BAND, 0>);
-  auto kern = k_upscale9f<BAND, false, 1, LOAD>;
+  int smem = (int)sizeof(Up9fSmem<BAND, 0, T>);
+  auto kern = k_upscale9f<BAND, false, 1, LOAD, T>;
   if (prev) {
     switch (blend_n) {
-      case 1: kern = k_upscale9f<BAND, true, 1, LOAD>; smem = sizeof(Up9fSmem<BAND, 0>); break;
-      case 2: kern = k_upscale9f<BAND, true, 2, LOAD>; smem = sizeof(Up9fSmem<BAND, 1>); break;
-      case 3: kern = k_upscale9f<BAND, true, 3, LOAD>; smem = sizeof(Up9fSmem<BAND, 2>); break;
-      default: kern = k_upscale9f<BAND, true, 4, LOAD>; smem = sizeof(Up9fSmem<BAND, 3>); break;
+      case 1: kern = k_upscale9f<BAND, true, 1, LOAD, T>; smem = sizeof(Up9fSmem<BAND, 0, T>); break;
+      case 2: kern = k_upscale9f<BAND, true, 2, LOAD, T>; smem = sizeof(Up9fSmem<BAND, 1, T>); break;
+      case 3: kern = k_upscale9f<BAND, true, 3, LOAD, T>; smem = sizeof(Up9fSmem<BAND, 2, T>); break;
+      default: kern = k_upscale9f<BAND, true, 4, LOAD, T>; smem = sizeof(Up9fSmem<BAND, 3, T>); break;
     }
   }
   SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -838,18 +878,34 @@ extern "C" int sst_upscale_blend9(const float* img, int G, int h, int w, int s, 
   // cp.async 1.49 / 2.12 ms.  Earlier layouts, since removed: one frame per
   // pass with TMA-store tiles 2.37 / 2.88 ms, column-private threads 3.0 / 4.1,
   // 32-row bands 2.24 / 3.28 (cp.async) and 3.5 / 4.8 (register-staged).
+  // Window element type: float (default: 16-row bands, three CTAs per SM,
+  // ~2 float32 <-> float64 conversions per output sample on the XU pipe) or
+  // double (SST_K5_9W=f64: each source sample widened once, 12-row bands, two
+  // CTAs per SM).  Measured (scripts/k5_9_micro.py, 32 x 1080p GoPs, s=3,
+  // without / with blend): float 1.345 / 1.609 ms, double 1.959 / 2.331 ms --
+  // the halved occupancy and the widening pass cost more than the XU work
+  // they remove, so float stays the default.
+  const char* ww = getenv("SST_K5_9W");
+  const bool f32w = !(ww && !strcmp(ww, "f64"));
+  constexpr int kB64 = 12, kB32 = 16;
   CUtensorMap imap;
   memset(&imap, 0, sizeof(imap));
   const bool tma_in = make_tmap_f32_3d(&imap, img, (uint64_t)w * 3, (uint64_t)h,
-                                       (uint64_t)G * kGop, kWF9, Up9fGeom<16>::kWR);
+                                       (uint64_t)G * kGop, kWF9,
+                                       f32w ? Up9fGeom<kB32>::kWR : Up9fGeom<kB64>::kWR);
   int load = tma_in ? 2 : 1;
   if (const char* v9 = getenv("SST_K5_9")) {
     if (!strcmp(v9, "sync")) load = 0;
     else if (!strcmp(v9, "async")) load = 1;
   }
-  if (load == 2) return launch_k5_9f<16, 2>(imap, a, prev, blend_n, st);
-  if (load == 1) return launch_k5_9f<16, 1>(imap, a, prev, blend_n, st);
-  return launch_k5_9f<16, 0>(imap, a, prev, blend_n, st);
+  if (f32w) {
+    if (load == 2) return launch_k5_9f<kB32, 2, float>(imap, a, prev, blend_n, st);
+    if (load == 1) return launch_k5_9f<kB32, 1, float>(imap, a, prev, blend_n, st);
+    return launch_k5_9f<kB32, 0, float>(imap, a, prev, blend_n, st);
+  }
+  if (load == 2) return launch_k5_9f<kB64, 2, double>(imap, a, prev, blend_n, st);
+  if (load == 1) return launch_k5_9f<kB64, 1, double>(imap, a, prev, blend_n, st);
+  return launch_k5_9f<kB64, 0, double>(imap, a, prev, blend_n, st);
 }
 
 extern "C" int sst_upscale(const float* img, int64_t n, int h, int w, int s, int crop_h, int crop_w,
