@@ -758,54 +758,48 @@ def single_stream_latency(a, device) -> dict:
     """Real-time view (north_star: >= 30 fps per 1080p stream): ONE stream,
     one GoP at a time (each GoP blends with the previous one), variable scale
     3,3,2,2; device time per GoP (encode .. reconstruct, 9 frames) with the
-    GoP resident in HBM, and the frame rate that implies for a single stream."""
+    GoP resident in HBM -- eager (StreamBank) and with every step replayed as
+    a CUDA graph (GraphedStreamBank) -- and the frame rate that implies."""
     import torch
-    from paper_2602_03529_b200.pipeline import StreamBank
+    from paper_2602_03529_b200.pipeline import GraphedStreamBank, StreamBank
     H, W = a.height, a.width
-    bank = StreamBank(1, H, W)
     fr = make_inputs([0], H, W, device, n_sets=1)[0]
     out = torch.empty_like(fr)
     n, warm = 24, 4
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(n)]
-    for k in range(warm + n):
-        s = SCALE_PATTERN[k % len(SCALE_PATTERN)]
-        if k >= warm:
-            ev[k - warm][0].record()
-        bank.step({s: fr}, {s: out}, {s: [0]}, {s: [k]}, drop_rate=a.drop)
-        if k >= warm:
-            ev[k - warm][1].record()
-            torch.cuda.synchronize()          # one GoP in flight: latency, not throughput
-    ms = sorted(b.elapsed_time(e) for b, e in ev)
-    med = ms[len(ms) // 2]
-    # the same single stream at fixed scale 3, eager vs CUDA-graph replay
-    # (host wall time per GoP, one GoP in flight)
-    from paper_2602_03529_b200.pipeline import GopCodec, GraphedGopCodec
-    codec = GopCodec(1, H, W, 3)
-    drop_k = codec.drop_k(a.drop)
-    gr = GraphedGopCodec(codec, 1, fr, out, drop_k)
-    walls = {}
-    for mode in ("eager", "graph"):
-        t = []
+
+    def timed(run):
+        ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+              for _ in range(n)]
+        walls = []
         for k in range(warm + n):
+            s = SCALE_PATTERN[k % len(SCALE_PATTERN)]
             t0 = time.perf_counter()
-            if mode == "graph":
-                gr.step([k])
-            else:
-                codec.set_gop_ids([k])
-                codec.encode(fr, 1, drop_k)
-                codec.decode(1, k & 1)
-                codec.reconstruct(1, k & 1, out)
-            torch.cuda.synchronize()
             if k >= warm:
-                t.append((time.perf_counter() - t0) * 1e3)
-        t.sort()
-        walls[mode] = round(t[len(t) // 2], 3)
+                ev[k - warm][0].record()
+            run(k, s)
+            if k >= warm:
+                ev[k - warm][1].record()
+            torch.cuda.synchronize()          # one GoP in flight: latency, not throughput
+            if k >= warm:
+                walls.append((time.perf_counter() - t0) * 1e3)
+        ms = sorted(b.elapsed_time(e) for b, e in ev)
+        walls.sort()
+        return ms, walls
+
+    bank = StreamBank(1, H, W)
+    eager, eager_w = timed(lambda k, s: bank.step({s: fr}, {s: out}, {s: [0]}, {s: [k]},
+                                                  drop_rate=a.drop))
+    gbank = GraphedStreamBank(H, W, fr, out, drop_rate=a.drop)
+    graph, graph_w = timed(lambda k, s: gbank.step(s, k))
+    med = graph[len(graph) // 2]
     return {"stream": f"1 x {H}p, scales {SCALE_PATTERN}, {int(a.drop * 100)}% drop, blend n=2",
-            "gop_ms_median": round(med, 3), "gop_ms_max": round(ms[-1], 3),
+            "gop_ms_median": round(med, 3), "gop_ms_max": round(graph[-1], 3),
+            "path": "GraphedStreamBank (each step one CUDA-graph replay, 14 kernels)",
+            "eager_gop_ms_median": round(eager[len(eager) // 2], 3),
             "frames_per_s_single_stream": round(GOP / med * 1e3, 1),
             "realtime_30fps_budget_ms_per_gop": round(GOP / 30 * 1e3, 1),
-            "host_wall_ms_per_gop_s3": walls}
+            "host_wall_ms_per_gop": {"eager": round(eager_w[len(eager_w) // 2], 3),
+                                     "graph": round(graph_w[len(graph_w) // 2], 3)}}
 
 
 def loss_legs(a, device) -> dict:

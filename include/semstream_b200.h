@@ -168,10 +168,12 @@ SST_API int sst_topk_mask(const double* sim, int G, int64_t n, const int32_t* k,
 SST_API int sst_apply_mask(double* values, uint8_t* mask, const uint8_t* drop, int64_t n, int C,
                    void* stream);
 
-/* Fused intelligent drop for a GoP batch: top_k_drop_mask on sim[g] then
- * apply_token_mask on the P tokens of tok[g] ([G][2][H'][W'][12] layout).
- * mask: the batch's token mask [G][2][H'][W'] (the P half is updated);
- * drop: [G][H'][W'] out or NULL. */
+/* Fused intelligent drop for a freshly encoded GoP batch: top_k_drop_mask on
+ * sim[g] then apply_token_mask on the P tokens of tok[g] ([G][2][H'][W'][12]
+ * layout).  Every token of an encoder batch is valid (codec.py:155-157), so
+ * the P half of mask [G][2][H'][W'] is ASSIGNED: P mask = not dropped (k = 0
+ * restores an all-true P mask); the I half is not touched.  Dropped P values
+ * are zeroed.  drop: [G][H'][W'] out or NULL. */
 SST_API int sst_select_drop(const double* sim, double* tok, uint8_t* mask, int G, int Ht, int Wt,
                     const int32_t* k, uint8_t* drop, void* stream);
 

@@ -15,7 +15,8 @@
 
 namespace sst {
 
-__device__ __constant__ CrcTables kCrc = make_crc_tables();
+// global (not __constant__): the table fill reads 32 different entries per warp
+__device__ const CrcTables kCrc = make_crc_tables();
 
 constexpr int kPackWarps = 4;
 
@@ -28,13 +29,14 @@ struct PackArgs {
   const uint8_t* scale;
   uint8_t* arena;
   int64_t slot;
-  int64_t scratch;   // per-warp smem: slot bytes + Wt prefix ints, 16-aligned
+  int64_t scratch;   // per-warp smem: slot bytes + Wt prefix ints [+ row staging], 16-aligned
   int32_t* lengths;
+  int64_t rowbuf;    // byte offset of the row staging (Wt*C doubles + Wt mask bytes) or 0
 };
 
 __device__ __forceinline__ void load_crc_tables(uint32_t* tab, uint32_t* x2n) {
-  for (int i = threadIdx.x; i < 256; i += blockDim.x) tab[i] = kCrc.byte[i];
-  for (int i = threadIdx.x; i < 32; i += blockDim.x) x2n[i] = kCrc.x2n[i];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) tab[i] = __ldg(&kCrc.byte[i]);
+  for (int i = threadIdx.x; i < 32; i += blockDim.x) x2n[i] = __ldg(&kCrc.x2n[i]);
 }
 
 // Seal the body staged in `buf` (len bytes) with its CRC and copy the packet
@@ -74,12 +76,27 @@ __global__ void __launch_bounds__(kPackWarps * 32) k_packetize(PackArgs a) {
   const int row = (int)(pk % a.Ht);
   const double* vrow = a.values + ((int64_t)mi * a.Ht + row) * Wt * C;
   const uint8_t* mrow = a.mask ? a.mask + ((int64_t)mi * a.Ht + row) * Wt : nullptr;
+  const int64_t nel = (int64_t)Wt * C;
+  // per-warp row staging (when it fits): the row's values and mask bytes are
+  // read from global memory once, with all of a lane's loads in flight
+  // together, and every later pass reads shared memory (the payload pass used
+  // to issue one dependent global load per element: latency-bound for a
+  // single GoP)
+  double* rowv = a.rowbuf ? reinterpret_cast<double*>(buf + a.rowbuf) : nullptr;
+  uint8_t* rowm = a.rowbuf ? reinterpret_cast<uint8_t*>(rowv + nel) : nullptr;
+  if (rowm) {
+    for (int t = lane; t < Wt; t += 32) rowm[t] = mrow ? (mrow[t] != 0) : 1;
+    __syncwarp();
+  }
+  auto valid_tok = [&](int t) -> bool {
+    return rowm ? rowm[t] != 0 : (mrow ? mrow[t] != 0 : true);
+  };
 
   // 1) valid-token prefix counts (ballot scan) and mask bytes, MSB first
   int running = 0;
   for (int base = 0; base < Wt; base += 32) {
     int t = base + lane;
-    bool v = t < Wt && (mrow ? mrow[t] != 0 : true);
+    bool v = t < Wt && valid_tok(t);
     unsigned bal = __ballot_sync(0xffffffffu, v);
     if (t < Wt) pre[t] = running + __popc(bal & ((1u << lane) - 1u));
     running += __popc(bal);
@@ -90,7 +107,7 @@ __global__ void __launch_bounds__(kPackWarps * 32) k_packetize(PackArgs a) {
     uint32_t byte = 0;
     for (int q = 0; q < 8; ++q) {
       int t = b * 8 + q;
-      bool v = t < Wt && (mrow ? mrow[t] != 0 : true);
+      bool v = t < Wt && valid_tok(t);
       byte |= (v ? 1u : 0u) << (7 - q);
     }
     buf[kHdr + b] = (uint8_t)byte;
@@ -99,22 +116,56 @@ __global__ void __launch_bounds__(kPackWarps * 32) k_packetize(PackArgs a) {
   // 2) masked row min / max over the valid tokens (transport.py:249-253)
   double lo = 0.0, hi = 0.0;
   bool any = false;
-  const int64_t nel = (int64_t)Wt * C;
-  // batches of 4 independent loads per lane keep several requests in flight
-  for (int64_t e0 = lane; e0 < nel; e0 += 32 * 4) {
-    double v[4];
-    bool ok[4];
+  // token-major fast path (C = 12, row staged): lane l owns tokens l, l+32,
+  // ...: six 16-byte loads per token, all of a lane's tokens in flight, and
+  // no per-element index divisions
+  const bool tok_major = rowv != nullptr && C == kChannels;
+  if (tok_major) {
+    for (int t0 = lane; t0 < Wt; t0 += 32 * 2) {
+      double2 v[2][6];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int64_t e = e0 + 32 * u;
-      ok[u] = e < nel && (mrow == nullptr || mrow[(int)(e / C)] != 0);
-      v[u] = ok[u] ? __ldg(vrow + e) : 0.0;
+      for (int u = 0; u < 2; ++u) {
+        const int t = t0 + 32 * u;
+        const double2* src = reinterpret_cast<const double2*>(vrow + (int64_t)t * kChannels);
+#pragma unroll
+        for (int i = 0; i < 6; ++i) v[u][i] = t < Wt ? __ldg(src + i) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int t = t0 + 32 * u;
+        if (t >= Wt) continue;
+        double2* dst = reinterpret_cast<double2*>(rowv + t * kChannels);
+#pragma unroll
+        for (int i = 0; i < 6; ++i) dst[i] = v[u][i];
+        if (!valid_tok(t)) continue;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          const double x0 = v[u][i].x, x1 = v[u][i].y;
+          if (!any) { lo = x0; hi = x0; any = true; }
+          else { lo = min_total(lo, x0); hi = max_total(hi, x0); }
+          lo = min_total(lo, x1);
+          hi = max_total(hi, x1);
+        }
+      }
     }
+  } else {
+    // batches of 8 independent loads per lane keep several requests in flight
+    for (int e0 = lane; e0 < (int)nel; e0 += 32 * 8) {
+      double v[8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      if (!ok[u]) continue;
-      if (!any) { lo = v[u]; hi = v[u]; any = true; }
-      else { lo = min_total(lo, v[u]); hi = max_total(hi, v[u]); }
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + 32 * u;
+        v[u] = e < nel ? __ldg(vrow + e) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int e = e0 + 32 * u;
+        if (e >= nel) continue;
+        if (rowv) rowv[e] = v[u];
+        if (!valid_tok(e / C)) continue;
+        if (!any) { lo = v[u]; hi = v[u]; any = true; }
+        else { lo = min_total(lo, v[u]); hi = max_total(hi, v[u]); }
+      }
     }
   }
   // lanes without values contribute neutral elements
@@ -122,6 +173,7 @@ __global__ void __launch_bounds__(kPackWarps * 32) k_packetize(PackArgs a) {
   if (!any) { lo = kInf; hi = -kInf; }
   lo = warp_min_total(lo);
   hi = warp_max_total(hi);
+  __syncwarp();
 
   double qmin32 = 0.0, qrange32 = 0.0;
   if (nvalid > 0) {
@@ -133,17 +185,36 @@ __global__ void __launch_bounds__(kPackWarps * 32) k_packetize(PackArgs a) {
   uint8_t* pay = buf + kHdr + mlen;
   const bool scaled = qrange32 > 0.0;
   const double mul = scaled ? 255.0 / qrange32 : 0.0;
-  for (int64_t e = lane; e < nel; e += 32) {
-    int t = (int)(e / C);
-    if (mrow && !mrow[t]) continue;
-    int c = (int)(e - (int64_t)t * C);
-    uint8_t q = 0;
-    if (scaled) {
-      double lv = rint((vrow[e] - qmin32) * mul);
-      lv = lv < 0.0 ? 0.0 : (lv > 255.0 ? 255.0 : lv);
-      q = (uint8_t)(int)lv;
+  if (tok_major) {
+    for (int t = lane; t < Wt; t += 32) {
+      if (!valid_tok(t)) continue;
+      uint8_t* dst = pay + pre[t] * kChannels;
+      const double* x = rowv + t * kChannels;
+#pragma unroll
+      for (int c = 0; c < kChannels; ++c) {
+        uint8_t q = 0;
+        if (scaled) {
+          double lv = rint((x[c] - qmin32) * mul);
+          lv = lv < 0.0 ? 0.0 : (lv > 255.0 ? 255.0 : lv);
+          q = (uint8_t)(int)lv;
+        }
+        dst[c] = q;
+      }
     }
-    pay[pre[t] * C + c] = q;
+  } else {
+    for (int e = lane; e < (int)nel; e += 32) {
+      int t = e / C;
+      if (!valid_tok(t)) continue;
+      int c = e - t * C;
+      uint8_t q = 0;
+      if (scaled) {
+        const double x = rowv ? rowv[e] : vrow[e];
+        double lv = rint((x - qmin32) * mul);
+        lv = lv < 0.0 ? 0.0 : (lv > 255.0 ? 255.0 : lv);
+        q = (uint8_t)(int)lv;
+      }
+      pay[pre[t] * C + c] = q;
+    }
   }
   // 4) header (transport.py:97-102)
   if (lane == 0) {
@@ -329,7 +400,12 @@ extern "C" int sst_packetize(const double* values, const uint8_t* mask, int m, i
   if (reinterpret_cast<uintptr_t>(arena) & 15) return SST_ERR_ARG;
   int64_t scratch = slot + (int64_t)Wt * 4;
   scratch = (scratch + 15) & ~(int64_t)15;
-  PackArgs a{values, mask, m, Ht, Wt, C, kind, gop_id, scale, arena, slot, scratch, lengths};
+  int64_t rowbuf = scratch;
+  int64_t staged = rowbuf + (int64_t)Wt * C * 8 + Wt;
+  staged = (staged + 15) & ~(int64_t)15;
+  if (staged * kPackWarps <= 160 * 1024) scratch = staged;   // row staging fits
+  else rowbuf = 0;
+  PackArgs a{values, mask, m, Ht, Wt, C, kind, gop_id, scale, arena, slot, scratch, lengths, rowbuf};
   int64_t smem = scratch * kPackWarps;
   if (smem > 200 * 1024) return SST_ERR_UNSUPPORTED;
   SST_CUDA_TRY(cudaFuncSetAttribute(k_packetize, cudaFuncAttributeMaxDynamicSharedMemorySize,

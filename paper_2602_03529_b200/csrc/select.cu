@@ -65,6 +65,11 @@ constexpr int kSelThreads = 1024;
 // Per map g: drop[j] = 1 for the k[g] highest-similarity positions.
 // Optionally applies the drop to the P tokens / mask of a [G][2][n][12]
 // token batch and its [G][2][n] mask (fused apply_token_mask).
+// PER > 0: the map's keys (n <= PER * 1024) are read from global memory once
+// into registers and every radix pass and the tie scan run from there (the
+// single-GoP case is latency-bound: one global round trip per pass cost
+// ~4 us); PER == 0 re-reads them per pass (any n).
+template <int PER>
 __global__ void __launch_bounds__(kSelThreads)
     k_topk(const double* __restrict__ sim, int64_t n, const int32_t* __restrict__ kk,
            uint8_t* __restrict__ drop, double* tok, uint8_t* p_mask, double* kth) {
@@ -73,13 +78,29 @@ __global__ void __launch_bounds__(kSelThreads)
   __shared__ int64_t s_krem;
   __shared__ int s_warp[kSelThreads / 32];
   __shared__ int64_t s_running;
+  __shared__ int s_done;
 
   const int g = blockIdx.x;
   const int tid = threadIdx.x;
   const double* sm = sim + (int64_t)g * n;
+  if (tid == 0) s_done = 0;
   int64_t k = kk[g];
   if (k < 0) k = 0;
   if (k > n) k = n;
+  const int nper = (int)((n + kSelThreads - 1) / kSelThreads);
+  uint64_t keys[PER > 0 ? PER : 1];
+  if (PER > 0) {
+#pragma unroll
+    for (int i = 0; i < PER; ++i) {
+      const int64_t j = (int64_t)i * kSelThreads + tid;
+      keys[i] = (i < nper && j < n) ? sim_key(__ldg(sm + j)) : 0;
+    }
+  }
+  auto key_at = [&](int i, int64_t j) -> uint64_t {
+    if (PER > 0) return keys[i < PER ? i : 0];
+    return sim_key(__ldg(sm + j));
+  };
+  const int iters = PER > 0 ? PER : nper;
 
   uint64_t prefix = 0, pmask = 0;
   int64_t krem = k;
@@ -88,9 +109,11 @@ __global__ void __launch_bounds__(kSelThreads)
     for (int shift = 56; shift >= 0; shift -= 8) {
       for (int b = tid; b < 256; b += kSelThreads) hist[b] = 0;
       __syncthreads();
-      for (int64_t base = 0; base < n; base += kSelThreads) {
-        const int64_t j = base + tid;
-        uint64_t key = j < n ? sim_key(__ldg(sm + j)) : 0;
+#pragma unroll
+      for (int i = 0; i < iters; ++i) {
+        if (i >= nper) break;                          // uniform across the CTA
+        const int64_t j = (int64_t)i * kSelThreads + tid;
+        uint64_t key = j < n ? key_at(i, j) : 0;
         const bool in = j < n && (key & pmask) == prefix;
         // warp-aggregated histogram update: similarity maps are dominated by
         // ties (static content), so many lanes share one bin
@@ -130,12 +153,20 @@ __global__ void __launch_bounds__(kSelThreads)
           const int d = 255 - (tid * 8 + i);
           s_prefix = prefix | ((uint64_t)d << shift);
           s_krem = krem - cum;
+          // every remaining candidate in this digit is dropped: the drop set
+          // is exactly {key >= prefix (lower digits zero)} -- stop early
+          // (not when the caller wants the k-th value itself)
+          if (kth == nullptr && (int64_t)c[i] == krem - cum) s_done = 1;
         }
       }
       __syncthreads();
       prefix = s_prefix;
       krem = s_krem;
       pmask |= (0xFFull << shift);
+      if (s_done) {            // uniform: T = prefix, all keys equal to T dropped
+        krem = n;
+        break;
+      }
       __syncthreads();
     }
     // prefix is now the k-th largest key T; krem = how many of the keys == T
@@ -149,11 +180,13 @@ __global__ void __launch_bounds__(kSelThreads)
   __syncthreads();
   const uint64_t T = prefix;
   const int lane = tid & 31, wid = tid >> 5;
-  for (int64_t base = 0; base < n; base += kSelThreads) {
-    int64_t j = base + tid;
+#pragma unroll
+  for (int i = 0; i < iters; ++i) {
+    if (i >= nper) break;
+    int64_t j = (int64_t)i * kSelThreads + tid;
     uint64_t key = 0;
     bool valid = j < n;
-    if (valid) key = sim_key(__ldg(sm + j));
+    if (valid) key = key_at(i, j);
     bool eq = valid && k > 0 && key == T;
     unsigned bal = __ballot_sync(0xffffffffu, eq);
     int before = __popc(bal & ((1u << lane) - 1u));
@@ -167,9 +200,11 @@ __global__ void __launch_bounds__(kSelThreads)
       if (drop) drop[(int64_t)g * n + j] = d ? 1 : 0;
       if (tok) {
         // apply_token_mask on the P matrix (codec.py:189-196)
+        // the batch is freshly encoded (every token valid, codec.py:155-157),
+        // so mask & ~drop == ~drop: assign, which also clears an earlier
+        // batch's drops without a reset pass
         uint8_t* mrow = p_mask + ((int64_t)g * 2 + 1) * n + j;   // [G][2][n]: P half
-        uint8_t m = *mrow;
-        uint8_t nm = (m && !d) ? 1 : 0;
+        const uint8_t nm = d ? 0 : 1;
         *mrow = nm;
         if (!nm) {
           double* v = tok + (((int64_t)g * 2 + 1) * n + j) * kChannels;
@@ -186,6 +221,18 @@ __global__ void __launch_bounds__(kSelThreads)
     }
     __syncthreads();
   }
+}
+
+template <typename... A>
+static void launch_topk(int G, int64_t n, cudaStream_t st, A... args) {
+  if (n <= 4 * kSelThreads)
+    k_topk<4><<<G, kSelThreads, 0, st>>>(args...);
+  else if (n <= 8 * kSelThreads)
+    k_topk<8><<<G, kSelThreads, 0, st>>>(args...);
+  else if (n <= 16 * kSelThreads)
+    k_topk<16><<<G, kSelThreads, 0, st>>>(args...);
+  else
+    k_topk<0><<<G, kSelThreads, 0, st>>>(args...);
 }
 
 __global__ void k_apply_mask(double* __restrict__ values, uint8_t* __restrict__ mask,
@@ -236,8 +283,8 @@ extern "C" int sst_topk_mask(const double* sim, int G, int64_t n, const int32_t*
   if (G < 0 || n < 0) return SST_ERR_ARG;
   if (G == 0 || n == 0) return SST_OK;
   if (!sim || !k || !drop) return SST_ERR_ARG;
-  k_topk<<<G, kSelThreads, 0, static_cast<cudaStream_t>(stream)>>>(sim, n, k, drop, nullptr,
-                                                                    nullptr, kth);
+  launch_topk(G, n, static_cast<cudaStream_t>(stream), sim, n, k, drop, (double*)nullptr,
+              (uint8_t*)nullptr, kth);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }
@@ -260,8 +307,8 @@ extern "C" int sst_select_drop(const double* sim, double* tok, uint8_t* p_mask, 
   int64_t n = (int64_t)Ht * Wt;
   if (G == 0 || n == 0) return SST_OK;
   if (!sim || !tok || !p_mask || !k) return SST_ERR_ARG;
-  k_topk<<<G, kSelThreads, 0, static_cast<cudaStream_t>(stream)>>>(sim, n, k, drop, tok, p_mask,
-                                                                    nullptr);
+  launch_topk(G, n, static_cast<cudaStream_t>(stream), sim, n, k, drop, tok, p_mask,
+              (double*)nullptr);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }

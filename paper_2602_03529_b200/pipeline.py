@@ -111,11 +111,19 @@ class GopCodec:
         f64, u8, i32 = torch.float64, torch.uint8, torch.int32
         self.tok = torch.empty((G, 2, self.Ht, self.Wt, CHANNELS), dtype=f64, device=dev)
         self.sim = torch.empty((G, self.Ht, self.Wt), dtype=f64, device=dev)
+        # token masks: the I half stays all-true (encode_gop, codec.py:155-157);
+        # the P half is assigned by K2 (P := not dropped), so no per-step reset
         self.mask = torch.ones((G, 2, self.Ht, self.Wt), dtype=u8, device=dev)
+        self._p_mask_dirty = False
         self.drop = torch.zeros((G, self.Ht, self.Wt), dtype=u8, device=dev)
         self.k = torch.zeros((G,), dtype=i32, device=dev)
+        self._k_val = 0
         self.kind = torch.tensor([0, 1] * G, dtype=u8, device=dev)
-        self.gop_id = torch.zeros((2 * G,), dtype=torch.int32, device=dev)   # u32 bits
+        # per-GoP ids, one buffer so a step's ids arrive with ONE host->device
+        # copy (no fill kernels): [exp_gop (G) | gop_id per matrix (2G)], u32 bits
+        self._ids = torch.zeros((3 * G,), dtype=torch.int32, device=dev)
+        self.exp_gop = self._ids[:G]
+        self.gop_id = self._ids[G:]
         self.scale = torch.full((2 * G,), s, dtype=u8, device=dev)
         npk = G * self.n_pkt_per_gop
         self.arena = torch.empty((npk, self.slot), dtype=u8, device=dev)
@@ -126,7 +134,6 @@ class GopCodec:
         tgt = np.repeat(np.arange(G) * 2, self.n_pkt_per_gop) + \
             np.tile(np.repeat([0, 1], self.Ht), G)
         self.target = torch.from_numpy(tgt.astype(np.int32)).to(dev)
-        self.exp_gop = torch.zeros((G,), dtype=torch.int32, device=dev)
         self.winner = torch.empty((2 * G * self.Ht,), dtype=torch.int32, device=dev)
         self.stats = torch.empty((2 * G * 2,), dtype=i32, device=dev)
         ws = _lib.load().sst_unpack_decode_workspace(G, self.Ht, self.Wt)
@@ -144,22 +151,16 @@ class GopCodec:
         return int(np.floor(rate * self.n + 0.5))
 
     def set_gop_ids(self, gop_ids) -> None:
-        """Per-GoP gop_id of the next batch.  Never blocks the host: a uniform
-        id is a device fill, otherwise the ids go through a pinned staging
-        ring (a pageable H2D copy would synchronise the stream)."""
+        """Per-GoP gop_id of the next batch: one asynchronous host->device copy
+        from a pinned staging ring into the id buffer (no kernel launch; a
+        pageable copy would synchronise the stream)."""
         ids = np.asarray(gop_ids, dtype=np.uint32)
         g = ids.size
-        if g and (ids == ids[0]).all():
-            v = int(ids[0].view(np.int32))
-            self.exp_gop[:g].fill_(v)
-            self.gop_id[:2 * g].fill_(v)
-            return
-        raw = np.repeat(ids, 2)
-        staged, slot = self._id_ring.stage(np.concatenate([ids, raw]).view(np.uint8))
-        both = staged[:3 * g * 4].view(torch.int32)
-        self.exp_gop[:g].copy_(both[:g])
-        self.gop_id[:2 * g].copy_(both[g:])
-        self._id_ring.release(slot)
+        G = self.g_max
+        raw = np.zeros(3 * G, dtype=np.uint32)
+        raw[:g] = ids
+        raw[G:G + 2 * g] = np.repeat(ids, 2)
+        self._id_ring.copy_to(raw.view(np.uint8), self._ids)
 
     # -- sender --------------------------------------------------------
     def encode(self, frames: torch.Tensor, g: int, drop_k: int = 0) -> None:
@@ -180,14 +181,17 @@ class GopCodec:
         """K2 (intelligent drop) + K3 (quantise, packetise, CRC)."""
         st = _dev.stream()
         tm = self.timer
-        self.mask[:g].fill_(1)
-        if drop_k > 0:
-            self.k[:g].fill_(drop_k)
+        if drop_k > 0 or self._p_mask_dirty:
+            if drop_k != self._k_val:
+                self.k.fill_(drop_k)           # only when the drop count changes
+                self._k_val = drop_k
+            # K2 assigns the P mask (P := not dropped): k = 0 just restores it
             tm.begin("K2_select_drop")
             _lib.call("sst_select_drop", self.sim.data_ptr(), self.tok.data_ptr(),
                       self.mask.data_ptr(), g, self.Ht, self.Wt, self.k.data_ptr(),
                       self.drop.data_ptr(), st)
             tm.end("K2_select_drop")
+            self._p_mask_dirty = drop_k > 0
         tm.begin("K3_packetize")
         _lib.call("sst_packetize", self.tok.data_ptr(), self.mask.data_ptr(), 2 * g, self.Ht,
                   self.Wt, CHANNELS, self.kind.data_ptr(), self.gop_id.data_ptr(),
@@ -261,6 +265,18 @@ class _DescRing:
         ev = torch.cuda.Event()
         ev.record()
         self.events[j] = ev
+
+    def copy_to(self, raw: np.ndarray, dst: torch.Tensor) -> None:
+        """Stage ``raw`` in the next pinned slot and copy it straight into the
+        device tensor ``dst`` (stream-ordered, no kernel)."""
+        j = self.i
+        self.i = (self.i + 1) % len(self.host)
+        if self.events[j] is not None:
+            self.events[j].synchronize()
+        n = raw.nbytes
+        self.host[j][:n].copy_(torch.from_numpy(raw.view(np.uint8)))
+        dst.view(torch.uint8)[:n].copy_(self.host[j][:n], non_blocking=True)
+        self.release(j)
 
 
 class StreamBank:
@@ -473,3 +489,70 @@ class GraphedGopCodec:
         idx = 0 if self.k == 0 else (1 if self.k % 2 == 1 else 2)
         self.graphs[idx].replay()
         self.k += 1
+
+
+class GraphedStreamBank:
+    """One stream, variable resolution (per-GoP scale), one GoP in flight,
+    every step replayed as a CUDA graph -- the latency case (real-time single
+    stream), where the ~14 launches of an eager step cost more than their
+    kernels.  Same semantics as ``StreamBank(1, H, W)``: GoP k is coded at
+    its own scale and blended with the stream's previous reconstruction,
+    whatever scale that had.  One graph per (scale, step parity, previous
+    scale or none): encode + drop + packetise + parse + decode + K5 with the
+    previous GoP's P image (the other parity's working image of the codec of
+    its scale) as the blend source.  Input frames are read from ``frames``
+    and reconstructions written to ``out`` (fixed device buffers)."""
+
+    def __init__(self, H: int, W: int, frames: torch.Tensor, out: torch.Tensor,
+                 drop_rate: float = 0.0, scales=(2, 3), blend_n: int = 2):
+        if blend_n > 4:
+            raise ValueError("the graphed bank blends at most 4 frames (K5 fused blend)")
+        check_gop_tensor(frames, 1, H, W, "frames")
+        check_gop_tensor(out, 1, H, W, "out")
+        self.frames, self.out, self.scales = frames, out, tuple(scales)
+        self.codecs = {s: GopCodec(1, H, W, s, blend_n) for s in scales}
+        self.drop_k = {s: c.drop_k(drop_rate) for s, c in self.codecs.items()}
+        dev = frames.device
+        # prev[(ps, par)]: the previous GoP coded at scale ps, whose working
+        # images are codecs[ps].img[par]
+        self.prev = {}
+        for ps, c in self.codecs.items():
+            for par in range(2):
+                d = np.zeros(1, dtype=_lib.PREV_DTYPE)
+                d[0]["p_img"] = c.img[par].data_ptr() + c.h * c.w * 3 * 4
+                d[0]["h"], d[0]["w"], d[0]["s"] = c.h, c.w, ps
+                self.prev[(ps, par)] = torch.from_numpy(d.view(np.uint8).copy()).to(dev)
+        plan = [(s, par, ps) for s in scales for par in range(2) for ps in (None,) + tuple(scales)]
+        for c in self.codecs.values():
+            c.set_gop_ids([0])
+        side = torch.cuda.Stream(device=dev)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):                 # warm-up outside capture
+            for key in plan:
+                self._body(*key)
+        torch.cuda.current_stream().wait_stream(side)
+        torch.cuda.synchronize()
+        self.graphs = {}
+        for key in plan:
+            gr = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(gr):
+                self._body(*key)
+            self.graphs[key] = gr
+        self.step_idx = 0
+        self.last_scale = None
+
+    def _body(self, s: int, parity: int, prev_scale) -> None:
+        c = self.codecs[s]
+        c.tokenize(self.frames, 1)
+        c.select_and_pack(1, self.drop_k[s])
+        c.decode(1, parity)
+        prev = None if prev_scale is None else self.prev[(prev_scale, 1 - parity)]
+        c.reconstruct(1, parity, self.out, prev)
+
+    def step(self, s: int, gop_id: int) -> None:
+        """Code the GoP now in ``frames`` at scale s into ``out``."""
+        par = self.step_idx & 1
+        self.codecs[s].set_gop_ids([gop_id])
+        self.graphs[(s, par, self.last_scale)].replay()
+        self.last_scale = s
+        self.step_idx += 1
