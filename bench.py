@@ -1003,6 +1003,77 @@ def parity_sample(a, device) -> dict:
             "bit_exact": bool(np.array_equal(gpu, ref))}
 
 
+def residual_leg(a, device) -> dict:
+    """SURVEY §8 rows f1 / f2 in the bench line: G x 1080p GoPs (s=3) through
+    the proxy codec, then the sender's residual enhancement layer (downscale,
+    residual against the decoded working images, sparsify, range encode) and
+    the receiver's (range decode, apply) -- the reference session's
+    residual path (session.py:173-193, 287-296) -- device-resident, CUDA-event
+    timed per stage; bitstreams round-trip exactly."""
+    import numpy as np
+    import torch
+    from paper_2602_03529_b200 import _dev, _lib
+    from paper_2602_03529_b200.pipeline import GopCodec
+    G, H, W, s = 32, a.height, a.width, 3
+    frames = make_inputs(list(range(G)), H, W, device, n_sets=1)[0]
+    c = GopCodec(G, H, W, s)
+    c.set_gop_ids([0] * G)
+    h, w = c.h, c.w
+    n = h * w * 3
+    f64, i16 = torch.float64, torch.int16
+    work = torch.empty((G, 9, h, w, 3), device=device)
+    avg = torch.empty((G, n), dtype=f64, device=device)
+    dense = torch.empty((G, n), dtype=i16, device=device)
+    mags = torch.empty((G, n), dtype=f64, device=device)
+    count = torch.empty((G,), dtype=torch.int32, device=device)
+    cap = n // 2 + 64
+    idx_ws = torch.empty((G * n,), dtype=torch.int64, device=device)
+    pay = torch.empty((G * cap,), dtype=torch.uint8, device=device)
+    plen = torch.empty((G,), dtype=torch.int64, device=device)
+    dec = torch.empty((G, n), dtype=i16, device=device)
+    status = torch.empty((G,), dtype=torch.int32, device=device)
+    offs = torch.arange(G, dtype=torch.int64, device=device) * cap
+    st = _dev.stream()
+    theta, step_q = 0.02, 1.0 / 127.0
+    stages = [
+        ("codec", lambda: (c.encode(frames, G, 0), c.decode(G, 0))),
+        ("downscale", lambda: _lib.call("sst_downscale", frames.data_ptr(), G * 9, H, W, s,
+                                        work.data_ptr(), st)),
+        ("residual", lambda: _lib.call("sst_residual", work.data_ptr(), c.img[0].data_ptr(), G, h,
+                                       w, theta, step_q, avg.data_ptr(), dense.data_ptr(),
+                                       mags.data_ptr(), count.data_ptr(), st)),
+        ("range_encode", lambda: _lib.call("sst_rc_encode", dense.data_ptr(), G, n,
+                                           idx_ws.data_ptr(), pay.data_ptr(), cap,
+                                           plen.data_ptr(), st)),
+        ("range_decode", lambda: _lib.call("sst_rc_decode", pay.data_ptr(), offs.data_ptr(),
+                                           plen.data_ptr(), G, n, dec.data_ptr(),
+                                           status.data_ptr(), st)),
+        ("apply", lambda: _lib.call("sst_apply_residual", c.img[0].data_ptr(), dec.data_ptr(),
+                                    count.data_ptr(), G, h, w, step_q, st)),
+    ]
+    times = {}
+    for it in range(5):
+        for name, fn in stages:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            if it >= 2:
+                times.setdefault(name, []).append((e0, e1))
+    torch.cuda.synchronize()
+    ms = {k: float(np.median([x.elapsed_time(y) for x, y in v])) for k, v in times.items()}
+    tot = sum(ms.values())
+    return {"workload": f"{G} x {H}p GoPs, s=3, residual theta={theta}, step 1/127, "
+                        "moving-square / noisy-motion synthetic streams",
+            "stage_ms": {k: round(v, 3) for k, v in ms.items()},
+            "frames_per_s": round(G * GOP / tot * 1e3, 1),
+            "entries_per_gop": round(float(count.float().mean()), 1),
+            "payload_bytes_per_gop": round(float(plen.float().mean()), 1),
+            "roundtrip_exact": bool(torch.equal(dec, dense)) and bool((status == 0).all()),
+            "range_coder": "one warp per stream, cumulative-table adaptive model (csrc/residual.cu "
+                           "k_rc_encode_c / k_rc_decode_c), bytes identical to the reference"}
+
+
 # ---------------------------------------------------------------------------
 # learned tokenizer leg (SURVEY.md §8 row f4): tcgen05 implicit-GEMM convs
 
@@ -1337,6 +1408,7 @@ def main():
             line["parity"] = parity_sample(a, dev)
             line["single_stream"] = single_stream_latency(a, dev)
             line["loss_recovery"] = loss_legs(a, dev)
+            line["residual_layer"] = residual_leg(a, dev)
             if a.height == 1080 and a.width == 1920:
                 line["small_configs"] = small_configs(a, dev)
         if world == 1 and not a.no_learned:

@@ -551,6 +551,257 @@ __global__ void __launch_bounds__(kRcThreads)
   if (lane == 0) status[g] = st;
 }
 
+// Chunked compaction for the cumulative-table coder (NT threads): thread t
+// counts the non-zeros of its contiguous chunk, one block scan places the
+// chunks, and a second pass writes the indices -- two barriers in total
+// instead of three per NT elements.
+template <int NT>
+__device__ int64_t compact_nonzero_chunked(const int16_t* scan, int64_t n, int64_t* idx,
+                                           int64_t* s_part) {
+  const int tid = threadIdx.x;
+  const int64_t chunk = (n + NT - 1) / NT;
+  const int64_t b0 = min(n, (int64_t)tid * chunk), b1 = min(n, b0 + chunk);
+  int64_t cnt = 0;
+  for (int64_t j = b0; j < b1; ++j) cnt += scan[j] != 0;
+  s_part[tid] = cnt;
+  __syncthreads();
+  if (tid == 0) {                     // exclusive scan of NT chunk counts
+    int64_t run = 0;
+    for (int i = 0; i < NT; ++i) {
+      const int64_t c = s_part[i];
+      s_part[i] = run;
+      run += c;
+    }
+    s_part[NT] = run;
+  }
+  __syncthreads();
+  int64_t o = s_part[tid];
+  for (int64_t j = b0; j < b1; ++j)
+    if (scan[j] != 0) idx[o++] = j;
+  __syncthreads();
+  return s_part[NT];
+}
+
+constexpr int kRcThreadsC = 256;
+
+// ---- cumulative-table coder (default) --------------------------------------
+// The same adaptive model held by one warp as a CUMULATIVE table: lane l keeps,
+// for its symbols s = 16l + k, the count cnt[k] and the exclusive prefix
+// cum[k] = sum of the counts of all symbols below s.  A symbol's (cum, cnt)
+// is then one register select in every lane plus ONE packed shuffle from its
+// owner (cum, cnt < 2^16 while total < 2^16), the decoder's search one ballot
+// (cum is strictly increasing: every live count is >= 1) plus one shuffle,
+// and the update 16 predicated adds per lane with no cross-lane dependency --
+// instead of a 5-shuffle warp reduction (encode) or scan (decode) per symbol.
+// The rare halving (rangecoder.py:147-149) rebuilds cum with one warp scan.
+struct CumModel {
+  uint32_t pc[16];                                 // (cum << 16) | cnt of symbol 16 lane + k
+  uint32_t total;
+};
+
+__device__ __forceinline__ void cm_rebuild(CumModel& m, int lane, const uint32_t (&cnt)[16]) {
+  uint32_t local = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) local += cnt[k];
+  uint32_t incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  uint32_t run = incl - local;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    m.pc[k] = (run << 16) | cnt[k];
+    run += cnt[k];
+  }
+  m.total = __shfl_sync(0xffffffffu, incl, 31);
+}
+
+__device__ __forceinline__ void cm_init(CumModel& m, int lane) {
+  uint32_t cnt[16];
+#pragma unroll
+  for (int k = 0; k < 16; ++k) cnt[k] = (16 * lane + k) < kAlpha ? 1u : 0u;
+  cm_rebuild(m, lane, cnt);
+}
+
+// (cum << 16) | cnt of symbol `sym` on every lane
+__device__ __forceinline__ uint32_t cm_lookup(const CumModel& m, int sym) {
+  const int off = sym & 15;
+  uint32_t v = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) v = (k == off) ? m.pc[k] : v;
+  return __shfl_sync(0xffffffffu, v, sym >> 4);
+}
+
+__device__ __forceinline__ void cm_update(CumModel& m, int lane, int sym) {
+  const int rel = sym - 16 * lane;                 // symbols above sym gain 1 in cum,
+#pragma unroll                                     // sym itself 1 in cnt
+  for (int k = 0; k < 16; ++k) m.pc[k] += k > rel ? 0x10000u : (k == rel ? 1u : 0u);
+  m.total += 1;
+  if (m.total >= (uint32_t)kBottom) {               // rangecoder.py:147-149
+    uint32_t cnt[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) cnt[k] = ((m.pc[k] & 0xFFFFu) + 1) / 2;   // 0 stays 0 (s >= 510)
+    cm_rebuild(m, lane, cnt);
+  }
+}
+
+// floor(a / b) for b >= 1 through a float reciprocal, corrected to exact
+__device__ __forceinline__ uint32_t udiv32(uint32_t a, uint32_t b) {
+  uint32_t q = __float2uint_rz(__fdividef((float)a, (float)b));
+  const int64_t r = (int64_t)a - (int64_t)q * b;
+  if (r < 0) q -= (uint32_t)((-r + b - 1) / b);   // rare: the estimate overshot
+  else if (r >= (int64_t)b) q += (uint32_t)(r / b);
+  return q;
+}
+
+__device__ __forceinline__ void cenc_symbol(WEnc& e, CumModel& m, int lane, int sym, uint8_t* out,
+                                            int64_t cap) {
+  const uint32_t cc = cm_lookup(m, sym);
+  const uint64_t r = (uint64_t)udiv32((uint32_t)e.range, m.total);
+  e.low += (uint64_t)(cc >> 16) * r;
+  e.range = (uint64_t)(cc & 0xFFFFu) * r;
+  while ((e.low ^ (e.low + e.range)) < kTop || e.range < kBottom) {
+    if ((e.low ^ (e.low + e.range)) >= kTop) e.range = (kMask32 + 1 - e.low) & (kBottom - 1);
+    if (lane == 0 && e.pos < cap) out[e.pos] = (uint8_t)((e.low >> 24) & 0xFF);
+    e.pos += 1;
+    e.low = (e.low << 8) & kMask32;
+    e.range <<= 8;
+  }
+  cm_update(m, lane, sym);
+}
+
+__global__ void __launch_bounds__(kRcThreadsC, 1)
+    k_rc_encode_c(const int16_t* __restrict__ scans, int64_t n, int64_t* __restrict__ idx_ws,
+                  uint8_t* __restrict__ out, int64_t cap, int64_t* __restrict__ out_len) {
+  __shared__ int64_t s_part[kRcThreadsC + 1];
+  const int g = blockIdx.x;
+  const int16_t* scan = scans + (int64_t)g * n;
+  int64_t* idx = idx_ws + (int64_t)g * n;
+  const int64_t nnz = compact_nonzero_chunked<kRcThreadsC>(scan, n, idx, s_part);
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  CumModel m;
+  cm_init(m, lane);
+  uint8_t* o = out + (int64_t)g * cap;
+  WEnc e{0, kMask32, 0};
+  int64_t pos = 0;
+  for (int64_t base = 0; base < nnz; base += 32) {
+    const int64_t ii = base + lane;
+    const int64_t jl = ii < nnz ? idx[ii] : 0;
+    const int vl = ii < nnz ? (int)scan[jl] : 0;
+    const int nb32 = (int)min((int64_t)32, nnz - base);
+    for (int t = 0; t < nb32; ++t) {                // rangecoder.py:75-94
+      const int64_t j = __shfl_sync(0xffffffffu, jl, t);
+      const int v = __shfl_sync(0xffffffffu, vl, t);
+      int64_t gap = j - pos;
+      while (gap > 255) {
+        cenc_symbol(e, m, lane, 255, o, cap);
+        gap -= 255;
+      }
+      if (gap) cenc_symbol(e, m, lane, (int)gap, o, cap);
+      cenc_symbol(e, m, lane, v < 0 ? v + 383 : v + 382, o, cap);
+      pos = j + 1;
+    }
+  }
+  cenc_symbol(e, m, lane, 0, o, cap);                // EOS
+  for (int k = 0; k < 4; ++k) {                      // rangecoder.py:182-184
+    if (lane == 0 && e.pos < cap) o[e.pos] = (uint8_t)((e.low >> 24) & 0xFF);
+    e.pos += 1;
+    e.low = (e.low << 8) & kMask32;
+  }
+  if (lane == 0) out_len[g] = e.pos > cap ? -e.pos : e.pos;
+}
+
+__global__ void __launch_bounds__(kRcThreadsC, 1)
+    k_rc_decode_c(const uint8_t* __restrict__ data, const int64_t* __restrict__ off,
+                  const int64_t* __restrict__ len, int64_t n, int16_t* __restrict__ scans,
+                  int32_t* __restrict__ status) {
+  const int g = blockIdx.x;
+  int16_t* scan = scans + (int64_t)g * n;
+  for (int64_t j = threadIdx.x; j < n; j += kRcThreadsC) scan[j] = 0;
+  __syncthreads();
+  if (threadIdx.x >= 32) return;
+  const int lane = threadIdx.x;
+  const uint8_t* src = data + off[g];
+  const int64_t nb = len[g];
+  int64_t p = 0;
+  int st = 0;
+  CumModel m;
+  cm_init(m, lane);
+  int64_t wbase = 0;
+  uint32_t wbyte = lane < nb ? src[lane] : 0;
+  auto next_byte = [&]() -> uint32_t {
+    if (p - wbase >= 32) {
+      wbase = p;
+      wbyte = wbase + lane < nb ? src[wbase + lane] : 0;
+    }
+    const uint32_t b = __shfl_sync(0xffffffffu, wbyte, (int)(p - wbase));
+    ++p;
+    return b;
+  };
+  uint64_t state = 0;
+  for (int k = 0; k < 4; ++k) {
+    if (p >= nb) { st = 1; break; }
+    state = (state << 8) | next_byte();
+  }
+  uint64_t low = 0, range = kMask32;
+  int64_t pos = 0, nsym = 0;
+  while (st == 0) {
+    const uint32_t total = m.total;
+    const uint64_t r = (uint64_t)udiv32((uint32_t)range, total);
+    const uint64_t diff = state - low;
+    // floor(diff / r) in float64: the quotient is < 2^16 unless clamped below,
+    // so the correctly rounded double quotient is within 2^-37 of the true
+    // one and r >= 1 keeps any non-integer quotient >= 2^-32 below the next
+    // integer: the floor is exact
+    uint64_t val = (diff >> 32) == 0
+                       ? (uint64_t)floor(__ddiv_rn((double)(uint32_t)diff, (double)(uint32_t)r))
+                       : diff / r;
+    if (val >= total) val = total - 1;
+    // owner = last lane whose first symbol starts at or below val; its count
+    // of symbols starting at or below val gives the offset
+    const uint32_t v32 = (uint32_t)val;              // val < total < 2^16
+    const unsigned bal = __ballot_sync(0xffffffffu, (m.pc[0] >> 16) <= v32);
+    const int owner = 31 - __clz(bal);
+    uint32_t pk = 0, kk = 0;                         // (cum << 16) | cnt, offset
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const bool le = (m.pc[k] >> 16) <= v32;
+      pk = le ? m.pc[k] : pk;
+      kk = le ? (uint32_t)k : kk;
+    }
+    pk = __shfl_sync(0xffffffffu, pk, owner);
+    kk = __shfl_sync(0xffffffffu, kk, owner);
+    const int sym = owner * 16 + (int)kk;
+    const uint32_t cumv = pk >> 16, cntv = pk & 0xFFFFu;
+    low += (uint64_t)cumv * r;
+    range = (uint64_t)cntv * r;
+    while ((low ^ (low + range)) < kTop || range < kBottom) {
+      if ((low ^ (low + range)) >= kTop) range = (kMask32 + 1 - low) & (kBottom - 1);
+      if (p >= nb) { st = 1; break; }
+      state = ((state << 8) | next_byte()) & kMask32;
+      low = (low << 8) & kMask32;
+      range <<= 8;
+    }
+    if (st) break;
+    cm_update(m, lane, sym);
+    ++nsym;
+    if (sym == 0) break;                            // EOS
+    if (sym <= 255) {                               // zero run (rangecoder.py:107-110)
+      pos += sym;
+      if (pos > n) { st = 2; break; }
+    } else {
+      if (pos >= n) { st = 3; break; }
+      if (lane == 0) scan[pos] = (int16_t)(sym <= 382 ? sym - 383 : sym - 382);
+      ++pos;
+    }
+    if (nsym >= (1 << 24)) { st = 4; break; }
+  }
+  if (lane == 0) status[g] = st;
+}
+
 // encode_stream for explicit symbol lists (one CTA / thread per stream)
 __global__ void k_rc_encode_symbols(const int32_t* __restrict__ syms, const int64_t* __restrict__ off,
                                     const int64_t* __restrict__ len, uint8_t* __restrict__ out,
@@ -711,13 +962,16 @@ extern "C" int sst_rc_encode(const int16_t* scans, int G, int64_t n, int64_t* id
   if (G < 0 || n < 0 || cap < 0) return SST_ERR_ARG;
   if (G == 0) return SST_OK;
   if ((n > 0 && (!scans || !idx_ws)) || !out || !out_len) return SST_ERR_ARG;
-  const char* mode = getenv("SST_RC");            // "fenwick": single-thread model (A/B)
+  // default: the cumulative-table warp coder; A/B: SST_RC=fenwick (single
+  // thread, Fenwick tree) or SST_RC=warp (warp-reduced counts)
+  const char* mode = getenv("SST_RC");
+  auto st = static_cast<cudaStream_t>(stream);
   if (mode && mode[0] == 'f')
-    k_rc_encode<<<G, kRcThreads, 0, static_cast<cudaStream_t>(stream)>>>(scans, n, idx_ws, out, cap,
-                                                                           out_len);
+    k_rc_encode<<<G, kRcThreads, 0, st>>>(scans, n, idx_ws, out, cap, out_len);
+  else if (mode && mode[0] == 'w')
+    k_rc_encode_w<<<G, kRcThreads, 0, st>>>(scans, n, idx_ws, out, cap, out_len);
   else
-    k_rc_encode_w<<<G, kRcThreads, 0, static_cast<cudaStream_t>(stream)>>>(scans, n, idx_ws, out,
-                                                                             cap, out_len);
+    k_rc_encode_c<<<G, kRcThreadsC, 0, st>>>(scans, n, idx_ws, out, cap, out_len);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }
@@ -728,12 +982,13 @@ extern "C" int sst_rc_decode(const uint8_t* data, const int64_t* off, const int6
   if (G == 0) return SST_OK;
   if (!data || !off || !len || !status || (n > 0 && !scans)) return SST_ERR_ARG;
   const char* mode = getenv("SST_RC");
+  auto st = static_cast<cudaStream_t>(stream);
   if (mode && mode[0] == 'f')
-    k_rc_decode<<<G, kRcThreads, 0, static_cast<cudaStream_t>(stream)>>>(data, off, len, n, scans,
-                                                                           status);
+    k_rc_decode<<<G, kRcThreads, 0, st>>>(data, off, len, n, scans, status);
+  else if (mode && mode[0] == 'w')
+    k_rc_decode_w<<<G, kRcThreads, 0, st>>>(data, off, len, n, scans, status);
   else
-    k_rc_decode_w<<<G, kRcThreads, 0, static_cast<cudaStream_t>(stream)>>>(data, off, len, n, scans,
-                                                                             status);
+    k_rc_decode_c<<<G, kRcThreadsC, 0, st>>>(data, off, len, n, scans, status);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }
