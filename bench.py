@@ -874,10 +874,10 @@ def small_configs(a, device) -> dict:
     import numpy as np
     import torch
 
-    from oracle import learned_oracle as LO
+    from oracle import learned_i8_oracle as LO8
     from oracle import semstream_oracle as O
     from oracle.synth import make_clip
-    from paper_2602_03529_b200.learned import LearnedConfig, LearnedGopCodec
+    from paper_2602_03529_b200.learned_i8 import LearnedI8Config, LearnedI8GopCodec
     from paper_2602_03529_b200.pipeline import GopCodec, StreamBank
 
     out = {}
@@ -885,8 +885,7 @@ def small_configs(a, device) -> dict:
     clip = make_clip("moving-square", 256, 256, 17, seed=0)
     gops = np.stack([clip.gop(0), clip.gop(1)])
     fr = torch.from_numpy(gops).to(device)
-    cfg = LearnedConfig()
-    lc = LearnedGopCodec(2, 256, 256, 2, cfg=cfg)
+    lc = LearnedI8GopCodec(2, 256, 256, 2, cfg=LearnedI8Config())
     o = torch.empty_like(fr)
     lc.set_gop_ids([0, 1])
     for _ in range(3):
@@ -899,9 +898,12 @@ def small_configs(a, device) -> dict:
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / 10
-    codes, idx, _, hw = lc.model.encode_frames(fr, 2)
-    oc, oi, _, _ = LO.encode(gops, 2, lc.model.host_weights, cfg.blocks)
+    codes, idx, mask, hw = lc.model.encode_frames(fr, 2)
+    oc, oi, _ = LO8.encode(gops, 2, lc.model.host_weights)
     agree = float((idx.cpu().numpy() == oi).mean())
+    dec = lc.model.decode_tokens(codes, mask, hw).cpu().numpy()
+    dec_exact = bool(np.array_equal(dec, LO8.decode(oc, np.ones(oc.shape[:-1], np.uint8), hw,
+                                                    lc.model.host_weights)))
     bank = StreamBank(1, 256, 256)
     po = torch.empty_like(fr[:1])
     prev, exact = None, True
@@ -914,6 +916,8 @@ def small_configs(a, device) -> dict:
         "learned_gop_ms": round(ms, 3),
         "learned_frames_per_s": round(17 / (ms / 1e3), 1),
         "learned_fsq_index_agreement_vs_oracle": round(agree, 5),
+        "learned_decoded_frames_bit_exact_vs_oracle": dec_exact,
+        "learned_model": "int8 (kind::i8), exact vs oracle/learned_i8_oracle.py",
         "proxy_s2_bit_exact_vs_cpu_reference": exact,
         "note": "one clip (2 GoPs per launch): launch-latency bound, not a throughput config"}
     # ---- configs[1]

@@ -60,7 +60,7 @@ def main():
     agg = launches(lcsv)
     tot = sum(v[0] for v in agg.values())
     lines += ["## Launch list (`ncu --metrics gpu__time_duration.sum --clock-control none -k regex:^k_` "
-              "over `python scripts/learned_step.py 32 2`: 2 steps of LearnedGopCodec, 32 x 1080p GoPs, s=3; "
+              "over `python scripts/learned_step.py 32 2 [i8|bf16]`: 2 steps of the learned codec, 32 x 1080p GoPs, s=3; "
               "cold-cache and serialised, so compare shares)", "",
               "| kernel | launches | total us | share |", "|---|---|---|---|"]
     for k, (v, n) in sorted(agg.items(), key=lambda x: -x[1][0]):
@@ -72,6 +72,10 @@ def main():
             for key, label in METRICS:
                 if key in d:
                     lines.append(f"| {label} (`{key}`) | {d[key]} {units.get(key, '')} |")
+            # int8 tensor-op paths (kind::i8: UTCIMMA), whatever their exact metric names
+            for key in sorted(k for k in d if "utcimma" in k and k.endswith("pct_of_peak_sustained_elapsed")
+                              and d[k] not in ("", "0")):
+                lines.append(f"| int8 tensor op % of peak (`{key}`) | {d[key]} |")
             stalls = {k: float(v) for k, v in d.items()
                       if k.startswith("smsp__pcsamp_warps_issue_stalled_") and not k.endswith("not_issued")
                       and v.replace('.', '', 1).isdigit()}
