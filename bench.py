@@ -109,9 +109,29 @@ def scale_of(stream: int, k: int) -> int:
     return SCALE_PATTERN[(k + half) % len(SCALE_PATTERN)]
 
 
+_CLOCK_POLL = r"""
+import sys, time, pynvml
+pynvml.nvmlInit()
+uuid = sys.argv[1]
+try:
+    h = pynvml.nvmlDeviceGetHandleByUUID(uuid)
+except Exception:
+    h = pynvml.nvmlDeviceGetHandleByIndex(int(sys.argv[2]))
+get = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+    pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+print("max", pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM), flush=True)
+while True:
+    print(time.monotonic(), pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM), int(get(h)),
+          flush=True)
+    time.sleep(0.002)
+"""
+
+
 class ClockSampler:
     """SM clock and clock-event (throttle) reasons sampled through NVML every
-    ~5 ms during the timed region (nvidia-smi's 100 ms loop is too coarse)."""
+    ~2 ms during the timed region, from a separate PROCESS (a thread of this
+    one competes with the launch loop for the GIL and sampled only a few
+    times per run).  Samples taken before the region opens are discarded."""
 
     BITS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
             0x4: "sw_power_cap", 0x80: "hw_power_brake_slowdown"}
@@ -121,42 +141,47 @@ class ClockSampler:
         self.samples = []
         self.max_mhz = None
         self.err = ""
-        self._stop = threading.Event()
+        self._p = None
+        self._lines = []
         self._t = None
+        self._t0 = None
+        self._t1 = None
 
     def __enter__(self):
+        import subprocess
         try:
-            import pynvml
             import torch
-            pynvml.nvmlInit()
             uuid = str(torch.cuda.get_device_properties(self.index).uuid)
             uuid = uuid if uuid.startswith("GPU-") else f"GPU-{uuid}"
-            try:
-                h = pynvml.nvmlDeviceGetHandleByUUID(uuid)
-            except Exception:
-                h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
-            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
-            get_reasons = getattr(pynvml, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
-                pynvml.nvmlDeviceGetCurrentClocksThrottleReasons
+            self._p = subprocess.Popen([sys.executable, "-c", _CLOCK_POLL, uuid, str(self.index)],
+                                       stdout=subprocess.PIPE, stderr=subprocess.DEVNULL,
+                                       text=True)
+            first = self._p.stdout.readline().split()          # wait until polling runs
+            if first and first[0] == "max":
+                self.max_mhz = int(first[1])
 
-            def poll():
-                while not self._stop.is_set():
-                    try:
-                        self.samples.append((pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM),
-                                             int(get_reasons(h))))
-                    except Exception as e:  # pragma: no cover
-                        self.err = str(e)
-                    time.sleep(0.005)
-            self._t = threading.Thread(target=poll, daemon=True)
+            def reader():                       # drain the pipe; filter by the poller's clock
+                for ln in self._p.stdout:
+                    self._lines.append(ln)
+            self._t = threading.Thread(target=reader, daemon=True)
             self._t.start()
+            self._t0 = time.monotonic()             # CLOCK_MONOTONIC: shared with the poller
         except Exception as e:
             self.err = f"{type(e).__name__}: {e}"
         return self
 
     def __exit__(self, *exc):
-        self._stop.set()
-        if self._t is not None:
-            self._t.join(timeout=2)
+        t1 = time.monotonic()
+        if self._p is not None:
+            time.sleep(0.01)
+            self._p.kill()
+            self._p.wait()
+            if self._t is not None:
+                self._t.join(timeout=2)
+        for ln in list(self._lines):
+            parts = ln.split()
+            if len(parts) == 3 and self._t0 <= float(parts[0]) <= t1:
+                self.samples.append((int(parts[1]), int(parts[2])))
 
     def summary(self) -> dict:
         if not self.samples:
@@ -166,7 +191,7 @@ class ClockSampler:
                           if r & bit})
         return {"sm_mhz": statistics.median(m for m, _ in self.samples),
                 "sm_max_mhz": self.max_mhz, "reasons": reasons, "samples": len(self.samples),
-                "source": "NVML, 5 ms polling inside the timed region"}
+                "source": "NVML, ~2 ms polling from a separate process inside the timed region"}
 
 
 def measured_hbm_peak():
@@ -1117,6 +1142,57 @@ def measured_i8_peak(device) -> tuple:
         return 2 * bf, f"2 x measured bf16 peak (int8 GEMM probe failed: {type(e).__name__})"
 
 
+def learned_e2e(a, device, model, Codec, s: int) -> dict:
+    """The learned codec end to end from pinned HOST frames: each step copies
+    the GoPs' frames host -> device, runs the whole codec (encode, FSQ, drop,
+    packetise, parse, decode, upscale + blend) and copies the reconstructed
+    frames device -> host, inside the timed region; lanes on their own CUDA
+    streams overlap the two PCIe directions with compute."""
+    import torch
+    E, nl, H, W = 8, 4, a.height, a.width
+    per = E // nl
+    gen = torch.Generator(device=device).manual_seed(1)
+    L = []
+    for j in range(nl):
+        c = Codec(per, H, W, s, model=model)
+        c.set_gop_ids(list(range(j * per, (j + 1) * per)))
+        h_in = torch.empty((per, GOP, H, W, 3), dtype=torch.float32, pin_memory=True)
+        h_in.copy_(torch.rand((per, GOP, H, W, 3), generator=gen, device=device))
+        L.append(dict(codec=c, h_in=h_in, h_out=torch.empty_like(h_in, pin_memory=True),
+                      d_in=torch.empty((per, GOP, H, W, 3), device=device),
+                      d_out=torch.empty((per, GOP, H, W, 3), device=device),
+                      stream=torch.cuda.Stream(device=device), k=c.drop_k(a.drop)))
+
+    def one():
+        for ln in L:
+            with torch.cuda.stream(ln["stream"]):
+                ln["d_in"].copy_(ln["h_in"], non_blocking=True)
+                ln["codec"].step(ln["d_in"], ln["d_out"], per, drop_k=ln["k"])
+                ln["h_out"].copy_(ln["d_out"], non_blocking=True)
+
+    main = torch.cuda.current_stream()
+    for _ in range(2):
+        one()
+    torch.cuda.synchronize()
+    K = 5
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(main)
+    for ln in L:
+        ln["stream"].wait_stream(main)
+    for _ in range(K):
+        one()
+    for ln in L:
+        main.wait_stream(ln["stream"])
+    e1.record(main)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / K
+    nbytes = E * GOP * H * W * 3 * 4
+    return {"value": round(E * GOP / ms * 1e3, 1), "unit": UNIT, "h2d_bytes_per_step": nbytes,
+            "d2h_bytes_per_step": nbytes, "gops_per_step": E, "lanes": nl,
+            "path": "pinned host frames -> learned codec step -> pinned host frames, per lane "
+                    "stream, all inside the timed region"}
+
+
 def run_learned(a, device, precision: str = "i8") -> dict:
     """G 1080p GoPs per step through the learned codec (encoder + FSQ ->
     similarity -> 10% drop -> packetise -> parse / reassemble -> decoder ->
@@ -1198,6 +1274,7 @@ def run_learned(a, device, precision: str = "i8") -> dict:
         single.append(b0.elapsed_time(b1))
     single.sort()
     del c1
+    e2e = learned_e2e(a, device, model, Codec, s)
     # serialised pass (full batch, one stream): time every tensor-core layer
     times = []
     orig = model._conv
@@ -1210,9 +1287,9 @@ def run_learned(a, device, precision: str = "i8") -> dict:
         N, Kd = model.W[name].shape
         nt = taps[0] if isinstance(taps, tuple) else len(taps)
         tok = in_shape[0] * out_grid[0] * out_grid[1]
-        if nt == 18 and precision == "i8":
-            # useful work: t = 1 sees both temporal taps, t = 0 only its own
-            # (the kernel skips the all-padding t-1 tap there)
+        if nt == 18:
+            # useful work = issued work: t = 1 sees both temporal taps, t = 0
+            # only its own (both kernels skip the all-padding t-1 tap there)
             flops = 2 * tok * N * (Kd + Kd // 2)
         else:
             flops = 2 * tok * t_cnt * N * Kd
@@ -1248,8 +1325,8 @@ def run_learned(a, device, precision: str = "i8") -> dict:
         "value": round(G * GOP / ms * 1e3, 1), "unit": UNIT, "ms_per_step": round(ms, 3),
         "roofline": {"kernel": kern, "bound": "tensor", "achieved": round(achieved, 1),
                      "peak": round(peak, 1), "unit": unit, "frac": round(achieved / peak, 4),
-                     "peak_source": src, "counted": "useful MACs only (no zero-padding taps)"
-                     if precision == "i8" else "all issued MMAs",
+                     "peak_source": src,
+                     "counted": "useful MACs (= issued: the t=0 zero-padding tap is skipped)",
                      "ops_per_launch": halo and int(sum(fl for _, fl in halo) / len(halo)),
                      "avg_launch_ms": round(sum(m for m, _ in halo) / len(halo), 4),
                      "launches_per_step": len(halo)},
@@ -1260,6 +1337,7 @@ def run_learned(a, device, precision: str = "i8") -> dict:
                           "realtime_30fps_budget_ms_per_gop": round(GOP / 30 * 1e3, 1)},
         "gpu_launches_per_step": launches_step,
         "dtype": dtype,
+        "e2e": e2e,
     }
     if precision == "i8":
         ops = model.ops_per_gop(codec.Ht, codec.Wt) * G

@@ -778,6 +778,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
     g = tile / a.t_cnt;
     x0 = tx * TILE; y0 = ty * TILE;
   };
+  // at t = 0 the causal conv's temporal tap t-1 reads only zero padding:
+  // skip its halo loads and MMAs (the same sums: the skipped products are 0)
+  auto first_hi = [&](int t) { return (kHalo && t == 0) ? a.kb_per_tap : 0; };
 
   if (warp == 0) {
     if (lane == 0) {
@@ -786,7 +789,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
       for (int u = pair; u < n_units; u += npairs) {
         int g, t, x0, y0, nb;
         decode(u, g, t, x0, y0, nb);
-        for (int hi = 0; hi < nh; ++hi, ++hc) {
+        for (int hi = first_hi(t); hi < nh; ++hi, ++hc) {
           const int kt = hi / a.kb_per_tap, cb = hi - kt * a.kb_per_tap;
           const int hs = hc % HSLOTS;
           if (hc >= HSLOTS) mbar_wait(&hempty[hs], ((hc / HSLOTS) - 1) & 1);
@@ -813,11 +816,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
       constexpr uint32_t idesc = tc::idesc_bf16_f32(256, kNU);
       int hc = 0, bc = 0, it = 0;
       for (int u = pair; u < n_units; u += npairs, ++it) {
+        int g, t, x0, y0, nb;
+        decode(u, g, t, x0, y0, nb);
+        const int hi0 = first_hi(t);
         const int ab = it & 1;
         if (it >= 2) mbar_wait(&aempty[ab], ((it >> 1) - 1) & 1);
         tc::fence_after_sync();
         const uint32_t acc = tmem + ab * 256;
-        for (int hi = 0; hi < nh; ++hi, ++hc) {
+        for (int hi = hi0; hi < nh; ++hi, ++hc) {
           const int hs = hc % HSLOTS;
           mbar_wait(&hfull[hs], (hc / HSLOTS) & 1);
           const uint32_t hbase = smem_u32(sH + hs * HALO_STRIDE);
@@ -830,7 +836,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
             const uint64_t ad = halo_desc_pitch(hbase + (uint32_t)((dy * kPitch + dx) * 128), kPitch);
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              tc::mma_bf16_pair(acc, ad + 2 * k, bd + 2 * k, idesc, (hi | sp | k) != 0);
+              tc::mma_bf16_pair(acc, ad + 2 * k, bd + 2 * k, idesc, (hi != hi0 || sp | k) != 0);
             tc::mma_commit_pair(&bempty[bs]);
           }
           tc::mma_commit_pair(&hempty[hs]);
