@@ -173,3 +173,51 @@ def test_acceptance_9_stream_determinism_gpu(tmp_path, monkeypatch):
     _swap_hot_path(monkeypatch)
     a, b = run("gpu1"), run("gpu2")
     assert a == b == stock
+
+
+# ---------------------------------------------------------------------------
+# batched sender / receiver around the reference's netem (netserve.py)
+
+def test_linked_stream_bank_over_reference_netem():
+    """Three streams through one batched GPU codec, each over its own
+    reference EmulatedLink (loss, queue, trace pacing, propagation delay):
+    every reconstruction equals the CPU reference algorithm fed exactly the
+    packets the link delivered before the playout deadline."""
+    import numpy as np
+    import torch
+    from semstream.netem import EmulatedLink, constant_trace
+
+    from oracle import semstream_oracle as O
+    from oracle.synth import make_clip
+    from paper_2602_03529_b200.netserve import LinkedStreamBank
+
+    H, W, n, gops = 72, 96, 3, 4
+    links = [EmulatedLink(constant_trace(rate), loss_rate=0.2, seed=10 + i, queue_bytes=q)
+             for i, (rate, q) in enumerate(((2_000_000, 60_000), (60_000, 12_000), (25_000, 800)))]
+    lb = LinkedStreamBank(n, H, W, links)
+    clips = [make_clip("noisy-motion" if i % 2 else "moving-square", W, H, 9 * gops, seed=i)
+             for i in range(n)]
+    sched = [(3, 2, 2, 3), (2, 2, 3, 3), (3, 3, 3, 2)]
+    prev = [None] * n
+    saw = {"lost": 0, "queue": 0, "late": 0}
+    for k in range(gops):
+        by_s = {}
+        for i in range(n):
+            by_s.setdefault(sched[i][k], []).append(i)
+        frames = {s: torch.from_numpy(np.stack([clips[i].gop(k) for i in ids])).cuda()
+                  for s, ids in by_s.items()}
+        outs = {s: torch.empty_like(f) for s, f in frames.items()}
+        delivered = lb.step(frames, outs, by_s, k, drop_rate=0.1)
+        torch.cuda.synchronize()
+        for s, ids in by_s.items():
+            for j, i in enumerate(ids):
+                lost = set(int(p) for p in np.flatnonzero(delivered[i] == 0))
+                ref = O.pipeline_gop(clips[i].gop(k), s, gop_id=k, drop_rate=0.1, lost=lost,
+                                     prev_out=prev[i])
+                prev[i] = ref["frames"]
+                assert np.array_equal(outs[s][j].cpu().numpy(), np.stack(ref["frames"])), (k, i)
+    for st in lb.stats:
+        for key in saw:
+            saw[key] += st[key]
+        assert st["sent"] == st["delivered"] + st["lost"] + st["queue"] + st["late"]
+    assert saw["lost"] > 0 and saw["queue"] > 0 and saw["late"] > 0   # the links really interfered
