@@ -130,6 +130,13 @@ SST_API int sst_blend(const float* prev, const float* curr, int G, int H, int W,
 SST_API int sst_upscale_blend9(const float* img, int G, int h, int w, int s, int H, int W,
                                const SstPrevDesc* prev, int blend_n, float* out, void* stream);
 
+/* The same for uint8 working frames q whose sample value is float(q / 255)
+ * (the int8 learned tokenizer's decoder output, SST_LT_EPI_PIXELS_U8);
+ * prev[g].p_img points at the previous GoP's uint8 frames.  Output identical
+ * to sst_upscale_blend9 on the equivalent float32 frames. */
+SST_API int sst_upscale_blend9_u8(const uint8_t* img, int G, int h, int w, int s, int H, int W,
+                                  const SstPrevDesc* prev, int blend_n, float* out, void* stream);
+
 /* ---- tokenizer ---------------------------------------------------------- */
 
 /* scale_gop(down) (codec.py:248-254) fused with encode_gop (codec.py:143-157)
@@ -302,6 +309,7 @@ SST_API int sst_rc_decode_symbols(const uint8_t* data, int64_t nbytes, int64_t m
 #define SST_LT_EPI_STORE 0   /* bf16 activation tensor (+bias, SiLU, +residual) */
 #define SST_LT_EPI_FSQ 1     /* FSQ head: codes f64 [G][2][H'][W'][12], idx i32 [..][2], mask u8 */
 #define SST_LT_EPI_PIXELS 2  /* unpatchify: frames f32 [G][9][h][w][3], clamp [0,1] */
+#define SST_LT_EPI_PIXELS_U8 3 /* (sst_lt8_conv) unpatchify to uint8 q: sample = float(q / 255) */
 
 typedef struct SstConvDesc {
   const void* in;          /* bf16 [G][in_T][in_H][in_W][in_C], in_C % 64 == 0 */

@@ -52,7 +52,7 @@ class SstConvDesc(C.Structure):
                 ("bias_i32", C.c_void_p), ("act_lut", C.c_void_p)]
 
 
-LT_EPI_STORE, LT_EPI_FSQ, LT_EPI_PIXELS = 0, 1, 2
+LT_EPI_STORE, LT_EPI_FSQ, LT_EPI_PIXELS, LT_EPI_PIXELS_U8 = 0, 1, 2, 3
 
 INFO_BYTES = C.sizeof(SstPacketInfo)          # 64
 PREV_BYTES = C.sizeof(SstPrevDesc)            # 24
@@ -87,6 +87,7 @@ SIGNATURES = {
     "sst_mean_diff": (_I, [_P, _P, _L, _L, _I, _P, _P]),
     "sst_similarity_gop": (_I, [_P, _I, _L, _I, _P, _P]),
     "sst_upscale_blend9": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P]),
+    "sst_upscale_blend9_u8": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P]),
     "sst_lt_conv": (_I, [C.POINTER(SstConvDesc), _P]),
     "sst_lt8_conv": (_I, [C.POINTER(SstConvDesc), _P]),
     "sst_lt8_patchify": (_I, [_P, _I, _I, _I, _I, _P, _P, _P]),

@@ -55,8 +55,9 @@ struct Args {
   double* codes;
   int32_t* idx;
   uint8_t* mask;
-  float* frames;
+  float* frames;               // PIXELS: float32 frames, or uint8 q frames when pix_u8
   int h, w, frame_base;
+  int pix_u8;
 };
 
 __device__ __forceinline__ int rq(int32_t acc, int32_t b, int sh) {
@@ -265,6 +266,26 @@ __global__ void __launch_bounds__(128)
         for (int i = 0; i < 32; ++i) v[q * 32 + i] = u[i];
       }
       if (!valid) continue;
+      if (a.pix_u8) {
+        uint8_t* fr8 = reinterpret_cast<uint8_t*>(a.frames);
+#pragma unroll
+        for (int pr = 0; pr < 4; ++pr) {
+          const int Y = y * 8 + half * 4 + pr;
+          if (Y >= a.h) continue;
+          const int X0 = x * 8;
+          uint8_t* dst = fr8 + ((((size_t)g * 9 + f) * a.h + Y) * a.w + X0) * 3;
+          const int npx = min(8, a.w - X0);
+#pragma unroll
+          for (int e = 0; e < 24; ++e) {
+            if (e / 3 >= npx) continue;
+            const int i = pr * 24 + e;
+            const int r8 = (__float_as_int(v[i]) + __ldg(a.bias + n0 + half * 96 + i) +
+                            (1 << (a.shift - 1))) >> a.shift;
+            dst[e] = (uint8_t)min(max(r8, 0), 255);
+          }
+        }
+        continue;
+      }
 #pragma unroll
       for (int i = 0; i < 96; ++i)
         v[i] = pixel(__float_as_int(v[i]), __ldg(a.bias + n0 + half * 96 + i), a.shift);
@@ -501,6 +522,61 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::THREADS, 1)
         const int f = a.frame_base + nb;
         const int nb0 = nb * kNU + half * 96;
         const int4* bp4 = reinterpret_cast<const int4*>(a.bias + nb0);
+        const int xs = x0 + 8 * (int)rank;
+        if (a.pix_u8) {
+          // uint8 q frames (sample value float(q / 255)): a quarter of the bytes
+          // q in place of the accumulator bits (no second 96-register array)
+          auto qf = [&](int acc, int b) {
+            return __int_as_float(min(max((acc + b + (1 << (a.shift - 1))) >> a.shift, 0), 255));
+          };
+#pragma unroll
+          for (int i4 = 0; i4 < 24; ++i4) {
+            const int4 bb = __ldg(bp4 + i4);
+            v[4 * i4 + 0] = qf(__float_as_int(v[4 * i4 + 0]), bb.x);
+            v[4 * i4 + 1] = qf(__float_as_int(v[4 * i4 + 1]), bb.y);
+            v[4 * i4 + 2] = qf(__float_as_int(v[4 * i4 + 2]), bb.z);
+            v[4 * i4 + 3] = qf(__float_as_int(v[4 * i4 + 3]), bb.w);
+          }
+#define qv(i) __float_as_int(v[(i)])
+          uint8_t* fr8 = reinterpret_cast<uint8_t*>(a.frames);
+          const bool seg8 = (a.w * 3) % 16 == 0 && xs + 8 <= a.Wt && xs * 8 + 64 <= a.w;
+          if (seg8) {
+            uint8_t* srow = sStage + (warp - 2) * 768;          // [4][192] bytes
+#pragma unroll
+            for (int pr = 0; pr < 4; ++pr) {
+              uint32_t* s32 = reinterpret_cast<uint32_t*>(srow + (lane >> 3) * 192 + (lane & 7) * 24);
+#pragma unroll
+              for (int e = 0; e < 6; ++e)
+                s32[e] = pack4(qv(pr * 24 + 4 * e), qv(pr * 24 + 4 * e + 1), qv(pr * 24 + 4 * e + 2),
+                               qv(pr * 24 + 4 * e + 3));
+              __syncwarp();
+              for (int i = lane; i < 48; i += 32) {
+                const int r = i / 12, c16 = i - r * 12;
+                const int yr = y0 + q * 4 + r;
+                const int Y = yr * 8 + half * 4 + pr;
+                if (yr < a.Ht && Y < a.h)
+                  reinterpret_cast<uint4*>(fr8 + ((((size_t)g * 9 + f) * a.h + Y) * a.w + xs * 8) * 3)[c16] =
+                      reinterpret_cast<const uint4*>(srow + r * 192)[c16];
+              }
+              __syncwarp();
+            }
+            continue;
+          }
+          if (!valid) continue;
+#pragma unroll
+          for (int pr = 0; pr < 4; ++pr) {
+            const int Y = y * 8 + half * 4 + pr;
+            if (Y >= a.h) continue;
+            const int X0 = x * 8;
+            uint8_t* dst = fr8 + ((((size_t)g * 9 + f) * a.h + Y) * a.w + X0) * 3;
+            const int npx = min(8, a.w - X0);
+#pragma unroll
+            for (int e = 0; e < 24; ++e)
+              if (e / 3 < npx) dst[e] = (uint8_t)qv(pr * 24 + e);
+          }
+#undef qv
+          continue;
+        }
 #pragma unroll
         for (int i4 = 0; i4 < 24; ++i4) {
           const int4 bb = __ldg(bp4 + i4);
@@ -510,7 +586,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::THREADS, 1)
           v[4 * i4 + 3] = pixel_lut(__float_as_int(v[4 * i4 + 3]), bb.w, a.shift, pix_lut);
         }
         const bool vec = (a.w & 3) == 0;
-        const int xs = x0 + 8 * (int)rank;
         const bool seg = vec && xs + 8 <= a.Wt && xs * 8 + 64 <= a.w;
         if (seg) {
           float* srow = reinterpret_cast<float*>(sStage) + (warp - 2) * 768;   // [4][192]
@@ -873,6 +948,7 @@ static void fill_args(Args& a, const SstConvDesc* d, int tile_x, int tile_y) {
   a.out = static_cast<int8_t*>(d->out);
   a.codes = d->codes; a.idx = d->idx; a.mask = d->mask;
   a.frames = d->frames; a.h = d->h; a.w = d->w; a.frame_base = d->frame_base;
+  a.pix_u8 = d->epi == SST_LT_EPI_PIXELS_U8;
 }
 
 template <int BN, int EPI>
@@ -992,6 +1068,7 @@ extern "C" int sst_lt8_conv(const SstConvDesc* d, void* stream) {
         return SST_ERR_ARG;
       return l8::launch_tile<16, SST_LT_EPI_FSQ>(d, st);
     case SST_LT_EPI_PIXELS:
+    case SST_LT_EPI_PIXELS_U8:
       if (!d->frames || d->h <= 0 || d->w <= 0 || d->frame_base < 0 ||
           d->frame_base + d->N / 192 > 9 || d->h > d->Ht * 8 || d->w > d->Wt * 8 || d->N % 192)
         return SST_ERR_ARG;

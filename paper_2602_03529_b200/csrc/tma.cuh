@@ -92,5 +92,7 @@ __device__ __forceinline__ void fence_proxy_async_smem() {
 // (caller then uses the plain-load kernel variant).
 bool make_tmap_f32_3d(CUtensorMap* map, const void* base, uint64_t dim0, uint64_t dim1,
                       uint64_t dim2, uint32_t box0, uint32_t box1);
+bool make_tmap_u8_3d(CUtensorMap* map, const void* base, uint64_t dim0, uint64_t dim1,
+                     uint64_t dim2, uint32_t box0, uint32_t box1);
 
 }  // namespace sst

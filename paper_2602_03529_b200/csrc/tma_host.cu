@@ -126,3 +126,26 @@ bool make_tmap_u8_2d(CUtensorMap* map, const void* base, uint64_t d0, uint64_t d
 }
 
 }  // namespace sst
+
+namespace sst {
+
+// uint8 3-D map without swizzle (K5-9's byte windows of the int8 tokenizer's
+// working frames): dims {d0 (bytes), d1, d2}, box {box0, box1, 1}
+bool make_tmap_u8_3d(CUtensorMap* map, const void* base, uint64_t dim0, uint64_t dim1,
+                     uint64_t dim2, uint32_t box0, uint32_t box1) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  if ((reinterpret_cast<uintptr_t>(base) & 15u) || (dim0 & 15u)) return false;
+  if (box0 > 256 || box1 > 256 || box0 % 16 != 0) return false;
+  if (dim0 >= (1ull << 32) || dim1 >= (1ull << 32) || dim2 >= (1ull << 32)) return false;
+  cuuint64_t gdim[3] = {dim0, dim1, dim2};
+  cuuint64_t gstride[2] = {dim0, dim0 * dim1};
+  cuuint32_t box[3] = {box0, box1, 1};
+  cuuint32_t estride[3] = {1, 1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(base), gdim, gstride,
+                  box, estride, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+}  // namespace sst

@@ -641,10 +641,18 @@ static int launch_k5_v2(const CUtensorMap& imap, const UpArgs& a, const SstPrevD
 // [G*9][h][w*3] working frames, out-of-range rows / columns zero-filled) with
 // cp.async for the previous GoP's windows (their base pointers are per-GoP
 // table entries, so they have no single tensor map).
-template <int kBand>
+// uint8 windows (the int8 learned tokenizer's q = round(255 x) working
+// frames): TMA box rows start on a 16-byte = 16-element boundary, so the
+// pitch covers kWF + 15 elements
+constexpr int kWF9u8 = 160;
+template <typename T>
+__host__ __device__ constexpr int k59_pitch() { return sizeof(T) == 1 ? kWF9u8 : kWF9; }
+
+template <int kBand, typename T = float>
 struct Up9fGeom {
   static constexpr int kWR = kBand / 2 + 2;                      // max source rows (s >= 2)
-  static constexpr int kWin = (kWR * kWF9 + 31) / 32 * 32;       // floats per window, 128 B aligned
+  static constexpr int kA = 128 / (int)sizeof(T);                // elements per 128 bytes
+  static constexpr int kWin = (kWR * k59_pitch<T>() + kA - 1) / kA * kA;   // elements, 128 B aligned
 };
 
 // Window element type T: float (the windows as loaded), or double -- each
@@ -655,8 +663,9 @@ struct Up9fGeom {
 // half of its own slot and are widened in place (read all, sync, write all).
 template <int kBand, int kP, typename T = float>
 struct Up9fSmem {
-  T win[kGop][Up9fGeom<kBand>::kWin];
-  T winp[kP > 0 ? kP : 1][Up9fGeom<kBand>::kWin];   // previous GoP's frames 9-n+f, f < n = kP
+  T win[kGop][Up9fGeom<kBand, T>::kWin];
+  T winp[kP > 0 ? kP : 1][Up9fGeom<kBand, T>::kWin];   // previous GoP's frames 9-n+f, f < n = kP
+  double lut[sizeof(T) == 1 ? 256 : 1];   // uint8 windows: sample value of q (= float(q / 255))
   AxisTap ty_c[kBand], ty_p[kBand];
   int wx0[2], wx1[2];
   int xs;                    // current window's column shift (TMA alignment), 0 for cp.async
@@ -670,6 +679,13 @@ struct Up9fSmem {
 template <typename T, int kWin>
 __device__ __forceinline__ float* k5_9_land(T* w) {
   return reinterpret_cast<float*>(w) + (sizeof(T) == 8 ? kWin : 0);
+}
+
+// a window sample as the float64 the reference computes with
+template <typename T>
+__device__ __forceinline__ double k59_val(const T* w, int i, const double* lut) {
+  if constexpr (sizeof(T) == 1) return lut[w[i]];
+  else return (double)w[i];
 }
 
 template <int kBand, int kP, int NF, int NB, typename T>
@@ -701,8 +717,8 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
       } else {
 #pragma unroll
         for (int j = 0; j < NF; ++j) {
-          const T* wr = &S.win[f0 + j][(ty.lo - r0) * kWF9];
-          ia[j] = (double)wr[xl] * tx.g + (double)wr[xh] * tx.f;     // codec.py:233
+          const T* wr = &S.win[f0 + j][(ty.lo - r0) * k59_pitch<T>()];
+          ia[j] = k59_val(wr, xl, S.lut) * tx.g + k59_val(wr, xh, S.lut) * tx.f;     // codec.py:233
         }
       }
       ya = ty.lo;
@@ -714,8 +730,8 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
       } else {
 #pragma unroll
         for (int j = 0; j < NF; ++j) {
-          const T* wr = &S.win[f0 + j][(ty.hi - r0) * kWF9];
-          ib[j] = (double)wr[xl] * tx.g + (double)wr[xh] * tx.f;
+          const T* wr = &S.win[f0 + j][(ty.hi - r0) * k59_pitch<T>()];
+          ib[j] = k59_val(wr, xl, S.lut) * tx.g + k59_val(wr, xh, S.lut) * tx.f;
         }
       }
       yb = ty.hi;
@@ -730,8 +746,8 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
         } else {
 #pragma unroll
           for (int j = 0; j < NQ; ++j) {
-            const T* wq = &S.winp[j][(tp.lo - pr0) * kWF9];
-            qva[j] = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
+            const T* wq = &S.winp[j][(tp.lo - pr0) * k59_pitch<T>()];
+            qva[j] = k59_val(wq, pxl, S.lut) * txp.g + k59_val(wq, pxh, S.lut) * txp.f;
           }
         }
         qa = tp.lo;
@@ -743,8 +759,8 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
         } else {
 #pragma unroll
           for (int j = 0; j < NQ; ++j) {
-            const T* wq = &S.winp[j][(tp.hi - pr0) * kWF9];
-            qvb[j] = (double)wq[pxl] * txp.g + (double)wq[pxh] * txp.f;
+            const T* wq = &S.winp[j][(tp.hi - pr0) * k59_pitch<T>()];
+            qvb[j] = k59_val(wq, pxl, S.lut) * txp.g + k59_val(wq, pxh, S.lut) * txp.f;
           }
         }
         qb = tp.hi;
@@ -787,11 +803,26 @@ __device__ __forceinline__ void k5_9_window(float* dst, const float* img, int w,
   }
 }
 
+// byte windows (uint8 working frames), register-staged loads
+__device__ __forceinline__ void k5_9_window_u8(uint8_t* dst, const uint8_t* img, int w, int r0, int r1,
+                                               int c0f, int c1f, int tid) {
+  const int ncol = c1f - c0f;
+  const int lane = tid & 31, wid = tid >> 5;
+  for (int j = wid; j <= r1 - r0; j += kTQ / 32) {
+    const uint8_t* src = img + ((int64_t)(r0 + j) * w) * 3 + c0f;
+    uint8_t* d = dst + j * kWF9u8;
+#pragma unroll
+    for (int c = lane; c < kWF; c += 32)
+      if (c < ncol) d[c] = __ldg(src + c);
+  }
+}
+
 template <int kBand, bool kPrev, int kN, int kLoad, typename T>
 __global__ void __launch_bounds__(kTQ, sizeof(T) == 8 ? 2 : 3)
     k_upscale9f(const __grid_constant__ CUtensorMap imap, const __grid_constant__ UpArgs a) {
   constexpr int kP = kPrev ? kN - 1 : 0;      // previous-GoP windows (alpha > 0 frames)
-  constexpr int kWin = Up9fGeom<kBand>::kWin;
+  constexpr int kWin = Up9fGeom<kBand, T>::kWin;
+  constexpr bool kU8 = sizeof(T) == 1;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   Up9fSmem<kBand, kP, T>& S = *reinterpret_cast<Up9fSmem<kBand, kP, T>*>(smem_raw);
   const int tid = threadIdx.x;
@@ -811,7 +842,7 @@ __global__ void __launch_bounds__(kTQ, sizeof(T) == 8 ? 2 : 3)
   } else if (tid == 2 * kBand) {
     S.wx0[0] = axis_tap(q0 / 3, a.w, a.s).lo;
     S.wx1[0] = axis_tap(qlast / 3, a.w, a.s).hi;
-    S.xs = kLoad == 2 ? (S.wx0[0] * 3) & 3 : 0;
+    S.xs = kLoad == 2 ? (S.wx0[0] * 3) & (kU8 ? 15 : 3) : 0;
     if (kLoad == 2) {
       mbar_init(&S.bar, 1);
       fence_mbar_init();
@@ -820,6 +851,7 @@ __global__ void __launch_bounds__(kTQ, sizeof(T) == 8 ? 2 : 3)
     S.wx0[1] = axis_tap(q0 / 3, pd.w, pd.s).lo;
     S.wx1[1] = axis_tap(qlast / 3, pd.w, pd.s).hi;
   }
+  if (kU8) S.lut[tid] = (double)__fdiv_rn((float)tid, 255.0f);   // kTQ = 256 threads
   __syncthreads();
 
   // ---- load phase ----
@@ -827,13 +859,21 @@ __global__ void __launch_bounds__(kTQ, sizeof(T) == 8 ? 2 : 3)
     const int r0 = S.ty_c[0].lo, r1 = S.ty_c[rows - 1].hi;
     if (kLoad == 2) {
       if (tid == 0) {
-        constexpr uint32_t kBox = Up9fGeom<kBand>::kWR * kWF9 * sizeof(float);
+        constexpr uint32_t kBox =
+            Up9fGeom<kBand, T>::kWR * k59_pitch<T>() * (kU8 ? 1 : (uint32_t)sizeof(float));
         mbar_expect_tx(&S.bar, kGop * kBox);
 #pragma unroll 1
-        for (int f = 0; f < kGop; ++f)
-          tma_load_3d(k5_9_land<T, kWin>(S.win[f]), &imap, S.wx0[0] * 3 - S.xs, r0, g * kGop + f,
-                      &S.bar);
+        for (int f = 0; f < kGop; ++f) {
+          void* dst = kU8 ? (void*)S.win[f] : (void*)k5_9_land<T, kWin>(S.win[f]);
+          tma_load_3d(dst, &imap, S.wx0[0] * 3 - S.xs, r0, g * kGop + f, &S.bar);
+        }
       }
+    } else if constexpr (kU8) {
+      const int64_t fimg = (int64_t)a.h * a.w * 3;
+      const uint8_t* cur = reinterpret_cast<const uint8_t*>(a.img) + (int64_t)g * kGop * fimg;
+#pragma unroll 1
+      for (int f = 0; f < kGop; ++f)
+        k5_9_window_u8(S.win[f], cur + f * fimg, a.w, r0, r1, S.wx0[0] * 3, S.wx1[0] * 3 + 3, tid);
     } else {
       const int64_t fimg = (int64_t)a.h * a.w * 3;
       const float* cur = a.img + (int64_t)g * kGop * fimg;
@@ -846,9 +886,14 @@ __global__ void __launch_bounds__(kTQ, sizeof(T) == 8 ? 2 : 3)
       const int pr0 = S.ty_p[0].lo, pr1 = S.ty_p[rows - 1].hi;
       const int64_t pimg = (int64_t)pd.h * pd.w * 3;
 #pragma unroll
-      for (int j = 0; j < kP; ++j)
-        k5_9_window<kLoad == 0 ? 0 : 1>(k5_9_land<T, kWin>(S.winp[j]), pd.p_img + (kGop - kN + j) * pimg, pd.w, pr0,
-                                        pr1, S.wx0[1] * 3, S.wx1[1] * 3 + 3, tid);
+      for (int j = 0; j < kP; ++j) {
+        if constexpr (kU8)
+          k5_9_window_u8(S.winp[j], reinterpret_cast<const uint8_t*>(pd.p_img) + (kGop - kN + j) * pimg,
+                         pd.w, pr0, pr1, S.wx0[1] * 3, S.wx1[1] * 3 + 3, tid);
+        else
+          k5_9_window<kLoad == 0 ? 0 : 1>(k5_9_land<T, kWin>(S.winp[j]), pd.p_img + (kGop - kN + j) * pimg,
+                                          pd.w, pr0, pr1, S.wx0[1] * 3, S.wx1[1] * 3 + 3, tid);
+      }
     }
     if (kLoad != 0) cp_async_wait_all();
     if (kLoad == 2) mbar_wait(&S.bar, 0);
@@ -1159,4 +1204,32 @@ extern "C" int sst_blend(const float* prev, const float* curr, int G, int H, int
       prev, curr, G, fe, n, out);
   SST_LAUNCH_CHECK();
   return SST_OK;
+}
+
+// K5-9 over uint8 working frames q (sample value float(q / 255)): the int8
+// learned tokenizer's decoder emits q directly (no float32 frames in HBM).
+extern "C" int sst_upscale_blend9_u8(const uint8_t* img, int G, int h, int w, int s, int H, int W,
+                                     const SstPrevDesc* prev, int blend_n, float* out,
+                                     void* stream) {
+  if (G < 0 || h <= 0 || w <= 0 || H <= 0 || W <= 0) return SST_ERR_ARG;
+  if (s != 2 && s != 3) return SST_ERR_ARG;
+  if (H > h * s || W > w * s) return SST_ERR_ARG;
+  if (blend_n < 1 || blend_n > 8) return SST_ERR_ARG;
+  if (prev && blend_n > 4) return SST_ERR_UNSUPPORTED;
+  if (G == 0) return SST_OK;
+  if (!img || !out || G > 65535) return SST_ERR_ARG;
+  UpArgs a{};
+  a.img = reinterpret_cast<const float*>(img); a.G = G; a.h = h; a.w = w; a.s = s; a.H = H; a.W = W;
+  a.prev = prev; a.n = blend_n; a.out = out;
+  for (int i = 1; i <= 4; ++i) {
+    a.alpha[i - 1] = (double)(blend_n - i) / (double)blend_n;
+    a.beta[i - 1] = 1.0 - a.alpha[i - 1];
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  CUtensorMap imap;
+  memset(&imap, 0, sizeof(imap));
+  const bool tma_in = make_tmap_u8_3d(&imap, img, (uint64_t)w * 3, (uint64_t)h, (uint64_t)G * kGop,
+                                      kWF9u8, Up9fGeom<16, uint8_t>::kWR);
+  if (tma_in) return launch_k5_9f<16, 2, uint8_t>(imap, a, prev, blend_n, st);
+  return launch_k5_9f<16, 0, uint8_t>(imap, a, prev, blend_n, st);
 }

@@ -287,12 +287,16 @@ class LearnedTokenizerI8:
         self._blocks("dec", hbuf, ubuf, G, Ht, Wt)
         if frames is None:
             frames = torch.empty((G, GOP_SIZE, h, w, 3), dtype=torch.float32, device=dev)
-        elif tuple(frames.shape) != (G, GOP_SIZE, h, w, 3) or not frames.is_contiguous():
-            raise ValueError("frames buffer must be a contiguous [G][9][h][w][3] tensor")
+        elif tuple(frames.shape) != (G, GOP_SIZE, h, w, 3) or not frames.is_contiguous() or \
+                frames.dtype not in (torch.float32, torch.uint8):
+            raise ValueError("frames buffer must be a contiguous float32 or uint8 [G][9][h][w][3] "
+                             "tensor")
+        # uint8 frames hold q with sample value float(q / 255) (PIXELS_U8)
+        epi = _lib.LT_EPI_PIXELS_U8 if frames.dtype == torch.uint8 else _lib.LT_EPI_PIXELS
         self._conv("out_i", hbuf, (G, 2, Ht, Wt, D), (Ht, Wt), (1, _TAP_0), 0, 1,
-                   _lib.LT_EPI_PIXELS, frames=frames, hw=(h, w), frame_base=0)
+                   epi, frames=frames, hw=(h, w), frame_base=0)
         self._conv("out_p", hbuf, (G, 2, Ht, Wt, D), (Ht, Wt), (1, _TAP_0), 1, 1,
-                   _lib.LT_EPI_PIXELS, frames=frames, hw=(h, w), frame_base=1)
+                   epi, frames=frames, hw=(h, w), frame_base=1)
         return frames
 
     def ops_per_gop(self, Ht: int, Wt: int) -> int:
@@ -358,14 +362,18 @@ class LearnedI8GopCodec(GopCodec):
                                  device=dev)
         ws = _lib.load().sst_lt8_unpack_workspace(g_max, self.Ht, self.Wt)
         self.dec_ws = torch.empty((ws,), dtype=torch.uint8, device=dev)
-        self.frames9 = [torch.empty((g_max, GOP_SIZE, self.h, self.w, 3), dtype=torch.float32,
+        # decoded working frames as uint8 q (sample value float(q / 255)):
+        # the pixel epilogue writes a quarter of the bytes and K5-9 reads
+        # byte windows converted through a 256-entry table (no float32 ->
+        # float64 conversions for the horizontal pass)
+        self.frames9 = [torch.empty((g_max, GOP_SIZE, self.h, self.w, 3), dtype=torch.uint8,
                                     device=dev) for _ in range(2)]
         self.prev_desc = []
         for par in range(2):
             d = np.zeros(g_max, dtype=_lib.PREV_DTYPE)
             src = self.frames9[1 - par]
             d["p_img"] = src.data_ptr() + np.arange(g_max, dtype=np.uint64) * np.uint64(
-                src[0].numel() * 4)
+                src[0].numel())
             d["h"], d["w"], d["s"] = self.h, self.w, s
             self.prev_desc.append(torch.from_numpy(d.view(np.uint8).copy()).to(dev))
         self.parity = 0
@@ -404,11 +412,18 @@ class LearnedI8GopCodec(GopCodec):
         tm.end("L_decode")
         return self.frames9[parity][:g]
 
+    def frames_f32(self, parity: int, g: int) -> torch.Tensor:
+        """The decoded working frames of a parity as float32 (q / 255)."""
+        # IEEE float32 q / 255 (numpy divides exactly; a CUDA division by a
+        # host scalar would multiply by a rounded reciprocal)
+        lut = torch.from_numpy(np.arange(256, dtype=np.float32) / np.float32(255.0))
+        return lut.to(self.frames9[0].device)[self.frames9[parity][:g].long()]
+
     def reconstruct(self, g: int, parity: int, out: torch.Tensor, blend: bool = True) -> None:
         check_gop_tensor(out, g, self.H, self.W, "out")
         self.timer.begin("K5_upscale_blend")
         prev = self.prev_desc[parity].data_ptr() if blend else None
-        _lib.call("sst_upscale_blend9", self.frames9[parity].data_ptr(), g, self.h, self.w,
+        _lib.call("sst_upscale_blend9_u8", self.frames9[parity].data_ptr(), g, self.h, self.w,
                   self.s, self.H, self.W, prev, self.blend_n, out.data_ptr(), _dev.stream())
         self.timer.end("K5_upscale_blend")
 

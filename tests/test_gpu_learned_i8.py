@@ -310,7 +310,7 @@ def test_i8_gop_codec_stages_bit_exact():
         torch.cuda.synchronize()
         ocodes, _, hw = LO.encode(fr, s, w)
         arena, lengths = codec.arena.cpu().numpy(), codec.lengths.cpu().numpy()
-        frames9 = codec.frames9[(codec.parity ^ 1)][:G].cpu().numpy()
+        frames9 = codec.frames_f32(codec.parity ^ 1, G).cpu().numpy()   # uint8 q -> q / 255
         got = out.cpu().numpy()
         for j in range(G):
             iv, pv = ocodes[j, 0], ocodes[j, 1]
@@ -333,3 +333,43 @@ def test_i8_gop_codec_stages_bit_exact():
                 up = O.blend(prev[j], up, 2)
             prev[j] = up
             assert np.array_equal(got[j], np.stack(up)), (k, j)
+
+
+@pytest.mark.parametrize("mode", ["pair", "tile"])
+def test_pixels_u8_equals_f32(mode, monkeypatch):
+    """PIXELS_U8 writes q with float(q / 255) == the float32 epilogue's sample."""
+    if mode == "tile":
+        monkeypatch.setenv("SST_LT8_GEMM", "tile")
+    rng = np.random.default_rng(12)
+    model = LearnedTokenizerI8(LearnedI8Config())
+    hw = (17 * 8 - 5, 29 * 8 - 3)
+    xin = torch.from_numpy(_i8(rng, (2, 2, 17, 29, 256), -40, 40)).cuda()
+    a = model.decode_inputs(xin, hw)
+    u8 = torch.empty((2, 9) + hw + (3,), dtype=torch.uint8, device="cuda")
+    model.decode_inputs(xin, hw, frames=u8)
+    lut = torch.arange(256, dtype=torch.float32, device="cuda") / torch.tensor(255.0, device="cuda")
+    assert torch.equal(lut[u8.long()], a)
+
+
+@pytest.mark.parametrize("s,n", [(3, 2), (2, 3), (3, 1)])
+def test_upscale_blend9_u8_equals_f32(s, n):
+    """K5-9 over uint8 q frames == K5-9 over the float32 frames q / 255."""
+    rng = np.random.default_rng(13)
+    G, H, W = 2, 270, 480
+    h, w = -(-H // s), -(-W // s)
+    q = torch.from_numpy(rng.integers(0, 256, (G, 9, h, w, 3)).astype(np.uint8)).cuda()
+    qp = torch.from_numpy(rng.integers(0, 256, (G, 9, h, w, 3)).astype(np.uint8)).cuda()
+    lut = torch.arange(256, dtype=torch.float32, device="cuda") / torch.tensor(255.0, device="cuda")
+    f, fp = lut[q.long()].contiguous(), lut[qp.long()].contiguous()
+    outs = []
+    for img, prv, fn in ((q, qp, "sst_upscale_blend9_u8"), (f, fp, "sst_upscale_blend9")):
+        d = np.zeros(G, dtype=_lib.PREV_DTYPE)
+        d["p_img"] = prv.data_ptr() + np.arange(G, dtype=np.uint64) * np.uint64(prv[0].numel() *
+                                                                              prv.element_size())
+        d["h"], d["w"], d["s"] = h, w, s
+        pd = torch.from_numpy(d.view(np.uint8).copy()).cuda()
+        o = torch.empty((G, 9, H, W, 3), dtype=torch.float32, device="cuda")
+        _lib.call(fn, img.data_ptr(), G, h, w, s, H, W, pd.data_ptr(), n, o.data_ptr(), _dev.stream())
+        outs.append(o)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1])
