@@ -817,8 +817,11 @@ __device__ __forceinline__ void k5_9_window_u8(uint8_t* dst, const uint8_t* img,
   }
 }
 
+#ifndef SST_K59_U8_MINB
+#define SST_K59_U8_MINB 3
+#endif
 template <int kBand, bool kPrev, int kN, int kLoad, typename T>
-__global__ void __launch_bounds__(kTQ, sizeof(T) == 8 ? 2 : 3)
+__global__ void __launch_bounds__(kTQ, sizeof(T) == 8 ? 2 : (sizeof(T) == 1 ? SST_K59_U8_MINB : 3))
     k_upscale9f(const __grid_constant__ CUtensorMap imap, const __grid_constant__ UpArgs a) {
   constexpr int kP = kPrev ? kN - 1 : 0;      // previous-GoP windows (alpha > 0 frames)
   constexpr int kWin = Up9fGeom<kBand, T>::kWin;
