@@ -269,6 +269,12 @@ SST_API int sst_sparsify(const double* avg, int G, int64_t n, double theta, doub
 SST_API int sst_apply_residual(float* img, const int16_t* dense, const int32_t* count, int G,
                                int h, int w, double step, void* stream);
 
+/* compute_residual (residual.py:62-73): out[e] = (double)x[e] - (double)xh[e]. */
+SST_API int sst_residual_diff(const float* x, const float* xh, int64_t n, double* out, void* stream);
+
+/* SparseResidual.dense (residual.py:56-59): out[e] = (double)q[e] * step. */
+SST_API int sst_dequant_i16(const int16_t* q, int64_t n, double step, double* out, void* stream);
+
 /* out[e] = keep[e] ? dense[e] : 0 (fit_to_budget candidate scan). */
 SST_API int sst_mask_scan(const int16_t* dense, const uint8_t* keep, int64_t total, int16_t* out,
                           void* stream);

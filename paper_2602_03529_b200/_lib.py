@@ -105,6 +105,8 @@ SIGNATURES = {
     "sst_sparsify": (_I, [_P, _I, _L, C.c_double, C.c_double, _P, _P, _P, _P]),
     "sst_apply_residual": (_I, [_P, _P, _P, _I, _I, _I, C.c_double, _P]),
     "sst_mask_scan": (_I, [_P, _P, _L, _P, _P]),
+    "sst_residual_diff": (_I, [_P, _P, _L, _P, _P]),
+    "sst_dequant_i16": (_I, [_P, _L, C.c_double, _P, _P]),
     "sst_rc_encode": (_I, [_P, _I, _L, _P, _P, _L, _P, _P]),
     "sst_rc_decode": (_I, [_P, _P, _P, _I, _L, _P, _P, _P]),
     "sst_rc_encode_symbols": (_I, [_P, _P, _P, _I, _P, _L, _P, _P]),

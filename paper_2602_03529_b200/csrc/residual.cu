@@ -992,3 +992,40 @@ extern "C" int sst_rc_decode(const uint8_t* data, const int64_t* off, const int6
   SST_LAUNCH_CHECK();
   return SST_OK;
 }
+
+// ---- compat-layer elementwise pieces of residual.py ------------------------
+namespace sst {
+__global__ void k_residual_diff(const float* __restrict__ x, const float* __restrict__ xh, int64_t n,
+                                double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (double)x[i] - (double)xh[i];
+}
+__global__ void k_dequant_i16(const int16_t* __restrict__ q, int64_t n, double step,
+                              double* __restrict__ out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = (double)q[i] * step;
+}
+}  // namespace sst
+
+// compute_residual (residual.py:62-73): out = float64(x) - float64(x_hat)
+extern "C" int sst_residual_diff(const float* x, const float* xh, int64_t n, double* out,
+                                 void* stream) {
+  if (n < 0) return SST_ERR_ARG;
+  if (n == 0) return SST_OK;
+  if (!x || !xh || !out) return SST_ERR_ARG;
+  k_residual_diff<<<(unsigned)ceil_div64(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      x, xh, n, out);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+// SparseResidual.dense (residual.py:56-59): out = float64(q) * step
+extern "C" int sst_dequant_i16(const int16_t* q, int64_t n, double step, double* out, void* stream) {
+  if (n < 0) return SST_ERR_ARG;
+  if (n == 0) return SST_OK;
+  if (!q || !out) return SST_ERR_ARG;
+  k_dequant_i16<<<(unsigned)ceil_div64(n, 256), 256, 0, static_cast<cudaStream_t>(stream)>>>(
+      q, n, step, out);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
