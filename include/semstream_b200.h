@@ -406,6 +406,13 @@ SST_API int sst_lt8_patchify(const float* frames, int G, int H, int W, int s, vo
 SST_API int sst_lt8_attn(const void* qkv, int G, int Ht, int Wt, int D, int shift,
                          const uint8_t* exp_lut, void* out, void* stream);
 
+/* The same with GLOBAL causal attention: every query attends all valid tokens
+ * of the latent frames <= its own (full H' x W' frames, no windows); keys
+ * stream through shared memory in 128-token tiles (two passes: row max, then
+ * P / sum / O += P V on tcgen05), bit-exact to the oracle. */
+SST_API int sst_lt8_attn_global(const void* qkv, int G, int Ht, int Wt, int D, int shift,
+                                const uint8_t* exp_lut, void* out, void* stream);
+
 /* Decoder input from a token matrix (plug-in path): received f64 codes
  * [G][2][H'][W'][12] + mask -> snapped, concealed codes (ws: G*2*H'*W'*16
  * bytes) -> the first layer's gathered (2,3,3) neighbourhood, int8

@@ -157,10 +157,36 @@ def attention_core(qkv: np.ndarray, D: int, hd: int, sh_s: int, exp_lut) -> np.n
     return out.astype(np.int8)
 
 
+def attention_core_global(qkv: np.ndarray, D: int, hd: int, sh_s: int, exp_lut) -> np.ndarray:
+    """Global causal attention: a query of latent frame t attends every token
+    of frames <= t (all H' x W' positions, no windows); same integer softmax."""
+    G, T, Ht, Wt, _ = qkv.shape
+    n = Ht * Wt
+    x = qkv.reshape(G, T * n, 3 * D)
+    frame = np.arange(T * n) // n
+    allowed = frame[None, :] <= frame[:, None]                     # [q][k]
+    lut = np.asarray(exp_lut, np.int64)
+    out = np.zeros((G, T * n, D), np.int64)
+    for g in range(G):
+        for h in range(D // hd):
+            q = x[g, :, h * hd:(h + 1) * hd].astype(np.float64)
+            k = x[g, :, D + h * hd:D + (h + 1) * hd].astype(np.float64)
+            v = x[g, :, 2 * D + h * hd:2 * D + (h + 1) * hd].astype(np.float64)
+            S = (q @ k.T).astype(np.int64)
+            m = np.where(allowed, S, np.iinfo(np.int64).min).max(axis=-1, keepdims=True)
+            d = np.minimum((m - np.where(allowed, S, m)) >> sh_s, 255)
+            e = np.where(allowed, lut[d], 0)
+            l_ = e.sum(axis=-1, keepdims=True)
+            Ov = (e.astype(np.float64) @ v).astype(np.int64)
+            out[g, :, h * hd:(h + 1) * hd] = np.clip((2 * Ov + l_) // (2 * l_), -127, 127)
+    return out.reshape(G, T, Ht, Wt, D).astype(np.int8)
+
+
 def attention_block(h: np.ndarray, w: dict, part: str) -> np.ndarray:
     D = h.shape[-1]
     qkv = linear(h, w, f"{part}_qkv")
-    o = attention_core(qkv, D, w["head_dim"], w["attn_shift"], w["exp"])
+    core = attention_core_global if w.get("attn_scope") == "global" else attention_core
+    o = core(qkv, D, w["head_dim"], w["attn_shift"], w["exp"])
     return linear(o, w, f"{part}_proj", residual=h)
 
 

@@ -880,6 +880,176 @@ __global__ void __launch_bounds__(128, 4)
   if (warp == 0) tc::tmem_dealloc(tmem, 128);
 }
 
+// ---- global causal attention (full-frame keys), integer softmax --------------
+// One CTA = one (GoP, latent frame t, 128-query tile, 128-dim head).  The
+// query attends every token of frames <= t (2 x H' x W' keys at t = 1), so the
+// keys stream through shared memory in tiles of 128 in two passes: pass 1
+// finds the row max (S = Q K^T per tile on tcgen05), pass 2 recomputes each
+// tile's S, forms P = EXP[min((max - S) >> sh, 255)] and accumulates O += P V
+// in TMEM (int32, exact in any order) -- the same arithmetic as the windowed
+// kernel over all keys, so the result is still bit-exact to the oracle.
+constexpr int AG_SMEM = 4 * 16384 + 1024 + 64 + 256;
+
+__global__ void __launch_bounds__(128, 2)
+    k_l8_attn_global(const int8_t* __restrict__ qkv, int G, int n, int D, int shift,
+                     const uint8_t* __restrict__ exp_lut, int8_t* __restrict__ out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;                 // [128 q][128 d]      A of S
+  uint8_t* sK = smem + 16384;         // [128 k][128 d]      B of S (K-major)
+  uint8_t* sV = smem + 32768;         // [128 k][128 d]      B of O (MN-major)
+  uint8_t* sP = smem + 49152;         // [128 q][128 k] u8   A of O
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 65536);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 2);
+  uint8_t* lut = smem + 65536 + 64;
+
+  const int head = blockIdx.y;
+  const int g = blockIdx.z >> 1, t = blockIdx.z & 1;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int qi = blockIdx.x * 128 + tid;
+  const bool valid_q = qi < n;
+  const size_t tok_q = ((size_t)g * 2 + t) * n + qi;
+  const int nkeys = (t + 1) * n;
+  const int ntiles = (nkeys + 127) / 128;
+
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    fence_mbar_init();
+  }
+  if (warp == 0) tc::tmem_alloc(tmem_slot, 256);
+  lut[tid] = exp_lut[tid];
+  lut[tid + 128] = exp_lut[tid + 128];
+  {
+    const uint4* qb = reinterpret_cast<const uint4*>(qkv + tok_q * 3 * D + head * AT_HD);
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      *reinterpret_cast<uint4*>(sQ + tid * 128 + ((j ^ (tid & 7)) << 4)) =
+          valid_q ? __ldg(qb + j) : make_uint4(0, 0, 0, 0);
+  }
+  auto load_kv = [&](int kt, bool with_v) {
+    const int k = kt * 128 + tid;
+    const bool vk = k < nkeys;
+    const int tt = vk ? k / n : 0, pos = vk ? k - tt * n : 0;
+    const uint4* kb = reinterpret_cast<const uint4*>(
+        qkv + (((size_t)g * 2 + tt) * n + pos) * 3 * D + D + head * AT_HD);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int off = tid * 128 + ((j ^ (tid & 7)) << 4);
+      *reinterpret_cast<uint4*>(sK + off) = vk ? __ldg(kb + j) : make_uint4(0, 0, 0, 0);
+      if (with_v)
+        *reinterpret_cast<uint4*>(sV + off) = vk ? __ldg(kb + D / 16 + j) : make_uint4(0, 0, 0, 0);
+    }
+    fence_proxy_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();
+    tc::fence_after_sync();
+  };
+  fence_proxy_async_smem();
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  constexpr uint32_t id1 = tc::idesc_i8_s32(128, 128, true, true);
+  constexpr uint32_t id2 = tc::idesc_i8_s32(128, 128, false, true) | (1u << 16);
+  uint32_t ph0 = 0, ph1 = 0;
+  auto mma_s = [&]() {
+    if (tid == 0) {
+      const uint64_t ad = tc::smem_desc_sw128(smem_u32(sQ));
+      const uint64_t bd = tc::smem_desc_sw128(smem_u32(sK));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) tc::mma_i8(tmem, ad + 2 * k, bd + 2 * k, id1, k);
+      tc::mma_commit(&bar[0]);
+    }
+    mbar_wait(&bar[0], ph0);
+    ph0 ^= 1;
+    tc::fence_after_sync();
+  };
+
+  // ---- pass 1: row max over all allowed keys ----
+  int m = INT_MIN;
+  for (int kt = 0; kt < ntiles; ++kt) {
+    load_kv(kt, false);
+    mma_s();
+#pragma unroll 1
+    for (int c = 0; c < 128; c += 32) {
+      float v[32];
+      tc::tmem_ld32(trow + c, v);
+#pragma unroll
+      for (int i = 0; i < 32; ++i)
+        if (kt * 128 + c + i < nkeys) m = max(m, __float_as_int(v[i]));
+    }
+    tc::fence_before_sync();
+    __syncthreads();                  // S read by every thread, sK free
+  }
+  // ---- pass 2: P = EXP[...], l = sum P, O += P V ----
+  int l = 0;
+  for (int kt = 0; kt < ntiles; ++kt) {
+    load_kv(kt, true);
+    mma_s();
+#pragma unroll 1
+    for (int c = 0; c < 128; c += 32) {
+      float v[32];
+      tc::tmem_ld32(trow + c, v);
+      int e[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const bool ok = valid_q && kt * 128 + c + i < nkeys;
+        e[i] = ok ? (int)lut[min((m - __float_as_int(v[i])) >> shift, 255)] : 0;
+        l += e[i];
+      }
+#pragma unroll
+      for (int qq = 0; qq < 2; ++qq) {
+        const int j = (c >> 4) + qq;
+        const int* ee = e + 16 * qq;
+        *reinterpret_cast<uint4*>(sP + tid * 128 + ((j ^ (tid & 7)) << 4)) =
+            make_uint4(pack4(ee[0], ee[1], ee[2], ee[3]), pack4(ee[4], ee[5], ee[6], ee[7]),
+                       pack4(ee[8], ee[9], ee[10], ee[11]), pack4(ee[12], ee[13], ee[14], ee[15]));
+      }
+    }
+    fence_proxy_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();                  // P complete, S read: O may accumulate
+    tc::fence_after_sync();
+    if (tid == 0) {
+      const uint64_t ad = tc::smem_desc_sw128(smem_u32(sP));
+      const uint64_t bd = tc::smem_desc_sw128(smem_u32(sV));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) tc::mma_i8(tmem + 128, ad + 2 * k, bd + 256 * k, id2, (kt | k) != 0);
+      tc::mma_commit(&bar[1]);
+    }
+    mbar_wait(&bar[1], ph1);          // sP / sV / S free for the next tile
+    ph1 ^= 1;
+    tc::fence_after_sync();
+  }
+  const int l2 = 2 * max(l, 1);
+  const float rcp = 1.0f / (float)l2;
+#pragma unroll 1
+  for (int c = 0; c < 128; c += 32) {
+    float v[32];
+    tc::tmem_ld32(trow + 128 + c, v);
+    if (!valid_q) continue;
+    int o[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int q = floor_div_pos(2 * __float_as_int(v[i]) + l, l2, rcp);
+      o[i] = min(max(q, -127), 127);
+    }
+    uint4* op = reinterpret_cast<uint4*>(out + tok_q * D + head * AT_HD + c);
+#pragma unroll
+    for (int qq = 0; qq < 2; ++qq)
+      op[qq] = make_uint4(pack4(o[qq * 16 + 0], o[qq * 16 + 1], o[qq * 16 + 2], o[qq * 16 + 3]),
+                          pack4(o[qq * 16 + 4], o[qq * 16 + 5], o[qq * 16 + 6], o[qq * 16 + 7]),
+                          pack4(o[qq * 16 + 8], o[qq * 16 + 9], o[qq * 16 + 10], o[qq * 16 + 11]),
+                          pack4(o[qq * 16 + 12], o[qq * 16 + 13], o[qq * 16 + 14], o[qq * 16 + 15]));
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 256);
+}
+
 // ---- patchify -------------------------------------------------------------------
 template <int S>
 __global__ void k_l8_patchify(const float* __restrict__ src, int G, int H, int W, int h, int w,
@@ -1116,6 +1286,25 @@ extern "C" int sst_lt8_attn(const void* qkv, int G, int Ht, int Wt, int D, int s
                                     l8::AT_SMEM));
   l8::k_l8_attn<<<grid, 128, l8::AT_SMEM, st>>>(static_cast<const int8_t*>(qkv), G, Ht, Wt, D,
                                                 shift, exp_lut, static_cast<int8_t*>(out));
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+extern "C" int sst_lt8_attn_global(const void* qkv, int G, int Ht, int Wt, int D, int shift,
+                                   const uint8_t* exp_lut, void* out, void* stream) {
+  if (!qkv || !out || !exp_lut || G <= 0 || Ht <= 0 || Wt <= 0 || D <= 0 || D % l8::AT_HD)
+    return SST_ERR_ARG;
+  if (shift < 0 || shift > 30 || 2 * (int64_t)G > 65535 || D / l8::AT_HD > 65535) return SST_ERR_ARG;
+  if ((reinterpret_cast<uintptr_t>(qkv) & 15u) || (reinterpret_cast<uintptr_t>(out) & 15u))
+    return SST_ERR_ARG;
+  const int64_t n = (int64_t)Ht * Wt;
+  if (n > (1 << 24)) return SST_ERR_ARG;
+  dim3 grid((unsigned)((n + 127) / 128), D / l8::AT_HD, 2 * G);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  SST_CUDA_TRY(cudaFuncSetAttribute(l8::k_l8_attn_global, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    l8::AG_SMEM));
+  l8::k_l8_attn_global<<<grid, 128, l8::AG_SMEM, st>>>(static_cast<const int8_t*>(qkv), G, (int)n,
+                                                       D, shift, exp_lut, static_cast<int8_t*>(out));
   SST_LAUNCH_CHECK();
   return SST_OK;
 }

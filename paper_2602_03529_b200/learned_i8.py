@@ -40,8 +40,13 @@ class LearnedI8Config:
     blocks: int = 2         # residual blocks per side
     seed: int = 0
     attn: bool = True
+    # "window": causal attention inside 8x8 token windows (default);
+    # "global": every query attends all tokens of the latent frames <= its own
+    attn_scope: str = "window"
 
     def __post_init__(self):
+        if self.attn_scope not in ("window", "global"):
+            raise ValueError(f"attn_scope must be 'window' or 'global', got {self.attn_scope!r}")
         if self.dim <= 0 or self.dim % 256:
             raise ValueError(f"dim must be a positive multiple of 256, got {self.dim}")
         if not 0 <= self.blocks <= 8:
@@ -102,7 +107,7 @@ def make_weights_i8(cfg: LearnedI8Config) -> dict:
     attn_shift = _shift(HEAD_DIM, 32.0, 32.0, 16.0 * 8.0 / 1.5)
     return {"W": W, "b": b, "sh": sh, "silu": silu_table(), "exp": exp_table(),
             "attn_shift": attn_shift, "head_dim": HEAD_DIM, "blocks": cfg.blocks,
-            "attn": cfg.attn, "dim": D}
+            "attn": cfg.attn, "attn_scope": cfg.attn_scope, "dim": D}
 
 
 # ---------------------------------------------------------------------------
@@ -201,7 +206,8 @@ class LearnedTokenizerI8:
         self._conv(f"{part}_qkv", h, shape, (Ht, Wt), (1, _TAP_0), 0, 2, _lib.LT_EPI_STORE,
                    out=qkv)
         o = torch.empty_like(h)
-        _lib.call("sst_lt8_attn", qkv.data_ptr(), G, Ht, Wt, D, self.host_weights["attn_shift"],
+        fn = "sst_lt8_attn_global" if self.cfg.attn_scope == "global" else "sst_lt8_attn"
+        _lib.call(fn, qkv.data_ptr(), G, Ht, Wt, D, self.host_weights["attn_shift"],
                   self.exp.data_ptr(), o.data_ptr(), _dev.stream())
         self.launches += 1
         self._conv(f"{part}_proj", o, shape, (Ht, Wt), (1, _TAP_0), 0, 2, _lib.LT_EPI_STORE,

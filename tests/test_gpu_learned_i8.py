@@ -373,3 +373,35 @@ def test_upscale_blend9_u8_equals_f32(s, n):
         outs.append(o)
     torch.cuda.synchronize()
     assert torch.equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("Ht,Wt", [(4, 6), (16, 16), (13, 37), (45, 80)])
+def test_global_attention_core_bit_exact(Ht, Wt):
+    rng = np.random.default_rng(14)
+    D = 256
+    qkv = _i8(rng, (2, 2, Ht, Wt, 3 * D), -60, 60)
+    lut = exp_table()
+    dev = _dev.device()
+    qd = torch.from_numpy(qkv).to(dev)
+    ld = torch.from_numpy(lut.copy()).to(dev)
+    out = torch.zeros((2, 2, Ht, Wt, D), dtype=torch.int8, device=dev)
+    _lib.call("sst_lt8_attn_global", qd.data_ptr(), 2, Ht, Wt, D, 9, ld.data_ptr(), out.data_ptr(),
+              _dev.stream())
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), LO.attention_core_global(qkv, D, 128, 9, lut))
+
+
+def test_global_attention_model_end_to_end():
+    clip = make_clip("moving-square", 256, 256, 9, seed=5)
+    fr = clip.gop(0)[None]
+    model = LearnedTokenizerI8(LearnedI8Config(attn_scope="global"))
+    codes, idx, mask, hw = model.encode_frames(torch.from_numpy(fr).cuda(), 2)
+    oc, oi, _ = LO.encode(fr, 2, model.host_weights)
+    assert np.array_equal(idx.cpu().numpy(), oi)
+    dec = model.decode_tokens(codes, mask, hw).cpu().numpy()
+    assert np.array_equal(dec, LO.decode(oc, np.ones(oc.shape[:-1], np.uint8), hw,
+                                         model.host_weights))
+    # and it differs from the windowed model (the 16x16 grid has 4 windows)
+    win = LearnedTokenizerI8(LearnedI8Config())
+    assert not np.array_equal(win.encode_frames(torch.from_numpy(fr).cuda(), 2)[1].cpu().numpy(),
+                              idx.cpu().numpy())
