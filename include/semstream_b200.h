@@ -400,6 +400,14 @@ SST_API int sst_lt8_conv(const SstConvDesc* d, void* stream);
 SST_API int sst_lt8_patchify(const float* frames, int G, int H, int W, int s, void* pI, void* pP,
                              void* stream);
 
+/* The same through the integer 3-D Haar wavelet front end (Cosmos' first
+ * stage): per 8x8 patch, three temporal levels over the eight
+ * P frames, then three spatial levels (horizontal, then vertical) on every
+ * frame slot; pairs (a, b) -> ((a + b) >> 1, (a - b) >> 1), Mallat layout,
+ * int8 throughout.  Same output layout; pP must be 16-byte aligned too. */
+SST_API int sst_lt8_patchify_haar(const float* frames, int G, int H, int W, int s, void* pI,
+                                  void* pP, void* stream);
+
 /* Causal 8x8-window attention core, 128-dim heads, integer softmax:
  * qkv int8 [G][2][H'][W'][3D] -> out int8 [G][2][H'][W'][D]; shift and
  * exp_lut (uint8[256]) as in the oracle. */

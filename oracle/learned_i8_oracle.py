@@ -20,7 +20,8 @@ arithmetic shift = floor):
 
 * pixel -> int8: ``rint(float64(px) * 255) - 128`` of the bit-exact
   working-resolution frame (codec.py:202-214 downscale, codec.py:99-105 edge
-  pad), patchified to I [H'][W'][192 -> 256 zero-padded] and P [H'][W'][1536];
+  pad), patchified to I [H'][W'][192 -> 256 zero-padded] and P [H'][W'][1536]
+  (optionally through an integer 3-D Haar front end, ``haar_front``);
 * layer: ``acc = sum_k x[k] * W[n][k]`` (K order tap-major, channel-minor;
   (2,3,3) taps see latent frames t-1, t and a 3x3 neighbourhood, zero
   outside), ``y = clamp(r(acc + b[n], sh), -127, 127)``, then SiLU as a
@@ -98,9 +99,49 @@ def quantize_pixels(px: np.ndarray) -> np.ndarray:
     return (np.rint(np.asarray(px, np.float32).astype(np.float64) * 255.0) - 128.0).astype(np.int8)
 
 
-def patchify(frames: np.ndarray, s: int):
+def haar_step(x: np.ndarray, axis: int, m: int) -> np.ndarray:
+    """One integer Haar analysis step on the first ``m`` entries of ``axis``:
+    pairs (a, b) = (x[2j], x[2j+1]) -> lo = (a + b) >> 1 at j, hi = (a - b) >> 1
+    at m/2 + j (floors; int8 in, int8 out: both stay in [-128, 127])."""
+    x = np.moveaxis(np.asarray(x, np.int64), axis, 0).copy()
+    a, b = x[0:m:2].copy(), x[1:m:2].copy()
+    x[:m // 2] = (a + b) >> 1
+    x[m // 2:m] = (a - b) >> 1
+    return np.moveaxis(x, 0, axis)
+
+
+def haar3(x: np.ndarray, axes) -> np.ndarray:
+    """Three dyadic levels (8 -> 4 -> 2 -> 1 low band) of the separable Haar
+    over ``axes`` (each of length 8), Mallat layout: at each level the low
+    band's region [0:m] along every axis is transformed, axes in the given
+    order (for the spatial pair: horizontal first, then vertical)."""
+    for m in (8, 4, 2):
+        sl = [slice(None)] * x.ndim
+        for ax in axes:
+            sl[ax] = slice(0, m)
+        sub = x[tuple(sl)]
+        for ax in axes:
+            sub = haar_step(sub, ax, m)
+        x = np.asarray(x, np.int64).copy()
+        x[tuple(sl)] = sub
+    return x
+
+
+def haar_front(q: np.ndarray) -> np.ndarray:
+    """Integer 3-D Haar wavelet front end (Cosmos' first stage),
+    applied to the quantised, patch-split pixels q int [G][Ht][Wt][9][8][8][3]
+    (frame, row, column, channel): the eight P frames get three temporal
+    levels (the I frame is the causal first frame and is transformed only in
+    space), then every frame slot three spatial levels (rows' horizontal pairs,
+    then columns').  Same coefficient layout as the pixels it replaces."""
+    q = np.asarray(q, np.int64).copy()
+    q[:, :, :, 1:] = haar3(q[:, :, :, 1:], (3,))
+    return haar3(q, (5, 4))
+
+
+def patchify(frames: np.ndarray, s: int, front: str = "patch"):
     """frames float32 [G][9][H][W][3] -> pI int8 [G][1][H'][W'][256] (192 used),
-    pP int8 [G][1][H'][W'][1536]."""
+    pP int8 [G][1][H'][W'][1536].  ``front="haar"`` inserts ``haar_front``."""
     fr = np.asarray(frames, dtype=np.float32)
     if s > 1:
         fr = O.downscale(fr, s)
@@ -108,6 +149,10 @@ def patchify(frames: np.ndarray, s: int):
     Ht, Wt = -(-h // 8), -(-w // 8)
     fr = np.pad(fr, ((0, 0), (0, 0), (0, Ht * 8 - h), (0, Wt * 8 - w), (0, 0)), mode="edge")
     q = quantize_pixels(fr).reshape(G, T, Ht, 8, Wt, 8, 3).transpose(0, 2, 4, 1, 3, 5, 6)
+    if front == "haar":
+        q = haar_front(q).astype(np.int8)
+    elif front != "patch":
+        raise ValueError(f"front must be 'patch' or 'haar', got {front!r}")
     pI = np.zeros((G, 1, Ht, Wt, 256), np.int8)
     pI[:, 0, :, :, :192] = q[:, :, :, 0].reshape(G, Ht, Wt, 192)
     pP = q[:, :, :, 1:].reshape(G, 1, Ht, Wt, 1536)
@@ -204,7 +249,7 @@ def fsq(acc: np.ndarray, b: np.ndarray, sh: int):
 
 def encode(frames: np.ndarray, s: int, w: dict):
     """-> (codes f64 [G][2][H'][W'][12], idx i32 [G][2][H'][W'][2], (h, w))."""
-    pI, pP, hw = patchify(frames, s)
+    pI, pP, hw = patchify(frames, s, w.get("front", "patch"))
     h0 = linear(pI, w, "pe_i")
     h1 = linear(pP, w, "pe_p")
     h = np.concatenate([h0, h1], axis=1)

@@ -91,6 +91,7 @@ SIGNATURES = {
     "sst_lt_conv": (_I, [C.POINTER(SstConvDesc), _P]),
     "sst_lt8_conv": (_I, [C.POINTER(SstConvDesc), _P]),
     "sst_lt8_patchify": (_I, [_P, _I, _I, _I, _I, _P, _P, _P]),
+    "sst_lt8_patchify_haar": (_I, [_P, _I, _I, _I, _I, _P, _P, _P]),
     "sst_lt8_attn": (_I, [_P, _I, _I, _I, _I, _I, _P, _P, _P]),
     "sst_lt8_attn_global": (_I, [_P, _I, _I, _I, _I, _I, _P, _P, _P]),
     "sst_lt8_dec_in": (_I, [_P, _P, _I, _I, _I, _P, _P, _P]),

@@ -6,6 +6,7 @@
 //
 //   k_l8_patchify  box downscale (bit-exact, codec.py:202-214) + edge pad +
 //                  8x8(x8) patchify -> int8 rint(px * 255) - 128
+//   k_l8_patchify_haar  the same through the integer 3-D Haar front end
 //   k_l8_tile      generic implicit-GEMM layer: one CTA = 128 tokens (16x8)
 //                  x BN channels, per-tap 5-D TMA loads, 4-stage ring; STORE
 //                  (requantise + SiLU table + saturating residual), FSQ head
@@ -1097,6 +1098,136 @@ __global__ void k_l8_patchify(const float* __restrict__ src, int G, int H, int W
   for (int ch = 0; ch < 3; ++ch) dst[ch] = px[ch];
 }
 
+// ---- patchify through the integer 3-D Haar front end -------------------------------
+// One CTA per (GoP, token row, 8 tokens): 64 x 8 threads, one pixel column of
+// the 8-row band each.  Each thread loads its pixel in all nine frames,
+// quantises it, runs the three temporal levels over the P frames in
+// registers and stores the frame slots straight into the OUTPUT layout held
+// in shared memory (I [8][256], P [8][1536]); the spatial levels then run
+// line by line in place (one thread per 8-, 4- or 2-long row / column of a
+// (frame slot, token, channel) plane), and the band leaves as two contiguous
+// 16-byte-vector runs.  Every coefficient stays in [-128, 127].
+constexpr int kHaarTok = 8;                 // tokens per CTA
+constexpr int kHaarThreads = kHaarTok * 8 * 8;
+
+template <int M>
+__device__ __forceinline__ void haar_line(int8_t* p, int stride) {
+  int v[M];
+#pragma unroll
+  for (int j = 0; j < M; ++j) v[j] = p[j * stride];
+#pragma unroll
+  for (int j = 0; j < M / 2; ++j) {
+    p[j * stride] = (int8_t)((v[2 * j] + v[2 * j + 1]) >> 1);
+    p[(M / 2 + j) * stride] = (int8_t)((v[2 * j] - v[2 * j + 1]) >> 1);
+  }
+}
+
+template <int M>
+__device__ __forceinline__ void haar_regs(int (&v)[8]) {
+  int t[M];
+#pragma unroll
+  for (int j = 0; j < M / 2; ++j) {
+    t[j] = (v[2 * j] + v[2 * j + 1]) >> 1;
+    t[M / 2 + j] = (v[2 * j] - v[2 * j + 1]) >> 1;
+  }
+#pragma unroll
+  for (int j = 0; j < M; ++j) v[j] = t[j];
+}
+
+// spatial level M over every (frame slot, token, channel) plane of the band
+template <int M>
+__device__ __forceinline__ void haar_spatial(int8_t* sI, int8_t* sP, int tid) {
+  constexpr int kPlanes = 9 * kHaarTok * 3;
+  // horizontal: row r < M of each plane, stride 3 (channel-interleaved)
+  for (int u = tid; u < kPlanes * M; u += kHaarThreads) {
+    const int r = u % M, pl = u / M;
+    const int ch = pl % 3, tok = (pl / 3) % kHaarTok, f = pl / (3 * kHaarTok);
+    int8_t* base = f == 0 ? sI + tok * 256 : sP + tok * 1536 + (f - 1) * 192;
+    haar_line<M>(base + r * 24 + ch, 3);
+  }
+  __syncthreads();
+  for (int u = tid; u < kPlanes * M; u += kHaarThreads) {       // vertical: column c < M
+    const int c = u % M, pl = u / M;
+    const int ch = pl % 3, tok = (pl / 3) % kHaarTok, f = pl / (3 * kHaarTok);
+    int8_t* base = f == 0 ? sI + tok * 256 : sP + tok * 1536 + (f - 1) * 192;
+    haar_line<M>(base + c * 3 + ch, 24);
+  }
+  __syncthreads();
+}
+
+template <int S>
+__global__ void __launch_bounds__(kHaarThreads, 2)
+    k_l8_patchify_haar(const float* __restrict__ src, int H, int W, int h, int w, int Ht, int Wt,
+                       int8_t* __restrict__ pI, int8_t* __restrict__ pP) {
+  __shared__ __align__(16) int8_t sI[kHaarTok * 256];
+  __shared__ __align__(16) int8_t sP[kHaarTok * 1536];
+  const int tid = threadIdx.x;
+  const int lx = tid & 63, py = tid >> 6;          // 64 pixel columns x 8 rows
+  const int tx0 = blockIdx.x * kHaarTok, ty = blockIdx.y, g = blockIdx.z;
+  const int X = tx0 * 8 + lx, Y = ty * 8 + py;
+  const int tok = lx >> 3, pxl = lx & 7;
+  const int xc = min(X, w - 1), yc = min(Y, h - 1);  // np.pad(mode="edge")
+  int q[3][8];                                      // P frames 1..8 per channel
+  int qi[3];
+  const bool live = X < Wt * 8;
+#pragma unroll
+  for (int f = 0; f < 9; ++f) {
+    const float* fr = src + ((int64_t)g * 9 + f) * (int64_t)H * W * 3;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      int val = 0;
+      if (live) {
+        float v;
+        if (S == 1) {
+          v = __ldg(fr + ((int64_t)yc * W + xc) * 3 + ch);
+        } else {
+          double acc = 0.0;
+#pragma unroll
+          for (int j = 0; j < S; ++j) {
+            const int rr = min(yc * S + j, H - 1);
+#pragma unroll
+            for (int l = 0; l < S; ++l) {
+              const int cc = min(xc * S + l, W - 1);
+              acc = acc + (double)__ldg(fr + ((int64_t)rr * W + cc) * 3 + ch);
+            }
+          }
+          v = __double2float_rn(acc / (double)(S * S));
+        }
+        val = (int)rint(__dmul_rn((double)v, 255.0)) - 128;
+      }
+      if (f == 0) qi[ch] = val;
+      else q[ch][f - 1] = val;
+    }
+  }
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {                  // temporal levels 8 -> 4 -> 2
+    haar_regs<8>(q[ch]);
+    haar_regs<4>(q[ch]);
+    haar_regs<2>(q[ch]);
+  }
+  const int po = (py * 8 + pxl) * 3;
+#pragma unroll
+  for (int ch = 0; ch < 3; ++ch) {
+    sI[tok * 256 + po + ch] = (int8_t)qi[ch];
+#pragma unroll
+    for (int f = 0; f < 8; ++f) sP[tok * 1536 + f * 192 + po + ch] = (int8_t)q[ch][f];
+  }
+  if (py == 7 && pxl < 4)                           // channels 192..255 of I are zero
+    reinterpret_cast<uint4*>(sI + tok * 256 + 192)[pxl] = make_uint4(0, 0, 0, 0);
+  __syncthreads();
+  haar_spatial<8>(sI, sP, tid);
+  haar_spatial<4>(sI, sP, tid);
+  haar_spatial<2>(sI, sP, tid);
+  const int ntok = min(kHaarTok, Wt - tx0);
+  const int64_t t0 = (int64_t)(g * Ht + ty) * Wt + tx0;
+  uint4* dI = reinterpret_cast<uint4*>(pI + t0 * 256);
+  uint4* dP = reinterpret_cast<uint4*>(pP + t0 * 1536);
+  const uint4* s4I = reinterpret_cast<const uint4*>(sI);
+  const uint4* s4P = reinterpret_cast<const uint4*>(sP);
+  for (int i = tid; i < ntok * 16; i += kHaarThreads) dI[i] = s4I[i];
+  for (int i = tid; i < ntok * 96; i += kHaarThreads) dP[i] = s4P[i];
+}
+
 // ---- launchers ----------------------------------------------------------------------
 static void fill_args(Args& a, const SstConvDesc* d, int tile_x, int tile_y) {
   memset(&a, 0, sizeof(a));
@@ -1266,6 +1397,28 @@ extern "C" int sst_lt8_patchify(const float* frames, int G, int H, int W, int s,
     case 1: l8::k_l8_patchify<1><<<blocks, threads, 0, st>>>(frames, G, H, W, h, w, Ht, Wt, i, p); break;
     case 2: l8::k_l8_patchify<2><<<blocks, threads, 0, st>>>(frames, G, H, W, h, w, Ht, Wt, i, p); break;
     default: l8::k_l8_patchify<3><<<blocks, threads, 0, st>>>(frames, G, H, W, h, w, Ht, Wt, i, p); break;
+  }
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+extern "C" int sst_lt8_patchify_haar(const float* frames, int G, int H, int W, int s, void* pI,
+                                     void* pP, void* stream) {
+  if (!frames || !pI || !pP || G <= 0 || H <= 0 || W <= 0) return SST_ERR_ARG;
+  if (s < 1 || s > 3) return SST_ERR_ARG;
+  if ((reinterpret_cast<uintptr_t>(pI) & 15u) || (reinterpret_cast<uintptr_t>(pP) & 15u))
+    return SST_ERR_ARG;
+  const int h = ceil_div(H, s), w = ceil_div(W, s);
+  const int Ht = ceil_div(h, 8), Wt = ceil_div(w, 8);
+  if (G > 65535 || Ht > 65535) return SST_ERR_ARG;
+  const dim3 blocks(ceil_div(Wt, l8::kHaarTok), Ht, G);
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  auto* i = static_cast<int8_t*>(pI);
+  auto* p = static_cast<int8_t*>(pP);
+  switch (s) {
+    case 1: l8::k_l8_patchify_haar<1><<<blocks, l8::kHaarThreads, 0, st>>>(frames, H, W, h, w, Ht, Wt, i, p); break;
+    case 2: l8::k_l8_patchify_haar<2><<<blocks, l8::kHaarThreads, 0, st>>>(frames, H, W, h, w, Ht, Wt, i, p); break;
+    default: l8::k_l8_patchify_haar<3><<<blocks, l8::kHaarThreads, 0, st>>>(frames, H, W, h, w, Ht, Wt, i, p); break;
   }
   SST_LAUNCH_CHECK();
   return SST_OK;

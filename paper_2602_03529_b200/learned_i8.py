@@ -43,8 +43,14 @@ class LearnedI8Config:
     # "window": causal attention inside 8x8 token windows (default);
     # "global": every query attends all tokens of the latent frames <= its own
     attn_scope: str = "window"
+    # "patch": quantised pixels straight into the patch embedding (default);
+    # "haar": through the integer 3-D Haar wavelet front end first (Cosmos'
+    # first stage), fused into the same pass over the frames
+    front: str = "patch"
 
     def __post_init__(self):
+        if self.front not in ("patch", "haar"):
+            raise ValueError(f"front must be 'patch' or 'haar', got {self.front!r}")
         if self.attn_scope not in ("window", "global"):
             raise ValueError(f"attn_scope must be 'window' or 'global', got {self.attn_scope!r}")
         if self.dim <= 0 or self.dim % 256:
@@ -107,7 +113,7 @@ def make_weights_i8(cfg: LearnedI8Config) -> dict:
     attn_shift = _shift(HEAD_DIM, 32.0, 32.0, 16.0 * 8.0 / 1.5)
     return {"W": W, "b": b, "sh": sh, "silu": silu_table(), "exp": exp_table(),
             "attn_shift": attn_shift, "head_dim": HEAD_DIM, "blocks": cfg.blocks,
-            "attn": cfg.attn, "attn_scope": cfg.attn_scope, "dim": D}
+            "attn": cfg.attn, "attn_scope": cfg.attn_scope, "front": cfg.front, "dim": D}
 
 
 # ---------------------------------------------------------------------------
@@ -231,8 +237,8 @@ class LearnedTokenizerI8:
         dev = frames.device
         pI = torch.empty((G, 1, Ht, Wt, PATCH_I_PAD), dtype=torch.int8, device=dev)
         pP = torch.empty((G, 1, Ht, Wt, PATCH_P), dtype=torch.int8, device=dev)
-        _lib.call("sst_lt8_patchify", frames.data_ptr(), G, H, Wd, s, pI.data_ptr(),
-                  pP.data_ptr(), _dev.stream())
+        fn = "sst_lt8_patchify_haar" if self.cfg.front == "haar" else "sst_lt8_patchify"
+        _lib.call(fn, frames.data_ptr(), G, H, Wd, s, pI.data_ptr(), pP.data_ptr(), _dev.stream())
         self.launches += 1
         hbuf = torch.empty((G, 2, Ht, Wt, D), dtype=torch.int8, device=dev)
         ubuf = torch.empty_like(hbuf)

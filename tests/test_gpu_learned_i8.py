@@ -405,3 +405,39 @@ def test_global_attention_model_end_to_end():
     win = LearnedTokenizerI8(LearnedI8Config())
     assert not np.array_equal(win.encode_frames(torch.from_numpy(fr).cuda(), 2)[1].cpu().numpy(),
                               idx.cpu().numpy())
+
+
+@pytest.mark.parametrize("H,W,s", [(128, 128, 1), (256, 200, 2), (90, 170, 3), (1080, 1920, 3)])
+def test_patchify_haar_bit_exact(H, W, s):
+    """The integer 3-D Haar front end fused into the patchify pass equals the
+    oracle's haar_front, including partial 8-token bands (W' % 8 != 0)."""
+    rng = np.random.default_rng(21)
+    fr = rng.random((2, 9, H, W, 3)).astype(np.float32)
+    fr[0, :, :5] = 0.0
+    fr[1, :, -3:] = 1.0
+    fr[1, 4:] = fr[1, 3:4]                              # a static tail: temporal highs 0
+    h, w = -(-H // s), -(-W // s)
+    Ht, Wt = -(-h // 8), -(-w // 8)
+    dev = _dev.device()
+    pI = torch.full((2, 1, Ht, Wt, PATCH_I_PAD), 55, dtype=torch.int8, device=dev)
+    pP = torch.full((2, 1, Ht, Wt, PATCH_P), 55, dtype=torch.int8, device=dev)
+    _lib.call("sst_lt8_patchify_haar", torch.from_numpy(fr).to(dev).data_ptr(), 2, H, W, s,
+              pI.data_ptr(), pP.data_ptr(), _dev.stream())
+    torch.cuda.synchronize()
+    oi, op, _ = LO.patchify(fr, s, front="haar")
+    assert np.array_equal(pI.cpu().numpy(), oi) and np.array_equal(pP.cpu().numpy(), op)
+
+
+def test_haar_front_model_end_to_end():
+    clip = make_clip("moving-square", 320, 200, 18, seed=6)
+    fr = np.stack([clip.gop(k) for k in range(2)])
+    model = LearnedTokenizerI8(LearnedI8Config(front="haar"))
+    codes, idx, mask, hw = model.encode_frames(torch.from_numpy(fr).cuda(), 2)
+    oc, oi, _ = LO.encode(fr, 2, model.host_weights)
+    assert np.array_equal(idx.cpu().numpy(), oi)
+    dec = model.decode_tokens(codes, mask, hw).cpu().numpy()
+    assert np.array_equal(dec, LO.decode(oc, np.ones(oc.shape[:-1], np.uint8), hw,
+                                         model.host_weights))
+    plain = LearnedTokenizerI8(LearnedI8Config())
+    assert not np.array_equal(plain.encode_frames(torch.from_numpy(fr).cuda(), 2)[1].cpu().numpy(),
+                              idx.cpu().numpy())

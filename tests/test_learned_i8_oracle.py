@@ -111,3 +111,41 @@ def test_encode_decode_small_deterministic():
     assert np.array_equal(i1, i2) and hw == (48, 64)
     dec = LO.decode(c1, np.ones(c1.shape[:-1], np.uint8), hw, w)
     assert dec.shape == (1, 9, 48, 64, 3) and dec.min() >= 0 and dec.max() <= 1
+
+
+def test_haar_front_loops():
+    """haar_front against a loop restatement: temporal levels over the eight
+    P frames, then spatial levels (rows, then columns) on every frame slot."""
+    def step(v):                                    # one level over a list
+        m = len(v)
+        lo = [(v[2 * j] + v[2 * j + 1]) >> 1 for j in range(m // 2)]
+        hi = [(v[2 * j] - v[2 * j + 1]) >> 1 for j in range(m // 2)]
+        return lo + hi
+
+    rng = np.random.default_rng(5)
+    q = rng.integers(-128, 128, (1, 1, 2, 9, 8, 8, 3))
+    got = LO.haar_front(q)
+    want = q.astype(np.int64).copy()
+    for tx in range(2):
+        for y in range(8):
+            for x in range(8):
+                for c in range(3):
+                    v = [int(want[0, 0, tx, 1 + f, y, x, c]) for f in range(8)]
+                    for m in (8, 4, 2):
+                        v[:m] = step(v[:m])
+                    want[0, 0, tx, 1:, y, x, c] = v
+        for f in range(9):
+            for c in range(3):
+                a = want[0, 0, tx, f, :, :, c].tolist()
+                for m in (8, 4, 2):
+                    for y in range(m):
+                        a[y][:m] = step(a[y][:m])
+                    for x in range(m):
+                        col = step([a[y][x] for y in range(m)])
+                        for y in range(m):
+                            a[y][x] = col[y]
+                want[0, 0, tx, f, :, :, c] = a
+    assert np.array_equal(got, want)
+    assert got.min() >= -128 and got.max() <= 127
+    flat = LO.haar_front(np.full((1, 1, 1, 9, 8, 8, 3), -77))   # flat GoP: DC only
+    assert np.count_nonzero(flat) == 6 and (flat[0, 0, 0, :2, 0, 0] == -77).all()
