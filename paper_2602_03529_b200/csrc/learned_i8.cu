@@ -1155,9 +1155,9 @@ __device__ __forceinline__ void haar_spatial(int8_t* sI, int8_t* sP, int tid) {
   __syncthreads();
 }
 
-template <int S>
+template <int S, bool kHaar>
 __global__ void __launch_bounds__(kHaarThreads, 2)
-    k_l8_patchify_haar(const float* __restrict__ src, int H, int W, int h, int w, int Ht, int Wt,
+    k_l8_patchify_band(const float* __restrict__ src, int H, int W, int h, int w, int Ht, int Wt,
                        int8_t* __restrict__ pI, int8_t* __restrict__ pP) {
   __shared__ __align__(16) int8_t sI[kHaarTok * 256];
   __shared__ __align__(16) int8_t sP[kHaarTok * 1536];
@@ -1199,11 +1199,13 @@ __global__ void __launch_bounds__(kHaarThreads, 2)
       else q[ch][f - 1] = val;
     }
   }
+  if (kHaar) {
 #pragma unroll
-  for (int ch = 0; ch < 3; ++ch) {                  // temporal levels 8 -> 4 -> 2
-    haar_regs<8>(q[ch]);
-    haar_regs<4>(q[ch]);
-    haar_regs<2>(q[ch]);
+    for (int ch = 0; ch < 3; ++ch) {                // temporal levels 8 -> 4 -> 2
+      haar_regs<8>(q[ch]);
+      haar_regs<4>(q[ch]);
+      haar_regs<2>(q[ch]);
+    }
   }
   const int po = (py * 8 + pxl) * 3;
 #pragma unroll
@@ -1215,9 +1217,11 @@ __global__ void __launch_bounds__(kHaarThreads, 2)
   if (py == 7 && pxl < 4)                           // channels 192..255 of I are zero
     reinterpret_cast<uint4*>(sI + tok * 256 + 192)[pxl] = make_uint4(0, 0, 0, 0);
   __syncthreads();
-  haar_spatial<8>(sI, sP, tid);
-  haar_spatial<4>(sI, sP, tid);
-  haar_spatial<2>(sI, sP, tid);
+  if (kHaar) {
+    haar_spatial<8>(sI, sP, tid);
+    haar_spatial<4>(sI, sP, tid);
+    haar_spatial<2>(sI, sP, tid);
+  }
   const int ntok = min(kHaarTok, Wt - tx0);
   const int64_t t0 = (int64_t)(g * Ht + ty) * Wt + tx0;
   uint4* dI = reinterpret_cast<uint4*>(pI + t0 * 256);
@@ -1380,6 +1384,10 @@ extern "C" int sst_lt8_conv(const SstConvDesc* d, void* stream) {
   }
 }
 
+template <bool kHaar>
+static int launch_patchify_band(const float* frames, int G, int H, int W, int s, void* pI, void* pP,
+                                void* stream);
+
 extern "C" int sst_lt8_patchify(const float* frames, int G, int H, int W, int s, void* pI, void* pP,
                                 void* stream) {
   if (!frames || !pI || !pP || G <= 0 || H <= 0 || W <= 0) return SST_ERR_ARG;
@@ -1387,6 +1395,14 @@ extern "C" int sst_lt8_patchify(const float* frames, int G, int H, int W, int s,
   if ((reinterpret_cast<uintptr_t>(pI) & 15u)) return SST_ERR_ARG;
   const int h = ceil_div(H, s), w = ceil_div(W, s);
   const int Ht = ceil_div(h, 8), Wt = ceil_div(w, 8);
+  // s = 1: the band kernel (8-row band staged in shared memory, stored as
+  // 16-byte vectors; the Haar kernel without the transform): 1.72 vs 2.82 ms
+  // per 32 x 1080p GoPs -- the per-pixel kernel's 3-byte stores dominate when
+  // nothing is averaged.  s >= 2: the per-pixel kernel (1.06 vs 1.18 ms at
+  // s = 3).  SST_LT8_PATCHIFY=band|pixel overrides (A/B).
+  const char* mode = getenv("SST_LT8_PATCHIFY");
+  const bool band = mode && mode[0] ? mode[0] == 'b' : s == 1;
+  if (band) return launch_patchify_band<false>(frames, G, H, W, s, pI, pP, stream);
   const int threads = 256;
   if ((int64_t)G * 9 > 65535 || Ht * 8 > 65535) return SST_ERR_ARG;
   const dim3 blocks(ceil_div(Wt * 8, threads), Ht * 8, G * 9);
@@ -1402,8 +1418,9 @@ extern "C" int sst_lt8_patchify(const float* frames, int G, int H, int W, int s,
   return SST_OK;
 }
 
-extern "C" int sst_lt8_patchify_haar(const float* frames, int G, int H, int W, int s, void* pI,
-                                     void* pP, void* stream) {
+template <bool kHaar>
+static int launch_patchify_band(const float* frames, int G, int H, int W, int s, void* pI, void* pP,
+                                void* stream) {
   if (!frames || !pI || !pP || G <= 0 || H <= 0 || W <= 0) return SST_ERR_ARG;
   if (s < 1 || s > 3) return SST_ERR_ARG;
   if ((reinterpret_cast<uintptr_t>(pI) & 15u) || (reinterpret_cast<uintptr_t>(pP) & 15u))
@@ -1415,13 +1432,19 @@ extern "C" int sst_lt8_patchify_haar(const float* frames, int G, int H, int W, i
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   auto* i = static_cast<int8_t*>(pI);
   auto* p = static_cast<int8_t*>(pP);
+  constexpr int T = l8::kHaarThreads;
   switch (s) {
-    case 1: l8::k_l8_patchify_haar<1><<<blocks, l8::kHaarThreads, 0, st>>>(frames, H, W, h, w, Ht, Wt, i, p); break;
-    case 2: l8::k_l8_patchify_haar<2><<<blocks, l8::kHaarThreads, 0, st>>>(frames, H, W, h, w, Ht, Wt, i, p); break;
-    default: l8::k_l8_patchify_haar<3><<<blocks, l8::kHaarThreads, 0, st>>>(frames, H, W, h, w, Ht, Wt, i, p); break;
+    case 1: l8::k_l8_patchify_band<1, kHaar><<<blocks, T, 0, st>>>(frames, H, W, h, w, Ht, Wt, i, p); break;
+    case 2: l8::k_l8_patchify_band<2, kHaar><<<blocks, T, 0, st>>>(frames, H, W, h, w, Ht, Wt, i, p); break;
+    default: l8::k_l8_patchify_band<3, kHaar><<<blocks, T, 0, st>>>(frames, H, W, h, w, Ht, Wt, i, p); break;
   }
   SST_LAUNCH_CHECK();
   return SST_OK;
+}
+
+extern "C" int sst_lt8_patchify_haar(const float* frames, int G, int H, int W, int s, void* pI,
+                                     void* pP, void* stream) {
+  return launch_patchify_band<true>(frames, G, H, W, s, pI, pP, stream);
 }
 
 extern "C" int sst_lt8_attn(const void* qkv, int G, int Ht, int Wt, int D, int shift,

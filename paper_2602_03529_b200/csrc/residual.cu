@@ -625,13 +625,21 @@ __device__ __forceinline__ void cm_init(CumModel& m, int lane) {
   cm_rebuild(m, lane, cnt);
 }
 
+// a[idx] for idx in [0, 16) as a depth-4 select tree (a linear select chain
+// would put 16 dependent SELs on the coder's serial path)
+__device__ __forceinline__ uint32_t sel16(const uint32_t (&a)[16], int idx) {
+  uint32_t b[8], c[4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) b[i] = (idx & 1) ? a[2 * i + 1] : a[2 * i];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c[i] = (idx & 2) ? b[2 * i + 1] : b[2 * i];
+  const uint32_t d0 = (idx & 4) ? c[1] : c[0], d1 = (idx & 4) ? c[3] : c[2];
+  return (idx & 8) ? d1 : d0;
+}
+
 // (cum << 16) | cnt of symbol `sym` on every lane
 __device__ __forceinline__ uint32_t cm_lookup(const CumModel& m, int sym) {
-  const int off = sym & 15;
-  uint32_t v = 0;
-#pragma unroll
-  for (int k = 0; k < 16; ++k) v = (k == off) ? m.pc[k] : v;
-  return __shfl_sync(0xffffffffu, v, sym >> 4);
+  return __shfl_sync(0xffffffffu, sel16(m.pc, sym & 15), sym >> 4);
 }
 
 __device__ __forceinline__ void cm_update(CumModel& m, int lane, int sym) {
@@ -751,29 +759,30 @@ __global__ void __launch_bounds__(kRcThreadsC, 1)
   while (st == 0) {
     const uint32_t total = m.total;
     const uint64_t r = (uint64_t)udiv32((uint32_t)range, total);
+    // the symbol is the last one with cum * r <= min(diff, total r - 1), i.e.
+    // cum <= min(floor(diff / r), total - 1) (rangecoder.py:219-223) -- no
+    // division: every product is <= total r <= range < 2^32, so each lane
+    // compares its 16 cumulative counts in 32-bit arithmetic
     const uint64_t diff = state - low;
-    // floor(diff / r) in float64: the quotient is < 2^16 unless clamped below,
-    // so the correctly rounded double quotient is within 2^-37 of the true
-    // one and r >= 1 keeps any non-integer quotient >= 2^-32 below the next
-    // integer: the floor is exact
-    uint64_t val = (diff >> 32) == 0
-                       ? (uint64_t)floor(__ddiv_rn((double)(uint32_t)diff, (double)(uint32_t)r))
-                       : diff / r;
-    if (val >= total) val = total - 1;
-    // owner = last lane whose first symbol starts at or below val; its count
-    // of symbols starting at or below val gives the offset
-    const uint32_t v32 = (uint32_t)val;              // val < total < 2^16
-    const unsigned bal = __ballot_sync(0xffffffffu, (m.pc[0] >> 16) <= v32);
-    const int owner = 31 - __clz(bal);
-    uint32_t pk = 0, kk = 0;                         // (cum << 16) | cnt, offset
+    const uint32_t tr = total * (uint32_t)r;
+    const uint32_t d32 = diff < (uint64_t)tr ? (uint32_t)diff : tr - 1;
+    const uint32_t r32 = (uint32_t)r;
+    uint32_t le[16];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const bool le = (m.pc[k] >> 16) <= v32;
-      pk = le ? m.pc[k] : pk;
-      kk = le ? (uint32_t)k : kk;
-    }
-    pk = __shfl_sync(0xffffffffu, pk, owner);
-    kk = __shfl_sync(0xffffffffu, kk, owner);
+    for (int k = 0; k < 16; ++k) le[k] = (m.pc[k] >> 16) * r32 <= d32 ? 1u : 0u;
+    // owner = last lane whose first symbol qualifies; cum is non-decreasing,
+    // so the qualifying symbols of a lane are a prefix: offset = count - 1
+    const unsigned bal = __ballot_sync(0xffffffffu, le[0] != 0);
+    const int owner = 31 - __clz(bal);
+    uint32_t s8[8], s4[4];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) s8[i] = le[2 * i] + le[2 * i + 1];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) s4[i] = s8[2 * i] + s8[2 * i + 1];
+    const uint32_t nle = (s4[0] + s4[1]) + (s4[2] + s4[3]);
+    const int kl = nle > 0 ? (int)nle - 1 : 0;
+    const uint32_t pk = __shfl_sync(0xffffffffu, sel16(m.pc, kl), owner);
+    const uint32_t kk = (uint32_t)__shfl_sync(0xffffffffu, kl, owner);
     const int sym = owner * 16 + (int)kk;
     const uint32_t cumv = pk >> 16, cntv = pk & 0xFFFFu;
     low += (uint64_t)cumv * r;

@@ -1,6 +1,7 @@
 """Int8 patchify alone, 32 x 1080p GoPs at s=1 and s=3: plain
 (sst_lt8_patchify) vs the integer 3-D Haar front end (sst_lt8_patchify_haar).
 Both read the f32 frames once (224 MB per GoP) and write the int8 patches."""
+import os
 import sys
 sys.path.insert(0, ".")
 import torch
@@ -13,7 +14,9 @@ for s in (1, 3):
     Ht, Wt = -(-h // 8), -(-w // 8)
     pI = torch.empty((G, Ht, Wt, 256), dtype=torch.int8, device=dev)
     pP = torch.empty((G, Ht, Wt, 1536), dtype=torch.int8, device=dev)
-    for fn in ("sst_lt8_patchify", "sst_lt8_patchify_haar"):
+    for fn, env in (("sst_lt8_patchify", ""), ("sst_lt8_patchify", "band"),
+                    ("sst_lt8_patchify_haar", "")):
+        os.environ["SST_LT8_PATCHIFY"] = env
         def run():
             _lib.call(fn, fr.data_ptr(), G, H, W, s, pI.data_ptr(), pP.data_ptr(), _dev.stream())
         for _ in range(2):
@@ -27,4 +30,4 @@ for s in (1, 3):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / 5
         gb = (fr.numel() * 4 + pI.numel() + pP.numel()) / 1e9
-        print(f"s={s} {fn}: {ms:.3f} ms per launch, {gb / ms:.2f} TB/s")
+        print(f"s={s} {fn} {env}: {ms:.3f} ms per launch, {gb / ms:.2f} TB/s")
