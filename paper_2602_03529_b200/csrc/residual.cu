@@ -18,6 +18,7 @@
 //                   positions of the scan (ballot/popc, index order), then one
 //                   thread codes them with a Fenwick tree for the cumulative
 //                   frequencies (O(log 510) instead of the reference's O(510)).
+#include <climits>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -643,9 +644,15 @@ __device__ __forceinline__ uint32_t cm_lookup(const CumModel& m, int sym) {
 }
 
 __device__ __forceinline__ void cm_update(CumModel& m, int lane, int sym) {
-  const int rel = sym - 16 * lane;                 // symbols above sym gain 1 in cum,
-#pragma unroll                                     // sym itself 1 in cnt
-  for (int k = 0; k < 16; ++k) m.pc[k] += k > rel ? 0x10000u : (k == rel ? 1u : 0u);
+  // symbols above sym gain 1 in cum, sym itself 1 in cnt: one 32-bit mask
+  // holds both (bit k: symbol 16 lane + k is sym; bit 16 + k: it lies above),
+  // so each of the 16 entries costs a shift, an AND and an add
+  const int rc = min(max(sym - 16 * lane, -1), 16);
+  const uint32_t above = (0xFFFFu << (rc + 1)) & 0xFFFFu;
+  const uint32_t mine = (unsigned)rc < 16u ? 1u << rc : 0u;
+  const uint32_t inc = (above << 16) | mine;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) m.pc[k] += (inc >> k) & 0x10001u;
   m.total += 1;
   if (m.total >= (uint32_t)kBottom) {               // rangecoder.py:147-149
     uint32_t cnt[16];
@@ -760,9 +767,10 @@ __global__ void __launch_bounds__(kRcThreadsC, 1)
     const uint32_t total = m.total;
     const uint64_t r = (uint64_t)udiv32((uint32_t)range, total);
     // the symbol is the last one with cum * r <= min(diff, total r - 1), i.e.
-    // cum <= min(floor(diff / r), total - 1) (rangecoder.py:219-223) -- no
+    // cum <= min(floor(diff / r), total - 1) (rangecoder.py:216-221) -- no
     // division: every product is <= total r <= range < 2^32, so each lane
-    // compares its 16 cumulative counts in 32-bit arithmetic
+    // compares its 16 cumulative counts in 32-bit arithmetic (measured faster
+    // than a float quotient estimate plus correction on this serial path)
     const uint64_t diff = state - low;
     const uint32_t tr = total * (uint32_t)r;
     const uint32_t d32 = diff < (uint64_t)tr ? (uint32_t)diff : tr - 1;
@@ -810,6 +818,377 @@ __global__ void __launch_bounds__(kRcThreadsC, 1)
   }
   if (lane == 0) status[g] = st;
 }
+
+// ---- parallel-model encoder (default) -----------------------------------------
+// The ENCODER knows its whole symbol sequence up front, so the adaptive
+// model's state before every symbol -- (cum, cnt) of that symbol and the
+// running total -- is a function of the sequence prefix, computable in
+// parallel; only the range arithmetic itself stays serial.  Five launches:
+//   rcp_scan_summary  per 4096-entry scan chunk: first / last non-zero index
+//                     and the symbols of every non-zero but the chunk's first
+//   rcp_chunk_offsets per stream, over its chunks: the previous non-zero of
+//                     each chunk, each chunk's first symbol index, the count
+//   rcp_symbolize     per chunk: zero-run + value symbols (rangecoder.py:75-94)
+//   rcp_model         per stream: chunks of <= 1024 symbols; per-warp
+//                     histograms, their prefix over warps and over the
+//                     alphabet, and an in-warp rank give every symbol's
+//                     (cum, cnt) = model at chunk start + what precedes it in
+//                     the chunk; a chunk ends exactly where the total reaches
+//                     2^16 so the halving (rangecoder.py:147-149) falls
+//                     between chunks, recorded as a (position, total) event
+//   rcp_code          per stream, one warp: the carry-less coder over the
+//                     precomputed (cum, cnt) words (rangecoder.py:155-184)
+// The scratch layout inside the caller's idx_ws slice of n int64 per stream:
+// symbols u16[n+1] | (cum << 16 | cnt) u32[n+1] | chunk records | events.
+namespace rcp {
+constexpr int kScanChunk = 4096;                  // scan entries per CTA
+constexpr int kScanThreads = 256;                 // 16 entries per thread
+constexpr int kSymChunk = 1024;                   // symbols per model step
+constexpr int kChunkRec = 4;                      // int32 per chunk record
+
+__host__ __device__ __forceinline__ int64_t al16(int64_t x) { return (x + 15) & ~(int64_t)15; }
+__host__ __device__ __forceinline__ int64_t n_chunks(int64_t n) {
+  return (n + kScanChunk - 1) / kScanChunk;
+}
+__host__ __device__ __forceinline__ int64_t max_events(int64_t n) { return (n + 1) / 32768 + 4; }
+// bytes of scratch one stream needs (checked against the 8 n bytes available)
+__host__ __device__ __forceinline__ int64_t ws_bytes(int64_t n) {
+  return al16(2 * (n + 1)) + al16(4 * (n + 1)) + al16(4 * kChunkRec * n_chunks(n)) +
+         8 * (max_events(n) + 1);
+}
+
+struct Ws {
+  uint16_t* sym;
+  uint32_t* par;
+  int32_t* rec;          // per chunk: first, last, internal symbols | prev, offset
+  int32_t* ev;           // [0] = symbol count S, [1] = events, then (pos, total) pairs
+};
+
+__device__ __forceinline__ Ws ws_of(int64_t* idx_ws, int g, int64_t n) {
+  uint8_t* b = reinterpret_cast<uint8_t*>(idx_ws + (int64_t)g * n);
+  Ws w;
+  w.sym = reinterpret_cast<uint16_t*>(b);
+  b += al16(2 * (n + 1));
+  w.par = reinterpret_cast<uint32_t*>(b);
+  b += al16(4 * (n + 1));
+  w.rec = reinterpret_cast<int32_t*>(b);
+  b += al16(4 * kChunkRec * n_chunks(n));
+  w.ev = reinterpret_cast<int32_t*>(b);
+  return w;
+}
+
+__device__ __forceinline__ int nrun(int gap) { return (gap + 254) / 255; }   // ceil(gap / 255)
+
+// block-wide exclusive scans over kScanThreads threads (sum / max)
+template <bool kMax>
+__device__ __forceinline__ int block_excl(int v, int* sh, int& total) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int inc = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int t = __shfl_up_sync(0xffffffffu, inc, o);
+    if (lane >= o) inc = kMax ? max(inc, t) : inc + t;
+  }
+  if (lane == 31) sh[warp] = inc;
+  __syncthreads();
+  if (warp == 0) {
+    int wv = lane < kScanThreads / 32 ? sh[lane] : (kMax ? -1 : 0);
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, wv, o);
+      if (lane >= o) wv = kMax ? max(wv, t) : wv + t;
+    }
+    if (lane < kScanThreads / 32) sh[lane] = wv;            // inclusive warp prefixes
+  }
+  __syncthreads();
+  const int before = warp > 0 ? sh[warp - 1] : (kMax ? -1 : 0);
+  total = sh[kScanThreads / 32 - 1];
+  int ex = __shfl_up_sync(0xffffffffu, inc, 1);
+  if (lane == 0) ex = kMax ? -1 : 0;
+  __syncthreads();                                             // sh reusable
+  return kMax ? max(before, ex) : before + ex;
+}
+
+struct ThreadRun {
+  int first, last, internal;
+};
+
+__device__ __forceinline__ ThreadRun thread_run(const int16_t* scan, int64_t n, int64_t j0) {
+  ThreadRun t{-1, -1, 0};
+#pragma unroll 4
+  for (int i = 0; i < kScanChunk / kScanThreads; ++i) {
+    const int64_t j = j0 + i;
+    if (j < n && scan[j] != 0) {
+      if (t.first < 0) t.first = (int)j;
+      else t.internal += nrun((int)j - t.last - 1) + 1;
+      t.last = (int)j;
+    }
+  }
+  return t;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+    rcp_scan_summary(const int16_t* __restrict__ scans, int64_t n, int64_t* __restrict__ idx_ws) {
+  __shared__ int sh[kScanThreads / 32];
+  const int c = blockIdx.x, g = blockIdx.y;
+  const int16_t* scan = scans + (int64_t)g * n;
+  const int64_t j0 = (int64_t)c * kScanChunk + threadIdx.x * (kScanChunk / kScanThreads);
+  const ThreadRun t = thread_run(scan, n, j0);
+  int chunk_last;
+  const int prev = block_excl<true>(t.last, sh, chunk_last);   // last non-zero of earlier threads
+  int gaps = t.internal + (t.first >= 0 && prev >= 0 ? nrun(t.first - prev - 1) + 1 : 0);
+  int internal;
+  block_excl<false>(gaps, sh, internal);
+  // the chunk's first non-zero: the first thread's with one (smallest index)
+  int first = t.first >= 0 ? t.first : INT_MAX;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) first = min(first, __shfl_xor_sync(0xffffffffu, first, o));
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = first;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < kScanThreads / 32; ++w) first = min(first, sh[w]);
+    int32_t* rec = ws_of(idx_ws, g, n).rec + (int64_t)c * kChunkRec;
+    rec[0] = first == INT_MAX ? -1 : first;
+    rec[1] = chunk_last;
+    rec[2] = internal;
+  }
+}
+
+// one thread per stream: chunk records -> (previous non-zero, first symbol)
+__global__ void rcp_chunk_offsets(int64_t n, int64_t* __restrict__ idx_ws) {
+  const int g = blockIdx.x;
+  const Ws w = ws_of(idx_ws, g, n);
+  const int64_t nc = n_chunks(n);
+  int prev = -1, off = 0;
+  for (int64_t c = 0; c < nc; ++c) {
+    int32_t* rec = w.rec + c * kChunkRec;
+    const int first = rec[0], last = rec[1], internal = rec[2];
+    rec[0] = prev;                                   // becomes: previous non-zero
+    rec[1] = off;                                    //          first symbol index
+    if (first >= 0) {
+      off += nrun(first - prev - 1) + 1 + internal;
+      prev = last;
+    }
+  }
+  w.sym[off] = 0;                                    // EOS
+  w.ev[0] = off + 1;                                 // symbols including EOS
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+    rcp_symbolize(const int16_t* __restrict__ scans, int64_t n, int64_t* __restrict__ idx_ws) {
+  __shared__ int sh[kScanThreads / 32];
+  const int c = blockIdx.x, g = blockIdx.y;
+  const int16_t* scan = scans + (int64_t)g * n;
+  const Ws w = ws_of(idx_ws, g, n);
+  const int32_t* rec = w.rec + (int64_t)c * kChunkRec;
+  const int64_t j0 = (int64_t)c * kScanChunk + threadIdx.x * (kScanChunk / kScanThreads);
+  const ThreadRun t = thread_run(scan, n, j0);
+  int dummy;
+  int prev = block_excl<true>(t.last, sh, dummy);
+  prev = max(prev, rec[0]);
+  const int nsym = t.first >= 0 ? nrun(t.first - prev - 1) + 1 + t.internal : 0;
+  int o = rec[1] + block_excl<false>(nsym, sh, dummy);
+  if (t.first < 0) return;
+  uint16_t* sym = w.sym;
+#pragma unroll 4
+  for (int i = 0; i < kScanChunk / kScanThreads; ++i) {
+    const int64_t j = j0 + i;
+    if (j >= n) break;
+    const int v = scan[j];
+    if (v == 0) continue;
+    int gap = (int)j - prev - 1;                     // rangecoder.py:75-94
+    while (gap > 255) {
+      sym[o++] = 255;
+      gap -= 255;
+    }
+    if (gap) sym[o++] = (uint16_t)gap;
+    sym[o++] = (uint16_t)(v < 0 ? v + 383 : v + 382);
+    prev = (int)j;
+  }
+}
+
+constexpr int kModelThreads = kSymChunk;
+constexpr int kAlphaPad = 512;
+constexpr int kModelSmem = (32 * kAlphaPad + 3 * kAlphaPad + 32) * 4;
+
+__global__ void __launch_bounds__(kModelThreads, 1)
+    rcp_model(int64_t n, int64_t* __restrict__ idx_ws) {
+  extern __shared__ uint32_t sm[];
+  uint32_t* hist = sm;                               // [32 warps][512]
+  uint32_t* cnt = hist + 32 * kAlphaPad;             // model counts at chunk start
+  uint32_t* cum = cnt + kAlphaPad;                   // their exclusive prefix
+  uint32_t* ccnt = cum + kAlphaPad;                  // this chunk's counts
+  uint32_t* red = ccnt + kAlphaPad;                  // 32 scratch words
+  const int g = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Ws w = ws_of(idx_ws, g, n);
+  const int S = w.ev[0];
+  if (tid < kAlphaPad) {
+    cnt[tid] = tid < kAlpha ? 1u : 0u;
+    cum[tid] = min(tid, kAlpha);
+  }
+  uint32_t total = kAlpha;
+  int nev = 0;
+  __syncthreads();
+  for (int base = 0; base < S;) {
+    const int len = min(min(kSymChunk, S - base), (int)(kBottom - total));
+    for (int i = tid; i < 32 * kAlphaPad; i += kModelThreads) hist[i] = 0;
+    __syncthreads();
+    const bool live = tid < len;
+    const int s = live ? w.sym[base + tid] : kAlphaPad - 1;
+    if (live) atomicAdd(&hist[warp * kAlphaPad + s], 1u);
+    __syncthreads();
+    if (tid < kAlphaPad) {                           // exclusive prefix over warps
+      uint32_t run = 0;
+      for (int ww = 0; ww < 32; ++ww) {
+        const uint32_t h = hist[ww * kAlphaPad + tid];
+        hist[ww * kAlphaPad + tid] = run;
+        run += h;
+      }
+      ccnt[tid] = run;
+    }
+    __syncthreads();
+    // counts of s in earlier warps, then this warp's row as a prefix over the
+    // alphabet: symbols below s in earlier warps
+    uint32_t* row = hist + warp * kAlphaPad;
+    const uint32_t eq_w = row[s];
+    __syncwarp();
+    uint32_t loc[16], acc = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      loc[k] = acc;
+      acc += row[lane * 16 + k];
+    }
+    uint32_t inc = acc;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += t;
+    }
+    const uint32_t lbase = inc - acc;
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) row[lane * 16 + k] = lbase + loc[k];
+    __syncwarp();
+    const uint32_t lt_w = row[s];
+    uint32_t lt = 0, eq = 0;                         // earlier lanes of this warp
+#pragma unroll 8
+    for (int j = 0; j < 32; ++j) {
+      const int v = __shfl_sync(0xffffffffu, s, j);
+      if (j < lane) {
+        lt += v < s;
+        eq += v == s;
+      }
+    }
+    if (live) w.par[base + tid] = ((cum[s] + lt_w + lt) << 16) | (cnt[s] + eq_w + eq);
+    __syncthreads();
+    total += (uint32_t)len;
+    const bool halve = total >= (uint32_t)kBottom;
+    if (tid < kAlphaPad) {
+      uint32_t c2 = cnt[tid] + ccnt[tid];
+      if (halve) c2 = (c2 + 1) >> 1;                 // rangecoder.py:147-149
+      cnt[tid] = c2;
+    }
+    __syncthreads();
+    if (tid < kAlphaPad) {                           // exclusive prefix of cnt
+      const uint32_t v = cnt[tid];
+      uint32_t x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += t;
+      }
+      if (lane == 31) red[warp] = x;
+      cum[tid] = x - v;                              // within-warp exclusive
+    }
+    __syncthreads();
+    if (tid < kAlphaPad) {
+      uint32_t before = 0;
+      for (int ww = 0; ww < warp; ++ww) before += red[ww];
+      cum[tid] += before;
+    }
+    if (halve) {
+      uint32_t t2 = 0;
+      for (int ww = 0; ww < kAlphaPad / 32; ++ww) t2 += red[ww];
+      total = t2;
+      if (tid == 0) {
+        w.ev[2 + 2 * nev] = base + len;
+        w.ev[3 + 2 * nev] = (int32_t)t2;
+      }
+      ++nev;
+    }
+    base += len;
+    __syncthreads();
+  }
+  if (tid == 0) w.ev[1] = nev;
+}
+
+__global__ void __launch_bounds__(32)
+    rcp_code(int64_t n, const int64_t* __restrict__ idx_ws_c, uint8_t* __restrict__ out, int64_t cap,
+             int64_t* __restrict__ out_len) {
+  const int g = blockIdx.x, lane = threadIdx.x;
+  const Ws w = ws_of(const_cast<int64_t*>(idx_ws_c), g, n);
+  const int S = w.ev[0], nev = w.ev[1];
+  uint8_t* o = out + (int64_t)g * cap;
+  int ev = 0;
+  int ev_pos = nev > 0 ? w.ev[2] : INT_MAX;
+  uint32_t tb = kAlpha;                              // total before symbol `base`
+  uint32_t low = 0, range = 0xFFFFFFFFu;
+  int64_t pos = 0;
+  for (int base = 0; base < S; base += 32) {
+    if (base == ev_pos) {                            // the model was halved here
+      tb = (uint32_t)w.ev[3 + 2 * ev];
+      ++ev;
+      ev_pos = ev < nev ? w.ev[2 + 2 * ev] : INT_MAX;
+    }
+    // per lane, off the serial path: its symbol's (cum, cnt), the total it
+    // is coded against (a halving inside the batch restarts the count) and
+    // floor(2^32 / total), so the coder's range / total is one multiply-high
+    // plus one correction (the estimate is exact or one short)
+    const int i = base + lane;
+    const uint32_t cc = i < S ? __ldcs(w.par + i) : 0u;
+    const bool after = ev_pos < base + 32 && i >= ev_pos;
+    const uint32_t ti = after ? (uint32_t)w.ev[3 + 2 * ev] + (uint32_t)(i - ev_pos) : tb + lane;
+    const uint32_t mi = (uint32_t)(0x100000000ull / ti);
+    const int nb = min(32, S - base);
+    uint32_t c_t = __shfl_sync(0xffffffffu, cc, 0), m_t = __shfl_sync(0xffffffffu, mi, 0);
+    uint32_t t_t = __shfl_sync(0xffffffffu, ti, 0);
+    for (int t = 0; t < nb; ++t) {
+      const int tn = t + 1 < 32 ? t + 1 : 31;        // next symbol's words, in flight
+      const uint32_t c_n = __shfl_sync(0xffffffffu, cc, tn);
+      const uint32_t m_n = __shfl_sync(0xffffffffu, mi, tn);
+      const uint32_t t_n = __shfl_sync(0xffffffffu, ti, tn);
+      uint32_t r = __umulhi(range, m_t);
+      if (range - r * t_t >= t_t) ++r;
+      low += (c_t >> 16) * r;                        // < 2^32 + range: carry-less
+      range = (c_t & 0xFFFFu) * r;
+      // renormalise (rangecoder.py:167-176) on the 33-bit low + range
+      while (((uint64_t)low ^ ((uint64_t)low + range)) < kTop || range < kBottom) {
+        if (((uint64_t)low ^ ((uint64_t)low + range)) >= kTop) range = (0u - low) & (uint32_t)(kBottom - 1);
+        if (lane == 0 && pos < cap) o[pos] = (uint8_t)(low >> 24);
+        ++pos;
+        low <<= 8;
+        range <<= 8;
+      }
+      c_t = c_n;
+      m_t = m_n;
+      t_t = t_n;
+    }
+    if (ev_pos < base + 32 && ev_pos > base) {       // consumed inside this batch
+      tb = (uint32_t)w.ev[3 + 2 * ev] + (uint32_t)(base + 32 - ev_pos);
+      ++ev;
+      ev_pos = ev < nev ? w.ev[2 + 2 * ev] : INT_MAX;
+    } else {
+      tb += 32;
+    }
+  }
+  for (int k = 0; k < 4; ++k) {                      // rangecoder.py:182-184
+    if (lane == 0 && pos < cap) o[pos] = (uint8_t)(low >> 24);
+    ++pos;
+    low <<= 8;
+  }
+  if (lane == 0) out_len[g] = pos > cap ? -pos : pos;
+}
+}  // namespace rcp
 
 // encode_stream for explicit symbol lists (one CTA / thread per stream)
 __global__ void k_rc_encode_symbols(const int32_t* __restrict__ syms, const int64_t* __restrict__ off,
@@ -971,16 +1350,35 @@ extern "C" int sst_rc_encode(const int16_t* scans, int G, int64_t n, int64_t* id
   if (G < 0 || n < 0 || cap < 0) return SST_ERR_ARG;
   if (G == 0) return SST_OK;
   if ((n > 0 && (!scans || !idx_ws)) || !out || !out_len) return SST_ERR_ARG;
-  // default: the cumulative-table warp coder; A/B: SST_RC=fenwick (single
-  // thread, Fenwick tree) or SST_RC=warp (warp-reduced counts)
+  // default: the parallel-model encoder (rcp::); A/B: SST_RC=cum (the
+  // one-warp cumulative-table coder), SST_RC=fenwick (single thread, Fenwick
+  // tree) or SST_RC=warp (warp-reduced counts)
   const char* mode = getenv("SST_RC");
   auto st = static_cast<cudaStream_t>(stream);
-  if (mode && mode[0] == 'f')
+  // the parallel-model encoder needs its scratch inside the 8 n bytes per
+  // stream and int32 positions; small scans take the one-launch warp coder
+  const bool par = n >= rcp::kScanChunk && n < ((int64_t)1 << 30) &&
+                   rcp::ws_bytes(n) <= 8 * n && G <= 65535;
+  if (mode && mode[0] == 'f') {
     k_rc_encode<<<G, kRcThreads, 0, st>>>(scans, n, idx_ws, out, cap, out_len);
-  else if (mode && mode[0] == 'w')
+  } else if (mode && mode[0] == 'w') {
     k_rc_encode_w<<<G, kRcThreads, 0, st>>>(scans, n, idx_ws, out, cap, out_len);
-  else
+  } else if ((mode && mode[0] == 'c') || !par) {
     k_rc_encode_c<<<G, kRcThreadsC, 0, st>>>(scans, n, idx_ws, out, cap, out_len);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      SST_CUDA_TRY(cudaFuncSetAttribute(rcp::rcp_model, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          rcp::kModelSmem));
+      attr = true;
+    }
+    const dim3 chunks((unsigned)rcp::n_chunks(n), G);
+    rcp::rcp_scan_summary<<<chunks, rcp::kScanThreads, 0, st>>>(scans, n, idx_ws);
+    rcp::rcp_chunk_offsets<<<G, 1, 0, st>>>(n, idx_ws);
+    rcp::rcp_symbolize<<<chunks, rcp::kScanThreads, 0, st>>>(scans, n, idx_ws);
+    rcp::rcp_model<<<G, rcp::kModelThreads, rcp::kModelSmem, st>>>(n, idx_ws);
+    rcp::rcp_code<<<G, 32, 0, st>>>(n, idx_ws, out, cap, out_len);
+  }
   SST_LAUNCH_CHECK();
   return SST_OK;
 }

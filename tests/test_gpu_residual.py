@@ -84,6 +84,29 @@ def test_dense_noisy_scan_matches_oracle(rng):
     assert np.array_equal(RC.decode_scan(pay, n), d)
 
 
+def test_parallel_encoder_chunk_edges(rng):
+    """The parallel-model encoder (4096-entry scan chunks, <= 1024-symbol model
+    steps, halving events between steps) on scans built to hit its seams:
+    non-zeros on and either side of chunk boundaries, zero runs spanning whole
+    chunks (runs of 255-symbols), an all-zero scan (EOS only), one non-zero
+    at the very end, and a dense scan long enough to halve the model."""
+    n = 3 * 4096 + 777
+    scans = [np.zeros(n, np.int16) for _ in range(6)]
+    for j in (0, 4095, 4096, 4097, 8191, 8192, n - 1):
+        scans[0][j] = (-1) ** j * (1 + j % 127)
+    scans[1][[5, 9000, n - 2]] = [7, -3, 127]            # runs across chunks
+    scans[3][n - 1] = -127
+    scans[4][:] = np.where(rng.random(n) < 0.9, rng.integers(-127, 128, n), 0)
+    scans[5][::256] = 1                                 # gaps of exactly 255
+    pays = RC.encode_scans(scans)
+    assert pays == [R.encode_scan(s) for s in scans]
+    for a, b in zip(RC.decode_scans(pays, n), scans):
+        assert np.array_equal(a, b)
+    big = np.where(rng.random(300_000) < 0.45, rng.integers(-127, 128, 300_000), 0)
+    big = big.astype(np.int16)                          # ~270k symbols: 7+ halvings
+    assert RC.encode_scan(big) == R.encode_scan(big)
+
+
 # ---------------------------------------------------------------------------
 # pkg/tests/test_rangecoder.py
 
