@@ -1101,8 +1101,10 @@ def residual_leg(a, device) -> dict:
             "entries_per_gop": round(float(count.float().mean()), 1),
             "payload_bytes_per_gop": round(float(plen.float().mean()), 1),
             "roundtrip_exact": bool(torch.equal(dec, dense)) and bool((status == 0).all()),
-            "range_coder": "one warp per stream, cumulative-table adaptive model (csrc/residual.cu "
-                           "k_rc_encode_c / k_rc_decode_c), bytes identical to the reference"}
+            "range_coder": "encoder: symbols and the adaptive model's per-symbol state computed "
+                           "in parallel, one warp per stream codes them (csrc/residual.cu rcp::); "
+                           "decoder: one warp per stream, cumulative-table model "
+                           "(k_rc_decode_c); bytes identical to the reference"}
 
 
 # ---------------------------------------------------------------------------
