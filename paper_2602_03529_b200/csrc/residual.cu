@@ -729,6 +729,7 @@ __global__ void __launch_bounds__(kRcThreadsC, 1)
   if (lane == 0) out_len[g] = e.pos > cap ? -e.pos : e.pos;
 }
 
+template <bool kFloatQ>
 __global__ void __launch_bounds__(kRcThreadsC, 1)
     k_rc_decode_c(const uint8_t* __restrict__ data, const int64_t* __restrict__ off,
                   const int64_t* __restrict__ len, int64_t n, int16_t* __restrict__ scans,
@@ -776,8 +777,20 @@ __global__ void __launch_bounds__(kRcThreadsC, 1)
     const uint32_t d32 = diff < (uint64_t)tr ? (uint32_t)diff : tr - 1;
     const uint32_t r32 = (uint32_t)r;
     uint32_t le[16];
+    if (kFloatQ) {
+      // A/B: val = floor(d32 / r) from an approximate float quotient (< 2^16,
+      // error < 0.05) corrected once, then 16 packed compares
+      uint32_t val = __float2uint_rz(__fdividef(__uint2float_rn(d32), __uint2float_rn(r32)));
+      const uint32_t vr = val * r32;
+      if (vr > d32) val -= 1;
+      else if (d32 - vr >= r32) val += 1;
+      const uint32_t vk = (val << 16) | 0xFFFFu;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) le[k] = (m.pc[k] >> 16) * r32 <= d32 ? 1u : 0u;
+      for (int k = 0; k < 16; ++k) le[k] = m.pc[k] <= vk ? 1u : 0u;
+    } else {
+#pragma unroll
+      for (int k = 0; k < 16; ++k) le[k] = (m.pc[k] >> 16) * r32 <= d32 ? 1u : 0u;
+    }
     // owner = last lane whose first symbol qualifies; cum is non-decreasing,
     // so the qualifying symbols of a lane are a prefix: offset = count - 1
     const unsigned bal = __ballot_sync(0xffffffffu, le[0] != 0);
@@ -1394,8 +1407,10 @@ extern "C" int sst_rc_decode(const uint8_t* data, const int64_t* off, const int6
     k_rc_decode<<<G, kRcThreads, 0, st>>>(data, off, len, n, scans, status);
   else if (mode && mode[0] == 'w')
     k_rc_decode_w<<<G, kRcThreads, 0, st>>>(data, off, len, n, scans, status);
+  else if (mode && mode[0] == 'q')
+    k_rc_decode_c<true><<<G, kRcThreadsC, 0, st>>>(data, off, len, n, scans, status);
   else
-    k_rc_decode_c<<<G, kRcThreadsC, 0, st>>>(data, off, len, n, scans, status);
+    k_rc_decode_c<false><<<G, kRcThreadsC, 0, st>>>(data, off, len, n, scans, status);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }
