@@ -1119,11 +1119,15 @@ def measured_bf16_peak():
 
 
 def measured_i8_peak(device) -> tuple:
-    """Dense int8 tensor peak measured in this run: cuBLASLt int8 GEMM
-    (torch._int_mm, 8192^3, int32 out), best of 10 after warm-up -- the int8
-    counterpart of MEASURED_PEAKS.json's bf16_tflops (which has no int8
-    entry).  Falls back to 2 x the measured bf16 peak."""
+    """The int8 tensor roofline denominator: 2 x MEASURED_PEAKS.json's
+    measured bf16 burst (B200's dense int8 rate is twice bf16, like fp8:
+    B200_PROFILING.md's table) -- MEASURED_PEAKS.json has no int8 entry.
+    Returned with it, as context: the cuBLASLt int8 GEMM measured in this
+    run (torch._int_mm, 8192^3, int32 out, best of 10), which reaches a
+    smaller fraction of nominal than cuBLAS bf16 does."""
     import torch
+    bf, bsrc = measured_bf16_peak()
+    lt = None
     try:
         n = 8192
         x = torch.randint(-127, 128, (n, n), dtype=torch.int8, device=device)
@@ -1140,10 +1144,10 @@ def measured_i8_peak(device) -> tuple:
             ms = e0.elapsed_time(e1)
             best = ms if best is None else min(best, ms)
         del x, y
-        return 2 * n ** 3 / (best / 1e3) / 1e12, "measured in-run (cuBLASLt int8 GEMM 8192^3, burst)"
-    except Exception as e:            # pragma: no cover
-        bf, _ = measured_bf16_peak()
-        return 2 * bf, f"2 x measured bf16 peak (int8 GEMM probe failed: {type(e).__name__})"
+        lt = round(2 * n ** 3 / (best / 1e3) / 1e12, 1)
+    except Exception:                 # pragma: no cover
+        pass
+    return 2 * bf, f"2 x {bsrc} (B200 dense int8 = 2 x bf16)", lt
 
 
 def learned_e2e(a, device, model, Codec, s: int) -> dict:
@@ -1311,7 +1315,7 @@ def run_learned(a, device, precision: str = "i8") -> dict:
     halo = [(ms_, fl) for n, nt, ms_, fl in per if nt == 18 and model.W[n].shape[0] % 256 == 0]
     conv_ms = sum(ms_ for _, _, ms_, _ in per)
     if precision == "i8":
-        peak, src = measured_i8_peak(device)
+        peak, src, cublaslt_i8 = measured_i8_peak(device)
         unit, dtype = "TOP/s", "int8 operands, int32 accumulate (TMEM), exact"
         kern = "k_l8_pair<true> (causal (2,3,3) conv, CTA-pair tcgen05 kind::i8 implicit GEMM)"
     else:
@@ -1344,6 +1348,7 @@ def run_learned(a, device, precision: str = "i8") -> dict:
         "e2e": e2e,
     }
     if precision == "i8":
+        res["roofline"]["cublaslt_i8_gemm_tops"] = cublaslt_i8
         ops = model.ops_per_gop(codec.Ht, codec.Wt) * G
         res["tensor_tops_path"] = round(ops / ms / 1e9, 1)
         # parity at the bench's own size: one 1080p GoP, GPU vs the exact oracle

@@ -13,6 +13,8 @@
 #include <cstdlib>
 #include <cstring>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "tma.cuh"
 
@@ -1231,6 +1233,26 @@ extern "C" int sst_upscale_blend9_u8(const uint8_t* img, int G, int h, int w, in
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   CUtensorMap imap;
   memset(&imap, 0, sizeof(imap));
+  // Output rows per CTA (SST_K59_U8_BAND=16|24|32|48|64 for A/B): byte
+  // windows are small enough for 64-row bands, which amortise the per-CTA
+  // setup (axis taps, window loads, LUT) over 4x the rows of the float
+  // kernel's 16.  Measured (scripts/k5_9u8_micro.py, 32 x 1080p GoPs, s=3,
+  // without / with blend n=2): 16 rows 1.500 / 1.696 ms, 32 rows 1.275 /
+  // 1.490, 48 rows 1.240 / 1.452, 64 rows 1.257 / 1.416 (s=2: 1.903 / 2.091
+  // -> 1.545 / 1.812).
+  const char* bs = getenv("SST_K59_U8_BAND");
+  const int band = bs ? atoi(bs) : 64;
+  auto go = [&](auto tag) -> int {
+    constexpr int B = decltype(tag)::value;
+    const bool t = make_tmap_u8_3d(&imap, img, (uint64_t)w * 3, (uint64_t)h, (uint64_t)G * kGop,
+                                   kWF9u8, Up9fGeom<B, uint8_t>::kWR);
+    return t ? launch_k5_9f<B, 2, uint8_t>(imap, a, prev, blend_n, st)
+             : launch_k5_9f<B, 0, uint8_t>(imap, a, prev, blend_n, st);
+  };
+  if (band == 24) return go(std::integral_constant<int, 24>{});
+  if (band == 32) return go(std::integral_constant<int, 32>{});
+  if (band == 48) return go(std::integral_constant<int, 48>{});
+  if (band == 64) return go(std::integral_constant<int, 64>{});
   const bool tma_in = make_tmap_u8_3d(&imap, img, (uint64_t)w * 3, (uint64_t)h, (uint64_t)G * kGop,
                                       kWF9u8, Up9fGeom<16, uint8_t>::kWR);
   if (tma_in) return launch_k5_9f<16, 2, uint8_t>(imap, a, prev, blend_n, st);

@@ -34,4 +34,6 @@ CS=/usr/local/cuda/bin/compute-sanitizer
 timeout -s KILL 900 $CS --tool memcheck --error-exitcode 9 --print-limit 20 python -m pytest tests/test_gpu_learned_i8.py -q -x -k "not 1080 and not 720 and not gop_codec" > gpurun_out/${TAG}_san_i8.log 2>&1; echo "memcheck i8 rc=$?"
 timeout -s KILL 900 $CS --tool racecheck --error-exitcode 9 --print-limit 20 python -m pytest tests/test_gpu_learned_i8.py -q -x -k "attention_core and 13" > gpurun_out/${TAG}_san_race_i8.log 2>&1; echo "racecheck i8 attn rc=$?"
 timeout -s KILL 900 $CS --tool memcheck --error-exitcode 9 --print-limit 20 python -m pytest tests/test_gpu_residual.py tests/test_gpu_metrics.py -q -x -k "not 1080" > gpurun_out/${TAG}_san_rc.log 2>&1; echo "memcheck rc/metrics rc=$?"
+timeout -s KILL 900 $CS --tool racecheck --error-exitcode 9 --print-limit 20 python -m pytest tests/test_gpu_residual.py -q -x -k "batched_coding" > gpurun_out/${TAG}_san_race_rc.log 2>&1; echo "racecheck rc encoder rc=$?"
+timeout -s KILL 900 $CS --tool racecheck --error-exitcode 9 --print-limit 20 python -m pytest tests/test_gpu_learned_i8.py -q -x -k "patchify_haar and 128" > gpurun_out/${TAG}_san_race_haar.log 2>&1; echo "racecheck haar rc=$?"
 ls gpurun_out | grep "^${TAG}" | head -50
