@@ -71,12 +71,54 @@ __device__ __forceinline__ uint32_t pack4(int a, int b, int c, int d) {
          ((uint32_t)(d & 0xFF) << 24);
 }
 
+// bytes (a, b, c, d) = sat_s8(a .. d), a lowest: two cvt.pack.sat (I2IP), the
+// saturation doing the upper clamp of a requantisation for free
+__device__ __forceinline__ uint32_t pack4_sat(int a, int b, int c, int d) {
+  uint32_t hi, r;
+  asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(d), "r"(c));
+  asm("cvt.pack.sat.s8.s32.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(a), "r"(hi));
+  return r;
+}
+
+// bytes = sat_u8 of four int32 (clamp to [0, 255] in the pack)
+__device__ __forceinline__ uint32_t pack4_satu8(int a, int b, int c, int d) {
+  uint32_t hi, r;
+  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, 0;" : "=r"(hi) : "r"(d), "r"(c));
+  asm("cvt.pack.sat.u8.s32.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(b), "r"(a), "r"(hi));
+  return r;
+}
+
+// requantise without the upper clamp (pack4_sat saturates at 127)
+__device__ __forceinline__ int rq_lo(int32_t acc, int32_t b_rnd, int sh) {
+  return max((acc + b_rnd) >> sh, -127);
+}
+
 // STORE epilogue of 32 accumulator columns (n0 .. n0+31): requantise, SiLU
 // table, saturating residual add; 32 int8 results packed into o[0..1].
 __device__ __forceinline__ void epi_store32(const float (&acc)[32], const Args& a, int n0,
                                             const uint4* res, uint4 (&o)[2]) {
   int y[32];
   const int4* bp = reinterpret_cast<const int4*>(a.bias + n0);
+  if (!a.act && res == nullptr) {
+    // plain requantisation: add, shift, lower clamp; the upper clamp is the
+    // pack's saturation
+    const int rnd = 1 << (a.shift - 1);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      uint32_t wd[4];
+#pragma unroll
+      for (int i4 = 0; i4 < 4; ++i4) {
+        const int4 bb = __ldg(bp + q * 4 + i4);
+        const int j = q * 16 + 4 * i4;
+        wd[i4] = pack4_sat(rq_lo(__float_as_int(acc[j + 0]), bb.x + rnd, a.shift),
+                           rq_lo(__float_as_int(acc[j + 1]), bb.y + rnd, a.shift),
+                           rq_lo(__float_as_int(acc[j + 2]), bb.z + rnd, a.shift),
+                           rq_lo(__float_as_int(acc[j + 3]), bb.w + rnd, a.shift));
+      }
+      o[q] = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+    }
+    return;
+  }
 #pragma unroll
   for (int i4 = 0; i4 < 8; ++i4) {
     const int4 bb = __ldg(bp + i4);
@@ -105,11 +147,11 @@ __device__ __forceinline__ void epi_store32(const float (&acc)[32], const Args& 
     }
   }
 #pragma unroll
-  for (int q = 0; q < 2; ++q)
-    o[q] = make_uint4(pack4(y[q * 16 + 0], y[q * 16 + 1], y[q * 16 + 2], y[q * 16 + 3]),
-                      pack4(y[q * 16 + 4], y[q * 16 + 5], y[q * 16 + 6], y[q * 16 + 7]),
-                      pack4(y[q * 16 + 8], y[q * 16 + 9], y[q * 16 + 10], y[q * 16 + 11]),
-                      pack4(y[q * 16 + 12], y[q * 16 + 13], y[q * 16 + 14], y[q * 16 + 15]));
+  for (int q = 0; q < 2; ++q)   // values in [-127, 127]: the saturating pack is exact
+    o[q] = make_uint4(pack4_sat(y[q * 16 + 0], y[q * 16 + 1], y[q * 16 + 2], y[q * 16 + 3]),
+                      pack4_sat(y[q * 16 + 4], y[q * 16 + 5], y[q * 16 + 6], y[q * 16 + 7]),
+                      pack4_sat(y[q * 16 + 8], y[q * 16 + 9], y[q * 16 + 10], y[q * 16 + 11]),
+                      pack4_sat(y[q * 16 + 12], y[q * 16 + 13], y[q * 16 + 14], y[q * 16 + 15]));
 }
 
 __device__ __forceinline__ float pixel(int32_t acc, int32_t b, int sh) {
@@ -527,9 +569,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::THREADS, 1)
         if (a.pix_u8) {
           // uint8 q frames (sample value float(q / 255)): a quarter of the bytes
           // q in place of the accumulator bits (no second 96-register array)
-          auto qf = [&](int acc, int b) {
-            return __int_as_float(min(max((acc + b + (1 << (a.shift - 1))) >> a.shift, 0), 255));
-          };
+          // the [0, 255] clamp happens in the saturating u8 pack below
+          const int rnd = 1 << (a.shift - 1);
+          auto qf = [&](int acc, int b) { return __int_as_float((acc + b + rnd) >> a.shift); };
 #pragma unroll
           for (int i4 = 0; i4 < 24; ++i4) {
             const int4 bb = __ldg(bp4 + i4);
@@ -548,8 +590,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::THREADS, 1)
               uint32_t* s32 = reinterpret_cast<uint32_t*>(srow + (lane >> 3) * 192 + (lane & 7) * 24);
 #pragma unroll
               for (int e = 0; e < 6; ++e)
-                s32[e] = pack4(qv(pr * 24 + 4 * e), qv(pr * 24 + 4 * e + 1), qv(pr * 24 + 4 * e + 2),
-                               qv(pr * 24 + 4 * e + 3));
+                s32[e] = pack4_satu8(qv(pr * 24 + 4 * e), qv(pr * 24 + 4 * e + 1),
+                                     qv(pr * 24 + 4 * e + 2), qv(pr * 24 + 4 * e + 3));
               __syncwarp();
               for (int i = lane; i < 48; i += 32) {
                 const int r = i / 12, c16 = i - r * 12;
@@ -573,7 +615,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::THREADS, 1)
             const int npx = min(8, a.w - X0);
 #pragma unroll
             for (int e = 0; e < 24; ++e)
-              if (e / 3 < npx) dst[e] = (uint8_t)qv(pr * 24 + e);
+              if (e / 3 < npx) dst[e] = (uint8_t)min(max(qv(pr * 24 + e), 0), 255);
           }
 #undef qv
           continue;
