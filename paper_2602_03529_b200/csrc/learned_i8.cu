@@ -370,8 +370,15 @@ namespace pc {
 constexpr int TILE = 16, PITCH = 10, HROWS = 18;
 constexpr int HALO_BYTES = PITCH * HROWS * 128;                   // 23040 (1x1: 8x16 box, 16384)
 constexpr int HALO_STRIDE = (HALO_BYTES + 1023) / 1024 * 1024;    // 23552
-constexpr int EPI_WARPS = 8;
-constexpr int THREADS = 64 + EPI_WARPS * 32;
+// Epilogue warps per CTA: 8 (two per TMEM lane quarter) for the convs and
+// the short-K GEMMs; 16 for the pixel layer, whose epilogue (requantise,
+// pack, stage, scatter into frame rows) bounds it -- measured 200 -> 147 us
+// for the P frames of 32 x 1080p GoPs, while the TMA-store GEMMs got slower
+// with 16 (named-barrier halves of 8 warps)
+template <bool kPix>
+__host__ __device__ constexpr int epi_warps() { return kPix ? 16 : 8; }
+template <bool kPix>
+__host__ __device__ constexpr int pair_threads() { return 64 + 32 * epi_warps<kPix>(); }
 }  // namespace pc
 
 template <bool kHalo, bool kTma>
@@ -384,7 +391,9 @@ template <bool kPix>
 __host__ __device__ constexpr int pair_bbytes() { return (kPix ? 96 : 128) * 128; }
 // TMA-store staging: [2 halves][128 rows][128 B]; pixel rows: 8 warps x 768 floats
 template <bool kTma, bool kPix>
-__host__ __device__ constexpr int pair_stage() { return kTma ? 2 * 16384 : (kPix ? 8 * 3072 : 0); }
+__host__ __device__ constexpr int pair_stage() {
+  return kTma ? 2 * 16384 : (kPix ? pc::epi_warps<true>() * 3072 : 0);
+}
 template <bool kHalo, bool kTma, bool kPix = false>
 __host__ __device__ constexpr int pair_smem() {
   return pair_hslots<kHalo>() * pair_hstride<kHalo>() + pair_bstages<kHalo, kTma>() * pair_bbytes<kPix>() +
@@ -409,10 +418,11 @@ __device__ __forceinline__ void named_bar(int id, int n) {
 }
 
 template <bool kHalo, bool kTma, bool kPix = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::pair_threads<kPix>(), 1)
     k_l8_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
               const __grid_constant__ CUtensorMap tmC, const Args a, int n_units, int n_blocks) {
   using namespace pc;
+  constexpr int EPI_WARPS = epi_warps<kPix>();
   constexpr int kPitch = kHalo ? PITCH : 8;
   constexpr int kBoxBytes = kHalo ? HALO_BYTES : 8 * 16 * 128;
   constexpr int kSpatial = kHalo ? 9 : 1;
@@ -534,12 +544,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::THREADS, 1)
       }
     }
   } else {
-    // ---- epilogue (both CTAs): warp w drains columns kNU/2*((w-2)/4).., lanes 32*(w%4) ----
+    // ---- epilogue (both CTAs): EPI_WARPS warps; warp w reads TMEM lanes
+    // 32 (w % 4) .. +31 (its token rows) and column group cq = (w - 2) / 4 of
+    // NCQ: 256 / NCQ columns of a 256-wide unit, or pixel rows 8 / NCQ .. of
+    // a 192-wide pixel unit.  Column groups 0 .. NCQ/2 - 1 form TMA-store half 0.
+    constexpr int NCQ = EPI_WARPS / 4;
+    constexpr int HALF_WARPS = EPI_WARPS / 2;
     const int e = warp - 2;
-    const int half = e >> 2, q = warp & 3;
+    const int cq = e >> 2, q = warp & 3;
+    const int half = e / HALF_WARPS;
     const int m = q * 32 + lane;
     const uint32_t aempty_leader = tc::mapa(smem_u32(&aempty[0]), 0);
-    const bool issuer = kTma && (e & 3) == 0 && lane == 0;     // first warp of each half
+    const bool issuer = kTma && (e % HALF_WARPS) == 0 && lane == 0;   // first warp of each half
     int it = 0;
     for (int u = pair; u < n_units; u += npairs, ++it) {
       int g, t, x0, y0, nb;
@@ -550,30 +566,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::THREADS, 1)
       const int y = y0 + (m >> 3), x = x0 + 8 * (int)rank + (m & 7);
       const bool valid = y < a.Ht && x < a.Wt;
       if (kPix) {
-        const uint32_t trp = tmem + ((uint32_t)(q * 32) << 16) + ab * 256 + half * 96;
-        float v[96];
+        // 192 columns = 8 pixel rows x 8 pixels x 3 channels of the token
+        constexpr int PR = 8 / NCQ;                  // pixel rows per warp
+        constexpr int CW = PR * 24;                  // columns per warp
+        const int prow0 = cq * PR;
+        const uint32_t trp = tmem + ((uint32_t)(q * 32) << 16) + ab * 256 + cq * CW;
+        float v[CW];
 #pragma unroll
-        for (int cc = 0; cc < 3; ++cc) {
-          float u32[32];
-          tc::tmem_ld32(trp + cc * 32, u32);
+        for (int cc = 0; cc < CW / 16; ++cc) {
+          float u16[16];
+          tc::tmem_ld16(trp + cc * 16, u16);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[cc * 32 + i] = u32[i];
+          for (int i = 0; i < 16; ++i) v[cc * 16 + i] = u16[i];
         }
         tc::fence_before_sync();
         __syncwarp();
         if (lane == 0) tc::mbar_arrive_cluster(aempty_leader + ab * 8);
         const int f = a.frame_base + nb;
-        const int nb0 = nb * kNU + half * 96;
+        const int nb0 = nb * kNU + cq * CW;
         const int4* bp4 = reinterpret_cast<const int4*>(a.bias + nb0);
         const int xs = x0 + 8 * (int)rank;
         if (a.pix_u8) {
-          // uint8 q frames (sample value float(q / 255)): a quarter of the bytes
-          // q in place of the accumulator bits (no second 96-register array)
-          // the [0, 255] clamp happens in the saturating u8 pack below
+          // uint8 q frames (sample value float(q / 255)): q in place of the
+          // accumulator bits; the [0, 255] clamp happens in the saturating pack
           const int rnd = 1 << (a.shift - 1);
           auto qf = [&](int acc, int b) { return __int_as_float((acc + b + rnd) >> a.shift); };
 #pragma unroll
-          for (int i4 = 0; i4 < 24; ++i4) {
+          for (int i4 = 0; i4 < CW / 4; ++i4) {
             const int4 bb = __ldg(bp4 + i4);
             v[4 * i4 + 0] = qf(__float_as_int(v[4 * i4 + 0]), bb.x);
             v[4 * i4 + 1] = qf(__float_as_int(v[4 * i4 + 1]), bb.y);
@@ -584,19 +603,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::THREADS, 1)
           uint8_t* fr8 = reinterpret_cast<uint8_t*>(a.frames);
           const bool seg8 = (a.w * 3) % 16 == 0 && xs + 8 <= a.Wt && xs * 8 + 64 <= a.w;
           if (seg8) {
-            uint8_t* srow = sStage + (warp - 2) * 768;          // [4][192] bytes
+            uint8_t* srow = sStage + e * 768;                  // [4][192] bytes
 #pragma unroll
-            for (int pr = 0; pr < 4; ++pr) {
+            for (int pr = 0; pr < PR; ++pr) {
               uint32_t* s32 = reinterpret_cast<uint32_t*>(srow + (lane >> 3) * 192 + (lane & 7) * 24);
 #pragma unroll
-              for (int e = 0; e < 6; ++e)
-                s32[e] = pack4_satu8(qv(pr * 24 + 4 * e), qv(pr * 24 + 4 * e + 1),
-                                     qv(pr * 24 + 4 * e + 2), qv(pr * 24 + 4 * e + 3));
+              for (int k = 0; k < 6; ++k)
+                s32[k] = pack4_satu8(qv(pr * 24 + 4 * k), qv(pr * 24 + 4 * k + 1),
+                                     qv(pr * 24 + 4 * k + 2), qv(pr * 24 + 4 * k + 3));
               __syncwarp();
               for (int i = lane; i < 48; i += 32) {
                 const int r = i / 12, c16 = i - r * 12;
                 const int yr = y0 + q * 4 + r;
-                const int Y = yr * 8 + half * 4 + pr;
+                const int Y = yr * 8 + prow0 + pr;
                 if (yr < a.Ht && Y < a.h)
                   reinterpret_cast<uint4*>(fr8 + ((((size_t)g * 9 + f) * a.h + Y) * a.w + xs * 8) * 3)[c16] =
                       reinterpret_cast<const uint4*>(srow + r * 192)[c16];
@@ -607,21 +626,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::THREADS, 1)
           }
           if (!valid) continue;
 #pragma unroll
-          for (int pr = 0; pr < 4; ++pr) {
-            const int Y = y * 8 + half * 4 + pr;
+          for (int pr = 0; pr < PR; ++pr) {
+            const int Y = y * 8 + prow0 + pr;
             if (Y >= a.h) continue;
             const int X0 = x * 8;
             uint8_t* dst = fr8 + ((((size_t)g * 9 + f) * a.h + Y) * a.w + X0) * 3;
             const int npx = min(8, a.w - X0);
 #pragma unroll
-            for (int e = 0; e < 24; ++e)
-              if (e / 3 < npx) dst[e] = (uint8_t)min(max(qv(pr * 24 + e), 0), 255);
+            for (int k = 0; k < 24; ++k)
+              if (k / 3 < npx) dst[k] = (uint8_t)min(max(qv(pr * 24 + k), 0), 255);
           }
 #undef qv
           continue;
         }
 #pragma unroll
-        for (int i4 = 0; i4 < 24; ++i4) {
+        for (int i4 = 0; i4 < CW / 4; ++i4) {
           const int4 bb = __ldg(bp4 + i4);
           v[4 * i4 + 0] = pixel_lut(__float_as_int(v[4 * i4 + 0]), bb.x, a.shift, pix_lut);
           v[4 * i4 + 1] = pixel_lut(__float_as_int(v[4 * i4 + 1]), bb.y, a.shift, pix_lut);
@@ -631,9 +650,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::THREADS, 1)
         const bool vec = (a.w & 3) == 0;
         const bool seg = vec && xs + 8 <= a.Wt && xs * 8 + 64 <= a.w;
         if (seg) {
-          float* srow = reinterpret_cast<float*>(sStage) + (warp - 2) * 768;   // [4][192]
+          float* srow = reinterpret_cast<float*>(sStage) + e * 768;   // [4][192]
 #pragma unroll
-          for (int pr = 0; pr < 4; ++pr) {
+          for (int pr = 0; pr < PR; ++pr) {
             float4* s4 = reinterpret_cast<float4*>(srow + (lane >> 3) * 192 + (lane & 7) * 24);
 #pragma unroll
             for (int e4 = 0; e4 < 6; ++e4)
@@ -644,7 +663,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::THREADS, 1)
             for (int i = 0; i < 6; ++i) {
               const int idx = i * 32 + lane, r = idx / 48, c4 = idx - r * 48;
               const int yr = y0 + q * 4 + r;
-              const int Y = yr * 8 + half * 4 + pr;
+              const int Y = yr * 8 + prow0 + pr;
               if (yr < a.Ht && Y < a.h) {
                 float4* d4 = reinterpret_cast<float4*>(
                     a.frames + ((((size_t)g * 9 + f) * a.h + Y) * a.w + xs * 8) * 3);
@@ -657,8 +676,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::THREADS, 1)
         }
         if (!valid) continue;
 #pragma unroll
-        for (int pr = 0; pr < 4; ++pr) {
-          const int Y = y * 8 + half * 4 + pr;
+        for (int pr = 0; pr < PR; ++pr) {
+          const int Y = y * 8 + prow0 + pr;
           if (Y >= a.h) continue;
           const int X0 = x * 8;
           float* dst = a.frames + ((((size_t)g * 9 + f) * a.h + Y) * a.w + X0) * 3;
@@ -677,25 +696,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::THREADS, 1)
         }
         continue;
       }
-      const int n0 = nb * 256 + half * 128;
-      const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + ab * 256 + half * 128;
+      constexpr int CW = 256 / NCQ;                  // columns per warp
+      const int n0 = nb * 256 + cq * CW;
+      const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16) + ab * 256 + cq * CW;
       const size_t tok = (((size_t)g * a.out_T + t) * a.Ht + y) * a.Wt + x;
       if constexpr (kTma) {
-        // short-K GEMM epilogue: the row's 128 residual bytes up front, the
-        // wait for the previous unit's TMA store deferred to the first write
+        // short-K GEMM epilogue: the row's residual bytes up front, the wait
+        // for the previous unit's TMA store deferred to the first write
         uint8_t* stage = sStage + half * 16384;
-        uint4 res[8];
+        const int co = (cq * CW) & 127;              // column offset inside the half
+        uint4 res[CW / 16];
         const bool has_res = valid && a.residual != nullptr;
         if (has_res) {
           const uint4* rp = reinterpret_cast<const uint4*>(a.residual + tok * a.N + n0);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) res[i] = __ldg(rp + i);
+          for (int i = 0; i < CW / 16; ++i) res[i] = __ldg(rp + i);
         }
 #pragma unroll
-        for (int c = 0; c < 128; c += 32) {
+        for (int c = 0; c < CW; c += 32) {
           float v[32];
           tc::tmem_ld32(trow + c, v);
-          if (c + 32 == 128) {
+          if (c + 32 == CW) {
             tc::fence_before_sync();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive_cluster(aempty_leader + ab * 8);
@@ -704,25 +725,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::THREADS, 1)
           epi_store32(v, a, n0 + c, has_res ? &res[c >> 4] : nullptr, o);
           if (c == 0) {
             if (issuer) tma_store_wait_read();
-            named_bar(1 + half, 128);
+            named_bar(1 + half, 32 * HALF_WARPS);
           }
-          const int j0 = c >> 4;
+          const int j0 = (co + c) >> 4;
 #pragma unroll
           for (int qq = 0; qq < 2; ++qq)
             *reinterpret_cast<uint4*>(stage + m * 128 + (((j0 + qq) ^ (m & 7)) << 4)) = o[qq];
         }
         fence_proxy_async_smem();
-        named_bar(1 + half, 128);
+        named_bar(1 + half, 32 * HALF_WARPS);
         if (issuer) {
-          tc::tma_store_5d(&tmC, stage, n0, x0 + 8 * (int)rank, y0, t, g);
+          tc::tma_store_5d(&tmC, stage, nb * 256 + half * 128, x0 + 8 * (int)rank, y0, t, g);
           tma_store_commit();
         }
       } else {
 #pragma unroll 1
-        for (int c = 0; c < 128; c += 32) {
+        for (int c = 0; c < CW; c += 32) {
           float v[32];
           tc::tmem_ld32(trow + c, v);
-          if (c + 32 == 128) {
+          if (c + 32 == CW) {
             tc::fence_before_sync();
             __syncwarp();
             if (lane == 0) tc::mbar_arrive_cluster(aempty_leader + ab * 8);
@@ -1370,7 +1391,8 @@ static int launch_pair(const SstConvDesc* d, cudaStream_t st, int kind) {
   const int smem = halo ? pair_smem<true, false>()
                         : (pix ? pair_smem<false, false, true>() : pair_smem<false, true>());
   SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  kern<<<(unsigned)(2 * pairs), pc::THREADS, smem, st>>>(tmA, tmB, tmC, a, (int)units, n_blocks);
+  const int threads = pix ? pc::pair_threads<true>() : pc::pair_threads<false>();
+  kern<<<(unsigned)(2 * pairs), threads, smem, st>>>(tmA, tmB, tmC, a, (int)units, n_blocks);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }
