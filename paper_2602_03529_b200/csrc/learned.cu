@@ -873,7 +873,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
         }
         tc::fence_before_sync();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive_cluster(aempty_leader + ab * 8);
+        if (lane == 0) tc::mbar_arrive_cluster_relaxed(aempty_leader + ab * 8);
         const int f = a.frame_base + nb;
         const int nb0 = nb * kNU + half * 96;
         const float4* bp4 = reinterpret_cast<const float4*>(a.bias + nb0);
@@ -962,7 +962,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
           if (c + 32 == 128) {
             tc::fence_before_sync();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive_cluster(aempty_leader + ab * 8);
+            if (lane == 0) tc::mbar_arrive_cluster_relaxed(aempty_leader + ab * 8);
           }
           const float4* bp = reinterpret_cast<const float4*>(a.bias + n0 + c);
 #pragma unroll
@@ -1022,7 +1022,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(c233c::THREADS, 1)
           if (c + 32 == 128) {
             tc::fence_before_sync();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive_cluster(aempty_leader + ab * 8);
+            if (lane == 0) tc::mbar_arrive_cluster_relaxed(aempty_leader + ab * 8);
           }
 #pragma unroll
           for (int i = 0; i < 32; ++i) {

@@ -581,7 +581,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::pair_threads<kPi
         }
         tc::fence_before_sync();
         __syncwarp();
-        if (lane == 0) tc::mbar_arrive_cluster(aempty_leader + ab * 8);
+        if (lane == 0) tc::mbar_arrive_cluster_relaxed(aempty_leader + ab * 8);
         const int f = a.frame_base + nb;
         const int nb0 = nb * kNU + cq * CW;
         const int4* bp4 = reinterpret_cast<const int4*>(a.bias + nb0);
@@ -719,7 +719,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::pair_threads<kPi
           if (c + 32 == CW) {
             tc::fence_before_sync();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive_cluster(aempty_leader + ab * 8);
+            if (lane == 0) tc::mbar_arrive_cluster_relaxed(aempty_leader + ab * 8);
           }
           uint4 o[2];
           epi_store32(v, a, n0 + c, has_res ? &res[c >> 4] : nullptr, o);
@@ -746,7 +746,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(pc::pair_threads<kPi
           if (c + 32 == CW) {
             tc::fence_before_sync();
             __syncwarp();
-            if (lane == 0) tc::mbar_arrive_cluster(aempty_leader + ab * 8);
+            if (lane == 0) tc::mbar_arrive_cluster_relaxed(aempty_leader + ab * 8);
           }
           if (!valid) continue;
           uint4 res[2];

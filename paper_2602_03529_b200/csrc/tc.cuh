@@ -199,6 +199,15 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
                : "memory");
 }
+// the same without release semantics: for the accumulator-empty signal, whose
+// only precondition -- the warp's TMEM loads -- is already complete
+// (tcgen05.wait::ld) and fenced (tcgen05.fence::before_thread_sync); the
+// release form costs a MEMBAR.ALL.CTA + ERRBAR that waits for every
+// outstanding global access of the warp (12 % of the 1x1 GEMMs' stall samples)
+__device__ __forceinline__ void mbar_arrive_cluster_relaxed(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
 // both CTAs of the pair load into their own smem; completion bytes go to the
 // even CTA's barrier (peer bit 24 of the shared::cluster address cleared)
 __device__ __forceinline__ void tma_load_5d_pair(void* dst, const CUtensorMap* map, int c0, int c1,
