@@ -832,6 +832,199 @@ __global__ void __launch_bounds__(kRcThreadsC, 1)
   if (lane == 0) status[g] = st;
 }
 
+// sum of 16 small values as a 3-input add tree (depth 3, not a 16-long chain)
+// (the values pass through an empty asm so the compiler cannot turn the tree
+// of 0/1 adds back into a chain of 16 conditional increments)
+__device__ __forceinline__ uint32_t sum16(uint32_t (&b)[16]) {
+#pragma unroll
+  for (int k = 0; k < 16; ++k) asm("" : "+r"(b[k]));
+  const uint32_t a0 = b[0] + b[1] + b[2], a1 = b[3] + b[4] + b[5], a2 = b[6] + b[7] + b[8];
+  const uint32_t a3 = b[9] + b[10] + b[11], a4 = b[12] + b[13] + b[14];
+  return (a0 + a1 + a2) + (a3 + a4 + b[15]);
+}
+
+// ---- decoder with a split cumulative table (default) --------------------------
+// One warp per CTA (one stream); lane l holds the exclusive cumulative counts
+// cum[k] of symbols 16 l + k and `end` = the cumulative count of symbol
+// 16 l + 16, so a symbol's count is the difference of two neighbours.  The
+// serial chain per symbol is kept short and the instruction count low:
+//  * r = range / total: one multiply-high by floor(2^32 / total), fetched from
+//    the lane that holds it one symbol ahead (total grows by one per symbol
+//    between halvings), plus one correction;
+//  * the search: 16 signed IMAD.WIDE per lane give d - cum * r as 64-bit
+//    values whose high words are 0 (cum * r <= d) or -1; their sum is the
+//    number of qualifying symbols of the lane (cum is increasing), the ballot
+//    of "any" the owner lane;
+//  * every lane prepares the (low, range) it would produce if it owned the
+//    symbol, so the owner's result is one shuffle away;
+//  * the model update is one compare + one predicated add per entry;
+//  * the next payload byte is fetched before it is needed.
+__device__ __forceinline__ uint32_t sel16x(const uint32_t (&a)[16], uint32_t e, int idx) {
+  // a[idx + 1] for idx in [0, 16), with a[16] = e
+  uint32_t b[8], c[4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) b[i] = (idx & 1) ? (2 * i + 2 < 16 ? a[2 * i + 2] : e) : a[2 * i + 1];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) c[i] = (idx & 2) ? b[2 * i + 1] : b[2 * i];
+  const uint32_t d0 = (idx & 4) ? c[1] : c[0], d1 = (idx & 4) ? c[3] : c[2];
+  return (idx & 8) ? d1 : d0;
+}
+
+// exclusive cumulative counts from per-entry counts (warp scan over lanes)
+__device__ __forceinline__ uint32_t cx_build(uint32_t (&cum)[16], uint32_t& end, int lane,
+                                             const uint32_t (&cnt)[16]) {
+  uint32_t local = 0;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) local += cnt[k];
+  uint32_t incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += t;
+  }
+  uint32_t run = incl - local;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    cum[k] = run;
+    run += cnt[k];
+  }
+  end = run;
+  return __shfl_sync(0xffffffffu, incl, 31);          // total
+}
+
+__global__ void __launch_bounds__(32)
+    k_rc_decode_x(const uint8_t* __restrict__ data, const int64_t* __restrict__ off,
+                  const int64_t* __restrict__ len, int64_t n, int16_t* __restrict__ scans,
+                  int32_t* __restrict__ status) {
+  const int g = blockIdx.x;
+  const int lane = threadIdx.x;
+  int16_t* scan = scans + (int64_t)g * n;
+  {
+    const int64_t head = min(n, (int64_t)((16 - ((uintptr_t)scan & 15)) & 15) / 2);
+    if (((uintptr_t)scan & 1) == 0) {
+      if (lane < head) scan[lane] = 0;
+      int4* body = reinterpret_cast<int4*>(scan + head);
+      const int64_t nv = (n - head) / 8;
+      for (int64_t j = lane; j < nv; j += 32) body[j] = make_int4(0, 0, 0, 0);
+      for (int64_t j = head + nv * 8 + lane; j < n; j += 32) scan[j] = 0;
+    } else {
+      for (int64_t j = lane; j < n; j += 32) scan[j] = 0;
+    }
+  }
+  __syncwarp();
+  const uint8_t* src = data + off[g];
+  const int64_t nb = len[g];
+  int st = 0;
+  uint32_t cum[16], end;
+  uint32_t total;
+  {
+    uint32_t cnt[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) cnt[k] = (16 * lane + k) < kAlpha ? 1u : 0u;
+    total = cx_build(cum, end, lane, cnt);
+  }
+  int64_t wbase = 0, p = 0;
+  uint32_t w0 = lane < nb ? src[lane] : 0u;
+  uint32_t w1 = 32 + lane < nb ? src[32 + lane] : 0u;
+  // the byte at p (valid while p < nb), fetched ahead of its use
+  auto fetch = [&]() -> uint32_t {
+    if (p - wbase >= 32) {
+      wbase += 32;
+      w0 = w1;
+      w1 = wbase + 32 + lane < nb ? src[wbase + 32 + lane] : 0u;
+    }
+    return __shfl_sync(0xffffffffu, w0, (int)(p - wbase));
+  };
+  uint32_t state = 0;
+  for (int k = 0; k < 4; ++k) {
+    if (p >= nb) { st = 1; break; }
+    state = (state << 8) | fetch();
+    ++p;
+  }
+  uint32_t bnext = fetch();
+  uint32_t low = 0, range = 0xFFFFFFFFu;
+  uint32_t t0 = total;                               // lane l: floor(2^32 / (t0 + l))
+  uint32_t minv = (uint32_t)(0x100000000ull / (t0 + lane));
+  uint32_t mt = __shfl_sync(0xffffffffu, minv, 0);
+  int64_t pos = 0, nsym = 0;
+  while (st == 0) {
+    uint32_t r = __umulhi(range, mt);
+    if (range - r * total >= total) ++r;
+    // val = min(floor((state - low) / r), total - 1) (rangecoder.py:216-219):
+    // compare cum * r against d = min(state - low, total r - 1); state < low
+    // (corrupt streams only) clamps like the 64-bit difference
+    const uint32_t dd = state < low ? 0xFFFFFFFFu : state - low;
+    const uint32_t d32 = min(total * r - 1u, dd);
+    const int nr = -(int)r;                          // r < 2^24: total >= 510
+    uint32_t b[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      b[k] = (uint32_t)((uint64_t)((int64_t)(int)cum[k] * nr + (int64_t)d32) >> 32);
+    const uint32_t nle = 16u + sum16(b);
+    const unsigned bal = __ballot_sync(0xffffffffu, nle != 0);
+    const int owner = 31 - __clz(bal);
+    const int kl = nle > 0 ? (int)nle - 1 : 0;
+    const uint32_t ca = sel16(cum, kl), cb = sel16x(cum, end, kl);
+    const uint32_t cand_low = low + ca * r;          // rangecoder.py:222-223 (carry-less)
+    const uint32_t cand_range = (cb - ca) * r;
+    low = __shfl_sync(0xffffffffu, cand_low, owner);
+    range = __shfl_sync(0xffffffffu, cand_range, owner);
+    const int kk = __shfl_sync(0xffffffffu, kl, owner);
+    const int sym = owner * 16 + kk;
+    // the next symbol's reciprocal, in flight during the renormalisation
+    // (replaced below when the batch ends or the model is halved)
+    uint32_t mt_n = __shfl_sync(0xffffffffu, minv, (int)((total + 1u - t0) & 31u));
+    for (;;) {                                       // rangecoder.py:224-231
+      const uint32_t hi = low + range;
+      const bool top_differs = hi < low || (low ^ hi) >= (uint32_t)kTop;
+      if (top_differs && range >= (uint32_t)kBottom) break;
+      if (top_differs) range = (0u - low) & (uint32_t)(kBottom - 1);
+      if (p >= nb) { st = 1; break; }
+      state = (state << 8) | bnext;
+      ++p;
+      bnext = fetch();
+      low <<= 8;
+      range <<= 8;
+    }
+    if (st) break;
+    // model update (rangecoder.py:143-149): symbols above sym gain one
+    const int t = lane > owner ? -1 : (lane == owner ? kk : 16);
+#pragma unroll
+    for (int k = 0; k < 16; ++k)                     // k > t: one compare + one predicated add
+      asm("{\n\t.reg .pred p;\n\tsetp.lt.s32 p, %1, %2;\n\t@p add.u32 %0, %0, 1;\n\t}"
+          : "+r"(cum[k]) : "r"(t), "r"(k));
+    end += (uint32_t)(t - 16) >> 31;
+    total += 1;
+    if (total >= (uint32_t)kBottom) {
+      uint32_t cnt[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const uint32_t nx = k + 1 < 16 ? cum[k + 1] : end;
+        cnt[k] = (nx - cum[k] + 1) / 2;              // 0 stays 0 (s >= 510)
+      }
+      total = cx_build(cum, end, lane, cnt);
+    }
+    if (total - t0 >= 32u) {                         // next batch of reciprocals
+      t0 = total;
+      minv = (uint32_t)(0x100000000ull / (t0 + lane));
+      mt_n = __shfl_sync(0xffffffffu, minv, 0);
+    }
+    mt = mt_n;
+    ++nsym;
+    if (sym == 0) break;                            // EOS
+    if (sym <= 255) {                               // zero run (rangecoder.py:107-110)
+      pos += sym;
+      if (pos > n) { st = 2; break; }
+    } else {
+      if (pos >= n) { st = 3; break; }
+      if (lane == 0) scan[pos] = (int16_t)(sym <= 382 ? sym - 383 : sym - 382);
+      ++pos;
+    }
+    if (nsym >= (1 << 24)) { st = 4; break; }
+  }
+  if (lane == 0) status[g] = st;
+}
+
 // ---- parallel-model encoder (default) -----------------------------------------
 // The ENCODER knows its whole symbol sequence up front, so the adaptive
 // model's state before every symbol -- (cum, cnt) of that symbol and the
@@ -1409,8 +1602,10 @@ extern "C" int sst_rc_decode(const uint8_t* data, const int64_t* off, const int6
     k_rc_decode_w<<<G, kRcThreads, 0, st>>>(data, off, len, n, scans, status);
   else if (mode && mode[0] == 'q')
     k_rc_decode_c<true><<<G, kRcThreadsC, 0, st>>>(data, off, len, n, scans, status);
-  else
+  else if (mode && mode[0] == 'c')
     k_rc_decode_c<false><<<G, kRcThreadsC, 0, st>>>(data, off, len, n, scans, status);
+  else
+    k_rc_decode_x<<<G, 32, 0, st>>>(data, off, len, n, scans, status);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }
