@@ -1067,9 +1067,9 @@ def residual_leg(a, device) -> dict:
     st = _dev.stream()
     theta, step_q = 0.02, 1.0 / 127.0
     stages = [
-        ("codec", lambda: (c.encode(frames, G, 0), c.decode(G, 0))),
-        ("downscale", lambda: _lib.call("sst_downscale", frames.data_ptr(), G * 9, H, W, s,
-                                        work.data_ptr(), st)),
+        # K1 writes the working frames (the residual's `working` GoP) as it
+        # box-filters them: no second read of the full-resolution frames
+        ("codec", lambda: (c.encode(frames, G, 0, work=work), c.decode(G, 0))),
         ("residual", lambda: _lib.call("sst_residual", work.data_ptr(), c.img[0].data_ptr(), G, h,
                                        w, theta, step_q, avg.data_ptr(), dense.data_ptr(),
                                        mags.data_ptr(), count.data_ptr(), st)),
@@ -1111,15 +1111,16 @@ def residual_leg(a, device) -> dict:
                            "table, k_rc_decode_x); bytes identical to the reference"}
 
 
-def residual_pipelined(a, device, frames, G, H, W, s, theta, step_q, depth=3, steps=12) -> dict:
+def residual_pipelined(a, device, frames, G, H, W, s, theta, step_q, depth=6, steps=18) -> dict:
     """The residual workload as a stream of steps: the range decoder is a serial
     chain per stream that occupies one warp of an SM (64 .. 512 streams decode
     in the same time: scripts/rc_decode_micro.py), so the receiver's decode +
-    apply of step k runs on its own CUDA stream while the sender codes step
-    k + 1 -- `depth` sets of codec / payload / scan buffers rotate (3: a set is
-    busy for the sender's ~9 ms plus the decoder's ~15 ms), and a set
-    is reused only after its previous decode + apply finished.  Every step's
-    decoded scans are checked against its encoded ones."""
+    apply of step k, and the sender's range encode (also one warp per
+    stream), run on a per-step CUDA stream while the next steps' proxy codec
+    and residual kernels run on the main one -- `depth` sets of codec /
+    payload / scan buffers rotate (a set is busy for ~20 ms of serial coding),
+    and a set is reused only after its previous decode + apply finished.
+    Every step's decoded scans are checked against its encoded ones."""
     import numpy as np
     import torch
     from paper_2602_03529_b200 import _dev, _lib
@@ -1133,7 +1134,6 @@ def residual_pipelined(a, device, frames, G, H, W, s, theta, step_q, depth=3, st
     work = torch.empty((G, 9, h, w, 3), device=device)
     avg = torch.empty((G, n), dtype=f64, device=device)
     mags = torch.empty((G, n), dtype=f64, device=device)
-    idx_ws = torch.empty((G * n,), dtype=torch.int64, device=device)
     offs = torch.arange(G, dtype=torch.int64, device=device) * cap
     sets = []
     for _ in range(depth):
@@ -1142,6 +1142,7 @@ def residual_pipelined(a, device, frames, G, H, W, s, theta, step_q, depth=3, st
         sets.append(dict(
             c=c, stream=torch.cuda.Stream(device=device),
             dense=torch.empty((G, n), dtype=i16, device=device),
+            idx_ws=torch.empty((G * n,), dtype=torch.int64, device=device),
             count=torch.empty((G,), dtype=torch.int32, device=device),
             pay=torch.empty((G * cap,), dtype=torch.uint8, device=device),
             plen=torch.empty((G,), dtype=torch.int64, device=device),
@@ -1157,19 +1158,18 @@ def residual_pipelined(a, device, frames, G, H, W, s, theta, step_q, depth=3, st
             cur.wait_event(S["done"])                # set free: its last decode + apply ended
         if check and k >= depth:
             ok[0] &= bool(torch.equal(S["dec"], S["dense"])) and bool((S["status"] == 0).all())
-        c.encode(frames, G, 0)
+        c.encode(frames, G, 0, work=work)
         c.decode(G, 0)
-        _lib.call("sst_downscale", frames.data_ptr(), G * 9, H, W, s, work.data_ptr(), main)
         _lib.call("sst_residual", work.data_ptr(), c.img[0].data_ptr(), G, h, w, theta, step_q,
                   avg.data_ptr(), S["dense"].data_ptr(), mags.data_ptr(), S["count"].data_ptr(),
                   main)
-        _lib.call("sst_rc_encode", S["dense"].data_ptr(), G, n, idx_ws.data_ptr(),
-                  S["pay"].data_ptr(), cap, S["plen"].data_ptr(), main)
         sent = torch.cuda.Event()
         sent.record(cur)
         rs = S["stream"]
         rs.wait_event(sent)
         with torch.cuda.stream(rs):
+            _lib.call("sst_rc_encode", S["dense"].data_ptr(), G, n, S["idx_ws"].data_ptr(),
+                      S["pay"].data_ptr(), cap, S["plen"].data_ptr(), _dev.stream())
             _lib.call("sst_rc_decode", S["pay"].data_ptr(), offs.data_ptr(), S["plen"].data_ptr(),
                       G, n, S["dec"].data_ptr(), S["status"].data_ptr(), _dev.stream())
             _lib.call("sst_apply_residual", c.img[0].data_ptr(), S["dec"].data_ptr(),
@@ -1197,8 +1197,11 @@ def residual_pipelined(a, device, frames, G, H, W, s, theta, step_q, depth=3, st
         ok[0] &= bool(torch.equal(S["dec"], S["dense"])) and bool((S["status"] == 0).all())
     return {"depth": depth, "steps": steps, "ms_per_step": round(ms, 3),
             "frames_per_s": round(G * GOP / ms * 1e3, 1), "roundtrip_exact": ok[0],
-            "how": "receiver (range decode + apply) of step k on its own CUDA stream while the "
-                   "sender codes step k+1; per-step GoP latency unchanged (~ the serial sum)"}
+            "how": "range encode + range decode + apply of step k on a per-step CUDA stream "
+                   "(the coders are one warp per stream, serial per stream) while the next "
+                   "steps' codec + residual kernels run on the main stream; timed from the "
+                   "first step's start to the last step's decode + apply (pipeline drain "
+                   "included); per-GoP latency unchanged (~ the serial sum)"}
 
 
 # ---------------------------------------------------------------------------

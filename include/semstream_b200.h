@@ -148,6 +148,14 @@ SST_API int sst_upscale_blend9_u8(const uint8_t* img, int G, int h, int w, int s
 SST_API int sst_encode(const float* frames, int G, int H, int W, int s, double* tok, double* sim,
                void* stream);
 
+/* sst_encode that also writes the working frames it box-filters (the
+ * downscaled GoP scale_gop(gop, s, "down"), codec.py:202-214 / 248-254) to
+ * work: [G][9][ceil(H/s)][ceil(W/s)][3] float32, or NULL (= sst_encode).
+ * The residual layer's `working` GoP (session.py:173-189) without a second
+ * read of the full-resolution frames. */
+SST_API int sst_encode_work(const float* frames, int G, int H, int W, int s, double* tok,
+               double* sim, float* work, void* stream);
+
 /* decode_gop (codec.py:160-186): IDCT of I and P tokens, crop to (h, w),
  * clip, conceal invalid P blocks with I blocks.
  *   i_tok, p_tok: [G][H'][W'][12] (any batch stride via tok_stride elements);

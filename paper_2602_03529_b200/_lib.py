@@ -71,6 +71,7 @@ SIGNATURES = {
     "sst_clip_cast": (_I, [_P, _L, _P, _P]),
     "sst_blend": (_I, [_P, _P, _I, _I, _I, _I, _P, _P]),
     "sst_encode": (_I, [_P, _I, _I, _I, _I, _P, _P, _P]),
+    "sst_encode_work": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P]),
     "sst_decode": (_I, [_P, _P, _L, _P, _I, _I, _I, _I, _I, _P, _P]),
     "sst_similarity": (_I, [_P, _P, _L, _I, _P, _P]),
     "sst_topk_mask": (_I, [_P, _I, _L, _P, _P, _P, _P]),

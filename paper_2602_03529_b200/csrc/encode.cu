@@ -44,6 +44,7 @@ struct EncArgs {
   int G, H, W, h, w, Ht, Wt;
   double* tok;
   double* sim;
+  float* work;   // optional: the working frames [G][9][h][w][3] (scale_gop(down))
 };
 
 // numpy pairwise order for a 12-long reduction (8-way unrolled block + tail)
@@ -123,6 +124,13 @@ __global__ void __launch_bounds__(EncCfg<S>::NT)
   float ival[3];
   double pacc[3];
   constexpr double div_ss = (double)(S * S);
+  // the working pixel this thread box-filters, written out when asked for
+  // (the residual layer's `working` GoP, session.py:173-189) -- only real
+  // pixels, not the block padding's edge replicas
+  const size_t work_frame = (size_t)a.h * a.w * 3;
+  float* wout = nullptr;
+  if (a.work != nullptr && ty * 8 + wy < a.h && tx0 * 8 + wx < a.w)
+    wout = a.work + (size_t)g * kGop * work_frame + ((size_t)(ty * 8 + wy) * a.w + tx0 * 8 + wx) * 3;
 
   for (int f = 0; f < kGop; ++f) {
     const int st = f % C::NST;
@@ -146,6 +154,7 @@ __global__ void __launch_bounds__(EncCfg<S>::NT)
 #pragma unroll
       for (int q = 1; q < S * S; ++q) acc = acc + (double)tile[off[q] + ch];
       float wv = __double2float_rn(acc / div_ss);     // Frame float32 storage
+      if (wout != nullptr) wout[(size_t)f * work_frame + ch] = wv;
       if (f == 0) {
         ival[ch] = wv;
       } else if (f == 1) {
@@ -255,7 +264,7 @@ __global__ void k_downscale(const float* __restrict__ src, int64_t n, int H, int
 }
 
 template <int S>
-static int launch_encode(const float* frames, int G, int H, int W, double* tok, double* sim,
+static int launch_encode(const float* frames, int G, int H, int W, double* tok, double* sim, float* work,
                          cudaStream_t stream) {
   using C = EncCfg<S>;
   EncArgs a;
@@ -267,6 +276,7 @@ static int launch_encode(const float* frames, int G, int H, int W, double* tok, 
   a.Wt = ceil_div(a.w, kBlock);
   a.tok = tok;
   a.sim = sim;
+  a.work = work;
   if (a.Ht > 65535 || G > 65535) return SST_ERR_ARG;
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
@@ -290,16 +300,21 @@ static int launch_encode(const float* frames, int G, int H, int W, double* tok, 
 
 using namespace sst;
 
-extern "C" int sst_encode(const float* frames, int G, int H, int W, int s, double* tok, double* sim,
-                          void* stream) {
+extern "C" int sst_encode_work(const float* frames, int G, int H, int W, int s, double* tok,
+                               double* sim, float* work, void* stream) {
   if (!frames || !tok || G <= 0 || H <= 0 || W <= 0) return SST_ERR_ARG;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   switch (s) {
-    case 1: return launch_encode<1>(frames, G, H, W, tok, sim, st);
-    case 2: return launch_encode<2>(frames, G, H, W, tok, sim, st);
-    case 3: return launch_encode<3>(frames, G, H, W, tok, sim, st);
+    case 1: return launch_encode<1>(frames, G, H, W, tok, sim, work, st);
+    case 2: return launch_encode<2>(frames, G, H, W, tok, sim, work, st);
+    case 3: return launch_encode<3>(frames, G, H, W, tok, sim, work, st);
     default: return SST_ERR_ARG;
   }
+}
+
+extern "C" int sst_encode(const float* frames, int G, int H, int W, int s, double* tok, double* sim,
+                          void* stream) {
+  return sst_encode_work(frames, G, H, W, s, tok, sim, nullptr, stream);
 }
 
 extern "C" int sst_downscale(const float* frames, int64_t n, int H, int W, int s, float* out,

@@ -25,6 +25,13 @@ struct AxisTap {
   double f, g;   // frac, 1 - frac
 };
 
+// a row's tap as kept in shared memory: one 16-byte LDS.128 per row (g is
+// recomputed as 1 - f, the same double operation axis_tap performs)
+struct __align__(16) RowTap {
+  int lo, hi;
+  double f;
+};
+
 // codec.py:222-228
 __device__ __forceinline__ AxisTap axis_tap(int o, int n_in, int s) {
   double c = ((double)o + 0.5) / (double)s - 0.5;
@@ -35,6 +42,17 @@ __device__ __forceinline__ AxisTap axis_tap(int o, int n_in, int s) {
   t.lo = lo;
   t.hi = min(lo + 1, n_in - 1);
   t.f = c - (double)lo;
+  t.g = 1.0 - t.f;
+  return t;
+}
+
+__device__ __forceinline__ RowTap to_row(const AxisTap& t) { return RowTap{t.lo, t.hi, t.f}; }
+__device__ __forceinline__ AxisTap from_row(const RowTap& r) {
+  const uint4 v = *reinterpret_cast<const uint4*>(&r);     // one 16-byte load
+  AxisTap t;
+  t.lo = (int)v.x;
+  t.hi = (int)v.y;
+  t.f = __hiloint2double((int)v.w, (int)v.z);
   t.g = 1.0 - t.f;
   return t;
 }
@@ -129,7 +147,7 @@ __device__ __forceinline__ void vstep(RowCache& c, const float* i0, const float*
 }
 
 __global__ void __launch_bounds__(kUpThreads) k_upscale_blend(const __grid_constant__ UpArgs a) {
-  __shared__ AxisTap ty_c[kUpRows], ty_p[kUpRows];
+  __shared__ RowTap ty_c[kUpRows], ty_p[kUpRows];
   const int tid = threadIdx.x;
   const int q = blockIdx.x * kUpThreads + tid;       // float column: pixel*3 + channel
   const int oy0 = blockIdx.y * kUpRows;
@@ -139,8 +157,8 @@ __global__ void __launch_bounds__(kUpThreads) k_upscale_blend(const __grid_const
   pd.h = pd.w = pd.s = 1;
   if (a.prev) pd = a.prev[g];
   const bool has_prev = pd.p_img != nullptr;
-  if (tid < kUpRows) ty_c[tid] = axis_tap(oy0 + tid, a.h, a.s);
-  else if (has_prev && tid < 2 * kUpRows) ty_p[tid - kUpRows] = axis_tap(oy0 + tid - kUpRows, pd.h, pd.s);
+  if (tid < kUpRows) ty_c[tid] = to_row(axis_tap(oy0 + tid, a.h, a.s));
+  else if (has_prev && tid < 2 * kUpRows) ty_p[tid - kUpRows] = to_row(axis_tap(oy0 + tid - kUpRows, pd.h, pd.s));
   __syncthreads();
   if (q >= a.W * 3) return;
   const int ox = q / 3, ch = q - ox * 3;
@@ -154,7 +172,7 @@ __global__ void __launch_bounds__(kUpThreads) k_upscale_blend(const __grid_const
   if (!has_prev) {
     for (int r = 0; r < rows; ++r, o += a.W * 3) {
       float u[2];
-      vstep<2>(cc, iimg, pimg, a.w, ty_c[r], tx, ch, u);
+      vstep<2>(cc, iimg, pimg, a.w, from_row(ty_c[r]), tx, ch, u);
       __stcs(o, u[0]);
 #pragma unroll
       for (int f = 1; f < kGop; ++f) __stcs(o + f * fstride, u[1]);
@@ -165,8 +183,8 @@ __global__ void __launch_bounds__(kUpThreads) k_upscale_blend(const __grid_const
   RowCache cp{-1, -1, 0.0, 0.0, 0.0, 0.0};
   for (int r = 0; r < rows; ++r, o += a.W * 3) {
     float u[2], uq[2];
-    vstep<2>(cc, iimg, pimg, a.w, ty_c[r], tx, ch, u);
-    vstep<1>(cp, pd.p_img, nullptr, pd.w, ty_p[r], txp, ch, uq);
+    vstep<2>(cc, iimg, pimg, a.w, from_row(ty_c[r]), tx, ch, u);
+    vstep<1>(cp, pd.p_img, nullptr, pd.w, from_row(ty_p[r]), txp, ch, uq);
     // frame f < n: alpha*prev[9-n+f] + (1-alpha)*curr[f]  (codec.py:289-293);
     // the previous GoP's tail frames are its unblended P upscale when n <= 4
     __stcs(o, (float)clip01(a.alpha[0] * (double)uq[0] + a.beta[0] * (double)u[0]));
@@ -205,7 +223,7 @@ struct UpTmaSmem {
   static constexpr int kWR = BAND / 2 + 2;   // max source rows per band (s >= 2)
   static constexpr int kWin = (kWR * kWF9 + 31) / 32 * 32;   // floats per window, 128 B aligned
   float win[3][kWin];                      // I, P, previous P windows (row pitch kWF9)
-  AxisTap ty_c[BAND], ty_p[BAND];
+  RowTap ty_c[BAND], ty_p[BAND];
   int wx0[2], wx1[2];                      // window column range (source px) cur / prev
   int xs;                                  // I/P window column shift (TMA alignment)
   uint64_t bar;                            // TMA window loads
@@ -261,9 +279,9 @@ __global__ void __launch_bounds__(kTQ)
   const bool has_prev = kPrev && pd.p_img != nullptr;
   const int rows = min(kBand, a.H - oy0);
   const int qlast = min(q0 + kTQ, a.W * 3) - 1;
-  if (tid < kBand) S.ty_c[tid] = axis_tap(oy0 + min(tid, rows - 1), a.h, a.s);
+  if (tid < kBand) S.ty_c[tid] = to_row(axis_tap(oy0 + min(tid, rows - 1), a.h, a.s));
   else if (tid < 2 * kBand) {
-    if (has_prev) S.ty_p[tid - kBand] = axis_tap(oy0 + min(tid - kBand, rows - 1), pd.h, pd.s);
+    if (has_prev) S.ty_p[tid - kBand] = to_row(axis_tap(oy0 + min(tid - kBand, rows - 1), pd.h, pd.s));
   } else if (tid == 2 * kBand) {
     S.wx0[0] = axis_tap(q0 / 3, a.w, a.s).lo;
     S.wx1[0] = axis_tap(qlast / 3, a.w, a.s).hi;
@@ -332,7 +350,7 @@ __global__ void __launch_bounds__(kTQ)
     }
     const int cend = min(c0 + kTR, rows);
     for (int r = c0; r < cend; ++r) {
-      const AxisTap ty = S.ty_c[r];
+      const AxisTap ty = from_row(S.ty_c[r]);
       if (ty.lo != ya) {
         if (ty.lo == yb) { ia = ib; pa = pb; }
         else {
@@ -360,7 +378,7 @@ __global__ void __launch_bounds__(kTQ)
         float fv[kN];
         float f0 = ui;
         if (has_prev) {
-          const AxisTap tp = S.ty_p[r];
+          const AxisTap tp = from_row(S.ty_p[r]);
           if (tp.lo != qa) {
             if (tp.lo == qb) qva = qvb;
             else {
@@ -395,7 +413,7 @@ __global__ void __launch_bounds__(kTQ)
       }
       tile[nb][rr][tid] = up;
       if (has_prev) {
-        const AxisTap tp = S.ty_p[r];
+        const AxisTap tp = from_row(S.ty_p[r]);
         if (tp.lo != qa) {
           if (tp.lo == qb) qva = qvb;
           else {
@@ -460,9 +478,9 @@ __global__ void __launch_bounds__(kV2Threads)
   const bool has_prev = kPrev && pd.p_img != nullptr;
   const int rows = min(kBand, a.H - oy0);
   const int qlast = min(q0 + kTQ, a.W * 3) - 1;
-  if (tid < kBand) S.ty_c[tid] = axis_tap(oy0 + min(tid, rows - 1), a.h, a.s);
+  if (tid < kBand) S.ty_c[tid] = to_row(axis_tap(oy0 + min(tid, rows - 1), a.h, a.s));
   else if (tid < 2 * kBand) {
-    if (has_prev) S.ty_p[tid - kBand] = axis_tap(oy0 + min(tid - kBand, rows - 1), pd.h, pd.s);
+    if (has_prev) S.ty_p[tid - kBand] = to_row(axis_tap(oy0 + min(tid - kBand, rows - 1), pd.h, pd.s));
   } else if (tid == 2 * kBand) {
     S.wx0[0] = axis_tap(q0 / 3, a.w, a.s).lo;
     S.wx1[0] = axis_tap(qlast / 3, a.w, a.s).hi;
@@ -522,7 +540,7 @@ __global__ void __launch_bounds__(kV2Threads)
   const int64_t fstride = (int64_t)a.H * orow;
   float* obase = a.out + ((int64_t)g * kGop * a.H + oy0) * orow + qa0;
   for (int r = 0; r < rows; ++r, obase += orow) {
-    const AxisTap ty = S.ty_c[r];
+    const AxisTap ty = from_row(S.ty_c[r]);
     if (ty.lo != ya) {
       if (ty.lo == yb) {
 #pragma unroll
@@ -563,7 +581,7 @@ __global__ void __launch_bounds__(kV2Threads)
 #pragma unroll
     for (int u = 0; u < 2; ++u) fv[0][u] = ui[u];
     if (has_prev) {
-      const AxisTap tp = S.ty_p[r];
+      const AxisTap tp = from_row(S.ty_p[r]);
       if (tp.lo != qa) {
         if (tp.lo == qb) {
 #pragma unroll
@@ -668,7 +686,7 @@ struct Up9fSmem {
   T win[kGop][Up9fGeom<kBand, T>::kWin];
   T winp[kP > 0 ? kP : 1][Up9fGeom<kBand, T>::kWin];   // previous GoP's frames 9-n+f, f < n = kP
   double lut[sizeof(T) == 1 ? 256 : 1];   // uint8 windows: sample value of q (= float(q / 255))
-  AxisTap ty_c[kBand], ty_p[kBand];
+  RowTap ty_c[kBand], ty_p[kBand];
   int wx0[2], wx1[2];
   int xs;                    // current window's column shift (TMA alignment), 0 for cp.async
   uint64_t bar;
@@ -695,6 +713,7 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
                                              int f0, int q0, int oy0, int rows,
                                              const AxisTap& tx, int xl, int xh,
                                              const AxisTap& txp, int pxl, int pxh) {
+  constexpr bool kU8 = sizeof(T) == 1;
   const int tid = threadIdx.x;
   const int r0 = S.ty_c[0].lo;
   // blended frames f < NB = n: alpha_f = (n - 1 - f) / n; the last one has
@@ -711,7 +730,7 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
 #pragma unroll
   for (int j = 0; j < NF; ++j) ia[j] = ib[j] = 0.0;
   for (int r = 0; r < rows; ++r, op += orow) {
-    const AxisTap ty = S.ty_c[r];
+    const AxisTap ty = from_row(S.ty_c[r]);
     if (ty.lo != ya) {
       if (ty.lo == yb) {
 #pragma unroll
@@ -740,7 +759,7 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
     }
     AxisTap tp = ty;
     if (BLEND) {
-      tp = S.ty_p[r];
+      tp = from_row(S.ty_p[r]);
       if (tp.lo != qa) {
         if (tp.lo == qb) {
 #pragma unroll
@@ -768,17 +787,48 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
         qb = tp.hi;
       }
     }
+    if constexpr (kU8) {
+      // uint8 windows: every sample is q / 255 in [0, 1] and every weight pair
+      // sums to 1 within an ulp, so each result is <= 1 + 2^-50 and its float
+      // rounding is <= 1.0f: the upper clip is the identity and is omitted.
+      // A row with fy = 0 (every third row at s = 3, the clamped top row) is
+      // ia * 1 + ib * 0 = ia exactly (ia >= +0), so it skips the vertical mix.
+      if (ty.f == 0.0) {
 #pragma unroll
-    for (int j = 0; j < NF; ++j) {
-      const float ui = f32_clip_hi1(ia[j] * ty.g + ib[j] * ty.f);     // codec.py:235
-      float v = ui;
-      if (j < NQ) {   // codec.py:289-293
-        const double dq = (double)f32_clip_hi1(qva[j] * tp.g + qvb[j] * tp.f);
-        v = f32_clip_hi1(a.alpha[f0 + j] * dq + a.beta[f0 + j] * (double)ui);
-      } else if (j < NB) {
-        v = ui + 0.0f;   // alpha = 0: -0.0 becomes +0.0 as in 0 * prev + cur
+        for (int j = 0; j < NF; ++j) {
+          const float ui = (float)ia[j];
+          float v = ui;
+          if (j < NQ) {
+            const double dq = (double)(float)(qva[j] * tp.g + qvb[j] * tp.f);
+            v = (float)(a.alpha[f0 + j] * dq + a.beta[f0 + j] * (double)ui);
+          }
+          __stcs(op + j * fstride, v);
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < NF; ++j) {
+          const float ui = (float)(ia[j] * ty.g + ib[j] * ty.f);   // codec.py:235
+          float v = ui;
+          if (j < NQ) {
+            const double dq = (double)(float)(qva[j] * tp.g + qvb[j] * tp.f);
+            v = (float)(a.alpha[f0 + j] * dq + a.beta[f0 + j] * (double)ui);
+          }
+          __stcs(op + j * fstride, v);
+        }
       }
-      __stcs(op + j * fstride, v);
+    } else {
+#pragma unroll
+      for (int j = 0; j < NF; ++j) {
+        const float ui = f32_clip_hi1(ia[j] * ty.g + ib[j] * ty.f);     // codec.py:235
+        float v = ui;
+        if (j < NQ) {   // codec.py:289-293
+          const double dq = (double)f32_clip_hi1(qva[j] * tp.g + qvb[j] * tp.f);
+          v = f32_clip_hi1(a.alpha[f0 + j] * dq + a.beta[f0 + j] * (double)ui);
+        } else if (j < NB) {
+          v = ui + 0.0f;   // alpha = 0: -0.0 becomes +0.0 as in 0 * prev + cur
+        }
+        __stcs(op + j * fstride, v);
+      }
     }
   }
 }
@@ -841,9 +891,9 @@ __global__ void __launch_bounds__(kTQ, sizeof(T) == 8 ? 2 : (sizeof(T) == 1 ? SS
   const bool has_prev = kPrev && pd.p_img != nullptr;
   const int rows = min(kBand, a.H - oy0);
   const int qlast = min(q0 + kTQ, a.W * 3) - 1;
-  if (tid < kBand) S.ty_c[tid] = axis_tap(oy0 + min(tid, rows - 1), a.h, a.s);
+  if (tid < kBand) S.ty_c[tid] = to_row(axis_tap(oy0 + min(tid, rows - 1), a.h, a.s));
   else if (tid < 2 * kBand) {
-    if (has_prev) S.ty_p[tid - kBand] = axis_tap(oy0 + min(tid - kBand, rows - 1), pd.h, pd.s);
+    if (has_prev) S.ty_p[tid - kBand] = to_row(axis_tap(oy0 + min(tid - kBand, rows - 1), pd.h, pd.s));
   } else if (tid == 2 * kBand) {
     S.wx0[0] = axis_tap(q0 / 3, a.w, a.s).lo;
     S.wx1[0] = axis_tap(qlast / 3, a.w, a.s).hi;

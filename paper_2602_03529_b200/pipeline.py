@@ -163,18 +163,24 @@ class GopCodec:
         self._id_ring.copy_to(raw.view(np.uint8), self._ids)
 
     # -- sender --------------------------------------------------------
-    def encode(self, frames: torch.Tensor, g: int, drop_k: int = 0) -> None:
-        """K1 + K2 + K3 for frames[:g] ([g, 9, H, W, 3] float32, contiguous)."""
-        self.tokenize(frames, g)
+    def encode(self, frames: torch.Tensor, g: int, drop_k: int = 0,
+               work: torch.Tensor | None = None) -> None:
+        """K1 + K2 + K3 for frames[:g] ([g, 9, H, W, 3] float32, contiguous);
+        `work` ([>= g, 9, h, w, 3] float32) also receives the working frames."""
+        self.tokenize(frames, g, work)
         self.select_and_pack(g, drop_k)
 
-    def tokenize(self, frames: torch.Tensor, g: int) -> None:
-        """K1: downscale + tokenize + similarity."""
+    def tokenize(self, frames: torch.Tensor, g: int, work: torch.Tensor | None = None) -> None:
+        """K1: downscale + tokenize + similarity (+ the working frames when
+        `work` is given: the residual layer's input, no second frame read)."""
         tm = self.timer
         check_gop_tensor(frames, g, self.H, self.W, "frames")
+        if work is not None:
+            check_gop_tensor(work, g, self.h, self.w, "work")
         tm.begin("K1_encode")
-        _lib.call("sst_encode", frames.data_ptr(), g, self.H, self.W, self.s,
-                  self.tok.data_ptr(), self.sim.data_ptr(), _dev.stream())
+        _lib.call("sst_encode_work", frames.data_ptr(), g, self.H, self.W, self.s,
+                  self.tok.data_ptr(), self.sim.data_ptr(),
+                  None if work is None else work.data_ptr(), _dev.stream())
         tm.end("K1_encode")
 
     def select_and_pack(self, g: int, drop_k: int = 0) -> None:

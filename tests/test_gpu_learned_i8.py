@@ -351,14 +351,22 @@ def test_pixels_u8_equals_f32(mode, monkeypatch):
     assert torch.equal(lut[u8.long()], a)
 
 
-@pytest.mark.parametrize("s,n", [(3, 2), (2, 3), (3, 1)])
-def test_upscale_blend9_u8_equals_f32(s, n):
-    """K5-9 over uint8 q frames == K5-9 over the float32 frames q / 255."""
+@pytest.mark.parametrize("s,n,fill", [(3, 2, "random"), (2, 3, "random"), (3, 1, "random"),
+                                      (3, 2, "extreme"), (2, 2, "extreme")])
+def test_upscale_blend9_u8_equals_f32(s, n, fill):
+    """K5-9 over uint8 q frames == K5-9 over the float32 frames q / 255 (the
+    float kernel keeps the reference's upper clip; the uint8 kernel omits it
+    as provably inactive -- "extreme" frames of 0 / 254 / 255 samples hit it)."""
     rng = np.random.default_rng(13)
     G, H, W = 2, 270, 480
     h, w = -(-H // s), -(-W // s)
-    q = torch.from_numpy(rng.integers(0, 256, (G, 9, h, w, 3)).astype(np.uint8)).cuda()
-    qp = torch.from_numpy(rng.integers(0, 256, (G, 9, h, w, 3)).astype(np.uint8)).cuda()
+    if fill == "random":
+        q = torch.from_numpy(rng.integers(0, 256, (G, 9, h, w, 3)).astype(np.uint8)).cuda()
+        qp = torch.from_numpy(rng.integers(0, 256, (G, 9, h, w, 3)).astype(np.uint8)).cuda()
+    else:
+        vals = np.array([0, 254, 255, 255, 255], np.uint8)
+        q = torch.from_numpy(vals[rng.integers(0, 5, (G, 9, h, w, 3))]).cuda()
+        qp = torch.from_numpy(vals[rng.integers(0, 5, (G, 9, h, w, 3))]).cuda()
     lut = torch.arange(256, dtype=torch.float32, device="cuda") / torch.tensor(255.0, device="cuda")
     f, fp = lut[q.long()].contiguous(), lut[qp.long()].contiguous()
     outs = []

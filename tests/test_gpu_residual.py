@@ -220,3 +220,28 @@ def test_residual_properties(rng):
                           R.apply(np.full((16, 16, 3), 0.5, np.float32),
                                   R.dense_delta(sr.indices, sr.qvalues, sr.quant_step, (16, 16, 3))))
     assert RS.raw_residual_rate(1920, 1080, 30) == 1920 * 1080 * 3 * 8 * 30
+
+
+@pytest.mark.parametrize("H,W,s", [(270, 480, 3), (73, 101, 2), (61, 97, 3), (120, 200, 2)])
+def test_encode_work_output_equals_downscale(H, W, s):
+    """K1's optional working-frame output (sst_encode_work) is scale_gop(down)
+    bit for bit (the standalone sst_downscale kernel, itself golden-checked),
+    tokens are unchanged by asking for it; odd sizes exercise the edge
+    replication and the block padding that must not be written."""
+    import torch
+    from paper_2602_03529_b200 import _dev, _lib
+    from paper_2602_03529_b200.pipeline import GopCodec
+    G = 2
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    frames = torch.rand((G, 9, H, W, 3), generator=gen, device="cuda")
+    c = GopCodec(G, H, W, s)
+    c.encode(frames, G, 0)
+    tok0 = c.tok.clone()
+    h, w = -(-H // s), -(-W // s)
+    work = torch.full((G, 9, h, w, 3), -7.0, device="cuda")
+    c.encode(frames, G, 0, work=work)
+    ref = torch.empty_like(work)
+    _lib.call("sst_downscale", frames.data_ptr(), G * 9, H, W, s, ref.data_ptr(), _dev.stream())
+    torch.cuda.synchronize()
+    assert torch.equal(c.tok, tok0)
+    assert torch.equal(work, ref)
