@@ -251,7 +251,7 @@ def quantize_row(vals: np.ndarray):
 
 def pack_row(kind: int, gop_id: int, row: int, values_row: np.ndarray,
              mask_row: np.ndarray, scale: int) -> bytes:
-    """One token-row packet, sealed (transport.py:97-102, 323-358)."""
+    """One token-row packet, sealed (transport.py:97-102, 236-271)."""
     width, channels = values_row.shape
     valid = values_row[np.asarray(mask_row, bool)]
     qmin32, qrange32, payload = quantize_row(valid)
@@ -278,7 +278,7 @@ def wire_size(width: int, channels: int, valid: int | None = None) -> int:
 
 
 def parse(data: bytes) -> dict:
-    """Token-packet parse + validation (transport.py:154-184, _check_seal 64-70)."""
+    """Token-packet parse + validation (transport.py:154-218, _check_seal 64-70)."""
     if len(data) < 4:
         raise OraclePacketError("packet shorter than its checksum")
     body = data[:-4]

@@ -1114,6 +1114,191 @@ __global__ void __launch_bounds__(128, 2)
   if (warp == 0) tc::tmem_dealloc(tmem, 256);
 }
 
+// ---- global causal attention, TMA-pipelined (default) ----------------------------
+// The same arithmetic as k_l8_attn_global, with the key / value tiles brought
+// in by TMA two jobs ahead instead of loaded synchronously by every thread:
+// the 2 x ntiles jobs (pass 1: K tiles for the row max; pass 2: K + V tiles for
+// P and O += P V) rotate through two smem stages, and thread 0 re-arms a stage
+// with job j + 2 as soon as job j's MMAs have consumed it.  The tiles come
+// straight from the [tokens][3 D] qkv rows through a 2-D tensor map with the
+// 128-byte swizzle the UMMA descriptors expect (K-major Q / K, MN-major V);
+// rows past the allowed keys are masked in the softmax as before.  The integer
+// softmax needs the exact row max before any P, so the two passes stay.
+constexpr int AG2_SMEM = 6 * 16384 + 1024 + 64 + 256;
+
+__global__ void __launch_bounds__(128, 2)
+    k_l8_attn_global_tma(const __grid_constant__ CUtensorMap tq, int G, int n, int D, int shift,
+                         const uint8_t* __restrict__ exp_lut, int8_t* __restrict__ out) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint8_t* sQ = smem;                         // [128 q][128 d]            A of S
+  uint8_t* sKV = smem + 16384;                // 2 stages x {K, V} [128][128]
+  uint8_t* sP = smem + 5 * 16384;             // [128 q][128 k] u8         A of O
+  uint64_t* bar = reinterpret_cast<uint64_t*>(smem + 6 * 16384);   // full0 full1 q s o
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bar + 5);
+  uint8_t* lut = smem + 6 * 16384 + 64;
+
+  const int head = blockIdx.y;
+  const int g = blockIdx.z >> 1, t = blockIdx.z & 1;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int qi = blockIdx.x * 128 + tid;
+  const bool valid_q = qi < n;
+  const size_t tok_q = ((size_t)g * 2 + t) * n + qi;
+  const int nkeys = (t + 1) * n;
+  const int ntiles = (nkeys + 127) / 128;
+  const int njobs = 2 * ntiles;
+  const int row0 = g * 2 * n;                 // first token row of this GoP
+  const int xk = D + head * AT_HD, xv = 2 * D + head * AT_HD;
+
+  auto issue = [&](int j) {                   // job j -> stage j & 1
+    const int st = j & 1;
+    const bool p2 = j >= ntiles;
+    const int kt = p2 ? j - ntiles : j;
+    uint8_t* dk = sKV + st * 32768;
+    mbar_expect_tx(&bar[st], p2 ? 32768u : 16384u);
+    tc::tma_load_2d(dk, &tq, xk, row0 + kt * 128, &bar[st]);
+    if (p2) tc::tma_load_2d(dk + 16384, &tq, xv, row0 + kt * 128, &bar[st]);
+  };
+  if (tid == 0) {
+    for (int i = 0; i < 5; ++i) mbar_init(&bar[i], 1);
+    fence_mbar_init();
+    tc::prefetch_tmap(&tq);
+    mbar_expect_tx(&bar[2], 16384u);
+    tc::tma_load_2d(sQ, &tq, head * AT_HD, row0 + t * n + blockIdx.x * 128, &bar[2]);
+    issue(0);
+    if (njobs > 1) issue(1);
+  }
+  if (warp == 0) tc::tmem_alloc(tmem_slot, 256);
+  lut[tid] = exp_lut[tid];
+  lut[tid + 128] = exp_lut[tid + 128];
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  constexpr uint32_t id1 = tc::idesc_i8_s32(128, 128, true, true);
+  constexpr uint32_t id2 = tc::idesc_i8_s32(128, 128, false, true) | (1u << 16);
+  if (tid == 0) mbar_wait(&bar[2], 0);
+  uint32_t ph_s = 0, ph_o = 0;
+  int m = INT_MIN;
+  uint32_t lsum = 0;
+  const int lim = (256 << shift) - 1;
+  for (int j = 0; j < njobs; ++j) {
+    const int st = j & 1;
+    const bool p2 = j >= ntiles;
+    const int kt = p2 ? j - ntiles : j;
+    uint8_t* sK = sKV + st * 32768;
+    if (tid == 0) {
+      mbar_wait(&bar[st], (j >> 1) & 1);
+      const uint64_t ad = tc::smem_desc_sw128(smem_u32(sQ));
+      const uint64_t bd = tc::smem_desc_sw128(smem_u32(sK));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) tc::mma_i8(tmem, ad + 2 * k, bd + 2 * k, id1, k);
+      tc::mma_commit(&bar[3]);
+    }
+    mbar_wait(&bar[3], ph_s);
+    ph_s ^= 1;
+    tc::fence_after_sync();
+    if (!p2) {
+      // pass 1: row max over all allowed keys
+      const bool full = (kt + 1) * 128 <= nkeys;   // every key of the tile allowed
+#pragma unroll 1
+      for (int c = 0; c < 128; c += 32) {
+        float v[32];
+        tc::tmem_ld32(trow + c, v);
+        if (full) {
+          int m2[4] = {m, m, m, m};
+#pragma unroll
+          for (int i = 0; i < 32; ++i) m2[i & 3] = max(m2[i & 3], __float_as_int(v[i]));
+          m = max(max(m2[0], m2[1]), max(m2[2], m2[3]));
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i)
+            if (kt * 128 + c + i < nkeys) m = max(m, __float_as_int(v[i]));
+        }
+      }
+      tc::fence_before_sync();
+      __syncthreads();                        // S read: TMEM S and stage st are free
+      if (tid == 0 && j + 2 < njobs) issue(j + 2);
+      continue;
+    }
+    // pass 2: P = EXP[...], l = sum P, O += P V
+    const bool full = valid_q && (kt + 1) * 128 <= nkeys;
+#pragma unroll 1
+    for (int c = 0; c < 128; c += 32) {
+      float v[32];
+      tc::tmem_ld32(trow + c, v);
+      int e[32];
+      if (full) {
+        // (m - S) >= 0 for every allowed key: min(m - S, lim) >> sh is
+        // min((m - S) >> sh, 255) in one add-min plus a shift
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          e[i] = (int)lut[(uint32_t)min(m - __float_as_int(v[i]), lim) >> shift];
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const bool ok = valid_q && kt * 128 + c + i < nkeys;
+          e[i] = ok ? (int)lut[min((m - __float_as_int(v[i])) >> shift, 255)] : 0;
+        }
+      }
+      uint32_t w[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        w[k] = pack4_satu8(e[4 * k], e[4 * k + 1], e[4 * k + 2], e[4 * k + 3]);
+        lsum = __dp4a(w[k], 0x01010101u, lsum);      // l += the four P bytes
+      }
+#pragma unroll
+      for (int qq = 0; qq < 2; ++qq) {
+        const int jj = (c >> 4) + qq;
+        *reinterpret_cast<uint4*>(sP + tid * 128 + ((jj ^ (tid & 7)) << 4)) =
+            make_uint4(w[4 * qq], w[4 * qq + 1], w[4 * qq + 2], w[4 * qq + 3]);
+      }
+    }
+    fence_proxy_async_smem();
+    tc::fence_before_sync();
+    __syncthreads();                          // P complete, S read: O may accumulate
+    tc::fence_after_sync();
+    if (tid == 0) {
+      const uint64_t ad = tc::smem_desc_sw128(smem_u32(sP));
+      const uint64_t bd = tc::smem_desc_sw128(smem_u32(sK + 16384));
+#pragma unroll
+      for (int k = 0; k < 4; ++k) tc::mma_i8(tmem + 128, ad + 2 * k, bd + 256 * k, id2, (kt | k) != 0);
+      tc::mma_commit(&bar[4]);
+    }
+    mbar_wait(&bar[4], ph_o);                 // sP, stage st and TMEM S free
+    ph_o ^= 1;
+    tc::fence_after_sync();
+    if (tid == 0 && j + 2 < njobs) issue(j + 2);
+  }
+  const int l = (int)lsum;
+  const int l2 = 2 * max(l, 1);
+  const float rcp = 1.0f / (float)l2;
+#pragma unroll 1
+  for (int c = 0; c < 128; c += 32) {
+    float v[32];
+    tc::tmem_ld32(trow + 128 + c, v);
+    if (!valid_q) continue;
+    int o[32];
+#pragma unroll
+    for (int i = 0; i < 32; ++i) {
+      const int q = floor_div_pos(2 * __float_as_int(v[i]) + l, l2, rcp);
+      o[i] = min(max(q, -127), 127);
+    }
+    uint4* op = reinterpret_cast<uint4*>(out + tok_q * D + head * AT_HD + c);
+#pragma unroll
+    for (int qq = 0; qq < 2; ++qq)
+      op[qq] = make_uint4(pack4(o[qq * 16 + 0], o[qq * 16 + 1], o[qq * 16 + 2], o[qq * 16 + 3]),
+                          pack4(o[qq * 16 + 4], o[qq * 16 + 5], o[qq * 16 + 6], o[qq * 16 + 7]),
+                          pack4(o[qq * 16 + 8], o[qq * 16 + 9], o[qq * 16 + 10], o[qq * 16 + 11]),
+                          pack4(o[qq * 16 + 12], o[qq * 16 + 13], o[qq * 16 + 14], o[qq * 16 + 15]));
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 256);
+}
+
 // ---- patchify -------------------------------------------------------------------
 template <int S>
 __global__ void k_l8_patchify(const float* __restrict__ src, int G, int H, int W, int h, int w,
@@ -1541,6 +1726,22 @@ extern "C" int sst_lt8_attn_global(const void* qkv, int G, int Ht, int Wt, int D
   if (n > (1 << 24)) return SST_ERR_ARG;
   dim3 grid((unsigned)((n + 127) / 128), D / l8::AT_HD, 2 * G);
   cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const char* mode = getenv("SST_AG");
+  CUtensorMap tq;
+  memset(&tq, 0, sizeof(tq));
+  if (!(mode && mode[0] == 'o') && 2 * (int64_t)G * n < (1ll << 31) &&
+      make_tmap_u8_2d(&tq, qkv, (uint64_t)3 * D, (uint64_t)2 * G * n, 128)) {
+    static bool attr = false;
+    if (!attr) {
+      SST_CUDA_TRY(cudaFuncSetAttribute(l8::k_l8_attn_global_tma,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, l8::AG2_SMEM));
+      attr = true;
+    }
+    l8::k_l8_attn_global_tma<<<grid, 128, l8::AG2_SMEM, st>>>(tq, G, (int)n, D, shift, exp_lut,
+                                                              static_cast<int8_t*>(out));
+    SST_LAUNCH_CHECK();
+    return SST_OK;
+  }
   SST_CUDA_TRY(cudaFuncSetAttribute(l8::k_l8_attn_global, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     l8::AG_SMEM));
   l8::k_l8_attn_global<<<grid, 128, l8::AG_SMEM, st>>>(static_cast<const int8_t*>(qkv), G, (int)n,
