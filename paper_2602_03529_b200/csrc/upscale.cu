@@ -665,6 +665,13 @@ static int launch_k5_v2(const CUtensorMap& imap, const UpArgs& a, const SstPrevD
 // frames): TMA box rows start on a 16-byte = 16-element boundary, so the
 // pitch covers kWF + 15 elements
 constexpr int kWF9u8 = 160;
+// q/255 table copies: 16 (conflict-free lookups, 32 KB) by default; measured
+// with 48-row bands (scripts/k5_9u8_micro.py, 32 x 1080p GoPs, blend n=2):
+// s=3 1.361 ms (1 copy, 64 rows: 1.350), s=2 1.637 ms (1 copy: 1.818)
+#ifndef SST_K59_LUTC
+#define SST_K59_LUTC 16
+#endif
+constexpr int kLutC = SST_K59_LUTC;
 template <typename T>
 __host__ __device__ constexpr int k59_pitch() { return sizeof(T) == 1 ? kWF9u8 : kWF9; }
 
@@ -685,7 +692,10 @@ template <int kBand, int kP, typename T = float>
 struct Up9fSmem {
   T win[kGop][Up9fGeom<kBand, T>::kWin];
   T winp[kP > 0 ? kP : 1][Up9fGeom<kBand, T>::kWin];   // previous GoP's frames 9-n+f, f < n = kP
-  double lut[sizeof(T) == 1 ? 256 : 1];   // uint8 windows: sample value of q (= float(q / 255))
+  // uint8 windows: sample value of q (= float(q / 255)), kLutC copies
+  // interleaved so that lane l reads copy l % kLutC: with 16 copies entry q of
+  // copy c sits in bank pair c, and a half-warp's 16 lookups never conflict
+  double lut[sizeof(T) == 1 ? 256 * kLutC : 1];
   RowTap ty_c[kBand], ty_p[kBand];
   int wx0[2], wx1[2];
   int xs;                    // current window's column shift (TMA alignment), 0 for cp.async
@@ -704,7 +714,7 @@ __device__ __forceinline__ float* k5_9_land(T* w) {
 // a window sample as the float64 the reference computes with
 template <typename T>
 __device__ __forceinline__ double k59_val(const T* w, int i, const double* lut) {
-  if constexpr (sizeof(T) == 1) return lut[w[i]];
+  if constexpr (sizeof(T) == 1) return lut[w[i] * kLutC];   // lut: this lane's copy
   else return (double)w[i];
 }
 
@@ -715,6 +725,7 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
                                              const AxisTap& txp, int pxl, int pxh) {
   constexpr bool kU8 = sizeof(T) == 1;
   const int tid = threadIdx.x;
+  const double* lutb = S.lut + (kU8 ? (tid & (kLutC - 1)) : 0);
   const int r0 = S.ty_c[0].lo;
   // blended frames f < NB = n: alpha_f = (n - 1 - f) / n; the last one has
   // alpha = 0, i.e. clip(0 * prev + 1 * cur) = cur + 0.0 (exact: prev is
@@ -739,7 +750,7 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
 #pragma unroll
         for (int j = 0; j < NF; ++j) {
           const T* wr = &S.win[f0 + j][(ty.lo - r0) * k59_pitch<T>()];
-          ia[j] = k59_val(wr, xl, S.lut) * tx.g + k59_val(wr, xh, S.lut) * tx.f;     // codec.py:233
+          ia[j] = k59_val(wr, xl, lutb) * tx.g + k59_val(wr, xh, lutb) * tx.f;     // codec.py:233
         }
       }
       ya = ty.lo;
@@ -752,7 +763,7 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
 #pragma unroll
         for (int j = 0; j < NF; ++j) {
           const T* wr = &S.win[f0 + j][(ty.hi - r0) * k59_pitch<T>()];
-          ib[j] = k59_val(wr, xl, S.lut) * tx.g + k59_val(wr, xh, S.lut) * tx.f;
+          ib[j] = k59_val(wr, xl, lutb) * tx.g + k59_val(wr, xh, lutb) * tx.f;
         }
       }
       yb = ty.hi;
@@ -768,7 +779,7 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
 #pragma unroll
           for (int j = 0; j < NQ; ++j) {
             const T* wq = &S.winp[j][(tp.lo - pr0) * k59_pitch<T>()];
-            qva[j] = k59_val(wq, pxl, S.lut) * txp.g + k59_val(wq, pxh, S.lut) * txp.f;
+            qva[j] = k59_val(wq, pxl, lutb) * txp.g + k59_val(wq, pxh, lutb) * txp.f;
           }
         }
         qa = tp.lo;
@@ -781,7 +792,7 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
 #pragma unroll
           for (int j = 0; j < NQ; ++j) {
             const T* wq = &S.winp[j][(tp.hi - pr0) * k59_pitch<T>()];
-            qvb[j] = k59_val(wq, pxl, S.lut) * txp.g + k59_val(wq, pxh, S.lut) * txp.f;
+            qvb[j] = k59_val(wq, pxl, lutb) * txp.g + k59_val(wq, pxh, lutb) * txp.f;
           }
         }
         qb = tp.hi;
@@ -906,7 +917,13 @@ __global__ void __launch_bounds__(kTQ, sizeof(T) == 8 ? 2 : (sizeof(T) == 1 ? SS
     S.wx0[1] = axis_tap(q0 / 3, pd.w, pd.s).lo;
     S.wx1[1] = axis_tap(qlast / 3, pd.w, pd.s).hi;
   }
-  if (kU8) S.lut[tid] = (double)__fdiv_rn((float)tid, 255.0f);   // kTQ = 256 threads
+  if (kU8) {                                   // kTQ = 256 threads; consecutive stores
+#pragma unroll
+    for (int k = 0; k < kLutC; ++k) {
+      const int e = k * kTQ + tid;
+      S.lut[e] = (double)__fdiv_rn((float)(e / kLutC), 255.0f);
+    }
+  }
   __syncthreads();
 
   // ---- load phase ----
@@ -1289,9 +1306,10 @@ extern "C" int sst_upscale_blend9_u8(const uint8_t* img, int G, int h, int w, in
   // kernel's 16.  Measured (scripts/k5_9u8_micro.py, 32 x 1080p GoPs, s=3,
   // without / with blend n=2): 16 rows 1.500 / 1.696 ms, 32 rows 1.275 /
   // 1.490, 48 rows 1.240 / 1.452, 64 rows 1.257 / 1.416 (s=2: 1.903 / 2.091
-  // -> 1.545 / 1.812).
+  // -> 1.545 / 1.812).  With the 16-copy table (32 KB more per CTA) 48 rows
+  // keep 3 CTAs per SM: s=3 1.216 / 1.361, s=2 1.325 / 1.637 ms.
   const char* bs = getenv("SST_K59_U8_BAND");
-  const int band = bs ? atoi(bs) : 64;
+  const int band = bs ? atoi(bs) : (kLutC > 1 ? 48 : 64);
   auto go = [&](auto tag) -> int {
     constexpr int B = decltype(tag)::value;
     const bool t = make_tmap_u8_3d(&imap, img, (uint64_t)w * 3, (uint64_t)h, (uint64_t)G * kGop,
@@ -1301,6 +1319,7 @@ extern "C" int sst_upscale_blend9_u8(const uint8_t* img, int G, int h, int w, in
   };
   if (band == 24) return go(std::integral_constant<int, 24>{});
   if (band == 32) return go(std::integral_constant<int, 32>{});
+  if (band == 40) return go(std::integral_constant<int, 40>{});
   if (band == 48) return go(std::integral_constant<int, 48>{});
   if (band == 64) return go(std::integral_constant<int, 64>{});
   const bool tma_in = make_tmap_u8_3d(&imap, img, (uint64_t)w * 3, (uint64_t)h, (uint64_t)G * kGop,
