@@ -10,6 +10,7 @@
 // upscale, P upscale and -- for boundary frames -- the previous GoP's P
 // upscale recomputed from its small working image instead of re-reading two
 // full-resolution frames) and streams the 9 frames out.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 
@@ -81,6 +82,58 @@ __device__ __forceinline__ double clip_hi1(double x) { return x > 1.0 ? 1.0 : x;
 // is bit-identical (including -0.0) and costs one FMNMX instead of a DSETP and
 // two FSELs on the 64-bit value.
 __device__ __forceinline__ float f32_clip_hi1(double x) { return fminf((float)x, 1.0f); }
+
+// Blend of boundary frame f (0-based) of a width-kN blend,
+// clip(alpha*q + (1-alpha)*u) with alpha = (kN-1-f)/kN (codec.py:289-293), for
+// q, u the float32 upscaled samples (in [0, 1], possibly -0.0).  Two weights
+// are evaluated in float arithmetic with bit-identical results:
+//  * alpha = 0: 0*q + 1*u is exact in either precision; fmaf(0, q, u) keeps
+//    IEEE's signed-zero rules (-0 + -0 = -0, -0 + +0 = +0).
+//  * alpha = 1/2: 0.5q + 0.5u = (q+u)/2.  When the exponents of q and u are
+//    within 28 the float64 sum is exact, so the reference's result is
+//    round_f32((q+u)/2); otherwise the smaller addend is < ulp32(larger)/32
+//    and both roundings return the larger one / 2.  round_f32((q+u)/2) =
+//    round_f32(q+u) * 0.5: binary scaling commutes with rounding while the
+//    half is normal, and when q+u < 2^-125 the float sum is exact (both are
+//    multiples of 2^-149 below the first binade whose ulp exceeds that) and
+//    the float multiply rounds the exact half once.  Signed zeros follow the
+//    same IEEE rules in both.  The sum is <= 1: the upper clip is inactive.
+// Other weights (n = 3, 4: 2/3, 3/4, ...) stay in float64.
+template <int kN, int f>
+__device__ __forceinline__ float blend_w(float q, float u, double alpha, double beta) {
+  constexpr int num = kN - 1 - f;
+  if constexpr (num == 0) {
+    return __fmaf_rn(0.0f, q, u);
+  } else if constexpr (2 * num == kN) {
+    return __fmul_rn(__fadd_rn(q, u), 0.5f);
+  } else {
+    return f32_clip_hi1(alpha * (double)q + beta * (double)u);
+  }
+}
+
+// A per-thread copy of a uniform 32-bit value: ptxas keeps it in a vector
+// register instead of a uniform one, so `base + f * v` below is ONE
+// IMAD.WIDE per address (instead of a uniform-to-vector move plus the
+// multiply-add, or a 64-bit add pair, per frame store).
+__device__ __forceinline__ int opaque_i32(int v) {
+  int r;
+  asm volatile("{ .reg .u32 t; mov.u32 t, %%tid.x; and.b32 t, t, 0x80000000; or.b32 %0, %1, t; }"
+               : "=r"(r) : "r"(v));
+  return r;
+}
+// element f * fs past p (fs < 2^31, 64-bit product)
+__device__ __forceinline__ float* frame_ptr(float* p, int fs, int f) {
+  return reinterpret_cast<float*>(reinterpret_cast<char*>(p) + (int64_t)fs * (int64_t)(4 * f));
+}
+
+// blend_w with the frame index a run-time value (folded once unrolled)
+template <int kN>
+__device__ __forceinline__ float blend_rt(int f, float q, float u, double alpha, double beta) {
+  const int num = kN - 1 - f;
+  if (num == 0) return __fmaf_rn(0.0f, q, u);
+  if (2 * num == kN) return __fmul_rn(__fadd_rn(q, u), 0.5f);
+  return f32_clip_hi1(alpha * (double)q + beta * (double)u);
+}
 
 __device__ __forceinline__ float blend_px(float prev, float curr, double alpha) {
   double v = alpha * (double)prev + (1.0 - alpha) * (double)curr;   // codec.py:293
@@ -537,7 +590,7 @@ __global__ void __launch_bounds__(kV2Threads)
   double ia[2] = {0, 0}, pa[2] = {0, 0}, ib[2] = {0, 0}, pb[2] = {0, 0};
   double qva[2] = {0, 0}, qvb[2] = {0, 0};
   const int64_t orow = (int64_t)a.W * 3;
-  const int64_t fstride = (int64_t)a.H * orow;
+  const int fsv = opaque_i32(a.H * a.W * 3);       // frame stride (elements)
   float* obase = a.out + ((int64_t)g * kGop * a.H + oy0) * orow + qa0;
   for (int r = 0; r < rows; ++r, obase += orow) {
     const AxisTap ty = from_row(S.ty_c[r]);
@@ -608,20 +661,21 @@ __global__ void __launch_bounds__(kV2Threads)
       }
 #pragma unroll
       for (int u = 0; u < 2; ++u) {            // codec.py:289-293
-        const double dq = (double)f32_clip_hi1(qva[u] * tp.g + qvb[u] * tp.f);
-        fv[0][u] = f32_clip_hi1(a.alpha[0] * dq + a.beta[0] * (double)ui[u]);
-        const double dp = (double)up[u];
-#pragma unroll
-        for (int f = 1; f < kN; ++f) fv[f][u] = f32_clip_hi1(a.alpha[f] * dq + a.beta[f] * dp);
+        const float qf = f32_clip_hi1(qva[u] * tp.g + qvb[u] * tp.f);
+        fv[0][u] = blend_w<kN, 0>(qf, ui[u], a.alpha[0], a.beta[0]);
+        if constexpr (kN > 1) fv[kN > 1 ? 1 : 0][u] = blend_w<kN, 1>(qf, up[u], a.alpha[1], a.beta[1]);
+        if constexpr (kN > 2) fv[kN > 2 ? 2 : 0][u] = blend_w<kN, 2>(qf, up[u], a.alpha[2], a.beta[2]);
+        if constexpr (kN > 3) fv[kN > 3 ? 3 : 0][u] = blend_w<kN, 3>(qf, up[u], a.alpha[3], a.beta[3]);
       }
     }
     if (col_ok) {
+      // frame f at obase + f * fsv: one IMAD.WIDE per store address
       __stcs(reinterpret_cast<float2*>(obase), make_float2(fv[0][0], fv[0][1]));
 #pragma unroll
       for (int f = 1; f < kGop; ++f) {
         const float2 v = (has_prev && f < kN) ? make_float2(fv[f < kN ? f : 0][0], fv[f < kN ? f : 0][1])
                                               : make_float2(up[0], up[1]);
-        __stcs(reinterpret_cast<float2*>(obase + f * fstride), v);
+        __stcs(reinterpret_cast<float2*>(frame_ptr(obase, fsv, f)), v);
       }
     }
   }
@@ -632,7 +686,14 @@ static int launch_k5_v2(const CUtensorMap& imap, const UpArgs& a, const SstPrevD
                         int blend_n, cudaStream_t st) {
   dim3 grid(ceil_div(a.W * 3, kTQ), ceil_div(a.H, BAND), a.G);
   if (grid.y > 65535) return SST_ERR_ARG;
-  const int smem = (int)sizeof(UpTmaSmem<BAND>);
+  // Residency capped at 4 CTAs/SM by the dynamic smem request (54 KB; the
+  // kernel needs 18 KB and 72 registers would allow 7): K5 is bound by its
+  // DRAM write stream, and fewer CTAs in flight keep the concurrently written
+  // rows of the 9 frames closer together.  Measured in bench.py (64 x 1080p
+  // streams, K5 ms per 32-GoP launch): 7/SM 1.248, 5/SM 1.232, 4/SM 1.225,
+  // 3/SM 1.255.  SST_K5_SMEM overrides the request (A/B).
+  const char* es = getenv("SST_K5_SMEM");
+  const int smem = std::max((int)sizeof(UpTmaSmem<BAND>), es ? atoi(es) : 54 * 1024);
   auto kern = k_upscale_blend_v2<BAND, false, 1>;
   if (prev) {
     switch (blend_n) {
@@ -718,6 +779,17 @@ __device__ __forceinline__ double k59_val(const T* w, int i, const double* lut) 
   else return (double)w[i];
 }
 
+// K5-9, float windows, the alpha = 0 blend frame of a -0.0 current sample:
+// 0 * prev + (-0.0) keeps the sign of 0 * prev (codec.py:289-293); prev is
+// the previous GoP's frame 8 upscaled at this output sample
+__device__ __noinline__ float k59_zero_blend(const UpArgs& a, int g, const RowTap& rt, const AxisTap& txp,
+                                             int q) {
+  const SstPrevDesc pd = a.prev[g];
+  const float* img = pd.p_img + (int64_t)(kGop - 1) * pd.h * pd.w * 3;
+  const float qf = f32_clip_hi1(bilerp(img, pd.w, from_row(rt), txp, q % 3));
+  return __fmaf_rn(0.0f, qf, -0.0f);
+}
+
 template <int kBand, int kP, int NF, int NB, typename T>
 __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const UpArgs& a, int g,
                                              int f0, int q0, int oy0, int rows,
@@ -734,7 +806,7 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
   constexpr bool BLEND = NQ > 0;
   const int pr0 = BLEND ? S.ty_p[0].lo : 0;
   const int64_t orow = (int64_t)a.W * 3;
-  const int64_t fstride = (int64_t)a.H * orow;
+  const int fsv = opaque_i32(a.H * a.W * 3);     // frame stride: one IMAD.WIDE per store
   float* op = a.out + ((int64_t)(g * kGop + f0) * a.H + oy0) * orow + q0 + tid;
   int ya = -1, yb = -1, qa = -1, qb = -1;
   double ia[NF], ib[NF], qva[BLEND ? NQ : 1], qvb[BLEND ? NQ : 1];
@@ -809,22 +881,16 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
         for (int j = 0; j < NF; ++j) {
           const float ui = (float)ia[j];
           float v = ui;
-          if (j < NQ) {
-            const double dq = (double)(float)(qva[j] * tp.g + qvb[j] * tp.f);
-            v = (float)(a.alpha[f0 + j] * dq + a.beta[f0 + j] * (double)ui);
-          }
-          __stcs(op + j * fstride, v);
+          if (j < NQ) v = blend_rt<NB>(j, (float)(qva[j] * tp.g + qvb[j] * tp.f), ui, a.alpha[j], a.beta[j]);
+          __stcs(frame_ptr(op, fsv, j), v);
         }
       } else {
 #pragma unroll
         for (int j = 0; j < NF; ++j) {
           const float ui = (float)(ia[j] * ty.g + ib[j] * ty.f);   // codec.py:235
           float v = ui;
-          if (j < NQ) {
-            const double dq = (double)(float)(qva[j] * tp.g + qvb[j] * tp.f);
-            v = (float)(a.alpha[f0 + j] * dq + a.beta[f0 + j] * (double)ui);
-          }
-          __stcs(op + j * fstride, v);
+          if (j < NQ) v = blend_rt<NB>(j, (float)(qva[j] * tp.g + qvb[j] * tp.f), ui, a.alpha[j], a.beta[j]);
+          __stcs(frame_ptr(op, fsv, j), v);
         }
       }
     } else {
@@ -833,12 +899,14 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
         const float ui = f32_clip_hi1(ia[j] * ty.g + ib[j] * ty.f);     // codec.py:235
         float v = ui;
         if (j < NQ) {   // codec.py:289-293
-          const double dq = (double)f32_clip_hi1(qva[j] * tp.g + qvb[j] * tp.f);
-          v = f32_clip_hi1(a.alpha[f0 + j] * dq + a.beta[f0 + j] * (double)ui);
+          v = blend_rt<NB>(j, f32_clip_hi1(qva[j] * tp.g + qvb[j] * tp.f), ui, a.alpha[j], a.beta[j]);
         } else if (j < NB) {
-          v = ui + 0.0f;   // alpha = 0: -0.0 becomes +0.0 as in 0 * prev + cur
+          // alpha = 0: 0 * prev + cur = cur, except that -0.0 + -0.0 stays
+          // -0.0: a -0.0 sample takes the previous GoP's frame 8 from global
+          // memory for its sign (its window is not staged)
+          v = __float_as_uint(ui) == 0x80000000u ? k59_zero_blend(a, g, S.ty_p[r], txp, q0 + tid) : ui + 0.0f;
         }
-        __stcs(op + j * fstride, v);
+        __stcs(frame_ptr(op, fsv, j), v);
       }
     }
   }
@@ -1032,6 +1100,7 @@ static int launch_k5_9f(const CUtensorMap& imap, const UpArgs& a, const SstPrevD
       default: kern = k_upscale9f<BAND, true, 4, LOAD, T>; smem = sizeof(Up9fSmem<BAND, 3, T>); break;
     }
   }
+  if (const char* es = getenv("SST_K59_SMEM")) smem = std::max(smem, atoi(es));   // A/B: cap CTAs/SM
   SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   kern<<<grid, kTQ, smem, st>>>(imap, a);
   SST_LAUNCH_CHECK();
