@@ -117,6 +117,89 @@ __global__ void __launch_bounds__(128) k_frame_major(float* out, int H, int W3) 
   for (int r = 0; r < rows; ++r)
     __stcs(reinterpret_cast<float2*>(base + (long)r * W3), make_float2(0.5f, 0.5f));
 }
+// k frames per CTA: blockIdx.z = g * ceil(9/k) + j covers frames j*k .. j*k+k-1
+template <int K>
+__global__ void __launch_bounds__(128) k_frame_group(float* out, int H, int W3) {
+  constexpr int NJ = (9 + K - 1) / K;
+  const int q = (blockIdx.x * 128 + threadIdx.x) * 2;
+  const int y0 = blockIdx.y * 16;
+  if (q >= W3) return;
+  const int g = blockIdx.z / NJ, j = blockIdx.z % NJ;
+  const long fs = (long)H * W3;
+  float* base = out + ((long)g * 9 + j * K) * fs + (long)y0 * W3 + q;
+  const int rows = min(16, H - y0);
+  const int nf = min(K, 9 - j * K);
+  for (int r = 0; r < rows; ++r)
+    for (int f = 0; f < nf; ++f)
+      __stcs(reinterpret_cast<float2*>(base + f * fs + (long)r * W3), make_float2(0.5f, 0.5f));
+}
+// the band pattern preceded, in every CTA, by a coalesced float4 read of
+// `rd` bytes at offset (CTA index * rd) modulo the source size (`wrap`):
+// K5's DRAM read/write mix without its arithmetic
+__global__ void __launch_bounds__(128) k_read_then_bands(float* out, const float4* src, long wrap4, int rd4,
+                                                         int H, int W3) {
+  __shared__ float4 buf[1536];
+  const long cta = ((long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  const long off = (cta * rd4) % wrap4;
+  for (int i = threadIdx.x; i < rd4; i += 128) buf[i] = src[off + i];
+  __syncthreads();
+  const int q = (blockIdx.x * 128 + threadIdx.x) * 2;
+  const int y0 = blockIdx.y * 16, g = blockIdx.z;
+  if (q >= W3) return;
+  const long fs = (long)H * W3;
+  float* base = out + (long)g * 9 * fs + (long)y0 * W3 + q;
+  const int rows = min(16, H - y0);
+  const float v = buf[threadIdx.x].x;
+  for (int r = 0; r < rows; ++r)
+    for (int f = 0; f < 9; ++f)
+      __stcs(reinterpret_cast<float2*>(base + f * fs + (long)r * W3), make_float2(v, v));
+}
+// ... with the reads batched: every PF-th CTA bulk-prefetches into L2 the
+// reads of the PF CTAs starting LA CTAs ahead (cp.async.bulk.prefetch.L2),
+// so DRAM sees a few large read bursts instead of a read per CTA
+__global__ void __launch_bounds__(128) k_read_then_bands_pf(float* out, const float4* src, long wrap4, int rd4,
+                                                            int H, int W3, int pf, int la) {
+  __shared__ float4 buf[1536];
+  const long cta = ((long)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  if (threadIdx.x == 0 && cta % pf == 0) {
+    const long first = cta + la;
+    for (long c = first; c < first + pf; c += 16) {
+      const long o = (c * rd4) % wrap4;
+      const long n = min((long)16 * rd4, wrap4 - o) * 16;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src + o), "r"((unsigned)n) : "memory");
+    }
+  }
+  const long off = (cta * rd4) % wrap4;
+  for (int i = threadIdx.x; i < rd4; i += 128) buf[i] = src[off + i];
+  __syncthreads();
+  const int q = (blockIdx.x * 128 + threadIdx.x) * 2;
+  const int y0 = blockIdx.y * 16, g = blockIdx.z;
+  if (q >= W3) return;
+  const long fs = (long)H * W3;
+  float* base = out + (long)g * 9 * fs + (long)y0 * W3 + q;
+  const int rows = min(16, H - y0);
+  const float v = buf[threadIdx.x].x;
+  for (int r = 0; r < rows; ++r)
+    for (int f = 0; f < 9; ++f)
+      __stcs(reinterpret_cast<float2*>(base + f * fs + (long)r * W3), make_float2(v, v));
+}
+void rdbpf(torch::Tensor out, torch::Tensor src, int64_t H, int64_t W3, int64_t G, int64_t rd_bytes,
+           int64_t wrap_bytes, int64_t pf, int64_t la) {
+  dim3 grid((W3 / 2 + 127) / 128, (H + 15) / 16, G);
+  k_read_then_bands_pf<<<grid, 128>>>(out.data_ptr<float>(), reinterpret_cast<const float4*>(src.data_ptr<float>()),
+                                      wrap_bytes / 16, (int)(rd_bytes / 16), H, W3, (int)pf, (int)la);
+}
+void rdb(torch::Tensor out, torch::Tensor src, int64_t H, int64_t W3, int64_t G, int64_t rd_bytes, int64_t wrap_bytes) {
+  dim3 grid((W3 / 2 + 127) / 128, (H + 15) / 16, G);
+  k_read_then_bands<<<grid, 128>>>(out.data_ptr<float>(), reinterpret_cast<const float4*>(src.data_ptr<float>()),
+                                   wrap_bytes / 16, (int)(rd_bytes / 16), H, W3);
+}
+void fgrp(torch::Tensor out, int64_t H, int64_t W3, int64_t G, int64_t k) {
+  dim3 grid((W3 / 2 + 127) / 128, (H + 15) / 16, 1);
+  if (k == 2) { grid.z = G * 5; k_frame_group<2><<<grid, 128>>>(out.data_ptr<float>(), H, W3); }
+  if (k == 3) { grid.z = G * 3; k_frame_group<3><<<grid, 128>>>(out.data_ptr<float>(), H, W3); }
+  if (k == 5) { grid.z = G * 2; k_frame_group<5><<<grid, 128>>>(out.data_ptr<float>(), H, W3); }
+}
 void fmaj(torch::Tensor out, int64_t H, int64_t W3, int64_t G, int64_t band) {
   if (band == 16) {
     dim3 grid((W3 / 2 + 127) / 128, (H + 15) / 16, G * 9);
@@ -152,8 +235,11 @@ void bands(torch::Tensor out, int64_t H, int64_t W3, int64_t G, int64_t v) {
 """
 m = load_inline("wpat2", cpp_sources="void bands(torch::Tensor out, int64_t H, int64_t W3, int64_t G, int64_t v);"
                 "void ldst(torch::Tensor out, torch::Tensor img, int64_t H, int64_t W3, int64_t G, int64_t pf, int64_t ctas);"
-                "void fmaj(torch::Tensor out, int64_t H, int64_t W3, int64_t G, int64_t band);",
-                cuda_sources=src, functions=["bands", "ldst", "fmaj"],
+                "void fmaj(torch::Tensor out, int64_t H, int64_t W3, int64_t G, int64_t band);"
+                "void fgrp(torch::Tensor out, int64_t H, int64_t W3, int64_t G, int64_t k);"
+                "void rdb(torch::Tensor out, torch::Tensor src, int64_t H, int64_t W3, int64_t G, int64_t rd_bytes, int64_t wrap_bytes);"
+                "void rdbpf(torch::Tensor out, torch::Tensor src, int64_t H, int64_t W3, int64_t G, int64_t rd_bytes, int64_t wrap_bytes, int64_t pf, int64_t la);",
+                cuda_sources=src, functions=["bands", "ldst", "fmaj", "fgrp", "rdb", "rdbpf"],
                 extra_cuda_cflags=["-gencode", "arch=compute_100a,code=sm_100a", "-O3"])
 G, H, W = 32, 1080, 1920
 out = torch.empty((G, 9, H, W, 3), device="cuda")
@@ -177,6 +263,21 @@ def t(fn, n=10):
     return e0.elapsed_time(e1) / n
 
 
+src_big = torch.rand(64 << 20, device="cuda")      # 256 MB: reads come from DRAM
+import sys
+if "--reads" in sys.argv:
+    for rep in range(2):
+        ms = t(lambda: m.bands(out, H, W * 3, G, 0))
+        print(f"{'band pattern, no reads':48s}: {ms:.3f} ms  {nbytes / ms / 1e6:.0f} GB/s")
+        for rd in (3584,):
+            for wrap in (1 << 20, 256 << 20):
+                ms = t(lambda: m.rdb(out, src_big, H, W * 3, G, rd, wrap))
+                print(f"{'+ %d B read per CTA from %d MB' % (rd, wrap >> 20):48s}: {ms:.3f} ms  {nbytes / ms / 1e6:.0f} GB/s")
+            for pf in (64, 256, 1024):
+                for la in (1024, 4096):
+                    ms = t(lambda: m.rdbpf(out, src_big, H, W * 3, G, rd, 256 << 20, pf, la))
+                    print(f"{'  L2 bulk prefetch: every %d CTAs, %d ahead' % (pf, la):48s}: {ms:.3f} ms  {nbytes / ms / 1e6:.0f} GB/s")
+    sys.exit(0)
 for rep in range(2):
     for v, nm in enumerate(names):
         ms = t(lambda: m.bands(out, H, W * 3, G, v))
@@ -186,6 +287,9 @@ for rep in range(2):
     for band in (16, 32, 64):
         ms = t(lambda: m.fmaj(out, H, W * 3, G, band))
         print(f"{'frame-major CTAs, band %d' % band:48s}: {ms:.3f} ms  {nbytes / ms / 1e6:.0f} GB/s")
+    for k in (2, 3, 5):
+        ms = t(lambda: m.fgrp(out, H, W * 3, G, k))
+        print(f"{'%d frames per CTA, band 16' % k:48s}: {ms:.3f} ms  {nbytes / ms / 1e6:.0f} GB/s")
     ms = t(lambda: m.ldst(out, img, H, W * 3, G, 0, 0))
     print(f"{'load windows, then store (one band per CTA)':48s}: {ms:.3f} ms  {nbytes / ms / 1e6:.0f} GB/s")
     for k in (4, 6, 8, 12):
