@@ -156,6 +156,15 @@ SST_API int sst_encode(const float* frames, int G, int H, int W, int s, double* 
 SST_API int sst_encode_work(const float* frames, int G, int H, int W, int s, double* tok,
                double* sim, float* work, void* stream);
 
+/* sst_encode_work over raw-rgb24 frames: frames [G][9][H][W][3] uint8, each
+ * byte q standing for the float32 sample float32(q) / 255 that
+ * load_raw_video builds from it (video.py:130-135) -- the reference CLI's
+ * encode input (cli.py:52-61,78-92).  Tokens, similarities and the optional
+ * float32 working frames are those of sst_encode_work on the converted
+ * frames, bit for bit. */
+SST_API int sst_encode_u8(const uint8_t* frames, int G, int H, int W, int s, double* tok,
+               double* sim, float* work, void* stream);
+
 /* decode_gop (codec.py:160-186): IDCT of I and P tokens, crop to (h, w),
  * clip, conceal invalid P blocks with I blocks.
  *   i_tok, p_tok: [G][H'][W'][12] (any batch stride via tok_stride elements);
@@ -250,6 +259,13 @@ SST_API int sst_unpack_decode(const uint8_t* buf, const int64_t* off, SstPacketI
  *   out: [G][9][H][W][3]. */
 SST_API int sst_upscale_blend(const float* img, int G, int h, int w, int s, int H, int W,
                       const SstPrevDesc* prev, int blend_n, float* out, void* stream);
+
+/* sst_upscale_blend with raw-rgb24 output: every output sample v is written
+ * as the byte write_raw_video stores for it (video.py:139-143,
+ * np.rint(v * 255.0).astype(np.uint8) on the float32 frame), i.e. the
+ * reference CLI's decode output (cli.py:181).  out: [G][9][H][W][3] uint8. */
+SST_API int sst_upscale_blend_u8(const float* img, int G, int h, int w, int s, int H, int W,
+                      const SstPrevDesc* prev, int blend_n, uint8_t* out, void* stream);
 
 /* ---- residual enhancement layer and range coder (f2) ------- */
 

@@ -463,6 +463,21 @@ def inter_frame_consistency(frames) -> float:
 
 
 # ---------------------------------------------------------------------------
+# raw-rgb24 boundary (the reference CLI's file formats, cli.py:52-61,181)
+
+def frames_from_rgb24(raw: np.ndarray) -> np.ndarray:
+    """load_raw_video's sample conversion (video.py:130-135): uint8 q ->
+    float32(q) / 255 (a float32 array over a Python float stays float32)."""
+    return np.asarray(raw, dtype=np.uint8).astype(np.float32) / 255.0
+
+
+def rgb24_from_frames(frames: np.ndarray) -> np.ndarray:
+    """write_raw_video's quantiser (video.py:139-143): the float32 product
+    v * 255, rounded half to even, as uint8."""
+    return np.rint(np.asarray(frames, dtype=np.float32) * 255.0).astype(np.uint8)
+
+
+# ---------------------------------------------------------------------------
 # full per-GoP pipeline (BASELINE.md §2 composition, session.py:134-170,323-348)
 
 def pipeline_gop(frames9: np.ndarray, s: int, gop_id: int = 0, drop_rate: float = 0.0,

@@ -72,6 +72,7 @@ SIGNATURES = {
     "sst_blend": (_I, [_P, _P, _I, _I, _I, _I, _P, _P]),
     "sst_encode": (_I, [_P, _I, _I, _I, _I, _P, _P, _P]),
     "sst_encode_work": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P]),
+    "sst_encode_u8": (_I, [_P, _I, _I, _I, _I, _P, _P, _P, _P]),
     "sst_decode": (_I, [_P, _P, _L, _P, _I, _I, _I, _I, _I, _P, _P]),
     "sst_similarity": (_I, [_P, _P, _L, _I, _P, _P]),
     "sst_topk_mask": (_I, [_P, _I, _L, _P, _P, _P, _P]),
@@ -84,6 +85,7 @@ SIGNATURES = {
     "sst_unpack_decode_workspace": (_L, [_I, _I, _I]),
     "sst_unpack_decode": (_I, [_P, _P, _P, _P, _L, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
     "sst_upscale_blend": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P]),
+    "sst_upscale_blend_u8": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P]),
     "sst_mse": (_I, [_P, _P, _L, _L, _P, _P]),
     "sst_mean_diff": (_I, [_P, _P, _L, _L, _I, _P, _P]),
     "sst_similarity_gop": (_I, [_P, _I, _L, _I, _P, _P]),

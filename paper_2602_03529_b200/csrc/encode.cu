@@ -233,6 +233,258 @@ __global__ void __launch_bounds__(EncCfg<S>::NT)
   }
 }
 
+// ---- K1 over raw-rgb24 frames (load_raw_video fused) ----
+//
+// The reference CLI ingests raw-rgb24 files: every byte q becomes the float32
+// sample f(q) = float32(q) / 255 (video.py:130-135; a float32 array divided by
+// a Python float stays float32, correctly rounded).  K1u8 reads the bytes --
+// a quarter of the float32 frames' HBM traffic -- and box-filters f(q)
+// exactly: f(q) >= 2^-8 has its lowest set bit at >= 2^-31 and f(q) <= 1, so
+// F(q) = f(q) * 2^31 is an integer < 2^31 + 1; the s x s window sum of F is
+// exact in uint64 and (double)sum * 2^-31 is the float64 sum numpy forms
+// (every partial sum of <= 9 such values is exact in float64, so numpy's
+// summation order does not matter).  F comes from a 256-entry table in
+// shared memory replicated 32x (entry q of copy c at word 32q + c, lane l
+// reads copy l): the lookups are bank-conflict free.
+//
+// Work mapping: each thread box-filters a QUAD of 4 horizontally adjacent
+// working pixels of one working row, so the quad's s rows x 12s bytes are
+// word-aligned in the tile and read as 3s 32-bit words.  A CTA covers one
+// token row x 8 token columns (128 threads); the 9 frame tiles stream
+// through a cp.async ring (16-byte copies) with a padded row pitch.
+constexpr int kU8Tpb = 8;
+
+template <int S>
+struct EncU8Cfg {
+  static constexpr int TPB = kU8Tpb;                // tokens per CTA
+  static constexpr int R = 8 * S;                   // full-res rows per tile
+  static constexpr int IN = TPB * 8 * S * 3;        // bytes per tile row
+  static constexpr int INP = IN + 16;               // padded pitch
+  static constexpr int NQ = TPB * 8 / 4;            // quads per working row
+  static constexpr int NT = 8 * NQ;                 // threads (128)
+  static constexpr int QB = 12 * S;                 // bytes per quad row segment
+  static constexpr int NST = S == 3 ? 3 : 4;        // ring depth
+  static constexpr int TILE = R * INP;              // bytes per ring stage
+  static constexpr int RING = NST * TILE;
+  static constexpr int IMG_D = 2 * 8 * 8 * TPB * 3;
+  static constexpr int S1_D = 2 * TPB * 3 * 3 * 8;
+  static constexpr int TOK_D = 2 * TPB * kChannels;
+  static constexpr int DCT_BYTES = (IMG_D + S1_D + TOK_D) * 8;
+  static constexpr int MAIN = ((RING > DCT_BYTES ? RING : DCT_BYTES) + 127) / 128 * 128;
+  static constexpr int LUT_WORDS = 256 * 32;
+  static constexpr int SMEM = MAIN + LUT_WORDS * 4;
+};
+
+struct EncU8Args {
+  const uint8_t* frames;
+  int G, H, W, h, w, Ht, Wt;
+  double* tok;
+  double* sim;
+  float* work;
+  int aligned;   // frames and rows 16-byte aligned: cp.async 16-byte tile copies
+};
+
+template <int S>
+__global__ void __launch_bounds__(EncU8Cfg<S>::NT) k_encode_u8(EncU8Args a) {
+  using C = EncU8Cfg<S>;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  uint8_t* ring = smem_raw;
+  uint32_t* lut = reinterpret_cast<uint32_t*>(smem_raw + C::MAIN);
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int tx0 = blockIdx.x * C::TPB;
+  const int ty = blockIdx.y;
+  const int g = blockIdx.z;
+  const int row0 = ty * C::R;
+  const int col0 = tx0 * 8 * S;
+  const size_t frame_bytes = (size_t)a.H * a.W * 3;
+  const uint8_t* gop = a.frames + (size_t)g * kGop * frame_bytes;
+
+  // tile f -> ring stage f % NST: rows row0..row0+R-1 (< H), bytes col0*3..
+  auto load_tile = [&](int f) {
+    uint8_t* dst = ring + (f % C::NST) * C::TILE;
+    const uint8_t* src = gop + (size_t)f * frame_bytes;
+    if (a.aligned) {
+      constexpr int kChunks = C::IN / 16;
+      for (int e = tid; e < C::R * kChunks; e += C::NT) {
+        const int r = e / kChunks, c = e % kChunks;
+        const int gr = row0 + r, gb = col0 * 3 + c * 16;
+        if (gr < a.H && gb < a.W * 3)      // W*3 % 16 == 0: chunks are whole
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + r * C::INP + c * 16)),
+                       "l"(src + (size_t)gr * a.W * 3 + gb)
+                       : "memory");
+      }
+    } else {
+      for (int e = tid; e < C::R * C::IN; e += C::NT) {
+        const int r = e / C::IN, c = e % C::IN;
+        const int gr = row0 + r, gb = col0 * 3 + c;
+        if (gr < a.H && gb < a.W * 3) dst[r * C::INP + c] = __ldg(src + (size_t)gr * a.W * 3 + gb);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+#pragma unroll 1
+  for (int f = 0; f < C::NST; ++f) load_tile(f);
+
+  // F(q) table: copy 0 first, then the 31 replicas (broadcast reads)
+  for (int q = tid; q < 256; q += C::NT)
+    lut[q * 32] = (uint32_t)((double)__fdiv_rn((float)q, 255.0f) * 2147483648.0);
+  __syncthreads();
+  for (int e = tid; e < C::LUT_WORDS; e += C::NT) lut[e] = lut[e & ~31];
+
+  const int wy = tid / C::NQ, qi = tid % C::NQ;
+  const int ay = min(ty * 8 + wy, a.h - 1);
+  const int px0 = tx0 * 8 + qi * 4;                // first working pixel of the quad
+  const bool interior = px0 + 3 < a.w && (px0 + 4) * S <= a.W;
+  const uint32_t* lutl = lut + lane;
+  constexpr double div_ss = (double)(S * S);
+  const size_t work_frame = (size_t)a.h * a.w * 3;
+  const bool wrow = a.work != nullptr && ty * 8 + wy < a.h;
+  float ival[4][3];
+  double pacc[4][3];
+
+#pragma unroll 1
+  for (int f = 0; f < kGop; ++f) {
+    asm volatile("cp.async.wait_group %0;" ::"n"(C::NST - 1) : "memory");
+    __syncthreads();                               // tile f (and, at f = 0, the table) visible
+    const uint8_t* tile = ring + (f % C::NST) * C::TILE;
+    uint64_t acc[4][3];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) acc[p][ch] = 0;
+#pragma unroll
+    for (int j = 0; j < S; ++j) {
+      const int r = min(ay * S + j, a.H - 1) - row0;
+      if (interior) {
+        const uint32_t* wp = reinterpret_cast<const uint32_t*>(tile + r * C::INP + qi * C::QB);
+        uint32_t wd[3 * S];
+#pragma unroll
+        for (int k = 0; k < 3 * S; ++k) wd[k] = wp[k];
+#pragma unroll
+        for (int b = 0; b < 12 * S; ++b) {         // byte b: pixel b / 3S, column (b % 3S) / 3, channel b % 3
+          const uint32_t q = (wd[b >> 2] >> (8 * (b & 3))) & 0xFFu;
+          acc[b / (3 * S)][b % 3] += lutl[q << 5];
+        }
+      } else {
+        const uint8_t* rp = tile + r * C::INP;
+#pragma unroll
+        for (int p = 0; p < 4; ++p) {
+          const int ax = min(px0 + p, a.w - 1);
+#pragma unroll
+          for (int l = 0; l < S; ++l) {
+            const int c = min(ax * S + l, a.W - 1) - col0;
+#pragma unroll
+            for (int ch = 0; ch < 3; ++ch) acc[p][ch] += lutl[(uint32_t)rp[c * 3 + ch] << 5];
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      float* wout = nullptr;
+      if (wrow && px0 + p < a.w)
+        wout = a.work + (size_t)g * kGop * work_frame + (size_t)f * work_frame +
+               ((size_t)(ty * 8 + wy) * a.w + px0 + p) * 3;
+#pragma unroll
+      for (int ch = 0; ch < 3; ++ch) {
+        const double sum = (double)acc[p][ch] * 0x1p-31;          // exact
+        const float wv = __double2float_rn(sum / div_ss);         // codec.py:212-214
+        if (wout != nullptr) wout[ch] = wv;
+        if (f == 0) ival[p][ch] = wv;
+        else if (f == 1) pacc[p][ch] = 0.0 + (double)wv;
+        else pacc[p][ch] = pacc[p][ch] + (double)wv;               // codec.py:151-152
+      }
+    }
+    __syncthreads();                               // stage f % NST free
+    if (f + C::NST < kGop) load_tile(f + C::NST);
+    else asm volatile("cp.async.commit_group;" ::: "memory");   // keep the group count uniform
+  }
+
+  // ---- 8x8 DCT of the I and P working blocks (the ring is free) ----
+  double* img = reinterpret_cast<double*>(smem_raw);                 // [2][8][8*TPB][3]
+  double* s1 = img + C::IMG_D;                                       // [2][TPB][3][3][8]
+  double* tk = s1 + C::S1_D;                                         // [2][TPB][12]
+#pragma unroll
+  for (int p = 0; p < 4; ++p) {
+    const int base = (wy * 8 * C::TPB + qi * 4 + p) * 3;
+#pragma unroll
+    for (int ch = 0; ch < 3; ++ch) {
+      img[base + ch] = (double)ival[p][ch];
+      img[8 * 8 * C::TPB * 3 + base + ch] = pacc[p][ch] / 8.0;
+    }
+  }
+  __syncthreads();
+  for (int it = tid; it < 48 * C::TPB; it += C::NT) {
+    int im = it / (24 * C::TPB);
+    int rem = it % (24 * C::TPB);
+    int t = rem / 24, ch = (rem % 24) / 8, x = rem % 8;
+    double c[8];
+    const double* src = img + im * (8 * 8 * C::TPB * 3) + (t * 8 + x) * 3 + ch;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) c[y] = src[y * 8 * C::TPB * 3];
+    dct2_8<true>(c, 1.0 / 16.0);
+    double* dst = s1 + ((im * C::TPB + t) * 3 + ch) * 24;
+    dst[x] = c[0];
+    dst[8 + x] = c[1];
+    dst[16 + x] = c[2];
+  }
+  __syncthreads();
+  for (int it = tid; it < 18 * C::TPB; it += C::NT) {
+    int im = it / (9 * C::TPB);
+    int rem = it % (9 * C::TPB);
+    int t = rem / 9, ch = (rem % 9) / 3, yk = rem % 3;
+    double c[8];
+    const double* src = s1 + ((im * C::TPB + t) * 3 + ch) * 24 + yk * 8;
+#pragma unroll
+    for (int x = 0; x < 8; ++x) c[x] = src[x];
+    dct2_8<false>(c, 1.0);
+    double* dst = tk + (im * C::TPB + t) * kChannels + ch * 4;
+    if (yk == 0) {
+      dst[0] = c[0];
+      dst[1] = c[1];
+    } else {
+      dst[yk + 1] = c[0];
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < 2 * C::TPB * kChannels; e += C::NT) {
+    int im = e / (C::TPB * kChannels);
+    int t = (e / kChannels) % C::TPB;
+    int k = e % kChannels;
+    int tx = tx0 + t;
+    if (tx < a.Wt)
+      a.tok[((((size_t)g * 2 + im) * a.Ht + ty) * a.Wt + tx) * kChannels + k] = tk[e];
+  }
+  if (a.sim != nullptr && tid < C::TPB && tx0 + tid < a.Wt) {
+    const double* iv = tk + tid * kChannels;
+    const double* pv = tk + (C::TPB + tid) * kChannels;
+    a.sim[((size_t)g * a.Ht + ty) * a.Wt + tx0 + tid] = cosine12(pv, iv);
+  }
+}
+
+template <int S>
+static int launch_encode_u8(const uint8_t* frames, int G, int H, int W, double* tok, double* sim,
+                            float* work, cudaStream_t stream) {
+  using C = EncU8Cfg<S>;
+  EncU8Args a;
+  a.frames = frames;
+  a.G = G; a.H = H; a.W = W;
+  a.h = ceil_div(H, S);
+  a.w = ceil_div(W, S);
+  a.Ht = ceil_div(a.h, kBlock);
+  a.Wt = ceil_div(a.w, kBlock);
+  a.tok = tok;
+  a.sim = sim;
+  a.work = work;
+  a.aligned = (reinterpret_cast<uintptr_t>(frames) & 15u) == 0 && ((int64_t)W * 3) % 16 == 0;
+  if (a.Ht > 65535 || G > 65535) return SST_ERR_ARG;
+  dim3 grid(ceil_div(a.Wt, C::TPB), a.Ht, G);
+  SST_CUDA_TRY(cudaFuncSetAttribute(k_encode_u8<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  k_encode_u8<S><<<grid, C::NT, C::SMEM, stream>>>(a);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
 // ---- standalone box downscale (downscale_frame, codec.py:202-214) ----
 template <int S>
 __global__ void k_downscale(const float* __restrict__ src, int64_t n, int H, int W, int h, int w,
@@ -308,6 +560,18 @@ extern "C" int sst_encode_work(const float* frames, int G, int H, int W, int s, 
     case 1: return launch_encode<1>(frames, G, H, W, tok, sim, work, st);
     case 2: return launch_encode<2>(frames, G, H, W, tok, sim, work, st);
     case 3: return launch_encode<3>(frames, G, H, W, tok, sim, work, st);
+    default: return SST_ERR_ARG;
+  }
+}
+
+extern "C" int sst_encode_u8(const uint8_t* frames, int G, int H, int W, int s, double* tok,
+                             double* sim, float* work, void* stream) {
+  if (!frames || !tok || G <= 0 || H <= 0 || W <= 0) return SST_ERR_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (s) {
+    case 1: return launch_encode_u8<1>(frames, G, H, W, tok, sim, work, st);
+    case 2: return launch_encode_u8<2>(frames, G, H, W, tok, sim, work, st);
+    case 3: return launch_encode_u8<3>(frames, G, H, W, tok, sim, work, st);
     default: return SST_ERR_ARG;
   }
 }

@@ -122,8 +122,9 @@ __device__ __forceinline__ int opaque_i32(int v) {
   return r;
 }
 // element f * fs past p (fs < 2^31, 64-bit product)
-__device__ __forceinline__ float* frame_ptr(float* p, int fs, int f) {
-  return reinterpret_cast<float*>(reinterpret_cast<char*>(p) + (int64_t)fs * (int64_t)(4 * f));
+template <typename T>
+__device__ __forceinline__ T* frame_ptr(T* p, int fs, int f) {
+  return reinterpret_cast<T*>(reinterpret_cast<char*>(p) + (int64_t)fs * (int64_t)(sizeof(T) * f));
 }
 
 // blend_w with the frame index a run-time value (folded once unrolled)
@@ -160,7 +161,29 @@ struct UpArgs {
   int n;                       // blend width (<= 4 when prev is used)
   double alpha[4], beta[4];    // alpha_i = (n - i) / n, beta = 1 - alpha (i = 1..n)
   float* out;                  // [G][9][H][W][3]
+  uint8_t* out8;               // raw-rgb24 output [G][9][H][W][3] (the uint8 entry points)
 };
+
+// write_raw_video's quantiser (video.py:143): np.rint(v * 255.0).astype(uint8)
+// on float32 samples -- the product rounds to float32 first (a float32 array
+// times a Python float stays float32), then rint rounds half to even.  Adding
+// 1.5 * 2^23 puts the round-to-nearest-even integer in the low mantissa bits.
+__device__ __forceinline__ uint32_t rgb24_q(float v) {
+  const float t = __fadd_rn(__fmul_rn(v, 255.0f), 12582912.0f);
+  return __float_as_uint(t) & 0xFFu;
+}
+
+// store one output sample (float32, or its raw-rgb24 byte)
+template <typename TOut>
+__device__ __forceinline__ void st_out(TOut* p, float v) {
+  if constexpr (sizeof(TOut) == 4) __stcs(p, v);
+  else *p = (uint8_t)rgb24_q(v);
+}
+template <typename TOut>
+__device__ __forceinline__ TOut* out_base(const UpArgs& a) {
+  if constexpr (sizeof(TOut) == 4) return a.out;
+  else return a.out8;
+}
 
 struct RowCache {
   int ya, yb;
@@ -199,6 +222,7 @@ __device__ __forceinline__ void vstep(RowCache& c, const float* i0, const float*
   if (NIMG == 2) u[1] = (float)clip01(lo[1] * ty.g + hi[1] * ty.f);
 }
 
+template <typename TOut>
 __global__ void __launch_bounds__(kUpThreads) k_upscale_blend(const __grid_constant__ UpArgs a) {
   __shared__ RowTap ty_c[kUpRows], ty_p[kUpRows];
   const int tid = threadIdx.x;
@@ -219,16 +243,16 @@ __global__ void __launch_bounds__(kUpThreads) k_upscale_blend(const __grid_const
   const float* iimg = a.img + (int64_t)g * 2 * a.h * a.w * 3;
   const float* pimg = iimg + (int64_t)a.h * a.w * 3;
   const int64_t fstride = (int64_t)a.H * a.W * 3;
-  float* o = a.out + (int64_t)g * kGop * fstride + (int64_t)oy0 * a.W * 3 + q;
+  TOut* o = out_base<TOut>(a) + (int64_t)g * kGop * fstride + (int64_t)oy0 * a.W * 3 + q;
   const int rows = min(kUpRows, a.H - oy0);
   RowCache cc{-1, -1, 0.0, 0.0, 0.0, 0.0};
   if (!has_prev) {
     for (int r = 0; r < rows; ++r, o += a.W * 3) {
       float u[2];
       vstep<2>(cc, iimg, pimg, a.w, from_row(ty_c[r]), tx, ch, u);
-      __stcs(o, u[0]);
+      st_out(o, u[0]);
 #pragma unroll
-      for (int f = 1; f < kGop; ++f) __stcs(o + f * fstride, u[1]);
+      for (int f = 1; f < kGop; ++f) st_out(o + f * fstride, u[1]);
     }
     return;
   }
@@ -240,12 +264,12 @@ __global__ void __launch_bounds__(kUpThreads) k_upscale_blend(const __grid_const
     vstep<1>(cp, pd.p_img, nullptr, pd.w, from_row(ty_p[r]), txp, ch, uq);
     // frame f < n: alpha*prev[9-n+f] + (1-alpha)*curr[f]  (codec.py:289-293);
     // the previous GoP's tail frames are its unblended P upscale when n <= 4
-    __stcs(o, (float)clip01(a.alpha[0] * (double)uq[0] + a.beta[0] * (double)u[0]));
+    st_out(o, (float)clip01(a.alpha[0] * (double)uq[0] + a.beta[0] * (double)u[0]));
 #pragma unroll
     for (int f = 1; f < kGop; ++f) {
       float v = u[1];
       if (f < a.n) v = (float)clip01(a.alpha[f] * (double)uq[0] + a.beta[f] * (double)u[1]);
-      __stcs(o + f * fstride, v);
+      st_out(o + f * fstride, v);
     }
   }
 }
@@ -515,7 +539,7 @@ __global__ void __launch_bounds__(kTQ)
 // rows) and an 8-byte aligned output; the windows arrive by TMA as before.
 constexpr int kV2Threads = kTQ / 2;
 
-template <int kBand, bool kPrev, int kN>
+template <int kBand, bool kPrev, int kN, typename TOut = float>
 __global__ void __launch_bounds__(kV2Threads)
     k_upscale_blend_v2(const __grid_constant__ CUtensorMap imap, const __grid_constant__ UpArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -591,7 +615,7 @@ __global__ void __launch_bounds__(kV2Threads)
   double qva[2] = {0, 0}, qvb[2] = {0, 0};
   const int64_t orow = (int64_t)a.W * 3;
   const int fsv = opaque_i32(a.H * a.W * 3);       // frame stride (elements)
-  float* obase = a.out + ((int64_t)g * kGop * a.H + oy0) * orow + qa0;
+  TOut* obase = out_base<TOut>(a) + ((int64_t)g * kGop * a.H + oy0) * orow + qa0;
   for (int r = 0; r < rows; ++r, obase += orow) {
     const AxisTap ty = from_row(S.ty_c[r]);
     if (ty.lo != ya) {
@@ -670,18 +694,33 @@ __global__ void __launch_bounds__(kV2Threads)
     }
     if (col_ok) {
       // frame f at obase + f * fsv: one IMAD.WIDE per store address
-      __stcs(reinterpret_cast<float2*>(obase), make_float2(fv[0][0], fv[0][1]));
+      if constexpr (sizeof(TOut) == 4) {
+        __stcs(reinterpret_cast<float2*>(obase), make_float2(fv[0][0], fv[0][1]));
 #pragma unroll
-      for (int f = 1; f < kGop; ++f) {
-        const float2 v = (has_prev && f < kN) ? make_float2(fv[f < kN ? f : 0][0], fv[f < kN ? f : 0][1])
-                                              : make_float2(up[0], up[1]);
-        __stcs(reinterpret_cast<float2*>(frame_ptr(obase, fsv, f)), v);
+        for (int f = 1; f < kGop; ++f) {
+          const float2 v = (has_prev && f < kN) ? make_float2(fv[f < kN ? f : 0][0], fv[f < kN ? f : 0][1])
+                                                : make_float2(up[0], up[1]);
+          __stcs(reinterpret_cast<float2*>(frame_ptr(obase, fsv, f)), v);
+        }
+      } else {
+        // raw-rgb24: the two samples' bytes as one 16-bit store per frame row
+        const unsigned short up8 = (unsigned short)(rgb24_q(up[0]) | (rgb24_q(up[1]) << 8));
+        __stcs(reinterpret_cast<unsigned short*>(obase),
+               (unsigned short)(rgb24_q(fv[0][0]) | (rgb24_q(fv[0][1]) << 8)));
+#pragma unroll
+        for (int f = 1; f < kGop; ++f) {
+          const unsigned short v =
+              (has_prev && f < kN)
+                  ? (unsigned short)(rgb24_q(fv[f < kN ? f : 0][0]) | (rgb24_q(fv[f < kN ? f : 0][1]) << 8))
+                  : up8;
+          __stcs(reinterpret_cast<unsigned short*>(frame_ptr(obase, fsv, f)), v);
+        }
       }
     }
   }
 }
 
-template <int BAND>
+template <int BAND, typename TOut = float>
 static int launch_k5_v2(const CUtensorMap& imap, const UpArgs& a, const SstPrevDesc* prev,
                         int blend_n, cudaStream_t st) {
   dim3 grid(ceil_div(a.W * 3, kTQ), ceil_div(a.H, BAND), a.G);
@@ -694,13 +733,13 @@ static int launch_k5_v2(const CUtensorMap& imap, const UpArgs& a, const SstPrevD
   // 3/SM 1.255.  SST_K5_SMEM overrides the request (A/B).
   const char* es = getenv("SST_K5_SMEM");
   const int smem = std::max((int)sizeof(UpTmaSmem<BAND>), es ? atoi(es) : 54 * 1024);
-  auto kern = k_upscale_blend_v2<BAND, false, 1>;
+  auto kern = k_upscale_blend_v2<BAND, false, 1, TOut>;
   if (prev) {
     switch (blend_n) {
-      case 1: kern = k_upscale_blend_v2<BAND, true, 1>; break;
-      case 2: kern = k_upscale_blend_v2<BAND, true, 2>; break;
-      case 3: kern = k_upscale_blend_v2<BAND, true, 3>; break;
-      default: kern = k_upscale_blend_v2<BAND, true, 4>; break;
+      case 1: kern = k_upscale_blend_v2<BAND, true, 1, TOut>; break;
+      case 2: kern = k_upscale_blend_v2<BAND, true, 2, TOut>; break;
+      case 3: kern = k_upscale_blend_v2<BAND, true, 3, TOut>; break;
+      default: kern = k_upscale_blend_v2<BAND, true, 4, TOut>; break;
     }
   }
   SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -1237,7 +1276,45 @@ extern "C" int sst_upscale_blend(const float* img, int G, int h, int w, int s, i
   }
   dim3 grid(ceil_div(W * 3, kUpThreads), ceil_div(H, kUpRows), G);
   if (grid.y > 65535) return SST_ERR_ARG;
-  k_upscale_blend<<<grid, kUpThreads, 0, st>>>(a);
+  k_upscale_blend<float><<<grid, kUpThreads, 0, st>>>(a);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+// sst_upscale_blend writing raw-rgb24 bytes: K5's float32 result quantised
+// as write_raw_video does (video.py:139-143), fused into the store -- the
+// reference CLI's decode output (cli.py:181) without a float32 frame pass.
+extern "C" int sst_upscale_blend_u8(const float* img, int G, int h, int w, int s, int H, int W,
+                                    const SstPrevDesc* prev, int blend_n, uint8_t* out, void* stream) {
+  if (G < 0 || h <= 0 || w <= 0 || H <= 0 || W <= 0) return SST_ERR_ARG;
+  if (s != 2 && s != 3) return SST_ERR_ARG;
+  if (H > h * s || W > w * s) return SST_ERR_ARG;
+  if (blend_n < 1 || blend_n > 8) return SST_ERR_ARG;
+  if (prev && blend_n > 4) return SST_ERR_UNSUPPORTED;
+  if (G == 0) return SST_OK;
+  if (!img || !out) return SST_ERR_ARG;
+  if (G > 65535) return SST_ERR_ARG;
+  UpArgs a{};
+  a.img = img; a.G = G; a.h = h; a.w = w; a.s = s; a.H = H; a.W = W;
+  a.prev = prev; a.n = blend_n; a.out8 = out;
+  for (int i = 1; i <= 4; ++i) {
+    a.alpha[i - 1] = (double)(blend_n - i) / (double)blend_n;
+    a.beta[i - 1] = 1.0 - a.alpha[i - 1];
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  // v2 (TMA windows, two samples per thread -> one 16-bit store per frame
+  // row) when the working images admit a tensor map and rows are 2-byte
+  // aligned; the one-sample-per-thread kernel otherwise
+  CUtensorMap imap;
+  memset(&imap, 0, sizeof(imap));
+  const char* var = getenv("SST_K5_VARIANT");
+  if (!(var && !strcmp(var, "v1")) && (W * 3) % 2 == 0 && (reinterpret_cast<uintptr_t>(out) & 1u) == 0 &&
+      make_tmap_f32_3d(&imap, img, (uint64_t)w * 3, (uint64_t)h, (uint64_t)G * 2, kWF9,
+                       UpTmaSmem<16>::kWR))
+    return launch_k5_v2<16, uint8_t>(imap, a, prev, blend_n, st);
+  dim3 grid(ceil_div(W * 3, kUpThreads), ceil_div(H, kUpRows), G);
+  if (grid.y > 65535) return SST_ERR_ARG;
+  k_upscale_blend<uint8_t><<<grid, kUpThreads, 0, st>>>(a);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }

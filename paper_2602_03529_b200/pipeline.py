@@ -35,14 +35,17 @@ def _cdiv(a: int, b: int) -> int:
     return -(-a // b)
 
 
-def check_gop_tensor(t: torch.Tensor, g: int, H: int, W: int, what: str) -> None:
-    """The kernels address [g][9][H][W][3] float32 by raw pointer: reject
-    anything else (a non-contiguous view, e.g. a transposed numpy array
-    wrapped by torch.from_numpy, would otherwise be read in the wrong order)."""
+def check_gop_tensor(t: torch.Tensor, g: int, H: int, W: int, what: str,
+                     dtypes=(torch.float32,)) -> None:
+    """The kernels address [g][9][H][W][3] float32 (or, where ``dtypes``
+    allows it, raw-rgb24 uint8) by raw pointer: reject anything else (a
+    non-contiguous view, e.g. a transposed numpy array wrapped by
+    torch.from_numpy, would otherwise be read in the wrong order)."""
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise ValueError(f"{what} must be a CUDA tensor")
-    if t.dtype != torch.float32:
-        raise ValueError(f"{what} must be float32, got {t.dtype}")
+    if t.dtype not in dtypes:
+        want = " or ".join(str(d).replace("torch.", "") for d in dtypes)
+        raise ValueError(f"{what} must be {want}, got {t.dtype}")
     if t.dim() != 5 or tuple(t.shape[1:]) != (GOP, H, W, 3) or t.shape[0] < g:
         raise ValueError(f"{what} must be [>= {g}, {GOP}, {H}, {W}, 3], got {tuple(t.shape)}")
     if not t.is_contiguous():
@@ -165,8 +168,10 @@ class GopCodec:
     # -- sender --------------------------------------------------------
     def encode(self, frames: torch.Tensor, g: int, drop_k: int = 0,
                work: torch.Tensor | None = None) -> None:
-        """K1 + K2 + K3 for frames[:g] ([g, 9, H, W, 3] float32, contiguous);
-        `work` ([>= g, 9, h, w, 3] float32) also receives the working frames."""
+        """K1 + K2 + K3 for frames[:g] ([g, 9, H, W, 3] float32 -- or uint8
+        raw-rgb24, sample q meaning float32(q) / 255 as load_raw_video reads
+        it (video.py:130-135) -- contiguous); `work` ([>= g, 9, h, w, 3]
+        float32) also receives the working frames."""
         self.tokenize(frames, g, work)
         self.select_and_pack(g, drop_k)
 
@@ -174,11 +179,12 @@ class GopCodec:
         """K1: downscale + tokenize + similarity (+ the working frames when
         `work` is given: the residual layer's input, no second frame read)."""
         tm = self.timer
-        check_gop_tensor(frames, g, self.H, self.W, "frames")
+        check_gop_tensor(frames, g, self.H, self.W, "frames", (torch.float32, torch.uint8))
         if work is not None:
             check_gop_tensor(work, g, self.h, self.w, "work")
         tm.begin("K1_encode")
-        _lib.call("sst_encode_work", frames.data_ptr(), g, self.H, self.W, self.s,
+        _lib.call("sst_encode_u8" if frames.dtype == torch.uint8 else "sst_encode_work",
+                  frames.data_ptr(), g, self.H, self.W, self.s,
                   self.tok.data_ptr(), self.sim.data_ptr(),
                   None if work is None else work.data_ptr(), _dev.stream())
         tm.end("K1_encode")
@@ -231,11 +237,13 @@ class GopCodec:
     # -- reconstruction ------------------------------------------------
     def reconstruct(self, g: int, parity: int, out: torch.Tensor,
                     prev: torch.Tensor | None = None) -> None:
-        """K5: [g, 9, H, W, 3] float32 output frames; prev = device
-        SstPrevDesc[g] as uint8 bytes (or None: no blending)."""
-        check_gop_tensor(out, g, self.H, self.W, "out")
+        """K5: [g, 9, H, W, 3] float32 output frames -- or uint8 raw-rgb24,
+        each sample quantised as write_raw_video does (video.py:139-143);
+        prev = device SstPrevDesc[g] as uint8 bytes (or None: no blending)."""
+        check_gop_tensor(out, g, self.H, self.W, "out", (torch.float32, torch.uint8))
         self.timer.begin("K5_upscale_blend")
-        _lib.call("sst_upscale_blend", self.img[parity].data_ptr(), g, self.h, self.w, self.s,
+        _lib.call("sst_upscale_blend_u8" if out.dtype == torch.uint8 else "sst_upscale_blend",
+                  self.img[parity].data_ptr(), g, self.h, self.w, self.s,
                   self.H, self.W, None if prev is None else prev.data_ptr(), self.blend_n,
                   out.data_ptr(), _dev.stream())
         self.timer.end("K5_upscale_blend")
@@ -393,6 +401,9 @@ class StreamBank:
                         if staged is not None:
                             self.rings[s].release(staged[1])
                     else:
+                        if out_by_scale[s].dtype != torch.float32:
+                            # the n >= 5 blend reads the previous float32 output back
+                            raise ValueError("blend widths 5..8 need float32 output frames")
                         codec.reconstruct(g, parity, out_by_scale[s], None)
                         self._blend_wide(ids, out_by_scale[s])
                 elif mid is not gs:

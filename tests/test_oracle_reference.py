@@ -149,3 +149,31 @@ def test_metrics(ref):
             for norm in ("l1", "l2"):
                 assert O.boundary_flicker(a, b, n, norm) == V.boundary_flicker(ga, gb, n, norm)
         assert O.inter_frame_consistency(b) == V.inter_frame_consistency(gb.frames)
+
+
+# ---------------------------------------------------------------------------
+# raw-rgb24 file formats (video.py:103-143): the CLI's ingest and egress
+
+def test_rgb24_conversions_match_reference_io(ref, tmp_path):
+    """frames_from_rgb24 == load_raw_video's frames and rgb24_from_frames ==
+    write_raw_video's bytes on every byte value and on float samples at and
+    around the rint ties (v * 255 = k + 1/2)."""
+    C, S, T, V = ref
+    rng = np.random.default_rng(24)
+    H, W = 6, 10
+    raw = np.concatenate([np.arange(256, dtype=np.uint8),
+                          rng.integers(0, 256, 2 * H * W * 3 - 256, dtype=np.uint8)])
+    path = tmp_path / "clip.rgb"
+    path.write_bytes(raw.tobytes())
+    frames = V.load_raw_video(str(path), W, H)
+    got = O.frames_from_rgb24(raw.reshape(2, H, W, 3))
+    for t in range(2):
+        assert _bits(frames[t].samples, got[t])
+    k = rng.integers(0, 255, H * W * 3)
+    ties = ((2 * k + 1) / 510.0).astype(np.float32)            # float32 near the k + 1/2 boundary
+    vals = np.concatenate([ties, np.nextafter(ties, np.float32(0)), np.nextafter(ties, np.float32(1)),
+                           rng.random(H * W * 3, dtype=np.float32)])
+    vals = np.clip(vals, 0, 1).astype(np.float32)[: 2 * H * W * 3].reshape(2, H, W, 3)
+    out = tmp_path / "out.rgb"
+    V.write_raw_video(str(out), [V.Frame(vals[t], timestamp_index=t) for t in range(2)])
+    assert out.read_bytes() == O.rgb24_from_frames(vals).tobytes()
