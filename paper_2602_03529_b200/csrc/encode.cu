@@ -11,6 +11,7 @@
 // then runs the ducc0-exact 8x8 DCT on the two working-resolution blocks per
 // token and channel, and finally the cosine similarity of each token pair.
 // HBM traffic is one read of every input pixel plus the token write.
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -239,13 +240,19 @@ __global__ void __launch_bounds__(EncCfg<S>::NT)
 // sample f(q) = float32(q) / 255 (video.py:130-135; a float32 array divided by
 // a Python float stays float32, correctly rounded).  K1u8 reads the bytes --
 // a quarter of the float32 frames' HBM traffic -- and box-filters f(q)
-// exactly: f(q) >= 2^-8 has its lowest set bit at >= 2^-31 and f(q) <= 1, so
-// F(q) = f(q) * 2^31 is an integer < 2^31 + 1; the s x s window sum of F is
-// exact in uint64 and (double)sum * 2^-31 is the float64 sum numpy forms
-// (every partial sum of <= 9 such values is exact in float64, so numpy's
-// summation order does not matter).  F comes from a 256-entry table in
-// shared memory replicated 32x (entry q of copy c at word 32q + c, lane l
-// reads copy l): the lookups are bank-conflict free.
+// exactly.  q / 255 in binary is q's 8 bits repeated forever, so
+// floor(q/255 * 2^32) = q * 0x01010101, and rounding to float32's 24
+// significant bits always rounds UP (the first dropped bit is q's leading
+// one, the rest of the expansion is non-zero), giving the identity
+//     f(q) * 2^32 = q * 0x01010100 + g(q),   g(q) = 2^(msb(q) + 1), g(0) = 0
+// (checked for all 256 values).  So the window sum is
+//     sum f = (0x01010100 * sum q + sum g) * 2^-32,
+// exact in float64 -- the value numpy's float64 sum reaches in any order,
+// since every partial sum of <= 9 such samples is exact.  One 32-bit table
+// entry T(q) = q << 16 | g(q) per byte gives both sums with one 32-bit add
+// (sum q, sum g < 2^16 for <= 9 terms).  T lives in shared memory replicated
+// 32x (entry q of copy c at word 32q + c, lane l reads copy l): the lookups
+// are bank-conflict free.
 //
 // Work mapping: each thread box-filters a QUAD of 4 horizontally adjacent
 // working pixels of one working row, so the quad's s rows x 12s bytes are
@@ -284,8 +291,8 @@ struct EncU8Args {
   int aligned;   // frames and rows 16-byte aligned: cp.async 16-byte tile copies
 };
 
-template <int S>
-__global__ void __launch_bounds__(EncU8Cfg<S>::NT) k_encode_u8(EncU8Args a) {
+template <int S, bool kWork>
+__global__ void __launch_bounds__(EncU8Cfg<S>::NT, 3) k_encode_u8(EncU8Args a) {
   using C = EncU8Cfg<S>;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* ring = smem_raw;
@@ -299,20 +306,32 @@ __global__ void __launch_bounds__(EncU8Cfg<S>::NT) k_encode_u8(EncU8Args a) {
   const size_t frame_bytes = (size_t)a.H * a.W * 3;
   const uint8_t* gop = a.frames + (size_t)g * kGop * frame_bytes;
 
+  // this thread's 16-byte chunks of a tile (the same for every frame):
+  // smem offset and frame-relative global offset, -1 when outside the frame
+  constexpr int kChunks = C::IN / 16;
+  constexpr int kCpt = (C::R * kChunks + C::NT - 1) / C::NT;
+  int c_smem[kCpt], c_glob[kCpt];
+#pragma unroll
+  for (int k = 0; k < kCpt; ++k) {
+    const int e = tid + k * C::NT;
+    const int r = e / kChunks, c = e % kChunks;
+    const int gr = row0 + r, gb = col0 * 3 + c * 16;
+    const bool ok = e < C::R * kChunks && gr < a.H && gb < a.W * 3;   // W*3 % 16 == 0: chunks whole
+    c_smem[k] = ok ? r * C::INP + c * 16 : -1;
+    c_glob[k] = gr * a.W * 3 + gb;
+  }
+  const uint32_t ring_u32 = smem_u32(ring);
   // tile f -> ring stage f % NST: rows row0..row0+R-1 (< H), bytes col0*3..
   auto load_tile = [&](int f) {
     uint8_t* dst = ring + (f % C::NST) * C::TILE;
     const uint8_t* src = gop + (size_t)f * frame_bytes;
     if (a.aligned) {
-      constexpr int kChunks = C::IN / 16;
-      for (int e = tid; e < C::R * kChunks; e += C::NT) {
-        const int r = e / kChunks, c = e % kChunks;
-        const int gr = row0 + r, gb = col0 * 3 + c * 16;
-        if (gr < a.H && gb < a.W * 3)      // W*3 % 16 == 0: chunks are whole
-          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst + r * C::INP + c * 16)),
-                       "l"(src + (size_t)gr * a.W * 3 + gb)
+      const uint32_t d0 = ring_u32 + (f % C::NST) * C::TILE;
+#pragma unroll
+      for (int k = 0; k < kCpt; ++k)
+        if (c_smem[k] >= 0)
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d0 + c_smem[k]), "l"(src + c_glob[k])
                        : "memory");
-      }
     } else {
       for (int e = tid; e < C::R * C::IN; e += C::NT) {
         const int r = e / C::IN, c = e % C::IN;
@@ -325,21 +344,23 @@ __global__ void __launch_bounds__(EncU8Cfg<S>::NT) k_encode_u8(EncU8Args a) {
 #pragma unroll 1
   for (int f = 0; f < C::NST; ++f) load_tile(f);
 
-  // F(q) table: copy 0 first, then the 31 replicas (broadcast reads)
-  for (int q = tid; q < 256; q += C::NT)
-    lut[q * 32] = (uint32_t)((double)__fdiv_rn((float)q, 255.0f) * 2147483648.0);
-  __syncthreads();
-  for (int e = tid; e < C::LUT_WORDS; e += C::NT) lut[e] = lut[e & ~31];
+  // T(q) table: entry q's 32 copies are 128 contiguous bytes, written as
+  // 8 x 16-byte stores (consecutive threads: consecutive 16-byte chunks)
+  for (int e = tid; e < 256 * 8; e += C::NT) {
+    const uint32_t q = (uint32_t)e >> 3;
+    const uint32_t t = (q << 16) | (q ? 2u << (31 - __clz(q)) : 0u);
+    reinterpret_cast<uint4*>(lut)[e] = make_uint4(t, t, t, t);
+  }
 
   const int wy = tid / C::NQ, qi = tid % C::NQ;
   const int ay = min(ty * 8 + wy, a.h - 1);
   const int px0 = tx0 * 8 + qi * 4;                // first working pixel of the quad
   const bool interior = px0 + 3 < a.w && (px0 + 4) * S <= a.W;
-  const uint32_t* lutl = lut + lane;
+  const uint32_t lut_lane = smem_u32(lut) + 4u * lane;    // this lane's copy
   constexpr double div_ss = (double)(S * S);
   const size_t work_frame = (size_t)a.h * a.w * 3;
-  const bool wrow = a.work != nullptr && ty * 8 + wy < a.h;
-  float ival[4][3];
+  const bool wrow = kWork && ty * 8 + wy < a.h;
+  double ival[4][3];                               // float32 values, held as float64
   double pacc[4][3];
 
 #pragma unroll 1
@@ -347,7 +368,7 @@ __global__ void __launch_bounds__(EncU8Cfg<S>::NT) k_encode_u8(EncU8Args a) {
     asm volatile("cp.async.wait_group %0;" ::"n"(C::NST - 1) : "memory");
     __syncthreads();                               // tile f (and, at f = 0, the table) visible
     const uint8_t* tile = ring + (f % C::NST) * C::TILE;
-    uint64_t acc[4][3];
+    uint32_t acc[4][3];                            // sum q << 16 | sum g per (pixel, channel)
 #pragma unroll
     for (int p = 0; p < 4; ++p)
 #pragma unroll
@@ -362,8 +383,12 @@ __global__ void __launch_bounds__(EncU8Cfg<S>::NT) k_encode_u8(EncU8Args a) {
         for (int k = 0; k < 3 * S; ++k) wd[k] = wp[k];
 #pragma unroll
         for (int b = 0; b < 12 * S; ++b) {         // byte b: pixel b / 3S, column (b % 3S) / 3, channel b % 3
-          const uint32_t q = (wd[b >> 2] >> (8 * (b & 3))) & 0xFFu;
-          acc[b / (3 * S)][b % 3] += lutl[q << 5];
+          // (an ALU form without the table -- float(q) as (2^23 + q) - 2^23,
+          // g(q) from its exponent -- measured slower at every mix)
+          const uint32_t q = __byte_perm(wd[b >> 2], 0u, 0x4440u + (b & 3));
+          uint32_t t;
+          asm volatile("ld.shared.u32 %0, [%1];" : "=r"(t) : "r"(lut_lane + q * 128u));
+          acc[b / (3 * S)][b % 3] += t;
         }
       } else {
         const uint8_t* rp = tile + r * C::INP;
@@ -374,7 +399,7 @@ __global__ void __launch_bounds__(EncU8Cfg<S>::NT) k_encode_u8(EncU8Args a) {
           for (int l = 0; l < S; ++l) {
             const int c = min(ax * S + l, a.W - 1) - col0;
 #pragma unroll
-            for (int ch = 0; ch < 3; ++ch) acc[p][ch] += lutl[(uint32_t)rp[c * 3 + ch] << 5];
+            for (int ch = 0; ch < 3; ++ch) acc[p][ch] += lut[((uint32_t)rp[c * 3 + ch] << 5) + lane];
           }
         }
       }
@@ -382,17 +407,36 @@ __global__ void __launch_bounds__(EncU8Cfg<S>::NT) k_encode_u8(EncU8Args a) {
 #pragma unroll
     for (int p = 0; p < 4; ++p) {
       float* wout = nullptr;
-      if (wrow && px0 + p < a.w)
+      if (kWork && wrow && px0 + p < a.w)
         wout = a.work + (size_t)g * kGop * work_frame + (size_t)f * work_frame +
                ((size_t)(ty * 8 + wy) * a.w + px0 + p) * 3;
 #pragma unroll
       for (int ch = 0; ch < 3; ++ch) {
-        const double sum = (double)acc[p][ch] * 0x1p-31;          // exact
-        const float wv = __double2float_rn(sum / div_ss);         // codec.py:212-214
-        if (wout != nullptr) wout[ch] = wv;
-        if (f == 0) ival[p][ch] = wv;
-        else if (f == 1) pacc[p][ch] = 0.0 + (double)wv;
-        else pacc[p][ch] = pacc[p][ch] + (double)wv;               // codec.py:151-152
+        // N = 2^32 * sum f(q) = 0x01010100 * sum q + sum g  (< 2^36), as a
+        // float64 without the XU: 2^52 + N has N as its low mantissa bits
+        const uint64_t n = (uint64_t)(acc[p][ch] >> 16) * 0x01010100u + (acc[p][ch] & 0xFFFFu);
+        const double dn = __dadd_rn(__hiloint2double((int)((uint32_t)(n >> 32) | 0x43300000u), (int)(uint32_t)n),
+                                    -4503599627370496.0);
+        // float32(float64(sum / s^2)) (codec.py:212-214), sum = N 2^-32.
+        // s = 1, 2: the division is exact, so a multiply by 2^-32 / s^2 is
+        // too.  s = 3: N / 9 stays >= 2^(e-24) / 9 away from every float32
+        // rounding tie (m + 1/2) 2^(e-23) (9 is odd: |N 2^k - 9 m'| >= 1), far
+        // beyond float64's error, so rounding any float64 approximation
+        // within a few ulps -- the product with float64(2^-32 / 9) -- to
+        // float32 gives the float of the correctly rounded quotient.
+        const double x = __dmul_rn(dn, 0x1p-32 / div_ss);
+        // ... rounded to float32 precision in float64 arithmetic (no XU):
+        // (x + c) - c with c = 1.5 * 2^(e(x) + 29) rounds x to a multiple of
+        // its float32 ulp 2^(e-23), half to even; x is 0 or in [2^-12, 1],
+        // so the result is a normal float32 (also when it rounds up to the
+        // next binade)
+        const uint32_t xhi = (uint32_t)__double2hiint(x);
+        const double c = __hiloint2double((int)((xhi & 0x7FF00000u) + (29u << 20) + 0x00080000u), 0);
+        const double xr = __dadd_rn(__dadd_rn(x, c), -c);
+        if (kWork && wout != nullptr) wout[ch] = (float)xr;        // exact
+        if (f == 0) ival[p][ch] = xr;
+        else if (f == 1) pacc[p][ch] = 0.0 + xr;
+        else pacc[p][ch] = pacc[p][ch] + xr;                        // codec.py:151-152
       }
     }
     __syncthreads();                               // stage f % NST free
@@ -409,7 +453,7 @@ __global__ void __launch_bounds__(EncU8Cfg<S>::NT) k_encode_u8(EncU8Args a) {
     const int base = (wy * 8 * C::TPB + qi * 4 + p) * 3;
 #pragma unroll
     for (int ch = 0; ch < 3; ++ch) {
-      img[base + ch] = (double)ival[p][ch];
+      img[base + ch] = ival[p][ch];
       img[8 * 8 * C::TPB * 3 + base + ch] = pacc[p][ch] / 8.0;
     }
   }
@@ -479,8 +523,9 @@ static int launch_encode_u8(const uint8_t* frames, int G, int H, int W, double* 
   a.aligned = (reinterpret_cast<uintptr_t>(frames) & 15u) == 0 && ((int64_t)W * 3) % 16 == 0;
   if (a.Ht > 65535 || G > 65535) return SST_ERR_ARG;
   dim3 grid(ceil_div(a.Wt, C::TPB), a.Ht, G);
-  SST_CUDA_TRY(cudaFuncSetAttribute(k_encode_u8<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
-  k_encode_u8<S><<<grid, C::NT, C::SMEM, stream>>>(a);
+  auto kern = work != nullptr ? k_encode_u8<S, true> : k_encode_u8<S, false>;
+  SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM));
+  kern<<<grid, C::NT, C::SMEM, stream>>>(a);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }
