@@ -71,6 +71,8 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-workers", type=int, default=0, help="0 = auto")
+    ap.add_argument("--no-rgb24", action="store_true",
+                    help="skip the raw-rgb24 leg (uint8 frames in and out, SURVEY §8(d) variant)")
     ap.add_argument("--no-learned", action="store_true",
                     help="skip the learned-tokenizer leg (SURVEY f4, tensor-core path)")
     ap.add_argument("--no-learned-bf16", action="store_true",
@@ -297,7 +299,17 @@ def total_streams(a, world: int, per: int | None = None) -> int:
     return per * world if a.scaling == "weak" else per
 
 
-def run_ours(a, rank, world, local_rank):
+def to_rgb24(frames):
+    """write_raw_video's bytes of float32 frames (video.py:139-143), on the device."""
+    import torch
+    return torch.round(frames * 255.0).to(torch.uint8)   # float32 product, half to even
+
+
+def run_ours(a, rank, world, local_rank, rgb24: bool = False):
+    """The bench workload through StreamBank.  rgb24: the same streams as
+    raw-rgb24 bytes in and out (the reference CLI's file formats, cli.py:52-61
+    and 181; the kernels fuse load_raw_video's q/255 and write_raw_video's
+    quantiser)."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -320,6 +332,9 @@ def run_ours(a, rank, world, local_rank):
     odd = [i for i in range(S) if i % 2 == 1]
     ne = len(even)
     inputs = make_inputs([mine[i] for i in even + odd], H, W, dev)
+    if rgb24:
+        inputs = [to_rgb24(x) for x in inputs]
+        torch.cuda.empty_cache()
     out = torch.empty_like(inputs[0])
     lanes = []
     per = max(1, a.lanes // 2)                  # lanes per phase
@@ -418,7 +433,8 @@ def run_ours(a, rank, world, local_rank):
     fr, ou, ids = groups(a.warmup + a.steps - 1)
     for s, o in ou.items():
         src = fr[s][0]
-        mse = ((o[0].double() - src.double()) ** 2).mean().item()
+        sc = 1.0 / 255.0 if rgb24 else 1.0
+        mse = (((o[0].double() - src.double()) * sc) ** 2).mean().item()
         psnr[f"s{s}"] = 99.0 if mse <= 0 else min(99.0, 10 * np.log10(1.0 / mse))
 
     res = dict(ms=ms_max, value=value, stages=stages, launches=launches,
@@ -426,19 +442,64 @@ def run_ours(a, rank, world, local_rank):
                per_rank=[{"rank": r, "streams": int(n), "ms": round(m, 3),
                           "frames_per_s": round(n * GOP * a.steps / (m / 1000.0), 1)}
                          for r, (m, n) in enumerate(per_rank)])
-    res["roofline"] = roofline(a, stages, S // len(lanes), a.roofline_steps * len(lanes))
+    res["roofline"] = roofline(a, stages, S // len(lanes), a.roofline_steps * len(lanes),
+                               bpe=1 if rgb24 else 4)
+    del inputs, out
+    torch.cuda.empty_cache()
     if not a.no_e2e:
-        del inputs, out
-        torch.cuda.empty_cache()
-        res["e2e"] = run_e2e(a, rank, world, local_rank)
+        res["e2e"] = run_e2e(a, rank, world, local_rank, rgb24=rgb24)
     return res
 
 
-def roofline(a, stages, gops_per_launch, _launches_hint=None) -> dict:
-    """Achieved GB/s of the dominant kernel: algorithmic bytes per launch /
-    average CUDA-event launch duration inside the timed region."""
+def rgb24_leg(a, rank, world, local_rank, dev) -> dict:
+    """The bench workload over raw-rgb24 frames (uint8 in, uint8 out: the
+    reference CLI's encode input and decode output, video.py:103-143), with a
+    device-side parity check: the uint8 output of two streams x two GoPs
+    equals write_raw_video's bytes of the float32 path's output on the same
+    (converted) input, bit for bit."""
+    import numpy as np
+    import torch
+
+    from paper_2602_03529_b200.pipeline import StreamBank
+    res = run_ours(a, rank, world, local_rank, rgb24=True)
+    out = {"workload": "as the headline, frames as raw-rgb24 bytes in and out "
+                       "(uint8 [S][9][1080][1920][3]; load_raw_video's q/255 fused into K1, "
+                       "write_raw_video's quantiser into K5)",
+           "value": round(res["value"], 2), "unit": UNIT,
+           "ms_per_step": round(res["ms"] / a.steps, 3), "gpu_launches": res["launches"],
+           "stages": {k: {"ms_per_launch": round(v[0] / v[1], 4), "launches": v[1]}
+                      for k, v in res["stages"].items()},
+           "roofline": res["roofline"], "path_roofline": path_roofline(a, res["value"] / world, bpe=1),
+           "clocks": res["clocks"], "psnr_db_vs_u8_source": res["psnr"], "e2e": res.get("e2e")}
+    # parity: uint8 path vs the float32 path + write_raw_video's quantiser
     H, W = a.height, a.width
-    frame_bytes = H * W * 3 * 4
+    src = to_rgb24(make_inputs([0, 1], H, W, dev, n_sets=2)[0])
+    b8, bf = StreamBank(2, H, W), StreamBank(2, H, W)
+    # load_raw_video's float32(q) / 255, correctly rounded (numpy; torch's
+    # CUDA division by a scalar multiplies by the reciprocal)
+    q255 = torch.from_numpy(np.arange(256, dtype=np.float32) / np.float32(255.0)).to(dev)
+    ok = True
+    for k, s in enumerate((3, 2)):
+        fr8 = src
+        frf = q255[src.long()]
+        o8, of = torch.empty_like(fr8), torch.empty_like(frf)
+        b8.step({s: fr8}, {s: o8}, {s: [0, 1]}, {s: [k, k]}, drop_rate=a.drop)
+        bf.step({s: frf}, {s: of}, {s: [0, 1]}, {s: [k, k]}, drop_rate=a.drop)
+        torch.cuda.synchronize()
+        ok = ok and bool(torch.equal(o8, to_rgb24(of)))
+    out["parity"] = {"sample": "2 streams x 2 GoPs (s=3 then s=2, blend n=2), 10% drop",
+                     "uint8_equals_quantised_float32_path": ok,
+                     "tests": "tests/test_gpu_rgb24.py (vs the oracle and the reference's own "
+                              "load_raw_video / write_raw_video)"}
+    return out
+
+
+def roofline(a, stages, gops_per_launch, _launches_hint=None, bpe: int = 4) -> dict:
+    """Achieved GB/s of the dominant kernel: algorithmic bytes per launch /
+    average CUDA-event launch duration inside the timed region (bpe: bytes
+    per frame sample, 4 = float32, 1 = raw-rgb24)."""
+    H, W = a.height, a.width
+    frame_bytes = H * W * 3 * bpe
     # per GoP (one stream): K1 reads 9 frames + writes tokens/sim;
     # K5 writes 9 frames + reads the two working images (+ the previous P image)
     def tokens_bytes(s):
@@ -469,25 +530,26 @@ def roofline(a, stages, gops_per_launch, _launches_hint=None) -> dict:
     best.pop("_tot")
     tr = ncu_traffic()
     best["traffic"] = None
-    if tr and best["kernel"] in tr:
+    if tr and best["kernel"] in tr and bpe == 4:
         # ncu --set full DRAM bytes per GoP x GoPs per launch of this run
         best["traffic"] = int(tr[best["kernel"]] * gops_per_launch)
         best["traffic_source"] = tr.get("_source")
     return best
 
 
-def path_roofline(a, fps) -> dict:
+def path_roofline(a, fps, bpe: int = 4) -> dict:
     """Whole path against HBM: SURVEY §8(d) algorithmic bytes per frame
-    (read the frame once, write it once, fp32, + packets) x frames/s."""
+    (read the frame once, write it once, fp32 -- or raw-rgb24 bytes -- +
+    packets) x frames/s."""
     peak, src = measured_hbm_peak()
-    per_frame = a.height * a.width * 3 * (4 + 4)
+    per_frame = a.height * a.width * 3 * (bpe + bpe)
     ach = per_frame * fps / 1e9
     return {"bytes_per_frame": per_frame, "achieved": round(ach, 1), "peak": peak,
             "unit": "GB/s", "frac": round(ach / peak, 4),
             "roofline_fps": round(peak * 1e9 / per_frame, 1)}
 
 
-def run_e2e(a, rank, world, local_rank) -> dict:
+def run_e2e(a, rank, world, local_rank, rgb24: bool = False) -> dict:
     """Same pipeline through the public batched API with pinned host buffers:
     frames H2D -> sender (K1-K3) -> packets D2H -> packets H2D -> receiver
     (K4, K5) -> frames D2H, every step, inside the timed region.  The streams
@@ -505,19 +567,22 @@ def run_e2e(a, rank, world, local_rank) -> dict:
     lanes = max(1, min(int(os.environ.get("SST_E2E_LANES", "8")), E))   # one stream per lane
     per = [list(range(E))[i::lanes] for i in range(lanes)]
     src_dev = make_inputs(mine, H, W, dev, n_sets=1)[0]
+    fdt, bpe = torch.float32, 4
+    if rgb24:
+        src_dev, fdt, bpe = to_rgb24(src_dev), torch.uint8, 1
     fshape = tuple(src_dev.shape[1:])
     L = []
     for ids in per:
         g = len(ids)
         bank = StreamBank(g, H, W)
         # pinned host frames of this lane's streams (one copy per lane only)
-        h_in = torch.empty((g,) + fshape, dtype=torch.float32, pin_memory=True)
+        h_in = torch.empty((g,) + fshape, dtype=fdt, pin_memory=True)
         h_in.copy_(src_dev[torch.tensor(ids, device=dev)])
         L.append(dict(
             ids=ids, bank=bank, stream=torch.cuda.Stream(device=dev),
-            h_in=h_in, h_out=torch.empty((g,) + fshape, dtype=torch.float32, pin_memory=True),
-            d_in=torch.empty((g,) + fshape, dtype=torch.float32, device=dev),
-            d_out=torch.empty((g,) + fshape, dtype=torch.float32, device=dev),
+            h_in=h_in, h_out=torch.empty((g,) + fshape, dtype=fdt, pin_memory=True),
+            d_in=torch.empty((g,) + fshape, dtype=fdt, device=dev),
+            d_out=torch.empty((g,) + fshape, dtype=fdt, device=dev),
             pk={s: torch.empty(c.arena.shape, dtype=torch.uint8).pin_memory()
                 for s, c in bank.codecs.items()},
             ln={s: torch.empty(c.lengths.shape, dtype=torch.int32).pin_memory()
@@ -533,7 +598,7 @@ def run_e2e(a, rank, world, local_rank) -> dict:
             with torch.cuda.stream(ln["stream"]):
                 c = bank.codecs[s]
                 ln["d_in"].copy_(ln["h_in"], non_blocking=True)
-                counters["h2d"] += ln["h_in"].numel() * 4
+                counters["h2d"] += ln["h_in"].numel() * bpe
                 parity = bank.step_idx & 1
                 c.set_gop_ids([k] * g)
                 c.encode(ln["d_in"], g, c.drop_k(a.drop))
@@ -554,7 +619,7 @@ def run_e2e(a, rank, world, local_rank) -> dict:
                     bank.last[i] = (s, parity, i)
                 bank.step_idx += 1
                 ln["h_out"].copy_(ln["d_out"], non_blocking=True)
-                counters["d2h"] += ln["h_out"].numel() * 4
+                counters["d2h"] += ln["h_out"].numel() * bpe
 
     def sync_all():
         for ln in L:
@@ -590,9 +655,10 @@ def run_e2e(a, rank, world, local_rank) -> dict:
             "d2h_bytes_per_step": int(counters["d2h"] // a.steps),
             "streams": total_streams(a, world, a.e2e_streams), "streams_this_rank": E,
             "lanes": lanes, "wall_s": round(wall, 3),
-            "path": "StreamBank public API on pinned host frames: frames H2D, packets D2H + "
-                    "H2D (network boundary), frames D2H, all inside the timed region; "
-                    f"{lanes} CUDA-stream lanes overlap PCIe directions with compute"}
+            "path": f"StreamBank public API on pinned host {'raw-rgb24' if rgb24 else 'float32'} "
+                    "frames: frames H2D, packets D2H + H2D (network boundary), frames D2H, all "
+                    f"inside the timed region; {lanes} CUDA-stream lanes overlap PCIe "
+                    "directions with compute"}
 
 
 # ---------------------------------------------------------------------------
@@ -1599,6 +1665,8 @@ def main():
             line["residual_layer"] = residual_leg(a, dev)
             if a.height == 1080 and a.width == 1920:
                 line["small_configs"] = small_configs(a, dev)
+        if world == 1 and not a.no_rgb24:
+            line["raw_rgb24"] = rgb24_leg(a, rank, world, local_rank, dev)
         if world == 1 and not a.no_learned:
             line["learned_tokenizer"] = run_learned(a, dev, "i8")
             if not a.no_learned_bf16:

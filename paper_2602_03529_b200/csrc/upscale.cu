@@ -748,6 +748,279 @@ static int launch_k5_v2(const CUtensorMap& imap, const UpArgs& a, const SstPrevD
   return SST_OK;
 }
 
+// ---- K5 raw-rgb24: float32 arithmetic, verified against the rint ties ----
+// A raw-rgb24 output byte is rint(float32(v * 255)) of the float64-exact
+// sample v (video.py:143), so v only has to be known well enough to decide
+// which side of a half-integer 255 v falls on.  The whole upscale + blend
+// runs in float32 FMA arithmetic (no float64, no XU conversions); a sample
+// whose estimate t' = 255 v' lies within tau of a half-integer takes the
+// float64 path (the reference's exact operation order, bilinear straight from
+// the smem windows) instead.  Bound: with samples in [0, 1] and float32
+// weights within 2^-25 of the reference's float64 ones, each bilinear pass
+// adds <= 2^-23 (two products, one sum, the weight error) so the upscale is
+// within 2^-22 of the real-number value and within 2^-22 + 2^-25 of the
+// reference's float32 result; a blend adds <= 5 * 2^-25; so
+// |t' - float32(255 v)| <= 255 (2^-22 + 6 * 2^-25) + 2 * 2^-17 < 1.3e-4 <
+// tau = 2^-12.  Outside the tau band the two roundings agree; inside it the
+// exact path decides (half-integers -- rint's ties -- included).  The band
+// holds ~0.05 % of samples.
+constexpr float kU8Tau = 0x1p-12f;
+
+struct UpU8Smem {
+  float win[3][UpTmaSmem<16>::kWin];       // I, P, previous P windows (row pitch kWF9)
+  RowTap ty_c[16], ty_p[16];
+  float2 wy_c[16], wy_p[16];               // float32 (1 - fy, fy) per row
+  int wx0[2], wx1[2];
+  int xs;
+  uint64_t bar;
+};
+
+// the reference's float32 upscale sample at one window position (codec.py:233-235, clip)
+__device__ __forceinline__ float exact_up(const float* win, int r_lo, int r_hi, const AxisTap& ty, int xl,
+                                          int xh, const AxisTap& tx) {
+  const float* w0 = win + r_lo * kWF9;
+  const float* w1 = win + r_hi * kWF9;
+  const double top = (double)w0[xl] * tx.g + (double)w0[xh] * tx.f;
+  const double bot = (double)w1[xl] * tx.g + (double)w1[xh] * tx.f;
+  return f32_clip_hi1(top * ty.g + bot * ty.f);
+}
+
+// t = v * 255 (float32) -> its rint byte (bits of t + 1.5 * 2^23) and whether t is within tau of a tie
+__device__ __forceinline__ uint32_t q8_check(float v, bool& near_tie) {
+  const float t = __fmul_rn(v, 255.0f);
+  const float m = __fadd_rn(t, 12582912.0f);
+  const float d = __fsub_rn(t, __fsub_rn(m, 12582912.0f));
+  near_tie |= fabsf(d) > 0.5f - kU8Tau;
+  return __float_as_uint(m) & 0xFFu;
+}
+
+template <bool kPrev, int kN>
+__global__ void __launch_bounds__(kV2Threads)
+    k_upscale_blend_u8f(const __grid_constant__ CUtensorMap imap, const __grid_constant__ UpArgs a) {
+  constexpr int kBand = 16;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  UpU8Smem& S = *reinterpret_cast<UpU8Smem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int q0 = blockIdx.x * kTQ;
+  const int oy0 = blockIdx.y * kBand;
+  const int g = blockIdx.z;
+  SstPrevDesc pd;
+  pd.p_img = nullptr;
+  pd.h = pd.w = pd.s = 1;
+  if (kPrev) pd = a.prev[g];
+  const bool has_prev = kPrev && pd.p_img != nullptr;
+  const int rows = min(kBand, a.H - oy0);
+  const int qlast = min(q0 + kTQ, a.W * 3) - 1;
+  if (tid < kBand) {
+    const AxisTap t = axis_tap(oy0 + min(tid, rows - 1), a.h, a.s);
+    S.ty_c[tid] = to_row(t);
+    S.wy_c[tid] = make_float2((float)t.g, (float)t.f);
+  } else if (tid < 2 * kBand) {
+    if (has_prev) {
+      const AxisTap t = axis_tap(oy0 + min(tid - kBand, rows - 1), pd.h, pd.s);
+      S.ty_p[tid - kBand] = to_row(t);
+      S.wy_p[tid - kBand] = make_float2((float)t.g, (float)t.f);
+    }
+  } else if (tid == 2 * kBand) {
+    S.wx0[0] = axis_tap(q0 / 3, a.w, a.s).lo;
+    S.wx1[0] = axis_tap(qlast / 3, a.w, a.s).hi;
+    S.xs = (S.wx0[0] * 3) & 3;
+    mbar_init(&S.bar, 1);
+    fence_mbar_init();
+  } else if (tid == 2 * kBand + 32 && has_prev) {
+    S.wx0[1] = axis_tap(q0 / 3, pd.w, pd.s).lo;
+    S.wx1[1] = axis_tap(qlast / 3, pd.w, pd.s).hi;
+  }
+  __syncthreads();
+  const int r0 = S.ty_c[0].lo;
+  const int pr0 = has_prev ? S.ty_p[0].lo : 0;
+  if (tid == 0) {
+    constexpr uint32_t kBox = UpTmaSmem<kBand>::kWR * kWF9 * sizeof(float);
+    mbar_expect_tx(&S.bar, 2 * kBox);
+    tma_load_3d(S.win[0], &imap, S.wx0[0] * 3 - S.xs, r0, 2 * g, &S.bar);
+    tma_load_3d(S.win[1], &imap, S.wx0[0] * 3 - S.xs, r0, 2 * g + 1, &S.bar);
+  }
+  if (has_prev) {
+    const int pr1 = S.ty_p[rows - 1].hi;
+    const int c0f = S.wx0[1] * 3, ncol = S.wx1[1] * 3 + 3 - c0f;
+    const int lane = tid & 31, wid = tid >> 5;
+    for (int j = wid; j <= pr1 - pr0; j += kV2Threads / 32) {
+      const float* src = pd.p_img + ((int64_t)(pr0 + j) * pd.w) * 3 + c0f;
+      float* dst = S.win[2] + j * kWF9;
+#pragma unroll
+      for (int c = lane; c < kWF; c += 32)
+        if (c < ncol) dst[c] = __ldg(src + c);
+    }
+  }
+  mbar_wait(&S.bar, 0);
+  __syncthreads();
+
+  const int qa0 = q0 + 2 * tid;
+  const bool col_ok = qa0 < a.W * 3;
+  AxisTap tx[2], txp[2];
+  int xl[2], xh[2], pxl[2] = {0, 0}, pxh[2] = {0, 0};
+  float gxf[2], fxf[2], gpf[2] = {0.f, 0.f}, fpf[2] = {0.f, 0.f};
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int q = min(qa0 + u, a.W * 3 - 1);
+    const int ox = q / 3, ch = q - ox * 3;
+    tx[u] = axis_tap(ox, a.w, a.s);
+    xl[u] = (tx[u].lo - S.wx0[0]) * 3 + ch + S.xs;
+    xh[u] = (tx[u].hi - S.wx0[0]) * 3 + ch + S.xs;
+    gxf[u] = (float)tx[u].g;
+    fxf[u] = (float)tx[u].f;
+    txp[u] = tx[u];
+    if (has_prev) {
+      txp[u] = axis_tap(ox, pd.w, pd.s);
+      pxl[u] = (txp[u].lo - S.wx0[1]) * 3 + ch;
+      pxh[u] = (txp[u].hi - S.wx0[1]) * 3 + ch;
+      gpf[u] = (float)txp[u].g;
+      fpf[u] = (float)txp[u].f;
+    }
+  }
+  float al[kN], be[kN];
+#pragma unroll
+  for (int f = 0; f < kN; ++f) {
+    al[f] = (float)a.alpha[f];
+    be[f] = (float)a.beta[f];
+  }
+  int ya = -1, yb = -1, qa = -1, qb = -1;
+  float ia[2] = {0, 0}, pa[2] = {0, 0}, ib[2] = {0, 0}, pb[2] = {0, 0}, qva[2] = {0, 0}, qvb[2] = {0, 0};
+  const int64_t orow = (int64_t)a.W * 3;
+  const int fsv = opaque_i32(a.H * a.W * 3);
+  uint8_t* obase = a.out8 + ((int64_t)g * kGop * a.H + oy0) * orow + qa0;
+  for (int r = 0; r < rows; ++r, obase += orow) {
+    const RowTap rt = S.ty_c[r];
+    const float2 wy = S.wy_c[r];
+    if (rt.lo != ya) {
+      if (rt.lo == yb) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) { ia[u] = ib[u]; pa[u] = pb[u]; }
+      } else {
+        const float* wi = &S.win[0][(rt.lo - r0) * kWF9];
+        const float* wp = &S.win[1][(rt.lo - r0) * kWF9];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          ia[u] = __fmaf_rn(wi[xl[u]], gxf[u], __fmul_rn(wi[xh[u]], fxf[u]));
+          pa[u] = __fmaf_rn(wp[xl[u]], gxf[u], __fmul_rn(wp[xh[u]], fxf[u]));
+        }
+      }
+      ya = rt.lo;
+    }
+    if (rt.hi != yb) {
+      if (rt.hi == ya) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) { ib[u] = ia[u]; pb[u] = pa[u]; }
+      } else {
+        const float* wi = &S.win[0][(rt.hi - r0) * kWF9];
+        const float* wp = &S.win[1][(rt.hi - r0) * kWF9];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          ib[u] = __fmaf_rn(wi[xl[u]], gxf[u], __fmul_rn(wi[xh[u]], fxf[u]));
+          pb[u] = __fmaf_rn(wp[xl[u]], gxf[u], __fmul_rn(wp[xh[u]], fxf[u]));
+        }
+      }
+      yb = rt.hi;
+    }
+    float ui[2], up[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      ui[u] = fminf(__fmaf_rn(ia[u], wy.x, __fmul_rn(ib[u], wy.y)), 1.0f);
+      up[u] = fminf(__fmaf_rn(pa[u], wy.x, __fmul_rn(pb[u], wy.y)), 1.0f);
+    }
+    bool tie = false;
+    uint32_t bf[kN][2], bp[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      bp[u] = q8_check(up[u], tie);
+      bf[0][u] = q8_check(ui[u], tie);
+    }
+    if (has_prev) {
+      const RowTap pt = S.ty_p[r];
+      const float2 wq = S.wy_p[r];
+      if (pt.lo != qa) {
+        if (pt.lo == qb) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) qva[u] = qvb[u];
+        } else {
+          const float* wv = &S.win[2][(pt.lo - pr0) * kWF9];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) qva[u] = __fmaf_rn(wv[pxl[u]], gpf[u], __fmul_rn(wv[pxh[u]], fpf[u]));
+        }
+        qa = pt.lo;
+      }
+      if (pt.hi != qb) {
+        if (pt.hi == qa) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) qvb[u] = qva[u];
+        } else {
+          const float* wv = &S.win[2][(pt.hi - pr0) * kWF9];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) qvb[u] = __fmaf_rn(wv[pxl[u]], gpf[u], __fmul_rn(wv[pxh[u]], fpf[u]));
+        }
+        qb = pt.hi;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const float qf = fminf(__fmaf_rn(qva[u], wq.x, __fmul_rn(qvb[u], wq.y)), 1.0f);
+#pragma unroll
+        for (int f = 0; f < kN; ++f)
+          bf[f][u] = q8_check(__fmaf_rn(al[f], qf, __fmul_rn(be[f], f == 0 ? ui[u] : up[u])), tie);
+      }
+    }
+    if (tie) {
+      // exact float64 path for this row's samples (codec.py:233-235, 289-293)
+      const AxisTap ty = from_row(rt);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const float eui = exact_up(S.win[0], ty.lo - r0, ty.hi - r0, ty, xl[u], xh[u], tx[u]);
+        const float eup = exact_up(S.win[1], ty.lo - r0, ty.hi - r0, ty, xl[u], xh[u], tx[u]);
+        bp[u] = rgb24_q(eup);
+        bf[0][u] = rgb24_q(eui);
+        if (has_prev) {
+          const AxisTap tp = from_row(S.ty_p[r]);
+          const float eq = exact_up(S.win[2], tp.lo - pr0, tp.hi - pr0, tp, pxl[u], pxh[u], txp[u]);
+          bf[0][u] = rgb24_q(blend_w<kN, 0>(eq, eui, a.alpha[0], a.beta[0]));
+          if constexpr (kN > 1) bf[kN > 1 ? 1 : 0][u] = rgb24_q(blend_w<kN, 1>(eq, eup, a.alpha[1], a.beta[1]));
+          if constexpr (kN > 2) bf[kN > 2 ? 2 : 0][u] = rgb24_q(blend_w<kN, 2>(eq, eup, a.alpha[2], a.beta[2]));
+          if constexpr (kN > 3) bf[kN > 3 ? 3 : 0][u] = rgb24_q(blend_w<kN, 3>(eq, eup, a.alpha[3], a.beta[3]));
+        }
+      }
+    }
+    if (col_ok) {
+      const unsigned short p8 = (unsigned short)(bp[0] | (bp[1] << 8));
+      __stcs(reinterpret_cast<unsigned short*>(obase), (unsigned short)(bf[0][0] | (bf[0][1] << 8)));
+#pragma unroll
+      for (int f = 1; f < kGop; ++f) {
+        const unsigned short v = (has_prev && f < kN)
+                                     ? (unsigned short)(bf[f < kN ? f : 0][0] | (bf[f < kN ? f : 0][1] << 8))
+                                     : p8;
+        __stcs(reinterpret_cast<unsigned short*>(frame_ptr(obase, fsv, f)), v);
+      }
+    }
+  }
+}
+
+static int launch_k5_u8f(const CUtensorMap& imap, const UpArgs& a, const SstPrevDesc* prev, int blend_n,
+                         cudaStream_t st) {
+  dim3 grid(ceil_div(a.W * 3, kTQ), ceil_div(a.H, 16), a.G);
+  if (grid.y > 65535) return SST_ERR_ARG;
+  const int smem = (int)sizeof(UpU8Smem);
+  auto kern = k_upscale_blend_u8f<false, 1>;
+  if (prev) {
+    switch (blend_n) {
+      case 1: kern = k_upscale_blend_u8f<true, 1>; break;
+      case 2: kern = k_upscale_blend_u8f<true, 2>; break;
+      case 3: kern = k_upscale_blend_u8f<true, 3>; break;
+      default: kern = k_upscale_blend_u8f<true, 4>; break;
+    }
+  }
+  SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<grid, kV2Threads, smem, st>>>(imap, a);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
 // ---- K5-9: all 9 frames per CTA, direct stores ----
 // A CTA owns a band of kBand output rows x kTQ output floats of one GoP.  It
 // loads the source windows of the GoP's 9 working frames (and of the previous
@@ -1311,7 +1584,8 @@ extern "C" int sst_upscale_blend_u8(const float* img, int G, int h, int w, int s
   if (!(var && !strcmp(var, "v1")) && (W * 3) % 2 == 0 && (reinterpret_cast<uintptr_t>(out) & 1u) == 0 &&
       make_tmap_f32_3d(&imap, img, (uint64_t)w * 3, (uint64_t)h, (uint64_t)G * 2, kWF9,
                        UpTmaSmem<16>::kWR))
-    return launch_k5_v2<16, uint8_t>(imap, a, prev, blend_n, st);
+    return (var && !strcmp(var, "v2")) ? launch_k5_v2<16, uint8_t>(imap, a, prev, blend_n, st)
+                                       : launch_k5_u8f(imap, a, prev, blend_n, st);
   dim3 grid(ceil_div(W * 3, kUpThreads), ceil_div(H, kUpRows), G);
   if (grid.y > 65535) return SST_ERR_ARG;
   k_upscale_blend<uint8_t><<<grid, kUpThreads, 0, st>>>(a);
