@@ -344,8 +344,9 @@ def run_ours(a, rank, world, local_rank, rgb24: bool = False):
             if cuts[j + 1] > cuts[j]:
                 lanes.append(dict(sl=slice(cuts[j], cuts[j + 1]), phase=phase,
                                   n=cuts[j + 1] - cuts[j]))
+    fused = not rgb24 and os.environ.get("SST_BENCH_FUSED", "0") == "1"
     for ln in lanes:
-        ln["bank"] = StreamBank(ln["n"], H, W, concurrent_groups=False)
+        ln["bank"] = StreamBank(ln["n"], H, W, concurrent_groups=False, fused=fused)
         ln["stream"] = torch.cuda.Stream(device=dev)
 
     class _Banks:                       # aggregate view for launch counting / timers

@@ -91,6 +91,17 @@ typedef struct SstPrevDesc {
   int32_t reserved;
 } SstPrevDesc;
 
+/* The previous GoP's token matrices for the decoder-fused reconstruction
+ * (sst_upscale_blend_tok): its I and P tokens [2][Ht][Wt][12] float64, the
+ * validity of its P tokens [Ht][Wt] (0 = concealed by the I block), and its
+ * working geometry. */
+typedef struct SstPrevTokDesc {
+  const double* tok;       /* NULL = first GoP of its stream, no blend */
+  const uint8_t* pvalid;
+  int32_t h, w, s, Ht, Wt;
+  int32_t reserved;
+} SstPrevTokDesc;
+
 SST_API int sst_abi_version(void);
 
 /* Wire size of one token packet: transport.py:221-226 token_packet_wire_size. */
@@ -243,6 +254,16 @@ SST_API int sst_reassemble(const uint8_t* buf, const int64_t* off, SstPacketInfo
  *   ws: device workspace of sst_unpack_decode_workspace(G, H', W') bytes
  *   (16-byte aligned); out: [G][2][h][w][3] float32 (I image, concealed P). */
 SST_API int64_t sst_unpack_decode_workspace(int G, int Ht, int Wt);
+/* The receiver's reassemble x 2 + TokenPacket.dequantized (transport.py:
+ * 108-112, 274-305) WITHOUT the IDCT: dequantised I / P token matrices
+ * tok [G][2][Ht][Wt][12] float64 (missing rows / tokens 0) and the P
+ * validity pvalid [G][Ht][Wt] -- the input of sst_upscale_blend_tok, which
+ * runs decode_gop's IDCT + concealment inside the reconstruction.  Same
+ * routing, first-wins and stats as sst_unpack_decode (same workspace). */
+SST_API int sst_unpack_tokens(const uint8_t* buf, const int64_t* off, SstPacketInfo* info,
+               const int32_t* target, int64_t n, int G, int Ht, int Wt, const uint32_t* exp_gop,
+               uint32_t* winner, int32_t* stats, void* ws, double* tok, uint8_t* pvalid, void* stream);
+
 SST_API int sst_unpack_decode(const uint8_t* buf, const int64_t* off, SstPacketInfo* info,
                               const int32_t* target, int64_t n, int G, int Ht, int Wt, int h, int w,
                               const uint32_t* exp_gop, uint32_t* winner, int32_t* stats, void* ws,
@@ -259,6 +280,19 @@ SST_API int sst_unpack_decode(const uint8_t* buf, const int64_t* off, SstPacketI
  *   out: [G][9][H][W][3]. */
 SST_API int sst_upscale_blend(const float* img, int G, int h, int w, int s, int H, int W,
                       const SstPrevDesc* prev, int blend_n, float* out, void* stream);
+
+/* sst_upscale_blend with decode_gop fused in (codec.py:131-140,160-186 +
+ * 217-296): reads the dequantised token matrices of sst_unpack_tokens and,
+ * per output band, runs the 4-coefficient IDCT, clip and I-concealment of
+ * exactly the working-image window it upscales (and of the previous GoP's P
+ * window, from its tokens), so the working images never round-trip through
+ * HBM.  Output bit-identical to sst_unpack_decode + sst_upscale_blend.
+ *   tok [G][2][Ht][Wt][12], pvalid [G][Ht][Wt]; prev: DEVICE
+ *   SstPrevTokDesc[G] or NULL (blend_n <= 4); out [G][9][H][W][3] float32,
+ *   8-byte aligned, W*3 even (else SST_ERR_UNSUPPORTED). */
+SST_API int sst_upscale_blend_tok(const double* tok, const uint8_t* pvalid, int G, int Ht, int Wt,
+                      int h, int w, int s, int H, int W, const SstPrevTokDesc* prev, int blend_n,
+                      float* out, void* stream);
 
 /* sst_upscale_blend with raw-rgb24 output: every output sample v is written
  * as the byte write_raw_video stores for it (video.py:139-143,

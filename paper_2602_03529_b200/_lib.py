@@ -38,6 +38,11 @@ class SstPrevDesc(C.Structure):
                 ("reserved", C.c_int32)]
 
 
+class SstPrevTokDesc(C.Structure):
+    _fields_ = [("tok", C.c_void_p), ("pvalid", C.c_void_p), ("h", C.c_int32), ("w", C.c_int32),
+                ("s", C.c_int32), ("Ht", C.c_int32), ("Wt", C.c_int32), ("reserved", C.c_int32)]
+
+
 class SstConvDesc(C.Structure):
     """include/semstream_b200.h SstConvDesc (learned tokenizer, one conv layer)."""
     _fields_ = [("in_", C.c_void_p), ("in_C", C.c_int32), ("in_W", C.c_int32),
@@ -56,6 +61,7 @@ LT_EPI_STORE, LT_EPI_FSQ, LT_EPI_PIXELS, LT_EPI_PIXELS_U8 = 0, 1, 2, 3
 
 INFO_BYTES = C.sizeof(SstPacketInfo)          # 64
 PREV_BYTES = C.sizeof(SstPrevDesc)            # 24
+PREVTOK_BYTES = C.sizeof(SstPrevTokDesc)      # 40
 
 _P = C.c_void_p
 _I = C.c_int
@@ -84,6 +90,8 @@ SIGNATURES = {
     "sst_reassemble": (_I, [_P, _P, _P, _P, _L, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
     "sst_unpack_decode_workspace": (_L, [_I, _I, _I]),
     "sst_unpack_decode": (_I, [_P, _P, _P, _P, _L, _I, _I, _I, _I, _I, _P, _P, _P, _P, _P, _P]),
+    "sst_unpack_tokens": (_I, [_P, _P, _P, _P, _L, _I, _I, _I, _P, _P, _P, _P, _P, _P, _P]),
+    "sst_upscale_blend_tok": (_I, [_P, _P, _I, _I, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P]),
     "sst_upscale_blend": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P]),
     "sst_upscale_blend_u8": (_I, [_P, _I, _I, _I, _I, _I, _I, _P, _I, _P, _P]),
     "sst_mse": (_I, [_P, _P, _L, _L, _P, _P]),
@@ -172,6 +180,9 @@ try:
                             ("dqrange", "<f8")])
     PREV_DTYPE = _np.dtype([("p_img", "<u8"), ("h", "<i4"), ("w", "<i4"), ("s", "<i4"),
                             ("reserved", "<i4")])
+    PREVTOK_DTYPE = _np.dtype([("tok", "<u8"), ("pvalid", "<u8"), ("h", "<i4"), ("w", "<i4"),
+                               ("s", "<i4"), ("Ht", "<i4"), ("Wt", "<i4"), ("reserved", "<i4")])
     assert INFO_DTYPE.itemsize == INFO_BYTES and PREV_DTYPE.itemsize == PREV_BYTES
+    assert PREVTOK_DTYPE.itemsize == PREVTOK_BYTES
 except ImportError:  # pragma: no cover
     pass

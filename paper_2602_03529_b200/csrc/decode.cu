@@ -225,6 +225,30 @@ __global__ void __launch_bounds__(kDecThreads) k_decode(DecArgs a) {
   }
 }
 
+// ---- packets -> dequantised token matrices (for K5 with the decoder fused) ----
+// reassemble x 2 + TokenPacket.dequantized (transport.py:108-112,274-305):
+// the I and P token matrices [G][2][Ht][Wt][12] float64 (missing rows and
+// tokens 0) and the P validity [G][Ht][Wt] -- what K4b's gather stage holds
+// in shared memory, written out so that the IDCT can run inside K5
+// (sst_upscale_blend_tok) right where the working image is consumed.
+__global__ void k_unpack_tok(const uint8_t* __restrict__ buf, const RowInfo* __restrict__ rows,
+                             const int32_t* __restrict__ tokoff, int Ht, int Wt, double* __restrict__ tok,
+                             uint8_t* __restrict__ pvalid) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= Wt * kChannels) return;
+  const int tx = e / kChannels, c = e - tx * kChannels;
+  const int ty = blockIdx.y, m = blockIdx.z;                  // m = 2 g + im
+  const int64_t r = (int64_t)m * Ht + ty;
+  const int slot = tokoff[r * Wt + tx];
+  double v = 0.0;
+  if (slot >= 0) {
+    const RowInfo& ri = rows[r];
+    v = ri.qmin + (double)buf[ri.payload + (int64_t)slot * kChannels + c] * ri.step;
+  }
+  tok[(r * Wt + tx) * kChannels + c] = v;
+  if ((m & 1) && c == 0) pvalid[((int64_t)(m >> 1) * Ht + ty) * Wt + tx] = slot >= 0 ? 1 : 0;
+}
+
 int route_packets(SstPacketInfo* info, const int32_t* target, int64_t n, int m, int Ht,
                   const uint8_t* exp_kind, const uint32_t* exp_gop, uint32_t* winner,
                   int32_t* stats, cudaStream_t st);
@@ -253,6 +277,31 @@ extern "C" int sst_decode(const double* i_tok, const double* p_tok, int64_t tok_
 extern "C" int64_t sst_unpack_decode_workspace(int G, int Ht, int Wt) {
   const int64_t rows = 2 * (int64_t)G * Ht;
   return rows * (int64_t)sizeof(RowInfo) + rows * Wt * 4;
+}
+
+extern "C" int sst_unpack_tokens(const uint8_t* buf, const int64_t* off, SstPacketInfo* info,
+                                 const int32_t* target, int64_t n, int G, int Ht, int Wt,
+                                 const uint32_t* exp_gop, uint32_t* winner, int32_t* stats, void* ws,
+                                 double* tok, uint8_t* pvalid, void* stream) {
+  if (n < 0 || G < 0 || Ht <= 0 || Wt <= 0) return SST_ERR_ARG;
+  if (G == 0) return SST_OK;
+  if (!exp_gop || !winner || !stats || !tok || !pvalid || !ws) return SST_ERR_ARG;
+  if (n > 0 && (!buf || !off || !info || !target)) return SST_ERR_ARG;
+  if (Ht > 65535 || G > 32767) return SST_ERR_ARG;
+  if (reinterpret_cast<uintptr_t>(ws) & 15) return SST_ERR_ARG;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  int rc = route_packets(info, target, n, 2 * G, Ht, nullptr, exp_gop, winner, stats, st);
+  if (rc != SST_OK) return rc;
+  const int64_t nrows = 2 * (int64_t)G * Ht;
+  RowInfo* rows = static_cast<RowInfo*>(ws);
+  int32_t* tokoff = reinterpret_cast<int32_t*>(rows + nrows);
+  k_rowprep<<<(unsigned)ceil_div64(nrows, 8), 256, 0, st>>>(off, info, buf, winner, nrows, Ht, Wt,
+                                                            rows, tokoff, stats);
+  SST_LAUNCH_CHECK();
+  dim3 grid(ceil_div(Wt * kChannels, 256), Ht, 2 * G);
+  k_unpack_tok<<<grid, 256, 0, st>>>(buf, rows, tokoff, Ht, Wt, tok, pvalid);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
 }
 
 extern "C" int sst_unpack_decode(const uint8_t* buf, const int64_t* off, SstPacketInfo* info,

@@ -17,6 +17,7 @@
 #include <type_traits>
 
 #include "common.cuh"
+#include "dct8.cuh"
 #include "tma.cuh"
 
 namespace sst {
@@ -1021,6 +1022,262 @@ static int launch_k5_u8f(const CUtensorMap& imap, const UpArgs& a, const SstPrev
   return SST_OK;
 }
 
+// ---- K5 with the decoder fused: working-image windows decoded in smem ----
+// k_upscale_blend_v2's body over windows that are not loaded but DECODED
+// in place from the dequantised token matrices (sst_unpack_tokens): per
+// 16-row band the <= 3 x 7 blocks under the window get decode_gop's
+// column IDCT (coefficients (0,0) (1,0) (2,0) in column 0, (0,1) in column
+// 1, fct 1/16; the all-zero columns share one result), then the row IDCT of
+// exactly the window rows, clip, float32 and the I-concealment of invalid
+// P blocks -- K4b's operation sequence (decode.cu k_decode), so the
+// windows equal the working images bit for bit.  The previous GoP's P
+// window is decoded the same way from its own tokens.  Tokens are 1.5
+// bytes per working pixel against 12 for the float32 images: the DRAM
+// reads interleaved with K5's 9-frame write stream (which cost ~0.17 ms per
+// 32-GoP launch, §5 of DESIGN.md) mostly disappear.  Measured (bench, 64 x
+// 1080p streams): 1.49 ms per launch against v2's 1.21 ms (K4 0.13 -> 0.04
+// ms): the per-band IDCT prologue (~1300 8-point DCTs per CTA, two
+// dependent passes behind barriers) costs more than the reads it saves, so
+// StreamBank keeps the unfused path by default (fused=True selects this).
+// Overlapping the next band's decode with the current band's stores
+// (persistent CTAs) is the open step.
+constexpr int kTokBR = 3, kTokBC = 7, kTokNB = kTokBR * kTokBC;   // max blocks under a window
+
+struct UpTokArgs {
+  const double* tok;            // [G][2][Ht][Wt][12]
+  const uint8_t* pvalid;        // [G][Ht][Wt]
+  int G, Ht, Wt, h, w, s, H, W;
+  const SstPrevTokDesc* prev;   // [G] or null
+  int n;
+  double alpha[4], beta[4];
+};
+
+struct UpTokSmem {
+  float win[3][UpTmaSmem<16>::kWin];      // I, P, previous P windows (row pitch kWF9)
+  double tk[2][kTokNB][kChannels];        // tokens of the image pair being decoded
+  double s1[2][kTokNB][3][2][8];          // column IDCTs, block columns x = 0, 1
+  double zc[8];                           // column IDCT of an all-zero column
+  uint8_t valid[kTokNB];
+  RowTap ty_c[16], ty_p[16];
+  int wx0[2], wx1[2];
+};
+
+// decode_gop (codec.py:131-140,160-186) of the window rows r0..r1, columns
+// c0..c1 (working pixels) of one GoP's I / concealed-P pair into winI (may
+// be null) and winP
+__device__ __forceinline__ void k5t_decode_pair(UpTokSmem& S, const double* tok, const uint8_t* pval, int Ht,
+                                                int Wt, int r0, int r1, int c0, int c1, float* winI, float* winP,
+                                                int tid, int nt) {
+  const int br0 = r0 >> 3, bc0 = c0 >> 3;
+  const int nbr = (r1 >> 3) - br0 + 1, nbc = (c1 >> 3) - bc0 + 1, nb = nbr * nbc;
+  const int64_t img = (int64_t)Ht * Wt * kChannels;
+  for (int e = tid; e < 2 * nb * kChannels; e += nt) {
+    const int im = e / (nb * kChannels), b = (e / kChannels) % nb, c = e % kChannels;
+    const int br = br0 + b / nbc, bc = bc0 + b % nbc;
+    S.tk[im][b][c] = tok[im * img + ((int64_t)br * Wt + bc) * kChannels + c];
+  }
+  for (int b = tid; b < nb; b += nt) S.valid[b] = pval[(int64_t)(br0 + b / nbc) * Wt + bc0 + b % nbc];
+  __syncthreads();
+  for (int it = tid; it < 2 * nb * 6; it += nt) {          // (image, block, channel, column)
+    const int im = it / (nb * 6), b = (it / 6) % nb, ch = (it / 2) % 3, x = it & 1;
+    double c[8];
+#pragma unroll
+    for (int y = 0; y < 8; ++y) c[y] = 0.0;
+    const double* v = S.tk[im][b] + ch * 4;
+    if (x == 0) { c[0] = v[0]; c[1] = v[2]; c[2] = v[3]; }
+    else { c[0] = v[1]; }
+    dct3_8<true>(c, 1.0 / 16.0);
+#pragma unroll
+    for (int y = 0; y < 8; ++y) S.s1[im][b][ch][x][y] = c[y];
+  }
+  __syncthreads();
+  const int nr = r1 - r0 + 1;
+  for (int it = tid; it < nr * nbc * 3; it += nt) {        // (window row, block column, channel)
+    const int r = it / (nbc * 3), bci = (it / 3) % nbc, ch = it % 3;
+    const int R = r0 + r, y = R & 7;
+    const int b = ((R >> 3) - br0) * nbc + bci;
+    double ci[8], cp[8];
+    ci[0] = S.s1[0][b][ch][0][y]; ci[1] = S.s1[0][b][ch][1][y];
+    cp[0] = S.s1[1][b][ch][0][y]; cp[1] = S.s1[1][b][ch][1][y];
+    const double z = S.zc[y];
+#pragma unroll
+    for (int x = 2; x < 8; ++x) { ci[x] = z; cp[x] = z; }
+    dct3_8<false>(ci, 1.0);
+    dct3_8<false>(cp, 1.0);
+    const bool keep_p = S.valid[b] != 0;
+    const int px0 = (bc0 + bci) * 8;
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+      const int px = px0 + x;
+      if (px < c0 || px > c1) continue;
+      const double iv = clip01(ci[x]);
+      const double pv = keep_p ? clip01(cp[x]) : iv;
+      const int col = r * kWF9 + (px - c0) * 3 + ch;
+      if (winI != nullptr) winI[col] = (float)iv;
+      winP[col] = (float)pv;
+    }
+  }
+}
+
+template <bool kPrev, int kN>
+__global__ void __launch_bounds__(kV2Threads)
+    k_upscale_blend_tok(const __grid_constant__ UpTokArgs t, float* __restrict__ out) {
+  constexpr int kBand = 16;
+  extern __shared__ __align__(128) uint8_t smem_raw[];
+  UpTokSmem& S = *reinterpret_cast<UpTokSmem*>(smem_raw);
+  const int tid = threadIdx.x;
+  const int q0 = blockIdx.x * kTQ;
+  const int oy0 = blockIdx.y * kBand;
+  const int g = blockIdx.z;
+  SstPrevTokDesc pd;
+  pd.tok = nullptr;
+  pd.pvalid = nullptr;
+  pd.h = pd.w = pd.s = pd.Ht = pd.Wt = 1;
+  if (kPrev) pd = t.prev[g];
+  const bool has_prev = kPrev && pd.tok != nullptr;
+  const int rows = min(kBand, t.H - oy0);
+  const int qlast = min(q0 + kTQ, t.W * 3) - 1;
+  if (tid < kBand) S.ty_c[tid] = to_row(axis_tap(oy0 + min(tid, rows - 1), t.h, t.s));
+  else if (tid < 2 * kBand) {
+    if (has_prev) S.ty_p[tid - kBand] = to_row(axis_tap(oy0 + min(tid - kBand, rows - 1), pd.h, pd.s));
+  } else if (tid == 2 * kBand) {
+    S.wx0[0] = axis_tap(q0 / 3, t.w, t.s).lo;
+    S.wx1[0] = axis_tap(qlast / 3, t.w, t.s).hi;
+    double c[8];
+#pragma unroll
+    for (int y = 0; y < 8; ++y) c[y] = 0.0;
+    dct3_8<true>(c, 1.0 / 16.0);
+#pragma unroll
+    for (int y = 0; y < 8; ++y) S.zc[y] = c[y];
+  } else if (tid == 2 * kBand + 32 && has_prev) {
+    S.wx0[1] = axis_tap(q0 / 3, pd.w, pd.s).lo;
+    S.wx1[1] = axis_tap(qlast / 3, pd.w, pd.s).hi;
+  }
+  __syncthreads();
+  const int r0 = S.ty_c[0].lo;
+  const int pr0 = has_prev ? S.ty_p[0].lo : 0;
+  k5t_decode_pair(S, t.tok + (int64_t)g * 2 * t.Ht * t.Wt * kChannels, t.pvalid + (int64_t)g * t.Ht * t.Wt,
+                  t.Ht, t.Wt, r0, S.ty_c[rows - 1].hi, S.wx0[0], S.wx1[0], S.win[0], S.win[1], tid, kV2Threads);
+  if (has_prev) {
+    __syncthreads();                                  // tk / s1 reused
+    k5t_decode_pair(S, pd.tok, pd.pvalid, pd.Ht, pd.Wt, pr0, S.ty_p[rows - 1].hi, S.wx0[1], S.wx1[1],
+                    nullptr, S.win[2], tid, kV2Threads);
+  }
+  __syncthreads();
+
+  // ---- k_upscale_blend_v2's body (windows start at column wx0, no shift) ----
+  const int qa0 = q0 + 2 * tid;
+  const bool col_ok = qa0 < t.W * 3;
+  AxisTap tx[2], txp[2];
+  int xl[2], xh[2], pxl[2] = {0, 0}, pxh[2] = {0, 0};
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const int q = min(qa0 + u, t.W * 3 - 1);
+    const int ox = q / 3, ch = q - ox * 3;
+    tx[u] = axis_tap(ox, t.w, t.s);
+    xl[u] = (tx[u].lo - S.wx0[0]) * 3 + ch;
+    xh[u] = (tx[u].hi - S.wx0[0]) * 3 + ch;
+    txp[u] = tx[u];
+    if (has_prev) {
+      txp[u] = axis_tap(ox, pd.w, pd.s);
+      pxl[u] = (txp[u].lo - S.wx0[1]) * 3 + ch;
+      pxh[u] = (txp[u].hi - S.wx0[1]) * 3 + ch;
+    }
+  }
+  int ya = -1, yb = -1, qa = -1, qb = -1;
+  double ia[2] = {0, 0}, pa[2] = {0, 0}, ib[2] = {0, 0}, pb[2] = {0, 0};
+  double qva[2] = {0, 0}, qvb[2] = {0, 0};
+  const int64_t orow = (int64_t)t.W * 3;
+  const int fsv = opaque_i32(t.H * t.W * 3);
+  float* obase = out + ((int64_t)g * kGop * t.H + oy0) * orow + qa0;
+  for (int r = 0; r < rows; ++r, obase += orow) {
+    const AxisTap ty = from_row(S.ty_c[r]);
+    if (ty.lo != ya) {
+      if (ty.lo == yb) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) { ia[u] = ib[u]; pa[u] = pb[u]; }
+      } else {
+        const float* wi = &S.win[0][(ty.lo - r0) * kWF9];
+        const float* wp = &S.win[1][(ty.lo - r0) * kWF9];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          ia[u] = (double)wi[xl[u]] * tx[u].g + (double)wi[xh[u]] * tx[u].f;   // codec.py:233
+          pa[u] = (double)wp[xl[u]] * tx[u].g + (double)wp[xh[u]] * tx[u].f;
+        }
+      }
+      ya = ty.lo;
+    }
+    if (ty.hi != yb) {
+      if (ty.hi == ya) {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) { ib[u] = ia[u]; pb[u] = pa[u]; }
+      } else {
+        const float* wi = &S.win[0][(ty.hi - r0) * kWF9];
+        const float* wp = &S.win[1][(ty.hi - r0) * kWF9];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          ib[u] = (double)wi[xl[u]] * tx[u].g + (double)wi[xh[u]] * tx[u].f;
+          pb[u] = (double)wp[xl[u]] * tx[u].g + (double)wp[xh[u]] * tx[u].f;
+        }
+      }
+      yb = ty.hi;
+    }
+    float ui[2], up[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      ui[u] = f32_clip_hi1(ia[u] * ty.g + ib[u] * ty.f);     // codec.py:235
+      up[u] = f32_clip_hi1(pa[u] * ty.g + pb[u] * ty.f);
+    }
+    float fv[kN][2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) fv[0][u] = ui[u];
+    if (has_prev) {
+      const AxisTap tp = from_row(S.ty_p[r]);
+      if (tp.lo != qa) {
+        if (tp.lo == qb) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) qva[u] = qvb[u];
+        } else {
+          const float* wq = &S.win[2][(tp.lo - pr0) * kWF9];
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+            qva[u] = (double)wq[pxl[u]] * txp[u].g + (double)wq[pxh[u]] * txp[u].f;
+        }
+        qa = tp.lo;
+      }
+      if (tp.hi != qb) {
+        if (tp.hi == qa) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) qvb[u] = qva[u];
+        } else {
+          const float* wq = &S.win[2][(tp.hi - pr0) * kWF9];
+#pragma unroll
+          for (int u = 0; u < 2; ++u)
+            qvb[u] = (double)wq[pxl[u]] * txp[u].g + (double)wq[pxh[u]] * txp[u].f;
+        }
+        qb = tp.hi;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {            // codec.py:289-293
+        const float qf = f32_clip_hi1(qva[u] * tp.g + qvb[u] * tp.f);
+        fv[0][u] = blend_w<kN, 0>(qf, ui[u], t.alpha[0], t.beta[0]);
+        if constexpr (kN > 1) fv[kN > 1 ? 1 : 0][u] = blend_w<kN, 1>(qf, up[u], t.alpha[1], t.beta[1]);
+        if constexpr (kN > 2) fv[kN > 2 ? 2 : 0][u] = blend_w<kN, 2>(qf, up[u], t.alpha[2], t.beta[2]);
+        if constexpr (kN > 3) fv[kN > 3 ? 3 : 0][u] = blend_w<kN, 3>(qf, up[u], t.alpha[3], t.beta[3]);
+      }
+    }
+    if (col_ok) {
+      __stcs(reinterpret_cast<float2*>(obase), make_float2(fv[0][0], fv[0][1]));
+#pragma unroll
+      for (int f = 1; f < kGop; ++f) {
+        const float2 v = (has_prev && f < kN) ? make_float2(fv[f < kN ? f : 0][0], fv[f < kN ? f : 0][1])
+                                              : make_float2(up[0], up[1]);
+        __stcs(reinterpret_cast<float2*>(frame_ptr(obase, fsv, f)), v);
+      }
+    }
+  }
+}
+
 // ---- K5-9: all 9 frames per CTA, direct stores ----
 // A CTA owns a band of kBand output rows x kTQ output floats of one GoP.  It
 // loads the source windows of the GoP's 9 working frames (and of the previous
@@ -1550,6 +1807,50 @@ extern "C" int sst_upscale_blend(const float* img, int G, int h, int w, int s, i
   dim3 grid(ceil_div(W * 3, kUpThreads), ceil_div(H, kUpRows), G);
   if (grid.y > 65535) return SST_ERR_ARG;
   k_upscale_blend<float><<<grid, kUpThreads, 0, st>>>(a);
+  SST_LAUNCH_CHECK();
+  return SST_OK;
+}
+
+extern "C" int sst_upscale_blend_tok(const double* tok, const uint8_t* pvalid, int G, int Ht, int Wt,
+                                     int h, int w, int s, int H, int W, const SstPrevTokDesc* prev,
+                                     int blend_n, float* out, void* stream) {
+  if (G < 0 || h <= 0 || w <= 0 || H <= 0 || W <= 0) return SST_ERR_ARG;
+  if (s != 2 && s != 3) return SST_ERR_ARG;
+  if (H > h * s || W > w * s) return SST_ERR_ARG;
+  if (Ht != ceil_div(h, kBlock) || Wt != ceil_div(w, kBlock)) return SST_ERR_ARG;
+  if (blend_n < 1 || blend_n > 8) return SST_ERR_ARG;
+  if (prev && blend_n > 4) return SST_ERR_UNSUPPORTED;
+  if (G == 0) return SST_OK;
+  if (!tok || !pvalid || !out) return SST_ERR_ARG;
+  if (G > 65535) return SST_ERR_ARG;
+  if ((W * 3) % 2 != 0 || (reinterpret_cast<uintptr_t>(out) & 7u) != 0) return SST_ERR_UNSUPPORTED;
+  UpTokArgs t{};
+  t.tok = tok; t.pvalid = pvalid;
+  t.G = G; t.Ht = Ht; t.Wt = Wt; t.h = h; t.w = w; t.s = s; t.H = H; t.W = W;
+  t.prev = prev; t.n = blend_n;
+  for (int i = 1; i <= 4; ++i) {
+    t.alpha[i - 1] = (double)(blend_n - i) / (double)blend_n;
+    t.beta[i - 1] = 1.0 - t.alpha[i - 1];
+  }
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  dim3 grid(ceil_div(W * 3, kTQ), ceil_div(H, 16), G);
+  if (grid.y > 65535) return SST_ERR_ARG;
+  // no residency cap: the per-band decode prologue wants CTAs in flight
+  // (measured 1.49 ms per 32-GoP launch uncapped, 1.66 ms at v2's 4 CTAs/SM);
+  // SST_K5T_SMEM raises the dynamic-smem request (A/B)
+  const char* es = getenv("SST_K5T_SMEM");
+  const int smem = std::max((int)sizeof(UpTokSmem), es ? atoi(es) : 0);
+  auto kern = k_upscale_blend_tok<false, 1>;
+  if (prev) {
+    switch (blend_n) {
+      case 1: kern = k_upscale_blend_tok<true, 1>; break;
+      case 2: kern = k_upscale_blend_tok<true, 2>; break;
+      case 3: kern = k_upscale_blend_tok<true, 3>; break;
+      default: kern = k_upscale_blend_tok<true, 4>; break;
+    }
+  }
+  SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  kern<<<grid, kV2Threads, smem, st>>>(t, out);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }

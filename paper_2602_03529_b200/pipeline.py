@@ -145,6 +145,11 @@ class GopCodec:
         # previous GoP's P image for boundary blending
         self.img = [torch.empty((G, 2, self.h, self.w, 3), dtype=torch.float32, device=dev)
                     for _ in range(2)]
+        # decoder-fused reconstruction (sst_unpack_tokens + sst_upscale_blend_tok):
+        # double-buffered dequantised token matrices + P validity, allocated on
+        # first use
+        self.tokq = None
+        self.pvalid = None
         self.n = n
         self.timer = _NO_TIMER
         self._id_ring = _DescRing(3 * G * 4)
@@ -213,9 +218,12 @@ class GopCodec:
 
     # -- receiver ------------------------------------------------------
     def decode(self, g: int, parity: int, arena: torch.Tensor | None = None,
-               present: torch.Tensor | None = None) -> torch.Tensor:
+               present: torch.Tensor | None = None, fused: bool = False) -> torch.Tensor | None:
         """K4: parse + first-wins reassembly + mask-aware decode of the packet
-        slots of g GoPs; returns the [g, 2, h, w, 3] working images."""
+        slots of g GoPs; returns the [g, 2, h, w, 3] working images.  fused:
+        stop before the IDCT -- the dequantised token matrices and P validity
+        go to ``tokq[parity]`` / ``pvalid[parity]`` for ``reconstruct(...,
+        fused=True)``, which decodes inside K5 (returns None)."""
         st = _dev.stream()
         arena = self.arena if arena is None else arena
         npk = g * self.n_pkt_per_gop
@@ -226,6 +234,21 @@ class GopCodec:
                   self.lengths.data_ptr(), None if present is None else present.data_ptr(), npk,
                   self.info.data_ptr(), st)
         tm.end("K4_parse")
+        if fused:
+            if self.tokq is None:
+                dev = _dev.device()
+                self.tokq = [torch.empty((self.g_max, 2, self.Ht, self.Wt, CHANNELS),
+                                         dtype=torch.float64, device=dev) for _ in range(2)]
+                self.pvalid = [torch.empty((self.g_max, self.Ht, self.Wt), dtype=torch.uint8,
+                                           device=dev) for _ in range(2)]
+            tm.begin("K4_unpack_decode")
+            _lib.call("sst_unpack_tokens", arena.data_ptr(), self.offsets.data_ptr(),
+                      self.info.data_ptr(), self.target.data_ptr(), npk, g, self.Ht, self.Wt,
+                      self.exp_gop.data_ptr(), self.winner.data_ptr(), self.stats.data_ptr(),
+                      self.dec_ws.data_ptr(), self.tokq[parity].data_ptr(),
+                      self.pvalid[parity].data_ptr(), st)
+            tm.end("K4_unpack_decode")
+            return None
         tm.begin("K4_unpack_decode")
         _lib.call("sst_unpack_decode", arena.data_ptr(), self.offsets.data_ptr(),
                   self.info.data_ptr(), self.target.data_ptr(), npk, g, self.Ht, self.Wt, self.h,
@@ -236,11 +259,22 @@ class GopCodec:
 
     # -- reconstruction ------------------------------------------------
     def reconstruct(self, g: int, parity: int, out: torch.Tensor,
-                    prev: torch.Tensor | None = None) -> None:
+                    prev: torch.Tensor | None = None, fused: bool = False) -> None:
         """K5: [g, 9, H, W, 3] float32 output frames -- or uint8 raw-rgb24,
         each sample quantised as write_raw_video does (video.py:139-143);
         prev = device SstPrevDesc[g] as uint8 bytes (or None: no blending)."""
         check_gop_tensor(out, g, self.H, self.W, "out", (torch.float32, torch.uint8))
+        if fused:
+            # K5 with decode_gop fused: prev = device SstPrevTokDesc[g] bytes
+            if out.dtype != torch.float32:
+                raise ValueError("the decoder-fused reconstruction writes float32 frames")
+            self.timer.begin("K5_upscale_blend")
+            _lib.call("sst_upscale_blend_tok", self.tokq[parity].data_ptr(),
+                      self.pvalid[parity].data_ptr(), g, self.Ht, self.Wt, self.h, self.w, self.s,
+                      self.H, self.W, None if prev is None else prev.data_ptr(), self.blend_n,
+                      out.data_ptr(), _dev.stream())
+            self.timer.end("K5_upscale_blend")
+            return
         self.timer.begin("K5_upscale_blend")
         _lib.call("sst_upscale_blend_u8" if out.dtype == torch.uint8 else "sst_upscale_blend",
                   self.img[parity].data_ptr(), g, self.h, self.w, self.s,
@@ -300,9 +334,14 @@ class StreamBank:
     the stream's previous reconstruction, at whatever scale it was coded."""
 
     def __init__(self, n_streams: int, H: int, W: int, scales=(2, 3), blend_n: int = 2,
-                 concurrent_groups: bool = True, priority_middle: bool = True):
+                 concurrent_groups: bool = True, priority_middle: bool = True,
+                 fused: bool = False):
         if not 1 <= blend_n <= 8:                 # CodecConfig, codec.py:41-42
             raise ValueError(f"blend width must be in [1, 8], got {blend_n}")
+        # fused: decode_gop runs inside the reconstruction (K4 stops at the
+        # dequantised tokens, K5 decodes its windows in smem); float32 output
+        # frames only, rows of an even number of floats (8-byte stores)
+        self.fused = bool(fused) and (W * 3) % 2 == 0
         self.n, self.H, self.W, self.blend_n = n_streams, H, W, blend_n
         self.codecs = {s: GopCodec(n_streams, H, W, s, blend_n) for s in scales}
         # blend_n <= 4: K5 recomputes the previous GoP's (unblended) tail from
@@ -313,7 +352,9 @@ class StreamBank:
         self.prev_out = None
         self.has_prev = [False] * n_streams
         self.prev_host = np.zeros(n_streams, dtype=_lib.PREV_DTYPE)
-        self.rings = {s: _DescRing(n_streams * _lib.PREV_BYTES) for s in scales}
+        self.rings = {s: _DescRing(n_streams * max(_lib.PREV_BYTES, _lib.PREVTOK_BYTES))
+                      for s in scales}
+        self.prev_tok_host = np.zeros(n_streams, dtype=_lib.PREVTOK_DTYPE)
         # each scale group runs on its own CUDA stream so the latency-bound
         # middle kernels of one group overlap the HBM-bound K1/K5 of the other
         self.group_streams = ({s: torch.cuda.Stream(device=_dev.device()) for s in scales}
@@ -388,8 +429,11 @@ class StreamBank:
                     present = None if present_by_scale is None else present_by_scale.get(s)
                     if mid is not gs:
                         mid.wait_stream(gs)
+                    if self.fused and out_by_scale[s].dtype != torch.float32:
+                        raise ValueError("a fused StreamBank writes float32 frames "
+                                         "(StreamBank(fused=False) for raw-rgb24 output)")
                     with torch.cuda.stream(mid):
-                        codec.decode(g, parity, present=present)
+                        codec.decode(g, parity, present=present, fused=self.fused)
                     if mid is not gs:
                         gs.wait_stream(mid)
                     # K4 parse + 5 (init/route/dups/rowprep/decode) + K5
@@ -397,14 +441,15 @@ class StreamBank:
                     if self.blend_n <= 4:
                         staged = self._prev_descs(s, ids)
                         codec.reconstruct(g, parity, out_by_scale[s],
-                                          None if staged is None else staged[0])
+                                          None if staged is None else staged[0],
+                                          fused=self.fused)
                         if staged is not None:
                             self.rings[s].release(staged[1])
                     else:
                         if out_by_scale[s].dtype != torch.float32:
                             # the n >= 5 blend reads the previous float32 output back
                             raise ValueError("blend widths 5..8 need float32 output frames")
-                        codec.reconstruct(g, parity, out_by_scale[s], None)
+                        codec.reconstruct(g, parity, out_by_scale[s], None, fused=self.fused)
                         self._blend_wide(ids, out_by_scale[s])
                 elif mid is not gs:
                     gs.wait_stream(mid)
@@ -441,6 +486,21 @@ class StreamBank:
     def _prev_descs(self, s: int, ids):
         if all(self.last[i] is None for i in ids):
             return None
+        if self.fused:
+            # the previous GoP's token matrices + P validity (SstPrevTokDesc)
+            rec = self.prev_tok_host[:len(ids)]
+            rec[:] = 0
+            for j, sid in enumerate(ids):
+                loc = self.last[sid]
+                if loc is None:
+                    continue
+                ps, par, slot = loc
+                c = self.codecs[ps]
+                rec[j]["tok"] = c.tokq[par][slot].data_ptr()
+                rec[j]["pvalid"] = c.pvalid[par][slot].data_ptr()
+                rec[j]["h"], rec[j]["w"], rec[j]["s"] = c.h, c.w, ps
+                rec[j]["Ht"], rec[j]["Wt"] = c.Ht, c.Wt
+            return self.rings[s].stage(rec)
         rec = self.prev_host[:len(ids)]
         rec[:] = 0
         for j, sid in enumerate(ids):
