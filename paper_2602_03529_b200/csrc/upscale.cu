@@ -795,10 +795,14 @@ __device__ __forceinline__ uint32_t q8_check(float v, bool& near_tie) {
   return __float_as_uint(m) & 0xFFu;
 }
 
-template <bool kPrev, int kN>
-__global__ void __launch_bounds__(kV2Threads)
+// kNC output samples per thread (2: one 16-bit store per frame row; 4: one
+// 32-bit store, the row control, tie checks' setup and store addressing
+// shared by twice the samples)
+template <bool kPrev, int kN, int kNC>
+__global__ void __launch_bounds__(kTQ / kNC)
     k_upscale_blend_u8f(const __grid_constant__ CUtensorMap imap, const __grid_constant__ UpArgs a) {
   constexpr int kBand = 16;
+  constexpr int kNT = kTQ / kNC;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   UpU8Smem& S = *reinterpret_cast<UpU8Smem*>(smem_raw);
   const int tid = threadIdx.x;
@@ -828,7 +832,7 @@ __global__ void __launch_bounds__(kV2Threads)
     S.xs = (S.wx0[0] * 3) & 3;
     mbar_init(&S.bar, 1);
     fence_mbar_init();
-  } else if (tid == 2 * kBand + 32 && has_prev) {
+  } else if (tid == 2 * kBand + (kNT > 64 ? 32 : 1) && has_prev) {
     S.wx0[1] = axis_tap(q0 / 3, pd.w, pd.s).lo;
     S.wx1[1] = axis_tap(qlast / 3, pd.w, pd.s).hi;
   }
@@ -845,7 +849,7 @@ __global__ void __launch_bounds__(kV2Threads)
     const int pr1 = S.ty_p[rows - 1].hi;
     const int c0f = S.wx0[1] * 3, ncol = S.wx1[1] * 3 + 3 - c0f;
     const int lane = tid & 31, wid = tid >> 5;
-    for (int j = wid; j <= pr1 - pr0; j += kV2Threads / 32) {
+    for (int j = wid; j <= pr1 - pr0; j += kNT / 32) {
       const float* src = pd.p_img + ((int64_t)(pr0 + j) * pd.w) * 3 + c0f;
       float* dst = S.win[2] + j * kWF9;
 #pragma unroll
@@ -856,13 +860,15 @@ __global__ void __launch_bounds__(kV2Threads)
   mbar_wait(&S.bar, 0);
   __syncthreads();
 
-  const int qa0 = q0 + 2 * tid;
+  const int qa0 = q0 + kNC * tid;
   const bool col_ok = qa0 < a.W * 3;
-  AxisTap tx[2], txp[2];
-  int xl[2], xh[2], pxl[2] = {0, 0}, pxh[2] = {0, 0};
-  float gxf[2], fxf[2], gpf[2] = {0.f, 0.f}, fpf[2] = {0.f, 0.f};
+  AxisTap tx[kNC], txp[kNC];
+  int xl[kNC], xh[kNC], pxl[kNC], pxh[kNC];
+  float gxf[kNC], fxf[kNC], gpf[kNC], fpf[kNC];
 #pragma unroll
-  for (int u = 0; u < 2; ++u) {
+  for (int u = 0; u < kNC; ++u) {
+    pxl[u] = pxh[u] = 0;
+    gpf[u] = fpf[u] = 0.f;
     const int q = min(qa0 + u, a.W * 3 - 1);
     const int ox = q / 3, ch = q - ox * 3;
     tx[u] = axis_tap(ox, a.w, a.s);
@@ -886,7 +892,9 @@ __global__ void __launch_bounds__(kV2Threads)
     be[f] = (float)a.beta[f];
   }
   int ya = -1, yb = -1, qa = -1, qb = -1;
-  float ia[2] = {0, 0}, pa[2] = {0, 0}, ib[2] = {0, 0}, pb[2] = {0, 0}, qva[2] = {0, 0}, qvb[2] = {0, 0};
+  float ia[kNC], pa[kNC], ib[kNC], pb[kNC], qva[kNC], qvb[kNC];
+#pragma unroll
+  for (int u = 0; u < kNC; ++u) ia[u] = pa[u] = ib[u] = pb[u] = qva[u] = qvb[u] = 0.f;
   const int64_t orow = (int64_t)a.W * 3;
   const int fsv = opaque_i32(a.H * a.W * 3);
   uint8_t* obase = a.out8 + ((int64_t)g * kGop * a.H + oy0) * orow + qa0;
@@ -896,12 +904,12 @@ __global__ void __launch_bounds__(kV2Threads)
     if (rt.lo != ya) {
       if (rt.lo == yb) {
 #pragma unroll
-        for (int u = 0; u < 2; ++u) { ia[u] = ib[u]; pa[u] = pb[u]; }
+        for (int u = 0; u < kNC; ++u) { ia[u] = ib[u]; pa[u] = pb[u]; }
       } else {
         const float* wi = &S.win[0][(rt.lo - r0) * kWF9];
         const float* wp = &S.win[1][(rt.lo - r0) * kWF9];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kNC; ++u) {
           ia[u] = __fmaf_rn(wi[xl[u]], gxf[u], __fmul_rn(wi[xh[u]], fxf[u]));
           pa[u] = __fmaf_rn(wp[xl[u]], gxf[u], __fmul_rn(wp[xh[u]], fxf[u]));
         }
@@ -911,28 +919,28 @@ __global__ void __launch_bounds__(kV2Threads)
     if (rt.hi != yb) {
       if (rt.hi == ya) {
 #pragma unroll
-        for (int u = 0; u < 2; ++u) { ib[u] = ia[u]; pb[u] = pa[u]; }
+        for (int u = 0; u < kNC; ++u) { ib[u] = ia[u]; pb[u] = pa[u]; }
       } else {
         const float* wi = &S.win[0][(rt.hi - r0) * kWF9];
         const float* wp = &S.win[1][(rt.hi - r0) * kWF9];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < kNC; ++u) {
           ib[u] = __fmaf_rn(wi[xl[u]], gxf[u], __fmul_rn(wi[xh[u]], fxf[u]));
           pb[u] = __fmaf_rn(wp[xl[u]], gxf[u], __fmul_rn(wp[xh[u]], fxf[u]));
         }
       }
       yb = rt.hi;
     }
-    float ui[2], up[2];
+    float ui[kNC], up[kNC];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < kNC; ++u) {
       ui[u] = fminf(__fmaf_rn(ia[u], wy.x, __fmul_rn(ib[u], wy.y)), 1.0f);
       up[u] = fminf(__fmaf_rn(pa[u], wy.x, __fmul_rn(pb[u], wy.y)), 1.0f);
     }
     bool tie = false;
-    uint32_t bf[kN][2], bp[2];
+    uint32_t bf[kN][kNC], bp[kNC];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
+    for (int u = 0; u < kNC; ++u) {
       bp[u] = q8_check(up[u], tie);
       bf[0][u] = q8_check(ui[u], tie);
     }
@@ -942,27 +950,27 @@ __global__ void __launch_bounds__(kV2Threads)
       if (pt.lo != qa) {
         if (pt.lo == qb) {
 #pragma unroll
-          for (int u = 0; u < 2; ++u) qva[u] = qvb[u];
+          for (int u = 0; u < kNC; ++u) qva[u] = qvb[u];
         } else {
           const float* wv = &S.win[2][(pt.lo - pr0) * kWF9];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) qva[u] = __fmaf_rn(wv[pxl[u]], gpf[u], __fmul_rn(wv[pxh[u]], fpf[u]));
+          for (int u = 0; u < kNC; ++u) qva[u] = __fmaf_rn(wv[pxl[u]], gpf[u], __fmul_rn(wv[pxh[u]], fpf[u]));
         }
         qa = pt.lo;
       }
       if (pt.hi != qb) {
         if (pt.hi == qa) {
 #pragma unroll
-          for (int u = 0; u < 2; ++u) qvb[u] = qva[u];
+          for (int u = 0; u < kNC; ++u) qvb[u] = qva[u];
         } else {
           const float* wv = &S.win[2][(pt.hi - pr0) * kWF9];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) qvb[u] = __fmaf_rn(wv[pxl[u]], gpf[u], __fmul_rn(wv[pxh[u]], fpf[u]));
+          for (int u = 0; u < kNC; ++u) qvb[u] = __fmaf_rn(wv[pxl[u]], gpf[u], __fmul_rn(wv[pxh[u]], fpf[u]));
         }
         qb = pt.hi;
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < kNC; ++u) {
         const float qf = fminf(__fmaf_rn(qva[u], wq.x, __fmul_rn(qvb[u], wq.y)), 1.0f);
 #pragma unroll
         for (int f = 0; f < kN; ++f)
@@ -973,7 +981,7 @@ __global__ void __launch_bounds__(kV2Threads)
       // exact float64 path for this row's samples (codec.py:233-235, 289-293)
       const AxisTap ty = from_row(rt);
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
+      for (int u = 0; u < kNC; ++u) {
         const float eui = exact_up(S.win[0], ty.lo - r0, ty.hi - r0, ty, xl[u], xh[u], tx[u]);
         const float eup = exact_up(S.win[1], ty.lo - r0, ty.hi - r0, ty, xl[u], xh[u], tx[u]);
         bp[u] = rgb24_q(eup);
@@ -989,35 +997,49 @@ __global__ void __launch_bounds__(kV2Threads)
       }
     }
     if (col_ok) {
-      const unsigned short p8 = (unsigned short)(bp[0] | (bp[1] << 8));
-      __stcs(reinterpret_cast<unsigned short*>(obase), (unsigned short)(bf[0][0] | (bf[0][1] << 8)));
+      if constexpr (kNC == 2) {
+        const unsigned short p8 = (unsigned short)__byte_perm(bp[0], bp[1], 0x0040);
+        __stcs(reinterpret_cast<unsigned short*>(obase), (unsigned short)__byte_perm(bf[0][0], bf[0][1], 0x0040));
 #pragma unroll
-      for (int f = 1; f < kGop; ++f) {
-        const unsigned short v = (has_prev && f < kN)
-                                     ? (unsigned short)(bf[f < kN ? f : 0][0] | (bf[f < kN ? f : 0][1] << 8))
-                                     : p8;
-        __stcs(reinterpret_cast<unsigned short*>(frame_ptr(obase, fsv, f)), v);
+        for (int f = 1; f < kGop; ++f) {
+          const unsigned short v = (has_prev && f < kN)
+                                       ? (unsigned short)__byte_perm(bf[f < kN ? f : 0][0], bf[f < kN ? f : 0][1], 0x0040)
+                                       : p8;
+          __stcs(reinterpret_cast<unsigned short*>(frame_ptr(obase, fsv, f)), v);
+        }
+      } else {
+        auto pack4 = [](const uint32_t* v) {
+          return __byte_perm(__byte_perm(v[0], v[1], 0x0040), __byte_perm(v[2], v[3], 0x0040), 0x5410);
+        };
+        const unsigned int p8 = pack4(bp);
+        __stcs(reinterpret_cast<unsigned int*>(obase), pack4(bf[0]));
+#pragma unroll
+        for (int f = 1; f < kGop; ++f) {
+          const unsigned int v = (has_prev && f < kN) ? pack4(bf[f < kN ? f : 0]) : p8;
+          __stcs(reinterpret_cast<unsigned int*>(frame_ptr(obase, fsv, f)), v);
+        }
       }
     }
   }
 }
 
+template <int kNC>
 static int launch_k5_u8f(const CUtensorMap& imap, const UpArgs& a, const SstPrevDesc* prev, int blend_n,
                          cudaStream_t st) {
   dim3 grid(ceil_div(a.W * 3, kTQ), ceil_div(a.H, 16), a.G);
   if (grid.y > 65535) return SST_ERR_ARG;
   const int smem = (int)sizeof(UpU8Smem);
-  auto kern = k_upscale_blend_u8f<false, 1>;
+  auto kern = k_upscale_blend_u8f<false, 1, kNC>;
   if (prev) {
     switch (blend_n) {
-      case 1: kern = k_upscale_blend_u8f<true, 1>; break;
-      case 2: kern = k_upscale_blend_u8f<true, 2>; break;
-      case 3: kern = k_upscale_blend_u8f<true, 3>; break;
-      default: kern = k_upscale_blend_u8f<true, 4>; break;
+      case 1: kern = k_upscale_blend_u8f<true, 1, kNC>; break;
+      case 2: kern = k_upscale_blend_u8f<true, 2, kNC>; break;
+      case 3: kern = k_upscale_blend_u8f<true, 3, kNC>; break;
+      default: kern = k_upscale_blend_u8f<true, 4, kNC>; break;
     }
   }
   SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  kern<<<grid, kV2Threads, smem, st>>>(imap, a);
+  kern<<<grid, kTQ / kNC, smem, st>>>(imap, a);
   SST_LAUNCH_CHECK();
   return SST_OK;
 }
@@ -1885,8 +1907,16 @@ extern "C" int sst_upscale_blend_u8(const float* img, int G, int h, int w, int s
   if (!(var && !strcmp(var, "v1")) && (W * 3) % 2 == 0 && (reinterpret_cast<uintptr_t>(out) & 1u) == 0 &&
       make_tmap_f32_3d(&imap, img, (uint64_t)w * 3, (uint64_t)h, (uint64_t)G * 2, kWF9,
                        UpTmaSmem<16>::kWR))
-    return (var && !strcmp(var, "v2")) ? launch_k5_v2<16, uint8_t>(imap, a, prev, blend_n, st)
-                                       : launch_k5_u8f(imap, a, prev, blend_n, st);
+  {
+    // two samples per thread (16-bit stores).  A/B: SST_K5_VARIANT=v2, the
+    // exact float64 kernel (0.80 / 0.91 ms per 32 x 1080p GoPs, s=3 / 2);
+    // u8f4, four samples per thread with 32-bit stores (needs rows 4-byte
+    // aligned): 157 registers, 0.82 / 0.90 ms against 0.72 / 0.77 ms
+    if (var && !strcmp(var, "v2")) return launch_k5_v2<16, uint8_t>(imap, a, prev, blend_n, st);
+    const bool four = (W * 3) % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 3u) == 0 &&
+                      var && !strcmp(var, "u8f4");
+    return four ? launch_k5_u8f<4>(imap, a, prev, blend_n, st) : launch_k5_u8f<2>(imap, a, prev, blend_n, st);
+  }
   dim3 grid(ceil_div(W * 3, kUpThreads), ceil_div(H, kUpRows), G);
   if (grid.y > 65535) return SST_ERR_ARG;
   k_upscale_blend<uint8_t><<<grid, kUpThreads, 0, st>>>(a);
