@@ -1542,7 +1542,7 @@ __device__ __forceinline__ void k5_9_window_u8(uint8_t* dst, const uint8_t* img,
 #ifndef SST_K59_U8_MINB
 #define SST_K59_U8_MINB 3
 #endif
-template <int kBand, bool kPrev, int kN, int kLoad, typename T>
+template <int kBand, bool kPrev, int kN, int kLoad, typename T, int kSplit = 5>
 __global__ void __launch_bounds__(kTQ, sizeof(T) == 8 ? 2 : (sizeof(T) == 1 ? SST_K59_U8_MINB : 3))
     k_upscale9f(const __grid_constant__ CUtensorMap imap, const __grid_constant__ UpArgs a) {
   constexpr int kP = kPrev ? kN - 1 : 0;      // previous-GoP windows (alpha > 0 frames)
@@ -1669,26 +1669,30 @@ __global__ void __launch_bounds__(kTQ, sizeof(T) == 8 ? 2 : (sizeof(T) == 1 ? SS
     // slower (32 x 1080p GoPs, s=3, n=2; 1.77 ms here): one 9-frame pass at
     // 3 CTAs/SM 2.07 ms (spills), at 2 CTAs/SM 1.93 ms; this split at 2
     // CTAs/SM 2.10 ms; a 2 + 7 split 1.79 ms
-    k5_9_compute<kBand, kP, 5, kN>(S, a, g, 0, q0, oy0, rows, tx, xl, xh, txp, pxl, pxh);
-    k5_9_compute<kBand, kP, kGop - 5, 0>(S, a, g, 5, q0, oy0, rows, tx, xl, xh, txp, pxl, pxh);
+    if constexpr (kSplit >= kGop) {
+      k5_9_compute<kBand, kP, kGop, kN>(S, a, g, 0, q0, oy0, rows, tx, xl, xh, txp, pxl, pxh);
+    } else {
+      k5_9_compute<kBand, kP, kSplit, kN>(S, a, g, 0, q0, oy0, rows, tx, xl, xh, txp, pxl, pxh);
+      k5_9_compute<kBand, kP, kGop - kSplit, 0>(S, a, g, kSplit, q0, oy0, rows, tx, xl, xh, txp, pxl, pxh);
+    }
   } else {
     k5_9_compute<kBand, kP, kGop, 0>(S, a, g, 0, q0, oy0, rows, tx, xl, xh, tx, 0, 0);
   }
 }
 
-template <int BAND, int LOAD, typename T>
+template <int BAND, int LOAD, typename T, int SPLIT = 5>
 static int launch_k5_9f(const CUtensorMap& imap, const UpArgs& a, const SstPrevDesc* prev,
                         int blend_n, cudaStream_t st) {
   dim3 grid(ceil_div(a.W * 3, kTQ), ceil_div(a.H, BAND), a.G);
   if (grid.y > 65535) return SST_ERR_ARG;
   int smem = (int)sizeof(Up9fSmem<BAND, 0, T>);
-  auto kern = k_upscale9f<BAND, false, 1, LOAD, T>;
+  auto kern = k_upscale9f<BAND, false, 1, LOAD, T, SPLIT>;
   if (prev) {
     switch (blend_n) {
-      case 1: kern = k_upscale9f<BAND, true, 1, LOAD, T>; smem = sizeof(Up9fSmem<BAND, 0, T>); break;
-      case 2: kern = k_upscale9f<BAND, true, 2, LOAD, T>; smem = sizeof(Up9fSmem<BAND, 1, T>); break;
-      case 3: kern = k_upscale9f<BAND, true, 3, LOAD, T>; smem = sizeof(Up9fSmem<BAND, 2, T>); break;
-      default: kern = k_upscale9f<BAND, true, 4, LOAD, T>; smem = sizeof(Up9fSmem<BAND, 3, T>); break;
+      case 1: kern = k_upscale9f<BAND, true, 1, LOAD, T, SPLIT>; smem = sizeof(Up9fSmem<BAND, 0, T>); break;
+      case 2: kern = k_upscale9f<BAND, true, 2, LOAD, T, SPLIT>; smem = sizeof(Up9fSmem<BAND, 1, T>); break;
+      case 3: kern = k_upscale9f<BAND, true, 3, LOAD, T, SPLIT>; smem = sizeof(Up9fSmem<BAND, 2, T>); break;
+      default: kern = k_upscale9f<BAND, true, 4, LOAD, T, SPLIT>; smem = sizeof(Up9fSmem<BAND, 3, T>); break;
     }
   }
   if (const char* es = getenv("SST_K59_SMEM")) smem = std::max(smem, atoi(es));   // A/B: cap CTAs/SM
@@ -2065,6 +2069,20 @@ extern "C" int sst_upscale_blend9_u8(const uint8_t* img, int G, int h, int w, in
     constexpr int B = decltype(tag)::value;
     const bool t = make_tmap_u8_3d(&imap, img, (uint64_t)w * 3, (uint64_t)h, (uint64_t)G * kGop,
                                    kWF9u8, Up9fGeom<B, uint8_t>::kWR);
+    // frames per pass when blending (the row-tap control repeats per pass,
+    // registers hold 2 x frames float64 taps): measured with blend n=2, 48-row
+    // bands (scripts/k5_9u8_micro.py, two runs) -- s=3: 5 + 4 1.320 ms, one
+    // 9-frame pass 1.302, 3 + 6 1.311 (stable); s=2: 1.58-1.79 ms for every
+    // split (run-to-run noise larger than the differences).  Default: one
+    // pass at s=3, 5 + 4 at s=2; SST_K59_SPLIT=3|5|9 (A/B)
+    const char* sp = getenv("SST_K59_SPLIT");
+    const int split = sp ? atoi(sp) : (s == 3 ? 9 : 5);
+    if (split == 9)
+      return t ? launch_k5_9f<B, 2, uint8_t, 9>(imap, a, prev, blend_n, st)
+               : launch_k5_9f<B, 0, uint8_t, 9>(imap, a, prev, blend_n, st);
+    if (split == 3)
+      return t ? launch_k5_9f<B, 2, uint8_t, 3>(imap, a, prev, blend_n, st)
+               : launch_k5_9f<B, 0, uint8_t, 3>(imap, a, prev, blend_n, st);
     return t ? launch_k5_9f<B, 2, uint8_t>(imap, a, prev, blend_n, st)
              : launch_k5_9f<B, 0, uint8_t>(imap, a, prev, blend_n, st);
   };
