@@ -1580,7 +1580,12 @@ __global__ void __launch_bounds__(kTQ, sizeof(T) == 8 ? 2 : (sizeof(T) == 1 ? SS
 #pragma unroll
     for (int k = 0; k < kLutC; ++k) {
       const int e = k * kTQ + tid;
-      S.lut[e] = (double)__fdiv_rn((float)(e / kLutC), 255.0f);
+      // float32(q) / 255 exactly, division-free: q * 0x01010100 + 2^(msb(q)+1)
+      // = f(q) * 2^32 (encode.cu, k_encode_u8; all 256 values checked)
+      const uint32_t q = (uint32_t)(e / kLutC);
+      const uint64_t n = (uint64_t)q * 0x01010100u + (q ? 2u << (31 - __clz(q)) : 0u);
+      S.lut[e] = __dmul_rn(__dadd_rn(__hiloint2double((int)((uint32_t)(n >> 32) | 0x43300000u),
+                                                      (int)(uint32_t)n), -4503599627370496.0), 0x1p-32);
     }
   }
   __syncthreads();
