@@ -39,7 +39,10 @@
 extern "C" {
 #endif
 
-#define SST_ABI_VERSION 2
+/* 3: + raw-rgb24 (sst_encode_u8, sst_upscale_blend_u8) and the decoder-fused
+ * reconstruction (sst_unpack_tokens, sst_upscale_blend_tok, SstPrevTokDesc);
+ * earlier entry points unchanged */
+#define SST_ABI_VERSION 3
 
 /* call status */
 #define SST_OK 0

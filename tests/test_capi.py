@@ -51,7 +51,7 @@ def test_struct_layouts(lib):
 
 def test_pure_host_entry_points(lib):
     # metadata-only entry points (no device work)
-    assert lib.sst_abi_version() == 2
+    assert lib.sst_abi_version() == 3
     # transport.py:221-226 / SURVEY §8 packet sizes
     assert lib.sst_packet_wire_size(80, 12, 80) == 996
     assert lib.sst_packet_wire_size(120, 12, 120) == 1481
