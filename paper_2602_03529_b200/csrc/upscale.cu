@@ -1349,6 +1349,10 @@ struct Up9fSmem {
   // copy c sits in bank pair c, and a half-warp's 16 lookups never conflict
   double lut[sizeof(T) == 1 ? 256 * kLutC : 1];
   RowTap ty_c[kBand], ty_p[kBand];
+  // per-row actions on the cached horizontal taps (bits 0-1: lo row -- 1 copy
+  // the cached hi, 2 load; bits 2-3: hi row -- 1 copy the new lo, 2 load):
+  // the row-cache decisions are the same for every thread, made once here
+  uint8_t rc_c[kBand], rc_p[kBand];
   int wx0[2], wx1[2];
   int xs;                    // current window's column shift (TMA alignment), 0 for cp.async
   uint64_t bar;
@@ -1399,14 +1403,14 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
   const int64_t orow = (int64_t)a.W * 3;
   const int fsv = opaque_i32(a.H * a.W * 3);     // frame stride: one IMAD.WIDE per store
   float* op = a.out + ((int64_t)(g * kGop + f0) * a.H + oy0) * orow + q0 + tid;
-  int ya = -1, yb = -1, qa = -1, qb = -1;
   double ia[NF], ib[NF], qva[BLEND ? NQ : 1], qvb[BLEND ? NQ : 1];
 #pragma unroll
   for (int j = 0; j < NF; ++j) ia[j] = ib[j] = 0.0;
   for (int r = 0; r < rows; ++r, op += orow) {
     const AxisTap ty = from_row(S.ty_c[r]);
-    if (ty.lo != ya) {
-      if (ty.lo == yb) {
+    const int rc = S.rc_c[r];                      // row-cache actions (set up once per CTA)
+    if (rc & 3) {
+      if (rc & 1) {
 #pragma unroll
         for (int j = 0; j < NF; ++j) ia[j] = ib[j];
       } else {
@@ -1416,10 +1420,9 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
           ia[j] = k59_val(wr, xl, lutb) * tx.g + k59_val(wr, xh, lutb) * tx.f;     // codec.py:233
         }
       }
-      ya = ty.lo;
     }
-    if (ty.hi != yb) {
-      if (ty.hi == ya) {
+    if (rc & 12) {
+      if (rc & 4) {
 #pragma unroll
         for (int j = 0; j < NF; ++j) ib[j] = ia[j];
       } else {
@@ -1429,13 +1432,13 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
           ib[j] = k59_val(wr, xl, lutb) * tx.g + k59_val(wr, xh, lutb) * tx.f;
         }
       }
-      yb = ty.hi;
     }
     AxisTap tp = ty;
     if (BLEND) {
       tp = from_row(S.ty_p[r]);
-      if (tp.lo != qa) {
-        if (tp.lo == qb) {
+      const int rp = S.rc_p[r];
+      if (rp & 3) {
+        if (rp & 1) {
 #pragma unroll
           for (int j = 0; j < NQ; ++j) qva[j] = qvb[j];
         } else {
@@ -1445,10 +1448,9 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
             qva[j] = k59_val(wq, pxl, lutb) * txp.g + k59_val(wq, pxh, lutb) * txp.f;
           }
         }
-        qa = tp.lo;
       }
-      if (tp.hi != qb) {
-        if (tp.hi == qa) {
+      if (rp & 12) {
+        if (rp & 4) {
 #pragma unroll
           for (int j = 0; j < NQ; ++j) qvb[j] = qva[j];
         } else {
@@ -1458,7 +1460,6 @@ __device__ __forceinline__ void k5_9_compute(Up9fSmem<kBand, kP, T>& S, const Up
             qvb[j] = k59_val(wq, pxl, lutb) * txp.g + k59_val(wq, pxh, lutb) * txp.f;
           }
         }
-        qb = tp.hi;
       }
     }
     if constexpr (kU8) {
@@ -1589,6 +1590,15 @@ __global__ void __launch_bounds__(kTQ, sizeof(T) == 8 ? 2 : (sizeof(T) == 1 ? SS
     }
   }
   __syncthreads();
+  if (tid < 2 * kBand && (tid < kBand || has_prev)) {
+    const RowTap* tt = tid < kBand ? S.ty_c : S.ty_p;
+    const int r = tid < kBand ? tid : tid - kBand;
+    const int plo = r > 0 ? tt[r - 1].lo : -1, phi = r > 0 ? tt[r - 1].hi : -1;
+    const int lo = tt[r].lo, hi = tt[r].hi;
+    const int al = lo == plo ? 0 : (lo == phi ? 1 : 2);
+    const int ah = hi == phi ? 0 : (hi == lo ? 1 : 2);
+    (tid < kBand ? S.rc_c : S.rc_p)[r] = (uint8_t)(al | (ah << 2));
+  }
 
   // ---- load phase ----
   {
