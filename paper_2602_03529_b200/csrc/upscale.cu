@@ -771,10 +771,21 @@ struct UpU8Smem {
   float win[3][UpTmaSmem<16>::kWin];       // I, P, previous P windows (row pitch kWF9)
   RowTap ty_c[16], ty_p[16];
   float2 wy_c[16], wy_p[16];               // float32 (1 - fy, fy) per row
+  uint8_t rc_c[16], rc_p[16];              // per-row cache actions (as Up9fSmem)
   int wx0[2], wx1[2];
   int xs;
   uint64_t bar;
 };
+
+// row-cache action byte of row r of a tap table (bits 0-1: lo -- 1 copy the
+// cached hi, 2 load; bits 2-3: hi -- 1 copy the new lo, 2 load)
+__device__ __forceinline__ uint8_t row_action(const RowTap* tt, int r) {
+  const int plo = r > 0 ? tt[r - 1].lo : -1, phi = r > 0 ? tt[r - 1].hi : -1;
+  const int lo = tt[r].lo, hi = tt[r].hi;
+  const int al = lo == plo ? 0 : (lo == phi ? 1 : 2);
+  const int ah = hi == phi ? 0 : (hi == lo ? 1 : 2);
+  return (uint8_t)(al | (ah << 2));
+}
 
 // the reference's float32 upscale sample at one window position (codec.py:233-235, clip)
 __device__ __forceinline__ float exact_up(const float* win, int r_lo, int r_hi, const AxisTap& ty, int xl,
@@ -837,6 +848,8 @@ __global__ void __launch_bounds__(kTQ / kNC)
     S.wx1[1] = axis_tap(qlast / 3, pd.w, pd.s).hi;
   }
   __syncthreads();
+  if (tid < 16) S.rc_c[tid] = row_action(S.ty_c, tid);
+  else if (tid < 32 && has_prev) S.rc_p[tid - 16] = row_action(S.ty_p, tid - 16);
   const int r0 = S.ty_c[0].lo;
   const int pr0 = has_prev ? S.ty_p[0].lo : 0;
   if (tid == 0) {
@@ -891,7 +904,6 @@ __global__ void __launch_bounds__(kTQ / kNC)
     al[f] = (float)a.alpha[f];
     be[f] = (float)a.beta[f];
   }
-  int ya = -1, yb = -1, qa = -1, qb = -1;
   float ia[kNC], pa[kNC], ib[kNC], pb[kNC], qva[kNC], qvb[kNC];
 #pragma unroll
   for (int u = 0; u < kNC; ++u) ia[u] = pa[u] = ib[u] = pb[u] = qva[u] = qvb[u] = 0.f;
@@ -901,8 +913,9 @@ __global__ void __launch_bounds__(kTQ / kNC)
   for (int r = 0; r < rows; ++r, obase += orow) {
     const RowTap rt = S.ty_c[r];
     const float2 wy = S.wy_c[r];
-    if (rt.lo != ya) {
-      if (rt.lo == yb) {
+    const int rc = S.rc_c[r];
+    if (rc & 3) {
+      if (rc & 1) {
 #pragma unroll
         for (int u = 0; u < kNC; ++u) { ia[u] = ib[u]; pa[u] = pb[u]; }
       } else {
@@ -914,10 +927,9 @@ __global__ void __launch_bounds__(kTQ / kNC)
           pa[u] = __fmaf_rn(wp[xl[u]], gxf[u], __fmul_rn(wp[xh[u]], fxf[u]));
         }
       }
-      ya = rt.lo;
     }
-    if (rt.hi != yb) {
-      if (rt.hi == ya) {
+    if (rc & 12) {
+      if (rc & 4) {
 #pragma unroll
         for (int u = 0; u < kNC; ++u) { ib[u] = ia[u]; pb[u] = pa[u]; }
       } else {
@@ -929,7 +941,6 @@ __global__ void __launch_bounds__(kTQ / kNC)
           pb[u] = __fmaf_rn(wp[xl[u]], gxf[u], __fmul_rn(wp[xh[u]], fxf[u]));
         }
       }
-      yb = rt.hi;
     }
     float ui[kNC], up[kNC];
 #pragma unroll
@@ -947,8 +958,9 @@ __global__ void __launch_bounds__(kTQ / kNC)
     if (has_prev) {
       const RowTap pt = S.ty_p[r];
       const float2 wq = S.wy_p[r];
-      if (pt.lo != qa) {
-        if (pt.lo == qb) {
+      const int rp = S.rc_p[r];
+      if (rp & 3) {
+        if (rp & 1) {
 #pragma unroll
           for (int u = 0; u < kNC; ++u) qva[u] = qvb[u];
         } else {
@@ -956,10 +968,9 @@ __global__ void __launch_bounds__(kTQ / kNC)
 #pragma unroll
           for (int u = 0; u < kNC; ++u) qva[u] = __fmaf_rn(wv[pxl[u]], gpf[u], __fmul_rn(wv[pxh[u]], fpf[u]));
         }
-        qa = pt.lo;
       }
-      if (pt.hi != qb) {
-        if (pt.hi == qa) {
+      if (rp & 12) {
+        if (rp & 4) {
 #pragma unroll
           for (int u = 0; u < kNC; ++u) qvb[u] = qva[u];
         } else {
@@ -967,7 +978,6 @@ __global__ void __launch_bounds__(kTQ / kNC)
 #pragma unroll
           for (int u = 0; u < kNC; ++u) qvb[u] = __fmaf_rn(wv[pxl[u]], gpf[u], __fmul_rn(wv[pxh[u]], fpf[u]));
         }
-        qb = pt.hi;
       }
 #pragma unroll
       for (int u = 0; u < kNC; ++u) {
@@ -1590,15 +1600,8 @@ __global__ void __launch_bounds__(kTQ, sizeof(T) == 8 ? 2 : (sizeof(T) == 1 ? SS
     }
   }
   __syncthreads();
-  if (tid < 2 * kBand && (tid < kBand || has_prev)) {
-    const RowTap* tt = tid < kBand ? S.ty_c : S.ty_p;
-    const int r = tid < kBand ? tid : tid - kBand;
-    const int plo = r > 0 ? tt[r - 1].lo : -1, phi = r > 0 ? tt[r - 1].hi : -1;
-    const int lo = tt[r].lo, hi = tt[r].hi;
-    const int al = lo == plo ? 0 : (lo == phi ? 1 : 2);
-    const int ah = hi == phi ? 0 : (hi == lo ? 1 : 2);
-    (tid < kBand ? S.rc_c : S.rc_p)[r] = (uint8_t)(al | (ah << 2));
-  }
+  if (tid < kBand) S.rc_c[tid] = row_action(S.ty_c, tid);
+  else if (tid < 2 * kBand && has_prev) S.rc_p[tid - kBand] = row_action(S.ty_p, tid - kBand);
 
   // ---- load phase ----
   {
