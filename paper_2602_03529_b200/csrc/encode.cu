@@ -270,16 +270,20 @@ struct EncU8Cfg {
   static constexpr int NQ = TPB * 8 / 4;            // quads per working row
   static constexpr int NT = 8 * NQ;                 // threads (128)
   static constexpr int QB = 12 * S;                 // bytes per quad row segment
-  static constexpr int NST = S == 3 ? 3 : 4;        // ring depth
+  static constexpr int NST = 3;                     // ring depth
   static constexpr int TILE = R * INP;              // bytes per ring stage
   static constexpr int RING = NST * TILE;
   static constexpr int IMG_D = 2 * 8 * 8 * TPB * 3;
   static constexpr int S1_D = 2 * TPB * 3 * 3 * 8;
   static constexpr int TOK_D = 2 * TPB * kChannels;
   static constexpr int DCT_BYTES = (IMG_D + S1_D + TOK_D) * 8;
-  static constexpr int MAIN = ((RING > DCT_BYTES ? RING : DCT_BYTES) + 127) / 128 * 128;
   static constexpr int LUT_WORDS = 256 * 32;
-  static constexpr int SMEM = MAIN + LUT_WORDS * 4;
+  // the table follows the ring; the DCT stage (after the frame loop) reuses
+  // both, so the footprint is max(ring + table, DCT) -- 52 KB at s = 1, 2:
+  // 4 CTAs per SM (s = 3: 75 KB, 3 CTAs)
+  static constexpr int LUT_OFF = (RING + 127) / 128 * 128;
+  static constexpr int SMEM = LUT_OFF + LUT_WORDS * 4 > DCT_BYTES ? LUT_OFF + LUT_WORDS * 4 : DCT_BYTES;
+  static constexpr int MIN_CTAS = S == 3 ? 3 : 4;
 };
 
 struct EncU8Args {
@@ -292,11 +296,11 @@ struct EncU8Args {
 };
 
 template <int S, bool kWork>
-__global__ void __launch_bounds__(EncU8Cfg<S>::NT, 3) k_encode_u8(EncU8Args a) {
+__global__ void __launch_bounds__(EncU8Cfg<S>::NT, EncU8Cfg<S>::MIN_CTAS) k_encode_u8(EncU8Args a) {
   using C = EncU8Cfg<S>;
   extern __shared__ __align__(128) uint8_t smem_raw[];
   uint8_t* ring = smem_raw;
-  uint32_t* lut = reinterpret_cast<uint32_t*>(smem_raw + C::MAIN);
+  uint32_t* lut = reinterpret_cast<uint32_t*>(smem_raw + C::LUT_OFF);
   const int tid = threadIdx.x, lane = tid & 31;
   const int tx0 = blockIdx.x * C::TPB;
   const int ty = blockIdx.y;
