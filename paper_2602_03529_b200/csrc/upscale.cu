@@ -761,11 +761,12 @@ static int launch_k5_v2(const CUtensorMap& imap, const UpArgs& a, const SstPrevD
 // adds <= 2^-23 (two products, one sum, the weight error) so the upscale is
 // within 2^-22 of the real-number value and within 2^-22 + 2^-25 of the
 // reference's float32 result; a blend adds <= 5 * 2^-25; so
-// |t' - float32(255 v)| <= 255 (2^-22 + 6 * 2^-25) + 2 * 2^-17 < 1.3e-4 <
-// tau = 2^-12.  Outside the tau band the two roundings agree; inside it the
-// exact path decides (half-integers -- rint's ties -- included).  The band
-// holds ~0.05 % of samples.
-constexpr float kU8Tau = 0x1p-12f;
+// |t' - float32(255 v)| <= 255 (2^-22 + 6 * 2^-25) + 2 * 2^-17 = 1.22e-4 <
+// tau = 1.25 * 2^-13 = 1.53e-4.  Outside the tau band the two roundings
+// agree; inside it the exact path decides (half-integers -- rint's ties --
+// included).  The band holds ~0.03 % of samples (tau = 2^-12 before: ~1 %
+// more time in the exact path, K5u8 0.716 ms).
+constexpr float kU8Tau = 0x1.4p-13f;
 
 struct UpU8Smem {
   float win[3][UpTmaSmem<16>::kWin];       // I, P, previous P windows (row pitch kWF9)
