@@ -949,12 +949,13 @@ __global__ void __launch_bounds__(kTQ / kNC)
       ui[u] = fminf(__fmaf_rn(ia[u], wy.x, __fmul_rn(ib[u], wy.y)), 1.0f);
       up[u] = fminf(__fmaf_rn(pa[u], wy.x, __fmul_rn(pb[u], wy.y)), 1.0f);
     }
-    bool tie = false;
+    bool tie[kNC];                                  // per sample column
     uint32_t bf[kN][kNC], bp[kNC];
 #pragma unroll
     for (int u = 0; u < kNC; ++u) {
-      bp[u] = q8_check(up[u], tie);
-      bf[0][u] = q8_check(ui[u], tie);
+      tie[u] = false;
+      bp[u] = q8_check(up[u], tie[u]);
+      bf[0][u] = q8_check(ui[u], tie[u]);
     }
     if (has_prev) {
       const RowTap pt = S.ty_p[r];
@@ -985,14 +986,19 @@ __global__ void __launch_bounds__(kTQ / kNC)
         const float qf = fminf(__fmaf_rn(qva[u], wq.x, __fmul_rn(qvb[u], wq.y)), 1.0f);
 #pragma unroll
         for (int f = 0; f < kN; ++f)
-          bf[f][u] = q8_check(__fmaf_rn(al[f], qf, __fmul_rn(be[f], f == 0 ? ui[u] : up[u])), tie);
+          bf[f][u] = q8_check(__fmaf_rn(al[f], qf, __fmul_rn(be[f], f == 0 ? ui[u] : up[u])), tie[u]);
       }
     }
-    if (tie) {
-      // exact float64 path for this row's samples (codec.py:233-235, 289-293)
+    bool any_tie = false;
+#pragma unroll
+    for (int u = 0; u < kNC; ++u) any_tie |= tie[u];
+    if (any_tie) {
+      // exact float64 path for the row's samples of the columns near a tie
+      // (codec.py:233-235, 289-293)
       const AxisTap ty = from_row(rt);
 #pragma unroll
       for (int u = 0; u < kNC; ++u) {
+        if (!tie[u]) continue;
         const float eui = exact_up(S.win[0], ty.lo - r0, ty.hi - r0, ty, xl[u], xh[u], tx[u]);
         const float eup = exact_up(S.win[1], ty.lo - r0, ty.hi - r0, ty, xl[u], xh[u], tx[u]);
         bp[u] = rgb24_q(eup);
