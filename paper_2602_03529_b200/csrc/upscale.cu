@@ -798,11 +798,14 @@ __device__ __forceinline__ float exact_up(const float* win, int r_lo, int r_hi, 
   return f32_clip_hi1(top * ty.g + bot * ty.f);
 }
 
-// t = v * 255 (float32) -> its rint byte (bits of t + 1.5 * 2^23) and whether t is within tau of a tie
+// t = 255 v (the exact product, inside two FMAs) -> its rint byte (bits of
+// t + 1.5 * 2^23, where the float32 ulp is 1) and whether t is within tau of
+// a tie (d = t - rint(t), one rounding of a value below 1: error <= 2^-25).
+// Using the exact product instead of float32(255 v) only removes a rounding
+// (2^-17) from the bound above.
 __device__ __forceinline__ uint32_t q8_check(float v, bool& near_tie) {
-  const float t = __fmul_rn(v, 255.0f);
-  const float m = __fadd_rn(t, 12582912.0f);
-  const float d = __fsub_rn(t, __fsub_rn(m, 12582912.0f));
+  const float m = __fmaf_rn(v, 255.0f, 12582912.0f);
+  const float d = __fmaf_rn(v, 255.0f, -__fsub_rn(m, 12582912.0f));
   near_tie |= fabsf(d) > 0.5f - kU8Tau;
   return __float_as_uint(m) & 0xFFu;
 }

@@ -13,8 +13,10 @@ exponent spreads beyond float64's reach, rounding ties.
       == float32(float64(N) * (2^-32 / 9))   for integers N < 9 * 2^32
 * encode.cu k_encode_u8:  (x + c) - c,  c = 1.5 * 2^(e(x) + 29)
       == float64(float32(x))   for x = 0 or x in [2^-12, 1]
-* upscale.cu q8_check: the float32 byte quantiser rint(float32(v * 255))
+* upscale.cu rgb24_q: the float32 byte quantiser rint(float32(v * 255))
       taken from the bits of t + 1.5 * 2^23
+* upscale.cu q8_check: the same byte from the exact product inside an FMA,
+      valid whenever the FMA-computed distance to a tie exceeds tau
 """
 
 import numpy as np
@@ -95,3 +97,31 @@ def test_byte_quantiser_from_magic_add():
     byte = m.view(np.uint32) & np.uint32(0xFF)
     ref = np.rint(v * 255.0).astype(np.uint8)                          # write_raw_video
     assert np.array_equal(byte.astype(np.uint8), ref)
+
+
+def test_fma_byte_quantiser_outside_tie_band():
+    """q8_check: m = fma(v, 255, 1.5 * 2^23) rounds the exact 255 v to an
+    integer (float32 ulp 1 there); d = fma(v, 255, -(m - 1.5 * 2^23)) is one
+    rounding of 255 v - rint(255 v).  Whenever |d| <= 0.5 - tau the byte is
+    write_raw_video's rint(float32(v * 255)), also for v perturbed by up to
+    the kernel's proven error bound (1.22e-4 / 255)."""
+    tau = np.float32(1.25 * 2.0 ** -13)
+    n = 2_000_000
+    v = _wide_float32(n)
+    k = RNG.integers(0, 255, n // 2)
+    t0 = ((2 * k + 1) / 510.0).astype(np.float32)
+    v = np.concatenate([v, t0, np.nextafter(t0, np.float32(0)), np.nextafter(t0, np.float32(1))])
+    t = v.astype(np.float64) * 255.0                       # exact: 24 + 8 bits
+    m = np.rint(t)                                         # the FMA's rounding to the integer grid
+    d = (t - m).astype(np.float32)                         # exact difference, one float32 rounding
+    ok = np.abs(d) <= np.float32(0.5) - tau
+    byte = m.astype(np.int64) & 0xFF
+    ref = np.rint(v * np.float32(255.0)).astype(np.uint8)   # write_raw_video on the float32 sample
+    assert np.array_equal(byte[ok], ref[ok].astype(np.int64))
+    # the reference's sample may differ from the kernel's estimate by the bound
+    eps = 1.22e-4 / 255.0
+    for sgn in (-1.0, 1.0):
+        vr = np.clip(v.astype(np.float64) + sgn * eps, 0.0, 1.0).astype(np.float32)
+        ref_r = np.rint(vr * np.float32(255.0)).astype(np.int64)
+        assert np.array_equal(byte[ok], ref_r[ok])
+    assert (~ok[:n]).mean() < 1e-3 and not ok[n:n + n // 2].any()   # few detours, every tie flagged
