@@ -767,12 +767,14 @@ static int launch_k5_v2(const CUtensorMap& imap, const UpArgs& a, const SstPrevD
 // included).  The band holds ~0.03 % of samples (tau = 2^-12 before: ~1 %
 // more time in the exact path, K5u8 0.716 ms).
 constexpr float kU8Tau = 0x1.4p-13f;
+constexpr int kK5u8Band = 32;              // output rows per CTA (default; SST_K5U8_BAND)
 
+template <int kBand>
 struct UpU8Smem {
-  float win[3][UpTmaSmem<16>::kWin];       // I, P, previous P windows (row pitch kWF9)
-  RowTap ty_c[16], ty_p[16];
-  float2 wy_c[16], wy_p[16];               // float32 (1 - fy, fy) per row
-  uint8_t rc_c[16], rc_p[16];              // per-row cache actions (as Up9fSmem)
+  float win[3][UpTmaSmem<kBand>::kWin];    // I, P, previous P windows (row pitch kWF9)
+  RowTap ty_c[kBand], ty_p[kBand];
+  float2 wy_c[kBand], wy_p[kBand];         // float32 (1 - fy, fy) per row
+  uint8_t rc_c[kBand], rc_p[kBand];        // per-row cache actions (as Up9fSmem)
   int wx0[2], wx1[2];
   int xs;
   uint64_t bar;
@@ -813,13 +815,14 @@ __device__ __forceinline__ uint32_t q8_check(float v, bool& near_tie) {
 // kNC output samples per thread (2: one 16-bit store per frame row; 4: one
 // 32-bit store, the row control, tie checks' setup and store addressing
 // shared by twice the samples)
-template <bool kPrev, int kN, int kNC>
+template <int kBand, bool kPrev, int kN, int kNC>
 __global__ void __launch_bounds__(kTQ / kNC)
     k_upscale_blend_u8f(const __grid_constant__ CUtensorMap imap, const __grid_constant__ UpArgs a) {
-  constexpr int kBand = 16;
   constexpr int kNT = kTQ / kNC;
+  constexpr int kWxP = 2 * kBand + (2 * kBand + 32 < kNT ? 32 : 1);   // thread of the previous window's range
+  static_assert(kWxP < kNT, "setup threads");
   extern __shared__ __align__(128) uint8_t smem_raw[];
-  UpU8Smem& S = *reinterpret_cast<UpU8Smem*>(smem_raw);
+  UpU8Smem<kBand>& S = *reinterpret_cast<UpU8Smem<kBand>*>(smem_raw);
   const int tid = threadIdx.x;
   const int q0 = blockIdx.x * kTQ;
   const int oy0 = blockIdx.y * kBand;
@@ -847,13 +850,13 @@ __global__ void __launch_bounds__(kTQ / kNC)
     S.xs = (S.wx0[0] * 3) & 3;
     mbar_init(&S.bar, 1);
     fence_mbar_init();
-  } else if (tid == 2 * kBand + (kNT > 64 ? 32 : 1) && has_prev) {
+  } else if (tid == kWxP && has_prev) {
     S.wx0[1] = axis_tap(q0 / 3, pd.w, pd.s).lo;
     S.wx1[1] = axis_tap(qlast / 3, pd.w, pd.s).hi;
   }
   __syncthreads();
-  if (tid < 16) S.rc_c[tid] = row_action(S.ty_c, tid);
-  else if (tid < 32 && has_prev) S.rc_p[tid - 16] = row_action(S.ty_p, tid - 16);
+  if (tid < kBand) S.rc_c[tid] = row_action(S.ty_c, tid);
+  else if (tid < 2 * kBand && has_prev) S.rc_p[tid - kBand] = row_action(S.ty_p, tid - kBand);
   const int r0 = S.ty_c[0].lo;
   const int pr0 = has_prev ? S.ty_p[0].lo : 0;
   if (tid == 0) {
@@ -1043,19 +1046,19 @@ __global__ void __launch_bounds__(kTQ / kNC)
   }
 }
 
-template <int kNC>
+template <int kBand, int kNC>
 static int launch_k5_u8f(const CUtensorMap& imap, const UpArgs& a, const SstPrevDesc* prev, int blend_n,
                          cudaStream_t st) {
-  dim3 grid(ceil_div(a.W * 3, kTQ), ceil_div(a.H, 16), a.G);
+  dim3 grid(ceil_div(a.W * 3, kTQ), ceil_div(a.H, kBand), a.G);
   if (grid.y > 65535) return SST_ERR_ARG;
-  const int smem = (int)sizeof(UpU8Smem);
-  auto kern = k_upscale_blend_u8f<false, 1, kNC>;
+  const int smem = (int)sizeof(UpU8Smem<kBand>);
+  auto kern = k_upscale_blend_u8f<kBand, false, 1, kNC>;
   if (prev) {
     switch (blend_n) {
-      case 1: kern = k_upscale_blend_u8f<true, 1, kNC>; break;
-      case 2: kern = k_upscale_blend_u8f<true, 2, kNC>; break;
-      case 3: kern = k_upscale_blend_u8f<true, 3, kNC>; break;
-      default: kern = k_upscale_blend_u8f<true, 4, kNC>; break;
+      case 1: kern = k_upscale_blend_u8f<kBand, true, 1, kNC>; break;
+      case 2: kern = k_upscale_blend_u8f<kBand, true, 2, kNC>; break;
+      case 3: kern = k_upscale_blend_u8f<kBand, true, 3, kNC>; break;
+      default: kern = k_upscale_blend_u8f<kBand, true, 4, kNC>; break;
     }
   }
   SST_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -1936,18 +1939,26 @@ extern "C" int sst_upscale_blend_u8(const float* img, int G, int h, int w, int s
   CUtensorMap imap;
   memset(&imap, 0, sizeof(imap));
   const char* var = getenv("SST_K5_VARIANT");
+  const bool four = (W * 3) % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 3u) == 0 && var &&
+                    !strcmp(var, "u8f4");
+  const bool v2 = var && !strcmp(var, "v2");
+  // rows per CTA of the float32 kernel (SST_K5U8_BAND=16 / 32, A/B)
+  const char* eb = getenv("SST_K5U8_BAND");
+  const int ebv = eb ? atoi(eb) : kK5u8Band;
+  const int band = (four || v2) ? 16 : (ebv == 16 || ebv == 48 ? ebv : 32);
   if (!(var && !strcmp(var, "v1")) && (W * 3) % 2 == 0 && (reinterpret_cast<uintptr_t>(out) & 1u) == 0 &&
       make_tmap_f32_3d(&imap, img, (uint64_t)w * 3, (uint64_t)h, (uint64_t)G * 2, kWF9,
-                       UpTmaSmem<16>::kWR))
+                       band == 48 ? UpTmaSmem<48>::kWR : band == 32 ? UpTmaSmem<32>::kWR : UpTmaSmem<16>::kWR))
   {
     // two samples per thread (16-bit stores).  A/B: SST_K5_VARIANT=v2, the
     // exact float64 kernel (0.80 / 0.91 ms per 32 x 1080p GoPs, s=3 / 2);
     // u8f4, four samples per thread with 32-bit stores (needs rows 4-byte
     // aligned): 157 registers, 0.82 / 0.90 ms against 0.72 / 0.77 ms
-    if (var && !strcmp(var, "v2")) return launch_k5_v2<16, uint8_t>(imap, a, prev, blend_n, st);
-    const bool four = (W * 3) % 4 == 0 && (reinterpret_cast<uintptr_t>(out) & 3u) == 0 &&
-                      var && !strcmp(var, "u8f4");
-    return four ? launch_k5_u8f<4>(imap, a, prev, blend_n, st) : launch_k5_u8f<2>(imap, a, prev, blend_n, st);
+    if (v2) return launch_k5_v2<16, uint8_t>(imap, a, prev, blend_n, st);
+    if (four) return launch_k5_u8f<16, 4>(imap, a, prev, blend_n, st);
+    if (band == 48) return launch_k5_u8f<48, 2>(imap, a, prev, blend_n, st);
+    return band == 32 ? launch_k5_u8f<32, 2>(imap, a, prev, blend_n, st)
+                      : launch_k5_u8f<16, 2>(imap, a, prev, blend_n, st);
   }
   dim3 grid(ceil_div(W * 3, kUpThreads), ceil_div(H, kUpRows), G);
   if (grid.y > 65535) return SST_ERR_ARG;

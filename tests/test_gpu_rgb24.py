@@ -84,9 +84,11 @@ def _ties(rng, shape):
 @pytest.mark.parametrize("s,H,W", [(2, 48, 64), (3, 45, 72), (3, 40, 56), (2, 33, 91)])
 @pytest.mark.parametrize("n", [1, 2, 4])
 @pytest.mark.parametrize("with_prev", [False, True])
-@pytest.mark.parametrize("variant", ["default", "u8f4", "v2"])
+@pytest.mark.parametrize("variant", ["default", "u8f4", "v2", "band16", "band32", "band48"])
 def test_upscale_blend_u8_equals_quantised_float(s, H, W, n, with_prev, variant, monkeypatch):
-    if variant != "default":
+    if variant.startswith("band"):
+        monkeypatch.setenv("SST_K5U8_BAND", variant[4:])
+    elif variant != "default":
         monkeypatch.setenv("SST_K5_VARIANT", variant)
     rng = np.random.default_rng(31 * s + n + H)
     h, w = -(-H // s), -(-W // s)
